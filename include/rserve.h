@@ -1,0 +1,238 @@
+/* rserve-b200 — C-ABI drop-in boundary for RServe's intra-request pipeline
+ * (chunked multimodal encode -> embedding tracker -> chunked prefill) on
+ * NVIDIA B200 (sm_100a).
+ *
+ * The reference (arxiv 2509.24381, /root/reference/proj, "lmmsim") exposes
+ * this path only as a header-only C++ API with an analytic cost seam; it has
+ * no FFI. Each entry point below names the reference interface it replaces
+ * (file:line under proj/include/lmmsim/). The C++ API itself is kept
+ * verbatim in include/lmmsim/ (our implementation), which the
+ * reference's own unit suites compile against unchanged.
+ *
+ * Conventions
+ *   - every function returns rs_status; RS_OK == 0. On error the thread-local
+ *     message (rs_last_error) holds the exact what() text the reference
+ *     would throw, and the status names the exception class
+ *     (reference errors.hpp:23-80).
+ *   - token indices / counts are uint64 (request.hpp:28-31), times are double
+ *     milliseconds.
+ *   - strings returned through char** are malloc'd; release with rs_free.
+ *   - device pointers are plain CUDA device addresses; no torch types.
+ *   - the product path has no CPU fallback: without a usable sm_100 device,
+ *     device entry points fail with RS_ERR_CUDA.
+ */
+#ifndef RSERVE_H_
+#define RSERVE_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes: one per reference exception class ------------------ */
+typedef enum rs_status {
+  RS_OK = 0,
+  RS_ERR_CONFIG = 1,               /* ConfigError            errors.hpp:29 */
+  RS_ERR_REGISTRY = 2,             /* RegistryError          errors.hpp:35 */
+  RS_ERR_DOUBLE_ENCODE = 3,        /* DoubleEncodeError      errors.hpp:41 */
+  RS_ERR_ALIGNMENT = 4,            /* AlignmentError         errors.hpp:47 */
+  RS_ERR_DEPENDENCY_VIOLATION = 5, /* DependencyViolation    errors.hpp:54 */
+  RS_ERR_INPUT = 6,                /* InputError             errors.hpp:60 */
+  RS_ERR_DATA = 7,                 /* DataError              errors.hpp:66 */
+  RS_ERR_IO = 8,                   /* IoError                errors.hpp:71 */
+  RS_ERR_INTERNAL = 9,             /* InternalError          errors.hpp:77 */
+  RS_ERR_SIM = 10,                 /* other SimError                        */
+  RS_ERR_CUDA = 20,                /* CUDA runtime / driver / no device     */
+  RS_ERR_NCCL = 21,                /* NCCL failure                          */
+  RS_ERR_UNKNOWN = 99
+} rs_status;
+
+const char* rs_last_error(void);
+void rs_free(void* p);
+/* Build identification, e.g. "rserve-b200 sm_100a tcgen05". */
+const char* rs_version(void);
+
+/* ---- host-side config PODs --------------------------------------------- */
+enum { RS_POLICY_VANILLA_PP = 0, RS_POLICY_EPD_BASELINE = 1,
+       RS_POLICY_INTRA_ONLY = 2, RS_POLICY_RSERVE = 3 };
+enum { RS_PIPELINE_DEFAULT = -1, RS_PIPELINE_CPP = 0, RS_PIPELINE_VANILLA = 1 };
+enum { RS_RELEASE_FIRST_STAGE = 0, RS_RELEASE_LAST_STAGE = 1 };
+#define RS_WHOLE_REQUEST UINT64_MAX /* encoder_sched.hpp:32-33 kWholeRequest */
+
+typedef struct rs_cost_model { /* cost_model.hpp:37-45 */
+  double alpha_enc_ms, beta_enc_ms_per_token;
+  double eps_tx_ms, zeta_tx_ms_per_token;
+  double gamma_stage_ms, delta_stage_ms_per_token, kappa_attn_ms;
+  double tp_speedup;
+} rs_cost_model;
+
+typedef struct rs_sim_config { /* simengine.hpp:48-75 SimConfig */
+  int32_t policy;          /* RS_POLICY_* */
+  int32_t pipeline_mode;   /* RS_PIPELINE_* */
+  int32_t stages;
+  int32_t encoder_workers;
+  uint64_t token_budget;           /* B */
+  uint64_t embedding_batch_tokens; /* C, or RS_WHOLE_REQUEST */
+  int32_t release_at;      /* RS_RELEASE_* */
+  uint32_t hidden_size;
+  rs_cost_model cost;
+} rs_sim_config;
+
+enum { RS_LAYOUT_ALTERNATING = 0, RS_LAYOUT_CONSECUTIVE_MM = 1,
+       RS_LAYOUT_TEXT_FIRST = 2 };
+typedef struct rs_int_dist { int32_t uniform; uint64_t lo, hi; } rs_int_dist;
+typedef struct rs_template { /* workload.hpp:71-107 RequestTemplate */
+  int32_t pattern;
+  rs_int_dist num_mm_items, mm_item_tokens, text_segment_tokens;
+  double probability;
+} rs_template;
+typedef struct rs_workload_config { /* workload.hpp:109-136 */
+  double arrival_rate, duration_s;
+  uint64_t seed;
+  const rs_template* templates;
+  int32_t n_templates;
+  int32_t has_slo;
+  double slo_ttft_ms;
+} rs_workload_config;
+
+/* ---- host scheduling core (no device needed) ---------------------------
+ * Workloads travel as the reference's workload-file text
+ * (`id,arrival_ms,slo|-,layout` lines; workload.hpp:217-265).            */
+
+/* generate_workload (workload.hpp:139-172) -> workload text */
+rs_status rs_generate_workload(const rs_workload_config* cfg, char** out_text);
+
+/* run_simulation (simengine.hpp:522-526) on the analytic cost model.
+ * out_result: canonical decision log (see DESIGN.md §"Decision log"):
+ * per-request records, slices, trace, release order; doubles in shortest
+ * round-trip form so equal text == bit-identical results.              */
+rs_status rs_simulate(const char* workload_text, const rs_sim_config* cfg,
+                      char** out_result, char** out_journal);
+
+/* One report row (experiment.hpp:72-101 run_cell + metrics.hpp:173-194):
+ * generate -> run -> compute_report -> CSV row. slo_ttft_ms < 0: none.   */
+rs_status rs_experiment_cell(const rs_workload_config* wcfg,
+                             const rs_sim_config* cfg, double slo_ttft_ms,
+                             char** out_csv_row);
+
+/* Algorithm 1 (encoder_sched.hpp:48-74): batches as text lines
+ * "request item_idx:start-end,... total". C == RS_WHOLE_REQUEST allowed. */
+rs_status rs_plan_batches(const char* layout, uint64_t request_id,
+                          uint64_t c_tokens, char** out_text);
+
+/* ---- device pipeline context -------------------------------------------- */
+typedef struct rs_ctx rs_ctx;
+
+enum { RS_MODEL_TINY = 0, RS_MODEL_QWEN25VL_7B = 1, RS_MODEL_QWEN25VL_72B_LLM = 2 };
+
+typedef struct rs_model_config {
+  /* vision encoder (ViT + 2x2 patch merger) */
+  int32_t vit_dim, vit_layers, vit_heads, vit_ff, vit_window; /* window: merged units/side */
+  int32_t vit_fullatt_every;  /* full attention at layers l % every == every-1 */
+  int32_t patch_dim;          /* 3*2*14*14 = 1176 */
+  /* LLM decoder */
+  int32_t llm_dim, llm_layers, llm_q_heads, llm_kv_heads, llm_head_dim, llm_ff;
+  int32_t vocab;
+  float rope_theta_llm, rope_theta_vit, rms_eps;
+  uint64_t weight_seed;
+} rs_model_config;
+
+/* Fills the preset shapes: TINY (cfg1), QWEN25VL_7B (cfg2-4), 72B-LLM (cfg5). */
+rs_status rs_model_preset(int32_t preset, rs_model_config* out);
+
+typedef struct rs_ctx_options {
+  int32_t device;              /* CUDA ordinal for this process            */
+  uint64_t max_prompt_tokens;  /* per-request cap, sizes staging buffers   */
+  uint64_t slot_tokens;        /* embedding-slot pool capacity (tokens)     */
+  uint64_t kv_tokens;          /* paged-KV pool capacity (tokens)           */
+  uint64_t max_chunk_tokens;   /* B upper bound (prefill M)                 */
+  uint64_t max_encode_tokens;  /* C upper bound incl. largest item (LLM tokens) */
+  int32_t layer_begin, layer_end; /* LLM layers owned here ([0,L) = all)    */
+  int32_t with_vit;            /* allocate the vision encoder here           */
+  int32_t with_lm_head;        /* allocate final norm + LM head here         */
+} rs_ctx_options;
+
+rs_status rs_ctx_create(const rs_model_config* model, const rs_ctx_options* opt,
+                        rs_ctx** out);
+rs_status rs_ctx_destroy(rs_ctx* ctx);
+
+/* ---- tracker data plane (device) ----------------------------------------
+ * Replaces EmbeddingTracker ctor (tracker.hpp:44-59) + create_tracker
+ * (193-198): reserves slot pages for the request, uploads text token ids,
+ * gathers text embeddings into the slots (K8), initialises the readiness
+ * bitmap with text = 1 and keeps the host tracker mirror.               */
+rs_status rs_request_create(rs_ctx* ctx, uint64_t id, const char* layout,
+                            const int32_t* text_token_ids /* may be NULL */);
+/* mark_encoded / on_embeddings_ready (tracker.hpp:83-105,
+ * token_sched.hpp:184-187): scatter [tokens, d_llm] bf16 rows (device
+ * pointer, row-major, in item order) into the item's slots and set its
+ * bitmap bits (K6); host mirror is updated and errors mirror the
+ * reference (AlignmentError / DoubleEncodeError).                       */
+rs_status rs_mark_encoded(rs_ctx* ctx, uint64_t id, uint64_t start, uint64_t end,
+                          const void* embeddings_dev);
+/* schedulable_tokens (tracker.hpp:79) from the host mirror, plus the
+ * device ready-prefix (K7, warp ballot over the bitmap) for cross-check. */
+rs_status rs_schedulable(rs_ctx* ctx, uint64_t id, uint64_t* host_count,
+                         uint64_t* device_count);
+/* advance_prefill (tracker.hpp:109-122). */
+rs_status rs_advance_prefill(rs_ctx* ctx, uint64_t id, uint64_t n,
+                             uint64_t* out_start, uint64_t* out_end);
+/* release (tracker.hpp:126-135) + slot-page free once fully released. */
+rs_status rs_release(rs_ctx* ctx, uint64_t id, uint64_t start, uint64_t end);
+rs_status rs_request_erase(rs_ctx* ctx, uint64_t id);
+/* Device bitmap words (ceil(T/32) u32) and slot rows (bf16) read back. */
+rs_status rs_read_bitmap(rs_ctx* ctx, uint64_t id, uint32_t* out_words, uint64_t n_words);
+rs_status rs_read_slots(rs_ctx* ctx, uint64_t id, uint64_t start, uint64_t end,
+                        void* out_host_bf16);
+/* live / peak / released token accounting of the host mirror. */
+rs_status rs_tracker_stats(rs_ctx* ctx, uint64_t id, uint64_t out[6]);
+
+/* ---- compute entry points ------------------------------------------------
+ * encode_time_ms seam (cost_model.hpp:68-71): ViT forward of one
+ * Algorithm-1 batch. `items` = (start,end) prompt ranges of the batch's
+ * items; patches: host or device bf16 [4*tokens, patch_dim] in item
+ * order (window-major patch order within an item).
+ * Output: merged embeddings [tokens, d_llm] bf16 (device, ctx staging) in
+ * LLM row-major token order; returned pointer valid until the next encode. */
+rs_status rs_encode(rs_ctx* ctx, const uint64_t* items, int32_t n_items,
+                    const void* patches, int32_t patches_on_host,
+                    void** out_embeddings_dev);
+/* stage_time_ms seam (cost_model.hpp:76-82): one chunk through this
+ * context's layers. slices: n x (request id, start, end). Reads the chunk
+ * rows from the request slots (first stage) and appends to the paged KV.
+ * When the context owns the LM head, requests whose slice ends at their
+ * prompt end get first-token logits (rs_logits).                        */
+rs_status rs_prefill_chunk(rs_ctx* ctx, const uint64_t* slices, int32_t n_slices);
+rs_status rs_logits(rs_ctx* ctx, uint64_t id, float* out_host, int32_t* out_argmax);
+rs_status rs_synchronize(rs_ctx* ctx);
+
+/* ---- the engine on the device ------------------------------------------
+ * run_simulation (simengine.hpp:522-526) with the B200 backend.
+ * clock: 0 = lock-step (event order from the cost model — bit-exact vs the
+ * reference; work executed for real), 1 = real clock (GPU timestamps).
+ * Payloads (pixels, token ids) are generated from per-request hashes.
+ * e2e: inputs staged from pinned host memory inside the run, logits read
+ * back to host at completion.                                          */
+typedef struct rs_run_options {
+  int32_t clock;        /* 0 lock-step, 1 real clock */
+  int32_t e2e;          /* 1: H2D inputs / D2H logits inside the run */
+  uint64_t payload_seed;
+} rs_run_options;
+typedef struct rs_run_stats {
+  double wall_ms;            /* host wall time of the run                 */
+  double gpu_ms;             /* first launch -> last completion (events)  */
+  uint64_t h2d_bytes, d2h_bytes;
+  uint64_t kernel_launches;  /* our kernels launched during the run       */
+  double encode_gpu_ms, prefill_gpu_ms; /* summed per-op device time      */
+} rs_run_stats;
+rs_status rs_engine_run(rs_ctx* ctx, const char* workload_text,
+                        const rs_sim_config* cfg, const rs_run_options* opt,
+                        char** out_result, char** out_journal,
+                        rs_run_stats* out_stats);
+
+#ifdef __cplusplus
+}  /* extern "C" */
+#endif
+#endif  /* RSERVE_H_ */

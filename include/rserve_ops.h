@@ -1,0 +1,36 @@
+/* rserve-b200 — op-level C-ABI: one product kernel per call, raw device
+ * pointers, explicit cudaStream_t (passed as void*; NULL = legacy default).
+ * Used by the parity tests (tests/test_ops_gpu.py) and the micro-benchmarks.
+ * These ops have no reference counterpart (the reference has no device
+ * code); each one implements a piece of the work hidden
+ * behind encode_time_ms / stage_time_ms (cost_model.hpp:68-82).           */
+#ifndef RSERVE_OPS_H_
+#define RSERVE_OPS_H_
+
+#include "rserve.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum { RS_EPI_STORE = 0, RS_EPI_RESIDUAL = 1, RS_EPI_SWIGLU = 2, RS_EPI_GELU = 3,
+       RS_EPI_STORE_F32 = 4 };
+
+/* C[M,N] = epi(A[M,K] . B[N,K]^T) on tcgen05 (K-major bf16 operands). */
+rs_status rs_op_gemm(const void* A, int lda, const void* B, int ldb, void* C, int ldc,
+                     const void* bias, const void* residual, int ldr, const int* row_map,
+                     int M, int N, int K, int epi, int force_bn, void* stream);
+/* y = rmsnorm(x) * w (Qwen2 semantics: fp32 normalise, bf16 cast, scale). */
+rs_status rs_op_rmsnorm(const void* x, int ldx, const void* w, void* y, int ldy, int rows,
+                        int dim, float eps, void* stream);
+/* Varlen bidirectional attention over packed QKV [total, 3*heads*hd]. */
+rs_status rs_op_attention_varlen(const void* qkv, int ld_qkv, void* out, int ld_out,
+                                 const int* cu_seqlens, int n_seqs, int max_seqlen, int total,
+                                 int heads, int head_dim, float scale, void* stream);
+/* Kernel launches issued by this process so far (our kernels only). */
+unsigned long long rs_kernel_launches(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RSERVE_OPS_H_ */

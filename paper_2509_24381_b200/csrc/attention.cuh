@@ -1,0 +1,43 @@
+// rserve-b200 — attention kernels.
+//
+// (a) ViT varlen bidirectional attention over packed QKV rows (window
+//     layers: one sequence per 8x8-patch window; full layers: one sequence
+//     per image), head_dim 64 / 80.
+// (b) LLM causal chunked-prefill attention: the chunk's query rows (one or
+//     more request slices) attend to their request's paged KV cache up to
+//     their own position, GQA, head_dim 64 / 128.
+// Both are flash-style (online softmax, fp32 statistics) on bf16 tensor-core
+// MMAs with cp.async double-buffered K/V tiles.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include "common.cuh"
+
+namespace rserve {
+
+void attention_varlen_bidir(const bf16* qkv, int ld_qkv, bf16* out, int ld_out,
+                            const int* cu_seqlens, int n_seqs, int max_seqlen, int total,
+                            int heads, int head_dim, float scale, cudaStream_t stream);
+
+// One unit of chunked-prefill attention work: 64 query rows of one slice.
+struct PrefillWork {
+  int q_row0;     // first chunk row of this block
+  int q_rows;     // valid rows (<= 64)
+  int q_pos0;     // prompt position of q_row0
+  int req_slot;   // index into the per-request page-table array
+};
+
+struct PagedKV {
+  bf16* k;  // [pages][kv_heads][page][head_dim] for one layer
+  bf16* v;
+  const int* const* page_tables;  // device array: req_slot -> int* page ids
+  int page_size;
+};
+
+void attention_prefill_paged(const bf16* q, int ld_q, bf16* out, int ld_out,
+                             const PrefillWork* work, int n_work, const PagedKV& kv,
+                             int q_heads, int kv_heads, int head_dim, float scale,
+                             cudaStream_t stream);
+
+}  // namespace rserve

@@ -1,0 +1,388 @@
+// rserve-b200 — HBM-bound kernels (see kernels.cuh). All row kernels use one
+// warp per row with 16-byte vector accesses; grids are sized to whole waves
+// of the 148 SMs and loop over rows.
+#include <cuda_runtime.h>
+
+#include <cmath>
+
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace rserve {
+namespace {
+
+constexpr int kWarpsPerBlock = 8;
+
+int row_grid(std::int64_t rows) {
+  const std::int64_t blocks = ceil_div64(rows, kWarpsPerBlock);
+  const std::int64_t cap = static_cast<std::int64_t>(kNumSMs) * 16;
+  return static_cast<int>(blocks < cap ? (blocks > 0 ? blocks : 1) : cap);
+}
+
+__global__ void fill_uniform_kernel(bf16* dst, std::int64_t rows, int cols, int ld,
+                                    std::uint64_t seed, std::uint64_t stream, float scale,
+                                    float offset) {
+  const std::int64_t total = rows * ld;
+  for (std::int64_t e = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; e < total;
+       e += static_cast<std::int64_t>(gridDim.x) * blockDim.x) {
+    const std::int64_t r = e / ld;
+    const int c = static_cast<int>(e % ld);
+    float v = 0.f;
+    if (c < cols) {
+      const std::uint64_t z = mix64(seed, stream, static_cast<std::uint64_t>(r) * cols + c);
+      const float u = static_cast<float>(z >> 40) * (1.0f / 16777216.0f);
+      v = (2.0f * u - 1.0f) * scale + offset;
+    }
+    dst[e] = __float2bfloat16_rn(v);
+  }
+}
+
+__global__ void fill_const_kernel(bf16* dst, std::int64_t n, float v) {
+  for (std::int64_t e = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; e < n;
+       e += static_cast<std::int64_t>(gridDim.x) * blockDim.x)
+    dst[e] = __float2bfloat16_rn(v);
+}
+
+__global__ void fill_ids_kernel(std::int32_t* dst, std::int64_t n, std::uint64_t seed,
+                                std::uint64_t stream, std::uint32_t modulo) {
+  for (std::int64_t e = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; e < n;
+       e += static_cast<std::int64_t>(gridDim.x) * blockDim.x)
+    dst[e] = static_cast<std::int32_t>(mix64(seed, stream, static_cast<std::uint64_t>(e)) % modulo);
+}
+
+__global__ void rmsnorm_kernel(const bf16* __restrict__ x, int ldx, const bf16* __restrict__ w,
+                               bf16* __restrict__ y, int ldy, int rows, int dim, float eps,
+                               const std::int64_t* __restrict__ row_map, bf16* __restrict__ x_copy,
+                               int ld_copy, const int* rows_dev) {
+  const int lane = threadIdx.x & 31;
+  const int n = rows_dev != nullptr ? min(*rows_dev, rows) : rows;
+  for (int m = blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5); m < n;
+       m += gridDim.x * kWarpsPerBlock) {
+    const std::int64_t src = row_map != nullptr ? row_map[m] : m;
+    const bf16* xr = x + src * ldx;
+    float ss = 0.f;
+    for (int c = lane * 8; c < dim; c += 256) {
+      const uint4 v = *reinterpret_cast<const uint4*>(xr + c);
+      const std::uint32_t vw[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        const float2 f = unpack_bf16x2(vw[t]);
+        ss += f.x * f.x + f.y * f.y;
+      }
+      if (x_copy != nullptr)
+        *reinterpret_cast<uint4*>(x_copy + static_cast<std::int64_t>(m) * ld_copy + c) = v;
+    }
+    ss = warp_sum(ss);
+    const float inv = rsqrtf(ss / static_cast<float>(dim) + eps);
+    bf16* yr = y + static_cast<std::int64_t>(m) * ldy;
+    for (int c = lane * 8; c < dim; c += 256) {
+      const uint4 v = *reinterpret_cast<const uint4*>(xr + c);
+      const uint4 g = *reinterpret_cast<const uint4*>(w + c);
+      const std::uint32_t vw[4] = {v.x, v.y, v.z, v.w};
+      const std::uint32_t gw[4] = {g.x, g.y, g.z, g.w};
+      std::uint32_t o[4];
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        const float2 f = unpack_bf16x2(vw[t]);
+        const float2 gg = unpack_bf16x2(gw[t]);
+        // Qwen2 RMSNorm: normalise in fp32, cast to bf16, then scale.
+        const float a = bf2f(f2bf(f.x * inv)) * gg.x;
+        const float b = bf2f(f2bf(f.y * inv)) * gg.y;
+        o[t] = pack_bf16x2(a, b);
+      }
+      *reinterpret_cast<uint4*>(yr + c) = make_uint4(o[0], o[1], o[2], o[3]);
+    }
+  }
+}
+
+// One warp per (row, head) pair of rotations for q and k.
+__global__ void rope_vit_kernel(bf16* qkv, int ld, const std::int32_t* __restrict__ pos_hw,
+                                int rows, int heads, int hd, float log2_theta) {
+  const int lane = threadIdx.x & 31;
+  const int half = hd / 2, quarter = hd / 4;
+  const std::int64_t items = static_cast<std::int64_t>(rows) * heads * 2;
+  for (std::int64_t it = blockIdx.x * static_cast<std::int64_t>(kWarpsPerBlock) + (threadIdx.x >> 5);
+       it < items; it += static_cast<std::int64_t>(gridDim.x) * kWarpsPerBlock) {
+    const int which = static_cast<int>(it % 2);  // 0 = q, 1 = k
+    const int head = static_cast<int>((it / 2) % heads);
+    const std::int64_t row = it / (2 * heads);
+    bf16* v = qkv + row * ld + (which * heads + head) * hd;
+    const float ph = static_cast<float>(pos_hw[2 * row]);
+    const float pw = static_cast<float>(pos_hw[2 * row + 1]);
+    for (int i = lane; i < half; i += 32) {
+      const int j = i < quarter ? i : i - quarter;
+      const float freq = exp2f(-log2_theta * (4.0f * j) / static_cast<float>(hd));
+      const float ang = (i < quarter ? ph : pw) * freq;
+      float s, c;
+      sincosf(ang, &s, &c);
+      const float a = bf2f(v[i]), b = bf2f(v[i + half]);
+      v[i] = f2bf(a * c - b * s);
+      v[i + half] = f2bf(b * c + a * s);
+    }
+  }
+}
+
+__global__ void rope_kv_append_kernel(bf16* qkv, int ld, const ChunkRowInfo* __restrict__ info,
+                                      int rows, int q_heads, int kv_heads, int hd,
+                                      float log2_theta, bf16* k_cache, bf16* v_cache,
+                                      const int* const* page_tables, int page_size,
+                                      const int* rows_dev) {
+  const int lane = threadIdx.x & 31;
+  const int half = hd / 2;
+  const int s_t = hd / 8, s_h = hd / 8 + (3 * hd) / 16;
+  const int n = rows_dev != nullptr ? min(*rows_dev, rows) : rows;
+  const int heads_total = q_heads + 2 * kv_heads;
+  const std::int64_t items = static_cast<std::int64_t>(n) * heads_total;
+  for (std::int64_t it = blockIdx.x * static_cast<std::int64_t>(kWarpsPerBlock) + (threadIdx.x >> 5);
+       it < items; it += static_cast<std::int64_t>(gridDim.x) * kWarpsPerBlock) {
+    const int head = static_cast<int>(it % heads_total);
+    const int row = static_cast<int>(it / heads_total);
+    const ChunkRowInfo ri = info[row];
+    bf16* v = qkv + static_cast<std::int64_t>(row) * ld + head * hd;
+    const bool is_v = head >= q_heads + kv_heads;
+    if (!is_v) {
+      for (int i = lane; i < half; i += 32) {
+        const int sec = i < s_t ? 0 : (i < s_h ? 1 : 2);
+        const float freq = exp2f(-log2_theta * (2.0f * i) / static_cast<float>(hd));
+        const float ang = static_cast<float>(ri.rope[sec]) * freq;
+        float s, c;
+        sincosf(ang, &s, &c);
+        const float a = bf2f(v[i]), b = bf2f(v[i + half]);
+        v[i] = f2bf(a * c - b * s);
+        v[i + half] = f2bf(b * c + a * s);
+      }
+    }
+    if (head >= q_heads) {
+      __syncwarp();
+      const int kvh = is_v ? head - q_heads - kv_heads : head - q_heads;
+      const int* pt = page_tables[ri.req_slot];
+      const std::int64_t dst =
+          ((static_cast<std::int64_t>(pt[ri.pos / page_size]) * kv_heads + kvh) * page_size +
+           ri.pos % page_size) *
+          hd;
+      bf16* cache = is_v ? v_cache : k_cache;
+      for (int c = lane * 8; c < hd; c += 256)
+        *reinterpret_cast<uint4*>(cache + dst + c) = *reinterpret_cast<const uint4*>(v + c);
+    }
+  }
+}
+
+__global__ void scatter_rows_kernel(const bf16* __restrict__ src, int n_rows,
+                                    const std::int64_t* __restrict__ dst_rows, bf16* slab, int d,
+                                    std::uint32_t* bitmap, const std::uint64_t* __restrict__ ranges,
+                                    int n_ranges) {
+  const int lane = threadIdx.x & 31;
+  const int warp_global = blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
+  const int warps = gridDim.x * kWarpsPerBlock;
+  // Bitmap bits: one thread per 32-bit word per range (few words).
+  if (blockIdx.x == 0) {
+    for (int r = 0; r < n_ranges; ++r) {
+      const std::uint64_t b = ranges[2 * r], e = ranges[2 * r + 1];
+      for (std::uint64_t w = (b >> 5) + threadIdx.x; w <= ((e - 1) >> 5); w += blockDim.x) {
+        const std::uint64_t lo = max(b, w << 5), hi = min(e, (w + 1) << 5);
+        const unsigned span = static_cast<unsigned>(hi - lo);
+        const std::uint32_t mask =
+            span == 32 ? 0xFFFFFFFFu : (((1u << span) - 1u) << static_cast<unsigned>(lo & 31));
+        atomicOr(bitmap + w, mask);
+      }
+    }
+  }
+  const int vec = d / 8;
+  for (int r = warp_global; r < n_rows; r += warps) {
+    const uint4* s = reinterpret_cast<const uint4*>(src + static_cast<std::int64_t>(r) * d);
+    uint4* o = reinterpret_cast<uint4*>(slab + dst_rows[r] * d);
+    for (int c = lane; c < vec; c += 32) o[c] = s[c];
+  }
+}
+
+__global__ void ready_prefix_kernel(const std::uint32_t* __restrict__ bitmap, std::uint64_t frontier,
+                                    std::uint64_t total, std::uint64_t* out) {
+  const int lane = threadIdx.x;
+  const std::uint64_t n_words = (total + 31) >> 5;
+  std::uint64_t result = total;
+  for (std::uint64_t w0 = frontier >> 5; w0 < n_words; w0 += 32) {
+    const std::uint64_t w = w0 + lane;
+    std::uint32_t word = w < n_words ? bitmap[w] : 0u;
+    if (w == (frontier >> 5)) word |= (1u << (frontier & 31)) - 1u;  // bits below frontier
+    const unsigned has_zero = __ballot_sync(0xffffffffu, w < n_words && word != 0xFFFFFFFFu);
+    if (has_zero != 0) {
+      const int first = __ffs(has_zero) - 1;
+      const std::uint32_t fw = __shfl_sync(0xffffffffu, word, first);
+      const std::uint64_t hit = ((w0 + first) << 5) + static_cast<std::uint64_t>(__ffs(~fw) - 1);
+      result = hit < total ? hit : total;
+      break;
+    }
+  }
+  if (lane == 0) *out = result;
+}
+
+__global__ void gather_text_kernel(const bf16* __restrict__ vocab, const std::int32_t* __restrict__ ids,
+                                   int n, const std::int64_t* __restrict__ dst_rows, bf16* slab,
+                                   int d) {
+  const int lane = threadIdx.x & 31;
+  const int vec = d / 8;
+  for (int r = blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5); r < n;
+       r += gridDim.x * kWarpsPerBlock) {
+    const uint4* s = reinterpret_cast<const uint4*>(vocab + static_cast<std::int64_t>(ids[r]) * d);
+    uint4* o = reinterpret_cast<uint4*>(slab + dst_rows[r] * d);
+    for (int c = lane; c < vec; c += 32) o[c] = s[c];
+  }
+}
+
+__global__ void bitmap_set_kernel(std::uint32_t* bitmap, const std::uint64_t* ranges, int n_ranges) {
+  for (int r = 0; r < n_ranges; ++r) {
+    const std::uint64_t b = ranges[2 * r], e = ranges[2 * r + 1];
+    if (e <= b) continue;
+    for (std::uint64_t w = (b >> 5) + threadIdx.x + static_cast<std::uint64_t>(blockIdx.x) * blockDim.x;
+         w <= ((e - 1) >> 5); w += static_cast<std::uint64_t>(gridDim.x) * blockDim.x) {
+      const std::uint64_t lo = max(b, w << 5), hi = min(e, (w + 1) << 5);
+      const unsigned span = static_cast<unsigned>(hi - lo);
+      const std::uint32_t mask =
+          span == 32 ? 0xFFFFFFFFu : (((1u << span) - 1u) << static_cast<unsigned>(lo & 31));
+      atomicOr(bitmap + w, mask);
+    }
+  }
+}
+
+__global__ void argmax_kernel(const float* __restrict__ logits, int vocab, std::int32_t* out) {
+  const float* row = logits + static_cast<std::int64_t>(blockIdx.x) * vocab;
+  float best = -INFINITY;
+  int idx = 0x7fffffff;
+  for (int i = threadIdx.x; i < vocab; i += blockDim.x) {
+    const float v = row[i];
+    if (v > best || (v == best && i < idx)) {
+      best = v;
+      idx = i;
+    }
+  }
+  __shared__ float sb[32];
+  __shared__ int si[32];
+  for (int o = 16; o > 0; o >>= 1) {
+    const float ob = __shfl_xor_sync(0xffffffffu, best, o);
+    const int oi = __shfl_xor_sync(0xffffffffu, idx, o);
+    if (ob > best || (ob == best && oi < idx)) {
+      best = ob;
+      idx = oi;
+    }
+  }
+  if ((threadIdx.x & 31) == 0) {
+    sb[threadIdx.x >> 5] = best;
+    si[threadIdx.x >> 5] = idx;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < static_cast<int>(blockDim.x >> 5); ++w)
+      if (sb[w] > best || (sb[w] == best && si[w] < idx)) {
+        best = sb[w];
+        idx = si[w];
+      }
+    out[blockIdx.x] = idx;
+  }
+}
+
+int elem_grid(std::int64_t n) {
+  const std::int64_t b = ceil_div64(n, 256);
+  const std::int64_t cap = static_cast<std::int64_t>(kNumSMs) * 32;
+  return static_cast<int>(b < 1 ? 1 : (b < cap ? b : cap));
+}
+
+}  // namespace
+
+void fill_uniform(bf16* dst, std::int64_t rows, int cols, int ld, std::uint64_t seed,
+                  std::uint64_t stream, float scale, float offset, cudaStream_t st) {
+  if (rows <= 0) return;
+  fill_uniform_kernel<<<elem_grid(rows * ld), 256, 0, st>>>(dst, rows, cols, ld, seed, stream,
+                                                           scale, offset);
+  RS_LAUNCH_CHECK();
+  count_launch();
+}
+
+void fill_const(bf16* dst, std::int64_t n, float v, cudaStream_t st) {
+  if (n <= 0) return;
+  fill_const_kernel<<<elem_grid(n), 256, 0, st>>>(dst, n, v);
+  RS_LAUNCH_CHECK();
+  count_launch();
+}
+
+void fill_ids(std::int32_t* dst, std::int64_t n, std::uint64_t seed, std::uint64_t stream,
+              std::uint32_t modulo, cudaStream_t st) {
+  if (n <= 0) return;
+  fill_ids_kernel<<<elem_grid(n), 256, 0, st>>>(dst, n, seed, stream, modulo);
+  RS_LAUNCH_CHECK();
+  count_launch();
+}
+
+void rmsnorm(const bf16* x, int ldx, const bf16* w, bf16* y, int ldy, int rows, int dim, float eps,
+             cudaStream_t st, const std::int64_t* row_map, bf16* x_copy, int ld_copy,
+             const int* rows_dev) {
+  if (rows <= 0) return;
+  if (dim % 8 != 0) throw DeviceError(RS_ERR_CUDA, "rmsnorm: dim % 8 != 0");
+  rmsnorm_kernel<<<row_grid(rows), 32 * kWarpsPerBlock, 0, st>>>(x, ldx, w, y, ldy, rows, dim, eps,
+                                                                row_map, x_copy, ld_copy, rows_dev);
+  RS_LAUNCH_CHECK();
+  count_launch();
+}
+
+void rope_vit(bf16* qkv, int ld, const std::int32_t* pos_hw, int rows, int heads, int hd,
+              float theta, cudaStream_t st) {
+  if (rows <= 0) return;
+  rope_vit_kernel<<<row_grid(static_cast<std::int64_t>(rows) * heads * 2), 32 * kWarpsPerBlock, 0,
+                    st>>>(qkv, ld, pos_hw, rows, heads, hd, std::log2(theta));
+  RS_LAUNCH_CHECK();
+  count_launch();
+}
+
+void rope_kv_append(bf16* qkv, int ld, const ChunkRowInfo* rows_info, int rows, int q_heads,
+                    int kv_heads, int hd, float theta, bf16* k_cache, bf16* v_cache,
+                    const int* const* page_tables, int page_size, cudaStream_t st,
+                    const int* rows_dev) {
+  if (rows <= 0) return;
+  rope_kv_append_kernel<<<row_grid(static_cast<std::int64_t>(rows) * (q_heads + 2 * kv_heads)),
+                          32 * kWarpsPerBlock, 0, st>>>(qkv, ld, rows_info, rows, q_heads, kv_heads,
+                                                        hd, std::log2(theta), k_cache, v_cache,
+                                                        page_tables, page_size, rows_dev);
+  RS_LAUNCH_CHECK();
+  count_launch();
+}
+
+void scatter_rows_and_mark(const bf16* src, int n_rows, const std::int64_t* dst_rows, bf16* slab,
+                           int d, std::uint32_t* bitmap, const std::uint64_t* ranges, int n_ranges,
+                           cudaStream_t st) {
+  if (d % 8 != 0) throw DeviceError(RS_ERR_CUDA, "scatter: d % 8 != 0");
+  scatter_rows_kernel<<<row_grid(n_rows > 0 ? n_rows : 1), 32 * kWarpsPerBlock, 0, st>>>(
+      src, n_rows, dst_rows, slab, d, bitmap, ranges, n_ranges);
+  RS_LAUNCH_CHECK();
+  count_launch();
+}
+
+void ready_prefix(const std::uint32_t* bitmap, std::uint64_t frontier, std::uint64_t total,
+                  std::uint64_t* out, cudaStream_t st) {
+  ready_prefix_kernel<<<1, 32, 0, st>>>(bitmap, frontier, total, out);
+  RS_LAUNCH_CHECK();
+  count_launch();
+}
+
+void gather_text_embeddings(const bf16* vocab, const std::int32_t* ids, int n,
+                            const std::int64_t* dst_rows, bf16* slab, int d, cudaStream_t st) {
+  if (n <= 0) return;
+  gather_text_kernel<<<row_grid(n), 32 * kWarpsPerBlock, 0, st>>>(vocab, ids, n, dst_rows, slab, d);
+  RS_LAUNCH_CHECK();
+  count_launch();
+}
+
+void bitmap_set_ranges(std::uint32_t* bitmap, const std::uint64_t* ranges, int n_ranges,
+                       cudaStream_t st) {
+  if (n_ranges <= 0) return;
+  bitmap_set_kernel<<<1, 256, 0, st>>>(bitmap, ranges, n_ranges);
+  RS_LAUNCH_CHECK();
+  count_launch();
+}
+
+void argmax_rows(const float* logits, int rows, int vocab, std::int32_t* out, cudaStream_t st) {
+  if (rows <= 0) return;
+  argmax_kernel<<<rows, 256, 0, st>>>(logits, vocab, out);
+  RS_LAUNCH_CHECK();
+  count_launch();
+}
+
+}  // namespace rserve

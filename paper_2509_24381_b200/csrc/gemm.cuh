@@ -1,0 +1,53 @@
+// rserve-b200 — persistent, warp-specialised tcgen05 GEMM for sm_100a.
+//
+//   C[M, N] = epilogue( A[M, K] . B[N, K]^T )      (A, B bf16, K-major)
+//
+// One CTA per SM (grid = min(tiles, 148)), 128 x BN output tiles, BK = 64.
+// warp 0: TMA producer (128B-swizzled tiles, multi-stage mbarrier ring);
+// warp 1: single-thread tcgen05.mma issuer (M=128, N=BN, K=16, FP32 in
+//         TMEM, double-buffered accumulators so the epilogue of tile i
+//         overlaps the MMAs of tile i+1);
+// warp 2: TMEM allocator; warps 4-7: epilogue (tcgen05.ld -> fused op ->
+//         bf16/fp32 global stores).
+// Fused epilogues cover every linear layer of the ViT and the LLM: bias,
+// in-place residual add, SwiGLU (gate/up interleaved in 16-row blocks),
+// exact-erf GELU, fp32 logits, and an optional output-row map used to scatter
+// merger rows straight into LLM token order / embedding slots.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "common.cuh"
+
+namespace rserve {
+
+enum class Epi : int {
+  Store = 0,     // C = acc (+ bias)                       bf16
+  Residual = 1,  // C = acc (+ bias) + R   (R may alias C)  bf16
+  SwiGLU = 2,    // C[:, j] = silu(g_j) * u_j, N/2 columns  bf16
+  Gelu = 3,      // C = gelu_erf(acc + bias)                bf16
+  StoreF32 = 4,  // C = acc (+ bias)                       fp32
+};
+
+struct GemmArgs {
+  const bf16* A = nullptr;  // [M, K] row stride lda (elements)
+  int lda = 0;
+  const bf16* B = nullptr;  // [N, K] row stride ldb
+  int ldb = 0;
+  void* C = nullptr;        // [M, N] (SwiGLU: [M, N/2]) row stride ldc
+  int ldc = 0;
+  const bf16* bias = nullptr;      // [N] or null
+  const bf16* residual = nullptr;  // Residual epilogue, row stride ldr
+  int ldr = 0;
+  const int* row_map = nullptr;    // optional: output row of input row m
+  int M = 0, N = 0, K = 0;
+  const int* M_dev = nullptr;      // optional device-side M (<= M), graph-friendly
+};
+
+/// Launches the tcgen05 GEMM. Requires K % 8 == 0, N % 16 == 0,
+/// 16-byte aligned rows. Tile width is picked for wave efficiency.
+void gemm(const GemmArgs& args, Epi epi, cudaStream_t stream, int force_bn = 0);
+
+}  // namespace rserve

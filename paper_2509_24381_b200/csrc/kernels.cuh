@@ -1,0 +1,85 @@
+// rserve-b200 — memory-bound kernels of the pipeline (HBM roofline):
+// norms, rotary embeddings, paged-KV append, the embedding-tracker data
+// plane (K6 scatter + bitmap, K7 ready prefix, K8 text gather, chunk
+// gather), LM-head helpers and the seeded weight / payload generators.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "common.cuh"
+
+namespace rserve {
+
+// ---- deterministic synthetic values (mirrored by oracle/model_oracle.py) ----
+// u = splitmix64(seed*G + stream*H + i) >> 40, scaled to [0, 1) with 24 bits.
+__host__ __device__ inline std::uint64_t mix64(std::uint64_t seed, std::uint64_t stream,
+                                               std::uint64_t i) {
+  std::uint64_t z = seed * 0x9E3779B97F4A7C15ull + stream * 0xD1B54A32D192ED03ull + i;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+/// dst[i] = bf16((2u - 1) * scale) (+ offset), i < n, row-padded: element
+/// (r, c) of a [rows, cols] tensor stored with stride ld; c >= cols -> 0.
+/// The hash index is r * cols + c (independent of padding).
+void fill_uniform(bf16* dst, std::int64_t rows, int cols, int ld, std::uint64_t seed,
+                  std::uint64_t stream, float scale, float offset, cudaStream_t st);
+/// Same values into an fp32 buffer (for oracles' consumption / debugging).
+void fill_const(bf16* dst, std::int64_t n, float v, cudaStream_t st);
+/// int32 ids in [0, modulo): id = mix64(seed, stream, i) % modulo.
+void fill_ids(std::int32_t* dst, std::int64_t n, std::uint64_t seed, std::uint64_t stream,
+              std::uint32_t modulo, cudaStream_t st);
+
+// ---- norms -------------------------------------------------------------------
+/// y[m] = x[src(m)] * rsqrt(mean(x^2) + eps) * w ; src(m) = row_map ? row_map[m] : m.
+/// When x_copy != null the raw source row is also copied to x_copy[m].
+void rmsnorm(const bf16* x, int ldx, const bf16* w, bf16* y, int ldy, int rows, int dim,
+             float eps, cudaStream_t st, const std::int64_t* row_map = nullptr,
+             bf16* x_copy = nullptr, int ld_copy = 0, const int* rows_dev = nullptr);
+
+// ---- rotary --------------------------------------------------------------------
+/// ViT 2D RoPE in place on packed QKV rows [P, 3*H*hd]: q and k of every
+/// head; pair (i, i + hd/2) rotated by pos_h * f_i (i < hd/4) or
+/// pos_w * f_{i - hd/4}, f_j = theta^(-4j/hd). pos: [P, 2] (h, w).
+void rope_vit(bf16* qkv, int ld, const std::int32_t* pos_hw, int rows, int heads, int hd,
+              float theta, cudaStream_t st);
+
+struct ChunkRowInfo {  // one chunk row (prefill token)
+  std::int32_t req_slot;  // per-request tables index
+  std::int32_t pos;       // prompt position (KV index)
+  std::int32_t rope[3];   // M-RoPE (t, h, w) position ids
+  std::int32_t pad;
+};
+/// LLM M-RoPE on q and k of packed QKV rows [M, (Hq + 2 Hkv) hd], then the
+/// rotated k and v are appended to the paged KV cache of the row's request.
+/// Sections over the hd/2 frequency pairs: t [0, hd/8), h [hd/8, 5hd/16),
+/// w [5hd/16, hd/2) (Qwen2-VL mrope_section [16, 24, 24] at hd = 128).
+void rope_kv_append(bf16* qkv, int ld, const ChunkRowInfo* rows_info, int rows, int q_heads,
+                    int kv_heads, int hd, float theta, bf16* k_cache, bf16* v_cache,
+                    const int* const* page_tables, int page_size, cudaStream_t st,
+                    const int* rows_dev = nullptr);
+
+// ---- embedding tracker data plane (K6 / K7 / K8) ----------------------------------
+/// K6: dst rows (slot rows of the slab) <- src rows, d bf16 each; and set
+/// readiness bits [bit_begin[i], bit_end[i]) of `bitmap` for n_ranges ranges.
+void scatter_rows_and_mark(const bf16* src, int n_rows, const std::int64_t* dst_rows, bf16* slab,
+                           int d, std::uint32_t* bitmap, const std::uint64_t* ranges,
+                           int n_ranges, cudaStream_t st);
+/// K7: first clear bit at or after `frontier` (capped at total) -> *out.
+void ready_prefix(const std::uint32_t* bitmap, std::uint64_t frontier, std::uint64_t total,
+                  std::uint64_t* out, cudaStream_t st);
+/// K8: slab[dst_rows[i]] <- vocab[ids[i]] for n text tokens.
+void gather_text_embeddings(const bf16* vocab, const std::int32_t* ids, int n,
+                            const std::int64_t* dst_rows, bf16* slab, int d, cudaStream_t st);
+/// Set bits [begin, end) for n ranges (text ranges at creation).
+void bitmap_set_ranges(std::uint32_t* bitmap, const std::uint64_t* ranges, int n_ranges,
+                       cudaStream_t st);
+
+// ---- LM head helpers ---------------------------------------------------------------------
+/// out[i] = argmax(logits[i, :vocab]) (first max).
+void argmax_rows(const float* logits, int rows, int vocab, std::int32_t* out, cudaStream_t st);
+
+}  // namespace rserve

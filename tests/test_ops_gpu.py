@@ -1,0 +1,144 @@
+"""Parity of the individual sm_100a kernels against plain fp32 PyTorch references.
+
+Tolerances (bf16 inputs, fp32 accumulation, bf16 outputs): relative error of
+the whole output tensor ||out - ref|| / ||ref|| <= 1e-2, plus elementwise
+|out - ref| <= 2e-2 * max|ref| + 2e-2.
+"""
+import math
+
+import pytest
+
+torch = pytest.importorskip("torch")
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def nat():
+    from paper_2509_24381_b200 import _native
+    return _native
+
+
+def _close(out, ref, rel=1e-2, atol_frac=2e-2):
+    out = out.float()
+    ref = ref.float()
+    err = (out - ref).norm() / ref.norm().clamp_min(1e-12)
+    assert err.item() <= rel, f"relative error {err.item():.3e}"
+    bound = atol_frac * ref.abs().max() + 2e-2
+    assert (out - ref).abs().max().item() <= bound.item()
+
+
+def _stream():
+    return torch.cuda.current_stream().cuda_stream
+
+
+def _gemm(nat, A, B, C, epi, bias=None, residual=None, row_map=None, bn=0, M=None):
+    M = A.shape[0] if M is None else M
+    N, K = B.shape
+    nat.check(nat.lib.rs_op_gemm(
+        A.data_ptr(), A.stride(0), B.data_ptr(), B.stride(0), C.data_ptr(), C.stride(0),
+        bias.data_ptr() if bias is not None else None,
+        residual.data_ptr() if residual is not None else None,
+        residual.stride(0) if residual is not None else 0,
+        row_map.data_ptr() if row_map is not None else None,
+        M, N, K, epi, bn, _stream()))
+
+
+SHAPES = [
+    (128, 256, 64), (1, 256, 64), (300, 384, 200), (4096, 1280, 1176), (512, 4608, 3584),
+    (129, 144, 72), (2048, 1280, 3424), (7, 152064 // 16, 512),
+]
+
+
+@pytest.mark.parametrize("M,N,K", SHAPES)
+@pytest.mark.parametrize("bn", [128, 256])
+def test_gemm_store(nat, M, N, K, bn):
+    torch.manual_seed(M * 7 + N + K)
+    A = torch.randn(M, K, device="cuda", dtype=torch.bfloat16)
+    B = torch.randn(N, K, device="cuda", dtype=torch.bfloat16) * 0.05
+    bias = torch.randn(N, device="cuda", dtype=torch.bfloat16) * 0.1
+    C = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+    _gemm(nat, A, B, C, 0, bias=bias, bn=bn)
+    torch.cuda.synchronize()
+    ref = A.float() @ B.float().t() + bias.float()
+    _close(C, ref)
+
+
+def test_gemm_residual_inplace_and_f32(nat):
+    M, N, K = 777, 1280, 640
+    A = torch.randn(M, K, device="cuda", dtype=torch.bfloat16)
+    B = torch.randn(N, K, device="cuda", dtype=torch.bfloat16) * 0.05
+    X = torch.randn(M, N, device="cuda", dtype=torch.bfloat16)
+    ref = X.float() + A.float() @ B.float().t()
+    _gemm(nat, A, B, X, 1, residual=X)  # in place: X += A B^T
+    torch.cuda.synchronize()
+    _close(X, ref)
+    C = torch.empty(M, N, device="cuda", dtype=torch.float32)
+    _gemm(nat, A, B, C, 4)
+    torch.cuda.synchronize()
+    _close(C, A.float() @ B.float().t(), rel=5e-3)
+
+
+def test_gemm_swiglu_interleaved(nat):
+    M, ff, K = 300, 3424, 1280
+    A = torch.randn(M, K, device="cuda", dtype=torch.bfloat16)
+    G = torch.randn(ff, K, device="cuda", dtype=torch.bfloat16) * 0.03
+    U = torch.randn(ff, K, device="cuda", dtype=torch.bfloat16) * 0.03
+    # 16-row interleave: [g0..15, u0..15, g16..31, u16..31, ...]
+    W = torch.stack([G.view(ff // 16, 16, K), U.view(ff // 16, 16, K)], 1).reshape(2 * ff, K)
+    C = torch.empty(M, ff, device="cuda", dtype=torch.bfloat16)
+    _gemm(nat, A, W, C, 2)
+    torch.cuda.synchronize()
+    g = A.float() @ G.float().t()
+    u = A.float() @ U.float().t()
+    _close(C, torch.nn.functional.silu(g) * u)
+
+
+def test_gemm_gelu_rowmap(nat):
+    M, N, K = 256, 512, 256
+    A = torch.randn(M, K, device="cuda", dtype=torch.bfloat16)
+    B = torch.randn(N, K, device="cuda", dtype=torch.bfloat16) * 0.05
+    perm = torch.randperm(M, device="cuda").to(torch.int32)
+    C = torch.zeros(M, N, device="cuda", dtype=torch.bfloat16)
+    _gemm(nat, A, B, C, 3, row_map=perm)
+    torch.cuda.synchronize()
+    ref = torch.nn.functional.gelu(A.float() @ B.float().t())
+    out = torch.empty_like(C)
+    out[perm.long()] = C[perm.long()]
+    _close(C[perm.long()], ref)
+
+
+def test_rmsnorm(nat):
+    rows, dim = 1000, 3584
+    x = torch.randn(rows, dim, device="cuda", dtype=torch.bfloat16) * 3
+    w = torch.rand(dim, device="cuda", dtype=torch.bfloat16) + 0.5
+    y = torch.empty_like(x)
+    nat.check(nat.lib.rs_op_rmsnorm(x.data_ptr(), dim, w.data_ptr(), y.data_ptr(), dim, rows,
+                                    dim, 1e-6, _stream()))
+    torch.cuda.synchronize()
+    xf = x.float()
+    ref = (xf * torch.rsqrt(xf.pow(2).mean(-1, keepdim=True) + 1e-6)).bfloat16().float() * w.float()
+    _close(y, ref, rel=5e-3)
+
+
+@pytest.mark.parametrize("hd,heads,lens", [(80, 4, [64, 64, 37, 64]), (80, 2, [1024, 300]),
+                                           (64, 4, [256, 256, 5]), (128, 2, [130, 1])])
+def test_attention_varlen_bidir(nat, hd, heads, lens):
+    total = sum(lens)
+    qkv = torch.randn(total, 3 * heads * hd, device="cuda", dtype=torch.bfloat16)
+    cu = torch.tensor([0] + list(torch.tensor(lens).cumsum(0)), dtype=torch.int32, device="cuda")
+    out = torch.empty(total, heads * hd, device="cuda", dtype=torch.bfloat16)
+    scale = 1.0 / math.sqrt(hd)
+    nat.check(nat.lib.rs_op_attention_varlen(qkv.data_ptr(), qkv.stride(0), out.data_ptr(),
+                                             out.stride(0), cu.data_ptr(), len(lens), max(lens),
+                                             total, heads, hd, scale, _stream()))
+    torch.cuda.synchronize()
+    q, k, v = qkv.float().view(total, 3, heads, hd).unbind(1)
+    ref = torch.empty(total, heads, hd, device="cuda")
+    s0 = 0
+    for n in lens:
+        qs, ks, vs = q[s0:s0 + n], k[s0:s0 + n], v[s0:s0 + n]
+        att = torch.einsum("qhd,khd->hqk", qs, ks) * scale
+        ref[s0:s0 + n] = torch.einsum("hqk,khd->qhd", att.softmax(-1), vs)
+        s0 += n
+    _close(out, ref.view(total, heads * hd))
