@@ -27,6 +27,12 @@
 #include <stddef.h>
 #include <stdint.h>
 
+#if defined(__GNUC__)
+#define RS_API __attribute__((visibility("default")))
+#else
+#define RS_API
+#endif
+
 #ifdef __cplusplus
 extern "C" {
 #endif
@@ -49,10 +55,10 @@ typedef enum rs_status {
   RS_ERR_UNKNOWN = 99
 } rs_status;
 
-const char* rs_last_error(void);
-void rs_free(void* p);
+RS_API const char* rs_last_error(void);
+RS_API void rs_free(void* p);
 /* Build identification, e.g. "rserve-b200 sm_100a tcgen05". */
-const char* rs_version(void);
+RS_API const char* rs_version(void);
 
 /* ---- host-side config PODs --------------------------------------------- */
 enum { RS_POLICY_VANILLA_PP = 0, RS_POLICY_EPD_BASELINE = 1,
@@ -102,24 +108,24 @@ typedef struct rs_workload_config { /* workload.hpp:109-136 */
  * (`id,arrival_ms,slo|-,layout` lines; workload.hpp:217-265).            */
 
 /* generate_workload (workload.hpp:139-172) -> workload text */
-rs_status rs_generate_workload(const rs_workload_config* cfg, char** out_text);
+RS_API rs_status rs_generate_workload(const rs_workload_config* cfg, char** out_text);
 
 /* run_simulation (simengine.hpp:522-526) on the analytic cost model.
  * out_result: canonical decision log (see DESIGN.md §"Decision log"):
  * per-request records, slices, trace, release order; doubles in shortest
  * round-trip form so equal text == bit-identical results.              */
-rs_status rs_simulate(const char* workload_text, const rs_sim_config* cfg,
+RS_API rs_status rs_simulate(const char* workload_text, const rs_sim_config* cfg,
                       char** out_result, char** out_journal);
 
 /* One report row (experiment.hpp:72-101 run_cell + metrics.hpp:173-194):
  * generate -> run -> compute_report -> CSV row. slo_ttft_ms < 0: none.   */
-rs_status rs_experiment_cell(const rs_workload_config* wcfg,
+RS_API rs_status rs_experiment_cell(const rs_workload_config* wcfg,
                              const rs_sim_config* cfg, double slo_ttft_ms,
                              char** out_csv_row);
 
 /* Algorithm 1 (encoder_sched.hpp:48-74): batches as text lines
  * "request item_idx:start-end,... total". C == RS_WHOLE_REQUEST allowed. */
-rs_status rs_plan_batches(const char* layout, uint64_t request_id,
+RS_API rs_status rs_plan_batches(const char* layout, uint64_t request_id,
                           uint64_t c_tokens, char** out_text);
 
 /* ---- device pipeline context -------------------------------------------- */
@@ -140,7 +146,7 @@ typedef struct rs_model_config {
 } rs_model_config;
 
 /* Fills the preset shapes: TINY (cfg1), QWEN25VL_7B (cfg2-4), 72B-LLM (cfg5). */
-rs_status rs_model_preset(int32_t preset, rs_model_config* out);
+RS_API rs_status rs_model_preset(int32_t preset, rs_model_config* out);
 
 typedef struct rs_ctx_options {
   int32_t device;              /* CUDA ordinal for this process            */
@@ -154,40 +160,40 @@ typedef struct rs_ctx_options {
   int32_t with_lm_head;        /* allocate final norm + LM head here         */
 } rs_ctx_options;
 
-rs_status rs_ctx_create(const rs_model_config* model, const rs_ctx_options* opt,
+RS_API rs_status rs_ctx_create(const rs_model_config* model, const rs_ctx_options* opt,
                         rs_ctx** out);
-rs_status rs_ctx_destroy(rs_ctx* ctx);
+RS_API rs_status rs_ctx_destroy(rs_ctx* ctx);
 
 /* ---- tracker data plane (device) ----------------------------------------
  * Replaces EmbeddingTracker ctor (tracker.hpp:44-59) + create_tracker
  * (193-198): reserves slot pages for the request, uploads text token ids,
  * gathers text embeddings into the slots (K8), initialises the readiness
  * bitmap with text = 1 and keeps the host tracker mirror.               */
-rs_status rs_request_create(rs_ctx* ctx, uint64_t id, const char* layout,
+RS_API rs_status rs_request_create(rs_ctx* ctx, uint64_t id, const char* layout,
                             const int32_t* text_token_ids /* may be NULL */);
 /* mark_encoded / on_embeddings_ready (tracker.hpp:83-105,
  * token_sched.hpp:184-187): scatter [tokens, d_llm] bf16 rows (device
  * pointer, row-major, in item order) into the item's slots and set its
  * bitmap bits (K6); host mirror is updated and errors mirror the
  * reference (AlignmentError / DoubleEncodeError).                       */
-rs_status rs_mark_encoded(rs_ctx* ctx, uint64_t id, uint64_t start, uint64_t end,
+RS_API rs_status rs_mark_encoded(rs_ctx* ctx, uint64_t id, uint64_t start, uint64_t end,
                           const void* embeddings_dev);
 /* schedulable_tokens (tracker.hpp:79) from the host mirror, plus the
  * device ready-prefix (K7, warp ballot over the bitmap) for cross-check. */
-rs_status rs_schedulable(rs_ctx* ctx, uint64_t id, uint64_t* host_count,
+RS_API rs_status rs_schedulable(rs_ctx* ctx, uint64_t id, uint64_t* host_count,
                          uint64_t* device_count);
 /* advance_prefill (tracker.hpp:109-122). */
-rs_status rs_advance_prefill(rs_ctx* ctx, uint64_t id, uint64_t n,
+RS_API rs_status rs_advance_prefill(rs_ctx* ctx, uint64_t id, uint64_t n,
                              uint64_t* out_start, uint64_t* out_end);
 /* release (tracker.hpp:126-135) + slot-page free once fully released. */
-rs_status rs_release(rs_ctx* ctx, uint64_t id, uint64_t start, uint64_t end);
-rs_status rs_request_erase(rs_ctx* ctx, uint64_t id);
+RS_API rs_status rs_release(rs_ctx* ctx, uint64_t id, uint64_t start, uint64_t end);
+RS_API rs_status rs_request_erase(rs_ctx* ctx, uint64_t id);
 /* Device bitmap words (ceil(T/32) u32) and slot rows (bf16) read back. */
-rs_status rs_read_bitmap(rs_ctx* ctx, uint64_t id, uint32_t* out_words, uint64_t n_words);
-rs_status rs_read_slots(rs_ctx* ctx, uint64_t id, uint64_t start, uint64_t end,
+RS_API rs_status rs_read_bitmap(rs_ctx* ctx, uint64_t id, uint32_t* out_words, uint64_t n_words);
+RS_API rs_status rs_read_slots(rs_ctx* ctx, uint64_t id, uint64_t start, uint64_t end,
                         void* out_host_bf16);
 /* live / peak / released token accounting of the host mirror. */
-rs_status rs_tracker_stats(rs_ctx* ctx, uint64_t id, uint64_t out[6]);
+RS_API rs_status rs_tracker_stats(rs_ctx* ctx, uint64_t id, uint64_t out[6]);
 
 /* ---- compute entry points ------------------------------------------------
  * encode_time_ms seam (cost_model.hpp:68-71): ViT forward of one
@@ -196,7 +202,7 @@ rs_status rs_tracker_stats(rs_ctx* ctx, uint64_t id, uint64_t out[6]);
  * order (window-major patch order within an item).
  * Output: merged embeddings [tokens, d_llm] bf16 (device, ctx staging) in
  * LLM row-major token order; returned pointer valid until the next encode. */
-rs_status rs_encode(rs_ctx* ctx, const uint64_t* items, int32_t n_items,
+RS_API rs_status rs_encode(rs_ctx* ctx, const uint64_t* items, int32_t n_items,
                     const void* patches, int32_t patches_on_host,
                     void** out_embeddings_dev);
 /* stage_time_ms seam (cost_model.hpp:76-82): one chunk through this
@@ -204,9 +210,9 @@ rs_status rs_encode(rs_ctx* ctx, const uint64_t* items, int32_t n_items,
  * rows from the request slots (first stage) and appends to the paged KV.
  * When the context owns the LM head, requests whose slice ends at their
  * prompt end get first-token logits (rs_logits).                        */
-rs_status rs_prefill_chunk(rs_ctx* ctx, const uint64_t* slices, int32_t n_slices);
-rs_status rs_logits(rs_ctx* ctx, uint64_t id, float* out_host, int32_t* out_argmax);
-rs_status rs_synchronize(rs_ctx* ctx);
+RS_API rs_status rs_prefill_chunk(rs_ctx* ctx, const uint64_t* slices, int32_t n_slices);
+RS_API rs_status rs_logits(rs_ctx* ctx, uint64_t id, float* out_host, int32_t* out_argmax);
+RS_API rs_status rs_synchronize(rs_ctx* ctx);
 
 /* ---- the engine on the device ------------------------------------------
  * run_simulation (simengine.hpp:522-526) with the B200 backend.
@@ -227,7 +233,7 @@ typedef struct rs_run_stats {
   uint64_t kernel_launches;  /* our kernels launched during the run       */
   double encode_gpu_ms, prefill_gpu_ms; /* summed per-op device time      */
 } rs_run_stats;
-rs_status rs_engine_run(rs_ctx* ctx, const char* workload_text,
+RS_API rs_status rs_engine_run(rs_ctx* ctx, const char* workload_text,
                         const rs_sim_config* cfg, const rs_run_options* opt,
                         char** out_result, char** out_journal,
                         rs_run_stats* out_stats);

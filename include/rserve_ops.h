@@ -17,18 +17,18 @@ enum { RS_EPI_STORE = 0, RS_EPI_RESIDUAL = 1, RS_EPI_SWIGLU = 2, RS_EPI_GELU = 3
        RS_EPI_STORE_F32 = 4 };
 
 /* C[M,N] = epi(A[M,K] . B[N,K]^T) on tcgen05 (K-major bf16 operands). */
-rs_status rs_op_gemm(const void* A, int lda, const void* B, int ldb, void* C, int ldc,
+RS_API rs_status rs_op_gemm(const void* A, int lda, const void* B, int ldb, void* C, int ldc,
                      const void* bias, const void* residual, int ldr, const int* row_map,
                      int M, int N, int K, int epi, int force_bn, void* stream);
 /* y = rmsnorm(x) * w (Qwen2 semantics: fp32 normalise, bf16 cast, scale). */
-rs_status rs_op_rmsnorm(const void* x, int ldx, const void* w, void* y, int ldy, int rows,
+RS_API rs_status rs_op_rmsnorm(const void* x, int ldx, const void* w, void* y, int ldy, int rows,
                         int dim, float eps, void* stream);
 /* Varlen bidirectional attention over packed QKV [total, 3*heads*hd]. */
-rs_status rs_op_attention_varlen(const void* qkv, int ld_qkv, void* out, int ld_out,
+RS_API rs_status rs_op_attention_varlen(const void* qkv, int ld_qkv, void* out, int ld_out,
                                  const int* cu_seqlens, int n_seqs, int max_seqlen, int total,
                                  int heads, int head_dim, float scale, void* stream);
 /* Kernel launches issued by this process so far (our kernels only). */
-unsigned long long rs_kernel_launches(void);
+RS_API unsigned long long rs_kernel_launches(void);
 
 #ifdef __cplusplus
 }

@@ -37,6 +37,8 @@
 // Only the POD config structs of the boundary header.
 #include "../include/rserve.h"
 
+#define REF_API __attribute__((visibility("default")))
+
 using namespace lmmsim;
 
 namespace {
@@ -198,10 +200,10 @@ std::vector<std::string> releases_from(const SimResult& r, int stages, bool firs
 
 extern "C" {
 
-const char* ref_last_error(void) { return g_err.c_str(); }
-void ref_free(void* p) { std::free(p); }
+REF_API const char* ref_last_error(void) { return g_err.c_str(); }
+REF_API void ref_free(void* p) { std::free(p); }
 
-int ref_generate_workload(const rs_workload_config* w, char** out) {
+REF_API int ref_generate_workload(const rs_workload_config* w, char** out) {
   try {
     std::ostringstream os;
     write_workload(os, generate_workload(to_wcfg(*w)));
@@ -212,7 +214,7 @@ int ref_generate_workload(const rs_workload_config* w, char** out) {
   }
 }
 
-int ref_simulate(const char* workload, const rs_sim_config* cfg, char** out) {
+REF_API int ref_simulate(const char* workload, const rs_sim_config* cfg, char** out) {
   try {
     const SimConfig sc = to_sim(*cfg);
     const SimResult r = run_simulation(parse_workload(workload), sc);
@@ -224,7 +226,7 @@ int ref_simulate(const char* workload, const rs_sim_config* cfg, char** out) {
 }
 
 // Wall-clock of run_simulation over `reps` repetitions (ns per run).
-int ref_time_simulate(const char* workload, const rs_sim_config* cfg, int reps,
+REF_API int ref_time_simulate(const char* workload, const rs_sim_config* cfg, int reps,
                       double* ns_per_run) {
   try {
     const SimConfig sc = to_sim(*cfg);
@@ -241,7 +243,7 @@ int ref_time_simulate(const char* workload, const rs_sim_config* cfg, int reps,
   }
 }
 
-int ref_experiment_cell(const rs_workload_config* w, const rs_sim_config* cfg,
+REF_API int ref_experiment_cell(const rs_workload_config* w, const rs_sim_config* cfg,
                         double slo, char** out) {
   try {
     const SimConfig sc = to_sim(*cfg);
@@ -282,7 +284,7 @@ int ref_experiment_cell(const rs_workload_config* w, const rs_sim_config* cfg,
   }
 }
 
-int ref_plan_batches(const char* layout, std::uint64_t id, std::uint64_t c, char** out) {
+REF_API int ref_plan_batches(const char* layout, std::uint64_t id, std::uint64_t c, char** out) {
   try {
     RequestSpec r;
     r.id = id;
@@ -308,7 +310,7 @@ int ref_plan_batches(const char* layout, std::uint64_t id, std::uint64_t c, char
 // are the reference engine's (simengine.hpp:275-441) written over the
 // reference components; only the ORDER comes from the journal. Output:
 // decision log without times.
-int ref_replay(const char* workload, const rs_sim_config* cfg, const char* journal,
+REF_API int ref_replay(const char* workload, const rs_sim_config* cfg, const char* journal,
                char** out) {
   try {
     const SimConfig sc = to_sim(*cfg);
@@ -393,12 +395,16 @@ int ref_replay(const char* workload, const rs_sim_config* cfg, const char* journ
       stage_trace(0, c);
     };
 
-    std::istringstream js(journal ? journal : "");
-    int kind;
-    std::uint32_t a;
-    std::uint64_t b;
-    std::string t;
-    while (js >> kind >> a >> b >> t) {
+    // Journal lines "<kind> <a> <b> <time>" parsed without iostream numeric
+    // facets (this .so may carry its own static C++ runtime).
+    std::vector<std::string_view> lines = split(journal ? journal : "", '\n');
+    for (std::string_view line : lines) {
+      if (line.empty()) continue;
+      const std::vector<std::string_view> f = split(line, ' ');
+      if (f.size() != 4) throw InputError("journal: bad line '" + std::string(line) + "'");
+      const int kind = static_cast<int>(parse_u64(f[0], "journal kind"));
+      const std::uint32_t a = static_cast<std::uint32_t>(parse_u64(f[1], "journal a"));
+      const std::uint64_t b = parse_u64(f[2], "journal b");
       switch (kind) {
         case 0: {
           const RequestSpec& q = reqs.at(b);

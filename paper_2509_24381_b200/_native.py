@@ -18,7 +18,7 @@ if not os.path.exists(LIB_PATH):
         f"rserve-b200 native library not built: {LIB_PATH} missing "
         "(run `python -c 'import __graft_entry__ as g; g.build()'`)")
 
-lib = C.CDLL(LIB_PATH, mode=C.RTLD_GLOBAL)
+lib = C.CDLL(LIB_PATH)
 
 # ---- status -----------------------------------------------------------------
 RS_OK = 0

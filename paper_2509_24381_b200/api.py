@@ -1,0 +1,322 @@
+"""Python mirror of the reference's host API, over the rserve-b200 C-ABI.
+
+Names and meanings follow proj/include/lmmsim/ (simengine.hpp SimConfig,
+cost_model.hpp CostModel, workload.hpp WorkloadConfig / RequestTemplate,
+token_sched.hpp Policy). Errors are raised as the same exception classes
+(errors.hpp:23-80). Everything here is a thin ctypes layer: the scheduling
+core is C++ (include/lmmsim/) and the compute is sm_100a CUDA.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+from typing import Dict, List, Optional, Sequence, Tuple
+
+from . import _native as N
+
+POLICIES = {"vanilla_pp": 0, "epd_baseline": 1, "intra_only": 2, "rserve": 3}
+PATTERNS = {"alternating": 0, "consecutive_mm": 1, "text_first": 2}
+WHOLE_REQUEST = 0xFFFFFFFFFFFFFFFF
+
+
+@dataclass
+class CostModel:  # cost_model.hpp:37-45
+    alpha_enc_ms: float = 0.0
+    beta_enc_ms_per_token: float = 0.0
+    eps_tx_ms: float = 0.0
+    zeta_tx_ms_per_token: float = 0.0
+    gamma_stage_ms: float = 0.0
+    delta_stage_ms_per_token: float = 0.0
+    kappa_attn_ms: float = 0.0
+    tp_speedup: float = 1.0
+
+
+@dataclass
+class SimConfig:  # simengine.hpp:48-75
+    policy: str = "rserve"
+    pipeline_mode: Optional[str] = None  # "cpp" | "vanilla" | None (policy default)
+    stages: int = 4
+    token_budget: int = 512
+    embedding_batch_tokens: int = 1024  # or WHOLE_REQUEST
+    encoder_workers: int = 1
+    release_at: str = "last_stage"
+    hidden_size: int = 4096
+    cost: CostModel = field(default_factory=CostModel)
+
+    def to_c(self) -> N.rs_sim_config:
+        c = N.rs_sim_config()
+        if self.policy not in POLICIES:
+            raise N.ConfigError(f"policy: unknown name '{self.policy}' (expected vanilla_pp, "
+                                "epd_baseline, intra_only or rserve)")
+        c.policy = POLICIES[self.policy]
+        c.pipeline_mode = {None: -1, "cpp": 0, "vanilla": 1}[self.pipeline_mode]
+        c.stages = self.stages
+        c.encoder_workers = self.encoder_workers
+        c.token_budget = self.token_budget
+        c.embedding_batch_tokens = self.embedding_batch_tokens
+        c.release_at = 0 if self.release_at == "first_stage" else 1
+        c.hidden_size = self.hidden_size
+        for k in ("alpha_enc_ms", "beta_enc_ms_per_token", "eps_tx_ms", "zeta_tx_ms_per_token",
+                  "gamma_stage_ms", "delta_stage_ms_per_token", "kappa_attn_ms", "tp_speedup"):
+            setattr(c.cost, k, getattr(self.cost, k))
+        return c
+
+
+@dataclass
+class IntDistribution:
+    lo: int = 1
+    hi: Optional[int] = None  # None = constant(lo)
+
+    def to_c(self) -> N.rs_int_dist:
+        d = N.rs_int_dist()
+        d.uniform = 0 if self.hi is None else 1
+        d.lo = self.lo
+        d.hi = self.lo if self.hi is None else self.hi
+        return d
+
+
+@dataclass
+class RequestTemplate:  # workload.hpp:71-107
+    pattern: str = "alternating"
+    num_mm_items: IntDistribution = field(default_factory=lambda: IntDistribution(1))
+    mm_item_tokens: IntDistribution = field(default_factory=lambda: IntDistribution(512))
+    text_segment_tokens: IntDistribution = field(default_factory=lambda: IntDistribution(128))
+    probability: float = 1.0
+
+
+@dataclass
+class WorkloadConfig:  # workload.hpp:109-136
+    arrival_rate: float = 1.0
+    duration_s: float = 10.0
+    seed: int = 0
+    templates: List[RequestTemplate] = field(default_factory=lambda: [RequestTemplate()])
+    slo_ttft_ms: Optional[float] = None
+
+    def to_c(self):
+        arr = (N.rs_template * len(self.templates))()
+        for i, t in enumerate(self.templates):
+            arr[i].pattern = PATTERNS[t.pattern]
+            arr[i].num_mm_items = t.num_mm_items.to_c()
+            arr[i].mm_item_tokens = t.mm_item_tokens.to_c()
+            arr[i].text_segment_tokens = t.text_segment_tokens.to_c()
+            arr[i].probability = t.probability
+        w = N.rs_workload_config()
+        w.arrival_rate = self.arrival_rate
+        w.duration_s = self.duration_s
+        w.seed = self.seed
+        w.templates = C.cast(arr, C.POINTER(N.rs_template))
+        w.n_templates = len(self.templates)
+        w.has_slo = 0 if self.slo_ttft_ms is None else 1
+        w.slo_ttft_ms = self.slo_ttft_ms or 0.0
+        return w, arr  # keep `arr` alive
+
+
+def _dist_from_json(j) -> IntDistribution:
+    if "constant" in j:
+        return IntDistribution(int(j["constant"]))
+    lo, hi = j["uniform"]
+    return IntDistribution(int(lo), int(hi))
+
+
+def experiment_from_json(j: dict):
+    """(WorkloadConfig template, SimConfig, policies, rates, seeds, slo) from an
+    experiment JSON (config.hpp:171-300 key names)."""
+    w = j["workload"]
+    templates = [RequestTemplate(t["pattern"], _dist_from_json(t["num_mm_items"]),
+                                 _dist_from_json(t["mm_item_tokens"]),
+                                 _dist_from_json(t["text_segment_tokens"]), float(t["probability"]))
+                 for t in w["templates"]]
+    cm = j["cost_model"]
+    cost = CostModel(**{k: float(v) for k, v in cm.items()})
+    c = j["embedding_batch_size_C"]
+    sim = SimConfig(stages=int(j["stages"]), token_budget=int(j["token_budget_B"]),
+                    embedding_batch_tokens=WHOLE_REQUEST if c == "whole_request" else int(c),
+                    encoder_workers=int(j.get("encoder_workers", 1)),
+                    release_at=j.get("release_at", "last_stage"),
+                    pipeline_mode=j.get("pipeline_mode"), hidden_size=int(j.get("hidden_size", 4096)),
+                    cost=cost)
+    slo = j.get("slo_ttft_ms")
+    wl = WorkloadConfig(duration_s=float(w["duration_s"]), templates=templates,
+                        slo_ttft_ms=None if slo is None else float(slo))
+    return wl, sim, list(j["policies"]), [float(r) for r in j["rates"]], \
+        [int(s) for s in j["seeds"]], slo
+
+
+def _out():
+    return C.c_char_p()
+
+
+def generate_workload(cfg: WorkloadConfig) -> str:
+    w, keep = cfg.to_c()
+    out = _out()
+    N.check(N.lib.rs_generate_workload(C.byref(w), C.byref(out)))
+    return N.take_string(out)
+
+
+def simulate(workload: str, cfg: SimConfig) -> Tuple[str, str]:
+    """run_simulation on the analytic cost model -> (decision log, journal)."""
+    res, jr = _out(), _out()
+    c = cfg.to_c()
+    N.check(N.lib.rs_simulate(workload.encode(), C.byref(c), C.byref(res), C.byref(jr)))
+    return N.take_string(res), N.take_string(jr)
+
+
+def experiment_cell(wcfg: WorkloadConfig, cfg: SimConfig, slo_ttft_ms: Optional[float]) -> str:
+    w, keep = wcfg.to_c()
+    c = cfg.to_c()
+    out = _out()
+    N.check(N.lib.rs_experiment_cell(C.byref(w), C.byref(c),
+                                     -1.0 if slo_ttft_ms is None else float(slo_ttft_ms),
+                                     C.byref(out)))
+    return N.take_string(out)
+
+
+def plan_batches(layout: str, request_id: int, c_tokens: int) -> str:
+    out = _out()
+    N.check(N.lib.rs_plan_batches(layout.encode(), request_id, c_tokens, C.byref(out)))
+    return N.take_string(out)
+
+
+def parse_decision_log(text: str) -> Dict[str, list]:
+    """Decision log text -> {'result': dict, 'req': [...], 'slice': [...], ...}."""
+    out: Dict[str, list] = {}
+    for line in text.splitlines():
+        kind, *fields = line.split(" ")
+        rec = {}
+        for f in fields:
+            k, _, v = f.partition("=")
+            rec[k] = v
+        out.setdefault(kind, []).append(rec)
+    return out
+
+
+# ---------------------------------------------------------------------------
+MODEL_PRESETS = {"tiny": 0, "qwen2.5-vl-7b": 1, "qwen2.5-vl-72b-llm": 2}
+
+
+def model_preset(name: str, **overrides) -> N.rs_model_config:
+    m = N.rs_model_config()
+    N.check(N.lib.rs_model_preset(MODEL_PRESETS[name], C.byref(m)))
+    for k, v in overrides.items():
+        setattr(m, k, v)
+    return m
+
+
+class Pipeline:
+    """One device context (rs_ctx): weights, embedding slots, KV pools."""
+
+    def __init__(self, model: N.rs_model_config, device: int = 0, max_prompt_tokens: int = 32768,
+                 slot_tokens: int = 65536, kv_tokens: int = 65536, max_chunk_tokens: int = 2048,
+                 max_encode_tokens: int = 2048, layer_begin: int = 0, layer_end: int = 0,
+                 with_vit: bool = True, with_lm_head: bool = True):
+        self.model = model
+        o = N.rs_ctx_options()
+        o.device = device
+        o.max_prompt_tokens = max_prompt_tokens
+        o.slot_tokens = slot_tokens
+        o.kv_tokens = kv_tokens
+        o.max_chunk_tokens = max_chunk_tokens
+        o.max_encode_tokens = max_encode_tokens
+        o.layer_begin = layer_begin
+        o.layer_end = layer_end
+        o.with_vit = int(with_vit)
+        o.with_lm_head = int(with_lm_head)
+        self.opts = o
+        h = C.c_void_p()
+        N.check(N.lib.rs_ctx_create(C.byref(model), C.byref(o), C.byref(h)))
+        self.h = h
+
+    def close(self):
+        if self.h:
+            N.check(N.lib.rs_ctx_destroy(self.h))
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # tracker data plane -------------------------------------------------------
+    def request_create(self, req_id: int, layout: str, text_ids=None):
+        ptr = None
+        if text_ids is not None:
+            import numpy as np
+            arr = np.ascontiguousarray(text_ids, dtype=np.int32)
+            self._keep = arr
+            ptr = arr.ctypes.data
+        N.check(N.lib.rs_request_create(self.h, req_id, layout.encode(), ptr))
+
+    def mark_encoded(self, req_id: int, start: int, end: int, emb_dev_ptr: int):
+        N.check(N.lib.rs_mark_encoded(self.h, req_id, start, end, emb_dev_ptr))
+
+    def schedulable(self, req_id: int) -> Tuple[int, int]:
+        a, b = C.c_uint64(), C.c_uint64()
+        N.check(N.lib.rs_schedulable(self.h, req_id, C.byref(a), C.byref(b)))
+        return a.value, b.value
+
+    def advance_prefill(self, req_id: int, n: int) -> Tuple[int, int]:
+        a, b = C.c_uint64(), C.c_uint64()
+        N.check(N.lib.rs_advance_prefill(self.h, req_id, n, C.byref(a), C.byref(b)))
+        return a.value, b.value
+
+    def release(self, req_id: int, start: int, end: int):
+        N.check(N.lib.rs_release(self.h, req_id, start, end))
+
+    def erase(self, req_id: int):
+        N.check(N.lib.rs_request_erase(self.h, req_id))
+
+    def read_bitmap(self, req_id: int, total_tokens: int):
+        import numpy as np
+        out = np.zeros((total_tokens + 31) // 32, dtype=np.uint32)
+        N.check(N.lib.rs_read_bitmap(self.h, req_id, out.ctypes.data, out.size))
+        return out
+
+    def read_slots(self, req_id: int, start: int, end: int):
+        import numpy as np
+        d = self.model.llm_dim
+        out = np.zeros((end - start, d), dtype=np.uint16)
+        N.check(N.lib.rs_read_slots(self.h, req_id, start, end, out.ctypes.data))
+        return out
+
+    def tracker_stats(self, req_id: int) -> Dict[str, int]:
+        a = (C.c_uint64 * 6)()
+        N.check(N.lib.rs_tracker_stats(self.h, req_id, a))
+        keys = ("live", "peak_live", "released", "frontier", "schedulable", "all_encoded")
+        return dict(zip(keys, list(a)))
+
+    # compute --------------------------------------------------------------------
+    def encode(self, items: Sequence[Tuple[int, int]], patches_ptr: int, on_host: bool) -> int:
+        arr = (C.c_uint64 * (2 * len(items)))(*[v for it in items for v in it])
+        out = C.c_void_p()
+        N.check(N.lib.rs_encode(self.h, arr, len(items), patches_ptr, int(on_host), C.byref(out)))
+        return out.value
+
+    def prefill_chunk(self, slices: Sequence[Tuple[int, int, int]]):
+        arr = (C.c_uint64 * (3 * len(slices)))(*[v for s in slices for v in s])
+        N.check(N.lib.rs_prefill_chunk(self.h, arr, len(slices)))
+
+    def logits(self, req_id: int):
+        import numpy as np
+        out = np.zeros(self.model.vocab, dtype=np.float32)
+        am = C.c_int32()
+        N.check(N.lib.rs_logits(self.h, req_id, out.ctypes.data, C.byref(am)))
+        return out, am.value
+
+    def synchronize(self):
+        N.check(N.lib.rs_synchronize(self.h))
+
+    def run(self, workload: str, cfg: SimConfig, clock: str = "lockstep", e2e: bool = False,
+            payload_seed: int = 7):
+        """Engine run on this device -> (decision log, journal, stats dict)."""
+        o = N.rs_run_options()
+        o.clock = 1 if clock == "real" else 0
+        o.e2e = int(e2e)
+        o.payload_seed = payload_seed
+        res, jr = _out(), _out()
+        st = N.rs_run_stats()
+        c = cfg.to_c()
+        N.check(N.lib.rs_engine_run(self.h, workload.encode(), C.byref(c), C.byref(o),
+                                    C.byref(res), C.byref(jr), C.byref(st)))
+        stats = {k: getattr(st, k) for k, _ in N.rs_run_stats._fields_}
+        return N.take_string(res), N.take_string(jr), stats

@@ -1,0 +1,324 @@
+// rserve-b200 — the B200 ExecutionBackend (see device_backend.cuh).
+#include <algorithm>
+#include <cstring>
+
+#include "device_backend.cuh"
+#include "kernels.cuh"
+
+namespace rserve {
+
+namespace {
+std::uint64_t pixel_stream(std::uint64_t req, std::uint64_t item) {
+  return (5ull << 32) | (req << 12) | item;
+}
+}  // namespace
+
+DeviceBackend::DeviceBackend(Context& ctx, const lmmsim::SimConfig& cfg, bool realtime, bool e2e,
+                             std::uint64_t payload_seed)
+    : ctx_(ctx), cfg_(cfg), realtime_(realtime), e2e_(e2e), seed_(payload_seed) {
+  if (cfg.stages < 1) throw lmmsim::ConfigError("stages: must be >= 1");
+  const int workers = cfg.encoder_workers;
+  const Shapes& s = ctx.shapes();
+  enc_streams_.resize(static_cast<std::size_t>(workers));
+  for (auto& st : enc_streams_) RS_CUDA_CHECK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  // One prefill stream: all stages of this GPU share the SMs and the per-stage
+  // scratch; each chunk owns its residual buffer so stages can interleave.
+  stage_streams_.resize(1);
+  RS_CUDA_CHECK(cudaStreamCreateWithFlags(&stage_streams_[0], cudaStreamNonBlocking));
+  RS_CUDA_CHECK(cudaStreamCreateWithFlags(&copy_stream_, cudaStreamNonBlocking));
+  const std::size_t max_tok = ctx.options().max_encode_tokens;
+  for (int i = 0; i < workers * kRing; ++i) {
+    void* p = nullptr;
+    RS_CUDA_CHECK(cudaMalloc(&p, max_tok * s.d * sizeof(bf16)));
+    staging_.push_back(static_cast<bf16*>(p));
+    staging_free_.push_back(nullptr);
+  }
+  enc_ring_pos_.assign(static_cast<std::size_t>(workers), 0);
+  if (e2e_) {
+    for (int w = 0; w < workers; ++w) {
+      void* p = nullptr;
+      RS_CUDA_CHECK(cudaMalloc(&p, 4 * max_tok * s.pdim * sizeof(bf16)));
+      enc_input_.push_back(static_cast<bf16*>(p));
+    }
+  }
+  const int n_x = std::max(2, cfg.stages + 2);
+  for (int i = 0; i < n_x; ++i) {
+    void* p = nullptr;
+    RS_CUDA_CHECK(cudaMalloc(&p, ctx.options().max_chunk_tokens * s.d * sizeof(bf16)));
+    xbufs_.push_back(static_cast<bf16*>(p));
+    xbuf_guard_.push_back(nullptr);
+    free_xbufs_.push_back(i);
+  }
+  RS_CUDA_CHECK(cudaEventCreate(&origin_));
+}
+
+DeviceBackend::~DeviceBackend() {
+  cudaDeviceSynchronize();
+  for (auto& [id, p] : payloads_) {
+    if (p.patches_dev) cudaFree(p.patches_dev);
+    if (p.patches_host) cudaFreeHost(p.patches_host);
+  }
+  for (auto& [id, p] : logits_host_) cudaFreeHost(p);
+  for (bf16* p : staging_) cudaFree(p);
+  for (bf16* p : enc_input_) cudaFree(p);
+  for (bf16* p : xbufs_) cudaFree(p);
+  for (cudaEvent_t e : event_pool_) cudaEventDestroy(e);
+  if (origin_) cudaEventDestroy(origin_);
+  for (auto st : enc_streams_) cudaStreamDestroy(st);
+  for (auto st : stage_streams_) cudaStreamDestroy(st);
+  if (copy_stream_) cudaStreamDestroy(copy_stream_);
+}
+
+cudaEvent_t DeviceBackend::timing_event() {
+  cudaEvent_t e;
+  RS_CUDA_CHECK(cudaEventCreate(&e));
+  event_pool_.push_back(e);
+  return e;
+}
+
+void DeviceBackend::prepare(const std::vector<lmmsim::RequestSpec>& workload) {
+  const Shapes& s = ctx_.shapes();
+  cudaStream_t st = ctx_.aux_stream();
+  for (const lmmsim::RequestSpec& req : workload) {
+    std::uint64_t patches = 0;
+    for (const lmmsim::SegmentSpec& seg : req.segments)
+      if (seg.kind == lmmsim::SegmentKind::Multimodal) patches += 4 * seg.tokens;
+    Payload p;
+    p.patches = patches;
+    if (patches > 0) {
+      void* dev = nullptr;
+      RS_CUDA_CHECK(cudaMalloc(&dev, patches * s.pdim * sizeof(bf16)));
+      p.patches_dev = static_cast<bf16*>(dev);
+      std::uint64_t off = 0, item = 0;
+      for (const lmmsim::SegmentSpec& seg : req.segments) {
+        if (seg.kind != lmmsim::SegmentKind::Multimodal) continue;
+        fill_uniform(p.patches_dev + off * s.pdim, static_cast<std::int64_t>(4 * seg.tokens),
+                     s.pdim, s.pdim, seed_, pixel_stream(req.id, item), kPixelScale, 0.f, st);
+        off += 4 * seg.tokens;
+        ++item;
+      }
+      if (e2e_) {
+        void* host = nullptr;
+        RS_CUDA_CHECK(cudaMallocHost(&host, patches * s.pdim * sizeof(bf16)));
+        p.patches_host = static_cast<bf16*>(host);
+        RS_CUDA_CHECK(cudaMemcpyAsync(host, p.patches_dev, patches * s.pdim * sizeof(bf16),
+                                      cudaMemcpyDeviceToHost, st));
+      }
+    }
+    if (e2e_) {
+      void* lh = nullptr;
+      RS_CUDA_CHECK(cudaMallocHost(&lh, static_cast<std::size_t>(s.vocab) * 4));
+      logits_host_[req.id] = static_cast<float*>(lh);
+    }
+    payloads_[req.id] = p;
+  }
+  RS_CUDA_CHECK(cudaStreamSynchronize(st));
+  if (e2e_) {  // e2e runs read the pixels from pinned host memory only
+    for (auto& [id, p] : payloads_) {
+      if (p.patches_dev) cudaFree(p.patches_dev);
+      p.patches_dev = nullptr;
+    }
+  }
+}
+
+void DeviceBackend::start() {
+  RS_CUDA_CHECK(cudaDeviceSynchronize());
+  launches0_ = launches_so_far();
+  upload0_ = ctx_.uploader().bytes_uploaded();
+  RS_CUDA_CHECK(cudaEventRecord(origin_, ctx_.tracker_stream()));
+  RS_CUDA_CHECK(cudaEventSynchronize(origin_));
+  t0_ = std::chrono::steady_clock::now();
+}
+
+lmmsim::TimeMs DeviceBackend::clock_ms() {
+  return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0_).count();
+}
+
+void DeviceBackend::track(lmmsim::OpKind k, std::uint32_t a, std::uint64_t b, cudaEvent_t begin,
+                          cudaEvent_t end) {
+  ops_.push_back({k, a, b, begin, end});
+  last_event_ = end;
+}
+
+void DeviceBackend::on_request_created(const lmmsim::RequestSpec& req, const lmmsim::EmbeddingTracker&) {
+  cudaStream_t st = ctx_.tracker_stream();
+  DevRequest& r = ctx_.create_request(req, nullptr, seed_, st);
+  done_slots_[req.id] = r.slot;
+  if (e2e_) {
+    std::uint64_t text = 0;
+    for (const auto& [b, e] : r.text_ranges) text += e - b;
+    stats_.h2d_bytes += text * 4;  // token ids
+  }
+  if (!tracker_tail_) tracker_tail_ = ctx_.new_event();
+  RS_CUDA_CHECK(cudaEventRecord(tracker_tail_, st));
+}
+
+double DeviceBackend::launch_encode(int worker, std::size_t slot, const lmmsim::EncodeBatch& b) {
+  cudaStream_t st = enc_streams_[static_cast<std::size_t>(worker)];
+  DevRequest& r = ctx_.get(b.request_id);
+  const Shapes& s = ctx_.shapes();
+  const int ring = worker * kRing + enc_ring_pos_[static_cast<std::size_t>(worker)];
+  enc_ring_pos_[static_cast<std::size_t>(worker)] = (enc_ring_pos_[static_cast<std::size_t>(worker)] + 1) % kRing;
+  if (staging_free_[static_cast<std::size_t>(ring)] != nullptr)
+    RS_CUDA_CHECK(cudaStreamWaitEvent(st, staging_free_[static_cast<std::size_t>(ring)], 0));
+  slot_staging_[slot] = ring;
+
+  std::vector<lmmsim::TokenRange> items;
+  for (const auto& it : b.items) items.push_back(it.second);
+  const std::size_t first_item = b.items.front().first;
+  const std::uint64_t p0 = r.item_patch_offset[first_item];
+  const std::uint64_t np = 4 * b.total_tokens;
+  cudaEvent_t begin = timing_event(), end = timing_event();
+  RS_CUDA_CHECK(cudaEventRecord(begin, st));
+  const Payload& pay = payloads_.at(b.request_id);
+  const bf16* patches = nullptr;
+  if (e2e_) {
+    RS_CUDA_CHECK(cudaMemcpyAsync(enc_input_[static_cast<std::size_t>(worker)],
+                                  pay.patches_host + p0 * s.pdim, np * s.pdim * sizeof(bf16),
+                                  cudaMemcpyHostToDevice, st));
+    stats_.h2d_bytes += np * s.pdim * sizeof(bf16);
+    patches = enc_input_[static_cast<std::size_t>(worker)];
+  } else {
+    patches = pay.patches_dev + p0 * s.pdim;
+  }
+  const VitBatchPlan plan = ctx_.plan_batch(r, items);
+  ctx_.encode(plan, patches, staging_[static_cast<std::size_t>(ring)], st);
+  RS_CUDA_CHECK(cudaEventRecord(end, st));
+  slot_done_[slot] = end;
+  track(lmmsim::OpKind::Encode, static_cast<std::uint32_t>(worker), slot, begin, end);
+  return realtime_ ? 0.0 : lmmsim::encode_time_ms(cfg_.cost, b);
+}
+
+double DeviceBackend::launch_transfer(int /*worker*/, std::size_t slot, const lmmsim::EncodeBatch& b) {
+  // Co-located encoder and prefill: the embeddings are already in this GPU's
+  // HBM; the link is the reference's zero-cost case.
+  if (realtime_) ready_transfers_.emplace_back(slot, slot_done_ms_.count(slot) ? slot_done_ms_[slot] : clock_ms());
+  return realtime_ ? 0.0 : lmmsim::transfer_time_ms(cfg_.cost, b.total_tokens);
+}
+
+void DeviceBackend::on_embeddings_ready(std::size_t slot, const lmmsim::EncodeBatch& b) {
+  cudaStream_t st = ctx_.tracker_stream();
+  RS_CUDA_CHECK(cudaStreamWaitEvent(st, slot_done_.at(slot), 0));
+  DevRequest& r = ctx_.get(b.request_id);
+  std::vector<lmmsim::TokenRange> items;
+  for (const auto& it : b.items) items.push_back(it.second);
+  const int ring = slot_staging_.at(slot);
+  ctx_.scatter_items(r, items, staging_[static_cast<std::size_t>(ring)], st);
+  cudaEvent_t ev = ctx_.new_event();
+  RS_CUDA_CHECK(cudaEventRecord(ev, st));
+  staging_free_[static_cast<std::size_t>(ring)] = ev;
+  if (!tracker_tail_) tracker_tail_ = ctx_.new_event();
+  RS_CUDA_CHECK(cudaEventRecord(tracker_tail_, st));
+}
+
+double DeviceBackend::launch_stage(int stage, const lmmsim::ChunkView& c) {
+  cudaStream_t st = stage_streams_[0];
+  ChunkState& cs = chunks_[c.chunk_id];
+  if (stage == 0) {
+    if (free_xbufs_.empty()) throw DeviceError(RS_ERR_CUDA, "no free chunk buffer");
+    cs.buf = free_xbufs_.back();
+    free_xbufs_.pop_back();
+    cs.x = xbufs_[static_cast<std::size_t>(cs.buf)];
+    if (xbuf_guard_[static_cast<std::size_t>(cs.buf)] != nullptr)
+      RS_CUDA_CHECK(cudaStreamWaitEvent(st, xbuf_guard_[static_cast<std::size_t>(cs.buf)], 0));
+    if (tracker_tail_ != nullptr) {
+      // Snapshot: every scatter / creation issued so far precedes this chunk.
+      cudaEvent_t snap = ctx_.new_event();
+      RS_CUDA_CHECK(cudaEventRecord(snap, ctx_.tracker_stream()));
+      RS_CUDA_CHECK(cudaStreamWaitEvent(st, snap, 0));
+    }
+  }
+  std::vector<SliceRef> slices;
+  for (const auto& [id, range] : *c.slices) slices.push_back({&ctx_.get(id), range.start, range.end});
+  // Layers of this stage within the context's range.
+  const int lb = ctx_.llm()->layer_begin(), le = ctx_.llm()->layer_end();
+  const int S = cfg_.stages, n = le - lb;
+  const int from = lb + n * stage / S, to = lb + n * (stage + 1) / S;
+  cudaEvent_t begin = timing_event(), end = timing_event();
+  RS_CUDA_CHECK(cudaEventRecord(begin, st));
+  ctx_.prefill(slices, cs.x, st, from, to);
+  RS_CUDA_CHECK(cudaEventRecord(end, st));
+  cs.last = end;
+  track(lmmsim::OpKind::Stage, static_cast<std::uint32_t>(stage), c.chunk_id, begin, end);
+  if (stage + 1 == S) {  // residual buffer free once the last stage ran
+    xbuf_guard_[static_cast<std::size_t>(cs.buf)] = end;
+    free_xbufs_.push_back(cs.buf);
+  }
+  return realtime_ ? 0.0 : lmmsim::stage_time_ms(cfg_.cost, c.total_tokens, c.weighted_context);
+}
+
+void DeviceBackend::on_release(std::size_t chunk, lmmsim::RequestId id, lmmsim::TokenRange r) {
+  const ChunkState& cs = chunks_.at(chunk);
+  release_guard_ = cs.last;
+  DevRequest& dr = ctx_.get(id);
+  ctx_.release_prefix(dr, r.end, release_guard_);
+}
+
+void DeviceBackend::on_request_erased(lmmsim::RequestId id) {
+  ctx_.erase_request(id, release_guard_, /*keep_slot=*/true);
+}
+
+void DeviceBackend::on_request_complete(lmmsim::RequestId id, std::size_t chunk) {
+  if (!e2e_) return;
+  const ChunkState& cs = chunks_.at(chunk);
+  RS_CUDA_CHECK(cudaStreamWaitEvent(copy_stream_, cs.last, 0));
+  ctx_.copy_logits(done_slots_.at(id), logits_host_.at(id), copy_stream_);
+  stats_.d2h_bytes += static_cast<std::uint64_t>(ctx_.shapes().vocab) * 4;
+}
+
+void DeviceBackend::poll(std::vector<lmmsim::OpCompletion>& out) {
+  for (const auto& [slot, t] : ready_transfers_) out.push_back({lmmsim::OpKind::Transfer, 0, slot, t});
+  ready_transfers_.clear();
+  for (std::size_t i = 0; i < ops_.size();) {
+    const cudaError_t q = cudaEventQuery(ops_[i].end);
+    if (q == cudaErrorNotReady) {
+      ++i;
+      continue;
+    }
+    RS_CUDA_CHECK(q);
+    float ms = 0;
+    RS_CUDA_CHECK(cudaEventElapsedTime(&ms, origin_, ops_[i].end));
+    if (ops_[i].kind == lmmsim::OpKind::Encode) slot_done_ms_[ops_[i].b] = ms;
+    out.push_back({ops_[i].kind, ops_[i].a, ops_[i].b, static_cast<double>(ms)});
+    ops_[i] = ops_.back();
+    ops_.pop_back();
+  }
+  std::stable_sort(out.begin(), out.end(),
+                   [](const lmmsim::OpCompletion& x, const lmmsim::OpCompletion& y) {
+                     return x.time_ms < y.time_ms;
+                   });
+}
+
+void DeviceBackend::finish() {
+  RS_CUDA_CHECK(cudaDeviceSynchronize());
+  stats_.wall_ms = clock_ms();
+  if (last_event_ != nullptr) {
+    float ms = 0;
+    RS_CUDA_CHECK(cudaEventElapsedTime(&ms, origin_, last_event_));
+    stats_.gpu_ms = ms;
+  }
+  stats_.kernel_launches = launches_so_far() - launches0_;
+  stats_.h2d_bytes += ctx_.uploader().bytes_uploaded() - upload0_;
+}
+
+void DeviceBackend::collect() {
+  const int vocab = ctx_.shapes().vocab;
+  std::vector<std::int32_t> am(static_cast<std::size_t>(ctx_.max_requests()));
+  if (ctx_.device_argmax() != nullptr)
+    RS_CUDA_CHECK(cudaMemcpy(am.data(), ctx_.device_argmax(), am.size() * 4, cudaMemcpyDeviceToHost));
+  for (const auto& [id, slot] : done_slots_) {
+    std::vector<float> row(static_cast<std::size_t>(vocab));
+    if (e2e_) {
+      std::memcpy(row.data(), logits_host_.at(id), row.size() * 4);
+    } else {
+      ctx_.copy_logits(slot, row.data(), ctx_.aux_stream());
+      RS_CUDA_CHECK(cudaStreamSynchronize(ctx_.aux_stream()));
+    }
+    logits_[id] = std::move(row);
+    argmax_[id] = am[static_cast<std::size_t>(slot)];
+    ctx_.free_slot(slot);
+  }
+  done_slots_.clear();
+}
+
+}  // namespace rserve

@@ -1,0 +1,396 @@
+// rserve-b200 — per-GPU pipeline context (see device_context.cuh).
+#include <algorithm>
+#include <cstring>
+#include <set>
+
+#include "device_context.cuh"
+#include "kernels.cuh"
+
+namespace rserve {
+
+// ---- PagePool --------------------------------------------------------------------
+void PagePool::reset(std::int64_t pages) {
+  free_.clear();
+  for (std::int64_t p = 0; p < pages; ++p) free_.emplace_back(static_cast<int>(p), nullptr);
+  cap_ = pages;
+}
+
+std::vector<int> PagePool::take(std::int64_t n, std::vector<cudaEvent_t>& guards) {
+  if (n > static_cast<std::int64_t>(free_.size()))
+    throw DeviceError(RS_ERR_CUDA, "page pool exhausted: need " + std::to_string(n) +
+                                       " pages, " + std::to_string(free_.size()) + " free of " +
+                                       std::to_string(cap_));
+  std::vector<int> out;
+  out.reserve(static_cast<std::size_t>(n));
+  for (std::int64_t i = 0; i < n; ++i) {
+    auto [page, ev] = free_.front();
+    free_.pop_front();
+    out.push_back(page);
+    if (ev != nullptr && (guards.empty() || guards.back() != ev)) guards.push_back(ev);
+  }
+  return out;
+}
+
+void PagePool::give(const std::vector<int>& pages, cudaEvent_t guard) {
+  for (int p : pages)
+    if (p >= 0) free_.emplace_back(p, guard);
+}
+
+// ---- Uploader ---------------------------------------------------------------------
+void Uploader::init(std::size_t bytes) {
+  cap_ = bytes;
+  RS_CUDA_CHECK(cudaMallocHost(&host_, bytes));
+  RS_CUDA_CHECK(cudaMalloc(&dev_, bytes));
+}
+
+Uploader::~Uploader() {
+  marks_.clear();
+  if (host_) cudaFreeHost(host_);
+  if (dev_) cudaFree(dev_);
+}
+
+void* Uploader::put(const void* src, std::size_t n, cudaStream_t st) {
+  const std::size_t len = n;
+  n = (n + 255) / 256 * 256;
+  if (n > cap_ / 4) throw DeviceError(RS_ERR_CUDA, "uploader: descriptor too large");
+  if (head_ + n > cap_) head_ = 0;  // wrap
+  const std::size_t b = head_, e = head_ + n;
+  // Regions still in use by enqueued work must be consumed before reuse.
+  for (auto it = marks_.begin(); it != marks_.end();) {
+    if (it->begin < e && b < it->end) {
+      RS_CUDA_CHECK(cudaEventSynchronize(it->ev.get()));
+      it = marks_.erase(it);
+    } else {
+      ++it;
+    }
+  }
+  if (len > 0) std::memcpy(host_ + b, src, len);
+  RS_CUDA_CHECK(cudaMemcpyAsync(dev_ + b, host_ + b, n, cudaMemcpyHostToDevice, st));
+  head_ = e;
+  uploaded_ += n;
+  if (pending_begin_ == kNone) pending_begin_ = b;
+  pending_.push_back({b, e});
+  return dev_ + b;
+}
+
+void Uploader::fence(cudaStream_t st) {
+  if (pending_.empty()) return;
+  cudaEvent_t raw;
+  RS_CUDA_CHECK(cudaEventCreateWithFlags(&raw, cudaEventDisableTiming));
+  RS_CUDA_CHECK(cudaEventRecord(raw, st));
+  std::shared_ptr<CUevent_st> ev(raw, [](cudaEvent_t e) { cudaEventDestroy(e); });
+  for (const auto& [b, e] : pending_) marks_.push_back({b, e, ev});
+  pending_.clear();
+  pending_begin_ = kNone;
+}
+
+// ---- Context ----------------------------------------------------------------------
+Context::Context(const rs_model_config& model, const rs_ctx_options& opt) : opt_(opt) {
+  int n_dev = 0;
+  if (cudaGetDeviceCount(&n_dev) != cudaSuccess || n_dev == 0)
+    throw DeviceError(RS_ERR_CUDA, "no CUDA device: the rserve-b200 product path has no CPU fallback");
+  RS_CUDA_CHECK(cudaSetDevice(opt.device));
+  cudaDeviceProp prop{};
+  RS_CUDA_CHECK(cudaGetDeviceProperties(&prop, opt.device));
+  if (prop.major != 10)
+    throw DeviceError(RS_ERR_CUDA, std::string("device ") + prop.name +
+                                       " is not sm_100 (tcgen05 kernels need a B200)");
+  s_ = Shapes::from(model);
+  if (opt_.layer_end <= 0 || opt_.layer_end > s_.L) opt_.layer_end = s_.L;
+  if (opt_.layer_begin < 0) opt_.layer_begin = 0;
+  RS_CUDA_CHECK(cudaStreamCreateWithFlags(&tracker_, cudaStreamNonBlocking));
+  RS_CUDA_CHECK(cudaStreamCreateWithFlags(&aux_, cudaStreamNonBlocking));
+  up_.init(64ull << 20);
+  max_requests_ = 512;
+
+  const bool first_stage = opt_.layer_begin == 0;
+  if (opt_.with_vit) {
+    vit_ = std::make_unique<Vit>();
+    vit_->init(s_, arena_, static_cast<int>(4 * opt_.max_encode_tokens), aux_);
+  }
+  llm_ = std::make_unique<Llm>();
+  const std::int64_t kv_pages = static_cast<std::int64_t>((opt_.kv_tokens + kPageTokens - 1) / kPageTokens);
+  llm_->init(s_, arena_, opt_.layer_begin, opt_.layer_end, first_stage, opt_.with_lm_head != 0,
+             static_cast<int>(opt_.max_chunk_tokens), kv_pages, kPageTokens, max_requests_, aux_);
+  kv_pages_.reset(kv_pages);
+  if (first_stage) {
+    const std::int64_t slab_pages =
+        static_cast<std::int64_t>((opt_.slot_tokens + kPageTokens - 1) / kPageTokens);
+    slab_ = static_cast<bf16*>(arena_.alloc(static_cast<std::size_t>(slab_pages) * kPageTokens *
+                                            s_.d * sizeof(bf16)));
+    slab_pages_.reset(slab_pages);
+  }
+  page_tables_dev_ = static_cast<int**>(arena_.alloc(sizeof(int*) * max_requests_));
+  RS_CUDA_CHECK(cudaMemsetAsync(page_tables_dev_, 0, sizeof(int*) * max_requests_, aux_));
+  page_tables_host_.assign(static_cast<std::size_t>(max_requests_), nullptr);
+  for (int i = max_requests_ - 1; i >= 0; --i) free_slots_.push_back(i);
+  prefix_dev_ = static_cast<std::uint64_t*>(arena_.alloc(64));
+  RS_CUDA_CHECK(cudaMallocHost(&prefix_host_, 64));
+  RS_CUDA_CHECK(cudaStreamSynchronize(aux_));
+}
+
+Context::~Context() {
+  cudaDeviceSynchronize();
+  reqs_.clear();
+  for (cudaEvent_t e : events_) cudaEventDestroy(e);
+  if (prefix_host_) cudaFreeHost(prefix_host_);
+  if (tracker_) cudaStreamDestroy(tracker_);
+  if (aux_) cudaStreamDestroy(aux_);
+}
+
+cudaEvent_t Context::new_event() {
+  cudaEvent_t e;
+  RS_CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  events_.push_back(e);
+  return e;
+}
+
+int Context::take_request_slot() {
+  if (free_slots_.empty())
+    throw DeviceError(RS_ERR_CUDA, "too many live requests on the device (max " +
+                                       std::to_string(max_requests_) + ")");
+  const int s = free_slots_.back();
+  free_slots_.pop_back();
+  return s;
+}
+
+DevRequest* Context::find(lmmsim::RequestId id) {
+  const auto it = reqs_.find(id);
+  return it == reqs_.end() ? nullptr : it->second.get();
+}
+
+DevRequest& Context::get(lmmsim::RequestId id) {
+  DevRequest* r = find(id);
+  if (r == nullptr) throw lmmsim::RegistryError("unknown request id " + lmmsim::format_u64(id));
+  return *r;
+}
+
+namespace {
+// Qwen2-VL get_rope_index: text advances (t,t,t); an image of merged grid
+// (gh, gw) gets (s, s+row, s+col) and the next position is s + max(gh, gw).
+void mrope_ids(const lmmsim::RequestSpec& req, std::vector<std::array<std::int32_t, 3>>& out) {
+  std::int32_t cur = 0;
+  for (const lmmsim::SegmentSpec& seg : req.segments) {
+    if (seg.kind == lmmsim::SegmentKind::Text) {
+      for (std::uint64_t i = 0; i < seg.tokens; ++i, ++cur) out.push_back({cur, cur, cur});
+    } else {
+      int gh, gw;
+      item_grid(seg.tokens, &gh, &gw);
+      for (int r = 0; r < gh; ++r)
+        for (int c = 0; c < gw; ++c) out.push_back({cur, cur + r, cur + c});
+      cur += std::max(gh, gw);
+    }
+  }
+}
+}  // namespace
+
+DevRequest& Context::create_request(const lmmsim::RequestSpec& req, const std::int32_t* text_ids,
+                                    std::uint64_t payload_seed, cudaStream_t st) {
+  if (find(req.id) != nullptr)
+    throw lmmsim::RegistryError("duplicate request id " + lmmsim::format_u64(req.id));
+  if (slab_ == nullptr) throw DeviceError(RS_ERR_CUDA, "context holds no embedding slab (not stage 0)");
+  auto owned = std::make_unique<DevRequest>();
+  DevRequest& r = *owned;
+  r.id = req.id;
+  r.total = req.total_tokens();
+  if (r.total > opt_.max_prompt_tokens)
+    throw lmmsim::ConfigError("request " + lmmsim::format_u64(req.id) + ": " +
+                              lmmsim::format_u64(r.total) + " tokens exceed max_prompt_tokens");
+  r.items = req.mm_item_ranges();
+  std::uint64_t pos = 0, patch = 0;
+  for (const lmmsim::SegmentSpec& seg : req.segments) {
+    if (seg.kind == lmmsim::SegmentKind::Text) r.text_ranges.emplace_back(pos, pos + seg.tokens);
+    else {
+      r.item_patch_offset.push_back(patch);
+      patch += 4 * seg.tokens;
+    }
+    pos += seg.tokens;
+  }
+  r.patches = patch;
+  mrope_ids(req, r.rope);
+  r.slot = take_request_slot();
+  const std::int64_t pages = static_cast<std::int64_t>((r.total + kPageTokens - 1) / kPageTokens);
+  std::vector<cudaEvent_t> guards;
+  r.slot_pages = slab_pages_.take(pages, guards);
+  for (cudaEvent_t g : guards) RS_CUDA_CHECK(cudaStreamWaitEvent(st, g, 0));
+  std::vector<cudaEvent_t> kv_guards;
+  r.kv_pages = kv_pages_.take(pages, kv_guards);
+
+  const std::size_t words = static_cast<std::size_t>((r.total + 31) / 32);
+  RS_CUDA_CHECK(cudaMallocAsync(reinterpret_cast<void**>(&r.bitmap), words * 4, st));
+  RS_CUDA_CHECK(cudaMemsetAsync(r.bitmap, 0, words * 4, st));
+  RS_CUDA_CHECK(cudaMallocAsync(reinterpret_cast<void**>(&r.kv_table),
+                                static_cast<std::size_t>(pages) * 4, st));
+  const void* kvt = up_.put(r.kv_pages.data(), r.kv_pages.size() * 4, st);
+  RS_CUDA_CHECK(cudaMemcpyAsync(r.kv_table, kvt, r.kv_pages.size() * 4, cudaMemcpyDeviceToDevice, st));
+  const void* ptr_src = up_.put(&r.kv_table, sizeof(int*), st);
+  RS_CUDA_CHECK(cudaMemcpyAsync(page_tables_dev_ + r.slot, ptr_src, sizeof(int*),
+                                cudaMemcpyDeviceToDevice, st));
+  page_tables_host_[static_cast<std::size_t>(r.slot)] = r.kv_table;
+
+  // Text: readiness bits + K8 gather of the token embeddings into the slots.
+  std::vector<std::uint64_t> ranges;
+  std::vector<std::int32_t> ids;
+  std::vector<std::int64_t> rows;
+  std::size_t k = 0;
+  for (const auto& [b, e] : r.text_ranges) {
+    ranges.push_back(b);
+    ranges.push_back(e);
+    for (std::uint64_t t = b; t < e; ++t, ++k) {
+      std::int32_t id;
+      if (text_ids != nullptr) {
+        id = text_ids[k];
+        if (id < 0 || id >= s_.vocab)
+          throw lmmsim::InputError("request " + lmmsim::format_u64(req.id) + ": token id " +
+                                   std::to_string(id) + " outside the vocabulary");
+      } else {
+        id = static_cast<std::int32_t>(mix64(payload_seed, (6ull << 32) | req.id, t) %
+                                       static_cast<std::uint64_t>(s_.vocab));
+      }
+      ids.push_back(id);
+      rows.push_back(r.slab_row(t));
+    }
+  }
+  if (!ranges.empty()) {
+    const auto* rng = static_cast<const std::uint64_t*>(up_.put(ranges.data(), ranges.size() * 8, st));
+    bitmap_set_ranges(r.bitmap, rng, static_cast<int>(ranges.size() / 2), st);
+    const auto* idd = static_cast<const std::int32_t*>(up_.put(ids.data(), ids.size() * 4, st));
+    const auto* rwd = static_cast<const std::int64_t*>(up_.put(rows.data(), rows.size() * 8, st));
+    gather_text_embeddings(llm_->embed(), idd, static_cast<int>(ids.size()), rwd, slab_, s_.d, st);
+  }
+  up_.fence(st);
+  DevRequest* raw = owned.get();
+  reqs_.emplace(req.id, std::move(owned));
+  return *raw;
+}
+
+void Context::scatter_items(DevRequest& r, const std::vector<lmmsim::TokenRange>& items,
+                            const bf16* rows_src, cudaStream_t st) {
+  std::vector<std::int64_t> rows;
+  std::vector<std::uint64_t> ranges;
+  for (const lmmsim::TokenRange& it : items) {
+    ranges.push_back(it.start);
+    ranges.push_back(it.end);
+    for (std::uint64_t t = it.start; t < it.end; ++t) rows.push_back(r.slab_row(t));
+  }
+  const auto* rwd = static_cast<const std::int64_t*>(up_.put(rows.data(), rows.size() * 8, st));
+  const auto* rng = static_cast<const std::uint64_t*>(up_.put(ranges.data(), ranges.size() * 8, st));
+  scatter_rows_and_mark(rows_src, static_cast<int>(rows.size()), rwd, slab_, s_.d, r.bitmap, rng,
+                        static_cast<int>(ranges.size() / 2), st);
+  up_.fence(st);
+}
+
+void Context::release_prefix(DevRequest& r, std::uint64_t released_end, cudaEvent_t guard) {
+  const std::uint64_t full_pages =
+      released_end >= r.total ? r.slot_pages.size() : released_end / kPageTokens;
+  std::vector<int> give;
+  for (std::uint64_t p = r.slot_freed_tokens / kPageTokens; p < full_pages; ++p) {
+    give.push_back(r.slot_pages[p]);
+    r.slot_pages[p] = -1;
+  }
+  r.slot_freed_tokens = full_pages * kPageTokens;
+  slab_pages_.give(give, guard);
+}
+
+void Context::erase_request(lmmsim::RequestId id, cudaEvent_t guard, bool keep_slot) {
+  auto it = reqs_.find(id);
+  if (it == reqs_.end()) throw lmmsim::RegistryError("erase of unknown request id " + lmmsim::format_u64(id));
+  DevRequest& r = *it->second;
+  release_prefix(r, r.total, guard);
+  kv_pages_.give(r.kv_pages, guard);
+  if (guard != nullptr) RS_CUDA_CHECK(cudaStreamWaitEvent(tracker_, guard, 0));
+  RS_CUDA_CHECK(cudaFreeAsync(r.bitmap, tracker_));
+  RS_CUDA_CHECK(cudaFreeAsync(r.kv_table, tracker_));
+  if (!keep_slot) free_slots_.push_back(r.slot);
+  reqs_.erase(it);
+}
+
+std::uint64_t Context::device_schedulable(DevRequest& r, std::uint64_t frontier) {
+  ready_prefix(r.bitmap, frontier, r.total, prefix_dev_, tracker_);
+  RS_CUDA_CHECK(cudaMemcpyAsync(prefix_host_, prefix_dev_, 8, cudaMemcpyDeviceToHost, tracker_));
+  RS_CUDA_CHECK(cudaStreamSynchronize(tracker_));
+  return *prefix_host_ - frontier;
+}
+
+VitBatchPlan Context::plan_batch(const DevRequest& /*r*/,
+                                 const std::vector<lmmsim::TokenRange>& items) const {
+  VitBatchPlan plan;
+  plan.cu_window.push_back(0);
+  plan.cu_item.push_back(0);
+  for (const lmmsim::TokenRange& it : items) {
+    int gh, gw;
+    item_grid(it.length(), &gh, &gw);
+    plan_item(gh, gw, s_.win, plan.tokens, plan);
+  }
+  return plan;
+}
+
+void Context::encode(const VitBatchPlan& plan, const bf16* patches_dev, bf16* out, cudaStream_t st) {
+  if (!vit_) throw DeviceError(RS_ERR_CUDA, "context holds no vision encoder");
+  const auto* pos = static_cast<const std::int32_t*>(up_.put(plan.pos_hw.data(), plan.pos_hw.size() * 4, st));
+  const auto* cuw = static_cast<const std::int32_t*>(up_.put(plan.cu_window.data(), plan.cu_window.size() * 4, st));
+  const auto* cui = static_cast<const std::int32_t*>(up_.put(plan.cu_item.data(), plan.cu_item.size() * 4, st));
+  const auto* orow = static_cast<const std::int32_t*>(up_.put(plan.out_row.data(), plan.out_row.size() * 4, st));
+  vit_->encode(plan, patches_dev, pos, cuw, cui, orow, out, st);
+  up_.fence(st);
+}
+
+void Context::prefill(const std::vector<SliceRef>& slices, bf16* x, cudaStream_t st,
+                      int layer_from, int layer_to) {
+  std::vector<ChunkRowInfo> rows;
+  std::vector<std::int64_t> gather;
+  std::vector<PrefillWork> work;
+  std::vector<std::int64_t> done_rows;
+  std::vector<std::int32_t> done_slots;
+  const int l_from = layer_from < 0 ? llm_->layer_begin() : layer_from;
+  const int l_to = layer_to < 0 ? llm_->layer_end() : layer_to;
+  const bool first = l_from == 0;
+  for (const SliceRef& sl : slices) {
+    const int base = static_cast<int>(rows.size());
+    for (std::uint64_t p = sl.start; p < sl.end; ++p) {
+      const auto& rp = sl.req->rope[p];
+      rows.push_back({sl.req->slot, static_cast<std::int32_t>(p), {rp[0], rp[1], rp[2]}, 0});
+      if (first) gather.push_back(sl.req->slab_row(p));
+    }
+    for (std::uint64_t q = sl.start; q < sl.end; q += 64)
+      work.push_back({base + static_cast<int>(q - sl.start),
+                      static_cast<int>(std::min<std::uint64_t>(64, sl.end - q)),
+                      static_cast<int>(q), sl.req->slot});
+    if (sl.end == sl.req->total) {
+      done_rows.push_back(base + static_cast<std::int64_t>(sl.end - sl.start) - 1);
+      done_slots.push_back(sl.req->slot);
+    }
+  }
+  ChunkDev c;
+  c.M = static_cast<int>(rows.size());
+  c.rows = static_cast<const ChunkRowInfo*>(up_.put(rows.data(), rows.size() * sizeof(ChunkRowInfo), st));
+  if (first) c.gather_rows = static_cast<const std::int64_t*>(up_.put(gather.data(), gather.size() * 8, st));
+  c.work = static_cast<const PrefillWork*>(up_.put(work.data(), work.size() * sizeof(PrefillWork), st));
+  c.n_work = static_cast<int>(work.size());
+  if (llm_->has_head() && l_to == llm_->layer_end() && !done_rows.empty()) {
+    c.done_rows = static_cast<const std::int64_t*>(up_.put(done_rows.data(), done_rows.size() * 8, st));
+    c.done_slots = static_cast<const std::int32_t*>(up_.put(done_slots.data(), done_slots.size() * 4, st));
+    c.n_done = static_cast<int>(done_rows.size());
+  }
+  llm_->forward_stage(c, slab_, x, page_tables_dev_, st, l_from, l_to);
+  up_.fence(st);
+}
+
+std::uint64_t Context::chunk_flops(const std::vector<SliceRef>& slices) const {
+  std::uint64_t tokens = 0, att = 0;
+  const std::uint64_t layers = static_cast<std::uint64_t>(llm_->layer_end() - llm_->layer_begin());
+  for (const SliceRef& sl : slices) {
+    tokens += sl.end - sl.start;
+    // causal attention over the prefix: 4 * hq * hd per (q, k) pair, k <= q
+    for (std::uint64_t q = sl.start; q < sl.end; ++q)
+      att += 4ull * static_cast<std::uint64_t>(s_.hq * s_.hd) * (q + 1);
+  }
+  return llm_->dense_flops(tokens) + att * layers;
+}
+
+void Context::copy_logits(int slot, float* host, cudaStream_t st) {
+  RS_CUDA_CHECK(cudaMemcpyAsync(host, llm_->logits_row(slot), static_cast<std::size_t>(s_.vocab) * 4,
+                                cudaMemcpyDeviceToHost, st));
+}
+
+}  // namespace rserve

@@ -1,0 +1,165 @@
+// rserve-b200 — per-GPU pipeline context: model weights, embedding-slot
+// slab + readiness bitmaps (the device tracker), paged KV pools, streams,
+// metadata uploads. Used by the C-ABI (capi_device.cu) both directly
+// (tracker-level entry points) and through the engine backend
+// (device_backend.cu).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <array>
+#include <cstdint>
+#include <deque>
+#include <list>
+#include <memory>
+#include <unordered_map>
+#include <vector>
+
+#include "common.cuh"
+#include "lmmsim/tracker.hpp"
+#include "model.cuh"
+#include "rserve.h"
+
+namespace rserve {
+
+constexpr int kPageTokens = 64;  // slot pages and KV pages
+
+/// Free list of fixed-size pages; a freed page may carry the CUDA event
+/// after which it is safe to overwrite (its last reader's completion).
+class PagePool {
+ public:
+  void reset(std::int64_t pages);
+  /// Takes n pages; appends guard events that writers must wait on.
+  std::vector<int> take(std::int64_t n, std::vector<cudaEvent_t>& guards);
+  void give(const std::vector<int>& pages, cudaEvent_t guard);
+  std::int64_t available() const { return static_cast<std::int64_t>(free_.size()); }
+  std::int64_t capacity() const { return cap_; }
+
+ private:
+  std::deque<std::pair<int, cudaEvent_t>> free_;
+  std::int64_t cap_ = 0;
+};
+
+/// Pinned-host -> device ring for per-op metadata (chunk / batch descriptors).
+class Uploader {
+ public:
+  void init(std::size_t bytes);
+  ~Uploader();
+  /// Copies `n` bytes from host to a device region (async on `st`), returns
+  /// the device pointer. Regions are recycled after the fence covering them.
+  void* put(const void* src, std::size_t n, cudaStream_t st);
+  /// Marks everything put so far as consumed once work now on `st` finishes.
+  void fence(cudaStream_t st);
+  std::uint64_t bytes_uploaded() const { return uploaded_; }
+
+ private:
+  static constexpr std::size_t kNone = ~std::size_t{0};
+  std::uint8_t* host_ = nullptr;
+  std::uint8_t* dev_ = nullptr;
+  std::size_t cap_ = 0, head_ = 0, pending_begin_ = kNone;
+  struct Mark {
+    std::size_t begin, end;
+    std::shared_ptr<CUevent_st> ev;
+  };
+  std::list<Mark> marks_;
+  std::vector<std::pair<std::size_t, std::size_t>> pending_;
+  std::uint64_t uploaded_ = 0;
+};
+
+struct DevRequest {
+  lmmsim::RequestId id = 0;
+  int slot = -1;                       // request table / logits slot
+  std::uint64_t total = 0;
+  std::vector<lmmsim::TokenRange> items;
+  std::vector<std::pair<std::uint64_t, std::uint64_t>> text_ranges;
+  std::vector<int> slot_pages;         // embedding slab pages (-1 once freed)
+  std::uint64_t slot_freed_tokens = 0; // prefix whose pages are back in the pool
+  std::vector<int> kv_pages;
+  std::uint32_t* bitmap = nullptr;     // device readiness words
+  int* kv_table = nullptr;             // device page table (kv_pages)
+  std::vector<std::array<std::int32_t, 3>> rope;  // M-RoPE ids per token
+  std::vector<std::uint64_t> item_patch_offset;   // first patch of each item
+  std::uint64_t patches = 0;
+
+  std::int64_t slab_row(std::uint64_t pos) const {
+    return static_cast<std::int64_t>(slot_pages[pos / kPageTokens]) * kPageTokens +
+           static_cast<std::int64_t>(pos % kPageTokens);
+  }
+};
+
+/// One prefill slice (request, [start, end)).
+struct SliceRef {
+  DevRequest* req;
+  std::uint64_t start, end;
+};
+
+class Context {
+ public:
+  Context(const rs_model_config& model, const rs_ctx_options& opt);
+  ~Context();
+
+  const Shapes& shapes() const { return s_; }
+  const rs_ctx_options& options() const { return opt_; }
+  Vit* vit() { return vit_.get(); }
+  Llm* llm() { return llm_.get(); }
+  cudaStream_t tracker_stream() const { return tracker_; }
+  cudaStream_t aux_stream() const { return aux_; }
+  Uploader& uploader() { return up_; }
+
+  // ---- device tracker data plane ----
+  /// Slot pages, bitmap (text bits set), KV pages + table, M-RoPE ids, and
+  /// the K8 text gather (ids from host, or hashed on device when null).
+  DevRequest& create_request(const lmmsim::RequestSpec& req, const std::int32_t* text_ids,
+                             std::uint64_t payload_seed, cudaStream_t st);
+  DevRequest* find(lmmsim::RequestId id);
+  DevRequest& get(lmmsim::RequestId id);
+  /// K6: rows [n, d] (LLM order, items concatenated) -> slots; set bits.
+  void scatter_items(DevRequest& r, const std::vector<lmmsim::TokenRange>& items,
+                     const bf16* rows, cudaStream_t st);
+  /// Frees slot pages whose tokens are all below `released_end`.
+  void release_prefix(DevRequest& r, std::uint64_t released_end, cudaEvent_t guard);
+  /// Frees the request's device state. keep_slot: its request / logits slot
+  /// stays reserved until free_slot() (logits not yet read back).
+  void erase_request(lmmsim::RequestId id, cudaEvent_t guard, bool keep_slot = false);
+  void free_slot(int slot) { free_slots_.push_back(slot); }
+  /// K7 on the device: schedulable count from `frontier` (synchronous).
+  std::uint64_t device_schedulable(DevRequest& r, std::uint64_t frontier);
+
+  // ---- compute ----
+  /// Builds + uploads the batch plan, runs the ViT; out = [tokens, d].
+  VitBatchPlan plan_batch(const DevRequest& r, const std::vector<lmmsim::TokenRange>& items) const;
+  void encode(const VitBatchPlan& plan, const bf16* patches_dev, bf16* out, cudaStream_t st);
+  /// One chunk through the local layers. x: [M, d] residual (per chunk).
+  void prefill(const std::vector<SliceRef>& slices, bf16* x, cudaStream_t st,
+               int layer_from = -1, int layer_to = -1);
+  std::uint64_t chunk_flops(const std::vector<SliceRef>& slices) const;
+
+  bf16* slab() { return slab_; }
+  const std::int32_t* argmax_host(int slot);
+  void copy_logits(int slot, float* host, cudaStream_t st);
+  std::int32_t* device_argmax() { return llm_ ? llm_->argmax_dev() : nullptr; }
+  int max_requests() const { return max_requests_; }
+  cudaEvent_t new_event();  // owned by the context
+
+ private:
+  int take_request_slot();
+  Shapes s_;
+  rs_ctx_options opt_;
+  DeviceArena arena_;
+  std::unique_ptr<Vit> vit_;
+  std::unique_ptr<Llm> llm_;
+  bf16* slab_ = nullptr;
+  PagePool slab_pages_, kv_pages_;
+  int** page_tables_dev_ = nullptr;   // [max_requests] -> kv page table
+  std::vector<int*> page_tables_host_;
+  std::vector<int> free_slots_;
+  int max_requests_ = 0;
+  std::unordered_map<lmmsim::RequestId, std::unique_ptr<DevRequest>> reqs_;
+  cudaStream_t tracker_ = nullptr, aux_ = nullptr;
+  Uploader up_;
+  std::vector<cudaEvent_t> events_;
+  std::uint64_t* prefix_dev_ = nullptr;
+  std::uint64_t* prefix_host_ = nullptr;
+};
+
+}  // namespace rserve

@@ -37,6 +37,25 @@ __global__ void fill_uniform_kernel(bf16* dst, std::int64_t rows, int cols, int 
   }
 }
 
+__global__ void fill_interleaved_kernel(bf16* dst, int rows_valid, int rows_pad, int cols, int ld,
+                                        std::uint64_t seed, std::uint64_t stream, float scale,
+                                        int which) {
+  const std::int64_t total = static_cast<std::int64_t>(rows_pad) * ld;
+  for (std::int64_t e = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; e < total;
+       e += static_cast<std::int64_t>(gridDim.x) * blockDim.x) {
+    const int r = static_cast<int>(e / ld);
+    const int c = static_cast<int>(e % ld);
+    float v = 0.f;
+    if (r < rows_valid && c < cols) {
+      const std::uint64_t z = mix64(seed, stream, static_cast<std::uint64_t>(r) * cols + c);
+      const float u = static_cast<float>(z >> 40) * (1.0f / 16777216.0f);
+      v = (2.0f * u - 1.0f) * scale;
+    }
+    const std::int64_t dst_row = static_cast<std::int64_t>(r / 16) * 32 + which * 16 + r % 16;
+    dst[dst_row * ld + c] = __float2bfloat16_rn(v);
+  }
+}
+
 __global__ void fill_const_kernel(bf16* dst, std::int64_t n, float v) {
   for (std::int64_t e = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; e < n;
        e += static_cast<std::int64_t>(gridDim.x) * blockDim.x)
@@ -244,8 +263,10 @@ __global__ void bitmap_set_kernel(std::uint32_t* bitmap, const std::uint64_t* ra
   }
 }
 
-__global__ void argmax_kernel(const float* __restrict__ logits, int vocab, std::int32_t* out) {
-  const float* row = logits + static_cast<std::int64_t>(blockIdx.x) * vocab;
+__global__ void argmax_kernel(const float* __restrict__ logits, int vocab, std::int32_t* out,
+                              const std::int32_t* rows_idx) {
+  const int rix = rows_idx != nullptr ? rows_idx[blockIdx.x] : static_cast<int>(blockIdx.x);
+  const float* row = logits + static_cast<std::int64_t>(rix) * vocab;
   float best = -INFINITY;
   int idx = 0x7fffffff;
   for (int i = threadIdx.x; i < vocab; i += blockDim.x) {
@@ -276,7 +297,7 @@ __global__ void argmax_kernel(const float* __restrict__ logits, int vocab, std::
         best = sb[w];
         idx = si[w];
       }
-    out[blockIdx.x] = idx;
+    out[rix] = idx;
   }
 }
 
@@ -293,6 +314,15 @@ void fill_uniform(bf16* dst, std::int64_t rows, int cols, int ld, std::uint64_t 
   if (rows <= 0) return;
   fill_uniform_kernel<<<elem_grid(rows * ld), 256, 0, st>>>(dst, rows, cols, ld, seed, stream,
                                                            scale, offset);
+  RS_LAUNCH_CHECK();
+  count_launch();
+}
+
+void fill_uniform_interleaved(bf16* dst, int rows_valid, int rows_pad, int cols, int ld,
+                              std::uint64_t seed, std::uint64_t stream, float scale, int which,
+                              cudaStream_t st) {
+  fill_interleaved_kernel<<<elem_grid(static_cast<std::int64_t>(rows_pad) * ld), 256, 0, st>>>(
+      dst, rows_valid, rows_pad, cols, ld, seed, stream, scale, which);
   RS_LAUNCH_CHECK();
   count_launch();
 }
@@ -378,9 +408,10 @@ void bitmap_set_ranges(std::uint32_t* bitmap, const std::uint64_t* ranges, int n
   count_launch();
 }
 
-void argmax_rows(const float* logits, int rows, int vocab, std::int32_t* out, cudaStream_t st) {
+void argmax_rows(const float* logits, int rows, int vocab, std::int32_t* out, cudaStream_t st,
+                 const std::int32_t* rows_idx) {
   if (rows <= 0) return;
-  argmax_kernel<<<rows, 256, 0, st>>>(logits, vocab, out);
+  argmax_kernel<<<rows, 256, 0, st>>>(logits, vocab, out, rows_idx);
   RS_LAUNCH_CHECK();
   count_launch();
 }

@@ -27,7 +27,13 @@ __host__ __device__ inline std::uint64_t mix64(std::uint64_t seed, std::uint64_t
 /// The hash index is r * cols + c (independent of padding).
 void fill_uniform(bf16* dst, std::int64_t rows, int cols, int ld, std::uint64_t seed,
                   std::uint64_t stream, float scale, float offset, cudaStream_t st);
-/// Same values into an fp32 buffer (for oracles' consumption / debugging).
+/// SwiGLU weight layout: logical rows r < rows_valid of a [rows_pad, cols]
+/// gate (which = 0) or up (which = 1) matrix land at interleaved row
+/// (r / 16) * 32 + which * 16 + r % 16 of the [2 * rows_pad, ld] buffer;
+/// padding rows are zero. Hash index = r * cols + c, as for fill_uniform.
+void fill_uniform_interleaved(bf16* dst, int rows_valid, int rows_pad, int cols, int ld,
+                              std::uint64_t seed, std::uint64_t stream, float scale, int which,
+                              cudaStream_t st);
 void fill_const(bf16* dst, std::int64_t n, float v, cudaStream_t st);
 /// int32 ids in [0, modulo): id = mix64(seed, stream, i) % modulo.
 void fill_ids(std::int32_t* dst, std::int64_t n, std::uint64_t seed, std::uint64_t stream,
@@ -79,7 +85,9 @@ void bitmap_set_ranges(std::uint32_t* bitmap, const std::uint64_t* ranges, int n
                        cudaStream_t st);
 
 // ---- LM head helpers ---------------------------------------------------------------------
-/// out[i] = argmax(logits[i, :vocab]) (first max).
-void argmax_rows(const float* logits, int rows, int vocab, std::int32_t* out, cudaStream_t st);
+/// out[row(i)] = argmax(logits[row(i), :vocab]) (first max); row(i) =
+/// rows_idx ? rows_idx[i] : i.
+void argmax_rows(const float* logits, int rows, int vocab, std::int32_t* out, cudaStream_t st,
+                 const std::int32_t* rows_idx = nullptr);
 
 }  // namespace rserve
