@@ -200,8 +200,9 @@ RS_API rs_status rs_tracker_stats(rs_ctx* ctx, uint64_t id, uint64_t out[6]);
  * Algorithm-1 batch. `items` = (start,end) prompt ranges of the batch's
  * items; patches: host or device bf16 [4*tokens, patch_dim] in item
  * order (window-major patch order within an item).
- * Output: merged embeddings [tokens, d_llm] bf16 (device, ctx staging) in
- * LLM row-major token order; returned pointer valid until the next encode. */
+ * Output: merged embeddings [tokens, d_llm] bf16 in LLM row-major token
+ * order, written to *out_embeddings_dev when non-NULL on entry (caller
+ * device memory), else to ctx staging (valid until the next encode).      */
 RS_API rs_status rs_encode(rs_ctx* ctx, const uint64_t* items, int32_t n_items,
                     const void* patches, int32_t patches_on_host,
                     void** out_embeddings_dev);

@@ -29,6 +29,11 @@ RS_API rs_status rs_op_attention_varlen(const void* qkv, int ld_qkv, void* out, 
                                  int heads, int head_dim, float scale, void* stream);
 /* Kernel launches issued by this process so far (our kernels only). */
 RS_API unsigned long long rs_kernel_launches(void);
+/* Live per-kernel-class timing: CUDA events recorded on each launch stream
+ * around our kernels while enabled. drain -> lines
+ * "<class> <launches> <ms> <algorithmic flops> <algorithmic bytes>". */
+RS_API rs_status rs_profile_enable(int on);
+RS_API rs_status rs_profile_drain(char** out_text);
 
 #ifdef __cplusplus
 }

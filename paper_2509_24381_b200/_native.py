@@ -178,6 +178,19 @@ _sig("rs_op_gemm", [VP, I, VP, I, VP, I, VP, VP, I, VP, I, I, I, I, I, VP])
 _sig("rs_op_rmsnorm", [VP, I, VP, VP, I, I, I, C.c_float, VP])
 _sig("rs_op_attention_varlen", [VP, I, VP, I, VP, I, I, I, I, I, C.c_float, VP])
 _sig("rs_kernel_launches", [], C.c_ulonglong)
+_sig("rs_profile_enable", [C.c_int])
+_sig("rs_profile_drain", [PCHAR])
+
+
+def profile_drain():
+    """{class: dict(launches, ms, flops, bytes)} accumulated since enable."""
+    out = C.c_char_p()
+    check(lib.rs_profile_drain(C.byref(out)))
+    res = {}
+    for line in take_string(out).splitlines():
+        k, n, ms, fl, by = line.split()
+        res[k] = dict(launches=int(n), ms=float(ms), flops=float(fl), bytes=float(by))
+    return res
 
 
 def version() -> str:

@@ -286,9 +286,11 @@ class Pipeline:
         return dict(zip(keys, list(a)))
 
     # compute --------------------------------------------------------------------
-    def encode(self, items: Sequence[Tuple[int, int]], patches_ptr: int, on_host: bool) -> int:
+    def encode(self, items: Sequence[Tuple[int, int]], patches_ptr: int, on_host: bool,
+               out_ptr: Optional[int] = None) -> int:
+        """ViT forward of one Algorithm-1 batch; returns the output device pointer."""
         arr = (C.c_uint64 * (2 * len(items)))(*[v for it in items for v in it])
-        out = C.c_void_p()
+        out = C.c_void_p(out_ptr)
         N.check(N.lib.rs_encode(self.h, arr, len(items), patches_ptr, int(on_host), C.byref(out)))
         return out.value
 

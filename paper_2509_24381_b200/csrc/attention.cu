@@ -292,8 +292,10 @@ void launch_bidir(const bf16* qkv, int ld, bf16* out, int ld_out, const int* cu,
     set = true;
   }
   dim3 grid(ceil_div(max_seqlen, kQ), n_seqs, heads);
+  const int tok = prof::begin(st);
   varlen_bidir_kernel<HD><<<grid, 128, smem, st>>>(qkv, ld, out, ld_out, cu, heads, scale * kLog2e);
   RS_LAUNCH_CHECK();
+  prof::end(tok, st, "attn_vit_mma", 0, 0);
   count_launch();
 }
 
@@ -308,10 +310,12 @@ void launch_paged(const bf16* q, int ld_q, bf16* out, int ld_out, const PrefillW
     set = true;
   }
   dim3 grid(n_work, qh);
+  const int tok = prof::begin(st);
   prefill_paged_kernel<HD><<<grid, 128, smem, st>>>(q, ld_q, out, ld_out, work, kv.k, kv.v,
                                                      kv.page_tables, kv.page_size, qh, kvh,
                                                      scale * kLog2e);
   RS_LAUNCH_CHECK();
+  prof::end(tok, st, "attn_prefill_paged_mma", 0, 0);
   count_launch();
 }
 

@@ -217,9 +217,10 @@ rs_status rs_encode(rs_ctx* c, const uint64_t* items, int32_t n_items, const voi
     }
     DevRequest dummy;
     const VitBatchPlan plan = x.ctx->plan_batch(dummy, its);
-    x.ctx->encode(plan, src, x.manual_out, st);
+    bf16* dst = *out_embeddings_dev != nullptr ? static_cast<bf16*>(*out_embeddings_dev) : x.manual_out;
+    x.ctx->encode(plan, src, dst, st);
     RS_CUDA_CHECK(cudaStreamSynchronize(st));
-    *out_embeddings_dev = x.manual_out;
+    *out_embeddings_dev = dst;
   });
 }
 

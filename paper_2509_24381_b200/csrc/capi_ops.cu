@@ -55,4 +55,12 @@ rs_status rs_op_attention_varlen(const void* qkv, int ld_qkv, void* out, int ld_
 
 unsigned long long rs_kernel_launches(void) { return launches_so_far(); }
 
+rs_status rs_profile_enable(int on) {
+  return guarded([&] { prof::enable(on != 0); });
+}
+
+rs_status rs_profile_drain(char** out_text) {
+  return guarded([&] { *out_text = c_string(prof::drain()); });
+}
+
 }  // extern "C"

@@ -32,6 +32,18 @@ constexpr int kNumSMs = 148;
 void count_launch(std::uint64_t n = 1);
 std::uint64_t launches_so_far();
 
+// Optional live per-kernel-class timing (CUDA events on the launch stream),
+// enabled per engine run for bench.py's roofline figures.
+namespace prof {
+bool enabled();
+void enable(bool on);
+/// Returns a token for end(); -1 when disabled.
+int begin(cudaStream_t st);
+void end(int token, cudaStream_t st, const char* klass, double flops, double bytes);
+/// "klass launches ms flops bytes" lines, aggregated; resets the counters.
+std::string drain();
+}  // namespace prof
+
 __host__ __device__ inline int ceil_div(int a, int b) { return (a + b - 1) / b; }
 __host__ __device__ inline std::int64_t ceil_div64(std::int64_t a, std::int64_t b) {
   return (a + b - 1) / b;

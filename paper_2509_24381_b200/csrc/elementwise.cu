@@ -347,9 +347,12 @@ void rmsnorm(const bf16* x, int ldx, const bf16* w, bf16* y, int ldy, int rows, 
              const int* rows_dev) {
   if (rows <= 0) return;
   if (dim % 8 != 0) throw DeviceError(RS_ERR_CUDA, "rmsnorm: dim % 8 != 0");
+  const int tok = prof::begin(st);
   rmsnorm_kernel<<<row_grid(rows), 32 * kWarpsPerBlock, 0, st>>>(x, ldx, w, y, ldy, rows, dim, eps,
                                                                 row_map, x_copy, ld_copy, rows_dev);
   RS_LAUNCH_CHECK();
+  prof::end(tok, st, row_map != nullptr ? "rmsnorm_gather" : "rmsnorm", 0,
+            2.0 * rows * dim * (x_copy != nullptr ? 3.0 : 2.0));
   count_launch();
 }
 
@@ -379,9 +382,13 @@ void scatter_rows_and_mark(const bf16* src, int n_rows, const std::int64_t* dst_
                            int d, std::uint32_t* bitmap, const std::uint64_t* ranges, int n_ranges,
                            cudaStream_t st) {
   if (d % 8 != 0) throw DeviceError(RS_ERR_CUDA, "scatter: d % 8 != 0");
+  const int tok = prof::begin(st);
   scatter_rows_kernel<<<row_grid(n_rows > 0 ? n_rows : 1), 32 * kWarpsPerBlock, 0, st>>>(
       src, n_rows, dst_rows, slab, d, bitmap, ranges, n_ranges);
   RS_LAUNCH_CHECK();
+  // algorithmic bytes: rows read + written, row indices, bitmap words
+  prof::end(tok, st, "tracker_scatter_k6", 0,
+            4.0 * n_rows * d + 8.0 * n_rows + 16.0 * n_ranges);
   count_launch();
 }
 

@@ -359,10 +359,15 @@ void gemm(const GemmArgs& a, Epi epi, cudaStream_t stream, int force_bn) {
     // fills the 148 SMs clearly better.
     bn = wave_eff(a.M, a.N, 128) > wave_eff(a.M, a.N, 256) + 0.15 ? 128 : 256;
   }
+  const int tok = prof::begin(stream);
   if (bn == 256)
     dispatch_epi<256>(a, epi, stream);
   else
     dispatch_epi<128>(a, epi, stream);
+  const double m = a.M, n = a.N, k = a.K;
+  const double out_bytes = epi == Epi::StoreF32 ? 4.0 : (epi == Epi::SwiGLU ? 1.0 : 2.0);
+  prof::end(tok, stream, "gemm_tcgen05", 2.0 * m * n * k,
+            2.0 * (m * k + n * k) + out_bytes * m * n + (epi == Epi::Residual ? 2.0 * m * n : 0.0));
 }
 
 }  // namespace rserve
