@@ -54,6 +54,7 @@ DeviceBackend::DeviceBackend(Context& ctx, const lmmsim::SimConfig& cfg, bool re
 
 DeviceBackend::~DeviceBackend() {
   cudaDeviceSynchronize();
+  ctx_.quiesce();  // page guards reference this backend's events
   for (auto& [id, p] : payloads_) {
     if (p.patches_dev) cudaFree(p.patches_dev);
     if (p.patches_host) cudaFreeHost(p.patches_host);

@@ -32,6 +32,10 @@ class PagePool {
   /// Takes n pages; appends guard events that writers must wait on.
   std::vector<int> take(std::int64_t n, std::vector<cudaEvent_t>& guards);
   void give(const std::vector<int>& pages, cudaEvent_t guard);
+  /// Drops all guard events (call only when the device is idle).
+  void clear_guards() {
+    for (auto& p : free_) p.second = nullptr;
+  }
   std::int64_t available() const { return static_cast<std::int64_t>(free_.size()); }
   std::int64_t capacity() const { return cap_; }
 
@@ -122,6 +126,12 @@ class Context {
   /// stays reserved until free_slot() (logits not yet read back).
   void erase_request(lmmsim::RequestId id, cudaEvent_t guard, bool keep_slot = false);
   void free_slot(int slot) { free_slots_.push_back(slot); }
+  /// After a device-wide synchronize: forget page guard events (their
+  /// owners — e.g. an engine run's backend — may be destroyed next).
+  void quiesce() {
+    slab_pages_.clear_guards();
+    kv_pages_.clear_guards();
+  }
   /// K7 on the device: schedulable count from `frontier` (synchronous).
   std::uint64_t device_schedulable(DevRequest& r, std::uint64_t frontier);
 

@@ -78,8 +78,8 @@ def test_vit_encode_matches_oracle(tiny, oracle_tiny):
     np.testing.assert_allclose(out2.float().cpu().numpy(), got[256:], atol=3e-2, rtol=3e-2)
     # host-resident patches take the same path after an H2D copy
     out3 = torch.empty_like(out)
-    tiny.encode([(0, 256), (256, 356)], host.view(np.uint32).ctypes.data if False else
-                torch.from_numpy(host).to(torch.bfloat16).contiguous().data_ptr(), on_host=True,
+    host_bf16 = torch.from_numpy(host).to(torch.bfloat16).contiguous()  # keep alive
+    tiny.encode([(0, 256), (256, 356)], host_bf16.data_ptr(), on_host=True,
                 out_ptr=out3.data_ptr())
     torch.cuda.synchronize()
     assert torch.equal(out3, out)
