@@ -27,6 +27,15 @@ RS_API rs_status rs_op_rmsnorm(const void* x, int ldx, const void* w, void* y, i
 RS_API rs_status rs_op_attention_varlen(const void* qkv, int ld_qkv, void* out, int ld_out,
                                  const int* cu_seqlens, int n_seqs, int max_seqlen, int total,
                                  int heads, int head_dim, float scale, void* stream);
+/* Causal chunked-prefill attention (tcgen05) of ONE slice: q rows
+ * [0, q_rows) at prompt positions q_pos0.. attend to keys [0, q_pos0+q_rows)
+ * of a paged cache: K [pages][kv_heads][64][hd], V^T [pages][kv_heads][hd][64],
+ * page_table (device int32) maps key page -> cache page. Synchronous. */
+RS_API rs_status rs_op_attention_prefill(const void* q, int ld_q, int rows_alloc, void* out,
+                                         int ld_out, int q_pos0, int q_rows, const void* k_cache,
+                                         const void* v_cache, long long kv_pages,
+                                         const int* page_table, int q_heads, int kv_heads,
+                                         int head_dim, float scale, void* stream);
 /* Kernel launches issued by this process so far (our kernels only). */
 RS_API unsigned long long rs_kernel_launches(void);
 /* Live per-kernel-class timing: CUDA events recorded on each launch stream

@@ -60,21 +60,6 @@ struct BidirSource {  // packed QKV rows of one sequence
   __device__ const bf16* v_row(int key) const { return vbase + static_cast<std::int64_t>(key) * ld; }
 };
 template <int HD>
-struct PagedSource {  // one request's paged cache for one kv head
-  const bf16* k;
-  const bf16* v;
-  const int* pages;
-  int page_size, kv_heads, kvh;
-  int n_keys;
-  __device__ std::int64_t off(int key) const {
-    const int pg = pages[key / page_size];
-    return ((static_cast<std::int64_t>(pg) * kv_heads + kvh) * page_size + key % page_size) * HD;
-  }
-  __device__ const bf16* k_row(int key) const { return k + off(key); }
-  __device__ const bf16* v_row(int key) const { return v + off(key); }
-};
-
-template <int HD>
 struct Smem {
   static constexpr int kLd = HD + 8;  // +16 B pad: conflict-free ldmatrix
   bf16 q[kQ][kLd];
@@ -262,23 +247,6 @@ __global__ void __launch_bounds__(128) varlen_bidir_kernel(const bf16* __restric
                   scale_log2, sm);
 }
 
-template <int HD>
-__global__ void __launch_bounds__(128) prefill_paged_kernel(
-    const bf16* __restrict__ q, int ld_q, bf16* __restrict__ out, int ld_out,
-    const PrefillWork* __restrict__ work, bf16* kc, bf16* vc, const int* const* page_tables,
-    int page_size, int q_heads, int kv_heads, float scale_log2) {
-  extern __shared__ __align__(16) std::uint8_t smem_raw[];
-  Smem<HD>& sm = *reinterpret_cast<Smem<HD>*>(smem_raw);
-  const PrefillWork w = work[blockIdx.x];
-  const int head = blockIdx.y;
-  const int kvh = head / (q_heads / kv_heads);
-  PagedSource<HD> src{kc, vc, page_tables[w.req_slot], page_size, kv_heads, kvh,
-                      w.q_pos0 + w.q_rows};
-  flash_block<HD>(q + static_cast<std::int64_t>(w.q_row0) * ld_q + head * HD, ld_q, w.q_rows,
-                  w.q_pos0, src, out + static_cast<std::int64_t>(w.q_row0) * ld_out + head * HD,
-                  ld_out, scale_log2, sm);
-}
-
 constexpr float kLog2e = 1.4426950408889634f;
 
 template <int HD>
@@ -299,26 +267,6 @@ void launch_bidir(const bf16* qkv, int ld, bf16* out, int ld_out, const int* cu,
   count_launch();
 }
 
-template <int HD>
-void launch_paged(const bf16* q, int ld_q, bf16* out, int ld_out, const PrefillWork* work,
-                  int n_work, const PagedKV& kv, int qh, int kvh, float scale, cudaStream_t st) {
-  const int smem = sizeof(Smem<HD>);
-  static bool set = false;
-  if (!set) {
-    RS_CUDA_CHECK(cudaFuncSetAttribute(prefill_paged_kernel<HD>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    set = true;
-  }
-  dim3 grid(n_work, qh);
-  const int tok = prof::begin(st);
-  prefill_paged_kernel<HD><<<grid, 128, smem, st>>>(q, ld_q, out, ld_out, work, kv.k, kv.v,
-                                                     kv.page_tables, kv.page_size, qh, kvh,
-                                                     scale * kLog2e);
-  RS_LAUNCH_CHECK();
-  prof::end(tok, st, "attn_prefill_paged_mma", 0, 0);
-  count_launch();
-}
-
 }  // namespace
 
 void attention_varlen_bidir(const bf16* qkv, int ld_qkv, bf16* out, int ld_out,
@@ -330,17 +278,6 @@ void attention_varlen_bidir(const bf16* qkv, int ld_qkv, bf16* out, int ld_out,
     case 80: return launch_bidir<80>(qkv, ld_qkv, out, ld_out, cu_seqlens, n_seqs, max_seqlen, heads, scale, stream);
     case 128: return launch_bidir<128>(qkv, ld_qkv, out, ld_out, cu_seqlens, n_seqs, max_seqlen, heads, scale, stream);
     default: throw DeviceError(RS_ERR_CUDA, "attention: unsupported head_dim " + std::to_string(head_dim));
-  }
-}
-
-void attention_prefill_paged(const bf16* q, int ld_q, bf16* out, int ld_out,
-                             const PrefillWork* work, int n_work, const PagedKV& kv, int q_heads,
-                             int kv_heads, int head_dim, float scale, cudaStream_t stream) {
-  if (n_work <= 0) return;
-  switch (head_dim) {
-    case 64: return launch_paged<64>(q, ld_q, out, ld_out, work, n_work, kv, q_heads, kv_heads, scale, stream);
-    case 128: return launch_paged<128>(q, ld_q, out, ld_out, work, n_work, kv, q_heads, kv_heads, scale, stream);
-    default: throw DeviceError(RS_ERR_CUDA, "prefill attention: unsupported head_dim " + std::to_string(head_dim));
   }
 }
 

@@ -20,24 +20,27 @@ void attention_varlen_bidir(const bf16* qkv, int ld_qkv, bf16* out, int ld_out,
                             const int* cu_seqlens, int n_seqs, int max_seqlen, int total,
                             int heads, int head_dim, float scale, cudaStream_t stream);
 
-// One unit of chunked-prefill attention work: 64 query rows of one slice.
+// One unit of chunked-prefill attention work: up to 128 query rows of one slice.
 struct PrefillWork {
   int q_row0;     // first chunk row of this block
-  int q_rows;     // valid rows (<= 64)
+  int q_rows;     // valid rows (<= 128)
   int q_pos0;     // prompt position of q_row0
   int req_slot;   // index into the per-request page-table array
 };
+constexpr int kPrefillRows = 128;
 
 struct PagedKV {
-  bf16* k;  // [pages][kv_heads][page][head_dim] for one layer
-  bf16* v;
+  bf16* k;  // [pages][kv_heads][64 tokens][head_dim] for one layer
+  bf16* v;  // TRANSPOSED: [pages][kv_heads][head_dim][64 tokens]
   const int* const* page_tables;  // device array: req_slot -> int* page ids
   int page_size;
 };
 
-void attention_prefill_paged(const bf16* q, int ld_q, bf16* out, int ld_out,
-                             const PrefillWork* work, int n_work, const PagedKV& kv,
-                             int q_heads, int kv_heads, int head_dim, float scale,
-                             cudaStream_t stream);
+/// tcgen05 / TMEM flash attention (attention_tc.cu). q: packed QKV rows of
+/// the chunk ([q_rows_alloc, (Hq + 2 Hkv) hd], q columns first).
+void attention_prefill_paged_tc(const bf16* q, int ld_q, int q_rows_alloc, bf16* out, int ld_out,
+                                const PrefillWork* work, int n_work, const PagedKV& kv,
+                                std::int64_t kv_pages, int q_heads, int kv_heads, int head_dim,
+                                float scale, cudaStream_t stream);
 
 }  // namespace rserve

@@ -2,6 +2,9 @@
 //
 // Each op takes raw device pointers and runs ONE of the product kernels on
 // the given stream; tests compare them against a plain fp32 reference.
+#include <algorithm>
+#include <vector>
+
 #include "attention.cuh"
 #include "common.cuh"
 #include "gemm.cuh"
@@ -50,6 +53,34 @@ rs_status rs_op_attention_varlen(const void* qkv, int ld_qkv, void* out, int ld_
     attention_varlen_bidir(static_cast<const bf16*>(qkv), ld_qkv, static_cast<bf16*>(out),
                            ld_out, cu_seqlens, n_seqs, max_seqlen, total, heads, head_dim, scale,
                            static_cast<cudaStream_t>(stream));
+  });
+}
+
+rs_status rs_op_attention_prefill(const void* q, int ld_q, int rows_alloc, void* out, int ld_out,
+                                  int q_pos0, int q_rows, const void* k_cache,
+                                  const void* v_cache, long long kv_pages, const int* page_table,
+                                  int q_heads, int kv_heads, int head_dim, float scale,
+                                  void* stream) {
+  return guarded([&] {
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    std::vector<PrefillWork> work;
+    for (int r = 0; r < q_rows; r += kPrefillRows)
+      work.push_back({r, std::min(kPrefillRows, q_rows - r), q_pos0 + r, 0});
+    PrefillWork* wd = nullptr;
+    const int** ptd = nullptr;
+    RS_CUDA_CHECK(cudaMallocAsync(reinterpret_cast<void**>(&wd), work.size() * sizeof(PrefillWork), st));
+    RS_CUDA_CHECK(cudaMallocAsync(reinterpret_cast<void**>(&ptd), sizeof(int*), st));
+    RS_CUDA_CHECK(cudaMemcpyAsync(wd, work.data(), work.size() * sizeof(PrefillWork),
+                                  cudaMemcpyHostToDevice, st));
+    RS_CUDA_CHECK(cudaMemcpyAsync(ptd, &page_table, sizeof(int*), cudaMemcpyHostToDevice, st));
+    PagedKV kv{const_cast<bf16*>(static_cast<const bf16*>(k_cache)),
+               const_cast<bf16*>(static_cast<const bf16*>(v_cache)), ptd, 64};
+    attention_prefill_paged_tc(static_cast<const bf16*>(q), ld_q, rows_alloc, static_cast<bf16*>(out),
+                               ld_out, wd, static_cast<int>(work.size()), kv, kv_pages, q_heads,
+                               kv_heads, head_dim, scale, st);
+    RS_CUDA_CHECK(cudaStreamSynchronize(st));  // host vectors above go out of scope
+    RS_CUDA_CHECK(cudaFreeAsync(wd, st));
+    RS_CUDA_CHECK(cudaFreeAsync(ptd, st));
   });
 }
 

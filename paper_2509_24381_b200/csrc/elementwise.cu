@@ -175,13 +175,16 @@ __global__ void rope_kv_append_kernel(bf16* qkv, int ld, const ChunkRowInfo* __r
       __syncwarp();
       const int kvh = is_v ? head - q_heads - kv_heads : head - q_heads;
       const int* pt = page_tables[ri.req_slot];
-      const std::int64_t dst =
-          ((static_cast<std::int64_t>(pt[ri.pos / page_size]) * kv_heads + kvh) * page_size +
-           ri.pos % page_size) *
-          hd;
-      bf16* cache = is_v ? v_cache : k_cache;
-      for (int c = lane * 8; c < hd; c += 256)
-        *reinterpret_cast<uint4*>(cache + dst + c) = *reinterpret_cast<const uint4*>(v + c);
+      const std::int64_t page_head = static_cast<std::int64_t>(pt[ri.pos / page_size]) * kv_heads + kvh;
+      const int off = ri.pos % page_size;
+      if (!is_v) {  // K: [page][kv head][token][hd]
+        bf16* dst = k_cache + (page_head * page_size + off) * hd;
+        for (int c = lane * 8; c < hd; c += 256)
+          *reinterpret_cast<uint4*>(dst + c) = *reinterpret_cast<const uint4*>(v + c);
+      } else {      // V transposed: [page][kv head][hd][token]
+        bf16* dst = v_cache + page_head * hd * page_size + off;
+        for (int c = lane; c < hd; c += 32) dst[static_cast<std::int64_t>(c) * page_size] = v[c];
+      }
     }
   }
 }

@@ -255,7 +255,11 @@ void Llm::init(const Shapes& s, DeviceArena& a, int lb, int le, bool with_embed,
     L.down_w = make_linear(a, s.d, s.ff, s.ff, seed, id(kLlm, lid, kDownW), st);
     L.k_cache = alloc_bf16(a, kv_elems);
     L.v_cache = alloc_bf16(a, kv_elems);
+    // Zero-init: masked keys of a partial page must be finite (P = 0 x V).
+    RS_CUDA_CHECK(cudaMemsetAsync(L.k_cache, 0, static_cast<std::size_t>(kv_elems) * 2, st));
+    RS_CUDA_CHECK(cudaMemsetAsync(L.v_cache, 0, static_cast<std::size_t>(kv_elems) * 2, st));
   }
+  kv_pages_ = kv_pages;
   if (with_head) {
     final_ln_ = make_ones(a, s.d, st);
     head_ = make_linear(a, s.vocab, s.d, s.d, seed, id(kTop, 0, kHead), st);
@@ -293,8 +297,8 @@ void Llm::forward_stage(const ChunkDev& c, const bf16* slab, bf16* x,
     rope_kv_append(qkv_, s.qkv_dim, c.rows, M, s.hq, s.hkv, s.hd, s.cfg.rope_theta_llm, L.k_cache,
                    L.v_cache, page_tables, page_size_, st);
     PagedKV kv{L.k_cache, L.v_cache, page_tables, page_size_};
-    attention_prefill_paged(qkv_, s.qkv_dim, att_, s.hq * s.hd, c.work, c.n_work, kv, s.hq, s.hkv,
-                            s.hd, scale, st);
+    attention_prefill_paged_tc(qkv_, s.qkv_dim, max_m_, att_, s.hq * s.hd, c.work, c.n_work, kv,
+                               kv_pages_, s.hq, s.hkv, s.hd, scale, st);
     g = GemmArgs{};
     g.A = att_; g.lda = s.hq * s.hd; g.B = L.o_w; g.ldb = s.hq * s.hd; g.C = x; g.ldc = s.d;
     g.residual = x; g.ldr = s.d; g.M = M; g.N = s.d; g.K = s.hq * s.hd;

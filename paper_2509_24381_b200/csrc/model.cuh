@@ -143,6 +143,7 @@ class Llm {
  private:
   Shapes s_;
   int lb_ = 0, le_ = 0, page_size_ = 64;
+  std::int64_t kv_pages_ = 0;
   bf16* embed_ = nullptr;
   std::vector<LlmLayer> layers_;
   bf16 *final_ln_ = nullptr, *head_ = nullptr;

@@ -121,6 +121,49 @@ def test_rmsnorm(nat):
     _close(y, ref, rel=5e-3)
 
 
+def _paged_case(nat, hd, hq, hkv, pos0, rows, seed=0):
+    """One slice of `rows` queries at prompt positions pos0.. over a paged cache
+    whose pages are shuffled; fp32 torch causal reference."""
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    T = pos0 + rows
+    n_pages = (T + 63) // 64
+    pool = n_pages + 5
+    perm = torch.randperm(pool, generator=g, device="cuda")[:n_pages].to(torch.int32)
+    K = torch.randn(T, hkv, hd, device="cuda", generator=g).bfloat16()
+    V = torch.randn(T, hkv, hd, device="cuda", generator=g).bfloat16()
+    kc = torch.zeros(pool, hkv, 64, hd, device="cuda", dtype=torch.bfloat16)
+    vc = torch.zeros(pool, hkv, hd, 64, device="cuda", dtype=torch.bfloat16)
+    for t in range(0, T, 64):
+        n = min(64, T - t)
+        p = int(perm[t // 64])
+        kc[p, :, :n] = K[t:t + n].transpose(0, 1)
+        vc[p, :, :, :n] = V[t:t + n].permute(1, 2, 0)
+    rows_alloc = ((rows + 127) // 128) * 128
+    qkv = torch.randn(rows_alloc, (hq + 2 * hkv) * hd, device="cuda", generator=g).bfloat16()
+    out = torch.zeros(rows, hq * hd, device="cuda", dtype=torch.bfloat16)
+    scale = 1.0 / math.sqrt(hd)
+    nat.check(nat.lib.rs_op_attention_prefill(qkv.data_ptr(), qkv.stride(0), rows_alloc, out.data_ptr(),
+                                              out.stride(0), pos0, rows, kc.data_ptr(), vc.data_ptr(),
+                                              pool, perm.data_ptr(), hq, hkv, hd, scale, _stream()))
+    torch.cuda.synchronize()
+    q = qkv[:rows, :hq * hd].float().view(rows, hq, hd)
+    kk = K.float().repeat_interleave(hq // hkv, dim=1)
+    vv = V.float().repeat_interleave(hq // hkv, dim=1)
+    s = torch.einsum("qhd,khd->hqk", q, kk) * scale
+    qpos = torch.arange(pos0, T, device="cuda")[:, None]
+    s = s.masked_fill(torch.arange(T, device="cuda")[None, :] > qpos, float("-inf"))
+    ref = torch.einsum("hqk,khd->qhd", s.softmax(-1), vv).reshape(rows, hq * hd)
+    return out, ref
+
+
+@pytest.mark.parametrize("hd,hq,hkv,pos0,rows", [(128, 28, 4, 0, 2048), (128, 28, 4, 6528, 2048),
+                                                 (128, 4, 1, 300, 77), (64, 8, 2, 0, 1),
+                                                 (64, 8, 2, 63, 130), (128, 7, 7, 1000, 256)])
+def test_attention_prefill_tcgen05(nat, hd, hq, hkv, pos0, rows):
+    out, ref = _paged_case(nat, hd, hq, hkv, pos0, rows)
+    _close(out, ref)
+
+
 @pytest.mark.parametrize("hd,heads,lens", [(80, 4, [64, 64, 37, 64]), (80, 2, [1024, 300]),
                                            (64, 4, [256, 256, 5]), (128, 2, [130, 1])])
 def test_attention_varlen_bidir(nat, hd, heads, lens):
