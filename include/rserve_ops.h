@@ -27,6 +27,12 @@ RS_API rs_status rs_op_rmsnorm(const void* x, int ldx, const void* w, void* y, i
 RS_API rs_status rs_op_attention_varlen(const void* qkv, int ld_qkv, void* out, int ld_out,
                                  const int* cu_seqlens, int n_seqs, int max_seqlen, int total,
                                  int heads, int head_dim, float scale, void* stream);
+/* Same contract as rs_op_attention_varlen, on the tcgen05 path used by the
+ * ViT (head-padded operands built by vit_qkv_split with identity RoPE).
+ * Synchronous. */
+RS_API rs_status rs_op_attention_varlen_tc(const void* qkv, int ld_qkv, void* out, int ld_out,
+                                           const int* cu_seqlens, int n_seqs, int total,
+                                           int heads, int head_dim, float scale, void* stream);
 /* Causal chunked-prefill attention (tcgen05) of ONE slice: q rows
  * [0, q_rows) at prompt positions q_pos0.. attend to keys [0, q_pos0+q_rows)
  * of a paged cache: K [pages][kv_heads][64][hd], V^T [pages][kv_heads][hd][64],

@@ -36,6 +36,21 @@ struct PagedKV {
   int page_size;
 };
 
+/// A 128-row query block of packed varlen sequences and the key range it
+/// may touch (the union of its rows' sequences).
+struct AttnBlock {
+  int q_row0, q_rows, key_begin, key_end;
+};
+
+/// tcgen05 varlen bidirectional attention (ViT). qp / kp: [rows_alloc,
+/// heads*128] (head-padded, rotated); vt: [heads*128, rows_alloc] (V^T,
+/// head-padded). out: [rows, heads*out_hd]. Visible keys of row t: its own
+/// sequence [cu[s], cu[s+1]).
+void attention_varlen_tc(const bf16* qp, const bf16* kp, const bf16* vt, int rows_alloc,
+                         int heads, bf16* out, int ld_out, int out_hd, const AttnBlock* blocks,
+                         int n_blocks, const int* cu_seqlens, int n_seqs, float scale,
+                         cudaStream_t stream);
+
 /// tcgen05 / TMEM flash attention (attention_tc.cu). q: packed QKV rows of
 /// the chunk ([q_rows_alloc, (Hq + 2 Hkv) hd], q columns first).
 void attention_prefill_paged_tc(const bf16* q, int ld_q, int q_rows_alloc, bf16* out, int ld_out,

@@ -1,19 +1,21 @@
-// rserve-b200 — chunked-prefill causal attention over the paged KV cache on
-// tcgen05 tensor cores (sm_100a).
+// rserve-b200 — flash attention on tcgen05 tensor cores (sm_100a).
 //
-// CTA = one 128-query block of one slice x one q head (GQA: kv head = h / g).
-// Per iteration of 128 keys (two 64-token KV pages):
-//   S_j  = Q . K_j^T      tcgen05.mma, Q and K from smem (TMA, SW128), S in TMEM
-//   P_j  = softmax rows   4 warps, one query row per thread, read S via
-//                         tcgen05.ld, online max / sum in fp32, P written to smem
-//                         as bf16 in the SW128 K-major layout
-//   O~_j = P_j . V_j      tcgen05.mma into TMEM (fresh accumulator); the softmax
-//                         warps fold it into their fp32 register accumulator
-//                         O = O * exp2(m_{j-1} - m_j) + O~_j
-// S and O~ are double-buffered in TMEM (4 x 128 columns) and K/V in smem, so the
-// tensor core computes S_{j+1} while the softmax warps work on P_j.
-// V is stored TRANSPOSED in the cache ([page][kv head][hd][64 tokens]) so that
-// both MMAs read K-major SW128 operands (the GEMM's descriptor path).
+// One kernel, two key sources:
+//   * kPaged  — LLM chunked prefill: a 128-query block of one slice attends
+//     causally to its request's paged KV cache (GQA: kv head = h / g).
+//   * kVarlen — ViT: a 128-token block of the packed sequence attends
+//     bidirectionally within each row's own sequence (window or image,
+//     cu_seqlens); Q / K are head-padded to 128 columns and V is transposed
+//     by vit_qkv_split (elementwise.cu) so the tiles are plain SW128 K-major.
+// Per iteration of 128 keys:
+//   S_j  = Q . K_j^T      tcgen05.mma (SS), S double-buffered in TMEM
+//   P_j  = softmax rows   4 warps, one query row per thread (tcgen05.ld), fp32
+//                         online max / sum, P -> smem bf16 in the SW128 layout
+//   O   += P_j . V_j      tcgen05.mma into one TMEM accumulator; the running max
+//                         is raised lazily (only when it grows by > 2^8) and O
+//                         is then rescaled in TMEM (tcgen05.ld / st)
+// V is held transposed ([hd][keys]) so both MMAs read K-major SW128 operands
+// with the same descriptors as the GEMM.
 #include <cuda.h>
 #include <cuda_runtime.h>
 
@@ -37,26 +39,45 @@ struct TcCfg {
   static constexpr int kHdAtoms = HD / 64;             // K-dim atoms of Q / K tiles
   static constexpr int kQBytes = kHdAtoms * kAtom;     // Q [128 x HD]
   static constexpr int kKBytes = kHdAtoms * kAtom;     // K [128 keys x HD]
-  static constexpr int kVAtom = HD * 128;              // V^T page [HD x 64 keys]
-  static constexpr int kVBytes = 2 * kVAtom;           // two pages
+  static constexpr int kVAtom = HD * 128;              // V^T [HD x 64 keys]
+  static constexpr int kVBytes = 2 * kVAtom;           // 128 keys
   static constexpr int kPBytes = 2 * kAtom;            // P [128 q x 128 keys]
   static constexpr int kStages = 2;
   static constexpr int kSmem = kQBytes + kStages * (kKBytes + kVBytes) + 2 * kPBytes + 1024 + 512;
-  static constexpr int kPageBytes = 64 * HD * 2 * 2;   // K + V of one page
+  static constexpr int kKvBytes = kKBytes + kVBytes;   // one iteration
+};
+
+enum class KvMode { kPaged, kVarlen };
+
+struct TcParams {
+  const PrefillWork* work;          // kPaged
+  const int* const* page_tables;    // kPaged
+  const AttnBlock* blocks;          // kVarlen
+  const int* cu_seqlens;            // kVarlen
+  int n_seqs;
+  int q_heads, kv_heads;
+  int q_head_stride;                // q / k column stride between heads
+  int out_hd;                       // output columns per head (<= HD)
+  float scale_log2;
+  bf16* out;
+  int ld_out;
 };
 
 __device__ __forceinline__ void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 
-template <int HD>
+// MUFU ex2 (flush-to-zero); ex2(-inf) = +0.
+__device__ __forceinline__ float fast_exp2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+template <int HD, KvMode MODE>
 __global__ void __launch_bounds__(kTcThreads, 1)
-    fa_prefill_tc_kernel(const __grid_constant__ CUtensorMap tmQ,
-                         const __grid_constant__ CUtensorMap tmK,
-                         const __grid_constant__ CUtensorMap tmV,
-                         const PrefillWork* __restrict__ work, const int* const* page_tables,
-                         int q_heads, int kv_heads, float scale_log2, bf16* __restrict__ out,
-                         int ld_out) {
+    fa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+                 const __grid_constant__ CUtensorMap tmV, const TcParams p) {
   using C = TcCfg<HD>;
   extern __shared__ __align__(1024) std::uint8_t smem_raw[];
   std::uint8_t* smem = reinterpret_cast<std::uint8_t*>(
@@ -73,17 +94,31 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   std::uint64_t* s_empty = bars + 7;
   std::uint64_t* p_full = bars + 9;
   std::uint64_t* o_full = bars + 11;
-  std::uint64_t* o_empty = bars + 13;
   std::uint32_t* tmem_holder = reinterpret_cast<std::uint32_t*>(bars + 16);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const PrefillWork w = work[blockIdx.x];
   const int head = blockIdx.y;
-  const int kvh = head / (q_heads / kv_heads);
-  const int n_keys = w.q_pos0 + w.q_rows;
-  const int n_pages = (n_keys + 63) / 64;
+  const int kvh = head / (p.q_heads / p.kv_heads);
+  int q_row0, q_rows, key_begin, key_end;
+  const int* pt = nullptr;
+  int q_pos0 = 0;
+  if constexpr (MODE == KvMode::kPaged) {
+    const PrefillWork w = p.work[blockIdx.x];
+    q_row0 = w.q_row0;
+    q_rows = w.q_rows;
+    q_pos0 = w.q_pos0;
+    key_begin = 0;
+    key_end = w.q_pos0 + w.q_rows;
+    pt = p.page_tables[w.req_slot];
+  } else {
+    const AttnBlock b = p.blocks[blockIdx.x];
+    q_row0 = b.q_row0;
+    q_rows = b.q_rows;
+    key_begin = b.key_begin;
+    key_end = b.key_end;
+  }
+  const int n_keys = key_end - key_begin;
   const int n_it = (n_keys + 127) / 128;
-  const int* pt = page_tables[w.req_slot];
 
   if (threadIdx.x == 0) {
     sm100::tma_prefetch_desc(&tmQ);
@@ -96,61 +131,66 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       sm100::mbar_init(&s_full[i], 1);
       sm100::mbar_init(&s_empty[i], 128);
       sm100::mbar_init(&p_full[i], 128);
-      sm100::mbar_init(&o_full[i], 1);
-      sm100::mbar_init(&o_empty[i], 128);
     }
+    sm100::mbar_init(o_full, 1);
     sm100::fence_mbar_init();
   }
   if (warp == 2) sm100::tmem_alloc(tmem_holder, 512);
   sm100::tc_fence_before();
   __syncthreads();
   sm100::tc_fence_after();
-  const std::uint32_t tmem = *tmem_holder;
-  // TMEM columns: S[0] 0, S[1] 128, O~[0] 256, O~[1] 384
+  const std::uint32_t tmem = *tmem_holder;  // S[0] 0, S[1] 128, O 256
 
   if (warp == 0 && lane == 0) {
     // ---------------- TMA producer ----------------
     sm100::mbar_expect_tx(q_full, C::kQBytes);
     for (int h = 0; h < C::kHdAtoms; ++h)
-      sm100::tma_load_2d(sQ + h * kAtom, &tmQ, q_full, head * HD + h * 64, w.q_row0);
+      sm100::tma_load_2d(sQ + h * kAtom, &tmQ, q_full, head * p.q_head_stride + h * 64, q_row0);
+    const int n_pages = (n_keys + 63) / 64;
     for (int j = 0; j < n_it; ++j) {
       const int st = j & 1;
       sm100::mbar_wait(&kv_empty[st], ((j >> 1) & 1) ^ 1);
-      sm100::mbar_expect_tx(&kv_full[st], 2 * C::kPageBytes);
-      const int pa = pt[2 * j];
-      const int pb = 2 * j + 1 < n_pages ? pt[2 * j + 1] : pa;  // duplicate: finite, masked
+      sm100::mbar_expect_tx(&kv_full[st], C::kKvBytes);
       std::uint8_t* k = sK + st * C::kKBytes;
       std::uint8_t* v = sV + st * C::kVBytes;
-      for (int h = 0; h < C::kHdAtoms; ++h) {
-        sm100::tma_load_2d(k + h * kAtom, &tmK, &kv_full[st], h * 64, (pa * kv_heads + kvh) * 64);
-        sm100::tma_load_2d(k + h * kAtom + 64 * 128, &tmK, &kv_full[st], h * 64,
-                           (pb * kv_heads + kvh) * 64);
+      if constexpr (MODE == KvMode::kPaged) {
+        const int pa = pt[2 * j];
+        const int pb = 2 * j + 1 < n_pages ? pt[2 * j + 1] : pa;  // duplicate: finite, masked
+        for (int h = 0; h < C::kHdAtoms; ++h) {
+          sm100::tma_load_2d(k + h * kAtom, &tmK, &kv_full[st], h * 64, (pa * p.kv_heads + kvh) * 64);
+          sm100::tma_load_2d(k + h * kAtom + 64 * 128, &tmK, &kv_full[st], h * 64,
+                             (pb * p.kv_heads + kvh) * 64);
+        }
+        sm100::tma_load_2d(v, &tmV, &kv_full[st], 0, (pa * p.kv_heads + kvh) * HD);
+        sm100::tma_load_2d(v + C::kVAtom, &tmV, &kv_full[st], 0, (pb * p.kv_heads + kvh) * HD);
+      } else {
+        const int k0 = key_begin + 128 * j;
+        for (int h = 0; h < C::kHdAtoms; ++h)
+          sm100::tma_load_2d(k + h * kAtom, &tmK, &kv_full[st], kvh * p.q_head_stride + h * 64, k0);
+        sm100::tma_load_2d(v, &tmV, &kv_full[st], k0, kvh * HD);
+        sm100::tma_load_2d(v + C::kVAtom, &tmV, &kv_full[st], k0 + 64, kvh * HD);
       }
-      sm100::tma_load_2d(v, &tmV, &kv_full[st], 0, (pa * kv_heads + kvh) * HD);
-      sm100::tma_load_2d(v + C::kVAtom, &tmV, &kv_full[st], 0, (pb * kv_heads + kvh) * HD);
     }
   } else if (warp == 1 && lane == 0) {
     // ---------------- MMA issuer ----------------
     constexpr std::uint32_t idesc_s = sm100::idesc_bf16_f32(128, 128);
     constexpr std::uint32_t idesc_o = sm100::idesc_bf16_f32(128, HD);
     sm100::mbar_wait(q_full, 0);
-    // O accumulates in one TMEM region (cols 256..) across all iterations.
     auto issue_pv = [&](int i) {
       const int b = i & 1;
       sm100::mbar_wait(&p_full[b], (i >> 1) & 1);
       sm100::tc_fence_after();
-      const std::uint32_t d = tmem + 256;
       std::uint8_t* v = sV + b * C::kVBytes;
-      std::uint8_t* p = sP + b * C::kPBytes;
+      std::uint8_t* pp = sP + b * C::kPBytes;
 #pragma unroll
       for (int a = 0; a < 2; ++a) {
-        const std::uint64_t pd = sm100::sw128_kmajor_desc(sm100::smem_u32(p + a * kAtom));
+        const std::uint64_t pd = sm100::sw128_kmajor_desc(sm100::smem_u32(pp + a * kAtom));
         const std::uint64_t vd = sm100::sw128_kmajor_desc(sm100::smem_u32(v + a * C::kVAtom));
 #pragma unroll
         for (int kk = 0; kk < 4; ++kk)
-          sm100::umma_bf16(d, pd + 2 * kk, vd + 2 * kk, idesc_o, (i | a | kk) != 0 ? 1u : 0u);
+          sm100::umma_bf16(tmem + 256, pd + 2 * kk, vd + 2 * kk, idesc_o, (i | a | kk) != 0 ? 1u : 0u);
       }
-      sm100::umma_commit(&o_full[0]);  // completion count = PV index + 1
+      sm100::umma_commit(o_full);  // completion count = PV index + 1
       sm100::umma_commit(&kv_empty[b]);
     };
     for (int j = 0; j < n_it; ++j) {
@@ -158,7 +198,6 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       sm100::mbar_wait(&kv_full[b], (j >> 1) & 1);
       sm100::mbar_wait(&s_empty[b], ((j >> 1) & 1) ^ 1);
       sm100::tc_fence_after();
-      const std::uint32_t d = tmem + 128 * b;
       std::uint8_t* k = sK + b * C::kKBytes;
 #pragma unroll
       for (int h = 0; h < C::kHdAtoms; ++h) {
@@ -166,41 +205,62 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         const std::uint64_t kd = sm100::sw128_kmajor_desc(sm100::smem_u32(k + h * kAtom));
 #pragma unroll
         for (int kk = 0; kk < 4; ++kk)
-          sm100::umma_bf16(d, qd + 2 * kk, kd + 2 * kk, idesc_s, (h | kk) != 0 ? 1u : 0u);
+          sm100::umma_bf16(tmem + 128 * b, qd + 2 * kk, kd + 2 * kk, idesc_s, (h | kk) != 0 ? 1u : 0u);
       }
       sm100::umma_commit(&s_full[b]);
       if (j >= 1) issue_pv(j - 1);
     }
     issue_pv(n_it - 1);
   } else if (warp >= 4) {
-    // ---------------- softmax / accumulation (one query row per thread) ----------------
+    // ---------------- softmax (one query row per thread) ----------------
     const int q = warp - 4;
     const int r = q * 32 + lane;
-    const int q_pos = w.q_pos0 + r;
     const std::uint32_t lane_off = static_cast<std::uint32_t>(q * 32) << 16;
     const std::uint32_t o_tmem = tmem + lane_off + 256;
-    // Running max used for P (lazily raised: only when the true max exceeds it
-    // by > 8 in log2 units, which bounds P by 2^8; O in TMEM is then rescaled).
+    // Visible keys of this row: absolute key index in [lo, hi).
+    int lo, hi;
+    if constexpr (MODE == KvMode::kPaged) {
+      lo = 0;
+      hi = min(q_pos0 + r + 1, key_end);
+    } else {
+      const int t = q_row0 + min(r, q_rows - 1);
+      int a = 0, b = p.n_seqs;  // largest s with cu[s] <= t
+      while (b - a > 1) {
+        const int mid = (a + b) >> 1;
+        if (p.cu_seqlens[mid] <= t) a = mid;
+        else b = mid;
+      }
+      lo = p.cu_seqlens[a];
+      hi = p.cu_seqlens[a + 1];
+    }
     float m = -INFINITY, l = 0.f;
     for (int j = 0; j < n_it; ++j) {
       const int b = j & 1;
       sm100::mbar_wait(&s_full[b], (j >> 1) & 1);
       sm100::tc_fence_after();
-      const int key0 = j * 128;
-      const int lim = min(q_pos, n_keys - 1);  // keys <= lim are visible
-      float mx = -INFINITY;
+      const int key0 = key_begin + j * 128;
+      const int c_lo = lo - key0, c_hi = hi - key0;  // visible columns [c_lo, c_hi)
+      // Whole S row in registers (one TMEM pass); masked entries -> -inf.
+      std::uint32_t sv[128];
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
-        std::uint32_t v[32];
+        std::uint32_t(&v)[32] = *reinterpret_cast<std::uint32_t(*)[32]>(&sv[32 * c]);
         sm100::tmem_ld_32x32b_x32(tmem + lane_off + 128 * b + 32 * c, v);
-        sm100::tmem_ld_wait();
-#pragma unroll
-        for (int t = 0; t < 32; ++t)
-          if (key0 + 32 * c + t <= lim) mx = fmaxf(mx, __uint_as_float(v[t]) * scale_log2);
       }
-      // PV_{j-1} must be complete before O may be rescaled (and, in order,
-      // before this step's P feeds PV_j).
-      if (j > 0) sm100::mbar_wait(&o_full[0], (j - 1) & 1);
+      sm100::tmem_ld_wait();
+      sm100::tc_fence_before();
+      sm100::mbar_arrive(&s_empty[b]);  // S buffer may be overwritten now
+      if (!(c_lo <= 0 && c_hi >= 128)) {
+#pragma unroll
+        for (int t = 0; t < 128; ++t)
+          if (t < c_lo || t >= c_hi) sv[t] = __float_as_uint(-INFINITY);
+      }
+      float mx = -INFINITY;
+#pragma unroll
+      for (int t = 0; t < 128; ++t) mx = fmaxf(mx, __uint_as_float(sv[t]));
+      mx *= p.scale_log2;
+      // PV_{j-1} must be complete before O may be rescaled (in order).
+      if (j > 0) sm100::mbar_wait(o_full, (j - 1) & 1);
       const bool raise = mx > m + 8.f || (m == -INFINITY && mx != -INFINITY);
       float alpha = 1.f;
       if (raise) {
@@ -220,26 +280,22 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         }
         sm100::tmem_st_wait();
       }
-      const float m_new = m;
-      float rs = 0.f;
+      const float mneg = m == -INFINITY ? 0.f : -m;
+      float rs0 = 0.f, rs1 = 0.f;
       std::uint8_t* prow = sP + b * C::kPBytes + r * 128;
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
-        std::uint32_t v[32];
-        sm100::tmem_ld_32x32b_x32(tmem + lane_off + 128 * b + 32 * c, v);
-        sm100::tmem_ld_wait();
         std::uint32_t packed[16];
 #pragma unroll
         for (int t = 0; t < 16; ++t) {
-          const int k0 = key0 + 32 * c + 2 * t;
-          const float s0 = __uint_as_float(v[2 * t]) * scale_log2;
-          const float s1 = __uint_as_float(v[2 * t + 1]) * scale_log2;
-          const float p0 = (k0 <= lim && m_new != -INFINITY) ? exp2f(s0 - m_new) : 0.f;
-          const float p1 = (k0 + 1 <= lim && m_new != -INFINITY) ? exp2f(s1 - m_new) : 0.f;
-          rs += p0 + p1;
+          // exp2(-inf) = 0 for masked entries
+          const float p0 = fast_exp2(fmaf(__uint_as_float(sv[32 * c + 2 * t]), p.scale_log2, mneg));
+          const float p1 = fast_exp2(fmaf(__uint_as_float(sv[32 * c + 2 * t + 1]), p.scale_log2, mneg));
+          rs0 += p0;
+          rs1 += p1;
           packed[t] = pack_bf16x2(p0, p1);
         }
-        // 32 keys = 4 16-byte chunks; atom = c / 2 (64 keys), chunk = (c % 2) * 4 + u
+        // 32 keys = 4 16-byte chunks; atom c/2 (64 keys), chunk (c%2)*4 + u, XOR-swizzled
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
           const int chunk = (c & 1) * 4 + u;
@@ -248,28 +304,29 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         }
       }
       sm100::tc_fence_before();
-      sm100::mbar_arrive(&s_empty[b]);
       fence_proxy_async_smem();
       sm100::mbar_arrive(&p_full[b]);
-      l = l * alpha + rs;
+      l = l * alpha + (rs0 + rs1);
     }
-    sm100::mbar_wait(&o_full[0], (n_it - 1) & 1);
+    sm100::mbar_wait(o_full, (n_it - 1) & 1);
     sm100::tc_fence_after();
     const float inv = l > 0.f ? 1.f / l : 0.f;
-    bf16* orow = out + static_cast<std::int64_t>(w.q_row0 + r) * ld_out + head * HD;
+    bf16* orow = p.out + static_cast<std::int64_t>(q_row0 + r) * p.ld_out + head * p.out_hd;
 #pragma unroll
     for (int c = 0; c < HD / 32; ++c) {
       std::uint32_t v[32];
       sm100::tmem_ld_32x32b_x32(o_tmem + 32 * c, v);
       sm100::tmem_ld_wait();
-      if (r < w.q_rows) {
+      if (r < q_rows) {
 #pragma unroll
-        for (int u = 0; u < 4; ++u)
-          reinterpret_cast<uint4*>(orow + 32 * c)[u] = make_uint4(
-              pack_bf16x2(__uint_as_float(v[8 * u]) * inv, __uint_as_float(v[8 * u + 1]) * inv),
-              pack_bf16x2(__uint_as_float(v[8 * u + 2]) * inv, __uint_as_float(v[8 * u + 3]) * inv),
-              pack_bf16x2(__uint_as_float(v[8 * u + 4]) * inv, __uint_as_float(v[8 * u + 5]) * inv),
-              pack_bf16x2(__uint_as_float(v[8 * u + 6]) * inv, __uint_as_float(v[8 * u + 7]) * inv));
+        for (int u = 0; u < 4; ++u) {
+          if (32 * c + 8 * u < p.out_hd)
+            reinterpret_cast<uint4*>(orow + 32 * c)[u] = make_uint4(
+                pack_bf16x2(__uint_as_float(v[8 * u]) * inv, __uint_as_float(v[8 * u + 1]) * inv),
+                pack_bf16x2(__uint_as_float(v[8 * u + 2]) * inv, __uint_as_float(v[8 * u + 3]) * inv),
+                pack_bf16x2(__uint_as_float(v[8 * u + 4]) * inv, __uint_as_float(v[8 * u + 5]) * inv),
+                pack_bf16x2(__uint_as_float(v[8 * u + 6]) * inv, __uint_as_float(v[8 * u + 7]) * inv));
+        }
       }
     }
   }
@@ -299,7 +356,8 @@ EncodeTiledFn encode_fn() {
 }
 
 // 2D bf16 [rows, cols] row-major (stride ld), box [box_rows, 64 cols], SW128.
-CUtensorMap map_2d(const void* base, std::int64_t rows, int cols, int ld, int box_rows) {
+CUtensorMap map_2d(const void* base, std::int64_t rows, std::int64_t cols, std::int64_t ld,
+                   int box_rows) {
   CUtensorMap tm;
   std::memset(&tm, 0, sizeof tm);
   const cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
@@ -317,8 +375,8 @@ CUtensorMap map_2d(const void* base, std::int64_t rows, int cols, int ld, int bo
 
 struct MapKey {
   const void* p;
-  std::int64_t rows;
-  int cols, ld, box;
+  std::int64_t rows, cols, ld;
+  int box;
   bool operator==(const MapKey& o) const {
     return p == o.p && rows == o.rows && cols == o.cols && ld == o.ld && box == o.box;
   }
@@ -330,7 +388,8 @@ struct MapHash {
   }
 };
 
-CUtensorMap cached_map(const void* base, std::int64_t rows, int cols, int ld, int box_rows) {
+CUtensorMap cached_map(const void* base, std::int64_t rows, std::int64_t cols, std::int64_t ld,
+                       int box_rows) {
   static std::mutex mu;
   static std::unordered_map<MapKey, CUtensorMap, MapHash> cache;
   const MapKey key{base, rows, cols, ld, box_rows};
@@ -341,26 +400,21 @@ CUtensorMap cached_map(const void* base, std::int64_t rows, int cols, int ld, in
   return cache.emplace(key, map_2d(base, rows, cols, ld, box_rows)).first->second;
 }
 
-template <int HD>
-void launch_tc(const bf16* q, int ld_q, int q_rows_alloc, bf16* out, int ld_out,
-               const PrefillWork* work, int n_work, const PagedKV& kv, std::int64_t kv_pages,
-               int qh, int kvh, float scale, cudaStream_t st) {
+template <int HD, KvMode MODE>
+void launch(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv, const TcParams& p,
+            int n_blocks, cudaStream_t st, const char* klass) {
   using C = TcCfg<HD>;
   static bool set = false;
   if (!set) {
-    RS_CUDA_CHECK(cudaFuncSetAttribute(fa_prefill_tc_kernel<HD>,
+    RS_CUDA_CHECK(cudaFuncSetAttribute(fa_tc_kernel<HD, MODE>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem));
     set = true;
   }
-  const CUtensorMap tq = cached_map(q, q_rows_alloc, (qh + 2 * kvh) * HD, ld_q, 128);
-  const CUtensorMap tk = cached_map(kv.k, kv_pages * kvh * 64, HD, HD, 64);
-  const CUtensorMap tv = cached_map(kv.v, kv_pages * kvh * HD, 64, 64, HD);
-  dim3 grid(n_work, qh);
+  dim3 grid(n_blocks, p.q_heads);
   const int tok = prof::begin(st);
-  fa_prefill_tc_kernel<HD><<<grid, kTcThreads, C::kSmem, st>>>(
-      tq, tk, tv, work, kv.page_tables, qh, kvh, scale * 1.4426950408889634f, out, ld_out);
+  fa_tc_kernel<HD, MODE><<<grid, kTcThreads, C::kSmem, st>>>(tq, tk, tv, p);
   RS_LAUNCH_CHECK();
-  prof::end(tok, st, "attn_prefill_tcgen05", 0, 0);
+  prof::end(tok, st, klass, 0, 0);
   count_launch();
 }
 
@@ -372,11 +426,47 @@ void attention_prefill_paged_tc(const bf16* q, int ld_q, int q_rows_alloc, bf16*
                                 float scale, cudaStream_t stream) {
   if (n_work <= 0) return;
   if (kv.page_size != 64) throw DeviceError(RS_ERR_CUDA, "tc attention needs 64-token pages");
+  TcParams p{};
+  p.work = work;
+  p.page_tables = kv.page_tables;
+  p.q_heads = q_heads;
+  p.kv_heads = kv_heads;
+  p.q_head_stride = head_dim;
+  p.out_hd = head_dim;
+  p.scale_log2 = scale * 1.4426950408889634f;
+  p.out = out;
+  p.ld_out = ld_out;
+  const CUtensorMap tq = cached_map(q, q_rows_alloc, (q_heads + 2 * kv_heads) * head_dim, ld_q, 128);
+  const CUtensorMap tk = cached_map(kv.k, kv_pages * kv_heads * 64, head_dim, head_dim, 64);
+  const CUtensorMap tv = cached_map(kv.v, kv_pages * kv_heads * head_dim, 64, 64, head_dim);
   switch (head_dim) {
-    case 64: return launch_tc<64>(q, ld_q, q_rows_alloc, out, ld_out, work, n_work, kv, kv_pages, q_heads, kv_heads, scale, stream);
-    case 128: return launch_tc<128>(q, ld_q, q_rows_alloc, out, ld_out, work, n_work, kv, kv_pages, q_heads, kv_heads, scale, stream);
+    case 64: return launch<64, KvMode::kPaged>(tq, tk, tv, p, n_work, stream, "attn_prefill_tcgen05");
+    case 128: return launch<128, KvMode::kPaged>(tq, tk, tv, p, n_work, stream, "attn_prefill_tcgen05");
     default: throw DeviceError(RS_ERR_CUDA, "tc attention: unsupported head_dim " + std::to_string(head_dim));
   }
+}
+
+void attention_varlen_tc(const bf16* qp, const bf16* kp, const bf16* vt, int rows_alloc,
+                         int heads, bf16* out, int ld_out, int out_hd, const AttnBlock* blocks,
+                         int n_blocks, const int* cu_seqlens, int n_seqs, float scale,
+                         cudaStream_t stream) {
+  if (n_blocks <= 0) return;
+  constexpr int HD = 128;
+  TcParams p{};
+  p.blocks = blocks;
+  p.cu_seqlens = cu_seqlens;
+  p.n_seqs = n_seqs;
+  p.q_heads = heads;
+  p.kv_heads = heads;
+  p.q_head_stride = HD;
+  p.out_hd = out_hd;
+  p.scale_log2 = scale * 1.4426950408889634f;
+  p.out = out;
+  p.ld_out = ld_out;
+  const CUtensorMap tq = cached_map(qp, rows_alloc, heads * HD, heads * HD, 128);
+  const CUtensorMap tk = cached_map(kp, rows_alloc, heads * HD, heads * HD, 128);
+  const CUtensorMap tv = cached_map(vt, static_cast<std::int64_t>(heads) * HD, rows_alloc, rows_alloc, HD);
+  launch<HD, KvMode::kVarlen>(tq, tk, tv, p, n_blocks, stream, "attn_vit_tcgen05");
 }
 
 }  // namespace rserve

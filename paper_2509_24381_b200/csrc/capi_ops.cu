@@ -56,6 +56,54 @@ rs_status rs_op_attention_varlen(const void* qkv, int ld_qkv, void* out, int ld_
   });
 }
 
+rs_status rs_op_attention_varlen_tc(const void* qkv, int ld_qkv, void* out, int ld_out,
+                                    const int* cu_seqlens, int n_seqs, int total, int heads,
+                                    int head_dim, float scale, void* stream) {
+  return guarded([&] {
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    std::vector<int> cu(static_cast<std::size_t>(n_seqs) + 1);
+    RS_CUDA_CHECK(cudaMemcpyAsync(cu.data(), cu_seqlens, cu.size() * 4, cudaMemcpyDeviceToHost, st));
+    RS_CUDA_CHECK(cudaStreamSynchronize(st));
+    std::vector<AttnBlock> blocks;
+    std::size_t s = 0;
+    for (int r = 0; r < total; r += kPrefillRows) {
+      const int r1 = std::min(total, r + kPrefillRows);
+      while (s + 1 < cu.size() && cu[s + 1] <= r) ++s;
+      std::size_t e = s;
+      while (e + 1 < cu.size() && cu[e + 1] < r1) ++e;
+      blocks.push_back({r, r1 - r, cu[s], cu[e + 1]});
+    }
+    const int rows_alloc = (total + 7) / 8 * 8;
+    const std::size_t padded = static_cast<std::size_t>(rows_alloc) * heads * 128 * 2;
+    void *qp, *kp, *vt, *pos, *bd;
+    RS_CUDA_CHECK(cudaMallocAsync(&qp, padded, st));
+    RS_CUDA_CHECK(cudaMallocAsync(&kp, padded, st));
+    RS_CUDA_CHECK(cudaMallocAsync(&vt, padded, st));
+    RS_CUDA_CHECK(cudaMallocAsync(&pos, static_cast<std::size_t>(total) * 8, st));
+    RS_CUDA_CHECK(cudaMallocAsync(&bd, blocks.size() * sizeof(AttnBlock), st));
+    RS_CUDA_CHECK(cudaMemsetAsync(qp, 0, padded, st));
+    RS_CUDA_CHECK(cudaMemsetAsync(kp, 0, padded, st));
+    RS_CUDA_CHECK(cudaMemsetAsync(vt, 0, padded, st));
+    RS_CUDA_CHECK(cudaMemsetAsync(pos, 0, static_cast<std::size_t>(total) * 8, st));  // RoPE = id
+    RS_CUDA_CHECK(cudaMemcpyAsync(bd, blocks.data(), blocks.size() * sizeof(AttnBlock),
+                                  cudaMemcpyHostToDevice, st));
+    void* table;
+    RS_CUDA_CHECK(cudaMallocAsync(&table, static_cast<std::size_t>(total) * head_dim / 2 * sizeof(float2), st));
+    vit_rope_table(static_cast<const std::int32_t*>(pos), total, head_dim, 10000.f,
+                   static_cast<float2*>(table), st);
+    vit_qkv_split(static_cast<const bf16*>(qkv), ld_qkv, static_cast<const float2*>(table), total,
+                  heads, head_dim, static_cast<bf16*>(qp), static_cast<bf16*>(kp),
+                  static_cast<bf16*>(vt), rows_alloc, st);
+    RS_CUDA_CHECK(cudaFreeAsync(table, st));
+    attention_varlen_tc(static_cast<bf16*>(qp), static_cast<bf16*>(kp), static_cast<bf16*>(vt),
+                        rows_alloc, heads, static_cast<bf16*>(out), ld_out, head_dim,
+                        static_cast<const AttnBlock*>(bd), static_cast<int>(blocks.size()),
+                        cu_seqlens, n_seqs, scale, st);
+    RS_CUDA_CHECK(cudaStreamSynchronize(st));
+    for (void* p : {qp, kp, vt, pos, bd}) RS_CUDA_CHECK(cudaFreeAsync(p, st));
+  });
+}
+
 rs_status rs_op_attention_prefill(const void* q, int ld_q, int rows_alloc, void* out, int ld_out,
                                   int q_pos0, int q_rows, const void* k_cache,
                                   const void* v_cache, long long kv_pages, const int* page_table,

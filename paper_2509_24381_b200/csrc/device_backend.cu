@@ -1,5 +1,6 @@
 // rserve-b200 — the B200 ExecutionBackend (see device_backend.cuh).
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 
 #include "device_backend.cuh"
@@ -19,12 +20,23 @@ DeviceBackend::DeviceBackend(Context& ctx, const lmmsim::SimConfig& cfg, bool re
   if (cfg.stages < 1) throw lmmsim::ConfigError("stages: must be >= 1");
   const int workers = cfg.encoder_workers;
   const Shapes& s = ctx.shapes();
-  enc_streams_.resize(static_cast<std::size_t>(workers));
-  for (auto& st : enc_streams_) RS_CUDA_CHECK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
   // One prefill stream: all stages of this GPU share the SMs and the per-stage
   // scratch; each chunk owns its residual buffer so stages can interleave.
   stage_streams_.resize(1);
   RS_CUDA_CHECK(cudaStreamCreateWithFlags(&stage_streams_[0], cudaStreamNonBlocking));
+  // RS_SERIALIZE=1 (diagnostics): encoders share the prefill stream, so
+  // per-kernel event times are not inflated by cross-stream queueing.
+  const char* ser = std::getenv("RS_SERIALIZE");
+  const bool serialize = ser != nullptr && ser[0] == '1';
+  enc_streams_.resize(static_cast<std::size_t>(workers));
+  for (auto& st : enc_streams_) {
+    if (serialize) {
+      st = stage_streams_[0];
+      shared_streams_ = true;
+    } else {
+      RS_CUDA_CHECK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    }
+  }
   RS_CUDA_CHECK(cudaStreamCreateWithFlags(&copy_stream_, cudaStreamNonBlocking));
   const std::size_t max_tok = ctx.options().max_encode_tokens;
   for (int i = 0; i < workers * kRing; ++i) {
@@ -65,7 +77,8 @@ DeviceBackend::~DeviceBackend() {
   for (bf16* p : xbufs_) cudaFree(p);
   for (cudaEvent_t e : event_pool_) cudaEventDestroy(e);
   if (origin_) cudaEventDestroy(origin_);
-  for (auto st : enc_streams_) cudaStreamDestroy(st);
+  if (!shared_streams_)
+    for (auto st : enc_streams_) cudaStreamDestroy(st);
   for (auto st : stage_streams_) cudaStreamDestroy(st);
   if (copy_stream_) cudaStreamDestroy(copy_stream_);
 }

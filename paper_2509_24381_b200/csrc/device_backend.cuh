@@ -88,6 +88,7 @@ class DeviceBackend final : public lmmsim::ExecutionBackend {
   bool realtime_, e2e_;
   std::uint64_t seed_;
   std::vector<cudaStream_t> enc_streams_;
+  bool shared_streams_ = false;
   std::vector<cudaStream_t> stage_streams_;
   cudaStream_t copy_stream_ = nullptr;
   cudaEvent_t origin_ = nullptr;

@@ -69,6 +69,57 @@ __global__ void fill_ids_kernel(std::int32_t* dst, std::int64_t n, std::uint64_t
     dst[e] = static_cast<std::int32_t>(mix64(seed, stream, static_cast<std::uint64_t>(e)) % modulo);
 }
 
+// Single-pass RMSNorm: the row stays in registers (VPL 16-byte vectors per
+// lane, dim = 256 * VPL), so HBM sees one read and one write per element.
+template <int VPL>
+__global__ void rmsnorm_reg_kernel(const bf16* __restrict__ x, int ldx, const bf16* __restrict__ w,
+                                   bf16* __restrict__ y, int ldy, int rows, float eps,
+                                   const std::int64_t* __restrict__ row_map,
+                                   bf16* __restrict__ x_copy, int ld_copy) {
+  constexpr int kDim = VPL * 256;
+  const int lane = threadIdx.x & 31;
+  for (int m = blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5); m < rows;
+       m += gridDim.x * kWarpsPerBlock) {
+    const std::int64_t src = row_map != nullptr ? row_map[m] : m;
+    const bf16* xr = x + src * ldx;
+    uint4 v[VPL];
+#pragma unroll
+    for (int k = 0; k < VPL; ++k) v[k] = *reinterpret_cast<const uint4*>(xr + lane * 8 + k * 256);
+    float ss = 0.f;
+#pragma unroll
+    for (int k = 0; k < VPL; ++k) {
+      const std::uint32_t vw[4] = {v[k].x, v[k].y, v[k].z, v[k].w};
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        const float2 f = unpack_bf16x2(vw[t]);
+        ss += f.x * f.x + f.y * f.y;
+      }
+    }
+    if (x_copy != nullptr) {
+#pragma unroll
+      for (int k = 0; k < VPL; ++k)
+        *reinterpret_cast<uint4*>(x_copy + static_cast<std::int64_t>(m) * ld_copy + lane * 8 + k * 256) = v[k];
+    }
+    ss = warp_sum(ss);
+    const float inv = rsqrtf(ss / static_cast<float>(kDim) + eps);
+    bf16* yr = y + static_cast<std::int64_t>(m) * ldy;
+#pragma unroll
+    for (int k = 0; k < VPL; ++k) {
+      const uint4 g = *reinterpret_cast<const uint4*>(w + lane * 8 + k * 256);
+      const std::uint32_t vw[4] = {v[k].x, v[k].y, v[k].z, v[k].w};
+      const std::uint32_t gw[4] = {g.x, g.y, g.z, g.w};
+      std::uint32_t o[4];
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        const float2 f = unpack_bf16x2(vw[t]);
+        const float2 gg = unpack_bf16x2(gw[t]);
+        o[t] = pack_bf16x2(bf2f(f2bf(f.x * inv)) * gg.x, bf2f(f2bf(f.y * inv)) * gg.y);
+      }
+      *reinterpret_cast<uint4*>(yr + lane * 8 + k * 256) = make_uint4(o[0], o[1], o[2], o[3]);
+    }
+  }
+}
+
 __global__ void rmsnorm_kernel(const bf16* __restrict__ x, int ldx, const bf16* __restrict__ w,
                                bf16* __restrict__ y, int ldy, int rows, int dim, float eps,
                                const std::int64_t* __restrict__ row_map, bf16* __restrict__ x_copy,
@@ -138,6 +189,84 @@ __global__ void rope_vit_kernel(bf16* qkv, int ld, const std::int32_t* __restric
       v[i] = f2bf(a * c - b * s);
       v[i + half] = f2bf(b * c + a * s);
     }
+  }
+}
+
+// cos / sin of the ViT 2D RoPE per (token, pair), shared by all layers.
+__global__ void vit_rope_table_kernel(const std::int32_t* __restrict__ pos_hw, int rows, int hd,
+                                      float log2_theta, float2* __restrict__ table) {
+  const int half = hd / 2, quarter = hd / 4;
+  const std::int64_t n = static_cast<std::int64_t>(rows) * half;
+  for (std::int64_t e = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; e < n;
+       e += static_cast<std::int64_t>(gridDim.x) * blockDim.x) {
+    const int t = static_cast<int>(e / half), i = static_cast<int>(e % half);
+    const int j = i < quarter ? i : i - quarter;
+    const float freq = exp2f(-log2_theta * (4.0f * j) / static_cast<float>(hd));
+    float s, c;
+    sincosf(static_cast<float>(pos_hw[2 * t + (i < quarter ? 0 : 1)]) * freq, &s, &c);
+    table[e] = make_float2(c, s);
+  }
+}
+
+// q / k RoPE + head padding: one thread per (token, q|k, head, 8 pairs);
+// 16-byte loads of x[i..i+7] and x[i+half..], 16-byte stores.
+__global__ void vit_qk_rope_pad_kernel(const bf16* __restrict__ qkv, int ld,
+                                       const float2* __restrict__ table, int rows, int heads,
+                                       int hd, bf16* __restrict__ qp, bf16* __restrict__ kp) {
+  const int half = hd / 2, chunks = half / 8;
+  const std::int64_t n = static_cast<std::int64_t>(rows) * 2 * heads * chunks;
+  const int ldp = heads * 128;
+  for (std::int64_t e = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; e < n;
+       e += static_cast<std::int64_t>(gridDim.x) * blockDim.x) {
+    const int ch = static_cast<int>(e % chunks);
+    const int h = static_cast<int>((e / chunks) % heads);
+    const int which = static_cast<int>((e / (chunks * heads)) % 2);
+    const int t = static_cast<int>(e / (2 * chunks * heads));
+    const int i0 = ch * 8;
+    const bf16* src = qkv + static_cast<std::int64_t>(t) * ld + (which * heads + h) * hd;
+    const uint4 a = *reinterpret_cast<const uint4*>(src + i0);
+    const uint4 b = *reinterpret_cast<const uint4*>(src + i0 + half);
+    const float2* cs = table + static_cast<std::int64_t>(t) * half + i0;
+    const std::uint32_t aw[4] = {a.x, a.y, a.z, a.w}, bw[4] = {b.x, b.y, b.z, b.w};
+    std::uint32_t lo[4], hi[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const float2 fa = unpack_bf16x2(aw[k]), fb = unpack_bf16x2(bw[k]);
+      const float2 c0 = cs[2 * k], c1 = cs[2 * k + 1];
+      lo[k] = pack_bf16x2(fa.x * c0.x - fb.x * c0.y, fa.y * c1.x - fb.y * c1.y);
+      hi[k] = pack_bf16x2(fb.x * c0.x + fa.x * c0.y, fb.y * c1.x + fa.y * c1.y);
+    }
+    bf16* dst = (which == 0 ? qp : kp) + static_cast<std::int64_t>(t) * ldp + h * 128;
+    *reinterpret_cast<uint4*>(dst + i0) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+    *reinterpret_cast<uint4*>(dst + i0 + half) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
+  }
+}
+
+// V [64 tokens, hd] of one head -> vt[head*128 + d][t0 .. t0+64) via smem.
+__global__ void vit_v_transpose_kernel(const bf16* __restrict__ qkv, int ld, int rows, int heads,
+                                       int hd, bf16* __restrict__ vt, int ld_vt) {
+  __shared__ bf16 tile[128][64 + 8];
+  const int t0 = blockIdx.x * 64, h = blockIdx.y;
+  const int vec = hd / 8;
+  for (int e = threadIdx.x; e < 64 * vec; e += blockDim.x) {
+    const int tt = e / vec, c = (e % vec) * 8;
+    uint4 v = make_uint4(0, 0, 0, 0);
+    if (t0 + tt < rows)
+      v = *reinterpret_cast<const uint4*>(qkv + static_cast<std::int64_t>(t0 + tt) * ld +
+                                          (2 * heads + h) * hd + c);
+    const bf16* pv = reinterpret_cast<const bf16*>(&v);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) tile[c + k][tt] = pv[k];
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < hd * 8; e += blockDim.x) {
+    const int d = e / 8, c = (e % 8) * 8;
+    if (t0 + c + 8 <= rows)
+      *reinterpret_cast<uint4*>(vt + static_cast<std::int64_t>(h * 128 + d) * ld_vt + t0 + c) =
+          *reinterpret_cast<const uint4*>(&tile[d][c]);
+    else
+      for (int k = 0; k < 8 && t0 + c + k < rows; ++k)
+        vt[static_cast<std::int64_t>(h * 128 + d) * ld_vt + t0 + c + k] = tile[d][c + k];
   }
 }
 
@@ -351,8 +480,23 @@ void rmsnorm(const bf16* x, int ldx, const bf16* w, bf16* y, int ldy, int rows, 
   if (rows <= 0) return;
   if (dim % 8 != 0) throw DeviceError(RS_ERR_CUDA, "rmsnorm: dim % 8 != 0");
   const int tok = prof::begin(st);
-  rmsnorm_kernel<<<row_grid(rows), 32 * kWarpsPerBlock, 0, st>>>(x, ldx, w, y, ldy, rows, dim, eps,
-                                                                row_map, x_copy, ld_copy, rows_dev);
+  const int grid = row_grid(rows);
+  const int blk = 32 * kWarpsPerBlock;
+  if (rows_dev == nullptr && dim % 256 == 0 && dim / 256 <= 32) {
+    switch (dim / 256) {
+#define RS_RMS_CASE(V) \
+  case V: rmsnorm_reg_kernel<V><<<grid, blk, 0, st>>>(x, ldx, w, y, ldy, rows, eps, row_map, x_copy, ld_copy); break;
+      RS_RMS_CASE(1) RS_RMS_CASE(2) RS_RMS_CASE(4) RS_RMS_CASE(5) RS_RMS_CASE(14) RS_RMS_CASE(20)
+      RS_RMS_CASE(32)
+#undef RS_RMS_CASE
+      default:
+        rmsnorm_kernel<<<grid, blk, 0, st>>>(x, ldx, w, y, ldy, rows, dim, eps, row_map, x_copy,
+                                             ld_copy, rows_dev);
+    }
+  } else {
+    rmsnorm_kernel<<<grid, blk, 0, st>>>(x, ldx, w, y, ldy, rows, dim, eps, row_map, x_copy, ld_copy,
+                                         rows_dev);
+  }
   RS_LAUNCH_CHECK();
   prof::end(tok, st, row_map != nullptr ? "rmsnorm_gather" : "rmsnorm", 0,
             2.0 * rows * dim * (x_copy != nullptr ? 3.0 : 2.0));
@@ -366,6 +510,29 @@ void rope_vit(bf16* qkv, int ld, const std::int32_t* pos_hw, int rows, int heads
                     st>>>(qkv, ld, pos_hw, rows, heads, hd, std::log2(theta));
   RS_LAUNCH_CHECK();
   count_launch();
+}
+
+void vit_rope_table(const std::int32_t* pos_hw, int rows, int hd, float theta, float2* table,
+                    cudaStream_t st) {
+  if (rows <= 0) return;
+  vit_rope_table_kernel<<<elem_grid(static_cast<std::int64_t>(rows) * hd / 2), 256, 0, st>>>(
+      pos_hw, rows, hd, std::log2(theta), table);
+  RS_LAUNCH_CHECK();
+  count_launch();
+}
+
+void vit_qkv_split(const bf16* qkv, int ld, const float2* rope_table, int rows, int heads, int hd,
+                   bf16* qp, bf16* kp, bf16* vt, int ld_vt, cudaStream_t st) {
+  if (rows <= 0) return;
+  if (hd > 128 || hd % 16 != 0) throw DeviceError(RS_ERR_CUDA, "vit_qkv_split: head_dim must be a multiple of 16, <= 128");
+  const int tok = prof::begin(st);
+  const std::int64_t items = static_cast<std::int64_t>(rows) * 2 * heads * (hd / 16);
+  vit_qk_rope_pad_kernel<<<elem_grid(items), 256, 0, st>>>(qkv, ld, rope_table, rows, heads, hd, qp, kp);
+  RS_LAUNCH_CHECK();
+  vit_v_transpose_kernel<<<dim3(ceil_div(rows, 64), heads), 256, 0, st>>>(qkv, ld, rows, heads, hd, vt, ld_vt);
+  RS_LAUNCH_CHECK();
+  prof::end(tok, st, "vit_qkv_split", 0, 2.0 * rows * heads * hd * 3 * 2);
+  count_launch(2);
 }
 
 void rope_kv_append(bf16* qkv, int ld, const ChunkRowInfo* rows_info, int rows, int q_heads,

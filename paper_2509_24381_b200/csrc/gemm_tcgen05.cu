@@ -28,20 +28,153 @@ struct GemmParams {
   const int* M_dev;
 };
 
-template <int BN>
+template <int BN, bool TMA_OUT = false>
 struct Cfg {
-  static constexpr int kStages = BN >= 256 ? 4 : 6;
+  static_assert(BN % 32 == 0 && BN >= 128 && BN <= 256, "tile width");
   static constexpr int kABytes = kBM * kBK * 2;
   static constexpr int kBBytes = BN * kBK * 2;
   static constexpr int kStageBytes = kABytes + kBBytes;
-  static constexpr int kTmemCols = 2 * BN;  // double-buffered accumulator
-  static constexpr int kSmem = kStages * kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
+  // epilogue staging: 4 warps x 2 buffers x [32 rows x 128 B] (TMA stores)
+  static constexpr int kEpiBuf = 4096;
+  static constexpr int kEpiBytes = TMA_OUT ? 4 * 2 * kEpiBuf : 0;
+  // as many pipeline stages as the 227 KB of shared memory allow (<= 8)
+  static constexpr int kStagesFit = (227 * 1024 - 1024 - 512 - kEpiBytes) / kStageBytes;
+  static constexpr int kStages = kStagesFit > 8 ? 8 : kStagesFit;
+  // double-buffered accumulator, allocation rounded up to a power of two
+  static constexpr int kTmemCols = 2 * BN <= 256 ? 256 : 512;
+  static constexpr int kSmem = kStages * kStageBytes + kEpiBytes + 1024 /*align*/ + 512 /*barriers*/;
 };
 
 __device__ __forceinline__ float gelu_erf(float x) {
   return 0.5f * x * (1.f + erff(x * 0.70710678118654752f));
 }
 __device__ __forceinline__ float silu(float x) { return x / (1.f + __expf(-x)); }
+__device__ __forceinline__ float bias_add(float x, const bf16* bias, int col) {
+  return bias != nullptr ? x + __bfloat162float(bias[col]) : x;
+}
+__device__ __forceinline__ float silu_plus(float x, const bf16* bias, int col) {
+  return silu(bias_add(x, bias, col));
+}
+
+// Epilogue of one accumulator tile through shared memory and TMA stores:
+// per warp (32 rows) and per 32-column output chunk, the accumulator is
+// read from TMEM, the fused op applied, the bf16 / fp32 row written to a
+// SW128-swizzled [32 x 32] smem box (conflict-free: 4 wavefronts per 512 B)
+// and stored by one TMA (coalesced, asynchronous). Residual tiles are
+// TMA-loaded one chunk ahead into the alternate buffer.
+template <int BN, int EPI>
+__device__ __forceinline__ void epilogue_tile_tma(const GemmParams& p, const CUtensorMap* tmC,
+                                                  const CUtensorMap* tmR, std::uint8_t* epi,
+                                                  std::uint64_t* rbar, std::uint32_t& rphase,
+                                                  std::uint32_t& ec, std::uint32_t t_row, int m0,
+                                                  int n0, int quad, int lane) {
+  constexpr bool kRes = EPI == static_cast<int>(Epi::Residual);
+  constexpr bool kSwi = EPI == static_cast<int>(Epi::SwiGLU);
+  constexpr bool kF32 = EPI == static_cast<int>(Epi::StoreF32);
+  constexpr int kAccPerChunk = kSwi ? 64 : 32;  // accumulator columns per output chunk
+  constexpr int kChunks = BN / kAccPerChunk;
+  constexpr int kRowBytes = kF32 ? 128 : 64;    // 32 output columns
+  const int row0 = m0 + quad * 32;
+  const int out_col0 = kSwi ? n0 / 2 : n0;
+  std::uint8_t* bufs = epi + quad * 2 * 4096;
+  auto issue_res = [&](int chunk, std::uint32_t b) {
+    sm100::mbar_expect_tx(&rbar[b], 32 * 64);
+    sm100::tma_load_2d(bufs + b * 4096, tmR, &rbar[b], n0 + chunk * 32, row0);
+  };
+  if constexpr (kRes) {
+    if (lane == 0) {
+      sm100::bulk_wait_read<0>();
+      issue_res(0, ec & 1);
+    }
+  }
+#pragma unroll 1
+  for (int c = 0; c < kChunks; ++c, ++ec) {
+    const std::uint32_t b = ec & 1;
+    std::uint8_t* buf = bufs + b * 4096;
+    if (lane == 0) {
+      if constexpr (kRes) {
+        sm100::bulk_wait_read<0>();  // buffer b^1 (chunk c-1's store) drained
+        if (c + 1 < kChunks) issue_res(c + 1, b ^ 1);
+      } else {
+        sm100::bulk_wait_read<1>();  // buffer b (chunk c-2's store) drained
+      }
+    }
+    __syncwarp();
+    float x[32];
+    {
+      std::uint32_t v[32];
+      sm100::tmem_ld_32x32b_x32(t_row + static_cast<std::uint32_t>(c * kAccPerChunk), v);
+      if constexpr (kSwi) {
+        std::uint32_t u[32];
+        sm100::tmem_ld_32x32b_x32(t_row + static_cast<std::uint32_t>(c * kAccPerChunk + 32), u);
+        sm100::tmem_ld_wait();
+        // [g0..15 u0..15 | g16..31 u16..31] -> 32 outputs
+#pragma unroll
+        for (int t = 0; t < 16; ++t) {
+          x[t] = silu_plus(__uint_as_float(v[t]), p.bias, n0 + c * 64 + t) *
+                 bias_add(__uint_as_float(v[16 + t]), p.bias, n0 + c * 64 + 16 + t);
+          x[16 + t] = silu_plus(__uint_as_float(u[t]), p.bias, n0 + c * 64 + 32 + t) *
+                      bias_add(__uint_as_float(u[16 + t]), p.bias, n0 + c * 64 + 48 + t);
+        }
+      } else {
+        sm100::tmem_ld_wait();
+        const int col = n0 + c * 32;
+        if (p.bias != nullptr && col < p.N) {
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const uint4 bb = *reinterpret_cast<const uint4*>(p.bias + col + q * 8);
+            const std::uint32_t bw[4] = {bb.x, bb.y, bb.z, bb.w};
+#pragma unroll
+            for (int t = 0; t < 4; ++t) {
+              const float2 f = unpack_bf16x2(bw[t]);
+              v[q * 8 + 2 * t] = __float_as_uint(__uint_as_float(v[q * 8 + 2 * t]) + f.x);
+              v[q * 8 + 2 * t + 1] = __float_as_uint(__uint_as_float(v[q * 8 + 2 * t + 1]) + f.y);
+            }
+          }
+        }
+#pragma unroll
+        for (int t = 0; t < 32; ++t) x[t] = __uint_as_float(v[t]);
+        if constexpr (EPI == static_cast<int>(Epi::Gelu)) {
+#pragma unroll
+          for (int t = 0; t < 32; ++t) x[t] = gelu_erf(x[t]);
+        }
+      }
+    }
+    if constexpr (kRes) {
+      sm100::mbar_wait(&rbar[b], (rphase >> b) & 1);
+      rphase ^= 1u << b;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const uint4 rv = *reinterpret_cast<const uint4*>(buf + sm100::sw128(lane * 64 + q * 16));
+        const std::uint32_t rw[4] = {rv.x, rv.y, rv.z, rv.w};
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          const float2 f = unpack_bf16x2(rw[t]);
+          x[q * 8 + 2 * t] += f.x;
+          x[q * 8 + 2 * t + 1] += f.y;
+        }
+      }
+    }
+    if constexpr (kF32) {
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+        *reinterpret_cast<float4*>(buf + sm100::sw128(lane * kRowBytes + q * 16)) =
+            make_float4(x[4 * q], x[4 * q + 1], x[4 * q + 2], x[4 * q + 3]);
+    } else {
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        *reinterpret_cast<uint4*>(buf + sm100::sw128(lane * kRowBytes + q * 16)) =
+            make_uint4(pack_bf16x2(x[8 * q], x[8 * q + 1]), pack_bf16x2(x[8 * q + 2], x[8 * q + 3]),
+                       pack_bf16x2(x[8 * q + 4], x[8 * q + 5]), pack_bf16x2(x[8 * q + 6], x[8 * q + 7]));
+    }
+    sm100::fence_proxy_async_smem();
+    __syncwarp();
+    if (lane == 0) {
+      sm100::tma_store_2d(tmC, buf, out_col0 + c * 32, row0);
+      sm100::bulk_commit();
+    }
+  }
+}
 
 template <int EPI>
 __device__ __forceinline__ void epilogue_chunk(const GemmParams& p, int row, int col,
@@ -115,22 +248,26 @@ __device__ __forceinline__ void epilogue_chunk(const GemmParams& p, int row, int
   }
 }
 
-template <int BN, int EPI>
+template <int BN, int EPI, bool TMA_OUT>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmA,
-                        const __grid_constant__ CUtensorMap tmB, const GemmParams p) {
-  using C = Cfg<BN>;
+                        const __grid_constant__ CUtensorMap tmB,
+                        const __grid_constant__ CUtensorMap tmC,
+                        const __grid_constant__ CUtensorMap tmR, const GemmParams p) {
+  using C = Cfg<BN, TMA_OUT>;
   extern __shared__ __align__(1024) std::uint8_t smem_raw[];
   std::uint8_t* smem = reinterpret_cast<std::uint8_t*>(
       (reinterpret_cast<std::uintptr_t>(smem_raw) + 1023) & ~std::uintptr_t(1023));
   std::uint8_t* smem_a = smem;
   std::uint8_t* smem_b = smem + C::kStages * C::kABytes;
-  std::uint64_t* bars = reinterpret_cast<std::uint64_t*>(smem + C::kStages * C::kStageBytes);
+  std::uint8_t* smem_epi = smem + C::kStages * C::kStageBytes;  // 1024-aligned
+  std::uint64_t* bars = reinterpret_cast<std::uint64_t*>(smem_epi + C::kEpiBytes);
   std::uint64_t* full = bars;
   std::uint64_t* empty = bars + C::kStages;
   std::uint64_t* tfull = bars + 2 * C::kStages;
   std::uint64_t* tempty = tfull + 2;
-  std::uint32_t* tmem_holder = reinterpret_cast<std::uint32_t*>(tempty + 2);
+  std::uint64_t* rbar = tempty + 2;  // [4 warps][2] residual-load barriers
+  std::uint32_t* tmem_holder = reinterpret_cast<std::uint32_t*>(rbar + 8);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -150,6 +287,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int a = 0; a < 2; ++a) {
       sm100::mbar_init(&tfull[a], 1);
       sm100::mbar_init(&tempty[a], 4);
+    }
+    for (int r = 0; r < 8; ++r) sm100::mbar_init(&rbar[r], 1);
+    if constexpr (TMA_OUT) {
+      sm100::tma_prefetch_desc(&tmC);
+      if (EPI == static_cast<int>(Epi::Residual)) sm100::tma_prefetch_desc(&tmR);
     }
     sm100::fence_mbar_init();
   }
@@ -214,26 +356,38 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ---------------- epilogue warps ----------------
     const int quad = warp - 4;  // TMEM lanes [32*quad, 32*quad + 32)
     int local = 0;
+    std::uint32_t ec = 0, rphase = 0;  // TMA-epilogue chunk counter / residual phases
     for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++local) {
       const int m0 = (tile % m_tiles) * kBM;
       const int n0 = (tile / m_tiles) * BN;
       const int acc = local & 1;
       const std::uint32_t acc_phase = (local >> 1) & 1;
-      sm100::mbar_wait(&tfull[acc], acc_phase);
-      sm100::tc_fence_after();
-      const int row = m0 + quad * 32 + lane;
       const std::uint32_t t_row =
           tmem_base + (static_cast<std::uint32_t>(quad * 32) << 16) + static_cast<std::uint32_t>(acc * BN);
+      if constexpr (TMA_OUT) {
+        sm100::mbar_wait(&tfull[acc], acc_phase);
+        sm100::tc_fence_after();
+        epilogue_tile_tma<BN, EPI>(p, &tmC, &tmR, smem_epi, rbar + 2 * quad, rphase, ec, t_row,
+                                   m0, n0, quad, lane);
+      } else {
+        sm100::mbar_wait(&tfull[acc], acc_phase);
+        sm100::tc_fence_after();
+        const int row = m0 + quad * 32 + lane;
 #pragma unroll 1
-      for (int c = 0; c < BN; c += 32) {
-        std::uint32_t v[32];
-        sm100::tmem_ld_32x32b_x32(t_row + static_cast<std::uint32_t>(c), v);
-        sm100::tmem_ld_wait();
-        if (row < M && n0 + c < p.N) epilogue_chunk<EPI>(p, row, n0 + c, v);
+        for (int c = 0; c < BN; c += 32) {
+          std::uint32_t v[32];
+          sm100::tmem_ld_32x32b_x32(t_row + static_cast<std::uint32_t>(c), v);
+          sm100::tmem_ld_wait();
+          if (row < M && n0 + c < p.N) epilogue_chunk<EPI>(p, row, n0 + c, v);
+        }
       }
       sm100::tc_fence_before();
       __syncwarp();
       if (lane == 0) sm100::mbar_arrive(&tempty[acc]);
+    }
+    if constexpr (TMA_OUT) {
+      if (lane == 0) sm100::bulk_wait<0>();  // stores complete before smem is released
+      __syncwarp();
     }
   }
   __syncthreads();
@@ -261,27 +415,30 @@ EncodeTiledFn encode_fn() {
   return fn;
 }
 
-// K-major bf16 matrix [rows, k] (row stride ld elements), box [box_rows, 64].
-CUtensorMap make_kmajor_map(const void* base, int rows, int k, int ld, int box_rows) {
+// 2D row-major matrix [rows, cols] (row stride ld elements), SW128 tiles of
+// [box_rows, box_cols]; cached per (pointer, shape, box).
+CUtensorMap make_map(const void* base, bool f32, int rows, int cols, int ld, int box_cols,
+                     int box_rows) {
   struct Key {
     const void* base;
-    int rows, k, ld, box;
+    int rows, cols, ld, bc, br;
+    bool f32;
     bool operator==(const Key& o) const {
-      return base == o.base && rows == o.rows && k == o.k && ld == o.ld && box == o.box;
+      return base == o.base && rows == o.rows && cols == o.cols && ld == o.ld && bc == o.bc &&
+             br == o.br && f32 == o.f32;
     }
   };
   struct KeyHash {
     std::size_t operator()(const Key& x) const {
       std::size_t h = reinterpret_cast<std::uintptr_t>(x.base);
-      h = h * 1000003u ^ static_cast<std::size_t>(x.rows);
-      h = h * 1000003u ^ static_cast<std::size_t>(x.k);
-      h = h * 1000003u ^ static_cast<std::size_t>(x.ld);
-      return h * 1000003u ^ static_cast<std::size_t>(x.box);
+      for (int v : {x.rows, x.cols, x.ld, x.bc, x.br, static_cast<int>(x.f32)})
+        h = h * 1000003u ^ static_cast<std::size_t>(v);
+      return h;
     }
   };
   static std::mutex mu;
   static std::unordered_map<Key, CUtensorMap, KeyHash> cache;
-  const Key key{base, rows, k, ld, box_rows};
+  const Key key{base, rows, cols, ld, box_cols, box_rows, f32};
   {
     std::lock_guard<std::mutex> g(mu);
     const auto it = cache.find(key);
@@ -289,59 +446,88 @@ CUtensorMap make_kmajor_map(const void* base, int rows, int k, int ld, int box_r
   }
   CUtensorMap tm;
   std::memset(&tm, 0, sizeof tm);
-  const cuuint64_t dims[2] = {static_cast<cuuint64_t>(k), static_cast<cuuint64_t>(rows)};
-  const cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld) * 2};
-  const cuuint32_t box[2] = {static_cast<cuuint32_t>(kBK), static_cast<cuuint32_t>(box_rows)};
+  const int esize = f32 ? 4 : 2;
+  const cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
+  const cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld) * esize};
+  const cuuint32_t box[2] = {static_cast<cuuint32_t>(box_cols), static_cast<cuuint32_t>(box_rows)};
   const cuuint32_t estr[2] = {1, 1};
-  const CUresult r = encode_fn()(&tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base),
-                                 dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                                 CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  const CUresult r = encode_fn()(
+      &tm, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+      const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+      CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS)
     throw DeviceError(RS_ERR_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string(r) +
-                                       ") rows=" + std::to_string(rows) + " k=" + std::to_string(k) +
-                                       " ld=" + std::to_string(ld));
+                                       ") rows=" + std::to_string(rows) + " cols=" +
+                                       std::to_string(cols) + " ld=" + std::to_string(ld));
   std::lock_guard<std::mutex> g(mu);
   if (cache.size() > 4096) cache.clear();
   cache.emplace(key, tm);
   return tm;
 }
 
-template <int BN, int EPI>
+template <int BN, int EPI, bool TMA_OUT>
 void launch(const GemmArgs& a, cudaStream_t stream) {
-  using C = Cfg<BN>;
+  using C = Cfg<BN, TMA_OUT>;
   static bool attr_set = false;
   if (!attr_set) {
-    RS_CUDA_CHECK(cudaFuncSetAttribute(gemm_tcgen05_kernel<BN, EPI>,
+    RS_CUDA_CHECK(cudaFuncSetAttribute(gemm_tcgen05_kernel<BN, EPI, TMA_OUT>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem));
     attr_set = true;
   }
-  const CUtensorMap tmA = make_kmajor_map(a.A, a.M, a.K, a.lda, kBM);
-  const CUtensorMap tmB = make_kmajor_map(a.B, a.N, a.K, a.ldb, BN);
+  const CUtensorMap tmA = make_map(a.A, false, a.M, a.K, a.lda, kBK, kBM);
+  const CUtensorMap tmB = make_map(a.B, false, a.N, a.K, a.ldb, kBK, BN);
+  CUtensorMap tmC = tmA, tmR = tmA;  // unused placeholders unless TMA_OUT
+  if constexpr (TMA_OUT) {
+    constexpr bool f32 = EPI == static_cast<int>(Epi::StoreF32);
+    const int out_cols = EPI == static_cast<int>(Epi::SwiGLU) ? a.N / 2 : a.N;
+    tmC = make_map(a.C, f32, a.M, out_cols, a.ldc, 32, 32);
+    if constexpr (EPI == static_cast<int>(Epi::Residual))
+      tmR = make_map(a.residual, false, a.M, a.N, a.ldr, 32, 32);
+  }
   GemmParams p{a.C, a.ldc, a.bias, a.residual, a.ldr, a.row_map, a.M, a.N, a.K, a.M_dev};
   const int tiles = ceil_div(a.M, kBM) * ceil_div(a.N, BN);
   const int grid = tiles < kNumSMs ? tiles : kNumSMs;
-  gemm_tcgen05_kernel<BN, EPI><<<grid, kThreads, C::kSmem, stream>>>(tmA, tmB, p);
+  gemm_tcgen05_kernel<BN, EPI, TMA_OUT><<<grid, kThreads, C::kSmem, stream>>>(tmA, tmB, tmC, tmR, p);
   RS_LAUNCH_CHECK();
   count_launch();
 }
 
 template <int BN>
 void dispatch_epi(const GemmArgs& a, Epi epi, cudaStream_t s) {
+  // Row-mapped outputs (scatter) keep the direct-store epilogue; everything
+  // else goes through smem + TMA stores.
+  const bool tma = a.row_map == nullptr && a.M_dev == nullptr;
   switch (epi) {
-    case Epi::Store: return launch<BN, 0>(a, s);
-    case Epi::Residual: return launch<BN, 1>(a, s);
-    case Epi::SwiGLU: return launch<BN, 2>(a, s);
-    case Epi::Gelu: return launch<BN, 3>(a, s);
-    case Epi::StoreF32: return launch<BN, 4>(a, s);
+    case Epi::Store: return tma ? launch<BN, 0, true>(a, s) : launch<BN, 0, false>(a, s);
+    case Epi::Residual: return tma ? launch<BN, 1, true>(a, s) : launch<BN, 1, false>(a, s);
+    case Epi::SwiGLU:
+      if constexpr (BN % 64 == 0)
+        return tma ? launch<BN, 2, true>(a, s) : launch<BN, 2, false>(a, s);
+      else
+        return launch<BN, 2, false>(a, s);
+    case Epi::Gelu: return tma ? launch<BN, 3, true>(a, s) : launch<BN, 3, false>(a, s);
+    case Epi::StoreF32: return tma ? launch<BN, 4, true>(a, s) : launch<BN, 4, false>(a, s);
   }
 }
 
-// Wave efficiency of a tile width: useful tiles / (waves * SMs).
-double wave_eff(int M, int N, int bn) {
-  const int tiles = ceil_div(M, kBM) * ceil_div(N, bn);
-  const int waves = ceil_div(tiles, kNumSMs);
-  return static_cast<double>(tiles) / (static_cast<double>(waves) * kNumSMs);
+// Tile width with the least wave-quantised time: a wave of the persistent
+// kernel costs ~BN (per-tile work at fixed BM and K), so minimise
+// waves * BN; ties go to the wider tile (fewer A re-reads).
+int pick_bn(int M, int N, bool swiglu) {
+  static constexpr int kCandidates[] = {256, 224, 192, 160, 128};
+  int best = 256;
+  long best_cost = -1;
+  for (int bn : kCandidates) {
+    if (swiglu && bn % 64 != 0) continue;  // 64-column gate/up chunks (TMA epilogue)
+    const long tiles = static_cast<long>(ceil_div(M, kBM)) * ceil_div(N, bn);
+    const long waves = (tiles + kNumSMs - 1) / kNumSMs;
+    const long cost = waves * bn;
+    if (best_cost < 0 || cost < best_cost) {
+      best = bn;
+      best_cost = cost;
+    }
+  }
+  return best;
 }
 
 }  // namespace
@@ -353,17 +539,16 @@ void gemm(const GemmArgs& a, Epi epi, cudaStream_t stream, int force_bn) {
                                        std::to_string(a.K) + ", N=" + std::to_string(a.N) + ")");
   if (epi == Epi::SwiGLU && a.N % 32 != 0)
     throw DeviceError(RS_ERR_CUDA, "gemm: SwiGLU needs N%32==0");
-  int bn = force_bn;
-  if (bn == 0) {
-    // Prefer the wide tile (half the A re-reads) unless the narrow one
-    // fills the 148 SMs clearly better.
-    bn = wave_eff(a.M, a.N, 128) > wave_eff(a.M, a.N, 256) + 0.15 ? 128 : 256;
-  }
+  const int bn = force_bn != 0 ? force_bn : pick_bn(a.M, a.N, epi == Epi::SwiGLU);
   const int tok = prof::begin(stream);
-  if (bn == 256)
-    dispatch_epi<256>(a, epi, stream);
-  else
-    dispatch_epi<128>(a, epi, stream);
+  switch (bn) {
+    case 256: dispatch_epi<256>(a, epi, stream); break;
+    case 224: dispatch_epi<224>(a, epi, stream); break;
+    case 192: dispatch_epi<192>(a, epi, stream); break;
+    case 160: dispatch_epi<160>(a, epi, stream); break;
+    case 128: dispatch_epi<128>(a, epi, stream); break;
+    default: throw DeviceError(RS_ERR_CUDA, "gemm: unsupported tile width " + std::to_string(bn));
+  }
   const double m = a.M, n = a.N, k = a.K;
   const double out_bytes = epi == Epi::StoreF32 ? 4.0 : (epi == Epi::SwiGLU ? 1.0 : 2.0);
   prof::end(tok, stream, "gemm_tcgen05", 2.0 * m * n * k,

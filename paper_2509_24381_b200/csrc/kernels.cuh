@@ -53,6 +53,16 @@ void rmsnorm(const bf16* x, int ldx, const bf16* w, bf16* y, int ldy, int rows, 
 void rope_vit(bf16* qkv, int ld, const std::int32_t* pos_hw, int rows, int heads, int hd,
               float theta, cudaStream_t st);
 
+/// ViT attention operands: 2D RoPE on q, k of packed QKV rows [P, 3*H*hd]
+/// (as rope_vit) written head-padded to 128 columns into qp / kp
+/// [P, H*128], and V transposed into vt [H*128, ld_vt] (row h*128+d, column
+/// = token). Pad columns / rows are never written (zero-initialised once).
+void vit_qkv_split(const bf16* qkv, int ld, const float2* rope_table, int rows, int heads, int hd,
+                   bf16* qp, bf16* kp, bf16* vt, int ld_vt, cudaStream_t st);
+/// cos / sin table [rows, hd/2] of the ViT 2D RoPE (shared by all layers).
+void vit_rope_table(const std::int32_t* pos_hw, int rows, int hd, float theta, float2* table,
+                    cudaStream_t st);
+
 struct ChunkRowInfo {  // one chunk row (prefill token)
   std::int32_t req_slot;  // per-request tables index
   std::int32_t pos;       // prompt position (KV index)

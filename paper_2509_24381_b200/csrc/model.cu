@@ -148,11 +148,42 @@ void Vit::init(const Shapes& s, DeviceArena& a, int max_patches, cudaStream_t st
   att_ = alloc_bf16(a, P * s.vd);
   h_ = alloc_bf16(a, P * s.vff_pad);
   mh_ = alloc_bf16(a, (P / 4 + 1) * s.merge_in);
+  // tcgen05 attention operands, head-padded to 128 (pad never written: zero)
+  const std::int64_t padded = P * s.vh * 128;
+  qp_ = alloc_bf16(a, padded);
+  kp_ = alloc_bf16(a, padded);
+  vt_ = alloc_bf16(a, padded);
+  RS_CUDA_CHECK(cudaMemsetAsync(qp_, 0, padded * 2, st));
+  RS_CUDA_CHECK(cudaMemsetAsync(kp_, 0, padded * 2, st));
+  RS_CUDA_CHECK(cudaMemsetAsync(vt_, 0, padded * 2, st));
+  rope_table_ = static_cast<float2*>(a.alloc(static_cast<std::size_t>(P) * (s.vhd / 2) * sizeof(float2)));
+}
+
+void finalize_plan(VitBatchPlan& plan) {
+  plan.full_blocks.clear();
+  plan.win_blocks.clear();
+  for (std::size_t i = 0; i + 1 < plan.cu_item.size(); ++i) {
+    const int a = plan.cu_item[i], b = plan.cu_item[i + 1];
+    for (int r = a; r < b; r += kPrefillRows)
+      plan.full_blocks.push_back({r, std::min(kPrefillRows, b - r), a, b});
+  }
+  // window layers: 128-row blocks over the packed tokens; keys = union of the
+  // windows the block's rows belong to.
+  const std::vector<std::int32_t>& cu = plan.cu_window;
+  std::size_t s = 0;
+  for (int r = 0; r < plan.patches; r += kPrefillRows) {
+    const int r1 = std::min(plan.patches, r + kPrefillRows);
+    while (s + 1 < cu.size() && cu[s + 1] <= r) ++s;
+    std::size_t e = s;
+    while (e + 1 < cu.size() && cu[e + 1] < r1) ++e;
+    plan.win_blocks.push_back({r, r1 - r, cu[s], cu[e + 1]});
+  }
 }
 
 void Vit::encode(const VitBatchPlan& plan, const bf16* patches, const std::int32_t* pos_hw,
                  const std::int32_t* cu_window, const std::int32_t* cu_item,
-                 const std::int32_t* out_row, bf16* out, cudaStream_t st) {
+                 const std::int32_t* out_row, const AttnBlock* win_blocks,
+                 const AttnBlock* full_blocks, bf16* out, cudaStream_t st) {
   const int P = plan.patches;
   if (P > max_p_)
     throw DeviceError(RS_ERR_CUDA, "vit: batch of " + std::to_string(P) +
@@ -167,6 +198,7 @@ void Vit::encode(const VitBatchPlan& plan, const bf16* patches, const std::int32
   gemm(g, Epi::Store, st);
   const int n_win = static_cast<int>(plan.cu_window.size()) - 1;
   const int n_items = static_cast<int>(plan.cu_item.size()) - 1;
+  vit_rope_table(pos_hw, P, s.vhd, s.cfg.rope_theta_vit, rope_table_, st);
   for (int l = 0; l < s.vl; ++l) {
     const VitLayer& L = layers_[static_cast<std::size_t>(l)];
     rmsnorm(x_, s.vd, L.ln1, xn_, s.vd, P, s.vd, s.eps, st);
@@ -174,13 +206,13 @@ void Vit::encode(const VitBatchPlan& plan, const bf16* patches, const std::int32
     g.A = xn_; g.lda = s.vd; g.B = L.qkv_w; g.ldb = s.vd; g.C = qkv_; g.ldc = 3 * s.vd;
     g.bias = L.qkv_b; g.M = P; g.N = 3 * s.vd; g.K = s.vd;
     gemm(g, Epi::Store, st);
-    rope_vit(qkv_, 3 * s.vd, pos_hw, P, s.vh, s.vhd, s.cfg.rope_theta_vit, st);
+    vit_qkv_split(qkv_, 3 * s.vd, rope_table_, P, s.vh, s.vhd, qp_, kp_, vt_, max_p_, st);
     if (s.full_attention_layer(l))
-      attention_varlen_bidir(qkv_, 3 * s.vd, att_, s.vd, cu_item, n_items, plan.max_item, P, s.vh,
-                             s.vhd, scale, st);
+      attention_varlen_tc(qp_, kp_, vt_, max_p_, s.vh, att_, s.vd, s.vhd, full_blocks,
+                          static_cast<int>(plan.full_blocks.size()), cu_item, n_items, scale, st);
     else
-      attention_varlen_bidir(qkv_, 3 * s.vd, att_, s.vd, cu_window, n_win, plan.max_window, P,
-                             s.vh, s.vhd, scale, st);
+      attention_varlen_tc(qp_, kp_, vt_, max_p_, s.vh, att_, s.vd, s.vhd, win_blocks,
+                          static_cast<int>(plan.win_blocks.size()), cu_window, n_win, scale, st);
     g = GemmArgs{};
     g.A = att_; g.lda = s.vd; g.B = L.o_w; g.ldb = s.vd; g.C = x_; g.ldc = s.vd; g.bias = L.o_b;
     g.residual = x_; g.ldr = s.vd; g.M = P; g.N = s.vd; g.K = s.vd;

@@ -81,7 +81,11 @@ struct VitBatchPlan {  // host-side metadata of one encode batch
   std::vector<std::int32_t> cu_item;    // image sequences
   std::vector<std::int32_t> out_row;    // merged row (window-major) -> output row (LLM order)
   int max_window = 0, max_item = 0;
+  std::vector<AttnBlock> win_blocks, full_blocks;  // tcgen05 attention work (finalize_plan)
 };
+
+/// 128-row attention blocks for the window and full-attention layers.
+void finalize_plan(VitBatchPlan& plan);
 
 /// Merged-token grid of an item of `tokens` LLM tokens: (gh, gw), gh <= gw.
 void item_grid(std::uint64_t tokens, int* gh, int* gw);
@@ -95,7 +99,8 @@ class Vit {
   /// meta_dev: uploaded VitBatchPlan arrays (see encode_meta_bytes()).
   void encode(const VitBatchPlan& plan, const bf16* patches, const std::int32_t* pos_hw_dev,
               const std::int32_t* cu_window_dev, const std::int32_t* cu_item_dev,
-              const std::int32_t* out_row_dev, bf16* out, cudaStream_t st);
+              const std::int32_t* out_row_dev, const AttnBlock* win_blocks_dev,
+              const AttnBlock* full_blocks_dev, bf16* out, cudaStream_t st);
   std::uint64_t flops_per_batch(const VitBatchPlan& plan) const;
   int max_patches() const { return max_p_; }
 
@@ -109,6 +114,8 @@ class Vit {
   // activations
   bf16 *x_ = nullptr, *xn_ = nullptr, *qkv_ = nullptr, *att_ = nullptr, *h_ = nullptr,
        *mh_ = nullptr;
+  bf16 *qp_ = nullptr, *kp_ = nullptr, *vt_ = nullptr;  // head-padded tcgen05 attention operands
+  float2* rope_table_ = nullptr;                         // [P, hd/2] cos/sin, per batch
 };
 
 /// Per-chunk device descriptor (uploaded before a stage runs).

@@ -64,7 +64,21 @@ def attn_case(lens, heads, hd):
                                              1 / math.sqrt(hd), st))
     ms = timeit(run)
     fl = sum(4 * n * n * hd * heads for n in lens)
-    return {"lens": f"{len(lens)}x{max(lens)}", "heads": heads, "hd": hd, "ms": ms, "tflops": fl / ms / 1e9}
+    res = {"lens": f"{len(lens)}x{max(lens)}", "heads": heads, "hd": hd, "ms_mma_sync": ms,
+           "tflops_mma_sync": fl / ms / 1e9}
+    # tcgen05 path, measured with the profiler's per-kernel events (the op wrapper
+    # allocates and synchronises around the kernels).
+    N.check(N.lib.rs_profile_enable(1))
+    for _ in range(5):
+        N.check(N.lib.rs_op_attention_varlen_tc(qkv.data_ptr(), qkv.stride(0), out.data_ptr(),
+                                                out.stride(0), cu.data_ptr(), len(lens), total,
+                                                heads, hd, 1 / math.sqrt(hd), st))
+    N.check(N.lib.rs_profile_enable(0))
+    prof = N.profile_drain()
+    a = prof["attn_vit_tcgen05"]
+    res["ms_tcgen05"] = a["ms"] / a["launches"]
+    res["tflops_tcgen05"] = fl / res["ms_tcgen05"] / 1e9
+    return res
 
 
 def prefill_case(hd, hq, hkv, pos0, rows):
@@ -101,8 +115,8 @@ def main():
         # big square sanity
         (8192, 8192, 8192, 0),
     ]
-    for M, N_, K, epi in shapes:
-        for bn in (128, 256):
+    for M, N_, K, epi in shapes if "--attn" not in sys.argv else []:
+        for bn in (0, 128, 160, 192, 224, 256):
             out["gemm"].append(gemm_case(M, N_, K, epi, bn))
     out["attention"].append(attn_case([64] * 64, 16, 80))
     out["attention"].append(attn_case([4096], 16, 80))

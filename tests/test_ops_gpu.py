@@ -51,7 +51,7 @@ SHAPES = [
 
 
 @pytest.mark.parametrize("M,N,K", SHAPES)
-@pytest.mark.parametrize("bn", [128, 256])
+@pytest.mark.parametrize("bn", [0, 128, 160, 192, 224, 256])
 def test_gemm_store(nat, M, N, K, bn):
     torch.manual_seed(M * 7 + N + K)
     A = torch.randn(M, K, device="cuda", dtype=torch.bfloat16)
@@ -164,17 +164,26 @@ def test_attention_prefill_tcgen05(nat, hd, hq, hkv, pos0, rows):
     _close(out, ref)
 
 
+@pytest.mark.parametrize("tc", [False, True])
 @pytest.mark.parametrize("hd,heads,lens", [(80, 4, [64, 64, 37, 64]), (80, 2, [1024, 300]),
-                                           (64, 4, [256, 256, 5]), (128, 2, [130, 1])])
-def test_attention_varlen_bidir(nat, hd, heads, lens):
+                                           (64, 4, [256, 256, 5]), (128, 2, [130, 1]),
+                                           (80, 16, [64] * 40 + [16, 48])])
+def test_attention_varlen_bidir(nat, hd, heads, lens, tc):
     total = sum(lens)
     qkv = torch.randn(total, 3 * heads * hd, device="cuda", dtype=torch.bfloat16)
     cu = torch.tensor([0] + list(torch.tensor(lens).cumsum(0)), dtype=torch.int32, device="cuda")
     out = torch.empty(total, heads * hd, device="cuda", dtype=torch.bfloat16)
     scale = 1.0 / math.sqrt(hd)
-    nat.check(nat.lib.rs_op_attention_varlen(qkv.data_ptr(), qkv.stride(0), out.data_ptr(),
-                                             out.stride(0), cu.data_ptr(), len(lens), max(lens),
-                                             total, heads, hd, scale, _stream()))
+    if tc:
+        if hd > 128:
+            pytest.skip("tc path pads heads to 128")
+        nat.check(nat.lib.rs_op_attention_varlen_tc(qkv.data_ptr(), qkv.stride(0), out.data_ptr(),
+                                                    out.stride(0), cu.data_ptr(), len(lens), total,
+                                                    heads, hd, scale, _stream()))
+    else:
+        nat.check(nat.lib.rs_op_attention_varlen(qkv.data_ptr(), qkv.stride(0), out.data_ptr(),
+                                                 out.stride(0), cu.data_ptr(), len(lens), max(lens),
+                                                 total, heads, hd, scale, _stream()))
     torch.cuda.synchronize()
     q, k, v = qkv.float().view(total, 3, heads, hd).unbind(1)
     ref = torch.empty(total, heads, hd, device="cuda")
