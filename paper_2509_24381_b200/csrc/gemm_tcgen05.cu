@@ -15,7 +15,8 @@ namespace {
 
 constexpr int kBM = 128;
 constexpr int kBK = 64;  // 64 bf16 = 128 B = one swizzle row
-constexpr int kThreads = 256;
+constexpr int kEpiWarps = 8;  // two per TMEM lane quadrant, splitting the tile's columns
+constexpr int kThreads = 128 + 32 * kEpiWarps;
 
 struct GemmParams {
   void* C;
@@ -34,9 +35,9 @@ struct Cfg {
   static constexpr int kABytes = kBM * kBK * 2;
   static constexpr int kBBytes = BN * kBK * 2;
   static constexpr int kStageBytes = kABytes + kBBytes;
-  // epilogue staging: 4 warps x 2 buffers x [32 rows x 128 B] (TMA stores)
-  static constexpr int kEpiBuf = 4096;
-  static constexpr int kEpiBytes = TMA_OUT ? 4 * 2 * kEpiBuf : 0;
+  // epilogue staging: 8 warps x 2 buffers x [32 rows x 64 B] (bf16 TMA stores)
+  static constexpr int kEpiBuf = 2048;
+  static constexpr int kEpiBytes = TMA_OUT ? kEpiWarps * 2 * kEpiBuf : 0;
   // as many pipeline stages as the 227 KB of shared memory allow (<= 8)
   static constexpr int kStagesFit = (227 * 1024 - 1024 - 512 - kEpiBytes) / kStageBytes;
   static constexpr int kStages = kStagesFit > 8 ? 8 : kStagesFit;
@@ -48,7 +49,9 @@ struct Cfg {
 __device__ __forceinline__ float gelu_erf(float x) {
   return 0.5f * x * (1.f + erff(x * 0.70710678118654752f));
 }
-__device__ __forceinline__ float silu(float x) { return x / (1.f + __expf(-x)); }
+__device__ __forceinline__ float silu(float x) {
+  return __fdividef(x, 1.f + __expf(-x));
+}
 __device__ __forceinline__ float bias_add(float x, const bf16* bias, int col) {
   return bias != nullptr ? x + __bfloat162float(bias[col]) : x;
 }
@@ -64,37 +67,41 @@ __device__ __forceinline__ float silu_plus(float x, const bf16* bias, int col) {
 // TMA-loaded one chunk ahead into the alternate buffer.
 template <int BN, int EPI>
 __device__ __forceinline__ void epilogue_tile_tma(const GemmParams& p, const CUtensorMap* tmC,
-                                                  const CUtensorMap* tmR, std::uint8_t* epi,
+                                                  const CUtensorMap* tmR, std::uint8_t* bufs,
                                                   std::uint64_t* rbar, std::uint32_t& rphase,
                                                   std::uint32_t& ec, std::uint32_t t_row, int m0,
-                                                  int n0, int quad, int lane) {
+                                                  int n0, int quad, int half, int lane) {
   constexpr bool kRes = EPI == static_cast<int>(Epi::Residual);
   constexpr bool kSwi = EPI == static_cast<int>(Epi::SwiGLU);
   constexpr bool kF32 = EPI == static_cast<int>(Epi::StoreF32);
+  static_assert(!kF32, "fp32 outputs use the direct epilogue");
   constexpr int kAccPerChunk = kSwi ? 64 : 32;  // accumulator columns per output chunk
   constexpr int kChunks = BN / kAccPerChunk;
   constexpr int kRowBytes = kF32 ? 128 : 64;    // 32 output columns
+  constexpr int kBuf = 2048;
+  // the two warps of a lane quadrant split the chunks
+  const int c_begin = half == 0 ? 0 : (kChunks + 1) / 2;
+  const int c_end = half == 0 ? (kChunks + 1) / 2 : kChunks;
   const int row0 = m0 + quad * 32;
   const int out_col0 = kSwi ? n0 / 2 : n0;
-  std::uint8_t* bufs = epi + quad * 2 * 4096;
   auto issue_res = [&](int chunk, std::uint32_t b) {
     sm100::mbar_expect_tx(&rbar[b], 32 * 64);
-    sm100::tma_load_2d(bufs + b * 4096, tmR, &rbar[b], n0 + chunk * 32, row0);
+    sm100::tma_load_2d(bufs + b * kBuf, tmR, &rbar[b], n0 + chunk * 32, row0);
   };
   if constexpr (kRes) {
-    if (lane == 0) {
+    if (lane == 0 && c_begin < c_end) {
       sm100::bulk_wait_read<0>();
-      issue_res(0, ec & 1);
+      issue_res(c_begin, ec & 1);
     }
   }
 #pragma unroll 1
-  for (int c = 0; c < kChunks; ++c, ++ec) {
+  for (int c = c_begin; c < c_end; ++c, ++ec) {
     const std::uint32_t b = ec & 1;
-    std::uint8_t* buf = bufs + b * 4096;
+    std::uint8_t* buf = bufs + b * kBuf;
     if (lane == 0) {
       if constexpr (kRes) {
         sm100::bulk_wait_read<0>();  // buffer b^1 (chunk c-1's store) drained
-        if (c + 1 < kChunks) issue_res(c + 1, b ^ 1);
+        if (c + 1 < c_end) issue_res(c + 1, b ^ 1);
       } else {
         sm100::bulk_wait_read<1>();  // buffer b (chunk c-2's store) drained
       }
@@ -145,7 +152,7 @@ __device__ __forceinline__ void epilogue_tile_tma(const GemmParams& p, const CUt
       rphase ^= 1u << b;
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
-        const uint4 rv = *reinterpret_cast<const uint4*>(buf + sm100::sw128(lane * 64 + q * 16));
+        const uint4 rv = *reinterpret_cast<const uint4*>(buf + sm100::sw64(lane * 64 + q * 16));
         const std::uint32_t rw[4] = {rv.x, rv.y, rv.z, rv.w};
 #pragma unroll
         for (int t = 0; t < 4; ++t) {
@@ -163,7 +170,7 @@ __device__ __forceinline__ void epilogue_tile_tma(const GemmParams& p, const CUt
     } else {
 #pragma unroll
       for (int q = 0; q < 4; ++q)
-        *reinterpret_cast<uint4*>(buf + sm100::sw128(lane * kRowBytes + q * 16)) =
+        *reinterpret_cast<uint4*>(buf + sm100::sw64(lane * kRowBytes + q * 16)) =
             make_uint4(pack_bf16x2(x[8 * q], x[8 * q + 1]), pack_bf16x2(x[8 * q + 2], x[8 * q + 3]),
                        pack_bf16x2(x[8 * q + 4], x[8 * q + 5]), pack_bf16x2(x[8 * q + 6], x[8 * q + 7]));
     }
@@ -266,8 +273,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   std::uint64_t* empty = bars + C::kStages;
   std::uint64_t* tfull = bars + 2 * C::kStages;
   std::uint64_t* tempty = tfull + 2;
-  std::uint64_t* rbar = tempty + 2;  // [4 warps][2] residual-load barriers
-  std::uint32_t* tmem_holder = reinterpret_cast<std::uint32_t*>(rbar + 8);
+  std::uint64_t* rbar = tempty + 2;  // [epilogue warps][2] residual-load barriers
+  std::uint32_t* tmem_holder = reinterpret_cast<std::uint32_t*>(rbar + 2 * kEpiWarps);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -286,9 +293,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int a = 0; a < 2; ++a) {
       sm100::mbar_init(&tfull[a], 1);
-      sm100::mbar_init(&tempty[a], 4);
+      sm100::mbar_init(&tempty[a], kEpiWarps);
     }
-    for (int r = 0; r < 8; ++r) sm100::mbar_init(&rbar[r], 1);
+    for (int r = 0; r < 2 * kEpiWarps; ++r) sm100::mbar_init(&rbar[r], 1);
     if constexpr (TMA_OUT) {
       sm100::tma_prefetch_desc(&tmC);
       if (EPI == static_cast<int>(Epi::Residual)) sm100::tma_prefetch_desc(&tmR);
@@ -354,7 +361,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else if (warp >= 4) {
     // ---------------- epilogue warps ----------------
-    const int quad = warp - 4;  // TMEM lanes [32*quad, 32*quad + 32)
+    const int quad = warp & 3;         // TMEM lanes [32*quad, 32*quad + 32) (warp % 4 rule)
+    const int half = (warp - 4) >> 2;  // which half of the tile's columns
     int local = 0;
     std::uint32_t ec = 0, rphase = 0;  // TMA-epilogue chunk counter / residual phases
     for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++local) {
@@ -367,14 +375,17 @@ __global__ void __launch_bounds__(kThreads, 1)
       if constexpr (TMA_OUT) {
         sm100::mbar_wait(&tfull[acc], acc_phase);
         sm100::tc_fence_after();
-        epilogue_tile_tma<BN, EPI>(p, &tmC, &tmR, smem_epi, rbar + 2 * quad, rphase, ec, t_row,
-                                   m0, n0, quad, lane);
+        epilogue_tile_tma<BN, EPI>(p, &tmC, &tmR, smem_epi + (warp - 4) * 2 * C::kEpiBuf,
+                                   rbar + 2 * (warp - 4), rphase, ec, t_row, m0, n0, quad, half,
+                                   lane);
       } else {
         sm100::mbar_wait(&tfull[acc], acc_phase);
         sm100::tc_fence_after();
         const int row = m0 + quad * 32 + lane;
+        constexpr int kCh = BN / 32;
+        const int c0 = half == 0 ? 0 : (kCh + 1) / 2, c1 = half == 0 ? (kCh + 1) / 2 : kCh;
 #pragma unroll 1
-        for (int c = 0; c < BN; c += 32) {
+        for (int c = 32 * c0; c < 32 * c1; c += 32) {
           std::uint32_t v[32];
           sm100::tmem_ld_32x32b_x32(t_row + static_cast<std::uint32_t>(c), v);
           sm100::tmem_ld_wait();
@@ -419,6 +430,8 @@ EncodeTiledFn encode_fn() {
 // [box_rows, box_cols]; cached per (pointer, shape, box).
 CUtensorMap make_map(const void* base, bool f32, int rows, int cols, int ld, int box_cols,
                      int box_rows) {
+  // Swizzle span = box row width: 128 B (SW128) or 64 B (SW64, 32 bf16 columns).
+  const bool sw64 = box_cols * (f32 ? 4 : 2) == 64;
   struct Key {
     const void* base;
     int rows, cols, ld, bc, br;
@@ -454,7 +467,8 @@ CUtensorMap make_map(const void* base, bool f32, int rows, int cols, int ld, int
   const CUresult r = encode_fn()(
       &tm, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
       const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-      CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+      sw64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B,
+      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS)
     throw DeviceError(RS_ERR_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string(r) +
                                        ") rows=" + std::to_string(rows) + " cols=" +
@@ -506,7 +520,7 @@ void dispatch_epi(const GemmArgs& a, Epi epi, cudaStream_t s) {
       else
         return launch<BN, 2, false>(a, s);
     case Epi::Gelu: return tma ? launch<BN, 3, true>(a, s) : launch<BN, 3, false>(a, s);
-    case Epi::StoreF32: return tma ? launch<BN, 4, true>(a, s) : launch<BN, 4, false>(a, s);
+    case Epi::StoreF32: return launch<BN, 4, false>(a, s);  // LM-head logits (row-mapped)
   }
 }
 

@@ -74,9 +74,14 @@ __device__ __forceinline__ void bulk_wait() {
 __device__ __forceinline__ void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
-// Byte offset inside a 1024-aligned TMA tile written with SWIZZLE_128B.
+// Byte offset inside a 1024-aligned TMA tile written with SWIZZLE_128B
+// (rows of 128 B): 16-byte chunk index ^= (offset / 128) % 8.
 __device__ __forceinline__ std::uint32_t sw128(std::uint32_t off) {
   return off ^ (((off >> 7) & 7u) << 4);
+}
+// Same for SWIZZLE_64B (rows of 64 B, 512-aligned tile): chunk ^= (offset / 128) % 4.
+__device__ __forceinline__ std::uint32_t sw64(std::uint32_t off) {
+  return off ^ (((off >> 7) & 3u) << 4);
 }
 
 // ---- tcgen05 / TMEM --------------------------------------------------------
