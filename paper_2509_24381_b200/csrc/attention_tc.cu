@@ -41,11 +41,11 @@ struct TcCfg {
   static constexpr int kKBytes = kHdAtoms * kAtom;     // K [128 keys x HD]
   static constexpr int kVAtom = HD * 128;              // V^T [HD x 64 keys]
   static constexpr int kVBytes = 2 * kVAtom;           // 128 keys
-  static constexpr int kPBytes = 2 * kAtom;            // P [128 q x 128 keys]
-  static constexpr int kStages = 2;
-  static constexpr int kSmem = kQBytes + kStages * (kKBytes + kVBytes) + 2 * kPBytes + 1024 + 512;
-  static constexpr int kKvBytes = kKBytes + kVBytes;   // one iteration
+  static constexpr int kStages = 3;                    // K and V rings (independent)
+  static constexpr int kSmem = kQBytes + kStages * (kKBytes + kVBytes) + 1024 + 512;
 };
+// TMEM columns: S[0] 0, S[1] 128, O 256 (HD), P[0] 384, P[1] 448 (bf16 pairs)
+constexpr std::uint32_t kTmemS = 0, kTmemO = 256, kTmemP = 384;
 
 enum class KvMode { kPaged, kVarlen };
 
@@ -73,28 +73,43 @@ __device__ __forceinline__ float fast_exp2(float x) {
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
+// exp2 on the FMA pipe (x <= ~8): 2^x = 2^n * 2^f, n = floor(x), f in [0,1),
+// 2^f by a degree-3 minimax polynomial (rel. err ~9e-5, below bf16's 4e-3);
+// x < -127 -> 0 (matches ftz ex2 for the masked -inf entries).
+__device__ __forceinline__ float poly_exp2(float x) {
+  x = fmaxf(x, -127.f);
+  const float n = floorf(x);
+  const float f = x - n;
+  float p = fmaf(0.0790209f, f, 0.2249531f);
+  p = fmaf(p, f, 0.6960277f);
+  p = fmaf(p, f, 0.99998863f);
+  const int bits = __float_as_int(p) + (static_cast<int>(n) << 23);
+  return x <= -127.f ? 0.f : __int_as_float(bits);
+}
 
 template <int HD, KvMode MODE>
 __global__ void __launch_bounds__(kTcThreads, 1)
     fa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                  const __grid_constant__ CUtensorMap tmV, const TcParams p) {
   using C = TcCfg<HD>;
+  constexpr int S = C::kStages;
   extern __shared__ __align__(1024) std::uint8_t smem_raw[];
   std::uint8_t* smem = reinterpret_cast<std::uint8_t*>(
       (reinterpret_cast<std::uintptr_t>(smem_raw) + 1023) & ~std::uintptr_t(1023));
   std::uint8_t* sQ = smem;
   std::uint8_t* sK = sQ + C::kQBytes;
-  std::uint8_t* sV = sK + C::kStages * C::kKBytes;
-  std::uint8_t* sP = sV + C::kStages * C::kVBytes;
-  std::uint64_t* bars = reinterpret_cast<std::uint64_t*>(sP + 2 * C::kPBytes);
+  std::uint8_t* sV = sK + S * C::kKBytes;
+  std::uint64_t* bars = reinterpret_cast<std::uint64_t*>(sV + S * C::kVBytes);
   std::uint64_t* q_full = bars;
-  std::uint64_t* kv_full = bars + 1;
-  std::uint64_t* kv_empty = bars + 3;
-  std::uint64_t* s_full = bars + 5;
-  std::uint64_t* s_empty = bars + 7;
-  std::uint64_t* p_full = bars + 9;
-  std::uint64_t* o_full = bars + 11;
-  std::uint32_t* tmem_holder = reinterpret_cast<std::uint32_t*>(bars + 16);
+  std::uint64_t* k_full = bars + 1;
+  std::uint64_t* k_empty = k_full + S;
+  std::uint64_t* v_full = k_empty + S;
+  std::uint64_t* v_empty = v_full + S;
+  std::uint64_t* s_full = v_empty + S;   // [2]
+  std::uint64_t* s_empty = s_full + 2;   // [2]
+  std::uint64_t* p_full = s_empty + 2;   // [2]
+  std::uint64_t* o_full = p_full + 2;    // [2]  PV_i completes o_full[i & 1]
+  std::uint32_t* tmem_holder = reinterpret_cast<std::uint32_t*>(o_full + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int head = blockIdx.y;
@@ -125,50 +140,64 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     sm100::tma_prefetch_desc(&tmK);
     sm100::tma_prefetch_desc(&tmV);
     sm100::mbar_init(q_full, 1);
+    for (int i = 0; i < S; ++i) {
+      sm100::mbar_init(&k_full[i], 1);
+      sm100::mbar_init(&k_empty[i], 1);
+      sm100::mbar_init(&v_full[i], 1);
+      sm100::mbar_init(&v_empty[i], 1);
+    }
     for (int i = 0; i < 2; ++i) {
-      sm100::mbar_init(&kv_full[i], 1);
-      sm100::mbar_init(&kv_empty[i], 1);
       sm100::mbar_init(&s_full[i], 1);
       sm100::mbar_init(&s_empty[i], 128);
       sm100::mbar_init(&p_full[i], 128);
+      sm100::mbar_init(&o_full[i], 1);
     }
-    sm100::mbar_init(o_full, 1);
     sm100::fence_mbar_init();
   }
   if (warp == 2) sm100::tmem_alloc(tmem_holder, 512);
   sm100::tc_fence_before();
   __syncthreads();
   sm100::tc_fence_after();
-  const std::uint32_t tmem = *tmem_holder;  // S[0] 0, S[1] 128, O 256
+  const std::uint32_t tmem = *tmem_holder;
 
   if (warp == 0 && lane == 0) {
-    // ---------------- TMA producer ----------------
+    // ---------------- TMA producer: K and V rings run ahead independently ----------------
     sm100::mbar_expect_tx(q_full, C::kQBytes);
     for (int h = 0; h < C::kHdAtoms; ++h)
       sm100::tma_load_2d(sQ + h * kAtom, &tmQ, q_full, head * p.q_head_stride + h * 64, q_row0);
     const int n_pages = (n_keys + 63) / 64;
     for (int j = 0; j < n_it; ++j) {
-      const int st = j & 1;
-      sm100::mbar_wait(&kv_empty[st], ((j >> 1) & 1) ^ 1);
-      sm100::mbar_expect_tx(&kv_full[st], C::kKvBytes);
-      std::uint8_t* k = sK + st * C::kKBytes;
-      std::uint8_t* v = sV + st * C::kVBytes;
+      const int st = j % S;
+      const std::uint32_t par = ((j / S) & 1) ^ 1;
+      int pa = 0, pb = 0;
       if constexpr (MODE == KvMode::kPaged) {
-        const int pa = pt[2 * j];
-        const int pb = 2 * j + 1 < n_pages ? pt[2 * j + 1] : pa;  // duplicate: finite, masked
+        pa = pt[2 * j];
+        pb = 2 * j + 1 < n_pages ? pt[2 * j + 1] : pa;  // duplicate: finite, masked
+      }
+      std::uint8_t* k = sK + st * C::kKBytes;
+      sm100::mbar_wait(&k_empty[st], par);
+      sm100::mbar_expect_tx(&k_full[st], C::kKBytes);
+      if constexpr (MODE == KvMode::kPaged) {
         for (int h = 0; h < C::kHdAtoms; ++h) {
-          sm100::tma_load_2d(k + h * kAtom, &tmK, &kv_full[st], h * 64, (pa * p.kv_heads + kvh) * 64);
-          sm100::tma_load_2d(k + h * kAtom + 64 * 128, &tmK, &kv_full[st], h * 64,
+          sm100::tma_load_2d(k + h * kAtom, &tmK, &k_full[st], h * 64, (pa * p.kv_heads + kvh) * 64);
+          sm100::tma_load_2d(k + h * kAtom + 64 * 128, &tmK, &k_full[st], h * 64,
                              (pb * p.kv_heads + kvh) * 64);
         }
-        sm100::tma_load_2d(v, &tmV, &kv_full[st], 0, (pa * p.kv_heads + kvh) * HD);
-        sm100::tma_load_2d(v + C::kVAtom, &tmV, &kv_full[st], 0, (pb * p.kv_heads + kvh) * HD);
+      } else {
+        for (int h = 0; h < C::kHdAtoms; ++h)
+          sm100::tma_load_2d(k + h * kAtom, &tmK, &k_full[st], kvh * p.q_head_stride + h * 64,
+                             key_begin + 128 * j);
+      }
+      std::uint8_t* v = sV + st * C::kVBytes;
+      sm100::mbar_wait(&v_empty[st], par);
+      sm100::mbar_expect_tx(&v_full[st], C::kVBytes);
+      if constexpr (MODE == KvMode::kPaged) {
+        sm100::tma_load_2d(v, &tmV, &v_full[st], 0, (pa * p.kv_heads + kvh) * HD);
+        sm100::tma_load_2d(v + C::kVAtom, &tmV, &v_full[st], 0, (pb * p.kv_heads + kvh) * HD);
       } else {
         const int k0 = key_begin + 128 * j;
-        for (int h = 0; h < C::kHdAtoms; ++h)
-          sm100::tma_load_2d(k + h * kAtom, &tmK, &kv_full[st], kvh * p.q_head_stride + h * 64, k0);
-        sm100::tma_load_2d(v, &tmV, &kv_full[st], k0, kvh * HD);
-        sm100::tma_load_2d(v + C::kVAtom, &tmV, &kv_full[st], k0 + 64, kvh * HD);
+        sm100::tma_load_2d(v, &tmV, &v_full[st], k0, kvh * HD);
+        sm100::tma_load_2d(v + C::kVAtom, &tmV, &v_full[st], k0 + 64, kvh * HD);
       }
     }
   } else if (warp == 1 && lane == 0) {
@@ -177,37 +206,40 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     constexpr std::uint32_t idesc_o = sm100::idesc_bf16_f32(128, HD);
     sm100::mbar_wait(q_full, 0);
     auto issue_pv = [&](int i) {
-      const int b = i & 1;
+      const int b = i & 1, st = i % S;
+      sm100::mbar_wait(&v_full[st], (i / S) & 1);
       sm100::mbar_wait(&p_full[b], (i >> 1) & 1);
       sm100::tc_fence_after();
-      std::uint8_t* v = sV + b * C::kVBytes;
-      std::uint8_t* pp = sP + b * C::kPBytes;
+      std::uint8_t* v = sV + st * C::kVBytes;
+      // O += P V: P (A operand) from TMEM, 8 columns (16 keys) per MMA
 #pragma unroll
       for (int a = 0; a < 2; ++a) {
-        const std::uint64_t pd = sm100::sw128_kmajor_desc(sm100::smem_u32(pp + a * kAtom));
         const std::uint64_t vd = sm100::sw128_kmajor_desc(sm100::smem_u32(v + a * C::kVAtom));
 #pragma unroll
         for (int kk = 0; kk < 4; ++kk)
-          sm100::umma_bf16(tmem + 256, pd + 2 * kk, vd + 2 * kk, idesc_o, (i | a | kk) != 0 ? 1u : 0u);
+          sm100::umma_bf16_ts(tmem + kTmemO, tmem + kTmemP + 64 * b + 32 * a + 8 * kk, vd + 2 * kk,
+                              idesc_o, (i | a | kk) != 0 ? 1u : 0u);
       }
-      sm100::umma_commit(o_full);  // completion count = PV index + 1
-      sm100::umma_commit(&kv_empty[b]);
+      sm100::umma_commit(&o_full[b]);
+      sm100::umma_commit(&v_empty[st]);
     };
     for (int j = 0; j < n_it; ++j) {
-      const int b = j & 1;
-      sm100::mbar_wait(&kv_full[b], (j >> 1) & 1);
+      const int b = j & 1, st = j % S;
+      sm100::mbar_wait(&k_full[st], (j / S) & 1);
       sm100::mbar_wait(&s_empty[b], ((j >> 1) & 1) ^ 1);
       sm100::tc_fence_after();
-      std::uint8_t* k = sK + b * C::kKBytes;
+      std::uint8_t* k = sK + st * C::kKBytes;
 #pragma unroll
       for (int h = 0; h < C::kHdAtoms; ++h) {
         const std::uint64_t qd = sm100::sw128_kmajor_desc(sm100::smem_u32(sQ + h * kAtom));
         const std::uint64_t kd = sm100::sw128_kmajor_desc(sm100::smem_u32(k + h * kAtom));
 #pragma unroll
         for (int kk = 0; kk < 4; ++kk)
-          sm100::umma_bf16(tmem + 128 * b, qd + 2 * kk, kd + 2 * kk, idesc_s, (h | kk) != 0 ? 1u : 0u);
+          sm100::umma_bf16(tmem + kTmemS + 128 * b, qd + 2 * kk, kd + 2 * kk, idesc_s,
+                           (h | kk) != 0 ? 1u : 0u);
       }
       sm100::umma_commit(&s_full[b]);
+      sm100::umma_commit(&k_empty[st]);  // K stage free as soon as S_j is computed
       if (j >= 1) issue_pv(j - 1);
     }
     issue_pv(n_it - 1);
@@ -216,7 +248,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     const int q = warp - 4;
     const int r = q * 32 + lane;
     const std::uint32_t lane_off = static_cast<std::uint32_t>(q * 32) << 16;
-    const std::uint32_t o_tmem = tmem + lane_off + 256;
+    const std::uint32_t o_tmem = tmem + lane_off + kTmemO;
     // Visible keys of this row: absolute key index in [lo, hi).
     int lo, hi;
     if constexpr (MODE == KvMode::kPaged) {
@@ -245,7 +277,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
         std::uint32_t(&v)[32] = *reinterpret_cast<std::uint32_t(*)[32]>(&sv[32 * c]);
-        sm100::tmem_ld_32x32b_x32(tmem + lane_off + 128 * b + 32 * c, v);
+        sm100::tmem_ld_32x32b_x32(tmem + lane_off + kTmemS + 128 * b + 32 * c, v);
       }
       sm100::tmem_ld_wait();
       sm100::tc_fence_before();
@@ -255,12 +287,18 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         for (int t = 0; t < 128; ++t)
           if (t < c_lo || t >= c_hi) sv[t] = __float_as_uint(-INFINITY);
       }
-      float mx = -INFINITY;
+      // max: 8 independent chains, then a tree
+      float mx8[8];
 #pragma unroll
-      for (int t = 0; t < 128; ++t) mx = fmaxf(mx, __uint_as_float(sv[t]));
+      for (int u = 0; u < 8; ++u) mx8[u] = __uint_as_float(sv[u]);
+#pragma unroll
+      for (int t = 8; t < 128; ++t) mx8[t & 7] = fmaxf(mx8[t & 7], __uint_as_float(sv[t]));
+      float mx = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
+                       fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7])));
       mx *= p.scale_log2;
-      // PV_{j-1} must be complete before O may be rescaled (in order).
-      if (j > 0) sm100::mbar_wait(o_full, (j - 1) & 1);
+      // P buffer b was last read by PV_{j-2} (o_full[b]); PV_{j-4} was awaited
+      // two steps ago, so this parity wait cannot alias.
+      if (j >= 2) sm100::mbar_wait(&o_full[b], ((j - 2) >> 1) & 1);
       const bool raise = mx > m + 8.f || (m == -INFINITY && mx != -INFINITY);
       float alpha = 1.f;
       if (raise) {
@@ -268,6 +306,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         m = mx;
       }
       if (j > 0 && __any_sync(0xffffffffu, raise && alpha != 1.f)) {
+        // rare: O must hold PV_{j-1} before it is rescaled in TMEM
+        sm100::mbar_wait(&o_full[(j - 1) & 1], ((j - 1) >> 1) & 1);
         sm100::tc_fence_after();
 #pragma unroll
         for (int c = 0; c < HD / 32; ++c) {
@@ -281,34 +321,31 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         sm100::tmem_st_wait();
       }
       const float mneg = m == -INFINITY ? 0.f : -m;
-      float rs0 = 0.f, rs1 = 0.f;
-      std::uint8_t* prow = sP + b * C::kPBytes + r * 128;
+      float rs8[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        std::uint32_t packed[16];
+      for (int c = 0; c < 2; ++c) {
+        std::uint32_t packed[32];  // 64 keys as bf16 pairs
 #pragma unroll
-        for (int t = 0; t < 16; ++t) {
-          // exp2(-inf) = 0 for masked entries
-          const float p0 = fast_exp2(fmaf(__uint_as_float(sv[32 * c + 2 * t]), p.scale_log2, mneg));
-          const float p1 = fast_exp2(fmaf(__uint_as_float(sv[32 * c + 2 * t + 1]), p.scale_log2, mneg));
-          rs0 += p0;
-          rs1 += p1;
+        for (int t = 0; t < 32; ++t) {
+          // exp2(-inf) = 0 for masked entries; every 4th pair on the FMA pipe
+          const float x0 = fmaf(__uint_as_float(sv[64 * c + 2 * t]), p.scale_log2, mneg);
+          const float x1 = fmaf(__uint_as_float(sv[64 * c + 2 * t + 1]), p.scale_log2, mneg);
+          const bool poly = (t & 3) == 3;
+          const float p0 = poly ? poly_exp2(x0) : fast_exp2(x0);
+          const float p1 = poly ? poly_exp2(x1) : fast_exp2(x1);
+          rs8[(2 * t) & 7] += p0;
+          rs8[(2 * t + 1) & 7] += p1;
           packed[t] = pack_bf16x2(p0, p1);
         }
-        // 32 keys = 4 16-byte chunks; atom c/2 (64 keys), chunk (c%2)*4 + u, XOR-swizzled
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int chunk = (c & 1) * 4 + u;
-          uint4* dst = reinterpret_cast<uint4*>(prow + (c >> 1) * kAtom + ((chunk ^ (r & 7)) << 4));
-          *dst = make_uint4(packed[4 * u], packed[4 * u + 1], packed[4 * u + 2], packed[4 * u + 3]);
-        }
+        sm100::tmem_st_32x32b_x32(tmem + lane_off + kTmemP + 64 * b + 32 * c, packed);
       }
+      sm100::tmem_st_wait();
       sm100::tc_fence_before();
-      fence_proxy_async_smem();
       sm100::mbar_arrive(&p_full[b]);
-      l = l * alpha + (rs0 + rs1);
+      l = l * alpha + (((rs8[0] + rs8[1]) + (rs8[2] + rs8[3])) + ((rs8[4] + rs8[5]) + (rs8[6] + rs8[7])));
     }
-    sm100::mbar_wait(o_full, (n_it - 1) & 1);
+    // PV complete in issue order: the last one implies all
+    sm100::mbar_wait(&o_full[(n_it - 1) & 1], ((n_it - 1) >> 1) & 1);
     sm100::tc_fence_after();
     const float inv = l > 0.f ? 1.f / l : 0.f;
     bf16* orow = p.out + static_cast<std::int64_t>(q_row0 + r) * p.ld_out + head * p.out_hd;

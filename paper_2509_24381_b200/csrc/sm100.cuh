@@ -114,6 +114,18 @@ __device__ __forceinline__ void umma_bf16(std::uint32_t tmem_d, std::uint64_t ad
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
       : "memory");
 }
+// D[tmem] (+)= A[tmem] * B[smem]^T (A: 128 lanes = rows, 2 bf16 per 32-bit
+// column along K), BF16 inputs, FP32 accumulate.
+__device__ __forceinline__ void umma_bf16_ts(std::uint32_t tmem_d, std::uint32_t tmem_a,
+                                             std::uint64_t bdesc, std::uint32_t idesc,
+                                             std::uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
 // Arrive on `bar` once all previously issued tcgen05.mma of this thread finish.
 __device__ __forceinline__ void umma_commit(std::uint64_t* bar) {
   asm volatile(
