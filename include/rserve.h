@@ -225,6 +225,7 @@ RS_API rs_status rs_synchronize(rs_ctx* ctx);
 typedef struct rs_run_options {
   int32_t clock;        /* 0 lock-step, 1 real clock */
   int32_t e2e;          /* 1: H2D inputs / D2H logits inside the run */
+  int32_t serialize;    /* 1: encoders share the prefill stream (profiling) */
   uint64_t payload_seed;
 } rs_run_options;
 typedef struct rs_run_stats {

@@ -291,8 +291,12 @@ class VisionOracle:
             seqs = item_seqs if c.full_attention(l) else win_seqs
             att = np.empty((P, nh, hd), dtype=np.float32)
             for a, b in seqs:
-                s = np.einsum("qhd,khd->hqk", q[a:b], k[a:b]) / np.float32(math.sqrt(hd))
-                att[a:b] = np.einsum("hqk,khd->qhd", softmax(s), v[a:b])
+                # batched BLAS matmuls over heads: [h, q, d] @ [h, d, k]
+                qh = np.ascontiguousarray(q[a:b].transpose(1, 0, 2))
+                kh = np.ascontiguousarray(k[a:b].transpose(1, 2, 0))
+                vh = np.ascontiguousarray(v[a:b].transpose(1, 0, 2))
+                s = np.matmul(qh, kh) / np.float32(math.sqrt(hd))
+                att[a:b] = np.matmul(softmax(s), vh).transpose(1, 0, 2)
             att = rnd(att.reshape(P, vd))
             x = rnd(x + att @ W.lin(VIT, l, O_W, vd, vd).T + W.vec(VIT, l, O_B, vd))
             xn = rnd(rmsnorm(x, ones, c.rms_eps))
@@ -363,10 +367,12 @@ class LlmOracle:
                 g = hq // hkv
                 kk = np.repeat(kc[:b], g, axis=1)
                 vv = np.repeat(vc[:b], g, axis=1)
-                s = np.einsum("qhd,khd->hqk", q, kk) / np.float32(math.sqrt(hd))
+                qh = np.ascontiguousarray(q.transpose(1, 0, 2))
+                s = np.matmul(qh, np.ascontiguousarray(kk.transpose(1, 2, 0))) / np.float32(math.sqrt(hd))
                 mask = np.arange(b)[None, :] > np.arange(a, b)[:, None]
                 s = np.where(mask[None], -np.inf, s)
-                att = rnd(np.einsum("hqk,khd->qhd", softmax(s), vv).reshape(b - a, hq * hd))
+                att = rnd(np.matmul(softmax(s), np.ascontiguousarray(vv.transpose(1, 0, 2)))
+                          .transpose(1, 0, 2).reshape(b - a, hq * hd))
                 x[a:b] = rnd(x[a:b] + att @ wo.T)
                 xn = rnd(rmsnorm(x[a:b], ones, c.rms_eps))
                 h = rnd(silu(xn @ wg.T) * (xn @ wu.T))

@@ -123,7 +123,8 @@ class rs_ctx_options(C.Structure):
 
 
 class rs_run_options(C.Structure):
-    _fields_ = [("clock", C.c_int32), ("e2e", C.c_int32), ("payload_seed", C.c_uint64)]
+    _fields_ = [("clock", C.c_int32), ("e2e", C.c_int32), ("serialize", C.c_int32),
+                ("payload_seed", C.c_uint64)]
 
 
 class rs_run_stats(C.Structure):

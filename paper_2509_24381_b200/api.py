@@ -309,11 +309,12 @@ class Pipeline:
         N.check(N.lib.rs_synchronize(self.h))
 
     def run(self, workload: str, cfg: SimConfig, clock: str = "lockstep", e2e: bool = False,
-            payload_seed: int = 7):
+            payload_seed: int = 7, serialize: bool = False):
         """Engine run on this device -> (decision log, journal, stats dict)."""
         o = N.rs_run_options()
         o.clock = 1 if clock == "real" else 0
         o.e2e = int(e2e)
+        o.serialize = int(serialize)
         o.payload_seed = payload_seed
         res, jr = _out(), _out()
         st = N.rs_run_stats()

@@ -290,7 +290,8 @@ rs_status rs_engine_run(rs_ctx* c, const char* workload_text, const rs_sim_confi
     sc.hidden_size = static_cast<std::uint32_t>(x.ctx->shapes().d);
     const bool realtime = opt != nullptr && opt->clock == 1;
     const bool e2e = opt != nullptr && opt->e2e != 0;
-    DeviceBackend backend(*x.ctx, sc, realtime, e2e, opt ? opt->payload_seed : 0);
+    DeviceBackend backend(*x.ctx, sc, realtime, e2e, opt ? opt->payload_seed : 0,
+                          opt != nullptr && opt->serialize != 0);
     backend.prepare(wl);
     lmmsim::PipelineEngine engine(wl, sc, backend);
     backend.start();

@@ -15,7 +15,7 @@ std::uint64_t pixel_stream(std::uint64_t req, std::uint64_t item) {
 }  // namespace
 
 DeviceBackend::DeviceBackend(Context& ctx, const lmmsim::SimConfig& cfg, bool realtime, bool e2e,
-                             std::uint64_t payload_seed)
+                             std::uint64_t payload_seed, bool serialize_streams)
     : ctx_(ctx), cfg_(cfg), realtime_(realtime), e2e_(e2e), seed_(payload_seed) {
   if (cfg.stages < 1) throw lmmsim::ConfigError("stages: must be >= 1");
   const int workers = cfg.encoder_workers;
@@ -24,10 +24,10 @@ DeviceBackend::DeviceBackend(Context& ctx, const lmmsim::SimConfig& cfg, bool re
   // scratch; each chunk owns its residual buffer so stages can interleave.
   stage_streams_.resize(1);
   RS_CUDA_CHECK(cudaStreamCreateWithFlags(&stage_streams_[0], cudaStreamNonBlocking));
-  // RS_SERIALIZE=1 (diagnostics): encoders share the prefill stream, so
-  // per-kernel event times are not inflated by cross-stream queueing.
+  // serialize (profiling; or RS_SERIALIZE=1): encoders share the prefill
+  // stream, so per-kernel event times are not inflated by cross-stream queueing.
   const char* ser = std::getenv("RS_SERIALIZE");
-  const bool serialize = ser != nullptr && ser[0] == '1';
+  const bool serialize = serialize_streams || (ser != nullptr && ser[0] == '1');
   enc_streams_.resize(static_cast<std::size_t>(workers));
   for (auto& st : enc_streams_) {
     if (serialize) {

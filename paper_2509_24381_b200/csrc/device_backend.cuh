@@ -37,7 +37,7 @@ struct Payload {
 class DeviceBackend final : public lmmsim::ExecutionBackend {
  public:
   DeviceBackend(Context& ctx, const lmmsim::SimConfig& cfg, bool realtime, bool e2e,
-                std::uint64_t payload_seed);
+                std::uint64_t payload_seed, bool serialize = false);
   ~DeviceBackend() override;
 
   /// Generates pixel payloads of `workload` (device or pinned host). Untimed.
