@@ -240,6 +240,45 @@ RS_API rs_status rs_engine_run(rs_ctx* ctx, const char* workload_text,
                         char** out_result, char** out_journal,
                         rs_run_stats* out_stats);
 
+/* ---- EP disaggregation: encoders and prefill stages on separate GPUs ----
+ * The paper's EP deployment (RServe §4; the reference models it only as the
+ * eps/zeta transfer cost, cost_model.hpp:84-88, and stages > 1,
+ * simengine.hpp:494-515). Ranks: P_s = s (s < stages), E_w = stages + w.
+ * Rank 0 (P0) runs the engine, the device tracker and prefill stage 0;
+ * encoder ranks run the ViT; ranks 1..stages-1 run later LLM layers (the
+ * last one holds the LM head). Messages go over one directed link per rank
+ * pair: NCCL (one process per GPU) or loopback (all ranks are threads of
+ * this process, each with its own rs_ctx, on any devices).              */
+typedef struct rs_ep rs_ep;
+typedef struct rs_ep_options {
+  int32_t stages;      /* prefill ranks (>= 1)                               */
+  int32_t encoders;    /* encoder ranks (>= 1)                               */
+  int32_t transport;   /* 0 loopback, 1 NCCL                                 */
+  int32_t rank;        /* NCCL: this process's rank; loopback: ignored       */
+  int32_t device;      /* NCCL: CUDA device of this rank                     */
+  const void* nccl_ids;/* NCCL: n_links x 128-byte ncclUniqueId, links order */
+} rs_ep_options;
+/* Directed links (src, dst) of a topology, in creation order: pairs must
+ * hold 2 * n entries (NULL: only *n_links is written).                    */
+RS_API rs_status rs_ep_links(int32_t stages, int32_t encoders, int32_t* n_links, int32_t* pairs);
+RS_API rs_status rs_nccl_unique_id(void* out128);
+RS_API rs_status rs_ep_create(const rs_ep_options* opt, rs_ep** out);
+RS_API rs_status rs_ep_destroy(rs_ep* ep);
+/* Worker ranks (NCCL): payloads of the run (encoders), then serve until P0
+ * sends STOP at the end of its rs_ep_engine_run.                          */
+RS_API rs_status rs_ep_worker_prepare(rs_ep* ep, rs_ctx* ctx, const char* workload_text,
+                                      uint64_t payload_seed, int32_t e2e);
+RS_API rs_status rs_ep_worker_run(rs_ep* ep, rs_ctx* ctx);
+/* P0: one engine run. Loopback: `workers` holds the contexts of ranks
+ * 1..world-1 (run on threads of this call); NCCL: workers = NULL.         */
+RS_API rs_status rs_ep_engine_run(rs_ep* ep, rs_ctx* p0, rs_ctx* const* workers,
+                                  const char* workload_text, const rs_sim_config* cfg,
+                                  const rs_run_options* opt, char** out_result,
+                                  char** out_journal, rs_run_stats* out_stats);
+/* Control-message codec (host only): text form <-> the 32 KB wire message. */
+RS_API rs_status rs_ep_ctrl_pack(const char* text, void* out_msg, uint64_t msg_bytes);
+RS_API rs_status rs_ep_ctrl_unpack(const void* msg, uint64_t msg_bytes, char** out_text);
+
 #ifdef __cplusplus
 }  /* extern "C" */
 #endif

@@ -173,6 +173,25 @@ _sig("rs_weight_info", [C.c_void_p, C.c_char_p, C.POINTER(C.c_void_p), C.POINTER
                         C.POINTER(C.c_int64), C.POINTER(C.c_int64)])
 _sig("rs_debug_buffer", [C.c_void_p, C.c_char_p, C.POINTER(C.c_void_p), C.POINTER(C.c_int64)])
 
+# EP disaggregation
+class rs_ep_options(C.Structure):
+    _fields_ = [("stages", C.c_int32), ("encoders", C.c_int32), ("transport", C.c_int32),
+                ("rank", C.c_int32), ("device", C.c_int32), ("nccl_ids", C.c_void_p)]
+
+
+_sig("rs_ep_links", [C.c_int32, C.c_int32, C.POINTER(C.c_int32), C.POINTER(C.c_int32)])
+_sig("rs_nccl_unique_id", [C.c_void_p])
+_sig("rs_ep_create", [C.POINTER(rs_ep_options), C.POINTER(C.c_void_p)])
+_sig("rs_ep_destroy", [C.c_void_p])
+_sig("rs_ep_worker_prepare", [C.c_void_p, C.c_void_p, C.c_char_p, C.c_uint64, C.c_int32])
+_sig("rs_ep_worker_run", [C.c_void_p, C.c_void_p])
+_sig("rs_ep_engine_run", [C.c_void_p, C.c_void_p, C.POINTER(C.c_void_p), C.c_char_p,
+                          C.POINTER(rs_sim_config), C.POINTER(rs_run_options), PCHAR, PCHAR,
+                          C.POINTER(rs_run_stats)])
+_sig("rs_ep_ctrl_pack", [C.c_char_p, C.c_void_p, C.c_uint64])
+_sig("rs_ep_ctrl_unpack", [C.c_void_p, C.c_uint64, PCHAR])
+EP_CTRL_BYTES = 4096 * 8
+
 # op-level ABI (include/rserve_ops.h)
 VP, I = C.c_void_p, C.c_int
 _sig("rs_op_gemm", [VP, I, VP, I, VP, I, VP, VP, I, VP, I, I, I, I, I, VP])

@@ -323,3 +323,117 @@ class Pipeline:
                                     C.byref(res), C.byref(jr), C.byref(st)))
         stats = {k: getattr(st, k) for k, _ in N.rs_run_stats._fields_}
         return N.take_string(res), N.take_string(jr), stats
+
+
+# ---- EP disaggregation (include/rserve.h "EP disaggregation") -------------------------------
+def ep_links(stages: int, encoders: int) -> List[Tuple[int, int]]:
+    """Directed links (src, dst) of an EP topology, in creation order."""
+    n = C.c_int32()
+    N.check(N.lib.rs_ep_links(stages, encoders, C.byref(n), None))
+    pairs = (C.c_int32 * (2 * n.value))()
+    N.check(N.lib.rs_ep_links(stages, encoders, C.byref(n), pairs))
+    return [(pairs[2 * i], pairs[2 * i + 1]) for i in range(n.value)]
+
+
+def ep_role(rank: int, stages: int, encoders: int) -> Tuple[str, int]:
+    """("prefill", s) for P_s = rank s; ("encoder", w) for E_w = rank stages + w."""
+    if not 0 <= rank < stages + encoders:
+        raise N.ConfigError(f"rank {rank} outside an EP world of {stages + encoders}")
+    return ("prefill", rank) if rank < stages else ("encoder", rank - stages)
+
+
+def ep_stage_layers(stage: int, stages: int, layers: int) -> Tuple[int, int]:
+    """LLM layers [begin, end) of prefill stage `stage` (even split)."""
+    return layers * stage // stages, layers * (stage + 1) // stages
+
+
+def ep_context(model: N.rs_model_config, rank: int, stages: int, encoders: int, device: int = 0,
+               **opts) -> "Pipeline":
+    """The device context of EP rank `rank`: ViT only on encoder ranks; the
+    stage's LLM layers on prefill ranks (LM head on the last one)."""
+    role, idx = ep_role(rank, stages, encoders)
+    L = model.llm_layers
+    if role == "encoder":
+        o = dict(opts, with_vit=True, with_lm_head=False, layer_begin=L, layer_end=L,
+                 kv_tokens=0, slot_tokens=0, max_chunk_tokens=64)
+        return Pipeline(model, device=device, **o)
+    lb, le = ep_stage_layers(idx, stages, L)
+    o = dict(opts, with_vit=False, with_lm_head=(idx == stages - 1), layer_begin=lb, layer_end=le)
+    if idx > 0:
+        o["slot_tokens"] = 0
+    return Pipeline(model, device=device, **o)
+
+
+def ep_ctrl_pack(text: str) -> bytes:
+    """Text form of a control message -> its 32 KB wire bytes."""
+    buf = C.create_string_buffer(N.EP_CTRL_BYTES)
+    N.check(N.lib.rs_ep_ctrl_pack(text.encode(), buf, N.EP_CTRL_BYTES))
+    return buf.raw
+
+
+def ep_ctrl_unpack(msg: bytes) -> str:
+    out = _out()
+    N.check(N.lib.rs_ep_ctrl_unpack(msg, len(msg), C.byref(out)))
+    return N.take_string(out)
+
+
+def nccl_unique_id() -> bytes:
+    buf = C.create_string_buffer(128)
+    N.check(N.lib.rs_nccl_unique_id(buf))
+    return buf.raw
+
+
+class EpGroup:
+    """EP endpoints: `transport="loopback"` (every rank a thread of this
+    process — one GPU is enough) or `"nccl"` (this process is `rank`; the
+    ncclUniqueIds of all links come from rank 0, one per ep_links() entry)."""
+
+    def __init__(self, stages: int, encoders: int, transport: str = "loopback", rank: int = 0,
+                 device: int = 0, nccl_ids: Optional[bytes] = None):
+        self.stages, self.encoders = stages, encoders
+        o = N.rs_ep_options()
+        o.stages, o.encoders = stages, encoders
+        o.transport = {"loopback": 0, "nccl": 1}[transport]
+        o.rank, o.device = rank, device
+        self._ids = C.create_string_buffer(nccl_ids, len(nccl_ids)) if nccl_ids else None
+        o.nccl_ids = C.cast(self._ids, C.c_void_p) if self._ids is not None else None
+        h = C.c_void_p()
+        N.check(N.lib.rs_ep_create(C.byref(o), C.byref(h)))
+        self.h = h
+
+    def close(self):
+        if self.h:
+            N.check(N.lib.rs_ep_destroy(self.h))
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def run(self, p0: "Pipeline", workers: Optional[Sequence["Pipeline"]], workload: str,
+            cfg: SimConfig, clock: str = "lockstep", e2e: bool = False, payload_seed: int = 7):
+        """Engine run on P0 (rank 0) -> (decision log, journal, stats).
+        Loopback: `workers` are the contexts of ranks 1..world-1."""
+        o = N.rs_run_options()
+        o.clock = 1 if clock == "real" else 0
+        o.e2e = int(e2e)
+        o.payload_seed = payload_seed
+        arr = None
+        if workers is not None:
+            arr = (C.c_void_p * len(workers))(*[w.h.value for w in workers])
+        res, jr = _out(), _out()
+        st = N.rs_run_stats()
+        c = cfg.to_c()
+        N.check(N.lib.rs_ep_engine_run(self.h, p0.h, arr, workload.encode(), C.byref(c), C.byref(o),
+                                       C.byref(res), C.byref(jr), C.byref(st)))
+        p0._ep_logits = True
+        stats = {k: getattr(st, k) for k, _ in N.rs_run_stats._fields_}
+        return N.take_string(res), N.take_string(jr), stats
+
+    def worker_prepare(self, ctx: "Pipeline", workload: str, payload_seed: int = 7, e2e: bool = False):
+        N.check(N.lib.rs_ep_worker_prepare(self.h, ctx.h, workload.encode(), payload_seed, int(e2e)))
+
+    def worker_run(self, ctx: "Pipeline"):
+        N.check(N.lib.rs_ep_worker_run(self.h, ctx.h))

@@ -5,6 +5,7 @@
 #include <unordered_map>
 
 #include "device_backend.cuh"
+#include "capi_ctx.cuh"
 #include "device_context.cuh"
 #include "host/config_bridge.hpp"
 #include "host/decision_log.hpp"
@@ -13,23 +14,6 @@
 #include "rserve.h"
 
 using namespace rserve;
-
-struct rs_ctx {
-  std::unique_ptr<Context> ctx;
-  lmmsim::TrackerRegistry registry;  // host mirrors of the manual API
-  bf16* manual_out = nullptr;        // rs_encode output
-  bf16* manual_in = nullptr;         // rs_encode patches staging (host input)
-  bf16* manual_x = nullptr;          // rs_prefill_chunk residual
-  std::unordered_map<lmmsim::RequestId, std::vector<float>> logits;
-  std::unordered_map<lmmsim::RequestId, std::int32_t> argmax;
-};
-
-namespace {
-rs_ctx& need(rs_ctx* c) {
-  if (c == nullptr || !c->ctx) throw lmmsim::InputError("null rs_ctx");
-  return *c;
-}
-}  // namespace
 
 extern "C" {
 

@@ -8,16 +8,22 @@
 
 namespace rserve {
 
-namespace {
-std::uint64_t pixel_stream(std::uint64_t req, std::uint64_t item) {
-  return (5ull << 32) | (req << 12) | item;
-}
-}  // namespace
-
 DeviceBackend::DeviceBackend(Context& ctx, const lmmsim::SimConfig& cfg, bool realtime, bool e2e,
-                             std::uint64_t payload_seed, bool serialize_streams)
-    : ctx_(ctx), cfg_(cfg), realtime_(realtime), e2e_(e2e), seed_(payload_seed) {
+                             std::uint64_t payload_seed, bool serialize_streams,
+                             const ep::Remote* remote)
+    : ctx_(ctx), cfg_(cfg), realtime_(realtime), e2e_(e2e), seed_(payload_seed), remote_(remote) {
   if (cfg.stages < 1) throw lmmsim::ConfigError("stages: must be >= 1");
+  if (remote_ != nullptr) {
+    remote_->topo.validate();
+    if (cfg.encoder_workers != remote_->topo.encoders)
+      throw lmmsim::ConfigError("encoder_workers: must equal the EP encoder ranks (" +
+                                std::to_string(remote_->topo.encoders) + ")");
+    if (cfg.stages != remote_->topo.stages)
+      throw lmmsim::ConfigError("stages: must equal the EP prefill ranks (" +
+                                std::to_string(remote_->topo.stages) + ")");
+    if (remote_->topo.stages > 1 && ctx.llm()->has_head())
+      throw lmmsim::ConfigError("EP: P0 must not hold the LM head when stages > 1");
+  }
   const int workers = cfg.encoder_workers;
   const Shapes& s = ctx.shapes();
   // One prefill stream: all stages of this GPU share the SMs and the per-stage
@@ -46,7 +52,7 @@ DeviceBackend::DeviceBackend(Context& ctx, const lmmsim::SimConfig& cfg, bool re
     staging_free_.push_back(nullptr);
   }
   enc_ring_pos_.assign(static_cast<std::size_t>(workers), 0);
-  if (e2e_) {
+  if (e2e_ && remote_ == nullptr) {
     for (int w = 0; w < workers; ++w) {
       void* p = nullptr;
       RS_CUDA_CHECK(cudaMalloc(&p, 4 * max_tok * s.pdim * sizeof(bf16)));
@@ -62,6 +68,24 @@ DeviceBackend::DeviceBackend(Context& ctx, const lmmsim::SimConfig& cfg, bool re
     free_xbufs_.push_back(i);
   }
   RS_CUDA_CHECK(cudaEventCreate(&origin_));
+  if (remote_ != nullptr) {
+    RS_CUDA_CHECK(cudaStreamCreateWithFlags(&ctrl_stream_, cudaStreamNonBlocking));
+    for (int i = 0; i < kCtrlRing; ++i) {
+      void* d = nullptr;
+      void* h = nullptr;
+      RS_CUDA_CHECK(cudaMalloc(&d, ep::kCtrlBytes));
+      RS_CUDA_CHECK(cudaMallocHost(&h, ep::kCtrlBytes));
+      ctrl_dev_.push_back(d);
+      ctrl_host_.push_back(static_cast<std::int64_t*>(h));
+      ctrl_free_.push_back(nullptr);
+    }
+    RS_CUDA_CHECK(cudaMalloc(&header_sink_, ep::kHeaderBytes));
+    if (remote_->topo.stages > 1) {
+      void* p = nullptr;
+      RS_CUDA_CHECK(cudaMalloc(&p, static_cast<std::size_t>(ctx.max_requests()) * s.vocab * 4));
+      remote_logits_ = static_cast<float*>(p);
+    }
+  }
 }
 
 DeviceBackend::~DeviceBackend() {
@@ -81,6 +105,13 @@ DeviceBackend::~DeviceBackend() {
     for (auto st : enc_streams_) cudaStreamDestroy(st);
   for (auto st : stage_streams_) cudaStreamDestroy(st);
   if (copy_stream_) cudaStreamDestroy(copy_stream_);
+  remote_ops_.clear();
+  slot_xfer_.clear();
+  for (void* p : ctrl_dev_) cudaFree(p);
+  for (std::int64_t* p : ctrl_host_) cudaFreeHost(p);
+  if (ctrl_stream_) cudaStreamDestroy(ctrl_stream_);
+  if (header_sink_) cudaFree(header_sink_);
+  if (remote_logits_) cudaFree(remote_logits_);
 }
 
 cudaEvent_t DeviceBackend::timing_event() {
@@ -99,7 +130,7 @@ void DeviceBackend::prepare(const std::vector<lmmsim::RequestSpec>& workload) {
       if (seg.kind == lmmsim::SegmentKind::Multimodal) patches += 4 * seg.tokens;
     Payload p;
     p.patches = patches;
-    if (patches > 0) {
+    if (patches > 0 && remote_ == nullptr) {  // EP: pixels live on the encoder ranks
       void* dev = nullptr;
       RS_CUDA_CHECK(cudaMalloc(&dev, patches * s.pdim * sizeof(bf16)));
       p.patches_dev = static_cast<bf16*>(dev);
@@ -158,6 +189,7 @@ void DeviceBackend::on_request_created(const lmmsim::RequestSpec& req, const lmm
   cudaStream_t st = ctx_.tracker_stream();
   DevRequest& r = ctx_.create_request(req, nullptr, seed_, st);
   done_slots_[req.id] = r.slot;
+  if (remote_ != nullptr) layouts_[req.id] = req.segments;
   if (e2e_) {
     std::uint64_t text = 0;
     for (const auto& [b, e] : r.text_ranges) text += e - b;
@@ -168,6 +200,10 @@ void DeviceBackend::on_request_created(const lmmsim::RequestSpec& req, const lmm
 }
 
 double DeviceBackend::launch_encode(int worker, std::size_t slot, const lmmsim::EncodeBatch& b) {
+  if (remote_ != nullptr) {
+    launch_remote_encode(worker, slot, b);
+    return realtime_ ? 0.0 : lmmsim::encode_time_ms(cfg_.cost, b);
+  }
   cudaStream_t st = enc_streams_[static_cast<std::size_t>(worker)];
   DevRequest& r = ctx_.get(b.request_id);
   const Shapes& s = ctx_.shapes();
@@ -204,6 +240,11 @@ double DeviceBackend::launch_encode(int worker, std::size_t slot, const lmmsim::
 }
 
 double DeviceBackend::launch_transfer(int /*worker*/, std::size_t slot, const lmmsim::EncodeBatch& b) {
+  if (remote_ != nullptr) {  // EP: the embeddings' receive was posted at launch_encode
+    for (RemoteOp& op : remote_ops_)
+      if (op.kind == lmmsim::OpKind::Transfer && op.b == slot) op.launched = true;
+    return realtime_ ? 0.0 : lmmsim::transfer_time_ms(cfg_.cost, b.total_tokens);
+  }
   // Co-located encoder and prefill: the embeddings are already in this GPU's
   // HBM; the link is the reference's zero-cost case.
   if (realtime_) ready_transfers_.emplace_back(slot, slot_done_ms_.count(slot) ? slot_done_ms_[slot] : clock_ms());
@@ -212,12 +253,14 @@ double DeviceBackend::launch_transfer(int /*worker*/, std::size_t slot, const lm
 
 void DeviceBackend::on_embeddings_ready(std::size_t slot, const lmmsim::EncodeBatch& b) {
   cudaStream_t st = ctx_.tracker_stream();
+  if (remote_ != nullptr) remote_->t->wait_posted(*slot_xfer_.at(slot));
   RS_CUDA_CHECK(cudaStreamWaitEvent(st, slot_done_.at(slot), 0));
   DevRequest& r = ctx_.get(b.request_id);
   std::vector<lmmsim::TokenRange> items;
   for (const auto& it : b.items) items.push_back(it.second);
   const int ring = slot_staging_.at(slot);
   ctx_.scatter_items(r, items, staging_[static_cast<std::size_t>(ring)], st);
+  slot_xfer_.erase(slot);
   cudaEvent_t ev = ctx_.new_event();
   RS_CUDA_CHECK(cudaEventRecord(ev, st));
   staging_free_[static_cast<std::size_t>(ring)] = ev;
@@ -226,6 +269,13 @@ void DeviceBackend::on_embeddings_ready(std::size_t slot, const lmmsim::EncodeBa
 }
 
 double DeviceBackend::launch_stage(int stage, const lmmsim::ChunkView& c) {
+  const double cost = realtime_ ? 0.0 : lmmsim::stage_time_ms(cfg_.cost, c.total_tokens, c.weighted_context);
+  if (remote_ != nullptr && stage > 0) {  // runs on rank P_stage; completion = its DONE message
+    for (RemoteOp& op : remote_ops_)
+      if (op.kind == lmmsim::OpKind::Stage && op.a == static_cast<std::uint32_t>(stage) && op.b == c.chunk_id)
+        op.launched = true;
+    return cost;
+  }
   cudaStream_t st = stage_streams_[0];
   ChunkState& cs = chunks_[c.chunk_id];
   if (stage == 0) {
@@ -246,24 +296,113 @@ double DeviceBackend::launch_stage(int stage, const lmmsim::ChunkView& c) {
   for (const auto& [id, range] : *c.slices) slices.push_back({&ctx_.get(id), range.start, range.end});
   // Layers of this stage within the context's range.
   const int lb = ctx_.llm()->layer_begin(), le = ctx_.llm()->layer_end();
-  const int S = cfg_.stages, n = le - lb;
+  const int S = remote_ != nullptr ? 1 : cfg_.stages, n = le - lb;  // EP: stage 0 = all local layers
   const int from = lb + n * stage / S, to = lb + n * (stage + 1) / S;
   cudaEvent_t begin = timing_event(), end = timing_event();
   RS_CUDA_CHECK(cudaEventRecord(begin, st));
   ctx_.prefill(slices, cs.x, st, from, to);
   RS_CUDA_CHECK(cudaEventRecord(end, st));
   cs.last = end;
+  if (stage == 0) cs.s0_end = end;
   track(lmmsim::OpKind::Stage, static_cast<std::uint32_t>(stage), c.chunk_id, begin, end);
-  if (stage + 1 == S) {  // residual buffer free once the last stage ran
+  if (remote_ != nullptr && cfg_.stages > 1) {
+    forward_chunk(c, cs);  // sets the residual buffer's guard to its send
+    free_xbufs_.push_back(cs.buf);
+  } else if (stage + 1 == S) {  // residual buffer free once the last stage ran
     xbuf_guard_[static_cast<std::size_t>(cs.buf)] = end;
     free_xbufs_.push_back(cs.buf);
   }
-  return realtime_ ? 0.0 : lmmsim::stage_time_ms(cfg_.cost, c.total_tokens, c.weighted_context);
+  return cost;
+}
+
+void* DeviceBackend::put_ctrl(const ep::Words& w) {
+  const int i = ctrl_pos_;
+  ctrl_pos_ = (ctrl_pos_ + 1) % kCtrlRing;
+  if (ctrl_free_[static_cast<std::size_t>(i)] != nullptr)  // previous message still in flight
+    RS_CUDA_CHECK(cudaEventSynchronize(ctrl_free_[static_cast<std::size_t>(i)]));
+  std::memcpy(ctrl_host_[static_cast<std::size_t>(i)], w.data(), ep::kCtrlBytes);
+  RS_CUDA_CHECK(cudaMemcpyAsync(ctrl_dev_[static_cast<std::size_t>(i)], ctrl_host_[static_cast<std::size_t>(i)],
+                                ep::kCtrlBytes, cudaMemcpyHostToDevice, ctrl_stream_));
+  stats_.h2d_bytes += ep::kCtrlBytes;
+  return ctrl_dev_[static_cast<std::size_t>(i)];
+}
+
+void DeviceBackend::launch_remote_encode(int worker, std::size_t slot, const lmmsim::EncodeBatch& b) {
+  const ep::Topology& topo = remote_->topo;
+  ep::Transport& t = *remote_->t;
+  DevRequest& r = ctx_.get(b.request_id);
+  const Shapes& s = ctx_.shapes();
+  const int ring = worker * kRing + enc_ring_pos_[static_cast<std::size_t>(worker)];
+  enc_ring_pos_[static_cast<std::size_t>(worker)] = (enc_ring_pos_[static_cast<std::size_t>(worker)] + 1) % kRing;
+  slot_staging_[slot] = ring;
+  ep::EncodeCmd cmd;
+  cmd.slot = slot;
+  cmd.request_id = b.request_id;
+  for (const auto& [idx, range] : b.items)
+    cmd.items.push_back({idx, range.start, range.end, r.item_patch_offset[idx]});
+  ep::Words w;
+  ep::pack(cmd, w);
+  void* dev = put_ctrl(w);
+  cudaEvent_t staged = timing_event();
+  RS_CUDA_CHECK(cudaEventRecord(staged, ctrl_stream_));
+  const int peer = topo.e_rank(worker);
+  ctrl_free_[static_cast<std::size_t>((ctrl_pos_ + kCtrlRing - 1) % kCtrlRing)] =
+      t.send(peer, dev, ep::kCtrlBytes, staged);
+  auto hdr = t.post_recv(peer, header_sink_, ep::kHeaderBytes, nullptr);
+  auto emb = t.post_recv(peer, staging_[static_cast<std::size_t>(ring)], b.total_tokens * s.d * sizeof(bf16),
+                         staging_free_[static_cast<std::size_t>(ring)]);
+  slot_done_[slot] = emb->done;
+  slot_xfer_[slot] = emb;
+  remote_ops_.push_back({lmmsim::OpKind::Encode, static_cast<std::uint32_t>(worker), slot, {hdr}, true});
+  remote_ops_.push_back({lmmsim::OpKind::Transfer, 0, slot, {emb}, false});
+}
+
+void DeviceBackend::forward_chunk(const lmmsim::ChunkView& c, const ChunkState& cs) {
+  const ep::Topology& topo = remote_->topo;
+  ep::Transport& t = *remote_->t;
+  const Shapes& s = ctx_.shapes();
+  ep::StageCmd cmd;
+  cmd.chunk_id = c.chunk_id;
+  for (const auto& [id, range] : *c.slices) cmd.slices.push_back({id, range.start, range.end, layouts_.at(id)});
+  ep::Words w;
+  ep::pack(cmd, w);
+  void* dev = put_ctrl(w);
+  cudaEvent_t staged = timing_event();
+  RS_CUDA_CHECK(cudaEventRecord(staged, ctrl_stream_));
+  const int p1 = topo.p_rank(1);
+  ctrl_free_[static_cast<std::size_t>((ctrl_pos_ + kCtrlRing - 1) % kCtrlRing)] =
+      t.send(p1, dev, ep::kCtrlBytes, staged);
+  // The residual rides behind the control message; its buffer is reusable
+  // once sent.
+  xbuf_guard_[static_cast<std::size_t>(cs.buf)] =
+      t.send(p1, cs.x, c.total_tokens * s.d * sizeof(bf16), cs.s0_end);
+  // Completions of the downstream stages: a DONE header each; the last stage
+  // then ships the logits row of every prompt that ends in this chunk.
+  for (int st = 1; st < topo.stages; ++st) {
+    RemoteOp op{lmmsim::OpKind::Stage, static_cast<std::uint32_t>(st), c.chunk_id, {}, false};
+    op.xfers.push_back(t.post_recv(topo.p_rank(st), header_sink_, ep::kHeaderBytes, nullptr));
+    if (st + 1 == topo.stages) {
+      for (const auto& [id, range] : *c.slices) {
+        const DevRequest& r = ctx_.get(id);
+        if (range.end != r.total) continue;
+        op.xfers.push_back(t.post_recv(topo.p_rank(st), remote_logits_ + static_cast<std::int64_t>(r.slot) * s.vocab,
+                                       static_cast<std::size_t>(s.vocab) * 4, nullptr));
+      }
+      chunk_logits_[c.chunk_id] = op.xfers.back()->done;
+    }
+    remote_ops_.push_back(std::move(op));
+  }
+}
+
+bool DeviceBackend::remote_done(RemoteOp& op) {
+  for (auto& x : op.xfers)
+    if (!remote_->t->test(*x)) return false;
+  return true;
 }
 
 void DeviceBackend::on_release(std::size_t chunk, lmmsim::RequestId id, lmmsim::TokenRange r) {
   const ChunkState& cs = chunks_.at(chunk);
-  release_guard_ = cs.last;
+  release_guard_ = remote_ != nullptr ? cs.s0_end : cs.last;
   DevRequest& dr = ctx_.get(id);
   ctx_.release_prefix(dr, r.end, release_guard_);
 }
@@ -275,8 +414,19 @@ void DeviceBackend::on_request_erased(lmmsim::RequestId id) {
 void DeviceBackend::on_request_complete(lmmsim::RequestId id, std::size_t chunk) {
   if (!e2e_) return;
   const ChunkState& cs = chunks_.at(chunk);
-  RS_CUDA_CHECK(cudaStreamWaitEvent(copy_stream_, cs.last, 0));
-  ctx_.copy_logits(done_slots_.at(id), logits_host_.at(id), copy_stream_);
+  if (remote_logits_ != nullptr) {  // EP: the logits row arrived from the last stage
+    for (RemoteOp& op : remote_ops_)
+      if (op.kind == lmmsim::OpKind::Stage && op.b == chunk)
+        for (auto& x : op.xfers) remote_->t->wait_posted(*x);
+    RS_CUDA_CHECK(cudaStreamWaitEvent(copy_stream_, chunk_logits_.at(chunk), 0));
+    RS_CUDA_CHECK(cudaMemcpyAsync(logits_host_.at(id),
+                                  remote_logits_ + static_cast<std::int64_t>(done_slots_.at(id)) * ctx_.shapes().vocab,
+                                  static_cast<std::size_t>(ctx_.shapes().vocab) * 4, cudaMemcpyDeviceToHost,
+                                  copy_stream_));
+  } else {
+    RS_CUDA_CHECK(cudaStreamWaitEvent(copy_stream_, cs.last, 0));
+    ctx_.copy_logits(done_slots_.at(id), logits_host_.at(id), copy_stream_);
+  }
   stats_.d2h_bytes += static_cast<std::uint64_t>(ctx_.shapes().vocab) * 4;
 }
 
@@ -297,6 +447,18 @@ void DeviceBackend::poll(std::vector<lmmsim::OpCompletion>& out) {
     ops_[i] = ops_.back();
     ops_.pop_back();
   }
+  for (std::size_t i = 0; i < remote_ops_.size();) {
+    RemoteOp& op = remote_ops_[i];
+    if (!op.launched || !remote_done(op)) {
+      ++i;
+      continue;
+    }
+    float ms = 0;
+    RS_CUDA_CHECK(cudaEventElapsedTime(&ms, origin_, op.xfers.back()->done));
+    remote_last_ms_ = std::max(remote_last_ms_, static_cast<double>(ms));
+    out.push_back({op.kind, op.a, op.b, static_cast<double>(ms)});
+    remote_ops_.erase(remote_ops_.begin() + static_cast<std::ptrdiff_t>(i));
+  }
   std::stable_sort(out.begin(), out.end(),
                    [](const lmmsim::OpCompletion& x, const lmmsim::OpCompletion& y) {
                      return x.time_ms < y.time_ms;
@@ -304,6 +466,13 @@ void DeviceBackend::poll(std::vector<lmmsim::OpCompletion>& out) {
 }
 
 void DeviceBackend::finish() {
+  for (RemoteOp& op : remote_ops_) {  // lock-step EP: arrivals not yet observed
+    for (auto& x : op.xfers) remote_->t->wait(*x);
+    float ms = 0;
+    RS_CUDA_CHECK(cudaEventElapsedTime(&ms, origin_, op.xfers.back()->done));
+    remote_last_ms_ = std::max(remote_last_ms_, static_cast<double>(ms));
+  }
+  remote_ops_.clear();
   RS_CUDA_CHECK(cudaDeviceSynchronize());
   stats_.wall_ms = clock_ms();
   if (last_event_ != nullptr) {
@@ -311,6 +480,7 @@ void DeviceBackend::finish() {
     RS_CUDA_CHECK(cudaEventElapsedTime(&ms, origin_, last_event_));
     stats_.gpu_ms = ms;
   }
+  stats_.gpu_ms = std::max(stats_.gpu_ms, remote_last_ms_);
   stats_.kernel_launches = launches_so_far() - launches0_;
   stats_.h2d_bytes += ctx_.uploader().bytes_uploaded() - upload0_;
 }
@@ -324,12 +494,17 @@ void DeviceBackend::collect() {
     std::vector<float> row(static_cast<std::size_t>(vocab));
     if (e2e_) {
       std::memcpy(row.data(), logits_host_.at(id), row.size() * 4);
+    } else if (remote_logits_ != nullptr) {
+      RS_CUDA_CHECK(cudaMemcpy(row.data(), remote_logits_ + static_cast<std::int64_t>(slot) * vocab,
+                               row.size() * 4, cudaMemcpyDeviceToHost));
     } else {
       ctx_.copy_logits(slot, row.data(), ctx_.aux_stream());
       RS_CUDA_CHECK(cudaStreamSynchronize(ctx_.aux_stream()));
     }
+    argmax_[id] = remote_logits_ != nullptr
+                      ? static_cast<std::int32_t>(std::max_element(row.begin(), row.end()) - row.begin())
+                      : am[static_cast<std::size_t>(slot)];
     logits_[id] = std::move(row);
-    argmax_[id] = am[static_cast<std::size_t>(slot)];
     ctx_.free_slot(slot);
   }
   done_slots_.clear();

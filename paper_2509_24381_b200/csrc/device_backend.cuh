@@ -23,6 +23,7 @@
 #include <vector>
 
 #include "device_context.cuh"
+#include "ep.cuh"
 #include "lmmsim/simengine.hpp"
 
 namespace rserve {
@@ -36,8 +37,11 @@ struct Payload {
 
 class DeviceBackend final : public lmmsim::ExecutionBackend {
  public:
+  /// remote != nullptr: EP mode — this is P0; encoders and stages >= 1 are
+  /// other ranks reached through remote->t (see ep.cuh).
   DeviceBackend(Context& ctx, const lmmsim::SimConfig& cfg, bool realtime, bool e2e,
-                std::uint64_t payload_seed, bool serialize = false);
+                std::uint64_t payload_seed, bool serialize = false,
+                const ep::Remote* remote = nullptr);
   ~DeviceBackend() override;
 
   /// Generates pixel payloads of `workload` (device or pinned host). Untimed.
@@ -78,7 +82,20 @@ class DeviceBackend final : public lmmsim::ExecutionBackend {
     bf16* x = nullptr;
     int buf = -1;
     cudaEvent_t last = nullptr;  // completion of the latest stage launched
+    cudaEvent_t s0_end = nullptr;  // stage 0 (the only reader of the slab rows)
   };
+  /// EP: an op whose completion is the arrival of one or more messages.
+  struct RemoteOp {
+    lmmsim::OpKind kind;
+    std::uint32_t a;
+    std::uint64_t b;
+    std::vector<std::shared_ptr<ep::Xfer>> xfers;
+    bool launched;  // engine has started it (completions before that are held)
+  };
+  void* put_ctrl(const ep::Words& w);
+  void launch_remote_encode(int worker, std::size_t slot, const lmmsim::EncodeBatch& b);
+  void forward_chunk(const lmmsim::ChunkView& c, const ChunkState& cs);
+  bool remote_done(RemoteOp& op);
   cudaEvent_t timing_event();
   void track(lmmsim::OpKind k, std::uint32_t a, std::uint64_t b, cudaEvent_t begin, cudaEvent_t end);
   int stage_of_layer_split(int s, int* lb, int* le) const;
@@ -121,6 +138,21 @@ class DeviceBackend final : public lmmsim::ExecutionBackend {
   rs_run_stats stats_{};
   std::uint64_t launches0_ = 0, upload0_ = 0;
   cudaEvent_t last_event_ = nullptr;
+  // EP (remote_ != nullptr)
+  const ep::Remote* remote_ = nullptr;
+  std::unordered_map<lmmsim::RequestId, std::vector<lmmsim::SegmentSpec>> layouts_;
+  std::vector<RemoteOp> remote_ops_;
+  std::unordered_map<std::size_t, std::shared_ptr<ep::Xfer>> slot_xfer_;
+  std::unordered_map<std::size_t, cudaEvent_t> chunk_logits_;  // chunk -> last logits arrival
+  static constexpr int kCtrlRing = 16;
+  std::vector<void*> ctrl_dev_;
+  std::vector<std::int64_t*> ctrl_host_;
+  std::vector<cudaEvent_t> ctrl_free_;
+  int ctrl_pos_ = 0;
+  cudaStream_t ctrl_stream_ = nullptr;
+  void* header_sink_ = nullptr;
+  float* remote_logits_ = nullptr;  // [max_requests, vocab] when the LM head is remote
+  double remote_last_ms_ = 0;
 };
 
 }  // namespace rserve

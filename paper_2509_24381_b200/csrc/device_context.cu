@@ -184,6 +184,39 @@ void mrope_ids(const lmmsim::RequestSpec& req, std::vector<std::array<std::int32
 }
 }  // namespace
 
+void Context::attach_kv(const lmmsim::RequestSpec& req, DevRequest& r, cudaStream_t st) {
+  mrope_ids(req, r.rope);
+  r.slot = take_request_slot();
+  const std::int64_t pages = static_cast<std::int64_t>((r.total + kPageTokens - 1) / kPageTokens);
+  std::vector<cudaEvent_t> kv_guards;  // KV pages: written only on the stage stream, in order
+  r.kv_pages = kv_pages_.take(pages, kv_guards);
+  RS_CUDA_CHECK(cudaMallocAsync(reinterpret_cast<void**>(&r.kv_table),
+                                static_cast<std::size_t>(pages) * 4, st));
+  const void* kvt = up_.put(r.kv_pages.data(), r.kv_pages.size() * 4, st);
+  RS_CUDA_CHECK(cudaMemcpyAsync(r.kv_table, kvt, r.kv_pages.size() * 4, cudaMemcpyDeviceToDevice, st));
+  const void* ptr_src = up_.put(&r.kv_table, sizeof(int*), st);
+  RS_CUDA_CHECK(cudaMemcpyAsync(page_tables_dev_ + r.slot, ptr_src, sizeof(int*),
+                                cudaMemcpyDeviceToDevice, st));
+  page_tables_host_[static_cast<std::size_t>(r.slot)] = r.kv_table;
+}
+
+DevRequest& Context::create_kv_request(const lmmsim::RequestSpec& req, cudaStream_t st) {
+  if (find(req.id) != nullptr)
+    throw lmmsim::RegistryError("duplicate request id " + lmmsim::format_u64(req.id));
+  auto owned = std::make_unique<DevRequest>();
+  DevRequest& r = *owned;
+  r.id = req.id;
+  r.total = req.total_tokens();
+  if (r.total > opt_.kv_tokens)
+    throw lmmsim::ConfigError("request " + lmmsim::format_u64(req.id) + ": " +
+                              lmmsim::format_u64(r.total) + " tokens exceed the KV pool");
+  attach_kv(req, r, st);
+  up_.fence(st);
+  DevRequest* raw = owned.get();
+  reqs_.emplace(req.id, std::move(owned));
+  return *raw;
+}
+
 DevRequest& Context::create_request(const lmmsim::RequestSpec& req, const std::int32_t* text_ids,
                                     std::uint64_t payload_seed, cudaStream_t st) {
   if (find(req.id) != nullptr)
@@ -207,26 +240,15 @@ DevRequest& Context::create_request(const lmmsim::RequestSpec& req, const std::i
     pos += seg.tokens;
   }
   r.patches = patch;
-  mrope_ids(req, r.rope);
-  r.slot = take_request_slot();
   const std::int64_t pages = static_cast<std::int64_t>((r.total + kPageTokens - 1) / kPageTokens);
   std::vector<cudaEvent_t> guards;
   r.slot_pages = slab_pages_.take(pages, guards);
   for (cudaEvent_t g : guards) RS_CUDA_CHECK(cudaStreamWaitEvent(st, g, 0));
-  std::vector<cudaEvent_t> kv_guards;
-  r.kv_pages = kv_pages_.take(pages, kv_guards);
+  attach_kv(req, r, st);
 
   const std::size_t words = static_cast<std::size_t>((r.total + 31) / 32);
   RS_CUDA_CHECK(cudaMallocAsync(reinterpret_cast<void**>(&r.bitmap), words * 4, st));
   RS_CUDA_CHECK(cudaMemsetAsync(r.bitmap, 0, words * 4, st));
-  RS_CUDA_CHECK(cudaMallocAsync(reinterpret_cast<void**>(&r.kv_table),
-                                static_cast<std::size_t>(pages) * 4, st));
-  const void* kvt = up_.put(r.kv_pages.data(), r.kv_pages.size() * 4, st);
-  RS_CUDA_CHECK(cudaMemcpyAsync(r.kv_table, kvt, r.kv_pages.size() * 4, cudaMemcpyDeviceToDevice, st));
-  const void* ptr_src = up_.put(&r.kv_table, sizeof(int*), st);
-  RS_CUDA_CHECK(cudaMemcpyAsync(page_tables_dev_ + r.slot, ptr_src, sizeof(int*),
-                                cudaMemcpyDeviceToDevice, st));
-  page_tables_host_[static_cast<std::size_t>(r.slot)] = r.kv_table;
 
   // Text: readiness bits + K8 gather of the token embeddings into the slots.
   std::vector<std::uint64_t> ranges;
@@ -299,7 +321,7 @@ void Context::erase_request(lmmsim::RequestId id, cudaEvent_t guard, bool keep_s
   release_prefix(r, r.total, guard);
   kv_pages_.give(r.kv_pages, guard);
   if (guard != nullptr) RS_CUDA_CHECK(cudaStreamWaitEvent(tracker_, guard, 0));
-  RS_CUDA_CHECK(cudaFreeAsync(r.bitmap, tracker_));
+  if (r.bitmap != nullptr) RS_CUDA_CHECK(cudaFreeAsync(r.bitmap, tracker_));
   RS_CUDA_CHECK(cudaFreeAsync(r.kv_table, tracker_));
   if (!keep_slot) free_slots_.push_back(r.slot);
   reqs_.erase(it);

@@ -24,6 +24,11 @@ namespace rserve {
 
 constexpr int kPageTokens = 64;  // slot pages and KV pages
 
+/// Hash stream of the synthetic pixels of multimodal item `item` of request `req`.
+inline std::uint64_t pixel_stream(std::uint64_t req, std::uint64_t item) {
+  return (5ull << 32) | (req << 12) | item;
+}
+
 /// Free list of fixed-size pages; a freed page may carry the CUDA event
 /// after which it is safe to overwrite (its last reader's completion).
 class PagePool {
@@ -115,6 +120,9 @@ class Context {
   /// the K8 text gather (ids from host, or hashed on device when null).
   DevRequest& create_request(const lmmsim::RequestSpec& req, const std::int32_t* text_ids,
                              std::uint64_t payload_seed, cudaStream_t st);
+  /// Downstream pipeline stage: KV pages, page table and M-RoPE ids only
+  /// (no embedding slot, no bitmap).
+  DevRequest& create_kv_request(const lmmsim::RequestSpec& req, cudaStream_t st);
   DevRequest* find(lmmsim::RequestId id);
   DevRequest& get(lmmsim::RequestId id);
   /// K6: rows [n, d] (LLM order, items concatenated) -> slots; set bits.
@@ -153,6 +161,7 @@ class Context {
 
  private:
   int take_request_slot();
+  void attach_kv(const lmmsim::RequestSpec& req, DevRequest& r, cudaStream_t st);
   Shapes s_;
   rs_ctx_options opt_;
   DeviceArena arena_;

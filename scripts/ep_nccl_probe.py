@@ -1,0 +1,86 @@
+"""EP over the NCCL transport, one process per rank (gloo for plumbing).
+
+    python scripts/ep_nccl_probe.py [--world 2] [--same-device]
+
+With --same-device every rank uses cuda:0 (a single-GPU box); NCCL may
+refuse two ranks of one communicator on one GPU, which this probe reports.
+"""
+import argparse
+import os
+import socket
+import sys
+import time
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+WL = "0,0,-,T64|M256|M256|T32|M256|M256\n1,3.5,-,T40|M64|T8\n2,4,-,M128|T16\n"
+
+
+def rank_main(rank, world, port, same, q):
+    import torch.distributed as dist
+    from paper_2509_24381_b200 import api, ep_launch
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        stages, encoders = ep_launch.topology_for(world)
+        ids = ep_launch.share_link_ids(stages, encoders)
+        dev = 0 if same else rank
+        m = api.model_preset("tiny")
+        kw = dict(max_prompt_tokens=8192, slot_tokens=1 << 15, kv_tokens=1 << 15, max_chunk_tokens=2048,
+                  max_encode_tokens=1024)
+        ctx = api.ep_context(m, rank, stages, encoders, device=dev, **kw)
+        t0 = time.time()
+        g = api.EpGroup(stages, encoders, "nccl", rank=rank, device=dev, nccl_ids=ids)
+        init_s = time.time() - t0
+        sc = api.SimConfig(policy="rserve", stages=stages, encoder_workers=encoders, token_budget=384,
+                           embedding_batch_tokens=256, hidden_size=512,
+                           cost=api.CostModel(alpha_enc_ms=0.5, beta_enc_ms_per_token=0.01, eps_tx_ms=0.2,
+                                              zeta_tx_ms_per_token=0.001, delta_stage_ms_per_token=0.01))
+        out = None
+        for clock in ("lockstep", "real"):
+            if rank == 0:
+                dist.barrier()
+                log, journal, stats = g.run(ctx, None, WL, sc, clock=clock, payload_seed=7)
+                ok = log == api.simulate(WL, sc)[0] if clock == "lockstep" else True
+                out = dict(clock=clock, decisions_equal=ok, gpu_ms=stats["gpu_ms"],
+                           argmax={r: ctx.logits(r)[1] for r in (0, 1, 2)})
+                q.put((rank, init_s, out))
+            else:
+                g.worker_prepare(ctx, WL, payload_seed=7)
+                dist.barrier()
+                g.worker_run(ctx)
+        dist.barrier()
+        if rank != 0:
+            q.put((rank, init_s, "ok"))
+        g.close()
+        ctx.close()
+    except Exception as e:  # report, do not hang the other rank
+        q.put((rank, -1, f"{type(e).__name__}: {e}"))
+        raise
+    finally:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--world", type=int, default=2)
+    ap.add_argument("--same-device", action="store_true")
+    a = ap.parse_args()
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    procs = [ctx.Process(target=rank_main, args=(r, a.world, port, a.same_device, q)) for r in range(a.world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=300)
+    while not q.empty():
+        print(q.get())
+    print("exitcodes", [p.exitcode for p in procs])
+
+
+if __name__ == "__main__":
+    main()
