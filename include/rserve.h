@@ -253,10 +253,12 @@ typedef struct rs_ep rs_ep;
 typedef struct rs_ep_options {
   int32_t stages;      /* prefill ranks (>= 1)                               */
   int32_t encoders;    /* encoder ranks (>= 1)                               */
-  int32_t transport;   /* 0 loopback, 1 NCCL                                 */
-  int32_t rank;        /* NCCL: this process's rank; loopback: ignored       */
-  int32_t device;      /* NCCL: CUDA device of this rank                     */
+  int32_t transport;   /* 0 loopback, 1 NCCL, 2 CUDA-IPC peer memory         */
+  int32_t rank;        /* NCCL / IPC: this process's rank; loopback: ignored */
+  int32_t device;      /* CUDA device of this rank (loopback: of all ranks)  */
   const void* nccl_ids;/* NCCL: n_links x 128-byte ncclUniqueId, links order */
+  uint64_t slot_bytes; /* IPC: mailbox slot size (>= the largest message)    */
+  const char* shm_name;/* IPC: POSIX shm name shared by the group's ranks    */
 } rs_ep_options;
 /* Directed links (src, dst) of a topology, in creation order: pairs must
  * hold 2 * n entries (NULL: only *n_links is written).                    */
@@ -264,6 +266,11 @@ RS_API rs_status rs_ep_links(int32_t stages, int32_t encoders, int32_t* n_links,
 RS_API rs_status rs_nccl_unique_id(void* out128);
 RS_API rs_status rs_ep_create(const rs_ep_options* opt, rs_ep** out);
 RS_API rs_status rs_ep_destroy(rs_ep* ep);
+/* IPC only, after rs_ep_create on every rank: this rank's receive handles
+ * (mailboxes, events) -> blob; then connect with all ranks' blobs (rank
+ * order, exchanged by the caller's plumbing, e.g. torch.distributed).      */
+RS_API rs_status rs_ep_ipc_export(rs_ep* ep, void* out, uint64_t capacity, uint64_t* size);
+RS_API rs_status rs_ep_ipc_connect(rs_ep* ep, const void* blobs, const uint64_t* sizes, int32_t n);
 /* Worker ranks (NCCL): payloads of the run (encoders), then serve until P0
  * sends STOP at the end of its rs_ep_engine_run.                          */
 RS_API rs_status rs_ep_worker_prepare(rs_ep* ep, rs_ctx* ctx, const char* workload_text,

@@ -176,13 +176,16 @@ _sig("rs_debug_buffer", [C.c_void_p, C.c_char_p, C.POINTER(C.c_void_p), C.POINTE
 # EP disaggregation
 class rs_ep_options(C.Structure):
     _fields_ = [("stages", C.c_int32), ("encoders", C.c_int32), ("transport", C.c_int32),
-                ("rank", C.c_int32), ("device", C.c_int32), ("nccl_ids", C.c_void_p)]
+                ("rank", C.c_int32), ("device", C.c_int32), ("nccl_ids", C.c_void_p),
+                ("slot_bytes", C.c_uint64), ("shm_name", C.c_char_p)]
 
 
 _sig("rs_ep_links", [C.c_int32, C.c_int32, C.POINTER(C.c_int32), C.POINTER(C.c_int32)])
 _sig("rs_nccl_unique_id", [C.c_void_p])
 _sig("rs_ep_create", [C.POINTER(rs_ep_options), C.POINTER(C.c_void_p)])
 _sig("rs_ep_destroy", [C.c_void_p])
+_sig("rs_ep_ipc_export", [C.c_void_p, C.c_void_p, C.c_uint64, C.POINTER(C.c_uint64)])
+_sig("rs_ep_ipc_connect", [C.c_void_p, C.c_void_p, C.POINTER(C.c_uint64), C.c_int32])
 _sig("rs_ep_worker_prepare", [C.c_void_p, C.c_void_p, C.c_char_p, C.c_uint64, C.c_int32])
 _sig("rs_ep_worker_run", [C.c_void_p, C.c_void_p])
 _sig("rs_ep_engine_run", [C.c_void_p, C.c_void_p, C.POINTER(C.c_void_p), C.c_char_p,

@@ -383,23 +383,52 @@ def nccl_unique_id() -> bytes:
     return buf.raw
 
 
+def ep_slot_bytes(model: N.rs_model_config, max_chunk_tokens: int = 2048,
+                  max_encode_tokens: int = 2048) -> int:
+    """Largest EP message: a chunk residual, an encode batch's embeddings, a
+    logits row or a control message."""
+    d = model.llm_dim
+    return max(max_chunk_tokens * d * 2, max_encode_tokens * d * 2, model.vocab * 4, N.EP_CTRL_BYTES)
+
+
 class EpGroup:
-    """EP endpoints: `transport="loopback"` (every rank a thread of this
-    process — one GPU is enough) or `"nccl"` (this process is `rank`; the
-    ncclUniqueIds of all links come from rank 0, one per ep_links() entry)."""
+    """EP endpoints of one rank (or of all ranks, for loopback).
+
+    transport: "loopback" — every rank a thread of this process (one GPU is
+    enough); "ipc" — one process per rank, CUDA-IPC mailboxes in each
+    receiver's HBM written over NVLink (call connect() with all ranks' export()
+    blobs); "nccl" — one process per GPU, one 2-rank communicator per link
+    (`nccl_ids`: rank 0's ncclUniqueIds, one per ep_links() entry)."""
 
     def __init__(self, stages: int, encoders: int, transport: str = "loopback", rank: int = 0,
-                 device: int = 0, nccl_ids: Optional[bytes] = None):
-        self.stages, self.encoders = stages, encoders
+                 device: int = 0, nccl_ids: Optional[bytes] = None, slot_bytes: int = 0,
+                 shm_name: Optional[str] = None):
+        self.stages, self.encoders, self.transport = stages, encoders, transport
         o = N.rs_ep_options()
         o.stages, o.encoders = stages, encoders
-        o.transport = {"loopback": 0, "nccl": 1}[transport]
+        o.transport = {"loopback": 0, "nccl": 1, "ipc": 2}[transport]
         o.rank, o.device = rank, device
         self._ids = C.create_string_buffer(nccl_ids, len(nccl_ids)) if nccl_ids else None
         o.nccl_ids = C.cast(self._ids, C.c_void_p) if self._ids is not None else None
+        o.slot_bytes = slot_bytes
+        o.shm_name = shm_name.encode() if shm_name else None
         h = C.c_void_p()
         N.check(N.lib.rs_ep_create(C.byref(o), C.byref(h)))
         self.h = h
+
+    def export(self) -> bytes:
+        """IPC: this rank's receive handles."""
+        n = C.c_uint64()
+        N.check(N.lib.rs_ep_ipc_export(self.h, None, 0, C.byref(n)))
+        buf = C.create_string_buffer(max(1, n.value))
+        N.check(N.lib.rs_ep_ipc_export(self.h, buf, n.value, C.byref(n)))
+        return buf.raw[:n.value]
+
+    def connect(self, blobs: Sequence[bytes]):
+        """IPC: map the peers' mailboxes (blobs of all ranks, rank order)."""
+        sizes = (C.c_uint64 * len(blobs))(*[len(b) for b in blobs])
+        joined = b"".join(blobs)
+        N.check(N.lib.rs_ep_ipc_connect(self.h, joined, sizes, len(blobs)))
 
     def close(self):
         if self.h:

@@ -23,7 +23,6 @@ struct rs_ep {
   std::unique_ptr<ep::EncoderWorker> encoder;              // NCCL worker state
   std::unique_ptr<ep::StageWorker> stage;
   rs_ctx* worker_ctx = nullptr;
-  ep::Transport& mine() { return *endpoints.at(transport == 0 ? 0 : 0); }
 };
 
 namespace {
@@ -83,8 +82,14 @@ rs_status rs_ep_create(const rs_ep_options* opt, rs_ep** out) {
       if (opt->rank < 0 || opt->rank >= e->topo.world())
         throw lmmsim::ConfigError("ep.rank: outside [0, world)");
       e->endpoints.push_back(ep::make_nccl(e->topo, opt->rank, opt->device, opt->nccl_ids));
+    } else if (opt->transport == 2) {
+      if (opt->shm_name == nullptr || opt->slot_bytes == 0)
+        throw lmmsim::InputError("rs_ep_create: IPC needs shm_name and slot_bytes");
+      if (opt->rank < 0 || opt->rank >= e->topo.world())
+        throw lmmsim::ConfigError("ep.rank: outside [0, world)");
+      e->endpoints.push_back(ep::make_ipc(e->topo, opt->rank, opt->device, opt->slot_bytes, opt->shm_name));
     } else {
-      throw lmmsim::ConfigError("ep.transport: 0 (loopback) or 1 (NCCL)");
+      throw lmmsim::ConfigError("ep.transport: 0 (loopback), 1 (NCCL) or 2 (CUDA IPC)");
     }
     *out = e.release();
   });
@@ -94,11 +99,36 @@ rs_status rs_ep_destroy(rs_ep* e) {
   return guarded([&] { delete e; });
 }
 
+rs_status rs_ep_ipc_export(rs_ep* e, void* out, uint64_t capacity, uint64_t* size) {
+  return guarded([&] {
+    rs_ep& x = need_ep(e);
+    const std::vector<char> blob = ep::ipc_export(*x.endpoints.at(0));
+    if (size) *size = blob.size();
+    if (out != nullptr) {
+      if (capacity < blob.size()) throw lmmsim::InputError("rs_ep_ipc_export: buffer too small");
+      std::memcpy(out, blob.data(), blob.size());
+    }
+  });
+}
+
+rs_status rs_ep_ipc_connect(rs_ep* e, const void* blobs, const uint64_t* sizes, int32_t n) {
+  return guarded([&] {
+    rs_ep& x = need_ep(e);
+    std::vector<std::vector<char>> all;
+    const char* p = static_cast<const char*>(blobs);
+    for (int32_t i = 0; i < n; ++i) {
+      all.emplace_back(p, p + sizes[i]);
+      p += sizes[i];
+    }
+    ep::ipc_connect(*x.endpoints.at(0), all);
+  });
+}
+
 rs_status rs_ep_worker_prepare(rs_ep* e, rs_ctx* c, const char* workload_text, uint64_t seed, int32_t e2e) {
   return guarded([&] {
     rs_ep& x = need_ep(e);
     rs_ctx& ctx = need(c);
-    if (x.transport != 1) throw lmmsim::ConfigError("rs_ep_worker_prepare: NCCL transport only");
+    if (x.transport == 0) throw lmmsim::ConfigError("rs_ep_worker_prepare: multi-process transports only");
     if (x.rank == 0) throw lmmsim::ConfigError("rs_ep_worker_prepare: rank 0 runs the engine");
     x.stage.reset();
     x.encoder.reset();
@@ -128,7 +158,7 @@ rs_status rs_ep_engine_run(rs_ep* e, rs_ctx* p0, rs_ctx* const* workers, const c
   return guarded([&] {
     rs_ep& x = need_ep(e);
     rs_ctx& c0 = need(p0);
-    if (x.transport == 1 && x.rank != 0) throw lmmsim::ConfigError("rs_ep_engine_run: rank 0 only");
+    if (x.transport != 0 && x.rank != 0) throw lmmsim::ConfigError("rs_ep_engine_run: rank 0 only");
     std::vector<lmmsim::RequestSpec> wl = parse_workload_text(workload_text);
     lmmsim::SimConfig sc = to_sim_config(*cfg);
     sc.hidden_size = static_cast<std::uint32_t>(c0.ctx->shapes().d);

@@ -38,6 +38,24 @@ def share_link_ids(stages: int, encoders: int, device=None) -> bytes:
     return bytes(buf.cpu().numpy().tobytes())
 
 
+def connect_ipc(group: "api.EpGroup") -> None:
+    """Exchange the CUDA-IPC export blobs of all ranks and connect."""
+    import torch.distributed as dist
+    blobs = [None] * dist.get_world_size()
+    dist.all_gather_object(blobs, group.export())
+    group.connect(blobs)
+    dist.barrier()
+
+
+def shm_name_for_group() -> str:
+    """One POSIX shm name per EP group, drawn on rank 0."""
+    import os
+    import torch.distributed as dist
+    name = [f"/rserve_ep_{os.getpid()}_{os.urandom(4).hex()}" if dist.get_rank() == 0 else None]
+    dist.broadcast_object_list(name, src=0)
+    return name[0]
+
+
 def max_over_ranks(value: float, device=None) -> float:
     """Job time = the slowest rank's device time."""
     import torch

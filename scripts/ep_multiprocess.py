@@ -1,11 +1,13 @@
-"""EP over the NCCL transport, one process per rank (gloo for plumbing).
+"""EP across processes, one per rank (gloo for plumbing), over the NCCL or
+the CUDA-IPC transport.
 
-    python scripts/ep_nccl_probe.py [--world 2] [--same-device]
+    python scripts/ep_multiprocess.py [--world 2] [--same-device] [--transport ipc|nccl]
 
-With --same-device every rank uses cuda:0 (a single-GPU box); NCCL may
-refuse two ranks of one communicator on one GPU, which this probe reports.
+With --same-device every rank uses cuda:0 (a single-GPU box); NCCL refuses two
+ranks of one communicator on one GPU, CUDA IPC does not.
 """
 import argparse
+import json
 import os
 import socket
 import sys
@@ -16,21 +18,25 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 WL = "0,0,-,T64|M256|M256|T32|M256|M256\n1,3.5,-,T40|M64|T8\n2,4,-,M128|T16\n"
 
 
-def rank_main(rank, world, port, same, q):
+def rank_main(rank, world, port, same, transport, q):
     import torch.distributed as dist
     from paper_2509_24381_b200 import api, ep_launch
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         stages, encoders = ep_launch.topology_for(world)
-        ids = ep_launch.share_link_ids(stages, encoders)
         dev = 0 if same else rank
+        ids = ep_launch.share_link_ids(stages, encoders) if transport == "nccl" else None
+        shm = ep_launch.shm_name_for_group() if transport == "ipc" else None
         m = api.model_preset("tiny")
         kw = dict(max_prompt_tokens=8192, slot_tokens=1 << 15, kv_tokens=1 << 15, max_chunk_tokens=2048,
                   max_encode_tokens=1024)
         ctx = api.ep_context(m, rank, stages, encoders, device=dev, **kw)
         t0 = time.time()
-        g = api.EpGroup(stages, encoders, "nccl", rank=rank, device=dev, nccl_ids=ids)
+        g = api.EpGroup(stages, encoders, transport, rank=rank, device=dev, nccl_ids=ids,
+                        slot_bytes=api.ep_slot_bytes(m, 2048, 1024), shm_name=shm)
+        if transport == "ipc":
+            ep_launch.connect_ipc(g)
         init_s = time.time() - t0
         sc = api.SimConfig(policy="rserve", stages=stages, encoder_workers=encoders, token_budget=384,
                            embedding_batch_tokens=256, hidden_size=512,
@@ -42,7 +48,9 @@ def rank_main(rank, world, port, same, q):
                 dist.barrier()
                 log, journal, stats = g.run(ctx, None, WL, sc, clock=clock, payload_seed=7)
                 ok = log == api.simulate(WL, sc)[0] if clock == "lockstep" else True
-                out = dict(clock=clock, decisions_equal=ok, gpu_ms=stats["gpu_ms"],
+                out = dict(clock=clock, decisions_equal=ok, gpu_ms=stats["gpu_ms"], log=log,
+                           journal=journal,
+                           logits={r: ctx.logits(r)[0].tolist() for r in (0, 1, 2)},
                            argmax={r: ctx.logits(r)[1] for r in (0, 1, 2)})
                 q.put((rank, init_s, out))
             else:
@@ -65,6 +73,8 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--world", type=int, default=2)
     ap.add_argument("--same-device", action="store_true")
+    ap.add_argument("--transport", default="ipc", choices=["ipc", "nccl"])
+    ap.add_argument("--json", default=None, help="write the per-rank results here")
     a = ap.parse_args()
     import torch.multiprocessing as mp
     ctx = mp.get_context("spawn")
@@ -72,14 +82,24 @@ def main():
     with socket.socket() as s:
         s.bind(("127.0.0.1", 0))
         port = s.getsockname()[1]
-    procs = [ctx.Process(target=rank_main, args=(r, a.world, port, a.same_device, q)) for r in range(a.world)]
+    procs = [ctx.Process(target=rank_main, args=(r, a.world, port, a.same_device, a.transport, q)) for r in range(a.world)]
     for p in procs:
         p.start()
     for p in procs:
         p.join(timeout=300)
+    results = []
     while not q.empty():
-        print(q.get())
+        results.append(q.get())
+    for rank, init_s, out in results:
+        if isinstance(out, dict):
+            print(f"rank {rank} {out['clock']}: decisions_equal={out['decisions_equal']} "
+                  f"gpu_ms={out['gpu_ms']:.3f} argmax={out['argmax']} init_s={init_s:.2f}")
+        else:
+            print(f"rank {rank}: {out}")
     print("exitcodes", [p.exitcode for p in procs])
+    if a.json:
+        with open(a.json, "w") as f:
+            json.dump(dict(results=results, exitcodes=[p.exitcode for p in procs]), f)
 
 
 if __name__ == "__main__":
