@@ -18,6 +18,8 @@
 #include <unistd.h>
 
 #include <atomic>
+#include <cstdio>
+#include <cstdlib>
 #include <chrono>
 #include <cstring>
 #include <mutex>
@@ -30,6 +32,22 @@ namespace rserve::ep {
 namespace {
 
 constexpr int kSlots = 4;
+
+bool trace_on() {
+  static const bool on = [] {
+    const char* v = std::getenv("RS_EP_TRACE");
+    return v != nullptr && v[0] == '1';
+  }();
+  return on;
+}
+#define EP_TRACE(...)                         \
+  do {                                        \
+    if (trace_on()) {                         \
+      std::fprintf(stderr, "[ep r%d] ", rank_); \
+      std::fprintf(stderr, __VA_ARGS__);      \
+      std::fprintf(stderr, "\n");             \
+    }                                         \
+  } while (0)
 
 struct alignas(64) Counter {
   std::atomic<std::uint64_t> v;
@@ -153,6 +171,7 @@ class IpcTransport final : public Transport {
       }
     }
     connected_ = true;
+    EP_TRACE("connected (%zu links)", links_.size());
     // Receives posted by this rank are drained even while its main thread
     // is blocked in send() on a full ring: that is what keeps a
     // P0 <-> worker pair from waiting on each other.
@@ -184,6 +203,7 @@ class IpcTransport final : public Transport {
       throw DeviceError(RS_ERR_CUDA, "ipc: message of " + std::to_string(bytes) + " bytes > slot of " +
                                          std::to_string(slot_bytes_));
     const std::uint64_t k = e.seq++;  // the send side of a link is one thread's
+    EP_TRACE("send l%d -> %d msg %llu bytes %zu", l, peer, static_cast<unsigned long long>(k), bytes);
     const int slot = static_cast<int>(k % kSlots);
     ShmLink& s = shm_[l];
     // Slot reuse: the receiver must have consumed message k - kSlots (spin
@@ -276,6 +296,7 @@ class IpcTransport final : public Transport {
       if (s.sent.v.load(std::memory_order_acquire) <= k) return;
       std::shared_ptr<Xfer> x = e.pending.front();
       const int slot = static_cast<int>(k % kSlots);
+      EP_TRACE("recv l%d <- %d msg %llu bytes %zu", l, x->peer, static_cast<unsigned long long>(k), x->bytes);
       if (s.bytes[slot] != x->bytes)
         throw DeviceError(RS_ERR_CUDA, "ipc: message of " + std::to_string(s.bytes[slot]) +
                                            " bytes for a receive of " + std::to_string(x->bytes));
