@@ -19,6 +19,8 @@ WL = "0,0,-,T64|M256|M256|T32|M256|M256\n1,3.5,-,T40|M64|T8\n2,4,-,M128|T16\n"
 
 
 def rank_main(rank, world, port, same, transport, q):
+    import faulthandler
+    faulthandler.dump_traceback_later(float(os.environ.get("RS_EP_WATCHDOG", "0")) or 1e9, exit=True)
     import torch.distributed as dist
     from paper_2509_24381_b200 import api, ep_launch
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
@@ -32,18 +34,21 @@ def rank_main(rank, world, port, same, transport, q):
         kw = dict(max_prompt_tokens=8192, slot_tokens=1 << 15, kv_tokens=1 << 15, max_chunk_tokens=2048,
                   max_encode_tokens=1024)
         ctx = api.ep_context(m, rank, stages, encoders, device=dev, **kw)
+        print(f"rank {rank}: context ready", flush=True)
         t0 = time.time()
         g = api.EpGroup(stages, encoders, transport, rank=rank, device=dev, nccl_ids=ids,
                         slot_bytes=api.ep_slot_bytes(m, 2048, 1024), shm_name=shm)
         if transport == "ipc":
             ep_launch.connect_ipc(g)
         init_s = time.time() - t0
+        print(f"rank {rank}: transport connected in {init_s:.2f}s", flush=True)
         sc = api.SimConfig(policy="rserve", stages=stages, encoder_workers=encoders, token_budget=384,
                            embedding_batch_tokens=256, hidden_size=512,
                            cost=api.CostModel(alpha_enc_ms=0.5, beta_enc_ms_per_token=0.01, eps_tx_ms=0.2,
                                               zeta_tx_ms_per_token=0.001, delta_stage_ms_per_token=0.01))
         out = None
         for clock in ("lockstep", "real"):
+            print(f"rank {rank}: {clock} run", flush=True)
             if rank == 0:
                 dist.barrier()
                 log, journal, stats = g.run(ctx, None, WL, sc, clock=clock, payload_seed=7)
@@ -85,11 +90,23 @@ def main():
     procs = [ctx.Process(target=rank_main, args=(r, a.world, port, a.same_device, a.transport, q)) for r in range(a.world)]
     for p in procs:
         p.start()
-    for p in procs:
-        p.join(timeout=300)
+    # Drain the queue before joining: a child blocks at exit until its queued
+    # results are written to the pipe.
     results = []
-    while not q.empty():
-        results.append(q.get())
+    expected = 2 + (a.world - 1)  # rank 0: one per clock; workers: one each
+    import queue
+    while len(results) < expected:
+        try:
+            results.append(q.get(timeout=300))
+        except queue.Empty:
+            break
+        if any(isinstance(o, str) and o != "ok" for _, _, o in results):
+            break
+    for p in procs:
+        p.join(timeout=60)
+        if p.is_alive():  # our own child: stop it rather than hang the caller
+            p.kill()
+            p.join()
     for rank, init_s, out in results:
         if isinstance(out, dict):
             print(f"rank {rank} {out['clock']}: decisions_equal={out['decisions_equal']} "
