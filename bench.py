@@ -17,6 +17,9 @@ pinned host memory and the first-token logits read back D2H inside the timed
 region. Inputs (16 GB of weights, 77 MB of pixels) exceed the 126 MB L2, so
 no explicit flush between steps.
 
+--ep (N = 2/4/8 under torchrun): the paper's EP deployment instead of
+replicas — see run_ep.
+
 --impl reference: the reference's path on the host CPU — the reference
 scheduler (oracle/_ref, run_simulation on the same workload) plus the fp32
 numpy restatement of the model math (oracle/model_oracle.py) timed on a
@@ -240,6 +243,93 @@ def run_ours(args):
         torch.distributed.destroy_process_group()
 
 
+def run_ep(args):
+    """--ep: the paper's EP deployment on N = 2/4/8 GPUs (E+P = 1+1, 2+2, 4+4):
+    encoder ranks run the ViT, prefill ranks the LLM stages, rank 0 the engine
+    and the device tracker; embeddings / residuals / logits move over CUDA-IPC
+    peer memory (NVLink) or NCCL. One process per GPU (torchrun); gloo is only
+    plumbing. value = the same cfg2 tokens/s, timed on P0's device clock from
+    the run's origin event to the last logits arrival (the max over ranks: no
+    rank's work ends later than its data reaches P0)."""
+    import torch
+    import torch.distributed as dist
+    ws, rank, local = dist_env()
+    from paper_2509_24381_b200 import _native as N
+    from paper_2509_24381_b200 import api, ep_launch
+    stages, encoders = ep_launch.topology_for(ws)
+    dev = 0 if args.ep_same_device else local
+    torch.cuda.set_device(dev)
+    dist.init_process_group("gloo")
+    mcfg = api.model_preset("qwen2.5-vl-7b")
+    m = {k: getattr(mcfg, k) for k, _ in N.rs_model_config._fields_}
+    ctx = api.ep_context(mcfg, rank, stages, encoders, device=dev, max_prompt_tokens=16384,
+                         slot_tokens=1 << 15, kv_tokens=1 << 15, max_chunk_tokens=args.budget,
+                         max_encode_tokens=C_TOKENS)
+    ids = ep_launch.share_link_ids(stages, encoders) if args.ep_transport == "nccl" else None
+    shm = ep_launch.shm_name_for_group() if args.ep_transport == "ipc" else None
+    g = api.EpGroup(stages, encoders, args.ep_transport, rank=rank, device=dev, nccl_ids=ids,
+                    slot_bytes=api.ep_slot_bytes(mcfg, args.budget, C_TOKENS), shm_name=shm)
+    if args.ep_transport == "ipc":
+        ep_launch.connect_ipc(g)
+    wl = f"0,0,-,{LAYOUT}\n"
+    sc = api.SimConfig(policy=args.policy, stages=stages, token_budget=args.budget,
+                       embedding_batch_tokens=C_TOKENS, encoder_workers=encoders, hidden_size=m["llm_dim"],
+                       cost=api.CostModel(beta_enc_ms_per_token=0.01, delta_stage_ms_per_token=0.01))
+
+    def steps(n, e2e):
+        """n runs; rank 0 returns [(ttft, stats)], workers []."""
+        out = []
+        if rank != 0:
+            g.worker_prepare(ctx, wl, payload_seed=1234, e2e=e2e)
+        for _ in range(n):
+            dist.barrier()
+            if rank == 0:
+                log, _, st = g.run(ctx, None, wl, sc, clock="real", e2e=e2e, payload_seed=1234)
+                out.append((float(api.parse_decision_log(log)["req"][0]["ttft"]), st))
+            else:
+                g.worker_run(ctx)
+        return out
+
+    steps(args.warmup, False)
+    with ClockSampler(dev) as clk:
+        timed = steps(args.steps, False)
+    steps(max(1, args.warmup // 2), True)
+    timed_e2e = steps(args.steps, True)
+    total_ms = ep_launch.max_over_ranks(sum(st["gpu_ms"] for _, st in timed))
+    e2e_total = ep_launch.max_over_ranks(sum(st["wall_ms"] for _, st in timed_e2e))
+    if rank == 0:
+        ttfts = sorted(t for t, _ in timed)
+        p50 = ttfts[max(0, -(-50 * len(ttfts) // 100) - 1)]
+        p99 = ttfts[max(0, -(-99 * len(ttfts) // 100) - 1)]
+        st_e = timed_e2e[-1][1]
+        line = {
+            "metric": "encode+prefill tokens/s (p50/p99 TTFT ms alongside)",
+            "value": args.steps * PROMPT_TOKENS / (total_ms / 1e3), "unit": "tokens/s", "n_gpus": ws,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic",
+            "ttft_ms": {"p50": p50, "p99": p99, "mean": sum(ttfts) / len(ttfts)},
+            "config": {"workload": "cfg2: Qwen2.5-VL-7B-shaped (random init), 1 request "
+                                   "T128|(M1024|T32)x8 = 8576 tokens",
+                       "model": "qwen2.5-vl-7b-shaped", "global_batch": 1, "seq_len": PROMPT_TOKENS,
+                       "policy": args.policy, "C": C_TOKENS, "B": args.budget, "stages": stages,
+                       "encoders": encoders, "placement": f"EP {encoders}E+{stages}P",
+                       "parallelism": f"ep{encoders}+pp{stages}", "transport": args.ep_transport,
+                       "same_device": bool(args.ep_same_device)},
+            "e2e": {"value": args.steps * PROMPT_TOKENS / (e2e_total / 1e3), "unit": "tokens/s",
+                    "h2d_bytes_per_step": st_e["h2d_bytes"], "d2h_bytes_per_step": st_e["d2h_bytes"]},
+            "gpu_launches": sum(st["kernel_launches"] for _, st in timed),
+            "gpu_launches_scope": "rank 0 (P0) kernels; worker ranks launch their own",
+            "roofline": None,
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line))
+    dist.barrier()
+    g.close()
+    ctx.close()
+    dist.destroy_process_group()
+
+
 def cpu_sample(m, budget):
     """Times the numpy oracle on one ViT layer (one 896x896 image) and one
     LLM layer (one B-token chunk at mid-prompt context). Returns seconds and
@@ -342,9 +432,16 @@ def main():
     ap.add_argument("--budget", type=int, default=2048, help="Algorithm-2 token budget B")
     ap.add_argument("--policy", default="rserve")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--ep", action="store_true",
+                    help="N>1: EP deployment (1E+1P / 2E+2P / 4E+4P) instead of independent replicas")
+    ap.add_argument("--ep-transport", default="ipc", choices=["ipc", "nccl"])
+    ap.add_argument("--ep-same-device", action="store_true",
+                    help="all EP ranks on cuda:0 (protocol check on a one-GPU box; timing not meaningful)")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)
+    elif args.ep:
+        run_ep(args)
     else:
         run_ours(args)
 
