@@ -282,6 +282,16 @@ RS_API rs_status rs_ep_engine_run(rs_ep* ep, rs_ctx* p0, rs_ctx* const* workers,
                                   const char* workload_text, const rs_sim_config* cfg,
                                   const rs_run_options* opt, char** out_result,
                                   char** out_journal, rs_run_stats* out_stats);
+/* Engine-backed experiment cell (the device counterpart of
+ * rs_experiment_cell / experiment.hpp run_cell): generates the workload of
+ * `wcfg`, runs it through the device engine — co-located on `ctx` (ep NULL)
+ * or EP with `ctx` as P0 — and returns the report CSV row (metrics.hpp
+ * report_csv_row) plus the Chrome trace (trace_to_json_text) whose spans
+ * are the engine's op launches and their CUDA-event completions.       */
+RS_API rs_status rs_engine_cell(rs_ctx* ctx, rs_ep* ep, rs_ctx* const* workers,
+                                const rs_workload_config* wcfg, const rs_sim_config* cfg,
+                                double slo_ttft_ms, const rs_run_options* opt,
+                                char** out_csv_row, char** out_trace_json, rs_run_stats* out_stats);
 /* Control-message codec (host only): text form <-> the 32 KB wire message. */
 RS_API rs_status rs_ep_ctrl_pack(const char* text, void* out_msg, uint64_t msg_bytes);
 RS_API rs_status rs_ep_ctrl_unpack(const void* msg, uint64_t msg_bytes, char** out_text);

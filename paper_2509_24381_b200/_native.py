@@ -191,6 +191,9 @@ _sig("rs_ep_worker_run", [C.c_void_p, C.c_void_p])
 _sig("rs_ep_engine_run", [C.c_void_p, C.c_void_p, C.POINTER(C.c_void_p), C.c_char_p,
                           C.POINTER(rs_sim_config), C.POINTER(rs_run_options), PCHAR, PCHAR,
                           C.POINTER(rs_run_stats)])
+_sig("rs_engine_cell", [C.c_void_p, C.c_void_p, C.POINTER(C.c_void_p), C.POINTER(rs_workload_config),
+                        C.POINTER(rs_sim_config), C.c_double, C.POINTER(rs_run_options), PCHAR, PCHAR,
+                        C.POINTER(rs_run_stats)])
 _sig("rs_ep_ctrl_pack", [C.c_char_p, C.c_void_p, C.c_uint64])
 _sig("rs_ep_ctrl_unpack", [C.c_void_p, C.c_uint64, PCHAR])
 EP_CTRL_BYTES = 4096 * 8

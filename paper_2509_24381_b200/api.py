@@ -466,3 +466,22 @@ class EpGroup:
 
     def worker_run(self, ctx: "Pipeline"):
         N.check(N.lib.rs_ep_worker_run(self.h, ctx.h))
+
+
+def engine_cell(ctx: "Pipeline", wcfg: WorkloadConfig, cfg: SimConfig, slo_ttft_ms: Optional[float] = None,
+                clock: str = "real", payload_seed: int = 7, ep: Optional[EpGroup] = None,
+                workers: Optional[Sequence["Pipeline"]] = None) -> Tuple[str, str, Dict]:
+    """One experiment cell on the device engine: the report CSV
+    row of experiment_cell() and the Chrome trace, from measured completions
+    (clock="real") or the cost model's event order (clock="lockstep")."""
+    o = N.rs_run_options()
+    o.clock = 1 if clock == "real" else 0
+    o.payload_seed = payload_seed
+    arr = (C.c_void_p * len(workers))(*[w.h.value for w in workers]) if workers else None
+    row, trace = _out(), _out()
+    st = N.rs_run_stats()
+    (wc, _keep), c = wcfg.to_c(), cfg.to_c()
+    N.check(N.lib.rs_engine_cell(ctx.h, ep.h if ep is not None else None, arr, C.byref(wc), C.byref(c),
+                                 -1.0 if slo_ttft_ms is None else slo_ttft_ms, C.byref(o),
+                                 C.byref(row), C.byref(trace), C.byref(st)))
+    return N.take_string(row), N.take_string(trace), {k: getattr(st, k) for k, _ in N.rs_run_stats._fields_}

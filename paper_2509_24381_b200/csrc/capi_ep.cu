@@ -10,6 +10,8 @@
 #include "host/config_bridge.hpp"
 #include "host/decision_log.hpp"
 #include "host/status.hpp"
+#include "lmmsim/metrics.hpp"
+#include "lmmsim/workload.hpp"
 
 using namespace rserve;
 
@@ -152,68 +154,117 @@ rs_status rs_ep_worker_run(rs_ep* e, rs_ctx* c) {
   });
 }
 
+}  // extern "C"
+
+namespace {
+struct EngineOutputs {
+  lmmsim::SimResult res;
+  std::vector<ReleaseRecord> releases;
+  std::string journal;
+  rs_run_stats stats{};
+};
+
+/// One engine run on the device: co-located on `c0` (ep == nullptr) or EP
+/// with `c0` as P0 (loopback worker ranks run on threads of this call).
+EngineOutputs run_engine(rs_ctx& c0, rs_ep* ep, rs_ctx* const* workers, std::vector<lmmsim::RequestSpec> wl,
+                         lmmsim::SimConfig sc, const rs_run_options* opt) {
+  sc.hidden_size = static_cast<std::uint32_t>(c0.ctx->shapes().d);
+  const bool realtime = opt != nullptr && opt->clock == 1;
+  const bool e2e = opt != nullptr && opt->e2e != 0;
+  const bool serialize = opt != nullptr && opt->serialize != 0;
+  const std::uint64_t seed = opt ? opt->payload_seed : 0;
+  EngineOutputs out;
+  auto finish = [&](DeviceBackend& backend, lmmsim::PipelineEngine& engine) {
+    backend.collect();
+    for (const auto& [id, row] : backend.logits()) c0.logits[id] = row;
+    for (const auto& [id, am] : backend.argmax()) c0.argmax[id] = am;
+    for (const lmmsim::ReleaseEvent& ev : engine.releases()) out.releases.push_back({ev.chunk, ev.id, ev.range});
+    out.journal = render_journal(engine.journal());
+    out.stats = backend.stats();
+  };
+  if (ep == nullptr) {
+    DeviceBackend backend(*c0.ctx, sc, realtime, e2e, seed, serialize);
+    backend.prepare(wl);
+    lmmsim::PipelineEngine engine(wl, sc, backend);
+    backend.start();
+    out.res = engine.run();
+    finish(backend, engine);
+    return out;
+  }
+  rs_ep& x = *ep;
+  if (x.transport != 0 && x.rank != 0) throw lmmsim::ConfigError("EP engine run: rank 0 only");
+  // Loopback: worker ranks are threads of this call.
+  std::vector<std::thread> threads;
+  std::vector<std::exception_ptr> errors(static_cast<std::size_t>(x.topo.world()));
+  if (x.transport == 0) {
+    if (workers == nullptr) throw lmmsim::InputError("EP engine run: loopback needs worker contexts");
+    for (int r = 1; r < x.topo.world(); ++r) {
+      rs_ctx& wc = need(workers[r - 1]);
+      threads.emplace_back([&x, &wc, &wl, &errors, r, seed, e2e] {
+        try {
+          run_worker(x, *x.endpoints[static_cast<std::size_t>(r)], r, wc, wl, seed, e2e);
+        } catch (...) {
+          errors[static_cast<std::size_t>(r)] = std::current_exception();
+        }
+      });
+    }
+  }
+  ep::Transport& t = *x.endpoints[0];
+  ep::Remote remote{&t, x.topo};
+  try {
+    DeviceBackend backend(*c0.ctx, sc, realtime, e2e, seed, serialize, &remote);
+    backend.prepare(wl);
+    lmmsim::PipelineEngine engine(wl, sc, backend);
+    backend.start();
+    out.res = engine.run();
+    ep::stop_workers(t, x.topo);
+    for (auto& th : threads) th.join();
+    threads.clear();
+    finish(backend, engine);
+  } catch (...) {
+    if (!threads.empty()) {  // unblock the worker threads before propagating
+      try {
+        ep::stop_workers(t, x.topo);
+      } catch (...) {
+      }
+      for (auto& th : threads) th.join();
+    }
+    throw;
+  }
+  for (auto& err : errors)
+    if (err) std::rethrow_exception(err);
+  return out;
+}
+}  // namespace
+
+extern "C" {
+
 rs_status rs_ep_engine_run(rs_ep* e, rs_ctx* p0, rs_ctx* const* workers, const char* workload_text,
                            const rs_sim_config* cfg, const rs_run_options* opt, char** out_result,
                            char** out_journal, rs_run_stats* out_stats) {
   return guarded([&] {
     rs_ep& x = need_ep(e);
-    rs_ctx& c0 = need(p0);
-    if (x.transport != 0 && x.rank != 0) throw lmmsim::ConfigError("rs_ep_engine_run: rank 0 only");
-    std::vector<lmmsim::RequestSpec> wl = parse_workload_text(workload_text);
-    lmmsim::SimConfig sc = to_sim_config(*cfg);
-    sc.hidden_size = static_cast<std::uint32_t>(c0.ctx->shapes().d);
-    const bool realtime = opt != nullptr && opt->clock == 1;
-    const bool e2e = opt != nullptr && opt->e2e != 0;
-    const std::uint64_t seed = opt ? opt->payload_seed : 0;
+    EngineOutputs o = run_engine(need(p0), &x, workers, parse_workload_text(workload_text), to_sim_config(*cfg), opt);
+    if (out_result) *out_result = c_string(render_decision_log(o.res, o.releases, true));
+    if (out_journal) *out_journal = c_string(o.journal);
+    if (out_stats) *out_stats = o.stats;
+  });
+}
 
-    // Loopback: worker ranks are threads of this call.
-    std::vector<std::thread> threads;
-    std::vector<std::exception_ptr> errors(static_cast<std::size_t>(x.topo.world()));
-    if (x.transport == 0) {
-      if (workers == nullptr) throw lmmsim::InputError("rs_ep_engine_run: loopback needs worker contexts");
-      for (int r = 1; r < x.topo.world(); ++r) {
-        rs_ctx& wc = need(workers[r - 1]);
-        threads.emplace_back([&x, &wc, &wl, &errors, r, seed, e2e] {
-          try {
-            run_worker(x, *x.endpoints[static_cast<std::size_t>(r)], r, wc, wl, seed, e2e);
-          } catch (...) {
-            errors[static_cast<std::size_t>(r)] = std::current_exception();
-          }
-        });
-      }
-    }
-    ep::Transport& t = *x.endpoints[0];
-    ep::Remote remote{&t, x.topo};
-    try {
-      DeviceBackend backend(*c0.ctx, sc, realtime, e2e, seed, false, &remote);
-      backend.prepare(wl);
-      lmmsim::PipelineEngine engine(wl, sc, backend);
-      backend.start();
-      const lmmsim::SimResult res = engine.run();
-      ep::stop_workers(t, x.topo);
-      for (auto& th : threads) th.join();
-      threads.clear();
-      backend.collect();
-      for (const auto& [id, row] : backend.logits()) c0.logits[id] = row;
-      for (const auto& [id, am] : backend.argmax()) c0.argmax[id] = am;
-      std::vector<ReleaseRecord> rel;
-      for (const lmmsim::ReleaseEvent& ev : engine.releases()) rel.push_back({ev.chunk, ev.id, ev.range});
-      if (out_result) *out_result = c_string(render_decision_log(res, rel, true));
-      if (out_journal) *out_journal = c_string(render_journal(engine.journal()));
-      if (out_stats) *out_stats = backend.stats();
-    } catch (...) {
-      // Unblock the worker threads before propagating.
-      if (!threads.empty()) {
-        try {
-          ep::stop_workers(t, x.topo);
-        } catch (...) {
-        }
-        for (auto& th : threads) th.join();
-      }
-      throw;
-    }
-    for (auto& err : errors)
-      if (err) std::rethrow_exception(err);
+rs_status rs_engine_cell(rs_ctx* ctx, rs_ep* ep, rs_ctx* const* workers, const rs_workload_config* wcfg,
+                         const rs_sim_config* cfg, double slo_ttft_ms, const rs_run_options* opt,
+                         char** out_csv_row, char** out_trace_json, rs_run_stats* out_stats) {
+  return guarded([&] {
+    if (wcfg == nullptr || cfg == nullptr) throw lmmsim::InputError("rs_engine_cell: null config");
+    const lmmsim::SimConfig sc = to_sim_config(*cfg);
+    EngineOutputs o = run_engine(need(ctx), ep, workers, lmmsim::generate_workload(to_workload_config(*wcfg)), sc, opt);
+    std::optional<double> slo;
+    if (slo_ttft_ms >= 0) slo = slo_ttft_ms;
+    const lmmsim::MetricsReport rep = lmmsim::compute_report(o.res, slo);
+    if (out_csv_row)
+      *out_csv_row = c_string(lmmsim::report_csv_row(lmmsim::to_string(sc.policy), wcfg->arrival_rate, wcfg->seed, rep));
+    if (out_trace_json) *out_trace_json = c_string(lmmsim::trace_to_json_text(o.res));
+    if (out_stats) *out_stats = o.stats;
   });
 }
 
