@@ -51,7 +51,7 @@ def test_lockstep_cells_equal_golden_rows(fig7, tiny, policy):
         row, trace, st = api.engine_cell(tiny, wl, sim, slo, clock="lockstep")
         assert row == index[(policy, rate, seed)]
         assert st["kernel_launches"] > 0
-        ev = json.loads(trace)["traceEvents"]
+        ev = json.loads(trace)
         assert any(e.get("name", "").startswith("encode_") for e in ev)
         assert any(e.get("name", "").startswith("chunk") for e in ev)
 
@@ -63,7 +63,7 @@ def test_realclock_cell_and_trace(fig7, tiny):
     row, trace, st = api.engine_cell(tiny, wl, sim, slo, clock="real")
     f = row.split(",")
     assert f[0] == "rserve" and float(f[3]) > 0 and float(f[7]) > 0
-    ev = json.loads(trace)["traceEvents"]
+    ev = json.loads(trace)
     spans = [e for e in ev if e.get("ph") == "X"]
     assert spans and all(e["dur"] >= 0 for e in spans)
     # measured spans: the device did the work, so stage spans have real duration
