@@ -46,7 +46,7 @@ def main():
         seeds = [int(s) for s in a.seeds.split(",")]
     m = api.model_preset(a.model)
     sim.hidden_size = m.llm_dim
-    kw = dict(max_prompt_tokens=1 << 15, slot_tokens=1 << 19, kv_tokens=1 << 19, max_chunk_tokens=max(2048, sim.token_budget),
+    kw = dict(max_prompt_tokens=1 << 15, slot_tokens=1 << 19, kv_tokens=1 << 19, max_chunk_tokens=max(8192, sim.token_budget),
               max_encode_tokens=4096)
     ep = workers = None
     if a.ep:

@@ -13,7 +13,9 @@ pytestmark = pytest.mark.gpu
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 GOLDEN = os.path.join(ROOT, "tests", "golden")
-KW = dict(max_prompt_tokens=1 << 15, slot_tokens=1 << 19, kv_tokens=1 << 19, max_chunk_tokens=2048,
+# whole-prompt policies (vanilla_pp) prefill a request in one chunk: size the
+# chunk buffers for the longest fig7 prompt
+KW = dict(max_prompt_tokens=1 << 15, slot_tokens=1 << 19, kv_tokens=1 << 19, max_chunk_tokens=8192,
           max_encode_tokens=4096)
 
 
