@@ -129,7 +129,10 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     const AttnBlock b = p.blocks[blockIdx.x];
     q_row0 = b.q_row0;
     q_rows = b.q_rows;
-    key_begin = b.key_begin;
+    // The V^T tile is a TMA load along the key dimension, whose start must be
+    // 16-byte aligned: start at a multiple of 8 keys. The extra leading keys
+    // belong to the previous sequence and are masked by the per-row [lo, hi).
+    key_begin = b.key_begin & ~7;
     key_end = b.key_end;
   }
   const int n_keys = key_end - key_begin;

@@ -95,6 +95,22 @@ def _engine_cfg(policy, C, B=512, stages=1):
 @pytest.mark.parametrize("policy,C,B,stages", [("rserve", 256, 512, 1), ("intra_only", 256, 256, 1),
                                                ("epd_baseline", 256, 512, 1), ("vanilla_pp", 256, 512, 1),
                                                ("rserve", 512, 128, 2)])
+def test_vit_odd_item_batches(tiny, oracle_tiny):
+    """Batches of items with odd token counts: item / window starts in the
+    packed patch sequence are not multiples of 8 (TMA alignment of the V^T
+    tile) and merged grids are 1 x prime."""
+    mo, cfg, w = oracle_tiny
+    vis = mo.VisionOracle(cfg, w)
+    for sizes in ([251, 349, 300], [349, 251], [251, 251, 251], [7, 1, 263]):
+        items = [(n, vis.patches(3, 1, i, n)) for i, n in enumerate(sizes)]
+        pt = torch.from_numpy(np.concatenate([x for _, x in items])).to(torch.bfloat16).cuda()
+        out = torch.empty(sum(sizes), cfg.llm_dim, dtype=torch.bfloat16, device="cuda")
+        ranges = [(sum(sizes[:i]), sum(sizes[:i + 1])) for i in range(len(sizes))]
+        tiny.encode(ranges, pt.data_ptr(), on_host=False, out_ptr=out.data_ptr())
+        torch.cuda.synchronize()
+        _check_emb(out.float().cpu().numpy(), vis.encode(items), 0.999)
+
+
 def test_engine_lockstep_decisions_and_logits(tiny, oracle_tiny, policy, C, B, stages):
     from oracle import ref
     from paper_2509_24381_b200 import api

@@ -167,7 +167,9 @@ def test_attention_prefill_tcgen05(nat, hd, hq, hkv, pos0, rows):
 @pytest.mark.parametrize("tc", [False, True])
 @pytest.mark.parametrize("hd,heads,lens", [(80, 4, [64, 64, 37, 64]), (80, 2, [1024, 300]),
                                            (64, 4, [256, 256, 5]), (128, 2, [130, 1]),
-                                           (80, 16, [64] * 40 + [16, 48])])
+                                           (80, 16, [64] * 40 + [16, 48]),
+                                           # sequence starts that are not multiples of 8 keys
+                                           (80, 4, [1004, 1396, 1200]), (64, 2, [4, 124, 12, 300])])
 def test_attention_varlen_bidir(nat, hd, heads, lens, tc):
     total = sum(lens)
     qkv = torch.randn(total, 3 * heads * hd, device="cuda", dtype=torch.bfloat16)
