@@ -92,9 +92,6 @@ def _engine_cfg(policy, C, B=512, stages=1):
                                                              delta_stage_ms_per_token=0.01))
 
 
-@pytest.mark.parametrize("policy,C,B,stages", [("rserve", 256, 512, 1), ("intra_only", 256, 256, 1),
-                                               ("epd_baseline", 256, 512, 1), ("vanilla_pp", 256, 512, 1),
-                                               ("rserve", 512, 128, 2)])
 def test_vit_odd_item_batches(tiny, oracle_tiny):
     """Batches of items with odd token counts: item / window starts in the
     packed patch sequence are not multiples of 8 (TMA alignment of the V^T
@@ -111,6 +108,9 @@ def test_vit_odd_item_batches(tiny, oracle_tiny):
         _check_emb(out.float().cpu().numpy(), vis.encode(items), 0.999)
 
 
+@pytest.mark.parametrize("policy,C,B,stages", [("rserve", 256, 512, 1), ("intra_only", 256, 256, 1),
+                                               ("epd_baseline", 256, 512, 1), ("vanilla_pp", 256, 512, 1),
+                                               ("rserve", 512, 128, 2)])
 def test_engine_lockstep_decisions_and_logits(tiny, oracle_tiny, policy, C, B, stages):
     from oracle import ref
     from paper_2509_24381_b200 import api
