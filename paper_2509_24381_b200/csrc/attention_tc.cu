@@ -112,13 +112,16 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   std::uint32_t* tmem_holder = reinterpret_cast<std::uint32_t*>(o_full + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int head = blockIdx.y;
+  // grid (heads, blocks): heads vary fastest, so blocks issue in work-list
+  // order — callers list the most expensive (most keys) first, which makes
+  // the hardware's in-order block dispatch an LPT schedule over the SMs.
+  const int head = blockIdx.x;
   const int kvh = head / (p.q_heads / p.kv_heads);
   int q_row0, q_rows, key_begin, key_end;
   const int* pt = nullptr;
   int q_pos0 = 0;
   if constexpr (MODE == KvMode::kPaged) {
-    const PrefillWork w = p.work[blockIdx.x];
+    const PrefillWork w = p.work[blockIdx.y];
     q_row0 = w.q_row0;
     q_rows = w.q_rows;
     q_pos0 = w.q_pos0;
@@ -126,7 +129,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     key_end = w.q_pos0 + w.q_rows;
     pt = p.page_tables[w.req_slot];
   } else {
-    const AttnBlock b = p.blocks[blockIdx.x];
+    const AttnBlock b = p.blocks[blockIdx.y];
     q_row0 = b.q_row0;
     q_rows = b.q_rows;
     // The V^T tile is a TMA load along the key dimension, whose start must be
@@ -450,7 +453,8 @@ void launch(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem));
     set = true;
   }
-  dim3 grid(n_blocks, p.q_heads);
+  if (n_blocks > 65535) throw DeviceError(RS_ERR_CUDA, "tc attention: too many blocks for grid.y");
+  dim3 grid(p.q_heads, n_blocks);
   const int tok = prof::begin(st);
   fa_tc_kernel<HD, MODE><<<grid, kTcThreads, C::kSmem, st>>>(tq, tk, tv, p);
   RS_LAUNCH_CHECK();

@@ -388,6 +388,11 @@ void Context::prefill(const std::vector<SliceRef>& slices, bf16* x, cudaStream_t
       done_slots.push_back(sl.req->slot);
     }
   }
+  // Most keys first: the attention grid issues work items in this order
+  // (LPT over the SMs; attention_tc.cu).
+  std::stable_sort(work.begin(), work.end(), [](const PrefillWork& a, const PrefillWork& b) {
+    return a.q_pos0 + a.q_rows > b.q_pos0 + b.q_rows;
+  });
   ChunkDev c;
   c.M = static_cast<int>(rows.size());
   c.rows = static_cast<const ChunkRowInfo*>(up_.put(rows.data(), rows.size() * sizeof(ChunkRowInfo), st));

@@ -208,14 +208,16 @@ __global__ void vit_rope_table_kernel(const std::int32_t* __restrict__ pos_hw, i
   }
 }
 
-// q / k RoPE + head padding: one thread per (token, q|k, head, 8 pairs);
-// 16-byte loads of x[i..i+7] and x[i+half..], 16-byte stores.
-__global__ void vit_qk_rope_pad_kernel(const bf16* __restrict__ qkv, int ld,
-                                       const float2* __restrict__ table, int rows, int heads,
-                                       int hd, bf16* __restrict__ qp, bf16* __restrict__ kp) {
+// q / k RoPE: one thread per (token, q|k, head, 8 pairs); 16-byte loads of
+// x[i..i+7] and x[i+half..], 16-byte stores. Destination row stride `ldp`,
+// head stride `hs`: head-padded qp / kp (ldp = heads*128, hs = 128) or in
+// place (qp = qkv, kp = qkv + heads*hd, ldp = ld, hs = hd; each thread
+// rewrites exactly the elements it read).
+__global__ void vit_qk_rope_pad_kernel(const bf16* qkv, int ld, const float2* __restrict__ table,
+                                       int rows, int heads, int hd, bf16* qp, bf16* kp, int ldp,
+                                       int hs) {
   const int half = hd / 2, chunks = half / 8;
   const std::int64_t n = static_cast<std::int64_t>(rows) * 2 * heads * chunks;
-  const int ldp = heads * 128;
   for (std::int64_t e = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; e < n;
        e += static_cast<std::int64_t>(gridDim.x) * blockDim.x) {
     const int ch = static_cast<int>(e % chunks);
@@ -236,7 +238,7 @@ __global__ void vit_qk_rope_pad_kernel(const bf16* __restrict__ qkv, int ld,
       lo[k] = pack_bf16x2(fa.x * c0.x - fb.x * c0.y, fa.y * c1.x - fb.y * c1.y);
       hi[k] = pack_bf16x2(fb.x * c0.x + fa.x * c0.y, fb.y * c1.x + fa.y * c1.y);
     }
-    bf16* dst = (which == 0 ? qp : kp) + static_cast<std::int64_t>(t) * ldp + h * 128;
+    bf16* dst = (which == 0 ? qp : kp) + static_cast<std::int64_t>(t) * ldp + h * hs;
     *reinterpret_cast<uint4*>(dst + i0) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
     *reinterpret_cast<uint4*>(dst + i0 + half) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
   }
@@ -527,12 +529,26 @@ void vit_qkv_split(const bf16* qkv, int ld, const float2* rope_table, int rows, 
   if (hd > 128 || hd % 16 != 0) throw DeviceError(RS_ERR_CUDA, "vit_qkv_split: head_dim must be a multiple of 16, <= 128");
   const int tok = prof::begin(st);
   const std::int64_t items = static_cast<std::int64_t>(rows) * 2 * heads * (hd / 16);
-  vit_qk_rope_pad_kernel<<<elem_grid(items), 256, 0, st>>>(qkv, ld, rope_table, rows, heads, hd, qp, kp);
+  vit_qk_rope_pad_kernel<<<elem_grid(items), 256, 0, st>>>(qkv, ld, rope_table, rows, heads, hd, qp, kp,
+                                                           heads * 128, 128);
   RS_LAUNCH_CHECK();
   vit_v_transpose_kernel<<<dim3(ceil_div(rows, 64), heads), 256, 0, st>>>(qkv, ld, rows, heads, hd, vt, ld_vt);
   RS_LAUNCH_CHECK();
   prof::end(tok, st, "vit_qkv_split", 0, 2.0 * rows * heads * hd * 3 * 2);
   count_launch(2);
+}
+
+void vit_qk_rope_inplace(bf16* qkv, int ld, const float2* rope_table, int rows, int heads, int hd,
+                         cudaStream_t st) {
+  if (rows <= 0) return;
+  if (hd % 16 != 0) throw DeviceError(RS_ERR_CUDA, "vit_qk_rope_inplace: head_dim must be a multiple of 16");
+  const int tok = prof::begin(st);
+  const std::int64_t items = static_cast<std::int64_t>(rows) * 2 * heads * (hd / 16);
+  vit_qk_rope_pad_kernel<<<elem_grid(items), 256, 0, st>>>(qkv, ld, rope_table, rows, heads, hd, qkv,
+                                                           qkv + heads * hd, ld, hd);
+  RS_LAUNCH_CHECK();
+  prof::end(tok, st, "vit_rope", 0, 2.0 * rows * heads * hd * 2 * 2);
+  count_launch();
 }
 
 void rope_kv_append(bf16* qkv, int ld, const ChunkRowInfo* rows_info, int rows, int q_heads,

@@ -60,6 +60,10 @@ void rope_vit(bf16* qkv, int ld, const std::int32_t* pos_hw, int rows, int heads
 void vit_qkv_split(const bf16* qkv, int ld, const float2* rope_table, int rows, int heads, int hd,
                    bf16* qp, bf16* kp, bf16* vt, int ld_vt, cudaStream_t st);
 /// cos / sin table [rows, hd/2] of the ViT 2D RoPE (shared by all layers).
+/// ViT q / k RoPE in place on the packed qkv rows (window layers, whose
+/// attention reads qkv directly).
+void vit_qk_rope_inplace(bf16* qkv, int ld, const float2* rope_table, int rows, int heads, int hd,
+                         cudaStream_t st);
 void vit_rope_table(const std::int32_t* pos_hw, int rows, int hd, float theta, float2* table,
                     cudaStream_t st);
 

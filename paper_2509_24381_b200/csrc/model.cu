@@ -167,6 +167,10 @@ void finalize_plan(VitBatchPlan& plan) {
     for (int r = a; r < b; r += kPrefillRows)
       plan.full_blocks.push_back({r, std::min(kPrefillRows, b - r), a, b});
   }
+  // largest images first (LPT issue order, see attention_tc.cu)
+  std::stable_sort(plan.full_blocks.begin(), plan.full_blocks.end(), [](const AttnBlock& x, const AttnBlock& y) {
+    return x.key_end - x.key_begin > y.key_end - y.key_begin;
+  });
   // window layers: 128-row blocks over the packed tokens; keys = union of the
   // windows the block's rows belong to.
   const std::vector<std::int32_t>& cu = plan.cu_window;
@@ -206,13 +210,19 @@ void Vit::encode(const VitBatchPlan& plan, const bf16* patches, const std::int32
     g.A = xn_; g.lda = s.vd; g.B = L.qkv_w; g.ldb = s.vd; g.C = qkv_; g.ldc = 3 * s.vd;
     g.bias = L.qkv_b; g.M = P; g.N = 3 * s.vd; g.K = s.vd;
     gemm(g, Epi::Store, st);
-    vit_qkv_split(qkv_, 3 * s.vd, rope_table_, P, s.vh, s.vhd, qp_, kp_, vt_, max_p_, st);
-    if (s.full_attention_layer(l))
+    if (s.full_attention_layer(l)) {
+      // full image attention: tcgen05 flash attention over head-padded q / k
+      // and transposed v (long sequences, tensor-bound)
+      vit_qkv_split(qkv_, 3 * s.vd, rope_table_, P, s.vh, s.vhd, qp_, kp_, vt_, max_p_, st);
       attention_varlen_tc(qp_, kp_, vt_, max_p_, s.vh, att_, s.vd, s.vhd, full_blocks,
                           static_cast<int>(plan.full_blocks.size()), cu_item, n_items, scale, st);
-    else
-      attention_varlen_tc(qp_, kp_, vt_, max_p_, s.vh, att_, s.vd, s.vhd, win_blocks,
-                          static_cast<int>(plan.win_blocks.size()), cu_window, n_win, scale, st);
+    } else {
+      // 8x8-patch windows (<= 64 keys): latency-bound tiles; the register-
+      // tiled kernel reads qkv in place (no padding / transpose pass)
+      vit_qk_rope_inplace(qkv_, 3 * s.vd, rope_table_, P, s.vh, s.vhd, st);
+      attention_varlen_bidir(qkv_, 3 * s.vd, att_, s.vd, cu_window, n_win, plan.max_window, P, s.vh,
+                             s.vhd, scale, st);
+    }
     g = GemmArgs{};
     g.A = att_; g.lda = s.vd; g.B = L.o_w; g.ldb = s.vd; g.C = x_; g.ldc = s.vd; g.bias = L.o_b;
     g.residual = x_; g.ldr = s.vd; g.M = P; g.N = s.vd; g.K = s.vd;
