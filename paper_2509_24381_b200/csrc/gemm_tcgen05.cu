@@ -2,6 +2,7 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <unordered_map>
@@ -27,7 +28,57 @@ struct GemmParams {
   const int* row_map;
   int M, N, K;
   const int* M_dev;
+  // Hybrid data-parallel + stream-K schedule (host-chosen, see launch()):
+  // tiles [0, dp_tiles) are whole-K units striding over the grid; the k
+  // iterations of the remaining sk_tiles are split evenly over the grid.
+  int dp_tiles, sk_tiles;
+  float* ws;     // stream-K partials: [grid][2 slots][kBM x BN] fp32
+  int* counters; // per stream-K tile arrival counts (self-resetting)
 };
+
+// ---- work units ---------------------------------------------------------------
+// A unit is (tile, [kb0, kb1)). Producer, MMA issuer and epilogue walk the same
+// unit sequence. Stream-K fixup never waits: each unit of a split tile stores
+// its fp32 partial and bumps the tile's counter; the unit completing the count
+// sums all partials in k order (deterministic) and runs the fused epilogue.
+struct Unit {
+  int tile, kb0, kb1;
+  bool split;
+};
+struct UnitIter {
+  int dp_next;
+  long sk_cur, sk_end;
+};
+struct Sched {
+  int dp_tiles, sk_tiles, num_kb, grid;
+  __device__ long sk_iters() const { return static_cast<long>(sk_tiles) * num_kb; }
+  __device__ long sk_start(int c) const {
+    const long t = sk_iters(), base = t / grid, extra = t % grid;
+    return c * base + min(static_cast<long>(c), extra);
+  }
+  __device__ int sk_cta_of(long it) const {  // CTA whose stream-K range holds iteration `it`
+    const long t = sk_iters(), base = t / grid, extra = t % grid, cut = extra * (base + 1);
+    return static_cast<int>(it < cut ? it / (base + 1) : extra + (it - cut) / base);
+  }
+  __device__ UnitIter begin(int c) const { return {c, sk_start(c), sk_start(c + 1)}; }
+  __device__ bool next(UnitIter& it, Unit& u) const {
+    if (it.dp_next < dp_tiles) {
+      u = {it.dp_next, 0, num_kb, false};
+      it.dp_next += grid;
+      return true;
+    }
+    if (it.sk_cur < it.sk_end) {
+      const int t = static_cast<int>(it.sk_cur / num_kb);
+      const int kb0 = static_cast<int>(it.sk_cur % num_kb);
+      const int kb1 = static_cast<int>(min(static_cast<long>(num_kb), kb0 + (it.sk_end - it.sk_cur)));
+      u = {dp_tiles + t, kb0, kb1, !(kb0 == 0 && kb1 == num_kb)};
+      it.sk_cur += kb1 - kb0;
+      return true;
+    }
+    return false;
+  }
+};
+constexpr int kMaxParts = 8;  // units per split tile (launch() guarantees the bound)
 
 template <int BN, bool TMA_OUT = false>
 struct Cfg {
@@ -65,12 +116,37 @@ __device__ __forceinline__ float silu_plus(float x, const bf16* bias, int col) {
 // SW128-swizzled [32 x 32] smem box (conflict-free: 4 wavefronts per 512 B)
 // and stored by one TMA (coalesced, asynchronous). Residual tiles are
 // TMA-loaded one chunk ahead into the alternate buffer.
-template <int BN, int EPI>
+// Sum of the stream-K partials of one split tile at (row, col..col+31), in
+// unit (k) order.
+template <int BN>
+__device__ __forceinline__ void ws_sum32(const float* const (&parts)[kMaxParts], int n_parts, int row,
+                                         int col, std::uint32_t (&v)[32]) {
+  float a[32];
+#pragma unroll
+  for (int i = 0; i < 32; ++i) a[i] = 0.f;
+  for (int k = 0; k < n_parts; ++k) {
+    const float4* src = reinterpret_cast<const float4*>(parts[k] + row * BN + col);
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const float4 f = __ldcg(src + q);
+      a[4 * q] += f.x;
+      a[4 * q + 1] += f.y;
+      a[4 * q + 2] += f.z;
+      a[4 * q + 3] += f.w;
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __float_as_uint(a[i]);
+}
+
+template <int BN, int EPI, bool FROM_WS = false>
 __device__ __forceinline__ void epilogue_tile_tma(const GemmParams& p, const CUtensorMap* tmC,
                                                   const CUtensorMap* tmR, std::uint8_t* bufs,
                                                   std::uint64_t* rbar, std::uint32_t& rphase,
                                                   std::uint32_t& ec, std::uint32_t t_row, int m0,
-                                                  int n0, int quad, int half, int lane) {
+                                                  int n0, int quad, int half, int lane,
+                                                  const float* const (&parts)[kMaxParts] = {},
+                                                  int n_parts = 0) {
   constexpr bool kRes = EPI == static_cast<int>(Epi::Residual);
   constexpr bool kSwi = EPI == static_cast<int>(Epi::SwiGLU);
   constexpr bool kF32 = EPI == static_cast<int>(Epi::StoreF32);
@@ -110,11 +186,17 @@ __device__ __forceinline__ void epilogue_tile_tma(const GemmParams& p, const CUt
     float x[32];
     {
       std::uint32_t v[32];
-      sm100::tmem_ld_32x32b_x32(t_row + static_cast<std::uint32_t>(c * kAccPerChunk), v);
+      const int prow = quad * 32 + lane;  // row within the tile (stream-K partials)
+      if constexpr (FROM_WS) ws_sum32<BN>(parts, n_parts, prow, c * kAccPerChunk, v);
+      else sm100::tmem_ld_32x32b_x32(t_row + static_cast<std::uint32_t>(c * kAccPerChunk), v);
       if constexpr (kSwi) {
         std::uint32_t u[32];
-        sm100::tmem_ld_32x32b_x32(t_row + static_cast<std::uint32_t>(c * kAccPerChunk + 32), u);
-        sm100::tmem_ld_wait();
+        if constexpr (FROM_WS) {
+          ws_sum32<BN>(parts, n_parts, prow, c * kAccPerChunk + 32, u);
+        } else {
+          sm100::tmem_ld_32x32b_x32(t_row + static_cast<std::uint32_t>(c * kAccPerChunk + 32), u);
+          sm100::tmem_ld_wait();
+        }
         // [g0..15 u0..15 | g16..31 u16..31] -> 32 outputs
 #pragma unroll
         for (int t = 0; t < 16; ++t) {
@@ -124,7 +206,7 @@ __device__ __forceinline__ void epilogue_tile_tma(const GemmParams& p, const CUt
                       bias_add(__uint_as_float(u[16 + t]), p.bias, n0 + c * 64 + 48 + t);
         }
       } else {
-        sm100::tmem_ld_wait();
+        if constexpr (!FROM_WS) sm100::tmem_ld_wait();
         const int col = n0 + c * 32;
         if (p.bias != nullptr && col < p.N) {
 #pragma unroll
@@ -275,6 +357,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   std::uint64_t* tempty = tfull + 2;
   std::uint64_t* rbar = tempty + 2;  // [epilogue warps][2] residual-load barriers
   std::uint32_t* tmem_holder = reinterpret_cast<std::uint32_t*>(rbar + 2 * kEpiWarps);
+  volatile int* sk_finisher = reinterpret_cast<volatile int*>(tmem_holder + 1);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -283,6 +366,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int n_tiles = (p.N + BN - 1) / BN;
   const int num_tiles = m_tiles * n_tiles;
   const int num_kb = (p.K + kBK - 1) / kBK;
+  // data-parallel only unless the host chose a stream-K tail
+  const Sched sched{p.sk_tiles > 0 ? p.dp_tiles : num_tiles, p.sk_tiles, num_kb, static_cast<int>(gridDim.x)};
 
   if (warp == 0 && lane == 0) {
     sm100::tma_prefetch_desc(&tmA);
@@ -312,10 +397,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ---------------- TMA producer ----------------
     int stage = 0;
     std::uint32_t phase = 0;
-    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
-      const int m0 = (tile % m_tiles) * kBM;
-      const int n0 = (tile / m_tiles) * BN;
-      for (int kb = 0; kb < num_kb; ++kb) {
+    UnitIter it = sched.begin(blockIdx.x);
+    Unit u;
+    while (sched.next(it, u)) {
+      const int m0 = (u.tile % m_tiles) * kBM;
+      const int n0 = (u.tile / m_tiles) * BN;
+      for (int kb = u.kb0; kb < u.kb1; ++kb) {
         sm100::mbar_wait(&empty[stage], phase ^ 1);
         sm100::mbar_expect_tx(&full[stage], C::kStageBytes);
         sm100::tma_load_2d(smem_a + stage * C::kABytes, &tmA, &full[stage], kb * kBK, m0);
@@ -332,13 +419,15 @@ __global__ void __launch_bounds__(kThreads, 1)
     int stage = 0;
     std::uint32_t phase = 0;
     int local = 0;
-    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++local) {
+    UnitIter it = sched.begin(blockIdx.x);
+    Unit u;
+    for (; sched.next(it, u); ++local) {
       const int acc = local & 1;
       const std::uint32_t acc_phase = (local >> 1) & 1;
       sm100::mbar_wait(&tempty[acc], acc_phase ^ 1);
       sm100::tc_fence_after();
       const std::uint32_t d_tmem = tmem_base + static_cast<std::uint32_t>(acc * BN);
-      for (int kb = 0; kb < num_kb; ++kb) {
+      for (int kb = u.kb0; kb < u.kb1; ++kb) {
         sm100::mbar_wait(&full[stage], phase);
         sm100::tc_fence_after();
         const std::uint64_t adesc =
@@ -349,7 +438,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int kk = 0; kk < kBK / 16; ++kk) {
           // +32 B along K inside the 128B swizzle atom = +2 in the >>4 field.
           sm100::umma_bf16(d_tmem, adesc + 2 * kk, bdesc + 2 * kk, idesc,
-                           (kb | kk) != 0 ? 1u : 0u);
+                           (kb != u.kb0 || kk != 0) ? 1u : 0u);
         }
         sm100::umma_commit(&empty[stage]);  // frees the smem slot when MMAs finish
         if (++stage == C::kStages) {
@@ -365,13 +454,68 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int half = (warp - 4) >> 2;  // which half of the tile's columns
     int local = 0;
     std::uint32_t ec = 0, rphase = 0;  // TMA-epilogue chunk counter / residual phases
-    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++local) {
-      const int m0 = (tile % m_tiles) * kBM;
-      const int n0 = (tile / m_tiles) * BN;
+    UnitIter it = sched.begin(blockIdx.x);
+    Unit u;
+    for (; sched.next(it, u); ++local) {
+      const int m0 = (u.tile % m_tiles) * kBM;
+      const int n0 = (u.tile / m_tiles) * BN;
       const int acc = local & 1;
       const std::uint32_t acc_phase = (local >> 1) & 1;
       const std::uint32_t t_row =
           tmem_base + (static_cast<std::uint32_t>(quad * 32) << 16) + static_cast<std::uint32_t>(acc * BN);
+      if (TMA_OUT && u.split) {
+        // ---- stream-K unit: store the fp32 partial, count, maybe finish ----
+        const int t_sk = u.tile - sched.dp_tiles;
+        const long t_begin = static_cast<long>(t_sk) * num_kb;
+        const int c_first = sched.sk_cta_of(t_begin);
+        const int n_parts = sched.sk_cta_of(t_begin + num_kb - 1) - c_first + 1;
+        auto part_ptr = [&](int c) {  // slot 0: the CTA's first unit; 1: its last
+          const int slot = sched.sk_start(c) >= t_begin ? 0 : 1;
+          return p.ws + (static_cast<std::int64_t>(c) * 2 + slot) * (kBM * BN);
+        };
+        sm100::mbar_wait(&tfull[acc], acc_phase);
+        sm100::tc_fence_after();
+        {
+          float* mine = part_ptr(blockIdx.x) + (quad * 32 + lane) * BN;
+          constexpr int kCh = BN / 32;
+          const int c0 = half == 0 ? 0 : (kCh + 1) / 2, c1 = half == 0 ? (kCh + 1) / 2 : kCh;
+#pragma unroll 1
+          for (int c = c0; c < c1; ++c) {
+            std::uint32_t v[32];
+            sm100::tmem_ld_32x32b_x32(t_row + static_cast<std::uint32_t>(c * 32), v);
+            sm100::tmem_ld_wait();
+            float4* dst = reinterpret_cast<float4*>(mine + c * 32);
+#pragma unroll
+            for (int q = 0; q < 8; ++q)
+              __stcg(dst + q, make_float4(__uint_as_float(v[4 * q]), __uint_as_float(v[4 * q + 1]),
+                                          __uint_as_float(v[4 * q + 2]), __uint_as_float(v[4 * q + 3])));
+          }
+        }
+        sm100::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) sm100::mbar_arrive(&tempty[acc]);  // TMEM buffer free
+        __threadfence();
+        asm volatile("bar.sync 1, %0;" ::"n"(32 * kEpiWarps));
+        if (warp == 4 && lane == 0) {
+          const int old = atomicAdd(p.counters + t_sk, 1);
+          const int fin = old == n_parts - 1;
+          if (fin) p.counters[t_sk] = 0;  // ready for the next launch on this stream
+          *sk_finisher = fin;
+        }
+        asm volatile("bar.sync 1, %0;" ::"n"(32 * kEpiWarps));
+        if (*sk_finisher) {
+          __threadfence();
+          const float* parts[kMaxParts];
+#pragma unroll
+          for (int k = 0; k < kMaxParts; ++k) parts[k] = k < n_parts ? part_ptr(c_first + k) : nullptr;
+          if constexpr (TMA_OUT)
+            epilogue_tile_tma<BN, EPI, true>(p, &tmC, &tmR, smem_epi + (warp - 4) * 2 * C::kEpiBuf,
+                                             rbar + 2 * (warp - 4), rphase, ec, t_row, m0, n0, quad, half,
+                                             lane, parts, n_parts);
+        }
+        asm volatile("bar.sync 1, %0;" ::"n"(32 * kEpiWarps));  // sk_finisher reuse
+        continue;
+      }
       if constexpr (TMA_OUT) {
         sm100::mbar_wait(&tfull[acc], acc_phase);
         sm100::tc_fence_after();
@@ -479,6 +623,33 @@ CUtensorMap make_map(const void* base, bool f32, int rows, int cols, int ld, int
   return tm;
 }
 
+// Stream-K workspace of one stream (GEMMs on a stream are serialised, so one
+// workspace per stream suffices): 2 partial slots per CTA + tile counters.
+struct SkWorkspace {
+  float* ws = nullptr;
+  int* counters = nullptr;
+};
+SkWorkspace& sk_workspace(cudaStream_t st) {
+  static std::mutex mu;
+  static std::unordered_map<cudaStream_t, SkWorkspace> all;
+  std::lock_guard<std::mutex> g(mu);
+  SkWorkspace& w = all[st];
+  if (w.ws == nullptr) {
+    RS_CUDA_CHECK(cudaMalloc(&w.ws, sizeof(float) * 2 * kNumSMs * kBM * 256));
+    RS_CUDA_CHECK(cudaMalloc(&w.counters, sizeof(int) * kNumSMs));
+    RS_CUDA_CHECK(cudaMemset(w.counters, 0, sizeof(int) * kNumSMs));
+  }
+  return w;
+}
+
+bool streamk_enabled() {
+  static const bool on = [] {
+    const char* v = std::getenv("RS_GEMM_STREAMK");
+    return v == nullptr || v[0] != '0';
+  }();
+  return on;
+}
+
 template <int BN, int EPI, bool TMA_OUT>
 void launch(const GemmArgs& a, cudaStream_t stream) {
   using C = Cfg<BN, TMA_OUT>;
@@ -498,9 +669,27 @@ void launch(const GemmArgs& a, cudaStream_t stream) {
     if constexpr (EPI == static_cast<int>(Epi::Residual))
       tmR = make_map(a.residual, false, a.M, a.N, a.ldr, 32, 32);
   }
-  GemmParams p{a.C, a.ldc, a.bias, a.residual, a.ldr, a.row_map, a.M, a.N, a.K, a.M_dev};
+  GemmParams p{a.C, a.ldc, a.bias, a.residual, a.ldr, a.row_map, a.M, a.N, a.K, a.M_dev,
+               0, 0, nullptr, nullptr};
   const int tiles = ceil_div(a.M, kBM) * ceil_div(a.N, BN);
   const int grid = tiles < kNumSMs ? tiles : kNumSMs;
+  // Stream-K tail: when the last wave of whole tiles would leave > 15% of the
+  // SMs idle, full waves stay data-parallel and the k iterations of the
+  // remaining R tiles are spread evenly over all CTAs. Needs each CTA's share
+  // to be >= 1/6 tile (so a split tile has <= kMaxParts units).
+  const int num_kb = ceil_div(a.K, kBK);
+  const int rem = tiles % kNumSMs;
+  if (TMA_OUT && a.M_dev == nullptr && streamk_enabled() && tiles > kNumSMs && rem > 0 &&
+      rem * 100 <= 85 * kNumSMs) {
+    const long share = static_cast<long>(rem) * num_kb / kNumSMs;
+    if (share >= 2 && share * 6 >= num_kb) {
+      SkWorkspace& w = sk_workspace(stream);
+      p.dp_tiles = tiles - rem;
+      p.sk_tiles = rem;
+      p.ws = w.ws;
+      p.counters = w.counters;
+    }
+  }
   gemm_tcgen05_kernel<BN, EPI, TMA_OUT><<<grid, kThreads, C::kSmem, stream>>>(tmA, tmB, tmC, tmR, p);
   RS_LAUNCH_CHECK();
   count_launch();

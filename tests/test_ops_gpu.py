@@ -64,6 +64,60 @@ def test_gemm_store(nat, M, N, K, bn):
     _close(C, ref)
 
 
+# Shapes whose last wave of whole tiles is < 85% full: the k iterations of the
+# remainder tiles are split over all CTAs (stream-K tail, gemm_tcgen05.cu).
+SK_SHAPES = [(4096, 1280, 3424, 160), (2048, 3584, 18944, 224), (4096, 3840, 1280, 256),
+             (1024, 5120, 5120, 160), (4096, 1280, 1176, 256)]
+
+
+@pytest.mark.parametrize("epi", [0, 1, 2, 3])
+@pytest.mark.parametrize("M,N,K,bn", SK_SHAPES)
+def test_gemm_streamk_tail(nat, epi, M, N, K, bn):
+    torch.manual_seed(M + N + K + epi)
+    A = torch.randn(M, K, device="cuda", dtype=torch.bfloat16)
+    B = torch.randn(N, K, device="cuda", dtype=torch.bfloat16) * (1.0 / K ** 0.5)
+    bias = torch.randn(N, device="cuda", dtype=torch.bfloat16) * 0.1
+    acc = A.float() @ B.float().t() + bias.float()
+    if epi == 2:  # SwiGLU: [g0..15, u0..15, ...] interleave of the B rows
+        C = torch.empty(M, N // 2, device="cuda", dtype=torch.bfloat16)
+        g = acc.view(M, N // 32, 2, 16)
+        ref = (torch.nn.functional.silu(g[:, :, 0]) * g[:, :, 1]).reshape(M, N // 2)
+        _gemm(nat, A, B, C, 2, bias=bias, bn=bn)
+    elif epi == 1:
+        C = torch.randn(M, N, device="cuda", dtype=torch.bfloat16)
+        ref = C.float() + acc
+        _gemm(nat, A, B, C, 1, bias=bias, residual=C, bn=bn)
+    else:
+        C = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+        ref = torch.nn.functional.gelu(acc) if epi == 3 else acc
+        _gemm(nat, A, B, C, epi, bias=bias, bn=bn)
+    torch.cuda.synchronize()
+    _close(C, ref)
+    if epi in (0, 3):  # deterministic: fixed-order partial sums
+        C2 = torch.empty_like(C)
+        _gemm(nat, A, B, C2, epi, bias=bias, bn=bn)
+        torch.cuda.synchronize()
+        assert torch.equal(C, C2)
+
+
+def test_gemm_streamk_concurrent_streams(nat):
+    """Stream-K units never wait on other CTAs, so two such GEMMs sharing the
+    SMs from different streams cannot deadlock."""
+    M, N, K = 4096, 1280, 3424
+    A = torch.randn(M, K, device="cuda", dtype=torch.bfloat16)
+    B = torch.randn(N, K, device="cuda", dtype=torch.bfloat16) * 0.02
+    outs = [torch.empty(M, N, device="cuda", dtype=torch.bfloat16) for _ in range(2)]
+    streams = [torch.cuda.Stream() for _ in range(2)]
+    for _ in range(20):
+        for s, C in zip(streams, outs):
+            nat.check(nat.lib.rs_op_gemm(A.data_ptr(), K, B.data_ptr(), K, C.data_ptr(), N, None, None, 0,
+                                         None, M, N, K, 0, 160, s.cuda_stream))
+    torch.cuda.synchronize()
+    ref = A.float() @ B.float().t()
+    for C in outs:
+        _close(C, ref)
+
+
 def test_gemm_residual_inplace_and_f32(nat):
     M, N, K = 777, 1280, 640
     A = torch.randn(M, K, device="cuda", dtype=torch.bfloat16)
