@@ -28,51 +28,41 @@ struct GemmParams {
   const int* row_map;
   int M, N, K;
   const int* M_dev;
-  // Hybrid data-parallel + stream-K schedule (host-chosen, see launch()):
-  // tiles [0, dp_tiles) are whole-K units striding over the grid; the k
-  // iterations of the remaining sk_tiles are split evenly over the grid.
-  int dp_tiles, sk_tiles;
-  float* ws;     // stream-K partials: [grid][2 slots][kBM x BN] fp32
-  int* counters; // per stream-K tile arrival counts (self-resetting)
+  // Tail split-K schedule (host-chosen, see launch()): tiles [0, dp_tiles)
+  // are whole-K units striding over the grid; each of the remaining sk_tiles
+  // is split into sk_splits equal k ranges, and those units are handed out
+  // split-major, so CTAs running at the same time work on the same k range
+  // of different tiles (the A / B slices stay shared in L2).
+  int dp_tiles, sk_tiles, sk_splits;
+  float* ws;     // split partials: [sk_splits][sk_tiles][kBM x BN] fp32
+  int* counters; // per split tile arrival counts (self-resetting)
 };
 
 // ---- work units ---------------------------------------------------------------
 // A unit is (tile, [kb0, kb1)). Producer, MMA issuer and epilogue walk the same
-// unit sequence. Stream-K fixup never waits: each unit of a split tile stores
-// its fp32 partial and bumps the tile's counter; the unit completing the count
-// sums all partials in k order (deterministic) and runs the fused epilogue.
+// unit sequence. The split-K fixup never waits: each unit of a split tile
+// stores its fp32 partial and bumps the tile's counter; the unit completing
+// the count sums all partials in k order (deterministic) and runs the fused
+// epilogue, so GEMMs sharing the SMs from several streams cannot deadlock.
 struct Unit {
-  int tile, kb0, kb1;
-  bool split;
+  int tile, kb0, kb1, split;  // split: k-range index, -1 for a whole tile
 };
 struct UnitIter {
-  int dp_next;
-  long sk_cur, sk_end;
+  int dp_next, sk_next;
 };
 struct Sched {
-  int dp_tiles, sk_tiles, num_kb, grid;
-  __device__ long sk_iters() const { return static_cast<long>(sk_tiles) * num_kb; }
-  __device__ long sk_start(int c) const {
-    const long t = sk_iters(), base = t / grid, extra = t % grid;
-    return c * base + min(static_cast<long>(c), extra);
-  }
-  __device__ int sk_cta_of(long it) const {  // CTA whose stream-K range holds iteration `it`
-    const long t = sk_iters(), base = t / grid, extra = t % grid, cut = extra * (base + 1);
-    return static_cast<int>(it < cut ? it / (base + 1) : extra + (it - cut) / base);
-  }
-  __device__ UnitIter begin(int c) const { return {c, sk_start(c), sk_start(c + 1)}; }
+  int dp_tiles, sk_tiles, sk_splits, num_kb, grid;
+  __device__ UnitIter begin(int c) const { return {c, c}; }
   __device__ bool next(UnitIter& it, Unit& u) const {
     if (it.dp_next < dp_tiles) {
-      u = {it.dp_next, 0, num_kb, false};
+      u = {it.dp_next, 0, num_kb, -1};
       it.dp_next += grid;
       return true;
     }
-    if (it.sk_cur < it.sk_end) {
-      const int t = static_cast<int>(it.sk_cur / num_kb);
-      const int kb0 = static_cast<int>(it.sk_cur % num_kb);
-      const int kb1 = static_cast<int>(min(static_cast<long>(num_kb), kb0 + (it.sk_end - it.sk_cur)));
-      u = {dp_tiles + t, kb0, kb1, !(kb0 == 0 && kb1 == num_kb)};
-      it.sk_cur += kb1 - kb0;
+    if (it.sk_next < sk_tiles * sk_splits) {
+      const int sp = it.sk_next / sk_tiles, t = it.sk_next % sk_tiles;
+      u = {dp_tiles + t, sp * num_kb / sk_splits, (sp + 1) * num_kb / sk_splits, sp};
+      it.sk_next += grid;
       return true;
     }
     return false;
@@ -367,7 +357,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int num_tiles = m_tiles * n_tiles;
   const int num_kb = (p.K + kBK - 1) / kBK;
   // data-parallel only unless the host chose a stream-K tail
-  const Sched sched{p.sk_tiles > 0 ? p.dp_tiles : num_tiles, p.sk_tiles, num_kb, static_cast<int>(gridDim.x)};
+  const Sched sched{p.sk_tiles > 0 ? p.dp_tiles : num_tiles, p.sk_tiles, p.sk_tiles > 0 ? p.sk_splits : 0,
+                    num_kb, static_cast<int>(gridDim.x)};
 
   if (warp == 0 && lane == 0) {
     sm100::tma_prefetch_desc(&tmA);
@@ -463,20 +454,17 @@ __global__ void __launch_bounds__(kThreads, 1)
       const std::uint32_t acc_phase = (local >> 1) & 1;
       const std::uint32_t t_row =
           tmem_base + (static_cast<std::uint32_t>(quad * 32) << 16) + static_cast<std::uint32_t>(acc * BN);
-      if (TMA_OUT && u.split) {
-        // ---- stream-K unit: store the fp32 partial, count, maybe finish ----
+      if (TMA_OUT && u.split >= 0) {
+        // ---- split unit: store the fp32 partial, count, maybe finish ----
         const int t_sk = u.tile - sched.dp_tiles;
-        const long t_begin = static_cast<long>(t_sk) * num_kb;
-        const int c_first = sched.sk_cta_of(t_begin);
-        const int n_parts = sched.sk_cta_of(t_begin + num_kb - 1) - c_first + 1;
-        auto part_ptr = [&](int c) {  // slot 0: the CTA's first unit; 1: its last
-          const int slot = sched.sk_start(c) >= t_begin ? 0 : 1;
-          return p.ws + (static_cast<std::int64_t>(c) * 2 + slot) * (kBM * BN);
+        const int n_parts = sched.sk_splits;
+        auto part_ptr = [&](int sp) {
+          return p.ws + (static_cast<std::int64_t>(sp) * sched.sk_tiles + t_sk) * (kBM * BN);
         };
         sm100::mbar_wait(&tfull[acc], acc_phase);
         sm100::tc_fence_after();
         {
-          float* mine = part_ptr(blockIdx.x) + (quad * 32 + lane) * BN;
+          float* mine = part_ptr(u.split) + (quad * 32 + lane) * BN;
           constexpr int kCh = BN / 32;
           const int c0 = half == 0 ? 0 : (kCh + 1) / 2, c1 = half == 0 ? (kCh + 1) / 2 : kCh;
 #pragma unroll 1
@@ -507,7 +495,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           __threadfence();
           const float* parts[kMaxParts];
 #pragma unroll
-          for (int k = 0; k < kMaxParts; ++k) parts[k] = k < n_parts ? part_ptr(c_first + k) : nullptr;
+          for (int k = 0; k < kMaxParts; ++k) parts[k] = k < n_parts ? part_ptr(k) : nullptr;
           if constexpr (TMA_OUT)
             epilogue_tile_tma<BN, EPI, true>(p, &tmC, &tmR, smem_epi + (warp - 4) * 2 * C::kEpiBuf,
                                              rbar + 2 * (warp - 4), rphase, ec, t_row, m0, n0, quad, half,
@@ -629,13 +617,14 @@ struct SkWorkspace {
   float* ws = nullptr;
   int* counters = nullptr;
 };
+constexpr std::size_t kSkWsBytes = 64ull << 20;
 SkWorkspace& sk_workspace(cudaStream_t st) {
   static std::mutex mu;
   static std::unordered_map<cudaStream_t, SkWorkspace> all;
   std::lock_guard<std::mutex> g(mu);
   SkWorkspace& w = all[st];
   if (w.ws == nullptr) {
-    RS_CUDA_CHECK(cudaMalloc(&w.ws, sizeof(float) * 2 * kNumSMs * kBM * 256));
+    RS_CUDA_CHECK(cudaMalloc(&w.ws, kSkWsBytes));
     RS_CUDA_CHECK(cudaMalloc(&w.counters, sizeof(int) * kNumSMs));
     RS_CUDA_CHECK(cudaMemset(w.counters, 0, sizeof(int) * kNumSMs));
   }
@@ -670,22 +659,33 @@ void launch(const GemmArgs& a, cudaStream_t stream) {
       tmR = make_map(a.residual, false, a.M, a.N, a.ldr, 32, 32);
   }
   GemmParams p{a.C, a.ldc, a.bias, a.residual, a.ldr, a.row_map, a.M, a.N, a.K, a.M_dev,
-               0, 0, nullptr, nullptr};
+               0, 0, 0, nullptr, nullptr};
   const int tiles = ceil_div(a.M, kBM) * ceil_div(a.N, BN);
   const int grid = tiles < kNumSMs ? tiles : kNumSMs;
-  // Stream-K tail: when the last wave of whole tiles would leave > 15% of the
-  // SMs idle, full waves stay data-parallel and the k iterations of the
-  // remaining R tiles are spread evenly over all CTAs. Needs each CTA's share
-  // to be >= 1/6 tile (so a split tile has <= kMaxParts units).
+  // Tail split-K: the last, partial wave of whole tiles (R tiles) costs one
+  // full tile time. Splitting each of those tiles into S k ranges turns it
+  // into ceil(R*S / 148) rounds of 1/S tile; pick the S (<= kMaxParts, k
+  // ranges >= 16 blocks) minimising that, if it saves >= 15% of the tail.
+  // Long-K GEMMs only: the fp32 partials' round trip must stay small next to
+  // the saved tail.
   const int num_kb = ceil_div(a.K, kBK);
   const int rem = tiles % kNumSMs;
-  if (TMA_OUT && a.M_dev == nullptr && streamk_enabled() && tiles > kNumSMs && rem > 0 &&
-      rem * 100 <= 85 * kNumSMs) {
-    const long share = static_cast<long>(rem) * num_kb / kNumSMs;
-    if (share >= 2 && share * 6 >= num_kb) {
+  if (TMA_OUT && a.M_dev == nullptr && streamk_enabled() && tiles > kNumSMs && rem > 0 && num_kb >= 48) {
+    int best_s = 1;
+    double best = 1.0;
+    for (int sp = 2; sp <= kMaxParts && num_kb / sp >= 16; ++sp) {
+      if (static_cast<std::size_t>(rem) * sp * kBM * BN * sizeof(float) > kSkWsBytes) break;
+      const double cost = static_cast<double>(ceil_div(rem * sp, kNumSMs)) / sp;
+      if (cost < best - 1e-9) {
+        best = cost;
+        best_s = sp;
+      }
+    }
+    if (best_s > 1 && best <= 0.85) {
       SkWorkspace& w = sk_workspace(stream);
       p.dp_tiles = tiles - rem;
       p.sk_tiles = rem;
+      p.sk_splits = best_s;
       p.ws = w.ws;
       p.counters = w.counters;
     }
