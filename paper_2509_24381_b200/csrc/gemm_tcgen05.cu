@@ -36,6 +36,7 @@ struct GemmParams {
   int dp_tiles, sk_tiles, sk_splits;
   float* ws;     // split partials: [sk_splits][sk_tiles][kBM x BN] fp32
   int* counters; // per split tile arrival counts (self-resetting)
+  int sk_debug;  // RS_GEMM_SK_DEBUG: 1 = no partial stores / fixup, 2 = no finisher epilogue
 };
 
 // ---- work units ---------------------------------------------------------------
@@ -463,6 +464,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         };
         sm100::mbar_wait(&tfull[acc], acc_phase);
         sm100::tc_fence_after();
+        if (p.sk_debug == 1) {
+          sm100::tc_fence_before();
+          __syncwarp();
+          if (lane == 0) sm100::mbar_arrive(&tempty[acc]);
+          continue;
+        }
         {
           float* mine = part_ptr(u.split) + (quad * 32 + lane) * BN;
           constexpr int kCh = BN / 32;
@@ -491,7 +498,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           *sk_finisher = fin;
         }
         asm volatile("bar.sync 1, %0;" ::"n"(32 * kEpiWarps));
-        if (*sk_finisher) {
+        if (*sk_finisher && p.sk_debug != 2) {
           __threadfence();
           const float* parts[kMaxParts];
 #pragma unroll
@@ -659,7 +666,8 @@ void launch(const GemmArgs& a, cudaStream_t stream) {
       tmR = make_map(a.residual, false, a.M, a.N, a.ldr, 32, 32);
   }
   GemmParams p{a.C, a.ldc, a.bias, a.residual, a.ldr, a.row_map, a.M, a.N, a.K, a.M_dev,
-               0, 0, 0, nullptr, nullptr};
+               0, 0, 0, nullptr, nullptr, 0};
+  if (const char* dbg = std::getenv("RS_GEMM_SK_DEBUG")) p.sk_debug = std::atoi(dbg);
   const int tiles = ceil_div(a.M, kBM) * ceil_div(a.N, BN);
   const int grid = tiles < kNumSMs ? tiles : kNumSMs;
   // Tail split-K: the last, partial wave of whole tiles (R tiles) costs one
