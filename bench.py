@@ -162,6 +162,13 @@ def run_ours(args):
             dev_ms.append(st["gpu_ms"])
             launches += st["kernel_launches"]
     torch.cuda.synchronize()
+    if args.launch_list:
+        # ncu launch-list pass: only the plain warm-up + timed steps above
+        pipe.close()
+        if rank == 0:
+            print(json.dumps({"launch_list": True, "steps": args.steps, "warmup": args.warmup,
+                              "ttft_ms": ttfts, "note": "timed under a profiler: not a bench value"}))
+        return
     # Per-kernel-class timing for the roofline: one extra step with CUDA events
     # around every launch, encoders on the prefill stream (serialised) so each
     # event pair measures the kernel alone, not cross-stream queueing.
@@ -436,6 +443,8 @@ def main():
     ap.add_argument("--budget", type=int, default=2048, help="Algorithm-2 token budget B")
     ap.add_argument("--policy", default="rserve")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--launch-list", action="store_true",
+                    help="run only the warm-up + timed steps (for the ncu launch list); no JSON bench line")
     ap.add_argument("--ep", action="store_true",
                     help="N>1: EP deployment (1E+1P / 2E+2P / 4E+4P) instead of independent replicas")
     ap.add_argument("--ep-transport", default="ipc", choices=["ipc", "nccl"])

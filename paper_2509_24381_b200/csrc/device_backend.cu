@@ -2,6 +2,7 @@
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>
+#include <string>
 
 #include "device_backend.cuh"
 #include "kernels.cuh"
@@ -28,8 +29,17 @@ DeviceBackend::DeviceBackend(Context& ctx, const lmmsim::SimConfig& cfg, bool re
   const Shapes& s = ctx.shapes();
   // One prefill stream: all stages of this GPU share the SMs and the per-stage
   // scratch; each chunk owns its residual buffer so stages can interleave.
+  // Stream priorities (RS_STREAM_PRIO = enc | prefill | none; default enc):
+  // an encode batch unblocks prefill of its span, so its CTAs go first when
+  // both streams have work pending; prefill fills the remaining SM time.
+  int prio_lo = 0, prio_hi = 0;
+  RS_CUDA_CHECK(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
+  const char* prio = std::getenv("RS_STREAM_PRIO");
+  const std::string pmode = prio != nullptr ? prio : "enc";
+  const int enc_prio = pmode == "enc" ? prio_hi : prio_lo;
+  const int stage_prio = pmode == "prefill" ? prio_hi : prio_lo;
   stage_streams_.resize(1);
-  RS_CUDA_CHECK(cudaStreamCreateWithFlags(&stage_streams_[0], cudaStreamNonBlocking));
+  RS_CUDA_CHECK(cudaStreamCreateWithPriority(&stage_streams_[0], cudaStreamNonBlocking, stage_prio));
   // serialize (profiling; or RS_SERIALIZE=1): encoders share the prefill
   // stream, so per-kernel event times are not inflated by cross-stream queueing.
   const char* ser = std::getenv("RS_SERIALIZE");
@@ -40,7 +50,7 @@ DeviceBackend::DeviceBackend(Context& ctx, const lmmsim::SimConfig& cfg, bool re
       st = stage_streams_[0];
       shared_streams_ = true;
     } else {
-      RS_CUDA_CHECK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+      RS_CUDA_CHECK(cudaStreamCreateWithPriority(&st, cudaStreamNonBlocking, enc_prio));
     }
   }
   RS_CUDA_CHECK(cudaStreamCreateWithFlags(&copy_stream_, cudaStreamNonBlocking));
