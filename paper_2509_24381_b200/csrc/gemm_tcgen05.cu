@@ -2,6 +2,7 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
@@ -71,11 +72,15 @@ struct Sched {
 };
 constexpr int kMaxParts = 8;  // units per split tile (launch() guarantees the bound)
 
-template <int BN, bool TMA_OUT = false>
+// CG = CTAs per tile: 1, or 2 for a CTA pair (cluster of 2 on one TPC) running
+// 256 x BN tiles with cta_group::2 MMAs — each CTA stages its own 128 A rows
+// and half of the B rows, halving per-SM shared-memory operand traffic.
+template <int BN, bool TMA_OUT = false, int CG = 1>
 struct Cfg {
   static_assert(BN % 32 == 0 && BN >= 128 && BN <= 256, "tile width");
+  static_assert(CG == 1 || (CG == 2 && BN % 32 == 0), "pair tiles split B in halves of 16-row multiples");
   static constexpr int kABytes = kBM * kBK * 2;
-  static constexpr int kBBytes = BN * kBK * 2;
+  static constexpr int kBBytes = (BN / CG) * kBK * 2;
   static constexpr int kStageBytes = kABytes + kBBytes;
   // epilogue staging: 8 warps x 2 buffers x [32 rows x 64 B] (bf16 TMA stores)
   static constexpr int kEpiBuf = 2048;
@@ -328,13 +333,13 @@ __device__ __forceinline__ void epilogue_chunk(const GemmParams& p, int row, int
   }
 }
 
-template <int BN, int EPI, bool TMA_OUT>
+template <int BN, int EPI, bool TMA_OUT, int CG>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmA,
                         const __grid_constant__ CUtensorMap tmB,
                         const __grid_constant__ CUtensorMap tmC,
                         const __grid_constant__ CUtensorMap tmR, const GemmParams p) {
-  using C = Cfg<BN, TMA_OUT>;
+  using C = Cfg<BN, TMA_OUT, CG>;
   extern __shared__ __align__(1024) std::uint8_t smem_raw[];
   std::uint8_t* smem = reinterpret_cast<std::uint8_t*>(
       (reinterpret_cast<std::uintptr_t>(smem_raw) + 1023) & ~std::uintptr_t(1023));
@@ -352,14 +357,17 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
+  // CTA pair: rank 0 (leader) issues the MMAs; both CTAs load and drain.
+  const std::uint32_t rank = CG == 2 ? sm100::cluster_ctarank() : 0u;
   const int M = p.M_dev != nullptr ? min(*p.M_dev, p.M) : p.M;
-  const int m_tiles = (M + kBM - 1) / kBM;
+  const int m_tiles = (M + kBM * CG - 1) / (kBM * CG);
   const int n_tiles = (p.N + BN - 1) / BN;
   const int num_tiles = m_tiles * n_tiles;
   const int num_kb = (p.K + kBK - 1) / kBK;
   // data-parallel only unless the host chose a stream-K tail
   const Sched sched{p.sk_tiles > 0 ? p.dp_tiles : num_tiles, p.sk_tiles, p.sk_tiles > 0 ? p.sk_splits : 0,
-                    num_kb, static_cast<int>(gridDim.x)};
+                    num_kb, static_cast<int>(gridDim.x) / CG};
+  const int unit0 = static_cast<int>(blockIdx.x) / CG;
 
   if (warp == 0 && lane == 0) {
     sm100::tma_prefetch_desc(&tmA);
@@ -370,7 +378,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int a = 0; a < 2; ++a) {
       sm100::mbar_init(&tfull[a], 1);
-      sm100::mbar_init(&tempty[a], kEpiWarps);
+      sm100::mbar_init(&tempty[a], kEpiWarps * CG);  // pair: both CTAs' epilogue warps
     }
     for (int r = 0; r < 2 * kEpiWarps; ++r) sm100::mbar_init(&rbar[r], 1);
     if constexpr (TMA_OUT) {
@@ -379,9 +387,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     sm100::fence_mbar_init();
   }
-  if (warp == 2) sm100::tmem_alloc(tmem_holder, C::kTmemCols);
+  if (warp == 2) {
+    if constexpr (CG == 2) sm100::tmem_alloc_cg2(tmem_holder, C::kTmemCols);
+    else sm100::tmem_alloc(tmem_holder, C::kTmemCols);
+  }
   sm100::tc_fence_before();
-  __syncthreads();
+  if constexpr (CG == 2) sm100::cluster_sync();  // peer barriers initialised before any remote use
+  else __syncthreads();
   sm100::tc_fence_after();
   const std::uint32_t tmem_base = *tmem_holder;
 
@@ -389,29 +401,37 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ---------------- TMA producer ----------------
     int stage = 0;
     std::uint32_t phase = 0;
-    UnitIter it = sched.begin(blockIdx.x);
+    UnitIter it = sched.begin(unit0);
     Unit u;
     while (sched.next(it, u)) {
-      const int m0 = (u.tile % m_tiles) * kBM;
-      const int n0 = (u.tile / m_tiles) * BN;
+      const int m0 = (u.tile % m_tiles) * (kBM * CG) + static_cast<int>(rank) * kBM;
+      const int n0 = (u.tile / m_tiles) * BN + static_cast<int>(rank) * (BN / CG);
       for (int kb = u.kb0; kb < u.kb1; ++kb) {
         sm100::mbar_wait(&empty[stage], phase ^ 1);
-        sm100::mbar_expect_tx(&full[stage], C::kStageBytes);
-        sm100::tma_load_2d(smem_a + stage * C::kABytes, &tmA, &full[stage], kb * kBK, m0);
-        sm100::tma_load_2d(smem_b + stage * C::kBBytes, &tmB, &full[stage], kb * kBK, n0);
+        if constexpr (CG == 2) {
+          // both CTAs' bytes complete on the leader's full barrier
+          if (rank == 0) sm100::mbar_expect_tx(&full[stage], 2 * C::kStageBytes);
+          const std::uint32_t fb = sm100::mapa(sm100::smem_u32(&full[stage]), 0);
+          sm100::tma_load_2d_cg2(smem_a + stage * C::kABytes, &tmA, fb, kb * kBK, m0);
+          sm100::tma_load_2d_cg2(smem_b + stage * C::kBBytes, &tmB, fb, kb * kBK, n0);
+        } else {
+          sm100::mbar_expect_tx(&full[stage], C::kStageBytes);
+          sm100::tma_load_2d(smem_a + stage * C::kABytes, &tmA, &full[stage], kb * kBK, m0);
+          sm100::tma_load_2d(smem_b + stage * C::kBBytes, &tmB, &full[stage], kb * kBK, n0);
+        }
         if (++stage == C::kStages) {
           stage = 0;
           phase ^= 1;
         }
       }
     }
-  } else if (warp == 1 && lane == 0) {
-    // ---------------- MMA issuer (single thread) ----------------
-    constexpr std::uint32_t idesc = sm100::idesc_bf16_f32(kBM, BN);
+  } else if (warp == 1 && lane == 0 && rank == 0) {
+    // ---------------- MMA issuer (single thread; pair leader) ----------------
+    constexpr std::uint32_t idesc = sm100::idesc_bf16_f32(kBM * CG, BN);
     int stage = 0;
     std::uint32_t phase = 0;
     int local = 0;
-    UnitIter it = sched.begin(blockIdx.x);
+    UnitIter it = sched.begin(unit0);
     Unit u;
     for (; sched.next(it, u); ++local) {
       const int acc = local & 1;
@@ -429,16 +449,24 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int kk = 0; kk < kBK / 16; ++kk) {
           // +32 B along K inside the 128B swizzle atom = +2 in the >>4 field.
-          sm100::umma_bf16(d_tmem, adesc + 2 * kk, bdesc + 2 * kk, idesc,
-                           (kb != u.kb0 || kk != 0) ? 1u : 0u);
+          if constexpr (CG == 2)
+            sm100::umma_bf16_cg2(d_tmem, adesc + 2 * kk, bdesc + 2 * kk, idesc,
+                                 (kb != u.kb0 || kk != 0) ? 1u : 0u);
+          else
+            sm100::umma_bf16(d_tmem, adesc + 2 * kk, bdesc + 2 * kk, idesc,
+                             (kb != u.kb0 || kk != 0) ? 1u : 0u);
         }
-        sm100::umma_commit(&empty[stage]);  // frees the smem slot when MMAs finish
+        // frees the smem slot (in both CTAs of a pair) when the MMAs finish
+        if constexpr (CG == 2) sm100::umma_commit_cg2(&empty[stage], 3);
+        else sm100::umma_commit(&empty[stage]);
         if (++stage == C::kStages) {
           stage = 0;
           phase ^= 1;
         }
       }
-      sm100::umma_commit(&tfull[acc]);  // accumulator ready for the epilogue
+      // accumulator ready for the epilogue (both CTAs' halves of a pair tile)
+      if constexpr (CG == 2) sm100::umma_commit_cg2(&tfull[acc], 3);
+      else sm100::umma_commit(&tfull[acc]);
     }
   } else if (warp >= 4) {
     // ---------------- epilogue warps ----------------
@@ -446,10 +474,15 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int half = (warp - 4) >> 2;  // which half of the tile's columns
     int local = 0;
     std::uint32_t ec = 0, rphase = 0;  // TMA-epilogue chunk counter / residual phases
-    UnitIter it = sched.begin(blockIdx.x);
+    UnitIter it = sched.begin(unit0);
     Unit u;
+    // accumulator-free signal goes to the MMA issuer's CTA (the pair leader)
+    auto release_acc = [&](int acc) {
+      if constexpr (CG == 2) sm100::mbar_arrive_cluster(sm100::mapa(sm100::smem_u32(&tempty[acc]), 0));
+      else sm100::mbar_arrive(&tempty[acc]);
+    };
     for (; sched.next(it, u); ++local) {
-      const int m0 = (u.tile % m_tiles) * kBM;
+      const int m0 = (u.tile % m_tiles) * (kBM * CG) + static_cast<int>(rank) * kBM;
       const int n0 = (u.tile / m_tiles) * BN;
       const int acc = local & 1;
       const std::uint32_t acc_phase = (local >> 1) & 1;
@@ -467,7 +500,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (p.sk_debug == 1) {
           sm100::tc_fence_before();
           __syncwarp();
-          if (lane == 0) sm100::mbar_arrive(&tempty[acc]);
+          if (lane == 0) release_acc(acc);
           continue;
         }
         {
@@ -488,7 +521,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         sm100::tc_fence_before();
         __syncwarp();
-        if (lane == 0) sm100::mbar_arrive(&tempty[acc]);  // TMEM buffer free
+        if (lane == 0) release_acc(acc);  // TMEM buffer free
         __threadfence();
         asm volatile("bar.sync 1, %0;" ::"n"(32 * kEpiWarps));
         if (warp == 4 && lane == 0) {
@@ -533,17 +566,19 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       sm100::tc_fence_before();
       __syncwarp();
-      if (lane == 0) sm100::mbar_arrive(&tempty[acc]);
+      if (lane == 0) release_acc(acc);
     }
     if constexpr (TMA_OUT) {
       if (lane == 0) sm100::bulk_wait<0>();  // stores complete before smem is released
       __syncwarp();
     }
   }
-  __syncthreads();
+  if constexpr (CG == 2) sm100::cluster_sync();  // peer done with our smem / TMEM / barriers
+  else __syncthreads();
   if (warp == 2) {
     sm100::tc_fence_after();
-    sm100::tmem_dealloc(tmem_base, C::kTmemCols);
+    if constexpr (CG == 2) sm100::tmem_dealloc_cg2(tmem_base, C::kTmemCols);
+    else sm100::tmem_dealloc(tmem_base, C::kTmemCols);
   }
 }
 
@@ -646,17 +681,17 @@ bool streamk_enabled() {
   return on;
 }
 
-template <int BN, int EPI, bool TMA_OUT>
+template <int BN, int EPI, bool TMA_OUT, int CG>
 void launch(const GemmArgs& a, cudaStream_t stream) {
-  using C = Cfg<BN, TMA_OUT>;
+  using C = Cfg<BN, TMA_OUT, CG>;
+  auto* kernel = gemm_tcgen05_kernel<BN, EPI, TMA_OUT, CG>;
   static bool attr_set = false;
   if (!attr_set) {
-    RS_CUDA_CHECK(cudaFuncSetAttribute(gemm_tcgen05_kernel<BN, EPI, TMA_OUT>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem));
+    RS_CUDA_CHECK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem));
     attr_set = true;
   }
   const CUtensorMap tmA = make_map(a.A, false, a.M, a.K, a.lda, kBK, kBM);
-  const CUtensorMap tmB = make_map(a.B, false, a.N, a.K, a.ldb, kBK, BN);
+  const CUtensorMap tmB = make_map(a.B, false, a.N, a.K, a.ldb, kBK, BN / CG);
   CUtensorMap tmC = tmA, tmR = tmA;  // unused placeholders unless TMA_OUT
   if constexpr (TMA_OUT) {
     constexpr bool f32 = EPI == static_cast<int>(Epi::StoreF32);
@@ -668,8 +703,8 @@ void launch(const GemmArgs& a, cudaStream_t stream) {
   GemmParams p{a.C, a.ldc, a.bias, a.residual, a.ldr, a.row_map, a.M, a.N, a.K, a.M_dev,
                0, 0, 0, nullptr, nullptr, 0};
   if (const char* dbg = std::getenv("RS_GEMM_SK_DEBUG")) p.sk_debug = std::atoi(dbg);
-  const int tiles = ceil_div(a.M, kBM) * ceil_div(a.N, BN);
-  const int grid = tiles < kNumSMs ? tiles : kNumSMs;
+  const int tiles = ceil_div(a.M, kBM * CG) * ceil_div(a.N, BN);
+  const int grid = CG * (tiles < kNumSMs / CG ? tiles : kNumSMs / CG);
   // Tail split-K: the last, partial wave of whole tiles (R tiles) costs one
   // full tile time. Splitting each of those tiles into S k ranges turns it
   // into ceil(R*S / 148) rounds of 1/S tile; pick the S (<= kMaxParts, k
@@ -678,7 +713,7 @@ void launch(const GemmArgs& a, cudaStream_t stream) {
   // the saved tail.
   const int num_kb = ceil_div(a.K, kBK);
   const int rem = tiles % kNumSMs;
-  if (TMA_OUT && a.M_dev == nullptr && streamk_enabled() && tiles > kNumSMs && rem > 0 && num_kb >= 48) {
+  if (CG == 1 && TMA_OUT && a.M_dev == nullptr && streamk_enabled() && tiles > kNumSMs && rem > 0 && num_kb >= 48) {
     int best_s = 1;
     double best = 1.0;
     for (int sp = 2; sp <= kMaxParts && num_kb / sp >= 16; ++sp) {
@@ -698,44 +733,81 @@ void launch(const GemmArgs& a, cudaStream_t stream) {
       p.counters = w.counters;
     }
   }
-  gemm_tcgen05_kernel<BN, EPI, TMA_OUT><<<grid, kThreads, C::kSmem, stream>>>(tmA, tmB, tmC, tmR, p);
+  if constexpr (CG == 1) {
+    kernel<<<grid, kThreads, C::kSmem, stream>>>(tmA, tmB, tmC, tmR, p);
+  } else {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = C::kSmem;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    RS_CUDA_CHECK(cudaLaunchKernelEx(&cfg, kernel, tmA, tmB, tmC, tmR, p));
+  }
   RS_LAUNCH_CHECK();
   count_launch();
 }
 
-template <int BN>
+template <int BN, int CG>
 void dispatch_epi(const GemmArgs& a, Epi epi, cudaStream_t s) {
   // Row-mapped outputs (scatter) keep the direct-store epilogue; everything
   // else goes through smem + TMA stores.
   const bool tma = a.row_map == nullptr && a.M_dev == nullptr;
   switch (epi) {
-    case Epi::Store: return tma ? launch<BN, 0, true>(a, s) : launch<BN, 0, false>(a, s);
-    case Epi::Residual: return tma ? launch<BN, 1, true>(a, s) : launch<BN, 1, false>(a, s);
+    case Epi::Store: return tma ? launch<BN, 0, true, CG>(a, s) : launch<BN, 0, false, CG>(a, s);
+    case Epi::Residual: return tma ? launch<BN, 1, true, CG>(a, s) : launch<BN, 1, false, CG>(a, s);
     case Epi::SwiGLU:
       if constexpr (BN % 64 == 0)
-        return tma ? launch<BN, 2, true>(a, s) : launch<BN, 2, false>(a, s);
+        return tma ? launch<BN, 2, true, CG>(a, s) : launch<BN, 2, false, CG>(a, s);
       else
-        return launch<BN, 2, false>(a, s);
-    case Epi::Gelu: return tma ? launch<BN, 3, true>(a, s) : launch<BN, 3, false>(a, s);
-    case Epi::StoreF32: return launch<BN, 4, false>(a, s);  // LM-head logits (row-mapped)
+        return launch<BN, 2, false, CG>(a, s);
+    case Epi::Gelu: return tma ? launch<BN, 3, true, CG>(a, s) : launch<BN, 3, false, CG>(a, s);
+    case Epi::StoreF32: return launch<BN, 4, false, CG>(a, s);  // LM-head logits (row-mapped)
   }
 }
 
-// Tile width with the least wave-quantised time: a wave of the persistent
-// kernel costs ~BN (per-tile work at fixed BM and K), so minimise
-// waves * BN; ties go to the wider tile (fewer A re-reads).
-int pick_bn(int M, int N, bool swiglu) {
+// Tile shape with the least wave-quantised time. A wave of the persistent
+// kernel costs ~BN (per-tile work at fixed BM and K): 148 single-CTA 128 x BN
+// tiles per wave, or 74 pair tiles of 256 x BN, whose per-FLOP cost is lower
+// (half the shared-memory operand traffic per SM). Calibrated on B200
+// (scripts/gemm_sweep.py, profiles/r01_gemm_sweep_pair.txt): pairs gain ~15%
+// on long K, ~7% on short K, and lose ~5-10% on short-K GEMMs of <= 2 waves
+// (per-tile fixed costs dominate). Ties go to the wider tile (fewer A
+// re-reads). RS_GEMM_CG=1/2 forces the CTA mode.
+struct TileChoice {
+  int bn, cg;
+};
+int cg_override() {
+  static const int v = [] {
+    const char* e = std::getenv("RS_GEMM_CG");
+    return e != nullptr ? std::atoi(e) : 0;
+  }();
+  return v;
+}
+TileChoice pick_tile(int M, int N, int K, bool swiglu) {
   static constexpr int kCandidates[] = {256, 224, 192, 160, 128};
-  int best = 256;
-  long best_cost = -1;
-  for (int bn : kCandidates) {
-    if (swiglu && bn % 64 != 0) continue;  // 64-column gate/up chunks (TMA epilogue)
-    const long tiles = static_cast<long>(ceil_div(M, kBM)) * ceil_div(N, bn);
-    const long waves = (tiles + kNumSMs - 1) / kNumSMs;
-    const long cost = waves * bn;
-    if (best_cost < 0 || cost < best_cost) {
-      best = bn;
-      best_cost = cost;
+  const int num_kb = ceil_div(K, kBK);
+  TileChoice best{256, 1};
+  double best_cost = -1;
+  for (int cg = 1; cg <= 2; ++cg) {
+    if (cg_override() != 0 && cg != cg_override()) continue;
+    for (int bn : kCandidates) {
+      if (swiglu && bn % 64 != 0) continue;  // 64-column gate/up chunks (TMA epilogue)
+      const long tiles = static_cast<long>(ceil_div(M, kBM * cg)) * ceil_div(N, bn);
+      const long slots = kNumSMs / cg;
+      const long waves = (tiles + slots - 1) / slots;
+      const double pair_gain = num_kb >= 32 ? 0.85 : (waves <= 2 ? 1.05 : 0.93);
+      const double cost = static_cast<double>(waves * bn) * (cg == 2 ? pair_gain : 1.0);
+      if (best_cost < 0 || cost < best_cost - 1e-9) {
+        best = {bn, cg};
+        best_cost = cost;
+      }
     }
   }
   return best;
@@ -750,19 +822,35 @@ void gemm(const GemmArgs& a, Epi epi, cudaStream_t stream, int force_bn) {
                                        std::to_string(a.K) + ", N=" + std::to_string(a.N) + ")");
   if (epi == Epi::SwiGLU && a.N % 32 != 0)
     throw DeviceError(RS_ERR_CUDA, "gemm: SwiGLU needs N%32==0");
-  const int bn = force_bn != 0 ? force_bn : pick_bn(a.M, a.N, epi == Epi::SwiGLU);
+  // force_bn > 0: single-CTA tiles of that width; < 0: CTA-pair tiles of |force_bn|
+  const TileChoice tc = force_bn > 0   ? TileChoice{force_bn, 1}
+                        : force_bn < 0 ? TileChoice{-force_bn, 2}
+                                       : pick_tile(a.M, a.N, a.K, epi == Epi::SwiGLU);
   const int tok = prof::begin(stream);
-  switch (bn) {
-    case 256: dispatch_epi<256>(a, epi, stream); break;
-    case 224: dispatch_epi<224>(a, epi, stream); break;
-    case 192: dispatch_epi<192>(a, epi, stream); break;
-    case 160: dispatch_epi<160>(a, epi, stream); break;
-    case 128: dispatch_epi<128>(a, epi, stream); break;
-    default: throw DeviceError(RS_ERR_CUDA, "gemm: unsupported tile width " + std::to_string(bn));
+  const int key = tc.bn * 4 + tc.cg;
+  switch (key) {
+    case 256 * 4 + 1: dispatch_epi<256, 1>(a, epi, stream); break;
+    case 224 * 4 + 1: dispatch_epi<224, 1>(a, epi, stream); break;
+    case 192 * 4 + 1: dispatch_epi<192, 1>(a, epi, stream); break;
+    case 160 * 4 + 1: dispatch_epi<160, 1>(a, epi, stream); break;
+    case 128 * 4 + 1: dispatch_epi<128, 1>(a, epi, stream); break;
+    case 256 * 4 + 2: dispatch_epi<256, 2>(a, epi, stream); break;
+    case 224 * 4 + 2: dispatch_epi<224, 2>(a, epi, stream); break;
+    case 192 * 4 + 2: dispatch_epi<192, 2>(a, epi, stream); break;
+    case 160 * 4 + 2: dispatch_epi<160, 2>(a, epi, stream); break;
+    case 128 * 4 + 2: dispatch_epi<128, 2>(a, epi, stream); break;
+    default:
+      throw DeviceError(RS_ERR_CUDA, "gemm: unsupported tile " + std::to_string(tc.bn) + " x cg" +
+                                         std::to_string(tc.cg));
   }
   const double m = a.M, n = a.N, k = a.K;
   const double out_bytes = epi == Epi::StoreF32 ? 4.0 : (epi == Epi::SwiGLU ? 1.0 : 2.0);
-  prof::end(tok, stream, "gemm_tcgen05", 2.0 * m * n * k,
+  if (tok < 0) return;
+  // per-shape class "gemm_tcgen05|M|N|K|epi|BN|CG" (the bench groups on the prefix)
+  char label[96];
+  std::snprintf(label, sizeof label, "gemm_tcgen05|%d|%d|%d|%d|%d|%d", a.M, a.N, a.K,
+                static_cast<int>(epi), tc.bn, tc.cg);
+  prof::end(tok, stream, label, 2.0 * m * n * k,
             2.0 * (m * k + n * k) + out_bytes * m * n + (epi == Epi::Residual ? 2.0 * m * n : 0.0));
 }
 

@@ -101,6 +101,75 @@ def test_gemm_streamk_tail(nat, epi, M, N, K, bn):
         assert torch.equal(C, C2)
 
 
+PAIR_SHAPES = [(256, 256, 64), (1, 256, 64), (300, 384, 200), (4096, 1280, 1176), (2048, 37888, 3584),
+               (129, 144, 72), (4096, 3840, 1280), (7, 9504, 512)]
+
+
+@pytest.mark.parametrize("M,N,K", PAIR_SHAPES)
+@pytest.mark.parametrize("bn", [128, 160, 192, 224, 256])
+@pytest.mark.parametrize("epi", [0, 1, 2, 3])
+def test_gemm_cta_pair(nat, M, N, K, bn, epi):
+    """CTA-pair tiles (cluster of 2, cta_group::2 MMAs, 256 x BN): every fused
+    epilogue, ragged M / N / K tails (force_bn < 0 selects the pair kernel)."""
+    if epi == 2 and (bn % 64 != 0 or N % 32 != 0):
+        pytest.skip("SwiGLU pair tiles need 64-column chunks")
+    if (M, N, K) == (2048, 37888, 3584) and (bn != 256 or epi not in (0, 2)):
+        pytest.skip("large shape: one tile width")
+    torch.manual_seed(M + N + K + bn + epi)
+    A = torch.randn(M, K, device="cuda", dtype=torch.bfloat16)
+    B = torch.randn(N, K, device="cuda", dtype=torch.bfloat16) * (1.0 / K ** 0.5)
+    bias = torch.randn(N, device="cuda", dtype=torch.bfloat16) * 0.1
+    acc = A.float() @ B.float().t() + bias.float()
+    if epi == 2:
+        C = torch.empty(M, N // 2, device="cuda", dtype=torch.bfloat16)
+        g = acc.view(M, N // 32, 2, 16)
+        ref = (torch.nn.functional.silu(g[:, :, 0]) * g[:, :, 1]).reshape(M, N // 2)
+        _gemm(nat, A, B, C, 2, bias=bias, bn=-bn)
+    elif epi == 1:
+        C = torch.randn(M, N, device="cuda", dtype=torch.bfloat16)
+        ref = C.float() + acc
+        _gemm(nat, A, B, C, 1, bias=bias, residual=C, bn=-bn)
+    else:
+        C = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+        ref = torch.nn.functional.gelu(acc) if epi == 3 else acc
+        _gemm(nat, A, B, C, epi, bias=bias, bn=-bn)
+    torch.cuda.synchronize()
+    _close(C, ref)
+
+
+def test_gemm_cta_pair_rowmap_f32(nat):
+    """Pair tiles on the direct-store epilogue (row map, fp32 logits)."""
+    M, N, K = 300, 1024, 256
+    A = torch.randn(M, K, device="cuda", dtype=torch.bfloat16)
+    B = torch.randn(N, K, device="cuda", dtype=torch.bfloat16) * 0.05
+    perm = torch.randperm(M, device="cuda").to(torch.int32)
+    C = torch.zeros(M, N, device="cuda", dtype=torch.bfloat16)
+    _gemm(nat, A, B, C, 3, row_map=perm, bn=-256)
+    F = torch.empty(M, N, device="cuda", dtype=torch.float32)
+    _gemm(nat, A, B, F, 4, bn=-192)
+    torch.cuda.synchronize()
+    ref = A.float() @ B.float().t()
+    _close(C[perm.long()], torch.nn.functional.gelu(ref))
+    _close(F, ref, rel=5e-3)
+
+
+def test_gemm_cta_pair_concurrent_streams(nat):
+    """Pair kernels and single-CTA stream-K kernels sharing the SMs."""
+    M, N, K = 1024, 5120, 5120
+    A = torch.randn(M, K, device="cuda", dtype=torch.bfloat16)
+    B = torch.randn(N, K, device="cuda", dtype=torch.bfloat16) * 0.02
+    outs = [torch.empty(M, N, device="cuda", dtype=torch.bfloat16) for _ in range(2)]
+    streams = [torch.cuda.Stream() for _ in range(2)]
+    for _ in range(20):
+        for i, (s, C) in enumerate(zip(streams, outs)):
+            nat.check(nat.lib.rs_op_gemm(A.data_ptr(), K, B.data_ptr(), K, C.data_ptr(), N, None, None, 0,
+                                         None, M, N, K, 0, -256 if i == 0 else 160, s.cuda_stream))
+    torch.cuda.synchronize()
+    ref = A.float() @ B.float().t()
+    for C in outs:
+        _close(C, ref)
+
+
 def test_gemm_streamk_concurrent_streams(nat):
     """Stream-K units never wait on other CTAs, so two such GEMMs sharing the
     SMs from different streams cannot deadlock."""
