@@ -2,6 +2,7 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -681,6 +682,41 @@ bool streamk_enabled() {
   return on;
 }
 
+// Split-K plan of a single-CTA GEMM (tiles of 128 x bn, num_kb k-blocks).
+//  * tail: the last, partial wave of whole tiles (R tiles) costs one full
+//    tile time; splitting each of those tiles into S k ranges turns it into
+//    ceil(R*S / 148) rounds of 1/S tile. Long-K GEMMs only (>= 48 k-blocks):
+//    the fp32 partials' round trip must stay small next to the saved tail.
+//  * small grid (tiles <= 74, e.g. the 128-token first chunk): every tile is
+//    split, so the weight stream (the bound at small M) is read by ~148 SMs.
+// cost = tile-times the launch takes (whole tiles = 1 each).
+struct SplitPlan {
+  int sk_tiles = 0, splits = 1;
+  double cost = 0;
+};
+SplitPlan plan_split(int tiles, int num_kb, int bn) {
+  SplitPlan best;
+  const int rem = tiles % kNumSMs;
+  const int full = tiles / kNumSMs;
+  best.cost = full + (rem > 0 ? 1.0 : 0.0);
+  // (measured: at K = 3584 the partials' round trip eats the gain; K = 18944 wins 30%)
+  const bool small = tiles <= kNumSMs / 2 && num_kb >= 128;
+  const bool tail = tiles > kNumSMs && rem > 0 && num_kb >= 48;
+  if (!small && !tail) return best;
+  const int min_kb = 16;
+  for (int sp = 2; sp <= kMaxParts && num_kb / sp >= min_kb; ++sp) {
+    if (static_cast<std::size_t>(rem) * sp * kBM * bn * sizeof(float) > kSkWsBytes) break;
+    // partial round trip: ~4% of a tile per extra split
+    const double tail_c = static_cast<double>(ceil_div(rem * sp, kNumSMs)) / sp + 0.04 * (sp - 1);
+    if (tail_c <= 0.85 && full + tail_c < best.cost - 1e-9) {
+      best.cost = full + tail_c;
+      best.sk_tiles = rem;
+      best.splits = sp;
+    }
+  }
+  return best;
+}
+
 template <int BN, int EPI, bool TMA_OUT, int CG>
 void launch(const GemmArgs& a, cudaStream_t stream) {
   using C = Cfg<BN, TMA_OUT, CG>;
@@ -704,33 +740,23 @@ void launch(const GemmArgs& a, cudaStream_t stream) {
                0, 0, 0, nullptr, nullptr, 0};
   if (const char* dbg = std::getenv("RS_GEMM_SK_DEBUG")) p.sk_debug = std::atoi(dbg);
   const int tiles = ceil_div(a.M, kBM * CG) * ceil_div(a.N, BN);
-  const int grid = CG * (tiles < kNumSMs / CG ? tiles : kNumSMs / CG);
+  int grid = CG * (tiles < kNumSMs / CG ? tiles : kNumSMs / CG);
   // Tail split-K: the last, partial wave of whole tiles (R tiles) costs one
   // full tile time. Splitting each of those tiles into S k ranges turns it
   // into ceil(R*S / 148) rounds of 1/S tile; pick the S (<= kMaxParts, k
   // ranges >= 16 blocks) minimising that, if it saves >= 15% of the tail.
   // Long-K GEMMs only: the fp32 partials' round trip must stay small next to
   // the saved tail.
-  const int num_kb = ceil_div(a.K, kBK);
-  const int rem = tiles % kNumSMs;
-  if (CG == 1 && TMA_OUT && a.M_dev == nullptr && streamk_enabled() && tiles > kNumSMs && rem > 0 && num_kb >= 48) {
-    int best_s = 1;
-    double best = 1.0;
-    for (int sp = 2; sp <= kMaxParts && num_kb / sp >= 16; ++sp) {
-      if (static_cast<std::size_t>(rem) * sp * kBM * BN * sizeof(float) > kSkWsBytes) break;
-      const double cost = static_cast<double>(ceil_div(rem * sp, kNumSMs)) / sp;
-      if (cost < best - 1e-9) {
-        best = cost;
-        best_s = sp;
-      }
-    }
-    if (best_s > 1 && best <= 0.85) {
+  if (CG == 1 && TMA_OUT && a.M_dev == nullptr && streamk_enabled()) {
+    const SplitPlan sp = plan_split(tiles, ceil_div(a.K, kBK), BN);
+    if (sp.splits > 1) {
       SkWorkspace& w = sk_workspace(stream);
-      p.dp_tiles = tiles - rem;
-      p.sk_tiles = rem;
-      p.sk_splits = best_s;
+      p.dp_tiles = tiles - sp.sk_tiles;
+      p.sk_tiles = sp.sk_tiles;
+      p.sk_splits = sp.splits;
       p.ws = w.ws;
       p.counters = w.counters;
+      grid = std::min(kNumSMs, p.dp_tiles + sp.sk_tiles * sp.splits);
     }
   }
   if constexpr (CG == 1) {
@@ -803,7 +829,8 @@ TileChoice pick_tile(int M, int N, int K, bool swiglu) {
       const long slots = kNumSMs / cg;
       const long waves = (tiles + slots - 1) / slots;
       const double pair_gain = num_kb >= 32 ? 0.85 : (waves <= 2 ? 1.05 : 0.93);
-      const double cost = static_cast<double>(waves * bn) * (cg == 2 ? pair_gain : 1.0);
+      const double cost = cg == 2 ? static_cast<double>(waves * bn) * pair_gain
+                                  : plan_split(static_cast<int>(tiles), num_kb, bn).cost * bn;
       if (best_cost < 0 || cost < best_cost - 1e-9) {
         best = {bn, cg};
         best_cost = cost;

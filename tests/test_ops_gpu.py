@@ -68,7 +68,9 @@ def test_gemm_store(nat, M, N, K, bn):
 # are split into k ranges (tail split-K, gemm_tcgen05.cu launch()); the others
 # check the schedule falls back to whole tiles.
 SK_SHAPES = [(2048, 3584, 18944, 224), (1024, 5120, 5120, 160), (1024, 5120, 5120, 256),
-             (4096, 1280, 3424, 160), (4096, 3840, 1280, 256)]
+             (4096, 1280, 3424, 160), (4096, 3840, 1280, 256),
+             # small grids: every tile split (the 128-token first chunk's GEMMs)
+             (128, 3584, 18944, 128), (128, 4608, 3584, 128), (100, 3584, 3584, 128), (128, 37888, 3584, 0)]
 
 
 @pytest.mark.parametrize("epi", [0, 1, 2, 3])
