@@ -173,12 +173,13 @@ def run_ours(args):
     if ws > 1:
         torch.distributed.barrier()
     torch.cuda.synchronize()
-    ttfts, dev_ms, launches = [], [], 0
+    ttfts, dev_ms, launches, host_gaps = [], [], 0, []
     with ClockSampler(local) as clk:
         for _ in range(args.steps):
             t, st = step()
             ttfts.append(t)
             dev_ms.append(st["gpu_ms"])
+            host_gaps.append(round(st["host_max_gap_ms"], 2))
             launches += st["kernel_launches"]
     torch.cuda.synchronize()
     if args.launch_list:
@@ -199,13 +200,14 @@ def run_ours(args):
     prof, gemm_shapes = group_profile(prof_raw)
     prof_steps = 1
     # e2e through the public API: H2D pixels from pinned host + D2H logits in the timed region
-    e2e_wall, e2e_gpu, h2d, d2h = [], [], 0, 0
+    e2e_wall, e2e_gpu, h2d, d2h, e2e_gaps = [], [], 0, 0, []
     for _ in range(max(1, args.warmup // 2)):
         step(e2e=True)
     for _ in range(args.steps):
         t, st = step(e2e=True)
         e2e_wall.append(st["wall_ms"])
         e2e_gpu.append(st["gpu_ms"])
+        e2e_gaps.append([round(st["host_max_gap_ms"], 2), round(st["host_last_seen_ms"], 2)])
         h2d, d2h = st["h2d_bytes"], st["d2h_bytes"]
     total_ms = sum(dev_ms)
     if ws > 1:
@@ -217,6 +219,7 @@ def run_ours(args):
         e2e_total = sum(e2e_wall)
     value = ws * args.steps * PROMPT_TOKENS / (total_ms / 1e3)
     e2e_value = ws * args.steps * PROMPT_TOKENS / (e2e_total / 1e3)
+    ttft_steps = list(ttfts)
     ttfts.sort()
     p50 = ttfts[max(0, -(-50 * len(ttfts) // 100) - 1)]
     p99 = ttfts[max(0, -(-99 * len(ttfts) // 100) - 1)]
@@ -237,6 +240,7 @@ def run_ours(args):
         "ms_per_step": total_ms / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
         "ttft_ms": {"p50": p50, "p99": p99, "mean": sum(ttfts) / len(ttfts),
+                    "per_step": [round(x, 2) for x in ttft_steps], "host_max_gap_ms": host_gaps,
                     "roofline_bound_ms": bound_sus_ms, "roofline_frac": bound_sus_ms / p50,
                     "roofline_bound_ms_burst_peak": bound_ms,
                     "roofline_note": "bound = model FLOPs / measured sustained bf16 peak (the step "
@@ -253,6 +257,7 @@ def run_ours(args):
                 "d2h_bytes_per_step": d2h, "p50_ms": statistics.median(e2e_wall),
                 "wall_ms_per_step": [round(x, 2) for x in e2e_wall],
                 "gpu_ms_per_step": [round(x, 2) for x in e2e_gpu],
+                "host_max_gap_and_last_seen_ms": e2e_gaps,
                 "timing": "host wall clock of each run (H2D pixels from pinned memory + D2H logits inside)"},
         "gpu_launches": launches,
         "roofline": {"bound": "tensor", "kernel": "gemm_tcgen05 (all GEMMs of the step)",

@@ -234,6 +234,8 @@ typedef struct rs_run_stats {
   uint64_t h2d_bytes, d2h_bytes;
   uint64_t kernel_launches;  /* our kernels launched during the run       */
   double encode_gpu_ms, prefill_gpu_ms; /* summed per-op device time      */
+  double host_max_gap_ms;    /* longest host stretch between engine polls  */
+  double host_last_seen_ms;  /* host clock when the last completion was seen */
 } rs_run_stats;
 RS_API rs_status rs_engine_run(rs_ctx* ctx, const char* workload_text,
                         const rs_sim_config* cfg, const rs_run_options* opt,

@@ -20,14 +20,20 @@ void attention_varlen_bidir(const bf16* qkv, int ld_qkv, bf16* out, int ld_out,
                             const int* cu_seqlens, int n_seqs, int max_seqlen, int total,
                             int heads, int head_dim, float scale, cudaStream_t stream);
 
-// One unit of chunked-prefill attention work: up to 128 query rows of one slice.
+// One unit of chunked-prefill attention work: up to attn_unit_rows() query
+// rows of one slice.
 struct PrefillWork {
   int q_row0;     // first chunk row of this block
-  int q_rows;     // valid rows (<= 128)
+  int q_rows;     // valid rows (<= attn_unit_rows())
   int q_pos0;     // prompt position of q_row0
   int req_slot;   // index into the per-request page-table array
 };
 constexpr int kPrefillRows = 128;
+/// Query rows per tcgen05 attention work unit: 256 for the two-tile
+/// ping-pong kernel (default), 128 for the single-tile kernel
+/// (RS_ATTN_PINGPONG=0). Callers build PrefillWork / AttnBlock units of
+/// this many rows.
+int attn_unit_rows();
 
 struct PagedKV {
   bf16* k;  // [pages][kv_heads][64 tokens][head_dim] for one layer

@@ -20,6 +20,7 @@
 #include <cuda_runtime.h>
 
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <unordered_map>
@@ -85,6 +86,20 @@ __device__ __forceinline__ float poly_exp2(float x) {
   p = fmaf(p, f, 0.99998863f);
   const int bits = __float_as_int(p) + (static_cast<int>(n) << 23);
   return x <= -127.f ? 0.f : __int_as_float(bits);
+}
+// Same on the FMA / ALU pipes only (no FRND / F2I, which share the MUFU
+// (XU) pipe): round(x) by the 1.5 * 2^23 magic add, whose low mantissa bits
+// then hold the integer part for the exponent add; 2^f on [-0.5, 0.5] by a
+// degree-3 minimax polynomial (rel. err 7.5e-5, below bf16's 3.9e-3).
+// x <= -125.5 -> 2^-125.5 (~1e-38; masked keys, vanishing next to the row max's 1).
+__device__ __forceinline__ float poly_exp2_fma(float x) {
+  x = fmaxf(x, -125.5f);
+  const float t = __fadd_rn(x, 12582912.f);
+  const float f = x - __fsub_rn(t, 12582912.f);
+  float p = fmaf(0.05517166f, f, 0.24261116f);
+  p = fmaf(p, f, 0.69326099f);
+  p = fmaf(p, f, 0.99992807f);
+  return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
 }
 
 template <int HD, KvMode MODE>
@@ -380,6 +395,339 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   }
 }
 
+// ---- two-tile ping-pong kernel -------------------------------------------------
+// A CTA owns a unit of up to 256 query rows (two 128-row tiles Q0 / Q1 of one
+// head) that share every K / V tile. The tensor core alternates between the
+// tiles — PV0_{j-1}, S0_j, PV1_{j-1}, S1_j, ... — so while one softmax
+// warpgroup turns S_t,j into P_t,j the tensor core works on the other tile:
+// the MMA pipe no longer idles for the softmax, and K / V are read from L2
+// once per 256 queries instead of per 128.
+// TMEM (512 columns): tile t owns [256t, 256t + 256): S_t (fp32, 128 cols) with
+// P_t (bf16 pairs) written over its first 64 columns, then O_t (HD cols).
+// S_t,j+1 is issued after PV_t,j (in-order tensor pipe), so P_t,j is never
+// overwritten early, and S_t,j's commit implies PV_t,j-1 is complete — the
+// softmax may rescale O_t right after S_t,j arrives, without another wait.
+// Warps: 0 TMA producer (Q, K ring), 1 MMA issuer (+ TMEM allocation), 2-5
+// softmax of Q0, 6-9 softmax of Q1 (warp w reads TMEM lanes 32 * (w % 4)),
+// 10 TMA producer (V ring).
+constexpr int kPpThreads = 352;
+
+template <int HD>
+struct PpCfg {
+  static constexpr int kHdAtoms = HD / 64;
+  static constexpr int kQBytes = kHdAtoms * kAtom;     // one 128-row Q tile
+  static constexpr int kKBytes = kHdAtoms * kAtom;     // 128 keys
+  static constexpr int kVAtom = HD * 128;              // V^T [HD x 64 keys]
+  static constexpr int kVBytes = 2 * kVAtom;           // 128 keys
+  // V ring: 2 stages (4 for small heads); K ring gets what is left (K_j is
+  // needed a full PV earlier than V_j in the issue order)
+  static constexpr int kBudget = 227 * 1024 - 2 * kQBytes - 1024 - 512;
+  static constexpr int kVStages = HD <= 64 ? 4 : 2;
+  static constexpr int kKFit = (kBudget - kVStages * kVBytes) / kKBytes;
+  static constexpr int kKStages = kKFit > 4 ? 4 : kKFit;
+  static constexpr int kSmem = 2 * kQBytes + kKStages * kKBytes + kVStages * kVBytes + 1024 + 512;
+};
+
+template <int HD, KvMode MODE>
+__global__ void __launch_bounds__(kPpThreads, 1)
+    fa_pp_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+                 const __grid_constant__ CUtensorMap tmV, const TcParams p) {
+  using C = PpCfg<HD>;
+  constexpr int SK = C::kKStages, SV = C::kVStages;
+  extern __shared__ __align__(1024) std::uint8_t smem_raw[];
+  std::uint8_t* smem = reinterpret_cast<std::uint8_t*>(
+      (reinterpret_cast<std::uintptr_t>(smem_raw) + 1023) & ~std::uintptr_t(1023));
+  std::uint8_t* sQ = smem;  // [2][kQBytes]
+  std::uint8_t* sK = sQ + 2 * C::kQBytes;
+  std::uint8_t* sV = sK + SK * C::kKBytes;
+  std::uint64_t* bars = reinterpret_cast<std::uint64_t*>(sV + SV * C::kVBytes);
+  std::uint64_t* q_full = bars;            // [2]
+  std::uint64_t* k_full = bars + 2;        // [SK]
+  std::uint64_t* k_empty = k_full + SK;    // [SK]
+  std::uint64_t* v_full = k_empty + SK;    // [SV]
+  std::uint64_t* v_empty = v_full + SV;    // [SV]
+  std::uint64_t* s_full = v_empty + SV;    // [2] S_t,j ready (and PV_t,j-1 done)
+  std::uint64_t* p_full = s_full + 2;      // [2] P_t,j written (128 softmax threads)
+  std::uint64_t* o_final = p_full + 2;     // [2] last PV_t done
+  std::uint32_t* tmem_holder = reinterpret_cast<std::uint32_t*>(o_final + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int head = blockIdx.x;
+  const int kvh = head / (p.q_heads / p.kv_heads);
+  int q_row0, q_rows, key_begin, key_end, q_pos0 = 0;
+  const int* pt = nullptr;
+  if constexpr (MODE == KvMode::kPaged) {
+    const PrefillWork w = p.work[blockIdx.y];
+    q_row0 = w.q_row0;
+    q_rows = w.q_rows;
+    q_pos0 = w.q_pos0;
+    key_begin = 0;
+    key_end = w.q_pos0 + w.q_rows;
+    pt = p.page_tables[w.req_slot];
+  } else {
+    const AttnBlock b = p.blocks[blockIdx.y];
+    q_row0 = b.q_row0;
+    q_rows = b.q_rows;
+    key_begin = b.key_begin & ~7;  // 16-B aligned V^T tile start (extra keys masked)
+    key_end = b.key_end;
+  }
+  const int rows_t[2] = {min(q_rows, 128), max(q_rows - 128, 0)};
+  int n_t[2];
+#pragma unroll
+  for (int t = 0; t < 2; ++t) {
+    const int hi = MODE == KvMode::kPaged ? q_pos0 + 128 * t + rows_t[t] : key_end;
+    n_t[t] = rows_t[t] > 0 ? (hi - key_begin + 127) / 128 : 0;
+  }
+  const int n_max = max(n_t[0], n_t[1]);
+  // last consumer of K_j / V_j (tile 1 covers every key tile tile 0 does)
+  auto last_user = [&](int j) { return j < n_t[1] ? 1 : 0; };
+
+  if (threadIdx.x == 0) {
+    sm100::tma_prefetch_desc(&tmQ);
+    sm100::tma_prefetch_desc(&tmK);
+    sm100::tma_prefetch_desc(&tmV);
+    for (int t = 0; t < 2; ++t) {
+      sm100::mbar_init(&q_full[t], 1);
+      sm100::mbar_init(&s_full[t], 1);
+      sm100::mbar_init(&p_full[t], 128);
+      sm100::mbar_init(&o_final[t], 1);
+    }
+    for (int i = 0; i < SK; ++i) {
+      sm100::mbar_init(&k_full[i], 1);
+      sm100::mbar_init(&k_empty[i], 1);
+    }
+    for (int i = 0; i < SV; ++i) {
+      sm100::mbar_init(&v_full[i], 1);
+      sm100::mbar_init(&v_empty[i], 1);
+    }
+    sm100::fence_mbar_init();
+  }
+  if (warp == 1) sm100::tmem_alloc(tmem_holder, 512);
+  sm100::tc_fence_before();
+  __syncthreads();
+  sm100::tc_fence_after();
+  const std::uint32_t tmem = *tmem_holder;
+
+  const int n_real_pages = (key_end - key_begin + 63) / 64;
+  auto pages = [&](int j, int& pa, int& pb) {
+    pa = pt[2 * j];
+    pb = 2 * j + 1 < n_real_pages ? pt[2 * j + 1] : pa;  // duplicate: finite, masked
+  };
+  if (warp == 0 && lane == 0) {
+    // ---------------- TMA producer: Q tiles and the K ring ----------------
+    for (int t = 0; t < 2; ++t) {
+      if (rows_t[t] == 0) continue;
+      sm100::mbar_expect_tx(&q_full[t], C::kQBytes);
+      for (int h = 0; h < C::kHdAtoms; ++h)
+        sm100::tma_load_2d(sQ + t * C::kQBytes + h * kAtom, &tmQ, &q_full[t],
+                           head * p.q_head_stride + h * 64, q_row0 + 128 * t);
+    }
+    for (int j = 0; j < n_max; ++j) {
+      const int st = j % SK;
+      std::uint8_t* k = sK + st * C::kKBytes;
+      sm100::mbar_wait(&k_empty[st], ((j / SK) & 1) ^ 1);
+      sm100::mbar_expect_tx(&k_full[st], C::kKBytes);
+      if constexpr (MODE == KvMode::kPaged) {
+        int pa, pb;
+        pages(j, pa, pb);
+        for (int h = 0; h < C::kHdAtoms; ++h) {
+          sm100::tma_load_2d(k + h * kAtom, &tmK, &k_full[st], h * 64, (pa * p.kv_heads + kvh) * 64);
+          sm100::tma_load_2d(k + h * kAtom + 64 * 128, &tmK, &k_full[st], h * 64,
+                             (pb * p.kv_heads + kvh) * 64);
+        }
+      } else {
+        for (int h = 0; h < C::kHdAtoms; ++h)
+          sm100::tma_load_2d(k + h * kAtom, &tmK, &k_full[st], kvh * p.q_head_stride + h * 64,
+                             key_begin + 128 * j);
+      }
+    }
+  } else if (warp == kPpThreads / 32 - 1 && lane == 0) {
+    // ---------------- TMA producer: the V ring (own thread: never queued behind K) ----------------
+    for (int j = 0; j < n_max; ++j) {
+      const int st = j % SV;
+      std::uint8_t* v = sV + st * C::kVBytes;
+      sm100::mbar_wait(&v_empty[st], ((j / SV) & 1) ^ 1);
+      sm100::mbar_expect_tx(&v_full[st], C::kVBytes);
+      if constexpr (MODE == KvMode::kPaged) {
+        int pa, pb;
+        pages(j, pa, pb);
+        sm100::tma_load_2d(v, &tmV, &v_full[st], 0, (pa * p.kv_heads + kvh) * HD);
+        sm100::tma_load_2d(v + C::kVAtom, &tmV, &v_full[st], 0, (pb * p.kv_heads + kvh) * HD);
+      } else {
+        const int k0 = key_begin + 128 * j;
+        sm100::tma_load_2d(v, &tmV, &v_full[st], k0, kvh * HD);
+        sm100::tma_load_2d(v + C::kVAtom, &tmV, &v_full[st], k0 + 64, kvh * HD);
+      }
+    }
+  } else if (warp == 1 && lane == 0) {
+    // ---------------- MMA issuer ----------------
+    constexpr std::uint32_t idesc_s = sm100::idesc_bf16_f32(128, 128);
+    constexpr std::uint32_t idesc_o = sm100::idesc_bf16_f32(128, HD);
+    for (int t = 0; t < 2; ++t)
+      if (rows_t[t] > 0) sm100::mbar_wait(&q_full[t], 0);
+    auto mma_s = [&](int t, int j) {
+      const int st = j % SK;
+      sm100::mbar_wait(&k_full[st], (j / SK) & 1);
+      sm100::tc_fence_after();
+      std::uint8_t* k = sK + st * C::kKBytes;
+#pragma unroll
+      for (int h = 0; h < C::kHdAtoms; ++h) {
+        const std::uint64_t qd = sm100::sw128_kmajor_desc(sm100::smem_u32(sQ + t * C::kQBytes + h * kAtom));
+        const std::uint64_t kd = sm100::sw128_kmajor_desc(sm100::smem_u32(k + h * kAtom));
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk)
+          sm100::umma_bf16(tmem + 256 * t, qd + 2 * kk, kd + 2 * kk, idesc_s, (h | kk) != 0 ? 1u : 0u);
+      }
+      sm100::umma_commit(&s_full[t]);
+      if (t == last_user(j)) sm100::umma_commit(&k_empty[st]);
+    };
+    auto mma_pv = [&](int t, int j) {
+      const int st = j % SV;
+      sm100::mbar_wait(&v_full[st], (j / SV) & 1);
+      sm100::mbar_wait(&p_full[t], j & 1);
+      sm100::tc_fence_after();
+      std::uint8_t* v = sV + st * C::kVBytes;
+#pragma unroll
+      for (int a = 0; a < 2; ++a) {
+        const std::uint64_t vd = sm100::sw128_kmajor_desc(sm100::smem_u32(v + a * C::kVAtom));
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk)
+          sm100::umma_bf16_ts(tmem + 256 * t + 128, tmem + 256 * t + 32 * a + 8 * kk, vd + 2 * kk,
+                              idesc_o, (j | a | kk) != 0 ? 1u : 0u);
+      }
+      if (t == last_user(j)) sm100::umma_commit(&v_empty[st]);
+      if (j == n_t[t] - 1) sm100::umma_commit(&o_final[t]);
+    };
+    if (n_t[0] > 0) mma_s(0, 0);
+    if (n_t[1] > 0) mma_s(1, 0);
+    for (int j = 1; j <= n_max; ++j) {
+      if (j - 1 < n_t[0]) mma_pv(0, j - 1);
+      if (j < n_t[0]) mma_s(0, j);
+      if (j - 1 < n_t[1]) mma_pv(1, j - 1);
+      if (j < n_t[1]) mma_s(1, j);
+    }
+  } else if (warp >= 2 && warp < 10) {
+    // ---------------- softmax: tile t, one query row per thread ----------------
+    const int t = (warp - 2) >> 2;
+    const int quad = warp & 3;
+    const int r = quad * 32 + lane;  // row within the tile
+    const int n_it = n_t[t];
+    if (n_it > 0) {
+      const std::uint32_t lane_off = static_cast<std::uint32_t>(quad * 32) << 16;
+      const std::uint32_t s_tm = tmem + lane_off + 256 * t;
+      const std::uint32_t o_tm = s_tm + 128;
+      int lo, hi;
+      if constexpr (MODE == KvMode::kPaged) {
+        lo = 0;
+        hi = min(q_pos0 + 128 * t + r + 1, key_end);
+      } else {
+        const int row = q_row0 + 128 * t + min(r, rows_t[t] - 1);
+        int a = 0, b = p.n_seqs;  // largest s with cu[s] <= row
+        while (b - a > 1) {
+          const int mid = (a + b) >> 1;
+          if (p.cu_seqlens[mid] <= row) a = mid;
+          else b = mid;
+        }
+        lo = p.cu_seqlens[a];
+        hi = p.cu_seqlens[a + 1];
+      }
+      float m = -INFINITY, l = 0.f;
+      for (int j = 0; j < n_it; ++j) {
+        sm100::mbar_wait(&s_full[t], j & 1);
+        sm100::tc_fence_after();
+        const int key0 = key_begin + j * 128;
+        const int c_lo = lo - key0, c_hi = hi - key0;  // visible columns [c_lo, c_hi)
+        std::uint32_t sv[128];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          std::uint32_t(&v)[32] = *reinterpret_cast<std::uint32_t(*)[32]>(&sv[32 * c]);
+          sm100::tmem_ld_32x32b_x32(s_tm + 32 * c, v);
+        }
+        sm100::tmem_ld_wait();
+        if (!(c_lo <= 0 && c_hi >= 128)) {
+#pragma unroll
+          for (int u = 0; u < 128; ++u)
+            if (u < c_lo || u >= c_hi) sv[u] = __float_as_uint(-INFINITY);
+        }
+        float mx8[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) mx8[u] = __uint_as_float(sv[u]);
+#pragma unroll
+        for (int u = 8; u < 128; ++u) mx8[u & 7] = fmaxf(mx8[u & 7], __uint_as_float(sv[u]));
+        float mx = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
+                         fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7])));
+        mx *= p.scale_log2;
+        const bool raise = mx > m + 8.f || (m == -INFINITY && mx != -INFINITY);
+        float alpha = 1.f;
+        if (raise) {
+          alpha = m == -INFINITY ? 0.f : exp2f(m - mx);
+          m = mx;
+        }
+        if (j > 0 && __any_sync(0xffffffffu, raise && alpha != 1.f)) {
+          // rare: rescale O_t in TMEM (PV_t,j-1 is complete: S_t,j was issued after it)
+#pragma unroll 1
+          for (int c = 0; c < HD / 32; ++c) {
+            std::uint32_t v[32];
+            sm100::tmem_ld_32x32b_x32(o_tm + 32 * c, v);
+            sm100::tmem_ld_wait();
+#pragma unroll
+            for (int u = 0; u < 32; ++u) v[u] = __float_as_uint(__uint_as_float(v[u]) * alpha);
+            sm100::tmem_st_32x32b_x32(o_tm + 32 * c, v);
+          }
+        }
+        const float mneg = m == -INFINITY ? 0.f : -m;
+        float rs8[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          std::uint32_t packed[16];  // 32 keys as bf16 pairs
+#pragma unroll
+          for (int u = 0; u < 16; ++u) {
+            const float x0 = fmaf(__uint_as_float(sv[32 * c + 2 * u]), p.scale_log2, mneg);
+            const float x1 = fmaf(__uint_as_float(sv[32 * c + 2 * u + 1]), p.scale_log2, mneg);
+            const bool poly = (u & 3) == 3;  // every 4th pair on the FMA pipe
+            const float p0 = poly ? poly_exp2_fma(x0) : fast_exp2(x0);
+            const float p1 = poly ? poly_exp2_fma(x1) : fast_exp2(x1);
+            rs8[(2 * u) & 7] += p0;
+            rs8[(2 * u + 1) & 7] += p1;
+            packed[u] = pack_bf16x2(p0, p1);
+          }
+          sm100::tmem_st_32x32b_x16(s_tm + 16 * c, packed);
+        }
+        sm100::tmem_st_wait();
+        sm100::tc_fence_before();
+        sm100::mbar_arrive(&p_full[t]);
+        l = l * alpha + (((rs8[0] + rs8[1]) + (rs8[2] + rs8[3])) + ((rs8[4] + rs8[5]) + (rs8[6] + rs8[7])));
+      }
+      sm100::mbar_wait(&o_final[t], 0);
+      sm100::tc_fence_after();
+      const float inv = l > 0.f ? 1.f / l : 0.f;
+      bf16* orow = p.out + static_cast<std::int64_t>(q_row0 + 128 * t + r) * p.ld_out + head * p.out_hd;
+#pragma unroll
+      for (int c = 0; c < HD / 32; ++c) {
+        std::uint32_t v[32];
+        sm100::tmem_ld_32x32b_x32(o_tm + 32 * c, v);
+        sm100::tmem_ld_wait();
+        if (r < rows_t[t]) {
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            if (32 * c + 8 * u < p.out_hd)
+              reinterpret_cast<uint4*>(orow + 32 * c)[u] = make_uint4(
+                  pack_bf16x2(__uint_as_float(v[8 * u]) * inv, __uint_as_float(v[8 * u + 1]) * inv),
+                  pack_bf16x2(__uint_as_float(v[8 * u + 2]) * inv, __uint_as_float(v[8 * u + 3]) * inv),
+                  pack_bf16x2(__uint_as_float(v[8 * u + 4]) * inv, __uint_as_float(v[8 * u + 5]) * inv),
+                  pack_bf16x2(__uint_as_float(v[8 * u + 6]) * inv, __uint_as_float(v[8 * u + 7]) * inv));
+          }
+        }
+      }
+    }
+  }
+  __syncthreads();
+  if (warp == 1) {
+    sm100::tc_fence_after();
+    sm100::tmem_dealloc(tmem, 512);
+  }
+}
+
 // ---- tensor maps ----------------------------------------------------------------
 using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
                                    const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
@@ -446,23 +794,35 @@ CUtensorMap cached_map(const void* base, std::int64_t rows, std::int64_t cols, s
 template <int HD, KvMode MODE>
 void launch(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv, const TcParams& p,
             int n_blocks, cudaStream_t st, const char* klass) {
-  using C = TcCfg<HD>;
   static bool set = false;
   if (!set) {
-    RS_CUDA_CHECK(cudaFuncSetAttribute(fa_tc_kernel<HD, MODE>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem));
+    RS_CUDA_CHECK(cudaFuncSetAttribute(fa_tc_kernel<HD, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       TcCfg<HD>::kSmem));
+    RS_CUDA_CHECK(cudaFuncSetAttribute(fa_pp_kernel<HD, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       PpCfg<HD>::kSmem));
     set = true;
   }
   if (n_blocks > 65535) throw DeviceError(RS_ERR_CUDA, "tc attention: too many blocks for grid.y");
   dim3 grid(p.q_heads, n_blocks);
   const int tok = prof::begin(st);
-  fa_tc_kernel<HD, MODE><<<grid, kTcThreads, C::kSmem, st>>>(tq, tk, tv, p);
+  if (attn_unit_rows() == 256)
+    fa_pp_kernel<HD, MODE><<<grid, kPpThreads, PpCfg<HD>::kSmem, st>>>(tq, tk, tv, p);
+  else
+    fa_tc_kernel<HD, MODE><<<grid, kTcThreads, TcCfg<HD>::kSmem, st>>>(tq, tk, tv, p);
   RS_LAUNCH_CHECK();
   prof::end(tok, st, klass, 0, 0);
   count_launch();
 }
 
 }  // namespace
+
+int attn_unit_rows() {
+  static const int rows = [] {
+    const char* e = std::getenv("RS_ATTN_PINGPONG");
+    return e != nullptr && e[0] == '0' ? 128 : 256;
+  }();
+  return rows;
+}
 
 void attention_prefill_paged_tc(const bf16* q, int ld_q, int q_rows_alloc, bf16* out, int ld_out,
                                 const PrefillWork* work, int n_work, const PagedKV& kv,

@@ -66,8 +66,9 @@ rs_status rs_op_attention_varlen_tc(const void* qkv, int ld_qkv, void* out, int 
     RS_CUDA_CHECK(cudaStreamSynchronize(st));
     std::vector<AttnBlock> blocks;
     std::size_t s = 0;
-    for (int r = 0; r < total; r += kPrefillRows) {
-      const int r1 = std::min(total, r + kPrefillRows);
+    const int unit = attn_unit_rows();
+    for (int r = 0; r < total; r += unit) {
+      const int r1 = std::min(total, r + unit);
       while (s + 1 < cu.size() && cu[s + 1] <= r) ++s;
       std::size_t e = s;
       while (e + 1 < cu.size() && cu[e + 1] < r1) ++e;
@@ -112,8 +113,9 @@ rs_status rs_op_attention_prefill(const void* q, int ld_q, int rows_alloc, void*
   return guarded([&] {
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     std::vector<PrefillWork> work;
-    for (int r = 0; r < q_rows; r += kPrefillRows)
-      work.push_back({r, std::min(kPrefillRows, q_rows - r), q_pos0 + r, 0});
+    const int unit = attn_unit_rows();
+    for (int r = 0; r < q_rows; r += unit)
+      work.push_back({r, std::min(unit, q_rows - r), q_pos0 + r, 0});
     PrefillWork* wd = nullptr;
     const int** ptd = nullptr;
     RS_CUDA_CHECK(cudaMallocAsync(reinterpret_cast<void**>(&wd), work.size() * sizeof(PrefillWork), st));

@@ -178,6 +178,9 @@ void DeviceBackend::prepare(const std::vector<lmmsim::RequestSpec>& workload) {
 
 void DeviceBackend::start() {
   RS_CUDA_CHECK(cudaDeviceSynchronize());
+  last_poll_ms_ = -1;
+  stats_.host_max_gap_ms = 0;
+  stats_.host_last_seen_ms = 0;
   launches0_ = launches_so_far();
   upload0_ = ctx_.uploader().bytes_uploaded();
   RS_CUDA_CHECK(cudaEventRecord(origin_, ctx_.tracker_stream()));
@@ -441,6 +444,19 @@ void DeviceBackend::on_request_complete(lmmsim::RequestId id, std::size_t chunk)
 }
 
 void DeviceBackend::poll(std::vector<lmmsim::OpCompletion>& out) {
+  const double now = clock_ms();
+  if (last_poll_ms_ >= 0) stats_.host_max_gap_ms = std::max(stats_.host_max_gap_ms, now - last_poll_ms_);
+  last_poll_ms_ = now;
+  const std::size_t n0 = out.size();
+  struct SeenStamp {  // host time of the poll that saw a completion
+    std::vector<lmmsim::OpCompletion>& v;
+    std::size_t n0;
+    double now;
+    double& seen;
+    ~SeenStamp() {
+      if (v.size() > n0) seen = now;
+    }
+  } stamp{out, n0, now, stats_.host_last_seen_ms};
   for (const auto& [slot, t] : ready_transfers_) out.push_back({lmmsim::OpKind::Transfer, 0, slot, t});
   ready_transfers_.clear();
   for (std::size_t i = 0; i < ops_.size();) {

@@ -153,6 +153,7 @@ class DeviceBackend final : public lmmsim::ExecutionBackend {
   void* header_sink_ = nullptr;
   float* remote_logits_ = nullptr;  // [max_requests, vocab] when the LM head is remote
   double remote_last_ms_ = 0;
+  double last_poll_ms_ = -1;  // host-side stall diagnostics (rs_run_stats)
 };
 
 }  // namespace rserve

@@ -379,9 +379,10 @@ void Context::prefill(const std::vector<SliceRef>& slices, bf16* x, cudaStream_t
       rows.push_back({sl.req->slot, static_cast<std::int32_t>(p), {rp[0], rp[1], rp[2]}, 0});
       if (first) gather.push_back(sl.req->slab_row(p));
     }
-    for (std::uint64_t q = sl.start; q < sl.end; q += kPrefillRows)
+    const std::uint64_t unit = static_cast<std::uint64_t>(attn_unit_rows());
+    for (std::uint64_t q = sl.start; q < sl.end; q += unit)
       work.push_back({base + static_cast<int>(q - sl.start),
-                      static_cast<int>(std::min<std::uint64_t>(kPrefillRows, sl.end - q)),
+                      static_cast<int>(std::min<std::uint64_t>(unit, sl.end - q)),
                       static_cast<int>(q), sl.req->slot});
     if (sl.end == sl.req->total) {
       done_rows.push_back(base + static_cast<std::int64_t>(sl.end - sl.start) - 1);

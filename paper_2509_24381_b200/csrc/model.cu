@@ -164,8 +164,9 @@ void finalize_plan(VitBatchPlan& plan) {
   plan.win_blocks.clear();
   for (std::size_t i = 0; i + 1 < plan.cu_item.size(); ++i) {
     const int a = plan.cu_item[i], b = plan.cu_item[i + 1];
-    for (int r = a; r < b; r += kPrefillRows)
-      plan.full_blocks.push_back({r, std::min(kPrefillRows, b - r), a, b});
+    const int unit = attn_unit_rows();
+    for (int r = a; r < b; r += unit)
+      plan.full_blocks.push_back({r, std::min(unit, b - r), a, b});
   }
   // largest images first (LPT issue order, see attention_tc.cu)
   std::stable_sort(plan.full_blocks.begin(), plan.full_blocks.end(), [](const AttnBlock& x, const AttnBlock& y) {

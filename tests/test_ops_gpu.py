@@ -284,7 +284,9 @@ def _paged_case(nat, hd, hq, hkv, pos0, rows, seed=0):
 
 @pytest.mark.parametrize("hd,hq,hkv,pos0,rows", [(128, 28, 4, 0, 2048), (128, 28, 4, 6528, 2048),
                                                  (128, 4, 1, 300, 77), (64, 8, 2, 0, 1),
-                                                 (64, 8, 2, 63, 130), (128, 7, 7, 1000, 256)])
+                                                 (64, 8, 2, 63, 130), (128, 7, 7, 1000, 256),
+                                                 # cfg2 per-image chunks (256-row units + ragged tail)
+                                                 (128, 28, 4, 1000, 1056), (128, 28, 4, 7520, 1056)])
 def test_attention_prefill_tcgen05(nat, hd, hq, hkv, pos0, rows):
     out, ref = _paged_case(nat, hd, hq, hkv, pos0, rows)
     _close(out, ref)
