@@ -179,7 +179,8 @@ def run_ours(args):
             t, st = step()
             ttfts.append(t)
             dev_ms.append(st["gpu_ms"])
-            host_gaps.append(round(st["host_max_gap_ms"], 2))
+            host_gaps.append([round(st["host_max_gap_ms"], 2), round(st["host_max_call_ms"], 2),
+                              int(st["host_max_call_kind"])])
             launches += st["kernel_launches"]
     torch.cuda.synchronize()
     if args.launch_list:

@@ -236,6 +236,9 @@ typedef struct rs_run_stats {
   double encode_gpu_ms, prefill_gpu_ms; /* summed per-op device time      */
   double host_max_gap_ms;    /* longest host stretch between engine polls  */
   double host_last_seen_ms;  /* host clock when the last completion was seen */
+  double host_max_call_ms;   /* longest backend call (launch / scatter)    */
+  int32_t host_max_call_kind; /* 0 encode, 1 stage, 2 scatter, 3 transfer  */
+  int32_t reserved0;
 } rs_run_stats;
 RS_API rs_status rs_engine_run(rs_ctx* ctx, const char* workload_text,
                         const rs_sim_config* cfg, const rs_run_options* opt,

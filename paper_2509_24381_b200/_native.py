@@ -131,7 +131,9 @@ class rs_run_stats(C.Structure):
     _fields_ = [("wall_ms", C.c_double), ("gpu_ms", C.c_double), ("h2d_bytes", C.c_uint64),
                 ("d2h_bytes", C.c_uint64), ("kernel_launches", C.c_uint64),
                 ("encode_gpu_ms", C.c_double), ("prefill_gpu_ms", C.c_double),
-                ("host_max_gap_ms", C.c_double), ("host_last_seen_ms", C.c_double)]
+                ("host_max_gap_ms", C.c_double), ("host_last_seen_ms", C.c_double),
+                ("host_max_call_ms", C.c_double), ("host_max_call_kind", C.c_int32),
+                ("reserved0", C.c_int32)]
 
 
 def _sig(name, argtypes, restype=C.c_int):

@@ -611,7 +611,8 @@ __global__ void __launch_bounds__(kPpThreads, 1)
     const int t = (warp - 2) >> 2;
     const int quad = warp & 3;
     const int r = quad * 32 + lane;  // row within the tile
-    const int n_it = n_t[t];
+    const int n_it = t == 0 ? n_t[0] : n_t[1];
+    const int my_rows = t == 0 ? rows_t[0] : rows_t[1];
     if (n_it > 0) {
       const std::uint32_t lane_off = static_cast<std::uint32_t>(quad * 32) << 16;
       const std::uint32_t s_tm = tmem + lane_off + 256 * t;
@@ -621,7 +622,7 @@ __global__ void __launch_bounds__(kPpThreads, 1)
         lo = 0;
         hi = min(q_pos0 + 128 * t + r + 1, key_end);
       } else {
-        const int row = q_row0 + 128 * t + min(r, rows_t[t] - 1);
+        const int row = q_row0 + 128 * t + min(r, my_rows - 1);
         int a = 0, b = p.n_seqs;  // largest s with cu[s] <= row
         while (b - a > 1) {
           const int mid = (a + b) >> 1;
@@ -707,7 +708,7 @@ __global__ void __launch_bounds__(kPpThreads, 1)
         std::uint32_t v[32];
         sm100::tmem_ld_32x32b_x32(o_tm + 32 * c, v);
         sm100::tmem_ld_wait();
-        if (r < rows_t[t]) {
+        if (r < my_rows) {
 #pragma unroll
           for (int u = 0; u < 4; ++u) {
             if (32 * c + 8 * u < p.out_hd)

@@ -181,6 +181,8 @@ void DeviceBackend::start() {
   last_poll_ms_ = -1;
   stats_.host_max_gap_ms = 0;
   stats_.host_last_seen_ms = 0;
+  stats_.host_max_call_ms = 0;
+  stats_.host_max_call_kind = -1;
   launches0_ = launches_so_far();
   upload0_ = ctx_.uploader().bytes_uploaded();
   RS_CUDA_CHECK(cudaEventRecord(origin_, ctx_.tracker_stream()));
@@ -212,7 +214,23 @@ void DeviceBackend::on_request_created(const lmmsim::RequestSpec& req, const lmm
   RS_CUDA_CHECK(cudaEventRecord(tracker_tail_, st));
 }
 
+// Host-side stall diagnostics: the longest backend call of a run.
+struct CallTimer {
+  DeviceBackend* be;
+  int kind;
+  std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
+  ~CallTimer() { be->note_call(kind, std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count()); }
+};
+
+void DeviceBackend::note_call(int kind, double ms) {
+  if (ms > stats_.host_max_call_ms) {
+    stats_.host_max_call_ms = ms;
+    stats_.host_max_call_kind = kind;
+  }
+}
+
 double DeviceBackend::launch_encode(int worker, std::size_t slot, const lmmsim::EncodeBatch& b) {
+  CallTimer timer{this, 0};
   if (remote_ != nullptr) {
     launch_remote_encode(worker, slot, b);
     return realtime_ ? 0.0 : lmmsim::encode_time_ms(cfg_.cost, b);
@@ -265,6 +283,7 @@ double DeviceBackend::launch_transfer(int /*worker*/, std::size_t slot, const lm
 }
 
 void DeviceBackend::on_embeddings_ready(std::size_t slot, const lmmsim::EncodeBatch& b) {
+  CallTimer timer{this, 2};
   cudaStream_t st = ctx_.tracker_stream();
   if (remote_ != nullptr) remote_->t->wait_posted(*slot_xfer_.at(slot));
   RS_CUDA_CHECK(cudaStreamWaitEvent(st, slot_done_.at(slot), 0));
@@ -282,6 +301,7 @@ void DeviceBackend::on_embeddings_ready(std::size_t slot, const lmmsim::EncodeBa
 }
 
 double DeviceBackend::launch_stage(int stage, const lmmsim::ChunkView& c) {
+  CallTimer timer{this, 1};
   const double cost = realtime_ ? 0.0 : lmmsim::stage_time_ms(cfg_.cost, c.total_tokens, c.weighted_context);
   if (remote_ != nullptr && stage > 0) {  // runs on rank P_stage; completion = its DONE message
     for (RemoteOp& op : remote_ops_)

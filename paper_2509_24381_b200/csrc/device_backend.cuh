@@ -67,6 +67,7 @@ class DeviceBackend final : public lmmsim::ExecutionBackend {
   void collect();
 
   rs_run_stats stats() const { return stats_; }
+  void note_call(int kind, double ms);
   /// Logits / argmax of completed requests (host copies after finish()).
   const std::unordered_map<lmmsim::RequestId, std::vector<float>>& logits() const { return logits_; }
   const std::unordered_map<lmmsim::RequestId, std::int32_t>& argmax() const { return argmax_; }
