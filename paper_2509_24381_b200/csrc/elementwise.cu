@@ -62,6 +62,17 @@ __global__ void fill_const_kernel(bf16* dst, std::int64_t n, float v) {
     dst[e] = __float2bfloat16_rn(v);
 }
 
+__global__ void fold_norm_weight_kernel(bf16* W, std::int64_t rows, int cols, int ld, const bf16* g) {
+  const std::int64_t n = rows * cols;
+  for (std::int64_t e = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; e < n;
+       e += static_cast<std::int64_t>(gridDim.x) * blockDim.x) {
+    const std::int64_t r = e / cols;
+    const int c = static_cast<int>(e - r * cols);
+    bf16& w = W[r * ld + c];
+    w = __float2bfloat16_rn(__bfloat162float(w) * __bfloat162float(g[c]));
+  }
+}
+
 __global__ void fill_ids_kernel(std::int32_t* dst, std::int64_t n, std::uint64_t seed,
                                 std::uint64_t stream, std::uint32_t modulo) {
   for (std::int64_t e = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; e < n;
@@ -457,6 +468,13 @@ void fill_uniform_interleaved(bf16* dst, int rows_valid, int rows_pad, int cols,
                               cudaStream_t st) {
   fill_interleaved_kernel<<<elem_grid(static_cast<std::int64_t>(rows_pad) * ld), 256, 0, st>>>(
       dst, rows_valid, rows_pad, cols, ld, seed, stream, scale, which);
+  RS_LAUNCH_CHECK();
+  count_launch();
+}
+
+void fold_norm_weight(bf16* W, std::int64_t rows, int cols, int ld, const bf16* g, cudaStream_t st) {
+  if (rows <= 0 || cols <= 0) return;
+  fold_norm_weight_kernel<<<elem_grid(rows * cols), 256, 0, st>>>(W, rows, cols, ld, g);
   RS_LAUNCH_CHECK();
   count_launch();
 }

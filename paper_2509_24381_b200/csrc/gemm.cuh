@@ -44,7 +44,21 @@ struct GemmArgs {
   const int* row_map = nullptr;    // optional: output row of input row m
   int M = 0, N = 0, K = 0;
   const int* M_dev = nullptr;      // optional device-side M (<= M), graph-friendly
+  // RMSNorm folded into the GEMMs around it (model.cu). A norm's consumer
+  // GEMM reads the un-normalised residual stream x and scales output row r by
+  // rsqrt(ss_in[r] * 2^-16 * ss_inv_dim + ss_eps) before the bias (the norm
+  // weight is folded into B's columns at load). The residual GEMM producing x
+  // adds each epilogue thread's sum of squares of its bf16 output row segment
+  // to ss_out[r] as 2^-16 fixed point (64-bit integer atomics: the total is
+  // independent of the order, so runs stay bit-reproducible) and zeroes
+  // ss_clear[0, ss_clear_n) for the next producer (ping-pong buffers).
+  const unsigned long long* ss_in = nullptr;
+  float ss_inv_dim = 0.f, ss_eps = 0.f;
+  unsigned long long* ss_out = nullptr;
+  unsigned long long* ss_clear = nullptr;
+  int ss_clear_n = 0;
 };
+constexpr float kSsFixedScale = 65536.f;  // 2^16
 
 /// Launches the tcgen05 GEMM. Requires K % 8 == 0, N % 16 == 0,
 /// 16-byte aligned rows. Tile width is picked for wave efficiency.

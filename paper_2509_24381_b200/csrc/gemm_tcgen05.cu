@@ -39,7 +39,23 @@ struct GemmParams {
   float* ws;     // split partials: [sk_splits][sk_tiles][kBM x BN] fp32
   int* counters; // per split tile arrival counts (self-resetting)
   int sk_debug;  // RS_GEMM_SK_DEBUG: 1 = no partial stores / fixup, 2 = no finisher epilogue
+  // folded RMSNorm (gemm.cuh GemmArgs)
+  const unsigned long long* ss_in;
+  float ss_inv_dim, ss_eps;
+  unsigned long long* ss_out;
+  unsigned long long* ss_clear;
+  int ss_clear_n;
 };
+
+// Row scale of a norm-consumer GEMM (1 when the GEMM has no folded norm).
+__device__ __forceinline__ float row_scale(const GemmParams& p, int row) {
+  if (p.ss_in == nullptr || row >= p.M) return 1.f;
+  const float ss = static_cast<float>(__ldcg(p.ss_in + row)) * (1.f / kSsFixedScale);
+  return rsqrtf(ss * p.ss_inv_dim + p.ss_eps);
+}
+__device__ __forceinline__ void ss_accumulate(const GemmParams& p, int row, float ss) {
+  atomicAdd(p.ss_out + row, static_cast<unsigned long long>(__float2ull_rn(ss * kSsFixedScale)));
+}
 
 // ---- work units ---------------------------------------------------------------
 // A unit is (tile, [kb0, kb1)). Producer, MMA issuer and epilogue walk the same
@@ -144,6 +160,9 @@ __device__ __forceinline__ void epilogue_tile_tma(const GemmParams& p, const CUt
                                                   int n0, int quad, int half, int lane,
                                                   const float* const (&parts)[kMaxParts] = {},
                                                   int n_parts = 0) {
+  const int my_row = m0 + quad * 32 + lane;
+  const float rs = row_scale(p, my_row);
+  float ss = 0.f;  // sum of squares of this thread's output row segment (ss_out)
   constexpr bool kRes = EPI == static_cast<int>(Epi::Residual);
   constexpr bool kSwi = EPI == static_cast<int>(Epi::SwiGLU);
   constexpr bool kF32 = EPI == static_cast<int>(Epi::StoreF32);
@@ -197,13 +216,17 @@ __device__ __forceinline__ void epilogue_tile_tma(const GemmParams& p, const CUt
         // [g0..15 u0..15 | g16..31 u16..31] -> 32 outputs
 #pragma unroll
         for (int t = 0; t < 16; ++t) {
-          x[t] = silu_plus(__uint_as_float(v[t]), p.bias, n0 + c * 64 + t) *
-                 bias_add(__uint_as_float(v[16 + t]), p.bias, n0 + c * 64 + 16 + t);
-          x[16 + t] = silu_plus(__uint_as_float(u[t]), p.bias, n0 + c * 64 + 32 + t) *
-                      bias_add(__uint_as_float(u[16 + t]), p.bias, n0 + c * 64 + 48 + t);
+          x[t] = silu_plus(rs * __uint_as_float(v[t]), p.bias, n0 + c * 64 + t) *
+                 bias_add(rs * __uint_as_float(v[16 + t]), p.bias, n0 + c * 64 + 16 + t);
+          x[16 + t] = silu_plus(rs * __uint_as_float(u[t]), p.bias, n0 + c * 64 + 32 + t) *
+                      bias_add(rs * __uint_as_float(u[16 + t]), p.bias, n0 + c * 64 + 48 + t);
         }
       } else {
         if constexpr (!FROM_WS) sm100::tmem_ld_wait();
+        if (p.ss_in != nullptr) {
+#pragma unroll
+          for (int t = 0; t < 32; ++t) v[t] = __float_as_uint(rs * __uint_as_float(v[t]));
+        }
         const int col = n0 + c * 32;
         if (p.bias != nullptr && col < p.N) {
 #pragma unroll
@@ -248,10 +271,21 @@ __device__ __forceinline__ void epilogue_tile_tma(const GemmParams& p, const CUt
             make_float4(x[4 * q], x[4 * q + 1], x[4 * q + 2], x[4 * q + 3]);
     } else {
 #pragma unroll
-      for (int q = 0; q < 4; ++q)
-        *reinterpret_cast<uint4*>(buf + sm100::sw64(lane * kRowBytes + q * 16)) =
-            make_uint4(pack_bf16x2(x[8 * q], x[8 * q + 1]), pack_bf16x2(x[8 * q + 2], x[8 * q + 3]),
-                       pack_bf16x2(x[8 * q + 4], x[8 * q + 5]), pack_bf16x2(x[8 * q + 6], x[8 * q + 7]));
+      for (int q = 0; q < 4; ++q) {
+        const uint4 o = make_uint4(pack_bf16x2(x[8 * q], x[8 * q + 1]), pack_bf16x2(x[8 * q + 2], x[8 * q + 3]),
+                                   pack_bf16x2(x[8 * q + 4], x[8 * q + 5]), pack_bf16x2(x[8 * q + 6], x[8 * q + 7]));
+        *reinterpret_cast<uint4*>(buf + sm100::sw64(lane * kRowBytes + q * 16)) = o;
+        if constexpr (kRes) {
+          if (p.ss_out != nullptr) {  // the bf16 values the next GEMM reads
+            const std::uint32_t ow[4] = {o.x, o.y, o.z, o.w};
+#pragma unroll
+            for (int t = 0; t < 4; ++t) {
+              const float2 f = unpack_bf16x2(ow[t]);
+              ss = fmaf(f.x, f.x, fmaf(f.y, f.y, ss));
+            }
+          }
+        }
+      }
     }
     sm100::fence_proxy_async_smem();
     __syncwarp();
@@ -260,14 +294,17 @@ __device__ __forceinline__ void epilogue_tile_tma(const GemmParams& p, const CUt
       sm100::bulk_commit();
     }
   }
+  if constexpr (kRes) {
+    if (p.ss_out != nullptr && c_begin < c_end && my_row < p.M) ss_accumulate(p, my_row, ss);
+  }
 }
 
 template <int EPI>
 __device__ __forceinline__ void epilogue_chunk(const GemmParams& p, int row, int col,
-                                               const std::uint32_t (&v)[32]) {
+                                               const std::uint32_t (&v)[32], float rs, float& ss) {
   float x[32];
 #pragma unroll
-  for (int i = 0; i < 32; ++i) x[i] = __uint_as_float(v[i]);
+  for (int i = 0; i < 32; ++i) x[i] = rs * __uint_as_float(v[i]);
   const int nvalid = min(32, p.N - col);  // 16 or 32 (N % 16 == 0)
   if (p.bias != nullptr) {
 #pragma unroll
@@ -326,11 +363,21 @@ __device__ __forceinline__ void epilogue_chunk(const GemmParams& p, int row, int
     bf16* c = static_cast<bf16*>(p.C) + static_cast<std::int64_t>(out_row) * p.ldc + col;
 #pragma unroll
     for (int q = 0; q < 4; ++q)
-      if (q * 8 < nvalid)
-        reinterpret_cast<uint4*>(c)[q] =
-            make_uint4(pack_bf16x2(x[8 * q], x[8 * q + 1]), pack_bf16x2(x[8 * q + 2], x[8 * q + 3]),
-                       pack_bf16x2(x[8 * q + 4], x[8 * q + 5]),
-                       pack_bf16x2(x[8 * q + 6], x[8 * q + 7]));
+      if (q * 8 < nvalid) {
+        const uint4 o = make_uint4(pack_bf16x2(x[8 * q], x[8 * q + 1]), pack_bf16x2(x[8 * q + 2], x[8 * q + 3]),
+                                   pack_bf16x2(x[8 * q + 4], x[8 * q + 5]),
+                                   pack_bf16x2(x[8 * q + 6], x[8 * q + 7]));
+        reinterpret_cast<uint4*>(c)[q] = o;
+        if (EPI == static_cast<int>(Epi::Residual) && p.ss_out != nullptr) {
+          const std::uint32_t ow[4] = {o.x, o.y, o.z, o.w};
+#pragma unroll
+          for (int t = 0; t < 4; ++t) {
+            const float2 f = unpack_bf16x2(ow[t]);
+            ss = fmaf(f.x, f.x, fmaf(f.y, f.y, ss));
+          }
+        }
+      }
+
   }
 }
 
@@ -358,6 +405,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
+  for (int i = blockIdx.x * kThreads + threadIdx.x; i < p.ss_clear_n; i += gridDim.x * kThreads)
+    p.ss_clear[i] = 0ull;
   // CTA pair: rank 0 (leader) issues the MMAs; both CTAs load and drain.
   const std::uint32_t rank = CG == 2 ? sm100::cluster_ctarank() : 0u;
   const int M = p.M_dev != nullptr ? min(*p.M_dev, p.M) : p.M;
@@ -557,13 +606,17 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int row = m0 + quad * 32 + lane;
         constexpr int kCh = BN / 32;
         const int c0 = half == 0 ? 0 : (kCh + 1) / 2, c1 = half == 0 ? (kCh + 1) / 2 : kCh;
+        const float rs = row_scale(p, row);
+        float ss = 0.f;
 #pragma unroll 1
         for (int c = 32 * c0; c < 32 * c1; c += 32) {
           std::uint32_t v[32];
           sm100::tmem_ld_32x32b_x32(t_row + static_cast<std::uint32_t>(c), v);
           sm100::tmem_ld_wait();
-          if (row < M && n0 + c < p.N) epilogue_chunk<EPI>(p, row, n0 + c, v);
+          if (row < M && n0 + c < p.N) epilogue_chunk<EPI>(p, row, n0 + c, v, rs, ss);
         }
+        if (EPI == static_cast<int>(Epi::Residual) && p.ss_out != nullptr && row < M && c0 < c1)
+          ss_accumulate(p, row, ss);
       }
       sm100::tc_fence_before();
       __syncwarp();
@@ -737,7 +790,8 @@ void launch(const GemmArgs& a, cudaStream_t stream) {
       tmR = make_map(a.residual, false, a.M, a.N, a.ldr, 32, 32);
   }
   GemmParams p{a.C, a.ldc, a.bias, a.residual, a.ldr, a.row_map, a.M, a.N, a.K, a.M_dev,
-               0, 0, 0, nullptr, nullptr, 0};
+               0, 0, 0, nullptr, nullptr, 0,
+               a.ss_in, a.ss_inv_dim, a.ss_eps, a.ss_out, a.ss_clear, a.ss_clear_n};
   if (const char* dbg = std::getenv("RS_GEMM_SK_DEBUG")) p.sk_debug = std::atoi(dbg);
   const int tiles = ceil_div(a.M, kBM * CG) * ceil_div(a.N, BN);
   int grid = CG * (tiles < kNumSMs / CG ? tiles : kNumSMs / CG);

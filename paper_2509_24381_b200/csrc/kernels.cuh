@@ -35,6 +35,10 @@ void fill_uniform_interleaved(bf16* dst, int rows_valid, int rows_pad, int cols,
                               std::uint64_t seed, std::uint64_t stream, float scale, int which,
                               cudaStream_t st);
 void fill_const(bf16* dst, std::int64_t n, float v, cudaStream_t st);
+/// Folds an RMSNorm weight into the consumer linear: W[r, c] *= g[c]
+/// ([rows, cols] with row stride ld), so the GEMM may read the
+/// un-normalised stream and apply the per-row rsqrt scale in its epilogue.
+void fold_norm_weight(bf16* W, std::int64_t rows, int cols, int ld, const bf16* g, cudaStream_t st);
 /// int32 ids in [0, modulo): id = mix64(seed, stream, i) % modulo.
 void fill_ids(std::int32_t* dst, std::int64_t n, std::uint64_t seed, std::uint64_t stream,
               std::uint32_t modulo, cudaStream_t st);

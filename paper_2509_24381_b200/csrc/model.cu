@@ -135,6 +135,12 @@ void Vit::init(const Shapes& s, DeviceArena& a, int max_patches, cudaStream_t st
     L.down_w = make_linear(a, s.vd, s.vff, s.vff_pad, seed, id(kVit, lid, kDownW), st);
     L.down_b = make_linear(a, 1, s.vd, s.vd, seed, id(kVit, lid, kDownB), st);
   }
+  // RMSNorm weights folded into the consumer GEMMs (QKV <- ln1, gate/up <- ln2)
+  for (VitLayer& L : layers_) {
+    fold_norm_weight(L.qkv_w, 3LL * s.vd, s.vd, s.vd, L.ln1, st);
+    fold_norm_weight(L.gu_w, 2LL * s.vff_pad, s.vd, s.vd, L.ln2, st);
+  }
+  unit_ln_ = make_ones(a, s.vd, st);
   merger_ln_ = make_ones(a, s.vd, st);
   fc1_w_ = make_linear(a, s.merge_in, s.merge_in, s.merge_in, seed, id(kMerger, 0, kFc1W), st);
   fc1_b_ = make_linear(a, 1, s.merge_in, s.merge_in, seed, id(kMerger, 0, kFc1B), st);
@@ -157,6 +163,8 @@ void Vit::init(const Shapes& s, DeviceArena& a, int max_patches, cudaStream_t st
   RS_CUDA_CHECK(cudaMemsetAsync(kp_, 0, padded * 2, st));
   RS_CUDA_CHECK(cudaMemsetAsync(vt_, 0, padded * 2, st));
   rope_table_ = static_cast<float2*>(a.alloc(static_cast<std::size_t>(P) * (s.vhd / 2) * sizeof(float2)));
+  ss_a_ = static_cast<unsigned long long*>(a.alloc(static_cast<std::size_t>(P) * 8));
+  ss_b_ = static_cast<unsigned long long*>(a.alloc(static_cast<std::size_t>(P) * 8));
 }
 
 void finalize_plan(VitBatchPlan& plan) {
@@ -204,11 +212,23 @@ void Vit::encode(const VitBatchPlan& plan, const bf16* patches, const std::int32
   const int n_win = static_cast<int>(plan.cu_window.size()) - 1;
   const int n_items = static_cast<int>(plan.cu_item.size()) - 1;
   vit_rope_table(pos_hw, P, s.vhd, s.cfg.rope_theta_vit, rope_table_, st);
+  // Folded RMSNorm (gemm.cuh): the residual GEMMs hand per-row sums of
+  // squares (ss_a_ after down, ss_b_ after O) to the norm-consumer GEMMs
+  // (QKV, gate/up), each zeroing the other buffer for the next producer;
+  // layer 0's ln1 input comes from the patch embedding: explicit norm.
+  RS_CUDA_CHECK(cudaMemsetAsync(ss_b_, 0, static_cast<std::size_t>(P) * 8, st));
+  const float inv_vd = 1.0f / static_cast<float>(s.vd);
   for (int l = 0; l < s.vl; ++l) {
     const VitLayer& L = layers_[static_cast<std::size_t>(l)];
-    rmsnorm(x_, s.vd, L.ln1, xn_, s.vd, P, s.vd, s.eps, st);
     g = GemmArgs{};
-    g.A = xn_; g.lda = s.vd; g.B = L.qkv_w; g.ldb = s.vd; g.C = qkv_; g.ldc = 3 * s.vd;
+    if (l == 0) {
+      rmsnorm(x_, s.vd, unit_ln_, xn_, s.vd, P, s.vd, s.eps, st);
+      g.A = xn_;
+    } else {
+      g.A = x_;
+      g.ss_in = ss_a_; g.ss_inv_dim = inv_vd; g.ss_eps = s.eps;
+    }
+    g.lda = s.vd; g.B = L.qkv_w; g.ldb = s.vd; g.C = qkv_; g.ldc = 3 * s.vd;
     g.bias = L.qkv_b; g.M = P; g.N = 3 * s.vd; g.K = s.vd;
     gemm(g, Epi::Store, st);
     if (s.full_attention_layer(l)) {
@@ -227,15 +247,17 @@ void Vit::encode(const VitBatchPlan& plan, const bf16* patches, const std::int32
     g = GemmArgs{};
     g.A = att_; g.lda = s.vd; g.B = L.o_w; g.ldb = s.vd; g.C = x_; g.ldc = s.vd; g.bias = L.o_b;
     g.residual = x_; g.ldr = s.vd; g.M = P; g.N = s.vd; g.K = s.vd;
+    g.ss_out = ss_b_; g.ss_clear = ss_a_; g.ss_clear_n = P;
     gemm(g, Epi::Residual, st);
-    rmsnorm(x_, s.vd, L.ln2, xn_, s.vd, P, s.vd, s.eps, st);
     g = GemmArgs{};
-    g.A = xn_; g.lda = s.vd; g.B = L.gu_w; g.ldb = s.vd; g.C = h_; g.ldc = s.vff_pad;
+    g.A = x_; g.lda = s.vd; g.B = L.gu_w; g.ldb = s.vd; g.C = h_; g.ldc = s.vff_pad;
     g.bias = L.gu_b; g.M = P; g.N = 2 * s.vff_pad; g.K = s.vd;
+    g.ss_in = ss_b_; g.ss_inv_dim = inv_vd; g.ss_eps = s.eps;
     gemm(g, Epi::SwiGLU, st);
     g = GemmArgs{};
     g.A = h_; g.lda = s.vff_pad; g.B = L.down_w; g.ldb = s.vff_pad; g.C = x_; g.ldc = s.vd;
     g.bias = L.down_b; g.residual = x_; g.ldr = s.vd; g.M = P; g.N = s.vd; g.K = s.vff_pad;
+    g.ss_out = ss_a_; g.ss_clear = ss_b_; g.ss_clear_n = P;
     gemm(g, Epi::Residual, st);
   }
   // patch merger: RMSNorm per patch, 2x2 groups are 4 consecutive rows ->
@@ -303,6 +325,12 @@ void Llm::init(const Shapes& s, DeviceArena& a, int lb, int le, bool with_embed,
     RS_CUDA_CHECK(cudaMemsetAsync(L.v_cache, 0, static_cast<std::size_t>(kv_elems) * 2, st));
   }
   kv_pages_ = kv_pages;
+  // RMSNorm weights folded into the consumer GEMMs (QKV <- ln1, gate/up <- ln2)
+  for (LlmLayer& L : layers_) {
+    fold_norm_weight(L.qkv_w, s.qkv_dim, s.d, s.d, L.ln1, st);
+    fold_norm_weight(L.gu_w, 2LL * s.ff, s.d, s.d, L.ln2, st);
+  }
+  unit_ln_ = make_ones(a, s.d, st);
   if (with_head) {
     final_ln_ = make_ones(a, s.d, st);
     head_ = make_linear(a, s.vocab, s.d, s.d, seed, id(kTop, 0, kHead), st);
@@ -311,6 +339,8 @@ void Llm::init(const Shapes& s, DeviceArena& a, int lb, int le, bool with_embed,
     xf_ = alloc_bf16(a, static_cast<std::int64_t>(max_chunk) * s.d);
   }
   const std::int64_t M = max_chunk;
+  ss_a_ = static_cast<unsigned long long*>(a.alloc(static_cast<std::size_t>(M) * 8));
+  ss_b_ = static_cast<unsigned long long*>(a.alloc(static_cast<std::size_t>(M) * 8));
   xn_ = alloc_bf16(a, M * s.d);
   qkv_ = alloc_bf16(a, M * s.qkv_dim);
   att_ = alloc_bf16(a, M * s.hq * s.hd);
@@ -327,14 +357,27 @@ void Llm::forward_stage(const ChunkDev& c, const bf16* slab, bf16* x,
   if (M > max_m_) throw DeviceError(RS_ERR_CUDA, "llm: chunk exceeds max_chunk_tokens");
   const float scale = 1.0f / std::sqrt(static_cast<float>(s.hd));
   GemmArgs g;
+  // Folded RMSNorm (gemm.cuh): the residual GEMMs hand per-row sums of
+  // squares (ss_a_ after down, ss_b_ after O) to the norm-consumer GEMMs
+  // (QKV, gate/up), each zeroing the other buffer for the next producer. The
+  // first layer of the call normalises explicitly (unit weight: ln1 lives in
+  // qkv_w).
+  RS_CUDA_CHECK(cudaMemsetAsync(ss_b_, 0, static_cast<std::size_t>(M) * 8, st));
+  const float inv_d = 1.0f / static_cast<float>(s.d);
   for (int l = l_from; l < l_to; ++l) {
     const LlmLayer& L = layers_[static_cast<std::size_t>(l - lb_)];
-    if (l == 0)  // chunk input: gather slot rows (K8 fused into the first norm)
-      rmsnorm(slab, s.d, L.ln1, xn_, s.d, M, s.d, s.eps, st, c.gather_rows, x, s.d);
-    else
-      rmsnorm(x, s.d, L.ln1, xn_, s.d, M, s.d, s.eps, st);
     g = GemmArgs{};
-    g.A = xn_; g.lda = s.d; g.B = L.qkv_w; g.ldb = s.d; g.C = qkv_; g.ldc = s.qkv_dim;
+    if (l == l_from) {
+      if (l == 0)  // chunk input: gather slot rows (K8 fused into the first norm)
+        rmsnorm(slab, s.d, unit_ln_, xn_, s.d, M, s.d, s.eps, st, c.gather_rows, x, s.d);
+      else
+        rmsnorm(x, s.d, unit_ln_, xn_, s.d, M, s.d, s.eps, st);
+      g.A = xn_;
+    } else {
+      g.A = x;
+      g.ss_in = ss_a_; g.ss_inv_dim = inv_d; g.ss_eps = s.eps;
+    }
+    g.lda = s.d; g.B = L.qkv_w; g.ldb = s.d; g.C = qkv_; g.ldc = s.qkv_dim;
     g.bias = L.qkv_b; g.M = M; g.N = s.qkv_dim; g.K = s.d;
     gemm(g, Epi::Store, st);
     rope_kv_append(qkv_, s.qkv_dim, c.rows, M, s.hq, s.hkv, s.hd, s.cfg.rope_theta_llm, L.k_cache,
@@ -345,15 +388,17 @@ void Llm::forward_stage(const ChunkDev& c, const bf16* slab, bf16* x,
     g = GemmArgs{};
     g.A = att_; g.lda = s.hq * s.hd; g.B = L.o_w; g.ldb = s.hq * s.hd; g.C = x; g.ldc = s.d;
     g.residual = x; g.ldr = s.d; g.M = M; g.N = s.d; g.K = s.hq * s.hd;
+    g.ss_out = ss_b_; g.ss_clear = ss_a_; g.ss_clear_n = M;
     gemm(g, Epi::Residual, st);
-    rmsnorm(x, s.d, L.ln2, xn_, s.d, M, s.d, s.eps, st);
     g = GemmArgs{};
-    g.A = xn_; g.lda = s.d; g.B = L.gu_w; g.ldb = s.d; g.C = h_; g.ldc = s.ff;
+    g.A = x; g.lda = s.d; g.B = L.gu_w; g.ldb = s.d; g.C = h_; g.ldc = s.ff;
     g.M = M; g.N = 2 * s.ff; g.K = s.d;
+    g.ss_in = ss_b_; g.ss_inv_dim = inv_d; g.ss_eps = s.eps;
     gemm(g, Epi::SwiGLU, st);
     g = GemmArgs{};
     g.A = h_; g.lda = s.ff; g.B = L.down_w; g.ldb = s.ff; g.C = x; g.ldc = s.d;
     g.residual = x; g.ldr = s.d; g.M = M; g.N = s.d; g.K = s.ff;
+    g.ss_out = ss_a_; g.ss_clear = ss_b_; g.ss_clear_n = M;
     gemm(g, Epi::Residual, st);
   }
   if (head_ != nullptr && l_to == le_ && c.n_done > 0) {

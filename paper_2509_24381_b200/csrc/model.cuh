@@ -115,6 +115,11 @@ class Vit {
   bf16 *x_ = nullptr, *xn_ = nullptr, *qkv_ = nullptr, *att_ = nullptr, *h_ = nullptr,
        *mh_ = nullptr;
   bf16 *qp_ = nullptr, *kp_ = nullptr, *vt_ = nullptr;  // head-padded tcgen05 attention operands
+  // folded RMSNorm: unit weight for the explicit norms (the layers' norm
+  // weights live in their consumer GEMMs' columns) and the per-row sums of
+  // squares handed from residual GEMMs to norm consumers (ping-pong)
+  bf16* unit_ln_ = nullptr;
+  unsigned long long *ss_a_ = nullptr, *ss_b_ = nullptr;  // [max patches], 2^-16 fixed point
   float2* rope_table_ = nullptr;                         // [P, hd/2] cos/sin, per batch
 };
 
@@ -155,6 +160,8 @@ class Llm {
   std::vector<LlmLayer> layers_;
   bf16 *final_ln_ = nullptr, *head_ = nullptr;
   bf16 *xn_ = nullptr, *qkv_ = nullptr, *att_ = nullptr, *h_ = nullptr, *xf_ = nullptr;
+  bf16* unit_ln_ = nullptr;                  // folded RMSNorm (see Vit)
+  unsigned long long *ss_a_ = nullptr, *ss_b_ = nullptr;
   float* logits_ = nullptr;
   std::int32_t* argmax_ = nullptr;
   float* head_scratch_ = nullptr;
