@@ -67,12 +67,31 @@ struct Smem {
   bf16 v[2][kKV][kLd];
 };
 
+// Rotary (rotate-half pairs (i, i + HD/2), cos / sin from a [rows, HD/2]
+// float2 table) applied in shared memory to `rows` rows of a tile: the ViT's
+// 2D RoPE fused into the window attention (no separate q / k pass).
+template <int HD>
+__device__ __forceinline__ void rope_tile_smem(bf16 (*t)[HD + 8], int rows, const float2* table) {
+  constexpr int kHalf = HD / 2, kPairs = kHalf / 2;  // bf16x2 pairs per half row
+  for (int e = threadIdx.x; e < rows * kPairs; e += blockDim.x) {
+    const int r = e / kPairs, i = (e % kPairs) * 2;
+    std::uint32_t* pa = reinterpret_cast<std::uint32_t*>(&t[r][i]);
+    std::uint32_t* pb = reinterpret_cast<std::uint32_t*>(&t[r][i + kHalf]);
+    const float2 a = unpack_bf16x2(*pa), b = unpack_bf16x2(*pb);
+    const float2 c0 = table[r * kHalf + i], c1 = table[r * kHalf + i + 1];
+    *pa = pack_bf16x2(a.x * c0.x - b.x * c0.y, a.y * c1.x - b.y * c1.y);
+    *pb = pack_bf16x2(b.x * c0.x + a.x * c0.y, b.y * c1.x + a.y * c1.y);
+  }
+}
+
 // Core: q rows [q_row0, q_row0 + q_rows) (row stride ld_q, head columns at
 // q_ptr), keys [0, src.n_keys). Causal when q_pos0 >= 0: key j visible to
-// query i iff j <= q_pos0 + i.
+// query i iff j <= q_pos0 + i. With q_rope / k_rope (tables at query row 0 /
+// key 0) q and k are rotated in shared memory after their loads.
 template <int HD, typename Src>
 __device__ void flash_block(const bf16* q_ptr, int ld_q, int q_rows, int q_pos0, const Src& src,
-                            bf16* o_ptr, int ld_o, float scale_log2, Smem<HD>& sm) {
+                            bf16* o_ptr, int ld_o, float scale_log2, Smem<HD>& sm,
+                            const float2* q_rope = nullptr, const float2* k_rope = nullptr) {
   constexpr int kDC = HD / 16;  // d chunks (k dim of QK^T)
   constexpr int kNT = HD / 8;   // d n-tiles of O
   const int tid = threadIdx.x;
@@ -116,6 +135,11 @@ __device__ void flash_block(const bf16* q_ptr, int ld_q, int q_rows, int q_pos0,
     cp_async_commit();
     cp_async_wait<1>();
     __syncthreads();
+    if (k_rope != nullptr) {
+      if (t == 0) rope_tile_smem<HD>(sm.q, q_rows, q_rope);
+      rope_tile_smem<HD>(sm.k[buf], min(kKV, n_keys - t * kKV), k_rope + static_cast<std::int64_t>(t) * kKV * (HD / 2));
+      __syncthreads();
+    }
     if (t == 0) {
 #pragma unroll
       for (int c = 0; c < kDC; ++c) {
@@ -232,7 +256,7 @@ template <int HD>
 __global__ void __launch_bounds__(128) varlen_bidir_kernel(const bf16* __restrict__ qkv, int ld,
                                                            bf16* __restrict__ out, int ld_out,
                                                            const int* __restrict__ cu, int heads,
-                                                           float scale_log2) {
+                                                           float scale_log2, const float2* rope) {
   extern __shared__ __align__(16) std::uint8_t smem_raw[];
   Smem<HD>& sm = *reinterpret_cast<Smem<HD>*>(smem_raw);
   const int seq = blockIdx.y, head = blockIdx.z;
@@ -244,14 +268,16 @@ __global__ void __launch_bounds__(128) varlen_bidir_kernel(const bf16* __restric
                   qkv + static_cast<std::int64_t>(s0) * ld + (2 * heads + head) * HD, ld, len};
   flash_block<HD>(qkv + static_cast<std::int64_t>(s0 + q0) * ld + head * HD, ld, min(kQ, len - q0),
                   -1, src, out + static_cast<std::int64_t>(s0 + q0) * ld_out + head * HD, ld_out,
-                  scale_log2, sm);
+                  scale_log2, sm,
+                  rope != nullptr ? rope + static_cast<std::int64_t>(s0 + q0) * (HD / 2) : nullptr,
+                  rope != nullptr ? rope + static_cast<std::int64_t>(s0) * (HD / 2) : nullptr);
 }
 
 constexpr float kLog2e = 1.4426950408889634f;
 
 template <int HD>
 void launch_bidir(const bf16* qkv, int ld, bf16* out, int ld_out, const int* cu, int n_seqs,
-                  int max_seqlen, int heads, float scale, cudaStream_t st) {
+                  int max_seqlen, int heads, float scale, cudaStream_t st, const float2* rope) {
   const int smem = sizeof(Smem<HD>);
   static bool set = false;
   if (!set) {
@@ -261,7 +287,7 @@ void launch_bidir(const bf16* qkv, int ld, bf16* out, int ld_out, const int* cu,
   }
   dim3 grid(ceil_div(max_seqlen, kQ), n_seqs, heads);
   const int tok = prof::begin(st);
-  varlen_bidir_kernel<HD><<<grid, 128, smem, st>>>(qkv, ld, out, ld_out, cu, heads, scale * kLog2e);
+  varlen_bidir_kernel<HD><<<grid, 128, smem, st>>>(qkv, ld, out, ld_out, cu, heads, scale * kLog2e, rope);
   RS_LAUNCH_CHECK();
   prof::end(tok, st, "attn_vit_mma", 0, 0);
   count_launch();
@@ -271,12 +297,13 @@ void launch_bidir(const bf16* qkv, int ld, bf16* out, int ld_out, const int* cu,
 
 void attention_varlen_bidir(const bf16* qkv, int ld_qkv, bf16* out, int ld_out,
                             const int* cu_seqlens, int n_seqs, int max_seqlen, int /*total*/,
-                            int heads, int head_dim, float scale, cudaStream_t stream) {
+                            int heads, int head_dim, float scale, cudaStream_t stream,
+                            const float2* rope_table) {
   if (n_seqs <= 0 || max_seqlen <= 0) return;
   switch (head_dim) {
-    case 64: return launch_bidir<64>(qkv, ld_qkv, out, ld_out, cu_seqlens, n_seqs, max_seqlen, heads, scale, stream);
-    case 80: return launch_bidir<80>(qkv, ld_qkv, out, ld_out, cu_seqlens, n_seqs, max_seqlen, heads, scale, stream);
-    case 128: return launch_bidir<128>(qkv, ld_qkv, out, ld_out, cu_seqlens, n_seqs, max_seqlen, heads, scale, stream);
+    case 64: return launch_bidir<64>(qkv, ld_qkv, out, ld_out, cu_seqlens, n_seqs, max_seqlen, heads, scale, stream, rope_table);
+    case 80: return launch_bidir<80>(qkv, ld_qkv, out, ld_out, cu_seqlens, n_seqs, max_seqlen, heads, scale, stream, rope_table);
+    case 128: return launch_bidir<128>(qkv, ld_qkv, out, ld_out, cu_seqlens, n_seqs, max_seqlen, heads, scale, stream, rope_table);
     default: throw DeviceError(RS_ERR_CUDA, "attention: unsupported head_dim " + std::to_string(head_dim));
   }
 }

@@ -16,9 +16,13 @@
 
 namespace rserve {
 
+/// rope_table (optional, [total, head_dim/2] float2 cos/sin per packed row):
+/// q and k are rotated (rotate-half pairs) in shared memory after loading,
+/// i.e. the ViT 2D RoPE fused into the attention.
 void attention_varlen_bidir(const bf16* qkv, int ld_qkv, bf16* out, int ld_out,
                             const int* cu_seqlens, int n_seqs, int max_seqlen, int total,
-                            int heads, int head_dim, float scale, cudaStream_t stream);
+                            int heads, int head_dim, float scale, cudaStream_t stream,
+                            const float2* rope_table = nullptr);
 
 // One unit of chunked-prefill attention work: up to attn_unit_rows() query
 // rows of one slice.

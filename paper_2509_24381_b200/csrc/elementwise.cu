@@ -331,6 +331,84 @@ __global__ void rope_kv_append_kernel(bf16* qkv, int ld, const ChunkRowInfo* __r
   }
 }
 
+// M-RoPE + paged KV append, vectorised (rope_kv_append_kernel is the
+// reference-shaped scalar version kept for rows_dev / odd head sizes).
+// blockIdx.y == 0: one warp per chunk row: the row's rotary cos / sin are
+// computed once (8 frequencies per lane) and applied to every q and k head
+// with 16-byte loads; k heads are also copied into the page. blockIdx.y == 1:
+// one warp per (32 rows, kv head), lane = row: V is written transposed, so
+// for each head dim the 32 lanes store 32 consecutive tokens of a page.
+template <int HD>
+__global__ void rope_kv_append_vec_kernel(bf16* qkv, int ld, const ChunkRowInfo* __restrict__ info,
+                                          int rows, int q_heads, int kv_heads, float log2_theta,
+                                          bf16* k_cache, bf16* v_cache,
+                                          const int* const* page_tables, int page_size) {
+  constexpr int kHalf = HD / 2, kLph = kHalf / 8, kHpp = 32 / kLph;
+  const int lane = threadIdx.x & 31;
+  const int warps_total = gridDim.x * kWarpsPerBlock;
+  const int wid = blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
+  if (blockIdx.y == 0) {
+    const int i0 = (lane % kLph) * 8;
+    const int hsub = lane / kLph;
+    constexpr int s_t = HD / 8, s_h = HD / 8 + (3 * HD) / 16;
+    for (int row = wid; row < rows; row += warps_total) {
+      const ChunkRowInfo ri = info[row];
+      float cs[8], sn[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int i = i0 + j;
+        const int sec = i < s_t ? 0 : (i < s_h ? 1 : 2);
+        const float freq = exp2f(-log2_theta * (2.0f * i) / static_cast<float>(HD));
+        sincosf(static_cast<float>(ri.rope[sec]) * freq, &sn[j], &cs[j]);
+      }
+      const int* pt = page_tables[ri.req_slot];
+      const std::int64_t page = pt[ri.pos / page_size];
+      const int off = ri.pos % page_size;
+      bf16* base = qkv + static_cast<std::int64_t>(row) * ld;
+      for (int h = hsub; h < q_heads + kv_heads; h += kHpp) {
+        bf16* v = base + h * HD;
+        const uint4 a = *reinterpret_cast<const uint4*>(v + i0);
+        const uint4 b = *reinterpret_cast<const uint4*>(v + i0 + kHalf);
+        const std::uint32_t aw[4] = {a.x, a.y, a.z, a.w}, bw[4] = {b.x, b.y, b.z, b.w};
+        std::uint32_t oa[4], ob[4];
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          const float2 fa = unpack_bf16x2(aw[t]), fb = unpack_bf16x2(bw[t]);
+          const float c0 = cs[2 * t], s0 = sn[2 * t], c1 = cs[2 * t + 1], s1 = sn[2 * t + 1];
+          oa[t] = pack_bf16x2(fa.x * c0 - fb.x * s0, fa.y * c1 - fb.y * s1);
+          ob[t] = pack_bf16x2(fb.x * c0 + fa.x * s0, fb.y * c1 + fa.y * s1);
+        }
+        const uint4 ua = make_uint4(oa[0], oa[1], oa[2], oa[3]), ub = make_uint4(ob[0], ob[1], ob[2], ob[3]);
+        *reinterpret_cast<uint4*>(v + i0) = ua;
+        *reinterpret_cast<uint4*>(v + i0 + kHalf) = ub;
+        if (h >= q_heads) {  // K: [page][kv head][token][hd]
+          bf16* dst = k_cache + ((page * kv_heads + (h - q_heads)) * page_size + off) * HD;
+          *reinterpret_cast<uint4*>(dst + i0) = ua;
+          *reinterpret_cast<uint4*>(dst + i0 + kHalf) = ub;
+        }
+      }
+    }
+  } else {
+    const int groups = ((rows + 31) / 32) * kv_heads;
+    for (int g = wid; g < groups; g += warps_total) {
+      const int kvh = g % kv_heads;
+      const int r = (g / kv_heads) * 32 + lane;
+      if (r >= rows) continue;
+      const ChunkRowInfo ri = info[r];
+      const std::int64_t page = page_tables[ri.req_slot][ri.pos / page_size];
+      const bf16* v = qkv + static_cast<std::int64_t>(r) * ld + (q_heads + kv_heads + kvh) * HD;
+      bf16* dst = v_cache + (page * kv_heads + kvh) * HD * page_size + ri.pos % page_size;
+#pragma unroll 4
+      for (int c0 = 0; c0 < HD; c0 += 8) {
+        const uint4 x = *reinterpret_cast<const uint4*>(v + c0);
+        const bf16* e = reinterpret_cast<const bf16*>(&x);
+#pragma unroll
+        for (int t = 0; t < 8; ++t) dst[static_cast<std::int64_t>(c0 + t) * page_size] = e[t];
+      }
+    }
+  }
+}
+
 __global__ void scatter_rows_kernel(const bf16* __restrict__ src, int n_rows,
                                     const std::int64_t* __restrict__ dst_rows, bf16* slab, int d,
                                     std::uint32_t* bitmap, const std::uint64_t* __restrict__ ranges,
@@ -574,6 +652,22 @@ void rope_kv_append(bf16* qkv, int ld, const ChunkRowInfo* rows_info, int rows, 
                     const int* const* page_tables, int page_size, cudaStream_t st,
                     const int* rows_dev) {
   if (rows <= 0) return;
+  if (rows_dev == nullptr && (hd == 64 || hd == 128)) {
+    const int tok = prof::begin(st);
+    const dim3 grid(row_grid(rows), 2);
+    if (hd == 128)
+      rope_kv_append_vec_kernel<128><<<grid, 32 * kWarpsPerBlock, 0, st>>>(
+          qkv, ld, rows_info, rows, q_heads, kv_heads, std::log2(theta), k_cache, v_cache, page_tables, page_size);
+    else
+      rope_kv_append_vec_kernel<64><<<grid, 32 * kWarpsPerBlock, 0, st>>>(
+          qkv, ld, rows_info, rows, q_heads, kv_heads, std::log2(theta), k_cache, v_cache, page_tables, page_size);
+    RS_LAUNCH_CHECK();
+    // algorithmic bytes: q, k read + written, k and v appended (v read once)
+    prof::end(tok, st, "rope_kv_append", 0,
+              2.0 * rows * hd * (2.0 * (q_heads + kv_heads) + 2.0 * kv_heads));
+    count_launch();
+    return;
+  }
   rope_kv_append_kernel<<<row_grid(static_cast<std::int64_t>(rows) * (q_heads + 2 * kv_heads)),
                           32 * kWarpsPerBlock, 0, st>>>(qkv, ld, rows_info, rows, q_heads, kv_heads,
                                                         hd, std::log2(theta), k_cache, v_cache,

@@ -240,9 +240,9 @@ void Vit::encode(const VitBatchPlan& plan, const bf16* patches, const std::int32
     } else {
       // 8x8-patch windows (<= 64 keys): latency-bound tiles; the register-
       // tiled kernel reads qkv in place (no padding / transpose pass)
-      vit_qk_rope_inplace(qkv_, 3 * s.vd, rope_table_, P, s.vh, s.vhd, st);
+      // (2D RoPE applied to q / k in shared memory inside the kernel)
       attention_varlen_bidir(qkv_, 3 * s.vd, att_, s.vd, cu_window, n_win, plan.max_window, P, s.vh,
-                             s.vhd, scale, st);
+                             s.vhd, scale, st, rope_table_);
     }
     g = GemmArgs{};
     g.A = att_; g.lda = s.vd; g.B = L.o_w; g.ldb = s.vd; g.C = x_; g.ldc = s.vd; g.bias = L.o_b;
