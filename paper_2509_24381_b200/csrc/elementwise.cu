@@ -333,11 +333,11 @@ __global__ void rope_kv_append_kernel(bf16* qkv, int ld, const ChunkRowInfo* __r
 
 // M-RoPE + paged KV append, vectorised (rope_kv_append_kernel is the
 // reference-shaped scalar version kept for rows_dev / odd head sizes).
-// blockIdx.y == 0: one warp per chunk row: the row's rotary cos / sin are
-// computed once (8 frequencies per lane) and applied to every q and k head
-// with 16-byte loads; k heads are also copied into the page. blockIdx.y == 1:
-// one warp per (32 rows, kv head), lane = row: V is written transposed, so
-// for each head dim the 32 lanes store 32 consecutive tokens of a page.
+// blockIdx.y == 0: one warp per (chunk row, group of 32 / (HD/16) heads):
+// cos / sin of 8 frequencies per lane, applied with 16-byte loads; k heads
+// are also copied into the page. blockIdx.y == 1: one warp per (32 rows, kv
+// head, 16 head dims), lane = row: V is written transposed, so for each head
+// dim the 32 lanes store 32 consecutive tokens of a page.
 template <int HD>
 __global__ void rope_kv_append_vec_kernel(bf16* qkv, int ld, const ChunkRowInfo* __restrict__ info,
                                           int rows, int q_heads, int kv_heads, float log2_theta,
@@ -351,7 +351,11 @@ __global__ void rope_kv_append_vec_kernel(bf16* qkv, int ld, const ChunkRowInfo*
     const int i0 = (lane % kLph) * 8;
     const int hsub = lane / kLph;
     constexpr int s_t = HD / 8, s_h = HD / 8 + (3 * HD) / 16;
-    for (int row = wid; row < rows; row += warps_total) {
+    const int heads = q_heads + kv_heads;
+    const int passes = (heads + kHpp - 1) / kHpp;
+    for (int item = wid; item < rows * passes; item += warps_total) {
+      const int row = item / passes;
+      const int h = (item % passes) * kHpp + hsub;
       const ChunkRowInfo ri = info[row];
       float cs[8], sn[8];
 #pragma unroll
@@ -365,7 +369,7 @@ __global__ void rope_kv_append_vec_kernel(bf16* qkv, int ld, const ChunkRowInfo*
       const std::int64_t page = pt[ri.pos / page_size];
       const int off = ri.pos % page_size;
       bf16* base = qkv + static_cast<std::int64_t>(row) * ld;
-      for (int h = hsub; h < q_heads + kv_heads; h += kHpp) {
+      if (h < heads) {
         bf16* v = base + h * HD;
         const uint4 a = *reinterpret_cast<const uint4*>(v + i0);
         const uint4 b = *reinterpret_cast<const uint4*>(v + i0 + kHalf);
@@ -389,17 +393,19 @@ __global__ void rope_kv_append_vec_kernel(bf16* qkv, int ld, const ChunkRowInfo*
       }
     }
   } else {
-    const int groups = ((rows + 31) / 32) * kv_heads;
+    constexpr int kSlices = HD / 16;
+    const int groups = ((rows + 31) / 32) * kv_heads * kSlices;
     for (int g = wid; g < groups; g += warps_total) {
-      const int kvh = g % kv_heads;
-      const int r = (g / kv_heads) * 32 + lane;
+      const int sl = g % kSlices;
+      const int kvh = (g / kSlices) % kv_heads;
+      const int r = (g / (kSlices * kv_heads)) * 32 + lane;
       if (r >= rows) continue;
       const ChunkRowInfo ri = info[r];
       const std::int64_t page = page_tables[ri.req_slot][ri.pos / page_size];
       const bf16* v = qkv + static_cast<std::int64_t>(r) * ld + (q_heads + kv_heads + kvh) * HD;
       bf16* dst = v_cache + (page * kv_heads + kvh) * HD * page_size + ri.pos % page_size;
-#pragma unroll 4
-      for (int c0 = 0; c0 < HD; c0 += 8) {
+#pragma unroll
+      for (int c0 = sl * 16; c0 < sl * 16 + 16; c0 += 8) {
         const uint4 x = *reinterpret_cast<const uint4*>(v + c0);
         const bf16* e = reinterpret_cast<const bf16*>(&x);
 #pragma unroll
@@ -654,7 +660,8 @@ void rope_kv_append(bf16* qkv, int ld, const ChunkRowInfo* rows_info, int rows, 
   if (rows <= 0) return;
   if (rows_dev == nullptr && (hd == 64 || hd == 128)) {
     const int tok = prof::begin(st);
-    const dim3 grid(row_grid(rows), 2);
+    const int passes = (q_heads + kv_heads + 32 / (hd / 16) - 1) / (32 / (hd / 16));
+    const dim3 grid(row_grid(static_cast<std::int64_t>(rows) * passes), 2);
     if (hd == 128)
       rope_kv_append_vec_kernel<128><<<grid, 32 * kWarpsPerBlock, 0, st>>>(
           qkv, ld, rows_info, rows, q_heads, kv_heads, std::log2(theta), k_cache, v_cache, page_tables, page_size);
