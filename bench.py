@@ -162,10 +162,17 @@ def run_ours(args):
                        embedding_batch_tokens=C_TOKENS, encoder_workers=1, hidden_size=m["llm_dim"],
                        cost=api.CostModel(beta_enc_ms_per_token=0.01, delta_stage_ms_per_token=0.01))
 
+    chunk_sizes = {}
+
     def step(e2e=False, serialize=False):
         log, journal, st = pipe.run(wl, sc, clock="real", e2e=e2e, payload_seed=1234,
                                     serialize=serialize)
-        rec = api.parse_decision_log(log)["req"][0]
+        parsed = api.parse_decision_log(log)
+        rec = parsed["req"][0]
+        sizes = {}
+        for sl in parsed.get("slice", []):
+            sizes[sl["chunk"]] = sizes.get(sl["chunk"], 0) + int(sl["end"]) - int(sl["start"])
+        chunk_sizes["serialized" if serialize else "e2e" if e2e else "timed"] = list(sizes.values())
         return float(rec["ttft"]), st
 
     for _ in range(args.warmup):
@@ -285,6 +292,7 @@ def run_ours(args):
                                "share": v["ms"] / prof_total_ms if prof_total_ms else None}
                            for k, v in prof.items()},
         "gemm_shapes": gemm_shapes[:16],
+        "prefill_chunk_tokens": chunk_sizes,
         "model_tflop_per_request": {"encode": vit_f / 1e12, "prefill": llm_f / 1e12},
         "clocks": clk.summary(),
     }

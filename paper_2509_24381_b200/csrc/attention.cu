@@ -259,6 +259,8 @@ __global__ void __launch_bounds__(128) varlen_bidir_kernel(const bf16* __restric
                                                            float scale_log2, const float2* rope) {
   extern __shared__ __align__(16) std::uint8_t smem_raw[];
   Smem<HD>& sm = *reinterpret_cast<Smem<HD>*>(smem_raw);
+  pdl_wait();
+  pdl_launch_dependents();
   const int seq = blockIdx.y, head = blockIdx.z;
   const int s0 = cu[seq], s1 = cu[seq + 1];
   const int q0 = blockIdx.x * kQ;
@@ -287,7 +289,8 @@ void launch_bidir(const bf16* qkv, int ld, bf16* out, int ld_out, const int* cu,
   }
   dim3 grid(ceil_div(max_seqlen, kQ), n_seqs, heads);
   const int tok = prof::begin(st);
-  varlen_bidir_kernel<HD><<<grid, 128, smem, st>>>(qkv, ld, out, ld_out, cu, heads, scale * kLog2e, rope);
+  launch_kernel(varlen_bidir_kernel<HD>, grid, dim3(128), smem, st, 1, qkv, ld, out, ld_out, cu, heads,
+                scale * kLog2e, rope);
   RS_LAUNCH_CHECK();
   prof::end(tok, st, "attn_vit_mma", 0, 0);
   count_launch();

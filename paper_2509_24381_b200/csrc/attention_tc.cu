@@ -127,6 +127,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   std::uint32_t* tmem_holder = reinterpret_cast<std::uint32_t*>(o_full + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  pdl_wait();
+  pdl_launch_dependents();
   // grid (heads, blocks): heads vary fastest, so blocks issue in work-list
   // order — callers list the most expensive (most keys) first, which makes
   // the hardware's in-order block dispatch an LPT schedule over the SMs.
@@ -452,6 +454,8 @@ __global__ void __launch_bounds__(kPpThreads, 1)
   std::uint32_t* tmem_holder = reinterpret_cast<std::uint32_t*>(o_final + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  pdl_wait();
+  pdl_launch_dependents();
   const int head = blockIdx.x;
   const int kvh = head / (p.q_heads / p.kv_heads);
   int q_row0, q_rows, key_begin, key_end, q_pos0 = 0;
@@ -807,9 +811,9 @@ void launch(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
   dim3 grid(p.q_heads, n_blocks);
   const int tok = prof::begin(st);
   if (attn_unit_rows() == 256)
-    fa_pp_kernel<HD, MODE><<<grid, kPpThreads, PpCfg<HD>::kSmem, st>>>(tq, tk, tv, p);
+    launch_kernel(fa_pp_kernel<HD, MODE>, grid, dim3(kPpThreads), PpCfg<HD>::kSmem, st, 1, tq, tk, tv, p);
   else
-    fa_tc_kernel<HD, MODE><<<grid, kTcThreads, TcCfg<HD>::kSmem, st>>>(tq, tk, tv, p);
+    launch_kernel(fa_tc_kernel<HD, MODE>, grid, dim3(kTcThreads), TcCfg<HD>::kSmem, st, 1, tq, tk, tv, p);
   RS_LAUNCH_CHECK();
   prof::end(tok, st, klass, 0, 0);
   count_launch();

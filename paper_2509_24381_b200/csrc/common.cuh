@@ -7,6 +7,7 @@
 
 #include <cstdint>
 #include <string>
+#include <utility>
 
 #include "host/status.hpp"
 
@@ -44,12 +45,55 @@ void end(int token, cudaStream_t st, const char* klass, double flops, double byt
 std::string drain();
 }  // namespace prof
 
+// Programmatic dependent launch (PDL): kernels of the hot path are launched
+// with programmatic stream serialization, so the next kernel of a stream is
+// scheduled while the current one drains (its CTAs queue at the stream's
+// priority instead of the other stream's kernel slipping into the gap, and
+// launch latency / prologue overlap the previous tail). Every such kernel
+// calls pdl_wait() before touching global memory. RS_PDL=0 disables.
+bool pdl_enabled();
+
+/// cudaLaunchKernelEx with the PDL attribute (when enabled) and an optional
+/// cluster dimension.
+template <typename... KArgs, typename... Args>
+inline void launch_kernel(void (*kernel)(KArgs...), dim3 grid, dim3 block, std::size_t smem,
+                          cudaStream_t st, int cluster_x, Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[2];
+  unsigned n = 0;
+  if (pdl_enabled()) {
+    attr[n].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[n].val.programmaticStreamSerializationAllowed = 1;
+    ++n;
+  }
+  if (cluster_x > 1) {
+    attr[n].id = cudaLaunchAttributeClusterDimension;
+    attr[n].val.clusterDim.x = static_cast<unsigned>(cluster_x);
+    attr[n].val.clusterDim.y = 1;
+    attr[n].val.clusterDim.z = 1;
+    ++n;
+  }
+  cfg.attrs = attr;
+  cfg.numAttrs = n;
+  RS_CUDA_CHECK(cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...));
+}
+
 __host__ __device__ inline int ceil_div(int a, int b) { return (a + b - 1) / b; }
 __host__ __device__ inline std::int64_t ceil_div64(std::int64_t a, std::int64_t b) {
   return (a + b - 1) / b;
 }
 
 #ifdef __CUDACC__
+// PDL device side: wait for the prerequisite grid (no-op without PDL), and
+// let the dependent grid launch early.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_launch_dependents() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
 __device__ __forceinline__ float bf2f(bf16 v) { return __bfloat162float(v); }
 __device__ __forceinline__ bf16 f2bf(float v) { return __float2bfloat16_rn(v); }
 

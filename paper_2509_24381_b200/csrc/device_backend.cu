@@ -266,6 +266,7 @@ double DeviceBackend::launch_encode(int worker, std::size_t slot, const lmmsim::
   ctx_.encode(plan, patches, staging_[static_cast<std::size_t>(ring)], st);
   RS_CUDA_CHECK(cudaEventRecord(end, st));
   slot_done_[slot] = end;
+  last_encode_end_ = end;
   track(lmmsim::OpKind::Encode, static_cast<std::uint32_t>(worker), slot, begin, end);
   return realtime_ ? 0.0 : lmmsim::encode_time_ms(cfg_.cost, b);
 }
@@ -311,6 +312,12 @@ double DeviceBackend::launch_stage(int stage, const lmmsim::ChunkView& c) {
   }
   cudaStream_t st = stage_streams_[0];
   ChunkState& cs = chunks_[c.chunk_id];
+  static const bool enc_first = [] {
+    const char* e = std::getenv("RS_ENCODE_FIRST");
+    return e != nullptr && e[0] == '1';
+  }();
+  if (enc_first && last_encode_end_ != nullptr && !shared_streams_)
+    RS_CUDA_CHECK(cudaStreamWaitEvent(st, last_encode_end_, 0));
   if (stage == 0) {
     if (free_xbufs_.empty()) throw DeviceError(RS_ERR_CUDA, "no free chunk buffer");
     cs.buf = free_xbufs_.back();

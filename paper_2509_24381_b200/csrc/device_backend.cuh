@@ -139,6 +139,7 @@ class DeviceBackend final : public lmmsim::ExecutionBackend {
   rs_run_stats stats_{};
   std::uint64_t launches0_ = 0, upload0_ = 0;
   cudaEvent_t last_event_ = nullptr;
+  cudaEvent_t last_encode_end_ = nullptr;  // RS_ENCODE_FIRST experiment
   // EP (remote_ != nullptr)
   const ep::Remote* remote_ = nullptr;
   std::unordered_map<lmmsim::RequestId, std::vector<lmmsim::SegmentSpec>> layouts_;

@@ -227,6 +227,8 @@ __global__ void vit_rope_table_kernel(const std::int32_t* __restrict__ pos_hw, i
 __global__ void vit_qk_rope_pad_kernel(const bf16* qkv, int ld, const float2* __restrict__ table,
                                        int rows, int heads, int hd, bf16* qp, bf16* kp, int ldp,
                                        int hs) {
+  pdl_wait();
+  pdl_launch_dependents();
   const int half = hd / 2, chunks = half / 8;
   const std::int64_t n = static_cast<std::int64_t>(rows) * 2 * heads * chunks;
   for (std::int64_t e = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; e < n;
@@ -259,6 +261,8 @@ __global__ void vit_qk_rope_pad_kernel(const bf16* qkv, int ld, const float2* __
 __global__ void vit_v_transpose_kernel(const bf16* __restrict__ qkv, int ld, int rows, int heads,
                                        int hd, bf16* __restrict__ vt, int ld_vt) {
   __shared__ bf16 tile[128][64 + 8];
+  pdl_wait();
+  pdl_launch_dependents();
   const int t0 = blockIdx.x * 64, h = blockIdx.y;
   const int vec = hd / 8;
   for (int e = threadIdx.x; e < 64 * vec; e += blockDim.x) {
@@ -344,6 +348,8 @@ __global__ void rope_kv_append_vec_kernel(bf16* qkv, int ld, const ChunkRowInfo*
                                           bf16* k_cache, bf16* v_cache,
                                           const int* const* page_tables, int page_size) {
   constexpr int kHalf = HD / 2, kLph = kHalf / 8, kHpp = 32 / kLph;
+  pdl_wait();
+  pdl_launch_dependents();
   const int lane = threadIdx.x & 31;
   const int warps_total = gridDim.x * kWarpsPerBlock;
   const int wid = blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
@@ -631,10 +637,11 @@ void vit_qkv_split(const bf16* qkv, int ld, const float2* rope_table, int rows, 
   if (hd > 128 || hd % 16 != 0) throw DeviceError(RS_ERR_CUDA, "vit_qkv_split: head_dim must be a multiple of 16, <= 128");
   const int tok = prof::begin(st);
   const std::int64_t items = static_cast<std::int64_t>(rows) * 2 * heads * (hd / 16);
-  vit_qk_rope_pad_kernel<<<elem_grid(items), 256, 0, st>>>(qkv, ld, rope_table, rows, heads, hd, qp, kp,
-                                                           heads * 128, 128);
+  launch_kernel(vit_qk_rope_pad_kernel, dim3(elem_grid(items)), dim3(256), 0, st, 1, qkv, ld, rope_table,
+                rows, heads, hd, qp, kp, heads * 128, 128);
   RS_LAUNCH_CHECK();
-  vit_v_transpose_kernel<<<dim3(ceil_div(rows, 64), heads), 256, 0, st>>>(qkv, ld, rows, heads, hd, vt, ld_vt);
+  launch_kernel(vit_v_transpose_kernel, dim3(ceil_div(rows, 64), heads), dim3(256), 0, st, 1, qkv, ld, rows,
+                heads, hd, vt, ld_vt);
   RS_LAUNCH_CHECK();
   prof::end(tok, st, "vit_qkv_split", 0, 2.0 * rows * heads * hd * 3 * 2);
   count_launch(2);
@@ -662,12 +669,9 @@ void rope_kv_append(bf16* qkv, int ld, const ChunkRowInfo* rows_info, int rows, 
     const int tok = prof::begin(st);
     const int passes = (q_heads + kv_heads + 32 / (hd / 16) - 1) / (32 / (hd / 16));
     const dim3 grid(row_grid(static_cast<std::int64_t>(rows) * passes), 2);
-    if (hd == 128)
-      rope_kv_append_vec_kernel<128><<<grid, 32 * kWarpsPerBlock, 0, st>>>(
-          qkv, ld, rows_info, rows, q_heads, kv_heads, std::log2(theta), k_cache, v_cache, page_tables, page_size);
-    else
-      rope_kv_append_vec_kernel<64><<<grid, 32 * kWarpsPerBlock, 0, st>>>(
-          qkv, ld, rows_info, rows, q_heads, kv_heads, std::log2(theta), k_cache, v_cache, page_tables, page_size);
+    launch_kernel(hd == 128 ? rope_kv_append_vec_kernel<128> : rope_kv_append_vec_kernel<64>, grid,
+                  dim3(32 * kWarpsPerBlock), 0, st, 1, qkv, ld, rows_info, rows, q_heads, kv_heads,
+                  std::log2(theta), k_cache, v_cache, page_tables, page_size);
     RS_LAUNCH_CHECK();
     // algorithmic bytes: q, k read + written, k and v appended (v read once)
     prof::end(tok, st, "rope_kv_append", 0,

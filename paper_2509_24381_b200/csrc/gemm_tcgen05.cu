@@ -405,6 +405,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
+  pdl_wait();  // inputs of the previous kernel of this stream are visible from here
+  pdl_launch_dependents();
   for (int i = blockIdx.x * kThreads + threadIdx.x; i < p.ss_clear_n; i += gridDim.x * kThreads)
     p.ss_clear[i] = 0ull;
   // CTA pair: rank 0 (leader) issues the MMAs; both CTAs load and drain.
@@ -813,23 +815,7 @@ void launch(const GemmArgs& a, cudaStream_t stream) {
       grid = std::min(kNumSMs, p.dp_tiles + sp.sk_tiles * sp.splits);
     }
   }
-  if constexpr (CG == 1) {
-    kernel<<<grid, kThreads, C::kSmem, stream>>>(tmA, tmB, tmC, tmR, p);
-  } else {
-    cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(grid);
-    cfg.blockDim = dim3(kThreads);
-    cfg.dynamicSmemBytes = C::kSmem;
-    cfg.stream = stream;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = 2;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    RS_CUDA_CHECK(cudaLaunchKernelEx(&cfg, kernel, tmA, tmB, tmC, tmR, p));
-  }
+  launch_kernel(kernel, dim3(grid), dim3(kThreads), C::kSmem, stream, CG, tmA, tmB, tmC, tmR, p);
   RS_LAUNCH_CHECK();
   count_launch();
 }

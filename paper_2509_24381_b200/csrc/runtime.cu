@@ -1,5 +1,6 @@
 // rserve-b200 — process-wide runtime bits: launch counter, live kernel timing.
 #include <atomic>
+#include <cstdlib>
 #include <map>
 #include <mutex>
 #include <vector>
@@ -13,6 +14,14 @@ std::atomic<std::uint64_t> g_launches{0};
 }
 
 void count_launch(std::uint64_t n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("RS_PDL");
+    return e == nullptr || e[0] != '0';
+  }();
+  return on;
+}
 std::uint64_t launches_so_far() { return g_launches.load(std::memory_order_relaxed); }
 
 namespace prof {
