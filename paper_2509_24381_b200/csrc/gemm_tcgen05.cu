@@ -542,10 +542,11 @@ __global__ void __launch_bounds__(kThreads, 1)
           tmem_base + (static_cast<std::uint32_t>(quad * 32) << 16) + static_cast<std::uint32_t>(acc * BN);
       if (TMA_OUT && u.split >= 0) {
         // ---- split unit: store the fp32 partial, count, maybe finish ----
-        const int t_sk = u.tile - sched.dp_tiles;
+        // split tile index of this CTA's 128-row half (pairs: one per rank)
+        const int t_sk = (u.tile - sched.dp_tiles) * CG + static_cast<int>(rank);
         const int n_parts = sched.sk_splits;
         auto part_ptr = [&](int sp) {
-          return p.ws + (static_cast<std::int64_t>(sp) * sched.sk_tiles + t_sk) * (kBM * BN);
+          return p.ws + (static_cast<std::int64_t>(sp) * sched.sk_tiles * CG + t_sk) * (kBM * BN);
         };
         sm100::mbar_wait(&tfull[acc], acc_phase);
         sm100::tc_fence_after();
@@ -749,20 +750,31 @@ struct SplitPlan {
   int sk_tiles = 0, splits = 1;
   double cost = 0;
 };
-SplitPlan plan_split(int tiles, int num_kb, int bn) {
+// cg = 2: pair tiles (256 x bn) on 74 cluster slots; each CTA of a pair keeps
+// its own 128-row partials / counter.
+SplitPlan plan_split(int tiles, int num_kb, int bn, int cg = 1) {
   SplitPlan best;
-  const int rem = tiles % kNumSMs;
-  const int full = tiles / kNumSMs;
+  const int slots = kNumSMs / cg;
+  const int rem = tiles % slots;
+  const int full = tiles / slots;
   best.cost = full + (rem > 0 ? 1.0 : 0.0);
   // (measured: at K = 3584 the partials' round trip eats the gain; K = 18944 wins 30%)
-  const bool small = tiles <= kNumSMs / 2 && num_kb >= 128;
-  const bool tail = tiles > kNumSMs && rem > 0 && num_kb >= 48;
+  const bool small = tiles <= slots / 2 && num_kb >= 128;
+  const bool tail = tiles > slots && rem > 0 && num_kb >= 48;
+  // Pair tiles: measured slower with split tails at every cfg2 shape (both
+  // CTAs' fp32 partials round-trip), so they run whole tiles only; the kernel
+  // path is kept and tested (RS_GEMM_PAIR_SPLIT=1).
+  if (cg == 2) {
+    const char* e = std::getenv("RS_GEMM_PAIR_SPLIT");
+    if (e == nullptr || e[0] != '1') return best;
+  }
   if (!small && !tail) return best;
   const int min_kb = 16;
   for (int sp = 2; sp <= kMaxParts && num_kb / sp >= min_kb; ++sp) {
-    if (static_cast<std::size_t>(rem) * sp * kBM * bn * sizeof(float) > kSkWsBytes) break;
+    if (static_cast<std::size_t>(rem) * cg * sp * kBM * bn * sizeof(float) > kSkWsBytes) break;
+    if (rem * cg > kNumSMs) break;  // tile counters
     // partial round trip: ~4% of a tile per extra split
-    const double tail_c = static_cast<double>(ceil_div(rem * sp, kNumSMs)) / sp + 0.04 * (sp - 1);
+    const double tail_c = static_cast<double>(ceil_div(rem * sp, slots)) / sp + 0.04 * (sp - 1);
     if (tail_c <= 0.85 && full + tail_c < best.cost - 1e-9) {
       best.cost = full + tail_c;
       best.sk_tiles = rem;
@@ -803,8 +815,8 @@ void launch(const GemmArgs& a, cudaStream_t stream) {
   // ranges >= 16 blocks) minimising that, if it saves >= 15% of the tail.
   // Long-K GEMMs only: the fp32 partials' round trip must stay small next to
   // the saved tail.
-  if (CG == 1 && TMA_OUT && a.M_dev == nullptr && streamk_enabled()) {
-    const SplitPlan sp = plan_split(tiles, ceil_div(a.K, kBK), BN);
+  if (TMA_OUT && a.M_dev == nullptr && streamk_enabled()) {
+    const SplitPlan sp = plan_split(tiles, ceil_div(a.K, kBK), BN, CG);
     if (sp.splits > 1) {
       SkWorkspace& w = sk_workspace(stream);
       p.dp_tiles = tiles - sp.sk_tiles;
@@ -812,7 +824,7 @@ void launch(const GemmArgs& a, cudaStream_t stream) {
       p.sk_splits = sp.splits;
       p.ws = w.ws;
       p.counters = w.counters;
-      grid = std::min(kNumSMs, p.dp_tiles + sp.sk_tiles * sp.splits);
+      grid = CG * std::min(kNumSMs / CG, p.dp_tiles + sp.sk_tiles * sp.splits);
     }
   }
   launch_kernel(kernel, dim3(grid), dim3(kThreads), C::kSmem, stream, CG, tmA, tmB, tmC, tmR, p);
@@ -869,8 +881,8 @@ TileChoice pick_tile(int M, int N, int K, bool swiglu) {
       const long slots = kNumSMs / cg;
       const long waves = (tiles + slots - 1) / slots;
       const double pair_gain = num_kb >= 32 ? 0.85 : (waves <= 2 ? 1.05 : 0.93);
-      const double cost = cg == 2 ? static_cast<double>(waves * bn) * pair_gain
-                                  : plan_split(static_cast<int>(tiles), num_kb, bn).cost * bn;
+      const double cost = plan_split(static_cast<int>(tiles), num_kb, bn, cg).cost * bn *
+                          (cg == 2 ? pair_gain : 1.0);
       if (best_cost < 0 || cost < best_cost - 1e-9) {
         best = {bn, cg};
         best_cost = cost;

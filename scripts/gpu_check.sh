@@ -1,7 +1,7 @@
 cd "${GRAFT_REPO_ROOT:-/root/repo}"
 mkdir -p gpurun_out
-timeout 1200 python -m pytest tests -m gpu -x -q -p no:cacheprovider > gpurun_out/pytest_gpu.log 2>&1; echo "pytest exit $?" >> gpurun_out/pytest_gpu.log
-tail -n 3 gpurun_out/pytest_gpu.log
+timeout 600 python -m pytest tests/test_ops_gpu.py -x -q -p no:cacheprovider > gpurun_out/ops_tests.log 2>&1; echo "exit $?" >> gpurun_out/ops_tests.log
+tail -n 3 gpurun_out/ops_tests.log
+timeout 600 python scripts/gemm_sweep.py --quick > gpurun_out/gemm_sweep.log 2>&1
 timeout 900 python bench.py --no-cpu-baseline > gpurun_out/bench.json 2> gpurun_out/bench.err; echo "bench exit $?" >> gpurun_out/bench.err
-RS_PDL=0 timeout 900 python bench.py --no-cpu-baseline > gpurun_out/bench_nopdl.json 2> gpurun_out/bench_nopdl.err; echo "bench exit $?" >> gpurun_out/bench_nopdl.err
-tail -n 2 gpurun_out/bench.err gpurun_out/bench_nopdl.err
+tail -n 2 gpurun_out/bench.err

@@ -70,7 +70,17 @@ def test_gemm_store(nat, M, N, K, bn):
 SK_SHAPES = [(2048, 3584, 18944, 224), (1024, 5120, 5120, 160), (1024, 5120, 5120, 256),
              (4096, 1280, 3424, 160), (4096, 3840, 1280, 256),
              # small grids: every tile split (the 128-token first chunk's GEMMs)
-             (128, 3584, 18944, 128), (128, 4608, 3584, 128), (100, 3584, 3584, 128), (128, 37888, 3584, 0)]
+             (128, 3584, 18944, 128), (128, 4608, 3584, 128), (100, 3584, 3584, 128), (128, 37888, 3584, 0),
+             # CTA-pair tiles with split tails (bn < 0), incl. a ragged M
+             (2048, 3584, 18944, -256), (2048, 3584, 3584, -256), (1056, 3584, 18944, -256),
+             (128, 3584, 18944, -128), (2048, 4608, 3584, -160)]
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _pair_split(request):
+    # exercise the CTA-pair split-tail path too (off by default in the heuristic)
+    import os
+    os.environ["RS_GEMM_PAIR_SPLIT"] = "1"
 
 
 @pytest.mark.parametrize("epi", [0, 1, 2, 3])
