@@ -19,6 +19,7 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -430,10 +431,62 @@ struct PpCfg {
   static constexpr int kSmem = 2 * kQBytes + kKStages * kKBytes + kVStages * kVBytes + 1024 + 512;
 };
 
+// Persistent: grid = min(units, 148) CTAs; unit u = (work item u / H, head
+// u % H) in the callers' longest-first order, dealt to CTAs in a snake
+// (round r: CTA c takes r*G + c, or r*G + G-1-c on odd rounds) so each SM
+// gets a balanced mix of long and short units. Barrier phases, the K / V
+// rings and the TMEM tiles carry over from unit to unit.
+struct PpUnit {
+  int head, kvh, q_row0, q_rows, q_pos0, key_begin, key_end;
+  int rows_t[2], n_t[2], n_max;
+  const int* pt;
+};
+
+template <KvMode MODE>
+__device__ __forceinline__ PpUnit pp_unit(const TcParams& p, int u) {
+  PpUnit x;
+  const int w = u / p.q_heads;
+  x.head = u - w * p.q_heads;
+  x.kvh = x.head / (p.q_heads / p.kv_heads);
+  x.q_pos0 = 0;
+  x.pt = nullptr;
+  if constexpr (MODE == KvMode::kPaged) {
+    const PrefillWork wk = p.work[w];
+    x.q_row0 = wk.q_row0;
+    x.q_rows = wk.q_rows;
+    x.q_pos0 = wk.q_pos0;
+    x.key_begin = 0;
+    x.key_end = wk.q_pos0 + wk.q_rows;
+    x.pt = p.page_tables[wk.req_slot];
+  } else {
+    const AttnBlock b = p.blocks[w];
+    x.q_row0 = b.q_row0;
+    x.q_rows = b.q_rows;
+    x.key_begin = b.key_begin & ~7;  // 16-B aligned V^T tile start (extra keys masked)
+    x.key_end = b.key_end;
+  }
+  x.rows_t[0] = min(x.q_rows, 128);
+  x.rows_t[1] = max(x.q_rows - 128, 0);
+#pragma unroll
+  for (int t = 0; t < 2; ++t) {
+    const int hi = MODE == KvMode::kPaged ? x.q_pos0 + 128 * t + x.rows_t[t] : x.key_end;
+    x.n_t[t] = x.rows_t[t] > 0 ? (hi - x.key_begin + 127) / 128 : 0;
+  }
+  x.n_max = max(x.n_t[0], x.n_t[1]);
+  return x;
+}
+
+// unit of CTA c in round r (snake order), -1 when past the end
+__device__ __forceinline__ int pp_unit_index(int r, int n_units) {
+  const int G = static_cast<int>(gridDim.x), c = static_cast<int>(blockIdx.x);
+  const int u = r * G + ((r & 1) ? G - 1 - c : c);
+  return u < n_units ? u : -1;
+}
+
 template <int HD, KvMode MODE>
 __global__ void __launch_bounds__(kPpThreads, 1)
     fa_pp_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
-                 const __grid_constant__ CUtensorMap tmV, const TcParams p) {
+                 const __grid_constant__ CUtensorMap tmV, const TcParams p, int n_units) {
   using C = PpCfg<HD>;
   constexpr int SK = C::kKStages, SV = C::kVStages;
   extern __shared__ __align__(1024) std::uint8_t smem_raw[];
@@ -444,47 +497,19 @@ __global__ void __launch_bounds__(kPpThreads, 1)
   std::uint8_t* sV = sK + SK * C::kKBytes;
   std::uint64_t* bars = reinterpret_cast<std::uint64_t*>(sV + SV * C::kVBytes);
   std::uint64_t* q_full = bars;            // [2]
-  std::uint64_t* k_full = bars + 2;        // [SK]
+  std::uint64_t* q_empty = bars + 2;       // [2] last S of the tile's unit issued+done
+  std::uint64_t* k_full = bars + 4;        // [SK]
   std::uint64_t* k_empty = k_full + SK;    // [SK]
   std::uint64_t* v_full = k_empty + SK;    // [SV]
   std::uint64_t* v_empty = v_full + SV;    // [SV]
   std::uint64_t* s_full = v_empty + SV;    // [2] S_t,j ready (and PV_t,j-1 done)
   std::uint64_t* p_full = s_full + 2;      // [2] P_t,j written (128 softmax threads)
-  std::uint64_t* o_final = p_full + 2;     // [2] last PV_t done
+  std::uint64_t* o_final = p_full + 2;     // [2] last PV_t of a unit done
   std::uint32_t* tmem_holder = reinterpret_cast<std::uint32_t*>(o_final + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   pdl_wait();
   pdl_launch_dependents();
-  const int head = blockIdx.x;
-  const int kvh = head / (p.q_heads / p.kv_heads);
-  int q_row0, q_rows, key_begin, key_end, q_pos0 = 0;
-  const int* pt = nullptr;
-  if constexpr (MODE == KvMode::kPaged) {
-    const PrefillWork w = p.work[blockIdx.y];
-    q_row0 = w.q_row0;
-    q_rows = w.q_rows;
-    q_pos0 = w.q_pos0;
-    key_begin = 0;
-    key_end = w.q_pos0 + w.q_rows;
-    pt = p.page_tables[w.req_slot];
-  } else {
-    const AttnBlock b = p.blocks[blockIdx.y];
-    q_row0 = b.q_row0;
-    q_rows = b.q_rows;
-    key_begin = b.key_begin & ~7;  // 16-B aligned V^T tile start (extra keys masked)
-    key_end = b.key_end;
-  }
-  const int rows_t[2] = {min(q_rows, 128), max(q_rows - 128, 0)};
-  int n_t[2];
-#pragma unroll
-  for (int t = 0; t < 2; ++t) {
-    const int hi = MODE == KvMode::kPaged ? q_pos0 + 128 * t + rows_t[t] : key_end;
-    n_t[t] = rows_t[t] > 0 ? (hi - key_begin + 127) / 128 : 0;
-  }
-  const int n_max = max(n_t[0], n_t[1]);
-  // last consumer of K_j / V_j (tile 1 covers every key tile tile 0 does)
-  auto last_user = [&](int j) { return j < n_t[1] ? 1 : 0; };
 
   if (threadIdx.x == 0) {
     sm100::tma_prefetch_desc(&tmQ);
@@ -492,6 +517,7 @@ __global__ void __launch_bounds__(kPpThreads, 1)
     sm100::tma_prefetch_desc(&tmV);
     for (int t = 0; t < 2; ++t) {
       sm100::mbar_init(&q_full[t], 1);
+      sm100::mbar_init(&q_empty[t], 1);
       sm100::mbar_init(&s_full[t], 1);
       sm100::mbar_init(&p_full[t], 128);
       sm100::mbar_init(&o_final[t], 1);
@@ -512,121 +538,159 @@ __global__ void __launch_bounds__(kPpThreads, 1)
   sm100::tc_fence_after();
   const std::uint32_t tmem = *tmem_holder;
 
-  const int n_real_pages = (key_end - key_begin + 63) / 64;
-  auto pages = [&](int j, int& pa, int& pb) {
-    pa = pt[2 * j];
-    pb = 2 * j + 1 < n_real_pages ? pt[2 * j + 1] : pa;  // duplicate: finite, masked
+  auto pages = [&](const PpUnit& x, int j, int& pa, int& pb) {
+    const int n_real_pages = (x.key_end - x.key_begin + 63) / 64;
+    pa = x.pt[2 * j];
+    pb = 2 * j + 1 < n_real_pages ? x.pt[2 * j + 1] : pa;  // duplicate: finite, masked
   };
+
   if (warp == 0 && lane == 0) {
     // ---------------- TMA producer: Q tiles and the K ring ----------------
-    for (int t = 0; t < 2; ++t) {
-      if (rows_t[t] == 0) continue;
-      sm100::mbar_expect_tx(&q_full[t], C::kQBytes);
-      for (int h = 0; h < C::kHdAtoms; ++h)
-        sm100::tma_load_2d(sQ + t * C::kQBytes + h * kAtom, &tmQ, &q_full[t],
-                           head * p.q_head_stride + h * 64, q_row0 + 128 * t);
-    }
-    for (int j = 0; j < n_max; ++j) {
-      const int st = j % SK;
-      std::uint8_t* k = sK + st * C::kKBytes;
-      sm100::mbar_wait(&k_empty[st], ((j / SK) & 1) ^ 1);
-      sm100::mbar_expect_tx(&k_full[st], C::kKBytes);
-      if constexpr (MODE == KvMode::kPaged) {
-        int pa, pb;
-        pages(j, pa, pb);
-        for (int h = 0; h < C::kHdAtoms; ++h) {
-          sm100::tma_load_2d(k + h * kAtom, &tmK, &k_full[st], h * 64, (pa * p.kv_heads + kvh) * 64);
-          sm100::tma_load_2d(k + h * kAtom + 64 * 128, &tmK, &k_full[st], h * 64,
-                             (pb * p.kv_heads + kvh) * 64);
-        }
-      } else {
+    std::uint32_t qn[2] = {0, 0};
+    std::uint32_t kn = 0;
+    for (int r = 0;; ++r) {
+      const int u = pp_unit_index(r, n_units);
+      if (u < 0) break;
+      const PpUnit x = pp_unit<MODE>(p, u);
+      for (int t = 0; t < 2; ++t) {
+        if (x.rows_t[t] == 0) continue;
+        sm100::mbar_wait(&q_empty[t], (qn[t] & 1) ^ 1);
+        ++qn[t];
+        sm100::mbar_expect_tx(&q_full[t], C::kQBytes);
         for (int h = 0; h < C::kHdAtoms; ++h)
-          sm100::tma_load_2d(k + h * kAtom, &tmK, &k_full[st], kvh * p.q_head_stride + h * 64,
-                             key_begin + 128 * j);
+          sm100::tma_load_2d(sQ + t * C::kQBytes + h * kAtom, &tmQ, &q_full[t],
+                             x.head * p.q_head_stride + h * 64, x.q_row0 + 128 * t);
+      }
+      for (int j = 0; j < x.n_max; ++j, ++kn) {
+        const int st = static_cast<int>(kn % SK);
+        std::uint8_t* k = sK + st * C::kKBytes;
+        sm100::mbar_wait(&k_empty[st], ((kn / SK) & 1) ^ 1);
+        sm100::mbar_expect_tx(&k_full[st], C::kKBytes);
+        if constexpr (MODE == KvMode::kPaged) {
+          int pa, pb;
+          pages(x, j, pa, pb);
+          for (int h = 0; h < C::kHdAtoms; ++h) {
+            sm100::tma_load_2d(k + h * kAtom, &tmK, &k_full[st], h * 64, (pa * p.kv_heads + x.kvh) * 64);
+            sm100::tma_load_2d(k + h * kAtom + 64 * 128, &tmK, &k_full[st], h * 64,
+                               (pb * p.kv_heads + x.kvh) * 64);
+          }
+        } else {
+          for (int h = 0; h < C::kHdAtoms; ++h)
+            sm100::tma_load_2d(k + h * kAtom, &tmK, &k_full[st], x.kvh * p.q_head_stride + h * 64,
+                               x.key_begin + 128 * j);
+        }
       }
     }
   } else if (warp == kPpThreads / 32 - 1 && lane == 0) {
     // ---------------- TMA producer: the V ring (own thread: never queued behind K) ----------------
-    for (int j = 0; j < n_max; ++j) {
-      const int st = j % SV;
-      std::uint8_t* v = sV + st * C::kVBytes;
-      sm100::mbar_wait(&v_empty[st], ((j / SV) & 1) ^ 1);
-      sm100::mbar_expect_tx(&v_full[st], C::kVBytes);
-      if constexpr (MODE == KvMode::kPaged) {
-        int pa, pb;
-        pages(j, pa, pb);
-        sm100::tma_load_2d(v, &tmV, &v_full[st], 0, (pa * p.kv_heads + kvh) * HD);
-        sm100::tma_load_2d(v + C::kVAtom, &tmV, &v_full[st], 0, (pb * p.kv_heads + kvh) * HD);
-      } else {
-        const int k0 = key_begin + 128 * j;
-        sm100::tma_load_2d(v, &tmV, &v_full[st], k0, kvh * HD);
-        sm100::tma_load_2d(v + C::kVAtom, &tmV, &v_full[st], k0 + 64, kvh * HD);
+    std::uint32_t vn = 0;
+    for (int r = 0;; ++r) {
+      const int u = pp_unit_index(r, n_units);
+      if (u < 0) break;
+      const PpUnit x = pp_unit<MODE>(p, u);
+      for (int j = 0; j < x.n_max; ++j, ++vn) {
+        const int st = static_cast<int>(vn % SV);
+        std::uint8_t* v = sV + st * C::kVBytes;
+        sm100::mbar_wait(&v_empty[st], ((vn / SV) & 1) ^ 1);
+        sm100::mbar_expect_tx(&v_full[st], C::kVBytes);
+        if constexpr (MODE == KvMode::kPaged) {
+          int pa, pb;
+          pages(x, j, pa, pb);
+          sm100::tma_load_2d(v, &tmV, &v_full[st], 0, (pa * p.kv_heads + x.kvh) * HD);
+          sm100::tma_load_2d(v + C::kVAtom, &tmV, &v_full[st], 0, (pb * p.kv_heads + x.kvh) * HD);
+        } else {
+          const int k0 = x.key_begin + 128 * j;
+          sm100::tma_load_2d(v, &tmV, &v_full[st], k0, x.kvh * HD);
+          sm100::tma_load_2d(v + C::kVAtom, &tmV, &v_full[st], k0 + 64, x.kvh * HD);
+        }
       }
     }
   } else if (warp == 1 && lane == 0) {
     // ---------------- MMA issuer ----------------
     constexpr std::uint32_t idesc_s = sm100::idesc_bf16_f32(128, 128);
     constexpr std::uint32_t idesc_o = sm100::idesc_bf16_f32(128, HD);
-    for (int t = 0; t < 2; ++t)
-      if (rows_t[t] > 0) sm100::mbar_wait(&q_full[t], 0);
-    auto mma_s = [&](int t, int j) {
-      const int st = j % SK;
-      sm100::mbar_wait(&k_full[st], (j / SK) & 1);
-      sm100::tc_fence_after();
-      std::uint8_t* k = sK + st * C::kKBytes;
+    std::uint32_t qn[2] = {0, 0}, pn[2] = {0, 0};
+    std::uint32_t kbase = 0;  // K / V tiles consumed before this unit
+    for (int r = 0;; ++r) {
+      const int u = pp_unit_index(r, n_units);
+      if (u < 0) break;
+      const PpUnit x = pp_unit<MODE>(p, u);
+      for (int t = 0; t < 2; ++t)
+        if (x.rows_t[t] > 0) {
+          sm100::mbar_wait(&q_full[t], qn[t] & 1);
+          ++qn[t];
+        }
+      // last consumer of K_j / V_j (tile 1 covers every key tile tile 0 does)
+      auto last_user = [&](int j) { return j < x.n_t[1] ? 1 : 0; };
+      auto mma_s = [&](int t, int j) {
+        const std::uint32_t kn = kbase + static_cast<std::uint32_t>(j);
+        const int st = static_cast<int>(kn % SK);
+        sm100::mbar_wait(&k_full[st], (kn / SK) & 1);
+        sm100::tc_fence_after();
+        std::uint8_t* k = sK + st * C::kKBytes;
 #pragma unroll
-      for (int h = 0; h < C::kHdAtoms; ++h) {
-        const std::uint64_t qd = sm100::sw128_kmajor_desc(sm100::smem_u32(sQ + t * C::kQBytes + h * kAtom));
-        const std::uint64_t kd = sm100::sw128_kmajor_desc(sm100::smem_u32(k + h * kAtom));
+        for (int h = 0; h < C::kHdAtoms; ++h) {
+          const std::uint64_t qd = sm100::sw128_kmajor_desc(sm100::smem_u32(sQ + t * C::kQBytes + h * kAtom));
+          const std::uint64_t kd = sm100::sw128_kmajor_desc(sm100::smem_u32(k + h * kAtom));
 #pragma unroll
-        for (int kk = 0; kk < 4; ++kk)
-          sm100::umma_bf16(tmem + 256 * t, qd + 2 * kk, kd + 2 * kk, idesc_s, (h | kk) != 0 ? 1u : 0u);
+          for (int kk = 0; kk < 4; ++kk)
+            sm100::umma_bf16(tmem + 256 * t, qd + 2 * kk, kd + 2 * kk, idesc_s, (h | kk) != 0 ? 1u : 0u);
+        }
+        sm100::umma_commit(&s_full[t]);
+        if (t == last_user(j)) sm100::umma_commit(&k_empty[st]);
+        if (j == (t == 0 ? x.n_t[0] : x.n_t[1]) - 1) sm100::umma_commit(&q_empty[t]);
+      };
+      auto mma_pv = [&](int t, int j) {
+        const std::uint32_t vn = kbase + static_cast<std::uint32_t>(j);
+        const int st = static_cast<int>(vn % SV);
+        sm100::mbar_wait(&v_full[st], (vn / SV) & 1);
+        sm100::mbar_wait(&p_full[t], pn[t] & 1);
+        ++pn[t];
+        sm100::tc_fence_after();
+        std::uint8_t* v = sV + st * C::kVBytes;
+#pragma unroll
+        for (int a = 0; a < 2; ++a) {
+          const std::uint64_t vd = sm100::sw128_kmajor_desc(sm100::smem_u32(v + a * C::kVAtom));
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk)
+            sm100::umma_bf16_ts(tmem + 256 * t + 128, tmem + 256 * t + 32 * a + 8 * kk, vd + 2 * kk,
+                                idesc_o, (j | a | kk) != 0 ? 1u : 0u);
+        }
+        if (t == last_user(j)) sm100::umma_commit(&v_empty[st]);
+        if (j == (t == 0 ? x.n_t[0] : x.n_t[1]) - 1) sm100::umma_commit(&o_final[t]);
+      };
+      if (x.n_t[0] > 0) mma_s(0, 0);
+      if (x.n_t[1] > 0) mma_s(1, 0);
+      for (int j = 1; j <= x.n_max; ++j) {
+        if (j - 1 < x.n_t[0]) mma_pv(0, j - 1);
+        if (j < x.n_t[0]) mma_s(0, j);
+        if (j - 1 < x.n_t[1]) mma_pv(1, j - 1);
+        if (j < x.n_t[1]) mma_s(1, j);
       }
-      sm100::umma_commit(&s_full[t]);
-      if (t == last_user(j)) sm100::umma_commit(&k_empty[st]);
-    };
-    auto mma_pv = [&](int t, int j) {
-      const int st = j % SV;
-      sm100::mbar_wait(&v_full[st], (j / SV) & 1);
-      sm100::mbar_wait(&p_full[t], j & 1);
-      sm100::tc_fence_after();
-      std::uint8_t* v = sV + st * C::kVBytes;
-#pragma unroll
-      for (int a = 0; a < 2; ++a) {
-        const std::uint64_t vd = sm100::sw128_kmajor_desc(sm100::smem_u32(v + a * C::kVAtom));
-#pragma unroll
-        for (int kk = 0; kk < 4; ++kk)
-          sm100::umma_bf16_ts(tmem + 256 * t + 128, tmem + 256 * t + 32 * a + 8 * kk, vd + 2 * kk,
-                              idesc_o, (j | a | kk) != 0 ? 1u : 0u);
-      }
-      if (t == last_user(j)) sm100::umma_commit(&v_empty[st]);
-      if (j == n_t[t] - 1) sm100::umma_commit(&o_final[t]);
-    };
-    if (n_t[0] > 0) mma_s(0, 0);
-    if (n_t[1] > 0) mma_s(1, 0);
-    for (int j = 1; j <= n_max; ++j) {
-      if (j - 1 < n_t[0]) mma_pv(0, j - 1);
-      if (j < n_t[0]) mma_s(0, j);
-      if (j - 1 < n_t[1]) mma_pv(1, j - 1);
-      if (j < n_t[1]) mma_s(1, j);
+      kbase += static_cast<std::uint32_t>(x.n_max);
     }
   } else if (warp >= 2 && warp < 10) {
     // ---------------- softmax: tile t, one query row per thread ----------------
     const int t = (warp - 2) >> 2;
     const int quad = warp & 3;
     const int r = quad * 32 + lane;  // row within the tile
-    const int n_it = t == 0 ? n_t[0] : n_t[1];
-    const int my_rows = t == 0 ? rows_t[0] : rows_t[1];
-    if (n_it > 0) {
-      const std::uint32_t lane_off = static_cast<std::uint32_t>(quad * 32) << 16;
-      const std::uint32_t s_tm = tmem + lane_off + 256 * t;
-      const std::uint32_t o_tm = s_tm + 128;
+    const std::uint32_t lane_off = static_cast<std::uint32_t>(quad * 32) << 16;
+    const std::uint32_t s_tm = tmem + lane_off + 256 * t;
+    const std::uint32_t o_tm = s_tm + 128;
+    std::uint32_t sn = 0, on = 0;
+    for (int rr = 0;; ++rr) {
+      const int u = pp_unit_index(rr, n_units);
+      if (u < 0) break;
+      const PpUnit x = pp_unit<MODE>(p, u);
+      const int n_it = t == 0 ? x.n_t[0] : x.n_t[1];
+      const int my_rows = t == 0 ? x.rows_t[0] : x.rows_t[1];
+      if (n_it == 0) continue;
       int lo, hi;
       if constexpr (MODE == KvMode::kPaged) {
         lo = 0;
-        hi = min(q_pos0 + 128 * t + r + 1, key_end);
+        hi = min(x.q_pos0 + 128 * t + r + 1, x.key_end);
       } else {
-        const int row = q_row0 + 128 * t + min(r, my_rows - 1);
+        const int row = x.q_row0 + 128 * t + min(r, my_rows - 1);
         int a = 0, b = p.n_seqs;  // largest s with cu[s] <= row
         while (b - a > 1) {
           const int mid = (a + b) >> 1;
@@ -638,9 +702,10 @@ __global__ void __launch_bounds__(kPpThreads, 1)
       }
       float m = -INFINITY, l = 0.f;
       for (int j = 0; j < n_it; ++j) {
-        sm100::mbar_wait(&s_full[t], j & 1);
+        sm100::mbar_wait(&s_full[t], sn & 1);
+        ++sn;
         sm100::tc_fence_after();
-        const int key0 = key_begin + j * 128;
+        const int key0 = x.key_begin + j * 128;
         const int c_lo = lo - key0, c_hi = hi - key0;  // visible columns [c_lo, c_hi)
         std::uint32_t sv[128];
 #pragma unroll
@@ -651,14 +716,14 @@ __global__ void __launch_bounds__(kPpThreads, 1)
         sm100::tmem_ld_wait();
         if (!(c_lo <= 0 && c_hi >= 128)) {
 #pragma unroll
-          for (int u = 0; u < 128; ++u)
-            if (u < c_lo || u >= c_hi) sv[u] = __float_as_uint(-INFINITY);
+          for (int q = 0; q < 128; ++q)
+            if (q < c_lo || q >= c_hi) sv[q] = __float_as_uint(-INFINITY);
         }
         float mx8[8];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) mx8[u] = __uint_as_float(sv[u]);
+        for (int q = 0; q < 8; ++q) mx8[q] = __uint_as_float(sv[q]);
 #pragma unroll
-        for (int u = 8; u < 128; ++u) mx8[u & 7] = fmaxf(mx8[u & 7], __uint_as_float(sv[u]));
+        for (int q = 8; q < 128; ++q) mx8[q & 7] = fmaxf(mx8[q & 7], __uint_as_float(sv[q]));
         float mx = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
                          fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7])));
         mx *= p.scale_log2;
@@ -676,7 +741,7 @@ __global__ void __launch_bounds__(kPpThreads, 1)
             sm100::tmem_ld_32x32b_x32(o_tm + 32 * c, v);
             sm100::tmem_ld_wait();
 #pragma unroll
-            for (int u = 0; u < 32; ++u) v[u] = __float_as_uint(__uint_as_float(v[u]) * alpha);
+            for (int q = 0; q < 32; ++q) v[q] = __float_as_uint(__uint_as_float(v[q]) * alpha);
             sm100::tmem_st_32x32b_x32(o_tm + 32 * c, v);
           }
         }
@@ -686,15 +751,15 @@ __global__ void __launch_bounds__(kPpThreads, 1)
         for (int c = 0; c < 4; ++c) {
           std::uint32_t packed[16];  // 32 keys as bf16 pairs
 #pragma unroll
-          for (int u = 0; u < 16; ++u) {
-            const float x0 = fmaf(__uint_as_float(sv[32 * c + 2 * u]), p.scale_log2, mneg);
-            const float x1 = fmaf(__uint_as_float(sv[32 * c + 2 * u + 1]), p.scale_log2, mneg);
-            const bool poly = (u & 3) == 3;  // every 4th pair on the FMA pipe
+          for (int q = 0; q < 16; ++q) {
+            const float x0 = fmaf(__uint_as_float(sv[32 * c + 2 * q]), p.scale_log2, mneg);
+            const float x1 = fmaf(__uint_as_float(sv[32 * c + 2 * q + 1]), p.scale_log2, mneg);
+            const bool poly = (q & 3) == 3;  // every 4th pair on the FMA pipe
             const float p0 = poly ? poly_exp2_fma(x0) : fast_exp2(x0);
             const float p1 = poly ? poly_exp2_fma(x1) : fast_exp2(x1);
-            rs8[(2 * u) & 7] += p0;
-            rs8[(2 * u + 1) & 7] += p1;
-            packed[u] = pack_bf16x2(p0, p1);
+            rs8[(2 * q) & 7] += p0;
+            rs8[(2 * q + 1) & 7] += p1;
+            packed[q] = pack_bf16x2(p0, p1);
           }
           sm100::tmem_st_32x32b_x16(s_tm + 16 * c, packed);
         }
@@ -703,10 +768,11 @@ __global__ void __launch_bounds__(kPpThreads, 1)
         sm100::mbar_arrive(&p_full[t]);
         l = l * alpha + (((rs8[0] + rs8[1]) + (rs8[2] + rs8[3])) + ((rs8[4] + rs8[5]) + (rs8[6] + rs8[7])));
       }
-      sm100::mbar_wait(&o_final[t], 0);
+      sm100::mbar_wait(&o_final[t], on & 1);
+      ++on;
       sm100::tc_fence_after();
       const float inv = l > 0.f ? 1.f / l : 0.f;
-      bf16* orow = p.out + static_cast<std::int64_t>(q_row0 + 128 * t + r) * p.ld_out + head * p.out_hd;
+      bf16* orow = p.out + static_cast<std::int64_t>(x.q_row0 + 128 * t + r) * p.ld_out + x.head * p.out_hd;
 #pragma unroll
       for (int c = 0; c < HD / 32; ++c) {
         std::uint32_t v[32];
@@ -714,16 +780,18 @@ __global__ void __launch_bounds__(kPpThreads, 1)
         sm100::tmem_ld_wait();
         if (r < my_rows) {
 #pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            if (32 * c + 8 * u < p.out_hd)
-              reinterpret_cast<uint4*>(orow + 32 * c)[u] = make_uint4(
-                  pack_bf16x2(__uint_as_float(v[8 * u]) * inv, __uint_as_float(v[8 * u + 1]) * inv),
-                  pack_bf16x2(__uint_as_float(v[8 * u + 2]) * inv, __uint_as_float(v[8 * u + 3]) * inv),
-                  pack_bf16x2(__uint_as_float(v[8 * u + 4]) * inv, __uint_as_float(v[8 * u + 5]) * inv),
-                  pack_bf16x2(__uint_as_float(v[8 * u + 6]) * inv, __uint_as_float(v[8 * u + 7]) * inv));
+          for (int q = 0; q < 4; ++q) {
+            if (32 * c + 8 * q < p.out_hd)
+              reinterpret_cast<uint4*>(orow + 32 * c)[q] = make_uint4(
+                  pack_bf16x2(__uint_as_float(v[8 * q]) * inv, __uint_as_float(v[8 * q + 1]) * inv),
+                  pack_bf16x2(__uint_as_float(v[8 * q + 2]) * inv, __uint_as_float(v[8 * q + 3]) * inv),
+                  pack_bf16x2(__uint_as_float(v[8 * q + 4]) * inv, __uint_as_float(v[8 * q + 5]) * inv),
+                  pack_bf16x2(__uint_as_float(v[8 * q + 6]) * inv, __uint_as_float(v[8 * q + 7]) * inv));
           }
         }
       }
+      // O_t is read out (tcgen05.ld waited): the next unit's first PV may overwrite it
+      sm100::tc_fence_before();
     }
   }
   __syncthreads();
@@ -810,8 +878,11 @@ void launch(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
   if (n_blocks > 65535) throw DeviceError(RS_ERR_CUDA, "tc attention: too many blocks for grid.y");
   dim3 grid(p.q_heads, n_blocks);
   const int tok = prof::begin(st);
-  if (attn_unit_rows() == 256)
-    launch_kernel(fa_pp_kernel<HD, MODE>, grid, dim3(kPpThreads), PpCfg<HD>::kSmem, st, 1, tq, tk, tv, p);
+  if (attn_unit_rows() == 256) {
+    const int units = p.q_heads * n_blocks;
+    launch_kernel(fa_pp_kernel<HD, MODE>, dim3(std::min(units, kNumSMs)), dim3(kPpThreads), PpCfg<HD>::kSmem,
+                  st, 1, tq, tk, tv, p, units);
+  }
   else
     launch_kernel(fa_tc_kernel<HD, MODE>, grid, dim3(kTcThreads), TcCfg<HD>::kSmem, st, 1, tq, tk, tv, p);
   RS_LAUNCH_CHECK();
