@@ -227,7 +227,20 @@ typedef struct rs_run_options {
   int32_t e2e;          /* 1: H2D inputs / D2H logits inside the run */
   int32_t serialize;    /* 1: encoders share the prefill stream (profiling) */
   uint64_t payload_seed;
+  const char* payload_text; /* optional payload file (see below); co-located runs */
 } rs_run_options;
+
+/* ---- payload files ---------------------------------------
+ * The reference's workload file (workload.hpp:217-265) carries layouts only.
+ * A payload file beside it pins per-segment inputs: image grids and pixel
+ * seeds, text token-id seeds or explicit ids:
+ *   # rserve payload v1
+ *   <req_id>,<segment_index>,M,grid=<gh>x<gw>[;seed=<u64>]
+ *   <req_id>,<segment_index>,T,seed=<u64> | ids=<id> <id> ...
+ * Errors: RS_ERR_INPUT with "payload line N: ..." / "payload: request ...". */
+RS_API rs_status rs_payload_generate(const char* workload_text, uint64_t seed, char** out_text);
+RS_API rs_status rs_payload_validate(const char* workload_text, const char* payload_text,
+                                     int32_t vocab, char** out_normalized);
 typedef struct rs_run_stats {
   double wall_ms;            /* host wall time of the run                 */
   double gpu_ms;             /* first launch -> last completion (events)  */

@@ -138,9 +138,9 @@ def item_grid(tokens: int) -> Tuple[int, int]:
     return best, tokens // best
 
 
-def item_plan(tokens: int, window: int):
+def item_plan(tokens: int, window: int, grid: Optional[Tuple[int, int]] = None):
     """(pos_hw [P,2], windows [list of (start,end)], out_row [T]) of one item."""
-    gh, gw = item_grid(tokens)
+    gh, gw = grid if grid is not None else item_grid(tokens)
     pos, wins, out_row = [], [], []
     p = 0
     for wy in range(0, gh, window):
@@ -158,16 +158,19 @@ def item_plan(tokens: int, window: int):
     return np.array(pos, dtype=np.int64), wins, np.array(out_row, dtype=np.int64)
 
 
-def mrope_positions(segments: Sequence[Tuple[str, int]]) -> np.ndarray:
+def mrope_positions(segments: Sequence[Tuple[str, int]],
+                    grids: Optional[Sequence[Tuple[int, int]]] = None) -> np.ndarray:
     out = []
     cur = 0
+    item = 0
     for kind, n in segments:
         if kind == "T":
             for _ in range(n):
                 out.append((cur, cur, cur))
                 cur += 1
         else:
-            gh, gw = item_grid(n)
+            gh, gw = grids[item] if grids is not None else item_grid(n)
+            item += 1
             for r in range(gh):
                 for c in range(gw):
                     out.append((cur, cur + r, cur + c))
@@ -255,14 +258,15 @@ class VisionOracle:
         return uniform(payload_seed, pixel_stream(req_id, item), 4 * tokens, self.c.patch_dim,
                        PIXEL_SCALE)
 
-    def encode(self, items: Sequence[Tuple[int, np.ndarray]], layers: Optional[int] = None,
+    def encode(self, items: Sequence[Tuple], layers: Optional[int] = None,
                bf16_acts: bool = False) -> np.ndarray:
-        """items: (tokens, patches [4*tokens, pdim]) in batch order ->
-        embeddings [sum tokens, d_llm] in LLM (row-major) order."""
+        """items: (tokens, patches [4*tokens, pdim][, grid (gh, gw)]) in batch
+        order -> embeddings [sum tokens, d_llm] in LLM (row-major) order."""
         c, W = self.c, self.w
         rnd = bf16_round if bf16_acts else (lambda a: a)
         vd, hd, nh = c.vit_dim, c.vit_dim // c.vit_heads, c.vit_heads
-        plans = [item_plan(t, c.vit_window) for t, _ in items]
+        plans = [item_plan(it[0], c.vit_window, it[2] if len(it) > 2 else None) for it in items]
+        items = [(it[0], it[1]) for it in items]
         x = np.concatenate([p for _, p in items]).astype(np.float32)
         pos = np.concatenate([pl[0] for pl in plans])
         P = x.shape[0]
@@ -388,10 +392,11 @@ class LlmOracle:
 # ---------------------------------------------------------------------------
 def request_embeddings(cfg: ModelConfig, weights: Weights, req_id: int, layout: str,
                        payload_seed: int, c_tokens: int, bf16_acts: bool = False,
-                       vit_layers: Optional[int] = None) -> np.ndarray:
+                       vit_layers: Optional[int] = None, payload=None) -> np.ndarray:
     """Input embeddings [T, d] of a request: text rows from the vocab table,
     multimodal rows from the vision encoder run on Algorithm-1 batches of
-    >= c_tokens tokens (encoder_sched.hpp:48-74)."""
+    >= c_tokens tokens (encoder_sched.hpp:48-74). `payload`: this request's
+    resolved payload (oracle/payload.py) — item grids / pixel seeds / token ids."""
     segs = parse_layout(layout)
     vis = VisionOracle(cfg, weights)
     T = sum(n for _, n in segs)
@@ -407,7 +412,9 @@ def request_embeddings(cfg: ModelConfig, weights: Weights, req_id: int, layout: 
         pos += n
     if text_pos:
         tp = np.array(text_pos, dtype=np.int64)
-        emb[tp] = weights.embed_rows(token_ids(payload_seed, req_id, tp, cfg.vocab))
+        ids = (np.asarray(payload["text_ids"], dtype=np.int64) if payload is not None
+               else token_ids(payload_seed, req_id, tp, cfg.vocab))
+        emb[tp] = weights.embed_rows(ids)
     batch: List[Tuple[int, int, int]] = []
     acc = 0
 
@@ -415,7 +422,11 @@ def request_embeddings(cfg: ModelConfig, weights: Weights, req_id: int, layout: 
         nonlocal batch, acc
         if not batch:
             return
-        ins = [(n, vis.patches(payload_seed, req_id, i, n)) for i, _, n in batch]
+        if payload is not None:
+            ins = [(n, vis.patches(payload["item_seeds"][i], req_id, i, n), tuple(payload["item_grids"][i]))
+                   for i, _, n in batch]
+        else:
+            ins = [(n, vis.patches(payload_seed, req_id, i, n)) for i, _, n in batch]
         out = vis.encode(ins, layers=vit_layers, bf16_acts=bf16_acts)
         r = 0
         for _, s, n in batch:

@@ -124,7 +124,7 @@ class rs_ctx_options(C.Structure):
 
 class rs_run_options(C.Structure):
     _fields_ = [("clock", C.c_int32), ("e2e", C.c_int32), ("serialize", C.c_int32),
-                ("payload_seed", C.c_uint64)]
+                ("payload_seed", C.c_uint64), ("payload_text", C.c_char_p)]
 
 
 class rs_run_stats(C.Structure):
@@ -211,6 +211,8 @@ _sig("rs_op_attention_prefill", [VP, I, I, VP, I, I, I, VP, VP, C.c_longlong, VP
                                   C.c_float, VP])
 _sig("rs_kernel_launches", [], C.c_ulonglong)
 _sig("rs_profile_enable", [C.c_int])
+_sig("rs_payload_generate", [C.c_char_p, C.c_uint64, PCHAR])
+_sig("rs_payload_validate", [C.c_char_p, C.c_char_p, C.c_int32, PCHAR])
 _sig("rs_profile_drain", [PCHAR])
 
 

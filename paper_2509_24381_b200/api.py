@@ -153,6 +153,23 @@ def generate_workload(cfg: WorkloadConfig) -> str:
     return N.take_string(out)
 
 
+def generate_payload(workload: str, seed: int) -> str:
+    """Payload file (rserve.h "payload files") for a workload:
+    per image a grid drawn among its token count's factorisations (aspect <= 4)
+    and a pixel seed, per text segment a token-id seed, all keyed by `seed`."""
+    out = _out()
+    N.check(N.lib.rs_payload_generate(workload.encode(), seed, C.byref(out)))
+    return N.take_string(out)
+
+
+def validate_payload(workload: str, payload: str, vocab: int) -> str:
+    """Checks a payload file against a workload; returns its normalised text.
+    Raises InputError ("payload line N: ..." / "payload: request ...")."""
+    out = _out()
+    N.check(N.lib.rs_payload_validate(workload.encode(), payload.encode(), vocab, C.byref(out)))
+    return N.take_string(out)
+
+
 def simulate(workload: str, cfg: SimConfig) -> Tuple[str, str]:
     """run_simulation on the analytic cost model -> (decision log, journal)."""
     res, jr = _out(), _out()
@@ -309,13 +326,15 @@ class Pipeline:
         N.check(N.lib.rs_synchronize(self.h))
 
     def run(self, workload: str, cfg: SimConfig, clock: str = "lockstep", e2e: bool = False,
-            payload_seed: int = 7, serialize: bool = False):
-        """Engine run on this device -> (decision log, journal, stats dict)."""
+            payload_seed: int = 7, serialize: bool = False, payload: Optional[str] = None):
+        """Engine run on this device -> (decision log, journal, stats dict).
+        `payload`: optional payload file text (grids, pixel seeds, token ids)."""
         o = N.rs_run_options()
         o.clock = 1 if clock == "real" else 0
         o.e2e = int(e2e)
         o.serialize = int(serialize)
         o.payload_seed = payload_seed
+        o.payload_text = payload.encode() if payload is not None else None
         res, jr = _out(), _out()
         st = N.rs_run_stats()
         c = cfg.to_c()

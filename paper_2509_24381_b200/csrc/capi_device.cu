@@ -276,6 +276,11 @@ rs_status rs_engine_run(rs_ctx* c, const char* workload_text, const rs_sim_confi
     const bool e2e = opt != nullptr && opt->e2e != 0;
     DeviceBackend backend(*x.ctx, sc, realtime, e2e, opt ? opt->payload_seed : 0,
                           opt != nullptr && opt->serialize != 0);
+    if (opt != nullptr && opt->payload_text != nullptr) {
+      PayloadSpec spec = parse_payload(opt->payload_text);
+      validate_payload(spec, wl, x.ctx->shapes().vocab);
+      backend.set_payload(std::move(spec));
+    }
     backend.prepare(wl);
     lmmsim::PipelineEngine engine(wl, sc, backend);
     backend.start();

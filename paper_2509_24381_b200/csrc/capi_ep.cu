@@ -173,6 +173,9 @@ EngineOutputs run_engine(rs_ctx& c0, rs_ep* ep, rs_ctx* const* workers, std::vec
   const bool e2e = opt != nullptr && opt->e2e != 0;
   const bool serialize = opt != nullptr && opt->serialize != 0;
   const std::uint64_t seed = opt ? opt->payload_seed : 0;
+  if (ep != nullptr && opt != nullptr && opt->payload_text != nullptr)
+    throw lmmsim::ConfigError("payload files: co-located engine runs only (EP encoder ranks derive "
+                              "pixels and grids from the layout)");
   EngineOutputs out;
   auto finish = [&](DeviceBackend& backend, lmmsim::PipelineEngine& engine) {
     backend.collect();
@@ -184,6 +187,11 @@ EngineOutputs run_engine(rs_ctx& c0, rs_ep* ep, rs_ctx* const* workers, std::vec
   };
   if (ep == nullptr) {
     DeviceBackend backend(*c0.ctx, sc, realtime, e2e, seed, serialize);
+    if (opt != nullptr && opt->payload_text != nullptr) {
+      PayloadSpec spec = parse_payload(opt->payload_text);
+      validate_payload(spec, wl, c0.ctx->shapes().vocab);
+      backend.set_payload(std::move(spec));
+    }
     backend.prepare(wl);
     lmmsim::PipelineEngine engine(wl, sc, backend);
     backend.start();

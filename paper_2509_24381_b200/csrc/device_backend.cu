@@ -135,6 +135,9 @@ void DeviceBackend::prepare(const std::vector<lmmsim::RequestSpec>& workload) {
   const Shapes& s = ctx_.shapes();
   cudaStream_t st = ctx_.aux_stream();
   for (const lmmsim::RequestSpec& req : workload) {
+    const auto pit = payload_.find(req.id);
+    const ResolvedPayload& rp = resolved_[req.id] =
+        resolve_payload(req, pit != payload_.end() ? &pit->second : nullptr, seed_, s.vocab);
     std::uint64_t patches = 0;
     for (const lmmsim::SegmentSpec& seg : req.segments)
       if (seg.kind == lmmsim::SegmentKind::Multimodal) patches += 4 * seg.tokens;
@@ -148,7 +151,7 @@ void DeviceBackend::prepare(const std::vector<lmmsim::RequestSpec>& workload) {
       for (const lmmsim::SegmentSpec& seg : req.segments) {
         if (seg.kind != lmmsim::SegmentKind::Multimodal) continue;
         fill_uniform(p.patches_dev + off * s.pdim, static_cast<std::int64_t>(4 * seg.tokens),
-                     s.pdim, s.pdim, seed_, pixel_stream(req.id, item), kPixelScale, 0.f, st);
+                     s.pdim, s.pdim, rp.item_seeds[item], pixel_stream(req.id, item), kPixelScale, 0.f, st);
         off += 4 * seg.tokens;
         ++item;
       }
@@ -202,7 +205,10 @@ void DeviceBackend::track(lmmsim::OpKind k, std::uint32_t a, std::uint64_t b, cu
 
 void DeviceBackend::on_request_created(const lmmsim::RequestSpec& req, const lmmsim::EmbeddingTracker&) {
   cudaStream_t st = ctx_.tracker_stream();
-  DevRequest& r = ctx_.create_request(req, nullptr, seed_, st);
+  const auto rit = resolved_.find(req.id);
+  DevRequest& r = rit != resolved_.end()
+                      ? ctx_.create_request(req, rit->second.text_ids.data(), seed_, st, &rit->second.item_grids)
+                      : ctx_.create_request(req, nullptr, seed_, st);
   done_slots_[req.id] = r.slot;
   if (remote_ != nullptr) layouts_[req.id] = req.segments;
   if (e2e_) {

@@ -24,6 +24,7 @@
 
 #include "device_context.cuh"
 #include "ep.cuh"
+#include "host/payload.hpp"
 #include "lmmsim/simengine.hpp"
 
 namespace rserve {
@@ -44,6 +45,8 @@ class DeviceBackend final : public lmmsim::ExecutionBackend {
                 const ep::Remote* remote = nullptr);
   ~DeviceBackend() override;
 
+  /// Payload file overrides (grids, pixel seeds, token ids); before prepare().
+  void set_payload(PayloadSpec spec) { payload_ = std::move(spec); }
   /// Generates pixel payloads of `workload` (device or pinned host). Untimed.
   void prepare(const std::vector<lmmsim::RequestSpec>& workload);
   /// Starts the clock: records the origin event.
@@ -156,6 +159,8 @@ class DeviceBackend final : public lmmsim::ExecutionBackend {
   float* remote_logits_ = nullptr;  // [max_requests, vocab] when the LM head is remote
   double remote_last_ms_ = 0;
   double last_poll_ms_ = -1;  // host-side stall diagnostics (rs_run_stats)
+  PayloadSpec payload_;
+  std::unordered_map<lmmsim::RequestId, ResolvedPayload> resolved_;
 };
 
 }  // namespace rserve

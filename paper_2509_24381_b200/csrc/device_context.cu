@@ -2,6 +2,7 @@
 #include <algorithm>
 #include <cstring>
 #include <set>
+#include <tuple>
 
 #include "device_context.cuh"
 #include "kernels.cuh"
@@ -168,14 +169,18 @@ DevRequest& Context::get(lmmsim::RequestId id) {
 namespace {
 // Qwen2-VL get_rope_index: text advances (t,t,t); an image of merged grid
 // (gh, gw) gets (s, s+row, s+col) and the next position is s + max(gh, gw).
-void mrope_ids(const lmmsim::RequestSpec& req, std::vector<std::array<std::int32_t, 3>>& out) {
+void mrope_ids(const lmmsim::RequestSpec& req, const std::vector<std::pair<int, int>>& grids,
+               std::vector<std::array<std::int32_t, 3>>& out) {
   std::int32_t cur = 0;
+  std::size_t item = 0;
   for (const lmmsim::SegmentSpec& seg : req.segments) {
     if (seg.kind == lmmsim::SegmentKind::Text) {
       for (std::uint64_t i = 0; i < seg.tokens; ++i, ++cur) out.push_back({cur, cur, cur});
     } else {
       int gh, gw;
-      item_grid(seg.tokens, &gh, &gw);
+      if (item < grids.size()) std::tie(gh, gw) = grids[item];
+      else item_grid(seg.tokens, &gh, &gw);
+      ++item;
       for (int r = 0; r < gh; ++r)
         for (int c = 0; c < gw; ++c) out.push_back({cur, cur + r, cur + c});
       cur += std::max(gh, gw);
@@ -185,7 +190,7 @@ void mrope_ids(const lmmsim::RequestSpec& req, std::vector<std::array<std::int32
 }  // namespace
 
 void Context::attach_kv(const lmmsim::RequestSpec& req, DevRequest& r, cudaStream_t st) {
-  mrope_ids(req, r.rope);
+  mrope_ids(req, r.item_grids, r.rope);
   r.slot = take_request_slot();
   const std::int64_t pages = static_cast<std::int64_t>((r.total + kPageTokens - 1) / kPageTokens);
   std::vector<cudaEvent_t> kv_guards;  // KV pages: written only on the stage stream, in order
@@ -218,7 +223,8 @@ DevRequest& Context::create_kv_request(const lmmsim::RequestSpec& req, cudaStrea
 }
 
 DevRequest& Context::create_request(const lmmsim::RequestSpec& req, const std::int32_t* text_ids,
-                                    std::uint64_t payload_seed, cudaStream_t st) {
+                                    std::uint64_t payload_seed, cudaStream_t st,
+                                    const std::vector<std::pair<int, int>>* grids) {
   if (find(req.id) != nullptr)
     throw lmmsim::RegistryError("duplicate request id " + lmmsim::format_u64(req.id));
   if (slab_ == nullptr) throw DeviceError(RS_ERR_CUDA, "context holds no embedding slab (not stage 0)");
@@ -240,6 +246,17 @@ DevRequest& Context::create_request(const lmmsim::RequestSpec& req, const std::i
     pos += seg.tokens;
   }
   r.patches = patch;
+  if (grids != nullptr) {
+    if (grids->size() != r.items.size())
+      throw lmmsim::InputError("request " + lmmsim::format_u64(req.id) + ": " + std::to_string(grids->size()) +
+                               " item grids for " + std::to_string(r.items.size()) + " items");
+    for (std::size_t i = 0; i < grids->size(); ++i)
+      if (static_cast<std::uint64_t>((*grids)[i].first) * static_cast<std::uint64_t>((*grids)[i].second) !=
+          r.items[i].length())
+        throw lmmsim::InputError("request " + lmmsim::format_u64(req.id) + ": item " + std::to_string(i) +
+                                 " grid does not cover its tokens");
+    r.item_grids = *grids;
+  }
   const std::int64_t pages = static_cast<std::int64_t>((r.total + kPageTokens - 1) / kPageTokens);
   std::vector<cudaEvent_t> guards;
   r.slot_pages = slab_pages_.take(pages, guards);
@@ -334,14 +351,16 @@ std::uint64_t Context::device_schedulable(DevRequest& r, std::uint64_t frontier)
   return *prefix_host_ - frontier;
 }
 
-VitBatchPlan Context::plan_batch(const DevRequest& /*r*/,
+VitBatchPlan Context::plan_batch(const DevRequest& r,
                                  const std::vector<lmmsim::TokenRange>& items) const {
   VitBatchPlan plan;
   plan.cu_window.push_back(0);
   plan.cu_item.push_back(0);
   for (const lmmsim::TokenRange& it : items) {
-    int gh, gw;
-    item_grid(it.length(), &gh, &gw);
+    int gh = 0, gw = 0;
+    for (std::size_t k = 0; k < r.item_grids.size() && k < r.items.size(); ++k)
+      if (r.items[k].start == it.start) std::tie(gh, gw) = r.item_grids[k];
+    if (gh == 0) item_grid(it.length(), &gh, &gw);
     plan_item(gh, gw, s_.win, plan.tokens, plan);
   }
   finalize_plan(plan);

@@ -88,6 +88,7 @@ struct DevRequest {
   int* kv_table = nullptr;             // device page table (kv_pages)
   std::vector<std::array<std::int32_t, 3>> rope;  // M-RoPE ids per token
   std::vector<std::uint64_t> item_patch_offset;   // first patch of each item
+  std::vector<std::pair<int, int>> item_grids;     // merged-token grid of each item
   std::uint64_t patches = 0;
 
   std::int64_t slab_row(std::uint64_t pos) const {
@@ -118,8 +119,11 @@ class Context {
   // ---- device tracker data plane ----
   /// Slot pages, bitmap (text bits set), KV pages + table, M-RoPE ids, and
   /// the K8 text gather (ids from host, or hashed on device when null).
+  /// grids: merged-token grid per MM item (payload files, host/payload.hpp);
+  /// null = the most square factorisation.
   DevRequest& create_request(const lmmsim::RequestSpec& req, const std::int32_t* text_ids,
-                             std::uint64_t payload_seed, cudaStream_t st);
+                             std::uint64_t payload_seed, cudaStream_t st,
+                             const std::vector<std::pair<int, int>>* grids = nullptr);
   /// Downstream pipeline stage: KV pages, page table and M-RoPE ids only
   /// (no embedding slot, no bitmap).
   DevRequest& create_kv_request(const lmmsim::RequestSpec& req, cudaStream_t st);
