@@ -228,7 +228,23 @@ typedef struct rs_run_options {
   int32_t serialize;    /* 1: encoders share the prefill stream (profiling) */
   uint64_t payload_seed;
   const char* payload_text; /* optional payload file (see below); co-located runs */
+  int32_t keep_kv;      /* 1: completed requests keep KV pages + slot for rs_decode */
 } rs_run_options;
+
+/* ---- decode after the first token ------------------------
+ * The reference fixes the output length to 1: TTFT ends the
+ * request. With keep_kv, requests completed by rs_engine_run stay on the
+ * device (paged KV, logits slot); rs_decode then runs `n_steps` greedy
+ * decode steps batched over the given requests — each step embeds the
+ * previous argmax (the first from the prefill logits), runs every layer on
+ * one row per request against its paged KV (appending the new K/V), and the
+ * LM head + argmax. out_tokens [n_steps][n_requests]; out_logits optional
+ * [n_steps][n_requests][vocab]; out_ms = device time of the loop.
+ * rs_decode_release frees a kept request.                                 */
+RS_API rs_status rs_decode(rs_ctx* ctx, const uint64_t* request_ids, int32_t n_requests,
+                           int32_t n_steps, int32_t* out_tokens, float* out_logits,
+                           double* out_ms);
+RS_API rs_status rs_decode_release(rs_ctx* ctx, uint64_t request_id);
 
 /* ---- payload files ---------------------------------------
  * The reference's workload file (workload.hpp:217-265) carries layouts only.

@@ -124,7 +124,7 @@ class rs_ctx_options(C.Structure):
 
 class rs_run_options(C.Structure):
     _fields_ = [("clock", C.c_int32), ("e2e", C.c_int32), ("serialize", C.c_int32),
-                ("payload_seed", C.c_uint64), ("payload_text", C.c_char_p)]
+                ("payload_seed", C.c_uint64), ("payload_text", C.c_char_p), ("keep_kv", C.c_int32)]
 
 
 class rs_run_stats(C.Structure):
@@ -213,6 +213,9 @@ _sig("rs_kernel_launches", [], C.c_ulonglong)
 _sig("rs_profile_enable", [C.c_int])
 _sig("rs_payload_generate", [C.c_char_p, C.c_uint64, PCHAR])
 _sig("rs_payload_validate", [C.c_char_p, C.c_char_p, C.c_int32, PCHAR])
+_sig("rs_decode", [C.c_void_p, C.POINTER(C.c_uint64), C.c_int32, C.c_int32, C.POINTER(C.c_int32),
+                  C.POINTER(C.c_float), C.POINTER(C.c_double)])
+_sig("rs_decode_release", [C.c_void_p, C.c_uint64])
 _sig("rs_profile_drain", [PCHAR])
 
 

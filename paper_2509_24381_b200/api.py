@@ -325,16 +325,37 @@ class Pipeline:
     def synchronize(self):
         N.check(N.lib.rs_synchronize(self.h))
 
+    def decode(self, request_ids: Sequence[int], steps: int, want_logits: bool = False):
+        """Greedy decode after the first token (rserve.h rs_decode) for requests
+        kept by run(keep_kv=True) -> (tokens [steps, n] int32, logits
+        [steps, n, vocab] float32 or None, device ms)."""
+        import numpy as np
+        n = len(request_ids)
+        ids = (C.c_uint64 * n)(*request_ids)
+        toks = np.zeros((steps, n), dtype=np.int32)
+        logits = np.zeros((steps, n, self.model.vocab), dtype=np.float32) if want_logits else None
+        ms = C.c_double()
+        N.check(N.lib.rs_decode(self.h, ids, n, steps, toks.ctypes.data_as(C.POINTER(C.c_int32)),
+                                logits.ctypes.data_as(C.POINTER(C.c_float)) if logits is not None else None,
+                                C.byref(ms)))
+        return toks, logits, ms.value
+
+    def decode_release(self, request_id: int):
+        N.check(N.lib.rs_decode_release(self.h, request_id))
+
     def run(self, workload: str, cfg: SimConfig, clock: str = "lockstep", e2e: bool = False,
-            payload_seed: int = 7, serialize: bool = False, payload: Optional[str] = None):
+            payload_seed: int = 7, serialize: bool = False, payload: Optional[str] = None,
+            keep_kv: bool = False):
         """Engine run on this device -> (decision log, journal, stats dict).
-        `payload`: optional payload file text (grids, pixel seeds, token ids)."""
+        `payload`: optional payload file text (grids, pixel seeds, token ids).
+        `keep_kv`: completed requests stay on the device for decode()."""
         o = N.rs_run_options()
         o.clock = 1 if clock == "real" else 0
         o.e2e = int(e2e)
         o.serialize = int(serialize)
         o.payload_seed = payload_seed
         o.payload_text = payload.encode() if payload is not None else None
+        o.keep_kv = int(keep_kv)
         res, jr = _out(), _out()
         st = N.rs_run_stats()
         c = cfg.to_c()

@@ -281,6 +281,11 @@ rs_status rs_engine_run(rs_ctx* c, const char* workload_text, const rs_sim_confi
       validate_payload(spec, wl, x.ctx->shapes().vocab);
       backend.set_payload(std::move(spec));
     }
+    if (opt != nullptr && opt->keep_kv != 0) {
+      if (!x.ctx->llm() || !x.ctx->llm()->has_head())
+        throw lmmsim::ConfigError("keep_kv: the context holds no LM head");
+      backend.set_keep_kv(true);
+    }
     backend.prepare(wl);
     lmmsim::PipelineEngine engine(wl, sc, backend);
     backend.start();
@@ -293,6 +298,26 @@ rs_status rs_engine_run(rs_ctx* c, const char* workload_text, const rs_sim_confi
     if (out_result) *out_result = c_string(render_decision_log(res, rel, true));
     if (out_journal) *out_journal = c_string(render_journal(engine.journal()));
     if (out_stats) *out_stats = backend.stats();
+  });
+}
+
+rs_status rs_decode(rs_ctx* c, const uint64_t* request_ids, int32_t n_requests, int32_t n_steps,
+                    int32_t* out_tokens, float* out_logits, double* out_ms) {
+  return guarded([&] {
+    rs_ctx& x = need(c);
+    if (n_requests <= 0 || n_steps <= 0 || request_ids == nullptr || out_tokens == nullptr)
+      throw lmmsim::ConfigError("rs_decode: need requests, steps > 0 and an output buffer");
+    std::vector<lmmsim::RequestId> ids(request_ids, request_ids + n_requests);
+    const double ms = x.ctx->decode(ids, n_steps, out_tokens, out_logits, x.ctx->aux_stream());
+    if (out_ms) *out_ms = ms;
+  });
+}
+
+rs_status rs_decode_release(rs_ctx* c, uint64_t request_id) {
+  return guarded([&] {
+    rs_ctx& x = need(c);
+    RS_CUDA_CHECK(cudaDeviceSynchronize());
+    x.ctx->free_kept(request_id);
   });
 }
 

@@ -454,6 +454,10 @@ void DeviceBackend::on_release(std::size_t chunk, lmmsim::RequestId id, lmmsim::
 }
 
 void DeviceBackend::on_request_erased(lmmsim::RequestId id) {
+  if (keep_kv_) {  // prompt slab pages are back (release_prefix); KV stays for decode
+    kept_.push_back(id);
+    return;
+  }
   ctx_.erase_request(id, release_guard_, /*keep_slot=*/true);
 }
 
@@ -564,7 +568,7 @@ void DeviceBackend::collect() {
                       ? static_cast<std::int32_t>(std::max_element(row.begin(), row.end()) - row.begin())
                       : am[static_cast<std::size_t>(slot)];
     logits_[id] = std::move(row);
-    ctx_.free_slot(slot);
+    if (!keep_kv_) ctx_.free_slot(slot);
   }
   done_slots_.clear();
 }

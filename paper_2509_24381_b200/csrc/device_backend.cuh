@@ -47,6 +47,9 @@ class DeviceBackend final : public lmmsim::ExecutionBackend {
 
   /// Payload file overrides (grids, pixel seeds, token ids); before prepare().
   void set_payload(PayloadSpec spec) { payload_ = std::move(spec); }
+  /// Keep completed requests' KV pages and request slots for decode (f3).
+  void set_keep_kv(bool on) { keep_kv_ = on; }
+  const std::vector<lmmsim::RequestId>& kept() const { return kept_; }
   /// Generates pixel payloads of `workload` (device or pinned host). Untimed.
   void prepare(const std::vector<lmmsim::RequestSpec>& workload);
   /// Starts the clock: records the origin event.
@@ -160,6 +163,8 @@ class DeviceBackend final : public lmmsim::ExecutionBackend {
   double remote_last_ms_ = 0;
   double last_poll_ms_ = -1;  // host-side stall diagnostics (rs_run_stats)
   PayloadSpec payload_;
+  bool keep_kv_ = false;
+  std::vector<lmmsim::RequestId> kept_;
   std::unordered_map<lmmsim::RequestId, ResolvedPayload> resolved_;
 };
 

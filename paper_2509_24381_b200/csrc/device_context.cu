@@ -132,6 +132,8 @@ Context::Context(const rs_model_config& model, const rs_ctx_options& opt) : opt_
 
 Context::~Context() {
   cudaDeviceSynchronize();
+  if (decode_x_) cudaFree(decode_x_);
+  if (decode_ids_) cudaFree(decode_ids_);
   reqs_.clear();
   for (cudaEvent_t e : events_) cudaEventDestroy(e);
   if (prefix_host_) cudaFreeHost(prefix_host_);
@@ -426,6 +428,112 @@ void Context::prefill(const std::vector<SliceRef>& slices, bf16* x, cudaStream_t
   }
   llm_->forward_stage(c, slab_, x, page_tables_dev_, st, l_from, l_to);
   up_.fence(st);
+}
+
+double Context::decode(const std::vector<lmmsim::RequestId>& ids, int steps, std::int32_t* out_tokens,
+                       float* out_logits, cudaStream_t st) {
+  if (!llm_ || !llm_->has_head() || llm_->layer_begin() != 0)
+    throw lmmsim::ConfigError("decode needs the whole LLM and its head on this context");
+  const int n = static_cast<int>(ids.size());
+  if (n <= 0 || steps <= 0) return 0.0;
+  if (n > opt_.max_chunk_tokens) throw lmmsim::ConfigError("decode: more requests than max_chunk_tokens");
+  std::vector<DevRequest*> reqs;
+  std::vector<std::int32_t> slots;
+  std::vector<std::int32_t> next_rope;
+  for (lmmsim::RequestId id : ids) {
+    DevRequest& r = get(id);
+    reqs.push_back(&r);
+    slots.push_back(r.slot);
+    std::int32_t mx = -1;
+    for (const auto& p : r.rope) mx = std::max({mx, p[0], p[1], p[2]});
+    next_rope.push_back(mx + 1);  // Qwen2-VL: generated text continues after the prompt's max id
+    // KV pages for every decoded token, appended to the request's page table
+    const std::uint64_t need = (r.total + static_cast<std::uint64_t>(steps) + kPageTokens - 1) / kPageTokens;
+    if (need > r.kv_pages.size()) {
+      std::vector<cudaEvent_t> guards;
+      const std::vector<int> more = kv_pages_.take(static_cast<std::int64_t>(need - r.kv_pages.size()), guards);
+      for (cudaEvent_t g : guards) RS_CUDA_CHECK(cudaStreamWaitEvent(st, g, 0));
+      r.kv_pages.insert(r.kv_pages.end(), more.begin(), more.end());
+      int* table = nullptr;
+      RS_CUDA_CHECK(cudaMallocAsync(reinterpret_cast<void**>(&table), r.kv_pages.size() * 4, st));
+      const void* src = up_.put(r.kv_pages.data(), r.kv_pages.size() * 4, st);
+      RS_CUDA_CHECK(cudaMemcpyAsync(table, src, r.kv_pages.size() * 4, cudaMemcpyDeviceToDevice, st));
+      RS_CUDA_CHECK(cudaFreeAsync(r.kv_table, st));
+      r.kv_table = table;
+      const void* ptr_src = up_.put(&r.kv_table, sizeof(int*), st);
+      RS_CUDA_CHECK(cudaMemcpyAsync(page_tables_dev_ + r.slot, ptr_src, sizeof(int*), cudaMemcpyDeviceToDevice, st));
+      page_tables_host_[static_cast<std::size_t>(r.slot)] = r.kv_table;
+    }
+  }
+  if (decode_x_cap_ < n) {
+    if (decode_x_ != nullptr) RS_CUDA_CHECK(cudaFreeAsync(decode_x_, st));
+    RS_CUDA_CHECK(cudaMallocAsync(reinterpret_cast<void**>(&decode_x_), static_cast<std::size_t>(n) * s_.d * 2, st));
+    RS_CUDA_CHECK(cudaMallocAsync(reinterpret_cast<void**>(&decode_ids_), static_cast<std::size_t>(n) * 4, st));
+    decode_x_cap_ = n;
+  }
+  std::int32_t* tok_dev = nullptr;
+  RS_CUDA_CHECK(cudaMallocAsync(reinterpret_cast<void**>(&tok_dev), static_cast<std::size_t>(steps) * n * 4, st));
+  std::vector<std::int64_t> done_rows(static_cast<std::size_t>(n));
+  for (int i = 0; i < n; ++i) done_rows[static_cast<std::size_t>(i)] = i;
+  const auto* rows_idx = static_cast<const std::int64_t*>(up_.put(done_rows.data(), done_rows.size() * 8, st));
+  const auto* slots_dev = static_cast<const std::int32_t*>(up_.put(slots.data(), slots.size() * 4, st));
+  up_.fence(st);
+  cudaEvent_t e0, e1;
+  RS_CUDA_CHECK(cudaEventCreate(&e0));
+  RS_CUDA_CHECK(cudaEventCreate(&e1));
+  RS_CUDA_CHECK(cudaEventRecord(e0, st));
+  for (int step = 0; step < steps; ++step) {
+    std::vector<ChunkRowInfo> info;
+    std::vector<PrefillWork> work;
+    for (int i = 0; i < n; ++i) {
+      const DevRequest& r = *reqs[static_cast<std::size_t>(i)];
+      const std::int32_t pos = static_cast<std::int32_t>(r.total) + step;
+      const std::int32_t rp = next_rope[static_cast<std::size_t>(i)] + step;
+      info.push_back({r.slot, pos, {rp, rp, rp}, 0});
+      work.push_back({i, 1, pos, r.slot});
+    }
+    ChunkDev c;
+    c.M = n;
+    c.rows = static_cast<const ChunkRowInfo*>(up_.put(info.data(), info.size() * sizeof(ChunkRowInfo), st));
+    c.work = static_cast<const PrefillWork*>(up_.put(work.data(), work.size() * sizeof(PrefillWork), st));
+    c.n_work = n;
+    c.done_rows = rows_idx;
+    c.done_slots = slots_dev;
+    c.n_done = n;
+    // previous token (prefill argmax, then each step's) -> embedding rows
+    gather_slots_i32(llm_->argmax_dev(), slots_dev, n, decode_ids_, st);
+    gather_text_embeddings(llm_->embed(), decode_ids_, n, rows_idx, decode_x_, s_.d, st);
+    llm_->forward_stage(c, nullptr, decode_x_, page_tables_dev_, st);
+    gather_slots_i32(llm_->argmax_dev(), slots_dev, n, tok_dev + static_cast<std::int64_t>(step) * n, st);
+    if (out_logits != nullptr)
+      for (int i = 0; i < n; ++i)
+        RS_CUDA_CHECK(cudaMemcpyAsync(out_logits + (static_cast<std::int64_t>(step) * n + i) * s_.vocab,
+                                      llm_->logits_row(slots[static_cast<std::size_t>(i)]),
+                                      static_cast<std::size_t>(s_.vocab) * 4, cudaMemcpyDeviceToHost, st));
+    up_.fence(st);
+  }
+  RS_CUDA_CHECK(cudaEventRecord(e1, st));
+  RS_CUDA_CHECK(cudaMemcpyAsync(out_tokens, tok_dev, static_cast<std::size_t>(steps) * n * 4,
+                                cudaMemcpyDeviceToHost, st));
+  RS_CUDA_CHECK(cudaFreeAsync(tok_dev, st));
+  RS_CUDA_CHECK(cudaStreamSynchronize(st));
+  float ms = 0;
+  RS_CUDA_CHECK(cudaEventElapsedTime(&ms, e0, e1));
+  RS_CUDA_CHECK(cudaEventDestroy(e0));
+  RS_CUDA_CHECK(cudaEventDestroy(e1));
+  for (DevRequest* r : reqs) r->total += static_cast<std::uint64_t>(steps);  // KV now holds the decoded tokens
+  return ms;
+}
+
+void Context::free_kept(lmmsim::RequestId id) {
+  DevRequest& r = get(id);
+  const int slot = r.slot;
+  r.slot_freed_tokens = r.total;  // slab pages were released with the prompt
+  kv_pages_.give(r.kv_pages, nullptr);
+  if (r.bitmap != nullptr) RS_CUDA_CHECK(cudaFreeAsync(r.bitmap, tracker_));
+  RS_CUDA_CHECK(cudaFreeAsync(r.kv_table, tracker_));
+  reqs_.erase(id);
+  free_slots_.push_back(slot);
 }
 
 std::uint64_t Context::chunk_flops(const std::vector<SliceRef>& slices) const {

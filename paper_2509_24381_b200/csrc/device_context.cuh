@@ -152,6 +152,16 @@ class Context {
   VitBatchPlan plan_batch(const DevRequest& r, const std::vector<lmmsim::TokenRange>& items) const;
   void encode(const VitBatchPlan& plan, const bf16* patches_dev, bf16* out, cudaStream_t st);
   /// One chunk through the local layers. x: [M, d] residual (per chunk).
+  /// Greedy decode after the first token, batched over
+  /// `ids` (requests kept alive after their prefill, rs_run_options.keep_kv):
+  /// each step embeds the previous argmax, runs all layers for one row per
+  /// request against its paged KV (appending the new K/V), LM head + argmax.
+  /// out_tokens [steps][n]; out_logits optional [steps][n][vocab] (host);
+  /// returns the device milliseconds of the decode loop.
+  double decode(const std::vector<lmmsim::RequestId>& ids, int steps, std::int32_t* out_tokens,
+                float* out_logits, cudaStream_t st);
+  /// Frees a request kept for decode (KV pages, tables, request slot).
+  void free_kept(lmmsim::RequestId id);
   void prefill(const std::vector<SliceRef>& slices, bf16* x, cudaStream_t st,
                int layer_from = -1, int layer_to = -1);
   std::uint64_t chunk_flops(const std::vector<SliceRef>& slices) const;
@@ -174,6 +184,9 @@ class Context {
   bf16* slab_ = nullptr;
   PagePool slab_pages_, kv_pages_;
   int** page_tables_dev_ = nullptr;   // [max_requests] -> kv page table
+  bf16* decode_x_ = nullptr;          // decode: [n, d] residual of the step
+  std::int32_t* decode_ids_ = nullptr;
+  int decode_x_cap_ = 0;
   std::vector<int*> page_tables_host_;
   std::vector<int> free_slots_;
   int max_requests_ = 0;

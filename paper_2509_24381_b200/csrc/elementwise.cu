@@ -562,6 +562,19 @@ void fill_uniform_interleaved(bf16* dst, int rows_valid, int rows_pad, int cols,
   count_launch();
 }
 
+__global__ void gather_slots_i32_kernel(const std::int32_t* src, const std::int32_t* idx, int n,
+                                        std::int32_t* out) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) out[i] = src[idx[i]];
+}
+
+void gather_slots_i32(const std::int32_t* src, const std::int32_t* idx, int n, std::int32_t* out,
+                      cudaStream_t st) {
+  if (n <= 0) return;
+  gather_slots_i32_kernel<<<(n + 255) / 256, 256, 0, st>>>(src, idx, n, out);
+  RS_LAUNCH_CHECK();
+  count_launch();
+}
+
 void fold_norm_weight(bf16* W, std::int64_t rows, int cols, int ld, const bf16* g, cudaStream_t st) {
   if (rows <= 0 || cols <= 0) return;
   fold_norm_weight_kernel<<<elem_grid(rows * cols), 256, 0, st>>>(W, rows, cols, ld, g);

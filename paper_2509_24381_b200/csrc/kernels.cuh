@@ -98,6 +98,9 @@ void ready_prefix(const std::uint32_t* bitmap, std::uint64_t frontier, std::uint
 /// K8: slab[dst_rows[i]] <- vocab[ids[i]] for n text tokens.
 void gather_text_embeddings(const bf16* vocab, const std::int32_t* ids, int n,
                             const std::int64_t* dst_rows, bf16* slab, int d, cudaStream_t st);
+/// out[i] = src[idx[i]], i < n (decode: per-request argmax of the logits table).
+void gather_slots_i32(const std::int32_t* src, const std::int32_t* idx, int n, std::int32_t* out,
+                      cudaStream_t st);
 /// Set bits [begin, end) for n ranges (text ranges at creation).
 void bitmap_set_ranges(std::uint32_t* bitmap, const std::uint64_t* ranges, int n_ranges,
                        cudaStream_t st);

@@ -368,7 +368,7 @@ void Llm::forward_stage(const ChunkDev& c, const bf16* slab, bf16* x,
     const LlmLayer& L = layers_[static_cast<std::size_t>(l - lb_)];
     g = GemmArgs{};
     if (l == l_from) {
-      if (l == 0)  // chunk input: gather slot rows (K8 fused into the first norm)
+      if (l == 0 && c.gather_rows != nullptr)  // chunk input: gather slot rows (K8 fused into the first norm)
         rmsnorm(slab, s.d, unit_ln_, xn_, s.d, M, s.d, s.eps, st, c.gather_rows, x, s.d);
       else
         rmsnorm(x, s.d, unit_ln_, xn_, s.d, M, s.d, s.eps, st);

@@ -1,0 +1,73 @@
+"""Decode after the first token on the device, checked
+step by step against the fp32 oracle with teacher forcing: step s feeds the
+token the device chose at step s-1 (the first: the prefill argmax) at prompt
+position T+s, M-RoPE id max(prompt ids)+1+s, and must give the oracle's
+logits of the whole sequence's last row within the first-token tolerance
+(max|dlogit| <= 0.1 std; argmax equal unless a near tie)."""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+LAYOUTS = {0: "T64|M256|M256|T32", 1: "T40|M64|T8"}
+WL = "0,0,-,T64|M256|M256|T32\n1,3.5,-,T40|M64|T8\n"
+STEPS = 5
+
+
+@pytest.fixture(scope="module")
+def tiny():
+    from paper_2509_24381_b200 import api
+    p = api.Pipeline(api.model_preset("tiny"), max_prompt_tokens=8192, slot_tokens=1 << 15,
+                     kv_tokens=1 << 15, max_chunk_tokens=2048, max_encode_tokens=1024)
+    yield p
+    p.close()
+
+
+def _cfg():
+    from paper_2509_24381_b200 import api
+    return api.SimConfig(policy="rserve", stages=1, token_budget=512, embedding_batch_tokens=256,
+                         hidden_size=512, cost=api.CostModel(beta_enc_ms_per_token=0.01,
+                                                             delta_stage_ms_per_token=0.01))
+
+
+def test_decode_matches_teacher_forced_oracle(tiny):
+    from oracle import model_oracle as mo
+    tiny.run(WL, _cfg(), clock="lockstep", payload_seed=7, keep_kv=True)
+    first = {rid: tiny.logits(rid)[1] for rid in LAYOUTS}
+    toks, logits, ms = tiny.decode([0, 1], STEPS, want_logits=True)
+    assert ms > 0 and toks.shape == (STEPS, 2)
+    cfg = mo.ModelConfig.tiny()
+    w = mo.Weights(cfg)
+    llm = mo.LlmOracle(cfg, w)
+    for i, (rid, layout) in enumerate(LAYOUTS.items()):
+        emb = mo.request_embeddings(cfg, w, rid, layout, 7, 256)
+        pos = mo.mrope_positions(mo.parse_layout(layout))
+        nxt = int(pos.max()) + 1
+        fed = [first[rid]] + [int(t) for t in toks[:-1, i]]
+        for s in range(STEPS):
+            seq = np.concatenate([emb, w.embed_rows(np.array(fed[:s + 1]))])
+            p3 = np.concatenate([pos, np.array([[nxt + k] * 3 for k in range(s + 1)])])
+            ref = llm.first_token_logits(llm.forward(seq, p3)[-1])
+            got = logits[s, i]
+            err = np.abs(got - ref).max()
+            assert err <= 0.1 * ref.std(), f"request {rid} step {s}: max|dlogit| {err:.4g}"
+            top = np.sort(ref)[-2:]
+            if top[1] - top[0] > 2 * err:
+                assert int(toks[s, i]) == int(ref.argmax())
+    for rid in LAYOUTS:
+        tiny.decode_release(rid)
+
+
+def test_decode_is_deterministic_and_release_frees(tiny):
+    from paper_2509_24381_b200 import _native as N
+    runs = []
+    for _ in range(2):
+        tiny.run(WL, _cfg(), clock="real", payload_seed=3, keep_kv=True)
+        toks, _, _ = tiny.decode([1, 0], 4)
+        runs.append(toks)
+        for rid in LAYOUTS:
+            tiny.decode_release(rid)
+    np.testing.assert_array_equal(runs[0], runs[1])
+    with pytest.raises(N.RegistryError):
+        tiny.decode([0], 1)
