@@ -228,6 +228,29 @@ def run_ours(args):
         e2e_gpu.append(st["gpu_ms"])
         e2e_gaps.append([round(st["host_max_gap_ms"], 2), round(st["host_last_seen_ms"], 2)])
         h2d, d2h = st["h2d_bytes"], st["d2h_bytes"]
+    # Decode after the first token (the reference stops at TTFT):
+    # the request's KV stays on the device, then greedy decode steps.
+    decode = None
+    if args.decode_steps > 0:
+        pipe.run(wl, sc, clock="real", payload_seed=1234, keep_kv=True)
+        warm, _, _ = pipe.decode([0], 2)
+        pipe.decode_release(0)
+        pipe.run(wl, sc, clock="real", payload_seed=1234, keep_kv=True)
+        toks, _, dms = pipe.decode([0], args.decode_steps)
+        pipe.decode_release(0)
+        hbm_gbs = peaks()[2]
+        llm_bytes = 2.0 * (m["llm_layers"] * (m["llm_dim"] * (m["llm_q_heads"] + 2 * m["llm_kv_heads"]) *
+                                               m["llm_head_dim"] + m["llm_q_heads"] * m["llm_head_dim"] *
+                                               m["llm_dim"] + 3 * m["llm_dim"] * m["llm_ff"]) +
+                           m["vocab"] * m["llm_dim"])
+        decode = {"steps": args.decode_steps, "batch": 1, "ms_per_step": dms / args.decode_steps,
+                  "tokens_per_s": args.decode_steps / (dms / 1e3),
+                  "context_tokens": PROMPT_TOKENS,
+                  "roofline": {"bound": "hbm", "bytes_per_step": llm_bytes,
+                               "bound_ms": llm_bytes / (hbm_gbs * 1e9) * 1e3,
+                               "frac": (llm_bytes / (hbm_gbs * 1e9) * 1e3) / (dms / args.decode_steps)},
+                  "note": "greedy decode of the cfg2 request after its first token (device time, "
+                          "CUDA events); per step every LLM weight is read once (batch 1)"}
     total_ms = sum(dev_ms)
     if ws > 1:
         import torch.distributed as dist
@@ -305,6 +328,7 @@ def run_ours(args):
                                "share": v["ms"] / prof_total_ms if prof_total_ms else None}
                            for k, v in prof.items()},
         "gemm_shapes": gemm_shapes[:16],
+        "decode": decode,
         "prefill_chunk_tokens": chunk_sizes,
         "model_tflop_per_request": {"encode": vit_f / 1e12, "prefill": llm_f / 1e12},
         "clocks": clk.summary(),
@@ -508,6 +532,8 @@ def main():
     ap.add_argument("--budget", type=int, default=2048, help="Algorithm-2 token budget B")
     ap.add_argument("--policy", default="rserve")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--decode-steps", type=int, default=32,
+                    help="greedy decode steps after the first token (0: skip)")
     ap.add_argument("--launch-list", action="store_true",
                     help="run only the warm-up + timed steps (for the ncu launch list); no JSON bench line")
     ap.add_argument("--ep", action="store_true",
