@@ -88,6 +88,37 @@ __device__ __forceinline__ float poly_exp2(float x) {
   const int bits = __float_as_int(p) + (static_cast<int>(n) << 23);
   return x <= -127.f ? 0.f : __int_as_float(bits);
 }
+// Packed fp32x2 arithmetic (sm_100 FFMA2 / FADD2: two lanes per instruction).
+__device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) {
+  unsigned long long r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;"
+      : "=l"(r)
+      : "l"(*reinterpret_cast<unsigned long long*>(&a)), "l"(*reinterpret_cast<unsigned long long*>(&b)),
+        "l"(*reinterpret_cast<unsigned long long*>(&c)));
+  return *reinterpret_cast<float2*>(&r);
+}
+__device__ __forceinline__ float2 add2(float2 a, float2 b) {
+  unsigned long long r;
+  asm("add.rn.f32x2 %0, %1, %2;"
+      : "=l"(r)
+      : "l"(*reinterpret_cast<unsigned long long*>(&a)), "l"(*reinterpret_cast<unsigned long long*>(&b)));
+  return *reinterpret_cast<float2*>(&r);
+}
+// poly_exp2_fma below on a pair, with the FMAs packed.
+__device__ __forceinline__ float2 poly_exp2_fma2(float2 x) {
+  x.x = fmaxf(x.x, -125.5f);
+  x.y = fmaxf(x.y, -125.5f);
+  const float2 magic = make_float2(12582912.f, 12582912.f);
+  const float2 t = add2(x, magic);
+  const float2 n = add2(t, make_float2(-12582912.f, -12582912.f));
+  const float2 f = add2(x, make_float2(-n.x, -n.y));
+  float2 p = fma2(make_float2(0.05517166f, 0.05517166f), f, make_float2(0.24261116f, 0.24261116f));
+  p = fma2(p, f, make_float2(0.69326099f, 0.69326099f));
+  p = fma2(p, f, make_float2(0.99992807f, 0.99992807f));
+  return make_float2(__int_as_float(__float_as_int(p.x) + (__float_as_int(t.x) << 23)),
+                     __int_as_float(__float_as_int(p.y) + (__float_as_int(t.y) << 23)));
+}
+
 // Same on the FMA / ALU pipes only (no FRND / F2I, which share the MUFU
 // (XU) pipe): round(x) by the 1.5 * 2^23 magic add, whose low mantissa bits
 // then hold the integer part for the exponent add; 2^f on [-0.5, 0.5] by a
@@ -746,27 +777,35 @@ __global__ void __launch_bounds__(kPpThreads, 1)
           }
         }
         const float mneg = m == -INFINITY ? 0.f : -m;
-        float rs8[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+        const float2 scale2 = make_float2(p.scale_log2, p.scale_log2), mneg2 = make_float2(mneg, mneg);
+        float2 rs2[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f),
+                         make_float2(0.f, 0.f)};
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
           std::uint32_t packed[16];  // 32 keys as bf16 pairs
 #pragma unroll
           for (int q = 0; q < 16; ++q) {
-            const float x0 = fmaf(__uint_as_float(sv[32 * c + 2 * q]), p.scale_log2, mneg);
-            const float x1 = fmaf(__uint_as_float(sv[32 * c + 2 * q + 1]), p.scale_log2, mneg);
-            const bool poly = (q & 3) == 3;  // every 4th pair on the FMA pipe
-            const float p0 = poly ? poly_exp2_fma(x0) : fast_exp2(x0);
-            const float p1 = poly ? poly_exp2_fma(x1) : fast_exp2(x1);
-            rs8[(2 * q) & 7] += p0;
-            rs8[(2 * q + 1) & 7] += p1;
-            packed[q] = pack_bf16x2(p0, p1);
+            const float2 x = fma2(make_float2(__uint_as_float(sv[32 * c + 2 * q]),
+                                              __uint_as_float(sv[32 * c + 2 * q + 1])),
+                                  scale2, mneg2);
+            float2 e;
+            if ((q & 3) == 3) {  // every 4th pair on the FMA pipe
+              e = poly_exp2_fma2(x);
+            } else {
+              e.x = fast_exp2(x.x);
+              e.y = fast_exp2(x.y);
+            }
+            rs2[q & 3] = add2(rs2[q & 3], e);
+            packed[q] = pack_bf16x2(e.x, e.y);
           }
           sm100::tmem_st_32x32b_x16(s_tm + 16 * c, packed);
         }
         sm100::tmem_st_wait();
         sm100::tc_fence_before();
         sm100::mbar_arrive(&p_full[t]);
-        l = l * alpha + (((rs8[0] + rs8[1]) + (rs8[2] + rs8[3])) + ((rs8[4] + rs8[5]) + (rs8[6] + rs8[7])));
+        const float2 r01 = add2(rs2[0], rs2[1]), r23 = add2(rs2[2], rs2[3]);
+        const float2 rsum = add2(r01, r23);
+        l = l * alpha + (rsum.x + rsum.y);
       }
       sm100::mbar_wait(&o_final[t], on & 1);
       ++on;
