@@ -6,7 +6,9 @@
 // in base-2 with fp32 running max / sum.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
+#include <unordered_map>
 
 #include "attention.cuh"
 #include "common.cuh"
@@ -309,6 +311,232 @@ void attention_varlen_bidir(const bf16* qkv, int ld_qkv, bf16* out, int ld_out,
     case 128: return launch_bidir<128>(qkv, ld_qkv, out, ld_out, cu_seqlens, n_seqs, max_seqlen, heads, scale, stream, rope_table);
     default: throw DeviceError(RS_ERR_CUDA, "attention: unsupported head_dim " + std::to_string(head_dim));
   }
+}
+
+
+// ---- decode attention -----------------------------------------------
+// One query row per request (the token being decoded) against its paged KV:
+// memory-bound (each K / V byte is read once per kv head), so CUDA-core math,
+// GQA-packed (the G = Hq / Hkv query heads of a kv head share every K / V tile
+// in shared memory) and split along the keys (flash-decoding) so a single
+// request still spreads over the SMs; a second kernel merges the splits in
+// split order (deterministic).
+namespace {
+
+constexpr int kDecThreads = 128;
+constexpr int kDecMaxG = 8;
+constexpr int kDecTile = 64;  // keys per tile = one KV page
+
+template <int HD>
+struct DecSmem {
+  float q[kDecMaxG][HD];
+  bf16 k[kDecTile][HD + 8];      // +16 B row pad: conflict-free column reads
+  bf16 vt[HD][kDecTile + 8];     // V^T tile [hd][keys]
+  float p[kDecMaxG][kDecTile];   // scores -> probabilities
+  float alpha[kDecMaxG];
+};
+
+template <int HD>
+__global__ void __launch_bounds__(kDecThreads) decode_attn_split_kernel(
+    const bf16* __restrict__ qkv, int ld_q, const PrefillWork* __restrict__ work,
+    const bf16* __restrict__ k_cache, const bf16* __restrict__ v_cache, const int* const* page_tables,
+    int q_heads, int kv_heads, int tiles_per_split, float scale_log2, float* part_o, float* part_ml,
+    int splits) {
+  __shared__ DecSmem<HD> sm;
+  pdl_wait();
+  pdl_launch_dependents();
+  const int split = blockIdx.x, kvh = blockIdx.y, req = blockIdx.z;
+  const int G = q_heads / kv_heads;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const PrefillWork w = work[req];
+  const int n_keys = w.q_pos0 + 1;  // keys [0, pos] (this token's K/V already appended)
+  const int n_tiles = (n_keys + kDecTile - 1) / kDecTile;
+  const int t0 = split * tiles_per_split, t1 = min(n_tiles, t0 + tiles_per_split);
+  const int* pt = page_tables[w.req_slot];
+  // q rows of the G heads (fp32, pre-scaled into the exp2 domain)
+  const bf16* qrow = qkv + static_cast<std::int64_t>(w.q_row0) * ld_q + kvh * G * HD;
+  for (int i = tid; i < G * HD; i += kDecThreads) sm.q[i / HD][i % HD] = bf2f(qrow[i]) * scale_log2;
+  float m_run = -INFINITY, l_run = 0.f;  // per (g = warp*2 + {0,1}) on lane 0.. (see below)
+  float acc[kDecMaxG];
+#pragma unroll
+  for (int g = 0; g < kDecMaxG; ++g) acc[g] = 0.f;
+  // running max / sum of row g live in warp (g / 2), replicated over its lanes
+  float mrow[2] = {-INFINITY, -INFINITY}, lrow[2] = {0.f, 0.f};
+  (void)m_run;
+  (void)l_run;
+  for (int t = t0; t < t1; ++t) {
+    const std::int64_t page = pt[t];
+    const bf16* kp = k_cache + (page * kv_heads + kvh) * kDecTile * HD;
+    const bf16* vp = v_cache + (page * kv_heads + kvh) * HD * kDecTile;
+    __syncthreads();  // previous tile's k / vt / p consumed
+    for (int i = tid; i < kDecTile * HD / 8; i += kDecThreads) {
+      const int r = i / (HD / 8), c = (i % (HD / 8)) * 8;
+      *reinterpret_cast<uint4*>(&sm.k[r][c]) = *reinterpret_cast<const uint4*>(kp + r * HD + c);
+    }
+    for (int i = tid; i < HD * kDecTile / 8; i += kDecThreads) {
+      const int r = i / (kDecTile / 8), c = (i % (kDecTile / 8)) * 8;
+      *reinterpret_cast<uint4*>(&sm.vt[r][c]) = *reinterpret_cast<const uint4*>(vp + r * kDecTile + c);
+    }
+    __syncthreads();
+    // S[g][key]: thread -> key (tid % 64), heads g = tid / 64 + 2j
+    {
+      const int key = tid & (kDecTile - 1);
+      const int g0 = tid >> 6;
+      float s[kDecMaxG / 2];
+#pragma unroll
+      for (int j = 0; j < kDecMaxG / 2; ++j) s[j] = 0.f;
+#pragma unroll 8
+      for (int d = 0; d < HD; d += 2) {
+        const float2 kk = unpack_bf16x2(*reinterpret_cast<const std::uint32_t*>(&sm.k[key][d]));
+#pragma unroll
+        for (int j = 0; j < kDecMaxG / 2; ++j) {
+          const int g = g0 + 2 * j;
+          if (g < G) s[j] = fmaf(sm.q[g][d], kk.x, fmaf(sm.q[g][d + 1], kk.y, s[j]));
+        }
+      }
+      const bool ok = t * kDecTile + key < n_keys;
+#pragma unroll
+      for (int j = 0; j < kDecMaxG / 2; ++j) {
+        const int g = g0 + 2 * j;
+        if (g < G) sm.p[g][key] = ok ? s[j] : -INFINITY;
+      }
+    }
+    __syncthreads();
+    // online softmax: warp w owns rows 2w, 2w+1 (G <= 8), 2 keys per lane
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int g = 2 * warp + h;
+      if (g >= G) continue;
+      const float a = sm.p[g][lane], b = sm.p[g][lane + 32];
+      float mx = fmaxf(a, b);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+      const float m_new = fmaxf(mrow[h], mx);
+      const float alpha = m_new == -INFINITY ? 1.f : exp2f(mrow[h] - m_new);
+      const float pa = m_new == -INFINITY ? 0.f : exp2f(a - m_new);
+      const float pb = m_new == -INFINITY ? 0.f : exp2f(b - m_new);
+      float rs = pa + pb;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) rs += __shfl_xor_sync(0xffffffffu, rs, o);
+      lrow[h] = lrow[h] * alpha + rs;
+      mrow[h] = m_new;
+      sm.p[g][lane] = pa;
+      sm.p[g][lane + 32] = pb;
+      if (lane == 0) sm.alpha[g] = alpha;
+    }
+    __syncthreads();
+    // O[g][d] += sum_k P[g][k] V[k][d]: thread -> d
+    for (int d = tid; d < HD; d += kDecThreads) {
+      float part[kDecMaxG];
+#pragma unroll
+      for (int g = 0; g < kDecMaxG; ++g) part[g] = 0.f;
+#pragma unroll 4
+      for (int k = 0; k < kDecTile; k += 2) {
+        const float2 vv = unpack_bf16x2(*reinterpret_cast<const std::uint32_t*>(&sm.vt[d][k]));
+#pragma unroll
+        for (int g = 0; g < kDecMaxG; ++g)
+          if (g < G) part[g] = fmaf(sm.p[g][k], vv.x, fmaf(sm.p[g][k + 1], vv.y, part[g]));
+      }
+#pragma unroll
+      for (int g = 0; g < kDecMaxG; ++g)
+        if (g < G) acc[g] = acc[g] * sm.alpha[g] + part[g];
+    }
+  }
+  // partials: o [req][head][split][HD] (unnormalised), ml [req][head][split][2]
+  for (int d = tid; d < HD; d += kDecThreads)
+    for (int g = 0; g < G; ++g) {
+      const int head = kvh * G + g;
+      part_o[((static_cast<std::int64_t>(req) * q_heads + head) * splits + split) * HD + d] = acc[g];
+    }
+  if (lane == 0) {
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int g = 2 * warp + h;
+      if (g >= G) continue;
+      float* ml = part_ml + ((static_cast<std::int64_t>(req) * q_heads + kvh * G + g) * splits + split) * 2;
+      ml[0] = mrow[h];
+      ml[1] = lrow[h];
+    }
+  }
+}
+
+template <int HD>
+__global__ void __launch_bounds__(HD) decode_attn_merge_kernel(const float* part_o, const float* part_ml,
+                                                               int q_heads, int splits, bf16* out,
+                                                               int ld_out, const PrefillWork* work) {
+  pdl_wait();
+  pdl_launch_dependents();
+  const int head = blockIdx.x, req = blockIdx.y, d = threadIdx.x;
+  const std::int64_t base = (static_cast<std::int64_t>(req) * q_heads + head) * splits;
+  float M = -INFINITY;
+  for (int s = 0; s < splits; ++s) M = fmaxf(M, part_ml[(base + s) * 2]);
+  float o = 0.f, l = 0.f;
+  for (int s = 0; s < splits; ++s) {
+    const float m = part_ml[(base + s) * 2];
+    if (m == -INFINITY) continue;
+    const float w = exp2f(m - M);
+    o += w * part_o[(base + s) * HD + d];
+    l += w * part_ml[(base + s) * 2 + 1];
+  }
+  out[static_cast<std::int64_t>(work[req].q_row0) * ld_out + head * HD + d] = f2bf(l > 0.f ? o / l : 0.f);
+}
+
+struct DecodeWs {
+  float* buf = nullptr;
+  std::size_t floats = 0;
+};
+
+}  // namespace
+
+void attention_decode_paged(const bf16* qkv, int ld_q, bf16* out, int ld_out, const PrefillWork* work,
+                            int n_req, int max_keys, const PagedKV& kv, int q_heads, int kv_heads,
+                            int head_dim, float scale, cudaStream_t st) {
+  if (n_req <= 0) return;
+  const int G = q_heads / kv_heads;
+  if (G > kDecMaxG || q_heads % kv_heads != 0)
+    throw DeviceError(RS_ERR_CUDA, "decode attention: GQA group above 8");
+  if (kv.page_size != kDecTile) throw DeviceError(RS_ERR_CUDA, "decode attention needs 64-token pages");
+  const int max_tiles = (max_keys + kDecTile - 1) / kDecTile;
+  // splits: ~2 CTAs per SM over all requests and kv heads
+  const int ctas_wanted = 2 * kNumSMs;
+  int splits = std::max(1, ctas_wanted / std::max(1, n_req * kv_heads));
+  splits = std::min(splits, max_tiles);
+  const int tiles_per_split = (max_tiles + splits - 1) / splits;
+  splits = (max_tiles + tiles_per_split - 1) / tiles_per_split;
+  static thread_local std::unordered_map<cudaStream_t, DecodeWs> ws_by_stream;
+  DecodeWs& ws = ws_by_stream[st];
+  const std::size_t need = static_cast<std::size_t>(n_req) * q_heads * splits * (head_dim + 2);
+  if (ws.floats < need) {
+    if (ws.buf != nullptr) RS_CUDA_CHECK(cudaFreeAsync(ws.buf, st));
+    RS_CUDA_CHECK(cudaMallocAsync(reinterpret_cast<void**>(&ws.buf), need * sizeof(float), st));
+    ws.floats = need;
+  }
+  float* part_o = ws.buf;
+  float* part_ml = ws.buf + static_cast<std::size_t>(n_req) * q_heads * splits * head_dim;
+  const float scale_log2 = scale * kLog2e;
+  const int tok = prof::begin(st);
+  const dim3 grid(splits, kv_heads, n_req);
+  switch (head_dim) {
+    case 64:
+      launch_kernel(decode_attn_split_kernel<64>, grid, dim3(kDecThreads), 0, st, 1, qkv, ld_q, work, kv.k, kv.v,
+                    kv.page_tables, q_heads, kv_heads, tiles_per_split, scale_log2, part_o, part_ml, splits);
+      launch_kernel(decode_attn_merge_kernel<64>, dim3(q_heads, n_req), dim3(64), 0, st, 1,
+                    static_cast<const float*>(part_o), static_cast<const float*>(part_ml), q_heads, splits, out,
+                    ld_out, work);
+      break;
+    case 128:
+      launch_kernel(decode_attn_split_kernel<128>, grid, dim3(kDecThreads), 0, st, 1, qkv, ld_q, work, kv.k, kv.v,
+                    kv.page_tables, q_heads, kv_heads, tiles_per_split, scale_log2, part_o, part_ml, splits);
+      launch_kernel(decode_attn_merge_kernel<128>, dim3(q_heads, n_req), dim3(128), 0, st, 1,
+                    static_cast<const float*>(part_o), static_cast<const float*>(part_ml), q_heads, splits, out,
+                    ld_out, work);
+      break;
+    default:
+      throw DeviceError(RS_ERR_CUDA, "decode attention: unsupported head_dim " + std::to_string(head_dim));
+  }
+  RS_LAUNCH_CHECK();
+  prof::end(tok, st, "attn_decode", 0, 0);
+  count_launch(2);
 }
 
 }  // namespace rserve

@@ -61,6 +61,13 @@ void attention_varlen_tc(const bf16* qp, const bf16* kp, const bf16* vt, int row
                          int n_blocks, const int* cu_seqlens, int n_seqs, float scale,
                          cudaStream_t stream);
 
+/// Decode attention (one query row per work item, q_rows == 1, keys
+/// [0, q_pos0]) over the paged KV: split along the keys, GQA-packed,
+/// deterministic split merge (attention.cu). max_keys >= every item's keys.
+void attention_decode_paged(const bf16* qkv, int ld_q, bf16* out, int ld_out, const PrefillWork* work,
+                            int n_req, int max_keys, const PagedKV& kv, int q_heads, int kv_heads,
+                            int head_dim, float scale, cudaStream_t st);
+
 /// tcgen05 / TMEM flash attention (attention_tc.cu). q: packed QKV rows of
 /// the chunk ([q_rows_alloc, (Hq + 2 Hkv) hd], q columns first).
 void attention_prefill_paged_tc(const bf16* q, int ld_q, int q_rows_alloc, bf16* out, int ld_out,

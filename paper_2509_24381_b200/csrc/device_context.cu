@@ -500,6 +500,12 @@ double Context::decode(const std::vector<lmmsim::RequestId>& ids, int steps, std
     c.done_rows = rows_idx;
     c.done_slots = slots_dev;
     c.n_done = n;
+    static const bool tc_decode = [] {  // RS_DECODE_ATTN=tc: prefill kernel (A/B)
+      const char* e = std::getenv("RS_DECODE_ATTN");
+      return e != nullptr && std::string(e) == "tc";
+    }();
+    c.decode = !tc_decode;
+    for (const PrefillWork& wk : work) c.max_keys = std::max(c.max_keys, wk.q_pos0 + 1);
     // previous token (prefill argmax, then each step's) -> embedding rows
     gather_slots_i32(llm_->argmax_dev(), slots_dev, n, decode_ids_, st);
     gather_text_embeddings(llm_->embed(), decode_ids_, n, rows_idx, decode_x_, s_.d, st);

@@ -383,8 +383,12 @@ void Llm::forward_stage(const ChunkDev& c, const bf16* slab, bf16* x,
     rope_kv_append(qkv_, s.qkv_dim, c.rows, M, s.hq, s.hkv, s.hd, s.cfg.rope_theta_llm, L.k_cache,
                    L.v_cache, page_tables, page_size_, st);
     PagedKV kv{L.k_cache, L.v_cache, page_tables, page_size_};
-    attention_prefill_paged_tc(qkv_, s.qkv_dim, max_m_, att_, s.hq * s.hd, c.work, c.n_work, kv,
-                               kv_pages_, s.hq, s.hkv, s.hd, scale, st);
+    if (c.decode)
+      attention_decode_paged(qkv_, s.qkv_dim, att_, s.hq * s.hd, c.work, c.n_work, c.max_keys, kv, s.hq,
+                             s.hkv, s.hd, scale, st);
+    else
+      attention_prefill_paged_tc(qkv_, s.qkv_dim, max_m_, att_, s.hq * s.hd, c.work, c.n_work, kv,
+                                 kv_pages_, s.hq, s.hkv, s.hd, scale, st);
     g = GemmArgs{};
     g.A = att_; g.lda = s.hq * s.hd; g.B = L.o_w; g.ldb = s.hq * s.hd; g.C = x; g.ldc = s.d;
     g.residual = x; g.ldr = s.d; g.M = M; g.N = s.d; g.K = s.hq * s.hd;

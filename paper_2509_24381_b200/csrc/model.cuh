@@ -133,6 +133,8 @@ struct ChunkDev {
   const std::int64_t* done_rows = nullptr;    // chunk rows that end a prompt
   const std::int32_t* done_slots = nullptr;   // their logits-table slots
   int n_done = 0;
+  bool decode = false;  // one row per work item (decode step): split-KV decode attention
+  int max_keys = 0;     // decode: longest key range
 };
 
 class Llm {

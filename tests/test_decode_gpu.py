@@ -71,3 +71,39 @@ def test_decode_is_deterministic_and_release_frees(tiny):
     np.testing.assert_array_equal(runs[0], runs[1])
     with pytest.raises(N.RegistryError):
         tiny.decode([0], 1)
+
+
+def test_decode_qwen7b_width_shallow():
+    """Decode kernel at the 7B shapes (hd 128, GQA 7:1, vocab 152064) with 2
+    layers, two requests batched, teacher-forced against the fp32 oracle."""
+    from oracle import model_oracle as mo
+    from paper_2509_24381_b200 import api
+    m = api.model_preset("qwen2.5-vl-7b", vit_layers=2, vit_fullatt_every=2, llm_layers=2)
+    p = api.Pipeline(m, max_prompt_tokens=4096, slot_tokens=8192, kv_tokens=8192,
+                     max_chunk_tokens=1024, max_encode_tokens=1024)
+    layouts = {0: "T32|M256|T16", 1: "T100|M64|T3"}
+    wl = "0,0,-,T32|M256|T16\n1,0,-,T100|M64|T3\n"
+    sc = api.SimConfig(policy="rserve", stages=1, token_budget=512, embedding_batch_tokens=256,
+                       hidden_size=3584, cost=api.CostModel(beta_enc_ms_per_token=0.01,
+                                                           delta_stage_ms_per_token=0.01))
+    p.run(wl, sc, payload_seed=5, keep_kv=True)
+    first = {rid: p.logits(rid)[1] for rid in layouts}
+    steps = 3
+    toks, logits, _ = p.decode([0, 1], steps, want_logits=True)
+    cfg = mo.ModelConfig.qwen7b(vit_layers=2, vit_fullatt_every=2, llm_layers=2)
+    w = mo.Weights(cfg)
+    llm = mo.LlmOracle(cfg, w)
+    for i, (rid, layout) in enumerate(layouts.items()):
+        emb = mo.request_embeddings(cfg, w, rid, layout, 5, 256)
+        pos = mo.mrope_positions(mo.parse_layout(layout))
+        nxt = int(pos.max()) + 1
+        fed = [first[rid]] + [int(t) for t in toks[:-1, i]]
+        for s in range(steps):
+            seq = np.concatenate([emb, w.embed_rows(np.array(fed[:s + 1]))])
+            p3 = np.concatenate([pos, np.array([[nxt + k] * 3 for k in range(s + 1)])])
+            ref = llm.first_token_logits(llm.forward(seq, p3)[-1])
+            err = np.abs(logits[s, i] - ref).max()
+            assert err <= 0.1 * ref.std(), f"request {rid} step {s}: max|dlogit| {err:.4g}"
+    for rid in layouts:
+        p.decode_release(rid)
+    p.close()
