@@ -64,4 +64,9 @@ constexpr float kSsFixedScale = 65536.f;  // 2^16
 /// 16-byte aligned rows. Tile width is picked for wave efficiency.
 void gemm(const GemmArgs& args, Epi epi, cudaStream_t stream, int force_bn = 0);
 
+/// Skinny GEMM for M <= 8 rows (decode) on the CUDA cores, same epilogues
+/// (gemv.cu). Returns false when the shape is not supported (caller falls
+/// back to the tcgen05 kernel). gemm() routes here by default.
+bool gemv_small_m(const GemmArgs& args, Epi epi, cudaStream_t stream);
+
 }  // namespace rserve

@@ -334,3 +334,38 @@ def test_attention_varlen_bidir(nat, hd, heads, lens, tc):
         ref[s0:s0 + n] = torch.einsum("hqk,khd->qhd", att.softmax(-1), vs)
         s0 += n
     _close(out, ref.view(total, heads * hd))
+
+
+@pytest.mark.parametrize("M", [1, 3, 8])
+@pytest.mark.parametrize("epi", [0, 1, 2, 3, 4])
+def test_gemv_small_m(nat, M, epi):
+    """M <= 8 rows (decode) take the CUDA-core skinny GEMM with the same fused
+    epilogues; fp32 torch reference."""
+    N, K = (3584, 18944) if epi == 1 else (4608, 3584)
+    torch.manual_seed(M * 10 + epi)
+    A = torch.randn(M, K, device="cuda", dtype=torch.bfloat16)
+    B = torch.randn(N, K, device="cuda", dtype=torch.bfloat16) * (1.0 / K ** 0.5)
+    bias = torch.randn(N, device="cuda", dtype=torch.bfloat16) * 0.1
+    acc = A.float() @ B.float().t() + bias.float()
+    if epi == 2:
+        C = torch.empty(M, N // 2, device="cuda", dtype=torch.bfloat16)
+        g = acc.view(M, N // 32, 2, 16)
+        ref = (torch.nn.functional.silu(g[:, :, 0]) * g[:, :, 1]).reshape(M, N // 2)
+        _gemm(nat, A, B, C, 2, bias=bias)
+    elif epi == 1:
+        C = torch.randn(M, N, device="cuda", dtype=torch.bfloat16)
+        ref = C.float() + acc
+        _gemm(nat, A, B, C, 1, bias=bias, residual=C)
+    elif epi == 4:
+        C = torch.zeros(2 * M + 1, N, device="cuda", dtype=torch.float32)
+        rows = torch.arange(M, device="cuda", dtype=torch.int32) * 2 + 1
+        _gemm(nat, A, B, C, 4, bias=bias, row_map=rows)
+        torch.cuda.synchronize()
+        _close(C[rows.long()], acc, rel=5e-3)
+        return
+    else:
+        C = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+        ref = torch.nn.functional.gelu(acc) if epi == 3 else acc
+        _gemm(nat, A, B, C, epi, bias=bias)
+    torch.cuda.synchronize()
+    _close(C, ref)
