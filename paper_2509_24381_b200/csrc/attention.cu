@@ -61,12 +61,14 @@ struct BidirSource {  // packed QKV rows of one sequence
   __device__ const bf16* k_row(int key) const { return base + static_cast<std::int64_t>(key) * ld; }
   __device__ const bf16* v_row(int key) const { return vbase + static_cast<std::int64_t>(key) * ld; }
 };
-template <int HD>
+// NBUF = 2: K/V tiles double-buffered; 1: single tile (windows of <= 64
+// keys): half the shared memory, so more CTAs are resident per SM.
+template <int HD, int NBUF = 2>
 struct Smem {
   static constexpr int kLd = HD + 8;  // +16 B pad: conflict-free ldmatrix
   bf16 q[kQ][kLd];
-  bf16 k[2][kKV][kLd];
-  bf16 v[2][kKV][kLd];
+  bf16 k[NBUF][kKV][kLd];
+  bf16 v[NBUF][kKV][kLd];
 };
 
 // Rotary (rotate-half pairs (i, i + HD/2), cos / sin from a [rows, HD/2]
@@ -90,9 +92,9 @@ __device__ __forceinline__ void rope_tile_smem(bf16 (*t)[HD + 8], int rows, cons
 // q_ptr), keys [0, src.n_keys). Causal when q_pos0 >= 0: key j visible to
 // query i iff j <= q_pos0 + i. With q_rope / k_rope (tables at query row 0 /
 // key 0) q and k are rotated in shared memory after their loads.
-template <int HD, typename Src>
+template <int HD, int NBUF, typename Src>
 __device__ void flash_block(const bf16* q_ptr, int ld_q, int q_rows, int q_pos0, const Src& src,
-                            bf16* o_ptr, int ld_o, float scale_log2, Smem<HD>& sm,
+                            bf16* o_ptr, int ld_o, float scale_log2, Smem<HD, NBUF>& sm,
                             const float2* q_rope = nullptr, const float2* k_rope = nullptr) {
   constexpr int kDC = HD / 16;  // d chunks (k dim of QK^T)
   constexpr int kNT = HD / 8;   // d n-tiles of O
@@ -132,8 +134,8 @@ __device__ void flash_block(const bf16* q_ptr, int ld_q, int q_rows, int q_pos0,
   const int q_base = warp * 16;
 
   for (int t = 0; t < n_tiles; ++t) {
-    const int buf = t & 1;
-    if (t + 1 < n_tiles) load_kv(t + 1, buf ^ 1);
+    const int buf = NBUF == 2 ? (t & 1) : 0;
+    if (NBUF == 2 && t + 1 < n_tiles) load_kv(t + 1, buf ^ 1);
     cp_async_commit();
     cp_async_wait<1>();
     __syncthreads();
@@ -254,13 +256,13 @@ __device__ void flash_block(const bf16* q_ptr, int ld_q, int q_rows, int q_pos0,
   }
 }
 
-template <int HD>
+template <int HD, int NBUF>
 __global__ void __launch_bounds__(128) varlen_bidir_kernel(const bf16* __restrict__ qkv, int ld,
                                                            bf16* __restrict__ out, int ld_out,
                                                            const int* __restrict__ cu, int heads,
                                                            float scale_log2, const float2* rope) {
   extern __shared__ __align__(16) std::uint8_t smem_raw[];
-  Smem<HD>& sm = *reinterpret_cast<Smem<HD>*>(smem_raw);
+  Smem<HD, NBUF>& sm = *reinterpret_cast<Smem<HD, NBUF>*>(smem_raw);
   pdl_wait();
   pdl_launch_dependents();
   const int seq = blockIdx.y, head = blockIdx.z;
@@ -270,7 +272,7 @@ __global__ void __launch_bounds__(128) varlen_bidir_kernel(const bf16* __restric
   if (q0 >= len) return;
   BidirSource src{qkv + static_cast<std::int64_t>(s0) * ld + (heads + head) * HD,
                   qkv + static_cast<std::int64_t>(s0) * ld + (2 * heads + head) * HD, ld, len};
-  flash_block<HD>(qkv + static_cast<std::int64_t>(s0 + q0) * ld + head * HD, ld, min(kQ, len - q0),
+  flash_block<HD, NBUF>(qkv + static_cast<std::int64_t>(s0 + q0) * ld + head * HD, ld, min(kQ, len - q0),
                   -1, src, out + static_cast<std::int64_t>(s0 + q0) * ld_out + head * HD, ld_out,
                   scale_log2, sm,
                   rope != nullptr ? rope + static_cast<std::int64_t>(s0 + q0) * (HD / 2) : nullptr,
@@ -279,23 +281,32 @@ __global__ void __launch_bounds__(128) varlen_bidir_kernel(const bf16* __restric
 
 constexpr float kLog2e = 1.4426950408889634f;
 
-template <int HD>
-void launch_bidir(const bf16* qkv, int ld, bf16* out, int ld_out, const int* cu, int n_seqs,
-                  int max_seqlen, int heads, float scale, cudaStream_t st, const float2* rope) {
-  const int smem = sizeof(Smem<HD>);
+template <int HD, int NBUF>
+void launch_bidir_n(const bf16* qkv, int ld, bf16* out, int ld_out, const int* cu, int n_seqs,
+                    int max_seqlen, int heads, float scale, cudaStream_t st, const float2* rope) {
+  const int smem = sizeof(Smem<HD, NBUF>);
   static bool set = false;
   if (!set) {
-    RS_CUDA_CHECK(cudaFuncSetAttribute(varlen_bidir_kernel<HD>,
+    RS_CUDA_CHECK(cudaFuncSetAttribute(varlen_bidir_kernel<HD, NBUF>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     set = true;
   }
   dim3 grid(ceil_div(max_seqlen, kQ), n_seqs, heads);
   const int tok = prof::begin(st);
-  launch_kernel(varlen_bidir_kernel<HD>, grid, dim3(128), smem, st, 1, qkv, ld, out, ld_out, cu, heads,
+  launch_kernel(varlen_bidir_kernel<HD, NBUF>, grid, dim3(128), smem, st, 1, qkv, ld, out, ld_out, cu, heads,
                 scale * kLog2e, rope);
   RS_LAUNCH_CHECK();
   prof::end(tok, st, "attn_vit_mma", 0, 0);
   count_launch();
+}
+
+template <int HD>
+void launch_bidir(const bf16* qkv, int ld, bf16* out, int ld_out, const int* cu, int n_seqs,
+                  int max_seqlen, int heads, float scale, cudaStream_t st, const float2* rope) {
+  if (max_seqlen <= kKV)  // one key tile per sequence (ViT windows)
+    launch_bidir_n<HD, 1>(qkv, ld, out, ld_out, cu, n_seqs, max_seqlen, heads, scale, st, rope);
+  else
+    launch_bidir_n<HD, 2>(qkv, ld, out, ld_out, cu, n_seqs, max_seqlen, heads, scale, st, rope);
 }
 
 }  // namespace
