@@ -152,6 +152,23 @@ __device__ __forceinline__ void ws_sum32(const float* const (&parts)[kMaxParts],
   for (int i = 0; i < 32; ++i) v[i] = __float_as_uint(a[i]);
 }
 
+// The first residual chunk of a tile, issued by lane 0 of the epilogue warp
+// before it waits for the accumulator (its latency hides behind the mainloop).
+template <int BN, int EPI>
+__device__ __forceinline__ void prefetch_residual(const CUtensorMap* tmR, std::uint8_t* bufs,
+                                                  std::uint64_t* rbar, std::uint32_t ec, int m0, int n0,
+                                                  int quad, int half, int lane) {
+  constexpr int kChunks = BN / 32;
+  const int c_begin = half == 0 ? 0 : (kChunks + 1) / 2;
+  const int c_end = half == 0 ? (kChunks + 1) / 2 : kChunks;
+  if (lane == 0 && c_begin < c_end) {
+    sm100::bulk_wait_read<0>();  // the previous tile's stores no longer read the buffers
+    const std::uint32_t b = ec & 1;
+    sm100::mbar_expect_tx(&rbar[b], 32 * 64);
+    sm100::tma_load_2d(bufs + b * 2048, tmR, &rbar[b], n0 + c_begin * 32, m0 + quad * 32);
+  }
+}
+
 template <int BN, int EPI, bool FROM_WS = false>
 __device__ __forceinline__ void epilogue_tile_tma(const GemmParams& p, const CUtensorMap* tmC,
                                                   const CUtensorMap* tmR, std::uint8_t* bufs,
@@ -159,7 +176,7 @@ __device__ __forceinline__ void epilogue_tile_tma(const GemmParams& p, const CUt
                                                   std::uint32_t& ec, std::uint32_t t_row, int m0,
                                                   int n0, int quad, int half, int lane,
                                                   const float* const (&parts)[kMaxParts] = {},
-                                                  int n_parts = 0) {
+                                                  int n_parts = 0, bool res_issued = false) {
   const int my_row = m0 + quad * 32 + lane;
   const float rs = row_scale(p, my_row);
   float ss = 0.f;  // sum of squares of this thread's output row segment (ss_out)
@@ -181,7 +198,7 @@ __device__ __forceinline__ void epilogue_tile_tma(const GemmParams& p, const CUt
     sm100::tma_load_2d(bufs + b * kBuf, tmR, &rbar[b], n0 + chunk * 32, row0);
   };
   if constexpr (kRes) {
-    if (lane == 0 && c_begin < c_end) {
+    if (lane == 0 && c_begin < c_end && !res_issued) {
       sm100::bulk_wait_read<0>();
       issue_res(c_begin, ec & 1);
     }
@@ -598,11 +615,16 @@ __global__ void __launch_bounds__(kThreads, 1)
         continue;
       }
       if constexpr (TMA_OUT) {
+        constexpr bool kRes = EPI == static_cast<int>(Epi::Residual);
+        if constexpr (kRes)
+          prefetch_residual<BN, EPI>(&tmR, smem_epi + (warp - 4) * 2 * C::kEpiBuf, rbar + 2 * (warp - 4), ec,
+                                     m0, n0, quad, half, lane);
         sm100::mbar_wait(&tfull[acc], acc_phase);
         sm100::tc_fence_after();
+        const float* const no_parts[kMaxParts] = {};
         epilogue_tile_tma<BN, EPI>(p, &tmC, &tmR, smem_epi + (warp - 4) * 2 * C::kEpiBuf,
                                    rbar + 2 * (warp - 4), rphase, ec, t_row, m0, n0, quad, half,
-                                   lane);
+                                   lane, no_parts, 0, kRes);
       } else {
         sm100::mbar_wait(&tfull[acc], acc_phase);
         sm100::tc_fence_after();
