@@ -539,7 +539,6 @@ __global__ void __launch_bounds__(kPpThreads, 1)
   std::uint32_t* tmem_holder = reinterpret_cast<std::uint32_t*>(o_final + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  pdl_wait();
   pdl_launch_dependents();
 
   if (threadIdx.x == 0) {
@@ -568,6 +567,7 @@ __global__ void __launch_bounds__(kPpThreads, 1)
   __syncthreads();
   sm100::tc_fence_after();
   const std::uint32_t tmem = *tmem_holder;
+  pdl_wait();  // setup overlapped the previous kernel's tail
 
   auto pages = [&](const PpUnit& x, int j, int& pa, int& pb) {
     const int n_real_pages = (x.key_end - x.key_begin + 63) / 64;

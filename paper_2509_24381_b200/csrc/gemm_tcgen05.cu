@@ -422,10 +422,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  pdl_wait();  // inputs of the previous kernel of this stream are visible from here
   pdl_launch_dependents();
-  for (int i = blockIdx.x * kThreads + threadIdx.x; i < p.ss_clear_n; i += gridDim.x * kThreads)
-    p.ss_clear[i] = 0ull;
   // CTA pair: rank 0 (leader) issues the MMAs; both CTAs load and drain.
   const std::uint32_t rank = CG == 2 ? sm100::cluster_ctarank() : 0u;
   const int M = p.M_dev != nullptr ? min(*p.M_dev, p.M) : p.M;
@@ -465,6 +462,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   else __syncthreads();
   sm100::tc_fence_after();
   const std::uint32_t tmem_base = *tmem_holder;
+  // PDL: the setup above (barriers, TMEM, descriptor prefetch) overlapped the
+  // previous kernel's tail; its outputs are visible from here on.
+  pdl_wait();
+  for (int i = blockIdx.x * kThreads + threadIdx.x; i < p.ss_clear_n; i += gridDim.x * kThreads)
+    p.ss_clear[i] = 0ull;
 
   if (warp == 0 && lane == 0) {
     // ---------------- TMA producer ----------------
