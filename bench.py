@@ -198,7 +198,7 @@ def run_ours(args):
             ttfts.append(t)
             dev_ms.append(st["gpu_ms"])
             host_gaps.append([round(st["host_max_gap_ms"], 2), round(st["host_max_call_ms"], 2),
-                              int(st["host_max_call_kind"])])
+                              int(st["host_max_call_kind"]), round(st["host_max_launch_ms"], 2)])
             launches += st["kernel_launches"]
     torch.cuda.synchronize()
     if args.launch_list:

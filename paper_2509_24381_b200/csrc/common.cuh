@@ -5,6 +5,7 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include <chrono>
 #include <cstdint>
 #include <string>
 #include <utility>
@@ -52,6 +53,10 @@ std::string drain();
 // launch latency / prologue overlap the previous tail). Every such kernel
 // calls pdl_wait() before touching global memory. RS_PDL=0 disables.
 bool pdl_enabled();
+/// Longest single kernel-launch API call since the last reset (host stall
+/// diagnostics: a full launch queue blocks the calling thread), in ms.
+void note_launch_ms(double ms);
+double take_max_launch_ms();
 
 /// cudaLaunchKernelEx with the PDL attribute (when enabled) and an optional
 /// cluster dimension.
@@ -79,7 +84,9 @@ inline void launch_kernel(void (*kernel)(KArgs...), dim3 grid, dim3 block, std::
   }
   cfg.attrs = attr;
   cfg.numAttrs = n;
+  const auto t0 = std::chrono::steady_clock::now();
   RS_CUDA_CHECK(cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...));
+  note_launch_ms(std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
 }
 
 __host__ __device__ inline int ceil_div(int a, int b) { return (a + b - 1) / b; }

@@ -186,6 +186,7 @@ void DeviceBackend::start() {
   stats_.host_last_seen_ms = 0;
   stats_.host_max_call_ms = 0;
   stats_.host_max_call_kind = -1;
+  take_max_launch_ms();
   launches0_ = launches_so_far();
   upload0_ = ctx_.uploader().bytes_uploaded();
   RS_CUDA_CHECK(cudaEventRecord(origin_, ctx_.tracker_stream()));
@@ -545,6 +546,7 @@ void DeviceBackend::finish() {
   }
   stats_.gpu_ms = std::max(stats_.gpu_ms, remote_last_ms_);
   stats_.kernel_launches = launches_so_far() - launches0_;
+  stats_.host_max_launch_ms = take_max_launch_ms();
   stats_.h2d_bytes += ctx_.uploader().bytes_uploaded() - upload0_;
 }
 

@@ -15,6 +15,17 @@ std::atomic<std::uint64_t> g_launches{0};
 
 void count_launch(std::uint64_t n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 
+namespace {
+std::atomic<std::uint64_t> g_max_launch_ns{0};
+}
+void note_launch_ms(double ms) {
+  const auto ns = static_cast<std::uint64_t>(ms * 1e6);
+  std::uint64_t cur = g_max_launch_ns.load(std::memory_order_relaxed);
+  while (ns > cur && !g_max_launch_ns.compare_exchange_weak(cur, ns, std::memory_order_relaxed)) {
+  }
+}
+double take_max_launch_ms() { return static_cast<double>(g_max_launch_ns.exchange(0)) * 1e-6; }
+
 bool pdl_enabled() {
   static const bool on = [] {
     const char* e = std::getenv("RS_PDL");
