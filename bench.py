@@ -325,7 +325,10 @@ def run_ours(args):
                                    "timed steps' chunk plan", "gpu_ms": prof_st["gpu_ms"],
                            "kernel_ms_sum": prof_total_ms},
         "kernel_classes": {k: {"launches": v["launches"], "ms_per_step": v["ms"] / prof_steps,
-                               "share": v["ms"] / prof_total_ms if prof_total_ms else None}
+                               "share": v["ms"] / prof_total_ms if prof_total_ms else None,
+                               # achieved rates from the algorithmic work each launch declares
+                               "tflops": v["flops"] / (v["ms"] / 1e3) / 1e12 if v["ms"] and v["flops"] else None,
+                               "gbs": v["bytes"] / (v["ms"] / 1e3) / 1e9 if v["ms"] and v["bytes"] else None}
                            for k, v in prof.items()},
         "gemm_shapes": gemm_shapes[:16],
         "decode": decode,
