@@ -346,7 +346,8 @@ template <int HD>
 __global__ void rope_kv_append_vec_kernel(bf16* qkv, int ld, const ChunkRowInfo* __restrict__ info,
                                           int rows, int q_heads, int kv_heads, float log2_theta,
                                           bf16* k_cache, bf16* v_cache,
-                                          const int* const* page_tables, int page_size) {
+                                          const int* const* page_tables, int page_size,
+                                          const float2* __restrict__ table) {
   constexpr int kHalf = HD / 2, kLph = kHalf / 8, kHpp = 32 / kLph;
   pdl_wait();
   pdl_launch_dependents();
@@ -364,12 +365,24 @@ __global__ void rope_kv_append_vec_kernel(bf16* qkv, int ld, const ChunkRowInfo*
       const int h = (item % passes) * kHpp + hsub;
       const ChunkRowInfo ri = info[row];
       float cs[8], sn[8];
+      if (table != nullptr) {  // per-chunk cos / sin table (mrope_table): shared by every layer
+        const float4* tp = reinterpret_cast<const float4*>(table + static_cast<std::int64_t>(row) * kHalf + i0);
 #pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        const int i = i0 + j;
-        const int sec = i < s_t ? 0 : (i < s_h ? 1 : 2);
-        const float freq = exp2f(-log2_theta * (2.0f * i) / static_cast<float>(HD));
-        sincosf(static_cast<float>(ri.rope[sec]) * freq, &sn[j], &cs[j]);
+        for (int j = 0; j < 4; ++j) {
+          const float4 q = tp[j];
+          cs[2 * j] = q.x;
+          sn[2 * j] = q.y;
+          cs[2 * j + 1] = q.z;
+          sn[2 * j + 1] = q.w;
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const int i = i0 + j;
+          const int sec = i < s_t ? 0 : (i < s_h ? 1 : 2);
+          const float freq = exp2f(-log2_theta * (2.0f * i) / static_cast<float>(HD));
+          sincosf(static_cast<float>(ri.rope[sec]) * freq, &sn[j], &cs[j]);
+        }
       }
       const int* pt = page_tables[ri.req_slot];
       const std::int64_t page = pt[ri.pos / page_size];
@@ -676,7 +689,7 @@ void vit_qk_rope_inplace(bf16* qkv, int ld, const float2* rope_table, int rows, 
 void rope_kv_append(bf16* qkv, int ld, const ChunkRowInfo* rows_info, int rows, int q_heads,
                     int kv_heads, int hd, float theta, bf16* k_cache, bf16* v_cache,
                     const int* const* page_tables, int page_size, cudaStream_t st,
-                    const int* rows_dev) {
+                    const int* rows_dev, const float2* table) {
   if (rows <= 0) return;
   if (rows_dev == nullptr && (hd == 64 || hd == 128)) {
     const int tok = prof::begin(st);
@@ -684,7 +697,7 @@ void rope_kv_append(bf16* qkv, int ld, const ChunkRowInfo* rows_info, int rows, 
     const dim3 grid(row_grid(static_cast<std::int64_t>(rows) * passes), 2);
     launch_kernel(hd == 128 ? rope_kv_append_vec_kernel<128> : rope_kv_append_vec_kernel<64>, grid,
                   dim3(32 * kWarpsPerBlock), 0, st, 1, qkv, ld, rows_info, rows, q_heads, kv_heads,
-                  std::log2(theta), k_cache, v_cache, page_tables, page_size);
+                  std::log2(theta), k_cache, v_cache, page_tables, page_size, table);
     RS_LAUNCH_CHECK();
     // algorithmic bytes: q, k read + written, k and v appended (v read once)
     prof::end(tok, st, "rope_kv_append", 0,
@@ -696,6 +709,30 @@ void rope_kv_append(bf16* qkv, int ld, const ChunkRowInfo* rows_info, int rows, 
                           32 * kWarpsPerBlock, 0, st>>>(qkv, ld, rows_info, rows, q_heads, kv_heads,
                                                         hd, std::log2(theta), k_cache, v_cache,
                                                         page_tables, page_size, rows_dev);
+  RS_LAUNCH_CHECK();
+  count_launch();
+}
+
+__global__ void mrope_table_kernel(const ChunkRowInfo* __restrict__ info, int rows, int hd,
+                                   float log2_theta, float2* table) {
+  pdl_wait();
+  pdl_launch_dependents();
+  const int half = hd / 2, s_t = hd / 8, s_h = hd / 8 + (3 * hd) / 16;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < rows * half; e += gridDim.x * blockDim.x) {
+    const int row = e / half, i = e % half;
+    const int sec = i < s_t ? 0 : (i < s_h ? 1 : 2);
+    const float freq = exp2f(-log2_theta * (2.0f * i) / static_cast<float>(hd));
+    float sn, cs;
+    sincosf(static_cast<float>(info[row].rope[sec]) * freq, &sn, &cs);
+    table[e] = make_float2(cs, sn);
+  }
+}
+
+void mrope_table(const ChunkRowInfo* rows_info, int rows, int hd, float theta, float2* table, cudaStream_t st) {
+  if (rows <= 0) return;
+  const int n = rows * hd / 2;
+  launch_kernel(mrope_table_kernel, dim3(std::min((n + 255) / 256, kNumSMs * 8)), dim3(256), 0, st, 1,
+                rows_info, rows, hd, std::log2(theta), table);
   RS_LAUNCH_CHECK();
   count_launch();
 }

@@ -81,10 +81,15 @@ struct ChunkRowInfo {  // one chunk row (prefill token)
 /// rotated k and v are appended to the paged KV cache of the row's request.
 /// Sections over the hd/2 frequency pairs: t [0, hd/8), h [hd/8, 5hd/16),
 /// w [5hd/16, hd/2) (Qwen2-VL mrope_section [16, 24, 24] at hd = 128).
+/// table (optional): the chunk's [rows, hd/2] (cos, sin) from mrope_table(),
+/// computed once per chunk instead of once per layer.
 void rope_kv_append(bf16* qkv, int ld, const ChunkRowInfo* rows_info, int rows, int q_heads,
                     int kv_heads, int hd, float theta, bf16* k_cache, bf16* v_cache,
                     const int* const* page_tables, int page_size, cudaStream_t st,
-                    const int* rows_dev = nullptr);
+                    const int* rows_dev = nullptr, const float2* table = nullptr);
+/// M-RoPE (cos, sin) of every chunk row and rotary frequency: [rows, hd/2].
+void mrope_table(const ChunkRowInfo* rows_info, int rows, int hd, float theta, float2* table,
+                 cudaStream_t st);
 
 // ---- embedding tracker data plane (K6 / K7 / K8) ----------------------------------
 /// K6: dst rows (slot rows of the slab) <- src rows, d bf16 each; and set

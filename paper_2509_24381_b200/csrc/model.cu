@@ -339,6 +339,7 @@ void Llm::init(const Shapes& s, DeviceArena& a, int lb, int le, bool with_embed,
     xf_ = alloc_bf16(a, static_cast<std::int64_t>(max_chunk) * s.d);
   }
   const std::int64_t M = max_chunk;
+  rope_table_ = static_cast<float2*>(a.alloc(static_cast<std::size_t>(M) * (s.hd / 2) * sizeof(float2)));
   ss_a_ = static_cast<unsigned long long*>(a.alloc(static_cast<std::size_t>(M) * 8));
   ss_b_ = static_cast<unsigned long long*>(a.alloc(static_cast<std::size_t>(M) * 8));
   xn_ = alloc_bf16(a, M * s.d);
@@ -364,6 +365,7 @@ void Llm::forward_stage(const ChunkDev& c, const bf16* slab, bf16* x,
   // qkv_w).
   RS_CUDA_CHECK(cudaMemsetAsync(ss_b_, 0, static_cast<std::size_t>(M) * 8, st));
   const float inv_d = 1.0f / static_cast<float>(s.d);
+  mrope_table(c.rows, M, s.hd, s.cfg.rope_theta_llm, rope_table_, st);  // shared by every layer
   for (int l = l_from; l < l_to; ++l) {
     const LlmLayer& L = layers_[static_cast<std::size_t>(l - lb_)];
     g = GemmArgs{};
@@ -381,7 +383,7 @@ void Llm::forward_stage(const ChunkDev& c, const bf16* slab, bf16* x,
     g.bias = L.qkv_b; g.M = M; g.N = s.qkv_dim; g.K = s.d;
     gemm(g, Epi::Store, st);
     rope_kv_append(qkv_, s.qkv_dim, c.rows, M, s.hq, s.hkv, s.hd, s.cfg.rope_theta_llm, L.k_cache,
-                   L.v_cache, page_tables, page_size_, st);
+                   L.v_cache, page_tables, page_size_, st, nullptr, rope_table_);
     PagedKV kv{L.k_cache, L.v_cache, page_tables, page_size_};
     if (c.decode)
       attention_decode_paged(qkv_, s.qkv_dim, att_, s.hq * s.hd, c.work, c.n_work, c.max_keys, kv, s.hq,

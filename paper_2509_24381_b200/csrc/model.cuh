@@ -163,6 +163,7 @@ class Llm {
   bf16 *final_ln_ = nullptr, *head_ = nullptr;
   bf16 *xn_ = nullptr, *qkv_ = nullptr, *att_ = nullptr, *h_ = nullptr, *xf_ = nullptr;
   bf16* unit_ln_ = nullptr;                  // folded RMSNorm (see Vit)
+  float2* rope_table_ = nullptr;             // [max chunk, hd/2] M-RoPE cos/sin of the chunk
   unsigned long long *ss_a_ = nullptr, *ss_b_ = nullptr;
   float* logits_ = nullptr;
   std::int32_t* argmax_ = nullptr;

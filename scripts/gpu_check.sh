@@ -1,5 +1,6 @@
 cd "${GRAFT_REPO_ROOT:-/root/repo}"
 mkdir -p gpurun_out
-timeout 600 ncu --set full --clock-control none -k regex:"rope_kv_append_vec" -s 40 -c 1 -o gpurun_out/hbm_rope python scripts/one_run.py 1 > gpurun_out/ncu_hbm.log 2>&1; echo "ncu exit $?" >> gpurun_out/ncu_hbm.log
-timeout 600 ncu --set full --clock-control none -k regex:"scatter_rows" -s 2 -c 1 -o gpurun_out/hbm_scatter python scripts/one_run.py 1 >> gpurun_out/ncu_hbm.log 2>&1; echo "ncu exit $?" >> gpurun_out/ncu_hbm.log
-tail -n 3 gpurun_out/ncu_hbm.log
+timeout 1200 python -m pytest tests/test_model_gpu.py tests/test_decode_gpu.py tests/test_ep_gpu.py -x -q -p no:cacheprovider > gpurun_out/pytest_gpu.log 2>&1; echo "pytest exit $?" >> gpurun_out/pytest_gpu.log
+tail -n 3 gpurun_out/pytest_gpu.log
+timeout 900 python bench.py --no-cpu-baseline --steps 5 --decode-steps 16 > gpurun_out/bench.json 2> gpurun_out/bench.err; echo "bench exit $?" >> gpurun_out/bench.err
+tail -n 3 gpurun_out/bench.err
