@@ -226,7 +226,8 @@ def run_ours(args):
         t, st = step(e2e=True)
         e2e_wall.append(st["wall_ms"])
         e2e_gpu.append(st["gpu_ms"])
-        e2e_gaps.append([round(st["host_max_gap_ms"], 2), round(st["host_last_seen_ms"], 2)])
+        e2e_gaps.append([round(st["host_max_gap_ms"], 2), round(st["host_last_seen_ms"], 2),
+                         round(st["host_finish_sync_ms"], 2)])
         h2d, d2h = st["h2d_bytes"], st["d2h_bytes"]
     # Decode after the first token (the reference stops at TTFT):
     # the request's KV stays on the device, then greedy decode steps.

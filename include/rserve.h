@@ -269,6 +269,7 @@ typedef struct rs_run_stats {
   int32_t host_max_call_kind; /* 0 encode, 1 stage, 2 scatter, 3 transfer  */
   int32_t reserved0;
   double host_max_launch_ms; /* longest single kernel-launch API call     */
+  double host_finish_sync_ms; /* final device synchronise of the run       */
 } rs_run_stats;
 RS_API rs_status rs_engine_run(rs_ctx* ctx, const char* workload_text,
                         const rs_sim_config* cfg, const rs_run_options* opt,

@@ -133,7 +133,8 @@ class rs_run_stats(C.Structure):
                 ("encode_gpu_ms", C.c_double), ("prefill_gpu_ms", C.c_double),
                 ("host_max_gap_ms", C.c_double), ("host_last_seen_ms", C.c_double),
                 ("host_max_call_ms", C.c_double), ("host_max_call_kind", C.c_int32),
-                ("reserved0", C.c_int32), ("host_max_launch_ms", C.c_double)]
+                ("reserved0", C.c_int32), ("host_max_launch_ms", C.c_double),
+                ("host_finish_sync_ms", C.c_double)]
 
 
 def _sig(name, argtypes, restype=C.c_int):

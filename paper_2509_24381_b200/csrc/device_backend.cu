@@ -537,8 +537,10 @@ void DeviceBackend::finish() {
     remote_last_ms_ = std::max(remote_last_ms_, static_cast<double>(ms));
   }
   remote_ops_.clear();
+  const double sync0 = clock_ms();
   RS_CUDA_CHECK(cudaDeviceSynchronize());
   stats_.wall_ms = clock_ms();
+  stats_.host_finish_sync_ms = stats_.wall_ms - sync0;
   if (last_event_ != nullptr) {
     float ms = 0;
     RS_CUDA_CHECK(cudaEventElapsedTime(&ms, origin_, last_event_));

@@ -96,6 +96,15 @@ Context::Context(const rs_model_config& model, const rs_ctx_options& opt) : opt_
   if (prop.major != 10)
     throw DeviceError(RS_ERR_CUDA, std::string("device ") + prop.name +
                                        " is not sm_100 (tcgen05 kernels need a B200)");
+  // Stream-ordered allocations (per-request tables, decode buffers) must not
+  // be trimmed back to the OS at every synchronisation (the default release
+  // threshold is 0): keep the pool.
+  {
+    cudaMemPool_t pool;
+    RS_CUDA_CHECK(cudaDeviceGetDefaultMemPool(&pool, opt.device));
+    std::uint64_t keep = ~0ull;
+    RS_CUDA_CHECK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
+  }
   s_ = Shapes::from(model);
   if (opt_.layer_end <= 0 || opt_.layer_end > s_.L) opt_.layer_end = s_.L;
   if (opt_.layer_begin < 0) opt_.layer_begin = 0;
