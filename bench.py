@@ -56,8 +56,9 @@ def peaks():
 class ClockSampler:
     """nvidia-smi clocks / throttle reasons sampled during the timed region."""
 
-    def __init__(self, device):
+    def __init__(self, device, interval_ms=200):
         self.device = device
+        self.interval_ms = interval_ms
         self.samples = []
         self._stop = threading.Event()
         self._t = None
@@ -69,7 +70,7 @@ class ClockSampler:
                  "clocks_event_reasons.sw_power_cap")
             try:
                 p = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={q}",
-                                      "--format=csv,noheader,nounits", "-lms", "200"],
+                                      "--format=csv,noheader,nounits", "-lms", str(self.interval_ms)],
                                      stdout=subprocess.PIPE, text=True)
             except OSError:
                 return
@@ -192,7 +193,7 @@ def run_ours(args):
         torch.distributed.barrier()
     torch.cuda.synchronize()
     ttfts, dev_ms, launches, host_gaps = [], [], 0, []
-    with ClockSampler(local) as clk:
+    with ClockSampler(local, args.clock_sample_ms) as clk:
         for _ in range(args.steps):
             t, st = step()
             ttfts.append(t)
@@ -536,6 +537,8 @@ def main():
     ap.add_argument("--budget", type=int, default=2048, help="Algorithm-2 token budget B")
     ap.add_argument("--policy", default="rserve")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--clock-sample-ms", type=int, default=200,
+                    help="nvidia-smi sampling interval during the timed steps")
     ap.add_argument("--decode-steps", type=int, default=32,
                     help="greedy decode steps after the first token (0: skip)")
     ap.add_argument("--launch-list", action="store_true",
