@@ -3,11 +3,12 @@
 // At batch-1 decode every LLM weight is read once per step, so the step is
 // bound by streaming B from HBM; the tcgen05 kernel's 128-row tiles would
 // leave most of the SMs idle (e.g. 36 tiles for the QKV projection). Here a
-// CTA owns 32 consecutive B rows (one SwiGLU interleave group), each of its 8
-// warps streams 4 rows over the full K with 16-byte loads (A rows come
-// through L1), lanes reduce by shuffles, and the block applies the same
-// fused epilogues as the tcgen05 GEMM (bias, residual + folded-norm sums of
-// squares, SwiGLU, GELU, fp32 row-mapped logits, folded-norm row scale).
+// CTA owns 4 B rows (for SwiGLU: 2 gate rows and their 2 up rows of one
+// 32-row interleave group) and its 8 warps split K, streaming the rows with
+// 16-byte loads (A rows come through L1); warp partials are summed in warp
+// order (deterministic) and the CTA applies the same fused epilogues as the
+// tcgen05 GEMM (bias, residual + folded-norm sums of squares, SwiGLU, GELU,
+// fp32 row-mapped logits, folded-norm row scale).
 #include <cuda_runtime.h>
 
 #include "gemm.cuh"
@@ -15,41 +16,53 @@
 namespace rserve {
 namespace {
 
-constexpr int kRowsPerBlock = 32, kWarps = 8, kRowsPerWarp = 4, kMaxM = 8;
+constexpr int kRows = 4, kWarps = 8, kMaxM = 8;
 
 __device__ __forceinline__ float gelu_erf_v(float x) { return 0.5f * x * (1.f + erff(x * 0.70710678118654752f)); }
 __device__ __forceinline__ float silu_v(float x) { return __fdividef(x, 1.f + __expf(-x)); }
 
+// B row of local row r (0..3) of block b
+template <bool SWIGLU>
+__device__ __forceinline__ int brow_of(int b, int r) {
+  if constexpr (SWIGLU) {
+    const int group = b >> 3, pair = b & 7;  // 8 blocks per 32-row group
+    return group * 32 + (r < 2 ? 2 * pair + r : 16 + 2 * pair + (r - 2));
+  } else {
+    return b * kRows + r;
+  }
+}
+
 template <int MM, int EPI>
 __global__ void __launch_bounds__(kWarps * 32) gemv_kernel(GemmArgs a) {
-  __shared__ float res[kRowsPerBlock][MM];
+  constexpr bool kSwi = EPI == static_cast<int>(Epi::SwiGLU);
+  __shared__ float part[kWarps][kRows][MM];
   pdl_wait();
   pdl_launch_dependents();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int n0 = blockIdx.x * kRowsPerBlock;
-  const int r0 = n0 + warp * kRowsPerWarp;
-  float acc[kRowsPerWarp][MM];
+  const int b = blockIdx.x;
+  float acc[kRows][MM];
 #pragma unroll
-  for (int r = 0; r < kRowsPerWarp; ++r)
+  for (int r = 0; r < kRows; ++r)
 #pragma unroll
     for (int m = 0; m < MM; ++m) acc[r][m] = 0.f;
   const int k8n = a.K / 8;
-  const uint4* brow[kRowsPerWarp];
+  const uint4* brow[kRows];
 #pragma unroll
-  for (int r = 0; r < kRowsPerWarp; ++r)
-    brow[r] = reinterpret_cast<const uint4*>(a.B + static_cast<std::int64_t>(min(r0 + r, a.N - 1)) * a.ldb);
+  for (int r = 0; r < kRows; ++r)
+    brow[r] = reinterpret_cast<const uint4*>(
+        a.B + static_cast<std::int64_t>(min(brow_of<kSwi>(b, r), a.N - 1)) * a.ldb);
 #pragma unroll 2
-  for (int k8 = lane; k8 < k8n; k8 += 32) {
-    uint4 bv[kRowsPerWarp];
+  for (int k8 = warp * 32 + lane; k8 < k8n; k8 += kWarps * 32) {
+    uint4 bv[kRows];
 #pragma unroll
-    for (int r = 0; r < kRowsPerWarp; ++r) bv[r] = __ldcs(brow[r] + k8);  // streamed once
+    for (int r = 0; r < kRows; ++r) bv[r] = __ldcs(brow[r] + k8);  // streamed once
 #pragma unroll
     for (int m = 0; m < MM; ++m) {
       if (m >= a.M) break;
       const uint4 av = __ldg(reinterpret_cast<const uint4*>(a.A + static_cast<std::int64_t>(m) * a.lda) + k8);
       const std::uint32_t aw[4] = {av.x, av.y, av.z, av.w};
 #pragma unroll
-      for (int r = 0; r < kRowsPerWarp; ++r) {
+      for (int r = 0; r < kRows; ++r) {
         const std::uint32_t bw[4] = {bv[r].x, bv[r].y, bv[r].z, bv[r].w};
 #pragma unroll
         for (int t = 0; t < 4; ++t) {
@@ -60,39 +73,46 @@ __global__ void __launch_bounds__(kWarps * 32) gemv_kernel(GemmArgs a) {
     }
   }
 #pragma unroll
-  for (int r = 0; r < kRowsPerWarp; ++r)
+  for (int r = 0; r < kRows; ++r)
 #pragma unroll
     for (int m = 0; m < MM; ++m) {
       float v = acc[r][m];
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-      if (lane == 0) res[warp * kRowsPerWarp + r][m] = v;
+      if (lane == 0) part[warp][r][m] = v;
     }
   __syncthreads();
-  // ---- fused epilogue: thread -> (row m, column c of the block) ----
+  // ---- fused epilogue: thread -> (row m, local column r) ----
   const int tid = threadIdx.x;
-  const int m = tid / kRowsPerBlock, c = tid % kRowsPerBlock;
-  if (m >= a.M || m >= MM) return;
+  if (tid >= kRows * MM) return;
+  const int m = tid / kRows, r = tid % kRows;
+  if (m >= a.M) return;
+  auto dot = [&](int rr) {
+    float s = 0.f;
+#pragma unroll
+    for (int w = 0; w < kWarps; ++w) s += part[w][rr][m];  // warp order: deterministic
+    return s;
+  };
   float rs = 1.f;
   if (a.ss_in != nullptr)
     rs = rsqrtf(static_cast<float>(__ldcg(a.ss_in + m)) * (1.f / kSsFixedScale) * a.ss_inv_dim + a.ss_eps);
   const int out_row = a.row_map != nullptr ? a.row_map[m] : m;
-  if constexpr (EPI == static_cast<int>(Epi::SwiGLU)) {
-    if (c >= 16) return;
-    const int gr = n0 + c, ur = n0 + 16 + c;  // 16-row gate / up interleave
-    float g = rs * res[c][m], u = rs * res[16 + c][m];
+  if constexpr (kSwi) {
+    if (r >= 2) return;
+    const int gr = brow_of<true>(b, r), ur = brow_of<true>(b, r + 2);
+    float g = rs * dot(r), u = rs * dot(r + 2);
     if (a.bias != nullptr) {
       g += __bfloat162float(a.bias[gr]);
       u += __bfloat162float(a.bias[ur]);
     }
-    bf16* C = static_cast<bf16*>(a.C);
-    C[static_cast<std::int64_t>(out_row) * a.ldc + (n0 / 32) * 16 + c] = __float2bfloat16_rn(silu_v(g) * u);
+    const int col = (gr / 32) * 16 + gr % 32;  // output column of gate row gr
+    static_cast<bf16*>(a.C)[static_cast<std::int64_t>(out_row) * a.ldc + col] = __float2bfloat16_rn(silu_v(g) * u);
   } else {
-    const int col = n0 + c;
+    const int col = brow_of<false>(b, r);
     float v = 0.f;
     const bool ok = col < a.N;
     if (ok) {
-      v = rs * res[c][m];
+      v = rs * dot(r);
       if (a.bias != nullptr) v += __bfloat162float(a.bias[col]);
       if constexpr (EPI == static_cast<int>(Epi::Gelu)) v = gelu_erf_v(v);
       if constexpr (EPI == static_cast<int>(Epi::Residual))
@@ -106,12 +126,13 @@ __global__ void __launch_bounds__(kWarps * 32) gemv_kernel(GemmArgs a) {
       }
     }
     if constexpr (EPI == static_cast<int>(Epi::Residual)) {
-      if (a.ss_out != nullptr) {  // sum of squares of this block's 32 output columns of row m
-        float sq = ok ? v * v : 0.f;
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
-        if (c == 0)
-          atomicAdd(a.ss_out + out_row, static_cast<unsigned long long>(__float2ull_rn(sq * kSsFixedScale)));
+      if (a.ss_out != nullptr) {  // the block's 4 columns of row m (lanes 4m..4m+3 of warp 0)
+        const unsigned long long q =
+            ok ? static_cast<unsigned long long>(__float2ull_rn(v * v * kSsFixedScale)) : 0ull;
+        const unsigned mask = __activemask();  // rows m < M: whole 4-lane groups
+        unsigned long long t = q + __shfl_down_sync(mask, q, 1, kRows);
+        t += __shfl_down_sync(mask, t, 2, kRows);
+        if (r == 0) atomicAdd(a.ss_out + out_row, t);  // 2^-16 fixed point: order-free
       }
     }
   }
@@ -125,7 +146,7 @@ __global__ void clear_u64_kernel(unsigned long long* p, int n) {
 
 template <int MM>
 void launch_m(const GemmArgs& a, Epi epi, cudaStream_t st) {
-  const dim3 grid((a.N + kRowsPerBlock - 1) / kRowsPerBlock), block(kWarps * 32);
+  const dim3 grid((a.N + kRows - 1) / kRows), block(kWarps * 32);
   switch (epi) {
     case Epi::Store: return launch_kernel(gemv_kernel<MM, 0>, grid, block, 0, st, 1, a);
     case Epi::Residual: return launch_kernel(gemv_kernel<MM, 1>, grid, block, 0, st, 1, a);
@@ -139,7 +160,7 @@ void launch_m(const GemmArgs& a, Epi epi, cudaStream_t st) {
 
 bool gemv_small_m(const GemmArgs& a, Epi epi, cudaStream_t st) {
   if (a.M > kMaxM || a.M_dev != nullptr || a.K % 8 != 0 || a.lda % 8 != 0 || a.ldb % 8 != 0) return false;
-  if (epi == Epi::SwiGLU && a.N % kRowsPerBlock != 0) return false;
+  if (epi == Epi::SwiGLU && a.N % 32 != 0) return false;
   if (a.ss_clear != nullptr && a.ss_clear_n > 0)
     launch_kernel(clear_u64_kernel, dim3((a.ss_clear_n + 255) / 256), dim3(256), 0, st, 1, a.ss_clear, a.ss_clear_n);
   if (a.M <= 1) launch_m<1>(a, epi, st);
