@@ -1,6 +1,12 @@
 cd "${GRAFT_REPO_ROOT:-/root/repo}"
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests/test_ops_gpu.py tests/test_decode_gpu.py -x -q -p no:cacheprovider -k "gemv or decode" > gpurun_out/pytest_gpu.log 2>&1; echo "pytest exit $?" >> gpurun_out/pytest_gpu.log
-tail -n 3 gpurun_out/pytest_gpu.log
-timeout 900 python bench.py --no-cpu-baseline --steps 3 --decode-steps 32 > gpurun_out/bench.json 2> gpurun_out/bench.err; echo "bench exit $?" >> gpurun_out/bench.err
-tail -n 3 gpurun_out/bench.err
+timeout 300 python -m pytest tests/test_ops_gpu.py -x -q -p no:cacheprovider -k "attention" > gpurun_out/attn_tests.log 2>&1; echo "exit $?" >> gpurun_out/attn_tests.log
+tail -n 3 gpurun_out/attn_tests.log
+timeout 300 python scripts/kernel_bench.py --attn > gpurun_out/kb_attn.json 2>&1
+RS_ATTN_SPLIT=0 timeout 300 python scripts/kernel_bench.py --attn > gpurun_out/kb_attn0.json 2>&1
+python - <<'PY'
+import json
+for f in ("gpurun_out/kb_attn.json","gpurun_out/kb_attn0.json"):
+    d=json.load(open(f))
+    print(f, [round(a.get("tflops", a.get("tflops_tcgen05", 0))) for a in d["attention"]])
+PY
