@@ -158,6 +158,7 @@ typedef struct rs_ctx_options {
   int32_t layer_begin, layer_end; /* LLM layers owned here ([0,L) = all)    */
   int32_t with_vit;            /* allocate the vision encoder here           */
   int32_t with_lm_head;        /* allocate final norm + LM head here         */
+  int32_t tp_size;             /* tensor-parallel LLM shards (0/1 = none); all on `device` (loopback) */
 } rs_ctx_options;
 
 RS_API rs_status rs_ctx_create(const rs_model_config* model, const rs_ctx_options* opt,

@@ -119,7 +119,7 @@ class rs_ctx_options(C.Structure):
                 ("slot_tokens", C.c_uint64), ("kv_tokens", C.c_uint64),
                 ("max_chunk_tokens", C.c_uint64), ("max_encode_tokens", C.c_uint64),
                 ("layer_begin", C.c_int32), ("layer_end", C.c_int32), ("with_vit", C.c_int32),
-                ("with_lm_head", C.c_int32)]
+                ("with_lm_head", C.c_int32), ("tp_size", C.c_int32)]
 
 
 class rs_run_options(C.Structure):

@@ -225,7 +225,7 @@ class Pipeline:
     def __init__(self, model: N.rs_model_config, device: int = 0, max_prompt_tokens: int = 32768,
                  slot_tokens: int = 65536, kv_tokens: int = 65536, max_chunk_tokens: int = 2048,
                  max_encode_tokens: int = 2048, layer_begin: int = 0, layer_end: int = 0,
-                 with_vit: bool = True, with_lm_head: bool = True):
+                 with_vit: bool = True, with_lm_head: bool = True, tp_size: int = 1):
         self.model = model
         o = N.rs_ctx_options()
         o.device = device
@@ -238,6 +238,7 @@ class Pipeline:
         o.layer_end = layer_end
         o.with_vit = int(with_vit)
         o.with_lm_head = int(with_lm_head)
+        o.tp_size = tp_size
         self.opts = o
         h = C.c_void_p()
         N.check(N.lib.rs_ctx_create(C.byref(model), C.byref(o), C.byref(h)))

@@ -120,8 +120,25 @@ Context::Context(const rs_model_config& model, const rs_ctx_options& opt) : opt_
   }
   llm_ = std::make_unique<Llm>();
   const std::int64_t kv_pages = static_cast<std::int64_t>((opt_.kv_tokens + kPageTokens - 1) / kPageTokens);
+  const int tp = opt_.tp_size > 1 ? opt_.tp_size : 1;
+  if (tp > 1 && (opt_.layer_begin != 0 || opt_.layer_end != s_.L))
+    throw lmmsim::ConfigError("tensor parallelism: the context must own every LLM layer");
   llm_->init(s_, arena_, opt_.layer_begin, opt_.layer_end, first_stage, opt_.with_lm_head != 0,
-             static_cast<int>(opt_.max_chunk_tokens), kv_pages, kPageTokens, max_requests_, aux_);
+             static_cast<int>(opt_.max_chunk_tokens), kv_pages, kPageTokens, max_requests_, aux_, 0, tp);
+  if (tp > 1) {
+    const std::int64_t M = static_cast<std::int64_t>(opt_.max_chunk_tokens);
+    for (int r = 1; r < tp; ++r) {
+      tp_shards_.push_back(std::make_unique<Llm>());
+      tp_shards_.back()->init(s_, arena_, opt_.layer_begin, opt_.layer_end, false, false,
+                              static_cast<int>(opt_.max_chunk_tokens), kv_pages, kPageTokens, max_requests_,
+                              aux_, r, tp);
+    }
+    for (int r = 0; r < tp; ++r)
+      tp_parts_.push_back(static_cast<bf16*>(arena_.alloc(static_cast<std::size_t>(M) * s_.d * sizeof(bf16))));
+    tp_parts_dev_ = static_cast<bf16**>(arena_.alloc(sizeof(bf16*) * tp));
+    RS_CUDA_CHECK(cudaMemcpyAsync(tp_parts_dev_, tp_parts_.data(), sizeof(bf16*) * tp, cudaMemcpyHostToDevice, aux_));
+    tp_ss_ = static_cast<unsigned long long*>(arena_.alloc(static_cast<std::size_t>(M) * 8));
+  }
   kv_pages_.reset(kv_pages);
   if (first_stage) {
     const std::int64_t slab_pages =
@@ -435,8 +452,36 @@ void Context::prefill(const std::vector<SliceRef>& slices, bf16* x, cudaStream_t
     c.done_slots = static_cast<const std::int32_t*>(up_.put(done_slots.data(), done_slots.size() * 4, st));
     c.n_done = static_cast<int>(done_rows.size());
   }
-  llm_->forward_stage(c, slab_, x, page_tables_dev_, st, l_from, l_to);
+  run_llm(c, slab_, x, st, l_from, l_to);
   up_.fence(st);
+}
+
+// Tensor-parallel pass over all shards (same device: loopback ranks; the
+// reduction reads every shard's partial through the pointer table, which on
+// an NVSwitch box holds peer addresses): per layer, every shard's attention
+// block -> O partial, reduce into x (shard order, + folded-norm sums of
+// squares), every shard's MLP -> down partial, reduce.
+void Context::run_llm(const ChunkDev& c, const bf16* slab, bf16* x, cudaStream_t st, int l_from, int l_to) {
+  if (tp_shards_.empty()) {
+    llm_->forward_stage(c, slab, x, page_tables_dev_, st, l_from, l_to);
+    return;
+  }
+  if (l_from < 0) l_from = llm_->layer_begin();
+  if (l_to < 0) l_to = llm_->layer_end();
+  std::vector<Llm*> sh{llm_.get()};
+  for (auto& p : tp_shards_) sh.push_back(p.get());
+  const int T = static_cast<int>(sh.size());
+  for (Llm* l : sh) l->tp_begin(c, st);
+  for (int l = l_from; l < l_to; ++l) {
+    for (int t = 0; t < T; ++t)
+      sh[static_cast<std::size_t>(t)]->tp_attn_partial(l, c, slab, x, l == l_from, tp_ss_, page_tables_dev_,
+                                                       tp_parts_[static_cast<std::size_t>(t)], st);
+    tp_reduce_residual(x, c.M, s_.d, tp_parts_dev_, T, tp_ss_, st);
+    for (int t = 0; t < T; ++t)
+      sh[static_cast<std::size_t>(t)]->tp_mlp_partial(l, c, x, tp_ss_, tp_parts_[static_cast<std::size_t>(t)], st);
+    tp_reduce_residual(x, c.M, s_.d, tp_parts_dev_, T, tp_ss_, st);
+  }
+  if (l_to == llm_->layer_end()) llm_->head_phase(c, x, st);
 }
 
 double Context::decode(const std::vector<lmmsim::RequestId>& ids, int steps, std::int32_t* out_tokens,
@@ -518,7 +563,7 @@ double Context::decode(const std::vector<lmmsim::RequestId>& ids, int steps, std
     // previous token (prefill argmax, then each step's) -> embedding rows
     gather_slots_i32(llm_->argmax_dev(), slots_dev, n, decode_ids_, st);
     gather_text_embeddings(llm_->embed(), decode_ids_, n, rows_idx, decode_x_, s_.d, st);
-    llm_->forward_stage(c, nullptr, decode_x_, page_tables_dev_, st);
+    run_llm(c, nullptr, decode_x_, st, -1, -1);
     gather_slots_i32(llm_->argmax_dev(), slots_dev, n, tok_dev + static_cast<std::int64_t>(step) * n, st);
     if (out_logits != nullptr)
       for (int i = 0; i < n; ++i)

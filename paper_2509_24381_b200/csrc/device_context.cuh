@@ -184,6 +184,13 @@ class Context {
   bf16* slab_ = nullptr;
   PagePool slab_pages_, kv_pages_;
   int** page_tables_dev_ = nullptr;   // [max_requests] -> kv page table
+  // tensor parallelism: shards 1..T-1 of the LLM (shard 0 is
+  // llm_), their O / down partials and the reduction's sums of squares
+  std::vector<std::unique_ptr<Llm>> tp_shards_;
+  std::vector<bf16*> tp_parts_;
+  bf16** tp_parts_dev_ = nullptr;
+  unsigned long long* tp_ss_ = nullptr;
+  void run_llm(const ChunkDev& c, const bf16* slab, bf16* x, cudaStream_t st, int l_from, int l_to);
   bf16* decode_x_ = nullptr;          // decode: [n, d] residual of the step
   std::int32_t* decode_ids_ = nullptr;
   int decode_x_cap_ = 0;

@@ -6,6 +6,7 @@
 #include <cmath>
 
 #include "common.cuh"
+#include "gemm.cuh"
 #include "kernels.cuh"
 
 namespace rserve {
@@ -21,7 +22,7 @@ int row_grid(std::int64_t rows) {
 
 __global__ void fill_uniform_kernel(bf16* dst, std::int64_t rows, int cols, int ld,
                                     std::uint64_t seed, std::uint64_t stream, float scale,
-                                    float offset) {
+                                    float offset, std::int64_t row0, int col0, int cols_full) {
   const std::int64_t total = rows * ld;
   for (std::int64_t e = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; e < total;
        e += static_cast<std::int64_t>(gridDim.x) * blockDim.x) {
@@ -29,7 +30,8 @@ __global__ void fill_uniform_kernel(bf16* dst, std::int64_t rows, int cols, int 
     const int c = static_cast<int>(e % ld);
     float v = 0.f;
     if (c < cols) {
-      const std::uint64_t z = mix64(seed, stream, static_cast<std::uint64_t>(r) * cols + c);
+      const std::uint64_t z =
+          mix64(seed, stream, static_cast<std::uint64_t>(row0 + r) * cols_full + (col0 + c));
       const float u = static_cast<float>(z >> 40) * (1.0f / 16777216.0f);
       v = (2.0f * u - 1.0f) * scale + offset;
     }
@@ -39,7 +41,7 @@ __global__ void fill_uniform_kernel(bf16* dst, std::int64_t rows, int cols, int 
 
 __global__ void fill_interleaved_kernel(bf16* dst, int rows_valid, int rows_pad, int cols, int ld,
                                         std::uint64_t seed, std::uint64_t stream, float scale,
-                                        int which) {
+                                        int which, int row0) {
   const std::int64_t total = static_cast<std::int64_t>(rows_pad) * ld;
   for (std::int64_t e = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; e < total;
        e += static_cast<std::int64_t>(gridDim.x) * blockDim.x) {
@@ -47,7 +49,7 @@ __global__ void fill_interleaved_kernel(bf16* dst, int rows_valid, int rows_pad,
     const int c = static_cast<int>(e % ld);
     float v = 0.f;
     if (r < rows_valid && c < cols) {
-      const std::uint64_t z = mix64(seed, stream, static_cast<std::uint64_t>(r) * cols + c);
+      const std::uint64_t z = mix64(seed, stream, static_cast<std::uint64_t>(row0 + r) * cols + c);
       const float u = static_cast<float>(z >> 40) * (1.0f / 16777216.0f);
       v = (2.0f * u - 1.0f) * scale;
     }
@@ -561,16 +563,26 @@ void fill_uniform(bf16* dst, std::int64_t rows, int cols, int ld, std::uint64_t 
                   std::uint64_t stream, float scale, float offset, cudaStream_t st) {
   if (rows <= 0) return;
   fill_uniform_kernel<<<elem_grid(rows * ld), 256, 0, st>>>(dst, rows, cols, ld, seed, stream,
-                                                           scale, offset);
+                                                           scale, offset, 0, 0, cols);
+  RS_LAUNCH_CHECK();
+  count_launch();
+}
+
+void fill_uniform_slice(bf16* dst, std::int64_t rows, int cols, int ld, std::uint64_t seed,
+                        std::uint64_t stream, float scale, std::int64_t row0, int col0, int cols_full,
+                        cudaStream_t st) {
+  if (rows <= 0) return;
+  fill_uniform_kernel<<<elem_grid(rows * ld), 256, 0, st>>>(dst, rows, cols, ld, seed, stream, scale, 0.f,
+                                                           row0, col0, cols_full);
   RS_LAUNCH_CHECK();
   count_launch();
 }
 
 void fill_uniform_interleaved(bf16* dst, int rows_valid, int rows_pad, int cols, int ld,
                               std::uint64_t seed, std::uint64_t stream, float scale, int which,
-                              cudaStream_t st) {
+                              cudaStream_t st, int row0) {
   fill_interleaved_kernel<<<elem_grid(static_cast<std::int64_t>(rows_pad) * ld), 256, 0, st>>>(
-      dst, rows_valid, rows_pad, cols, ld, seed, stream, scale, which);
+      dst, rows_valid, rows_pad, cols, ld, seed, stream, scale, which, row0);
   RS_LAUNCH_CHECK();
   count_launch();
 }
@@ -709,6 +721,60 @@ void rope_kv_append(bf16* qkv, int ld, const ChunkRowInfo* rows_info, int rows, 
                           32 * kWarpsPerBlock, 0, st>>>(qkv, ld, rows_info, rows, q_heads, kv_heads,
                                                         hd, std::log2(theta), k_cache, v_cache,
                                                         page_tables, page_size, rows_dev);
+  RS_LAUNCH_CHECK();
+  count_launch();
+}
+
+__global__ void tp_reduce_kernel(bf16* x, int rows, int d, bf16* const* parts, int n_parts,
+                                 unsigned long long* ss) {
+  pdl_wait();
+  pdl_launch_dependents();
+  // one warp per row, 8 bf16 per lane per step
+  const int lane = threadIdx.x & 31;
+  for (int row = blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5); row < rows; row += gridDim.x * kWarpsPerBlock) {
+    float sq = 0.f;
+    bf16* xr = x + static_cast<std::int64_t>(row) * d;
+    for (int c = lane * 8; c < d; c += 256) {
+      const uint4 xv = *reinterpret_cast<const uint4*>(xr + c);
+      const std::uint32_t xw[4] = {xv.x, xv.y, xv.z, xv.w};
+      float acc[8];
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        const float2 f = unpack_bf16x2(xw[t]);
+        acc[2 * t] = f.x;
+        acc[2 * t + 1] = f.y;
+      }
+      float part[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+      for (int p = 0; p < n_parts; ++p) {
+        const uint4 pv = *reinterpret_cast<const uint4*>(parts[p] + static_cast<std::int64_t>(row) * d + c);
+        const std::uint32_t pw[4] = {pv.x, pv.y, pv.z, pv.w};
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          const float2 f = unpack_bf16x2(pw[t]);
+          part[2 * t] += f.x;
+          part[2 * t + 1] += f.y;
+        }
+      }
+      std::uint32_t o[4];
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        o[t] = pack_bf16x2(acc[2 * t] + part[2 * t], acc[2 * t + 1] + part[2 * t + 1]);
+        const float2 f = unpack_bf16x2(o[t]);
+        sq = fmaf(f.x, f.x, fmaf(f.y, f.y, sq));
+      }
+      *reinterpret_cast<uint4*>(xr + c) = make_uint4(o[0], o[1], o[2], o[3]);
+    }
+    sq = warp_sum(sq);
+    if (lane == 0) ss[row] = static_cast<unsigned long long>(__float2ull_rn(sq * kSsFixedScale));
+  }
+}
+
+void tp_reduce_residual(bf16* x, int rows, int d, bf16* const* parts, int n_parts, unsigned long long* ss,
+                        cudaStream_t st) {
+  if (rows <= 0) return;
+  if (d % 256 != 0) throw DeviceError(RS_ERR_CUDA, "tp reduce: d % 256 != 0");
+  launch_kernel(tp_reduce_kernel, dim3(row_grid(rows)), dim3(32 * kWarpsPerBlock), 0, st, 1, x, rows, d, parts,
+                n_parts, ss);
   RS_LAUNCH_CHECK();
   count_launch();
 }

@@ -33,7 +33,13 @@ void fill_uniform(bf16* dst, std::int64_t rows, int cols, int ld, std::uint64_t 
 /// padding rows are zero. Hash index = r * cols + c, as for fill_uniform.
 void fill_uniform_interleaved(bf16* dst, int rows_valid, int rows_pad, int cols, int ld,
                               std::uint64_t seed, std::uint64_t stream, float scale, int which,
-                              cudaStream_t st);
+                              cudaStream_t st, int row0 = 0);
+/// fill_uniform of the sub-block [row0, row0+rows) x [col0, col0+cols) of a
+/// [*, cols_full] tensor (hash index (row0 + r) * cols_full + col0 + c):
+/// tensor-parallel shards generate exactly their slice of the full weight.
+void fill_uniform_slice(bf16* dst, std::int64_t rows, int cols, int ld, std::uint64_t seed,
+                        std::uint64_t stream, float scale, std::int64_t row0, int col0, int cols_full,
+                        cudaStream_t st);
 void fill_const(bf16* dst, std::int64_t n, float v, cudaStream_t st);
 /// Folds an RMSNorm weight into the consumer linear: W[r, c] *= g[c]
 /// ([rows, cols] with row stride ld), so the GEMM may read the
@@ -87,6 +93,12 @@ void rope_kv_append(bf16* qkv, int ld, const ChunkRowInfo* rows_info, int rows, 
                     int kv_heads, int hd, float theta, bf16* k_cache, bf16* v_cache,
                     const int* const* page_tables, int page_size, cudaStream_t st,
                     const int* rows_dev = nullptr, const float2* table = nullptr);
+/// Tensor-parallel reduction of the residual stream: x[m] += sum_t parts[t][m]
+/// (fp32, in shard order: identical on every shard), and ss[m] += sum of
+/// squares of the new bf16 row (2^-16 fixed point) for the folded norm.
+/// parts: device array of `n_parts` pointers to [rows, d] bf16.
+void tp_reduce_residual(bf16* x, int rows, int d, bf16* const* parts, int n_parts, unsigned long long* ss,
+                        cudaStream_t st);
 /// M-RoPE (cos, sin) of every chunk row and rotary frequency: [rows, hd/2].
 void mrope_table(const ChunkRowInfo* rows_info, int rows, int hd, float theta, float2* table,
                  cudaStream_t st);

@@ -292,9 +292,20 @@ std::uint64_t Vit::flops_per_batch(const VitBatchPlan& plan) const {
 }
 
 // ---- LLM --------------------------------------------------------------------------
-void Llm::init(const Shapes& s, DeviceArena& a, int lb, int le, bool with_embed, bool with_head,
+void Llm::init(const Shapes& sg, DeviceArena& a, int lb, int le, bool with_embed, bool with_head,
                int max_chunk, std::int64_t kv_pages, int page_size, int logits_slots,
-               cudaStream_t st) {
+               cudaStream_t st, int tp_rank, int tp_size) {
+  // local (shard) shapes; sg = the full model the weights are sliced from
+  Shapes s = sg;
+  if (tp_size > 1) {
+    if (sg.hq % tp_size != 0 || sg.hkv % tp_size != 0 || sg.ff % (16 * tp_size) != 0)
+      throw lmmsim::ConfigError("tensor parallelism: " + std::to_string(tp_size) +
+                                " does not divide the heads / SwiGLU width");
+    s.hq = sg.hq / tp_size;
+    s.hkv = sg.hkv / tp_size;
+    s.ff = sg.ff / tp_size;
+    s.qkv_dim = (s.hq + 2 * s.hkv) * s.hd;
+  }
   s_ = s;
   lb_ = lb;
   le_ = le;
@@ -312,12 +323,45 @@ void Llm::init(const Shapes& s, DeviceArena& a, int lb, int le, bool with_embed,
     const std::uint64_t lid = static_cast<std::uint64_t>(l);
     L.ln1 = make_ones(a, s.d, st);
     L.ln2 = make_ones(a, s.d, st);
-    L.qkv_w = make_linear(a, s.qkv_dim, s.d, s.d, seed, id(kLlm, lid, kQkvW), st);
-    L.qkv_b = make_linear(a, 1, s.qkv_dim, s.qkv_dim, seed, id(kLlm, lid, kQkvB), st);
-    L.o_w = make_linear(a, s.d, s.hq * s.hd, s.hq * s.hd, seed, id(kLlm, lid, kOW), st);
-    L.gu_w = make_gate_up(a, s.ff, s.ff, s.d, s.d, seed, id(kLlm, lid, kGateW),
-                          id(kLlm, lid, kUpW), st);
-    L.down_w = make_linear(a, s.d, s.ff, s.ff, seed, id(kLlm, lid, kDownW), st);
+    if (tp_size == 1) {
+      L.qkv_w = make_linear(a, s.qkv_dim, s.d, s.d, seed, id(kLlm, lid, kQkvW), st);
+      L.qkv_b = make_linear(a, 1, s.qkv_dim, s.qkv_dim, seed, id(kLlm, lid, kQkvB), st);
+      L.o_w = make_linear(a, s.d, s.hq * s.hd, s.hq * s.hd, seed, id(kLlm, lid, kOW), st);
+      L.gu_w = make_gate_up(a, s.ff, s.ff, s.d, s.d, seed, id(kLlm, lid, kGateW),
+                            id(kLlm, lid, kUpW), st);
+      L.down_w = make_linear(a, s.d, s.ff, s.ff, seed, id(kLlm, lid, kDownW), st);
+    } else {
+      // this shard's slices: q / k / v head rows, O and down input columns, gate / up rows
+      const int hd = s.hd;
+      const std::int64_t q0 = static_cast<std::int64_t>(tp_rank) * s.hq * hd;
+      const std::int64_t k0 = static_cast<std::int64_t>(sg.hq) * hd + static_cast<std::int64_t>(tp_rank) * s.hkv * hd;
+      const std::int64_t v0 = static_cast<std::int64_t>(sg.hq + sg.hkv) * hd +
+                              static_cast<std::int64_t>(tp_rank) * s.hkv * hd;
+      const std::int64_t nq = static_cast<std::int64_t>(s.hq) * hd, nk = static_cast<std::int64_t>(s.hkv) * hd;
+      L.qkv_w = alloc_bf16(a, static_cast<std::int64_t>(s.qkv_dim) * s.d);
+      L.qkv_b = alloc_bf16(a, s.qkv_dim);
+      const std::uint64_t wq = id(kLlm, lid, kQkvW), bq = id(kLlm, lid, kQkvB);
+      fill_uniform_slice(L.qkv_w, nq, s.d, s.d, seed, wq, kWeightScale, q0, 0, s.d, st);
+      fill_uniform_slice(L.qkv_w + nq * s.d, nk, s.d, s.d, seed, wq, kWeightScale, k0, 0, s.d, st);
+      fill_uniform_slice(L.qkv_w + (nq + nk) * s.d, nk, s.d, s.d, seed, wq, kWeightScale, v0, 0, s.d, st);
+      fill_uniform_slice(L.qkv_b, 1, static_cast<int>(nq), static_cast<int>(nq), seed, bq, kWeightScale, 0,
+                         static_cast<int>(q0), sg.qkv_dim, st);
+      fill_uniform_slice(L.qkv_b + nq, 1, static_cast<int>(nk), static_cast<int>(nk), seed, bq, kWeightScale, 0,
+                         static_cast<int>(k0), sg.qkv_dim, st);
+      fill_uniform_slice(L.qkv_b + nq + nk, 1, static_cast<int>(nk), static_cast<int>(nk), seed, bq,
+                         kWeightScale, 0, static_cast<int>(v0), sg.qkv_dim, st);
+      L.o_w = alloc_bf16(a, static_cast<std::int64_t>(s.d) * nq);
+      fill_uniform_slice(L.o_w, s.d, static_cast<int>(nq), static_cast<int>(nq), seed, id(kLlm, lid, kOW),
+                         kWeightScale, 0, static_cast<int>(q0), sg.hq * hd, st);
+      L.gu_w = alloc_bf16(a, 2LL * s.ff * s.d);
+      fill_uniform_interleaved(L.gu_w, s.ff, s.ff, s.d, s.d, seed, id(kLlm, lid, kGateW), kWeightScale, 0, st,
+                               tp_rank * s.ff);
+      fill_uniform_interleaved(L.gu_w, s.ff, s.ff, s.d, s.d, seed, id(kLlm, lid, kUpW), kWeightScale, 1, st,
+                               tp_rank * s.ff);
+      L.down_w = alloc_bf16(a, static_cast<std::int64_t>(s.d) * s.ff);
+      fill_uniform_slice(L.down_w, s.d, s.ff, s.ff, seed, id(kLlm, lid, kDownW), kWeightScale, 0, tp_rank * s.ff,
+                         sg.ff, st);
+    }
     L.k_cache = alloc_bf16(a, kv_elems);
     L.v_cache = alloc_bf16(a, kv_elems);
     // Zero-init: masked keys of a partial page must be finite (P = 0 x V).
@@ -415,6 +459,74 @@ void Llm::forward_stage(const ChunkDev& c, const bf16* slab, bf16* x,
     gemm(g, Epi::StoreF32, st);
     argmax_rows(logits_, c.n_done, s.vocab, argmax_, st, c.done_slots);
   }
+}
+
+// ---- tensor-parallel phases (tp_forward, device_context.cu) --------------------------
+void Llm::tp_attn_partial(int l, const ChunkDev& c, const bf16* slab, bf16* x, bool first,
+                          const unsigned long long* ss, const int* const* page_tables, bf16* part,
+                          cudaStream_t st) {
+  const Shapes& s = s_;
+  const LlmLayer& L = layers_[static_cast<std::size_t>(l - lb_)];
+  const int M = c.M;
+  const float scale = 1.0f / std::sqrt(static_cast<float>(s.hd));
+  GemmArgs g;
+  if (first) {
+    if (l == 0 && c.gather_rows != nullptr)  // chunk input gathered from the slab into x (K8)
+      rmsnorm(slab, s.d, unit_ln_, xn_, s.d, M, s.d, s.eps, st, c.gather_rows, x, s.d);
+    else
+      rmsnorm(x, s.d, unit_ln_, xn_, s.d, M, s.d, s.eps, st);
+    g.A = xn_;
+  } else {
+    g.A = x;
+    g.ss_in = ss; g.ss_inv_dim = 1.0f / static_cast<float>(s.d); g.ss_eps = s.eps;
+  }
+  g.lda = s.d; g.B = L.qkv_w; g.ldb = s.d; g.C = qkv_; g.ldc = s.qkv_dim;
+  g.bias = L.qkv_b; g.M = M; g.N = s.qkv_dim; g.K = s.d;
+  gemm(g, Epi::Store, st);
+  rope_kv_append(qkv_, s.qkv_dim, c.rows, M, s.hq, s.hkv, s.hd, s.cfg.rope_theta_llm, L.k_cache,
+                 L.v_cache, page_tables, page_size_, st, nullptr, rope_table_);
+  PagedKV kv{L.k_cache, L.v_cache, page_tables, page_size_};
+  if (c.decode)
+    attention_decode_paged(qkv_, s.qkv_dim, att_, s.hq * s.hd, c.work, c.n_work, c.max_keys, kv, s.hq,
+                           s.hkv, s.hd, scale, st);
+  else
+    attention_prefill_paged_tc(qkv_, s.qkv_dim, max_m_, att_, s.hq * s.hd, c.work, c.n_work, kv,
+                               kv_pages_, s.hq, s.hkv, s.hd, scale, st);
+  g = GemmArgs{};
+  g.A = att_; g.lda = s.hq * s.hd; g.B = L.o_w; g.ldb = s.hq * s.hd; g.C = part; g.ldc = s.d;
+  g.M = M; g.N = s.d; g.K = s.hq * s.hd;
+  gemm(g, Epi::Store, st);
+}
+
+void Llm::tp_mlp_partial(int l, const ChunkDev& c, const bf16* x, const unsigned long long* ss, bf16* part,
+                         cudaStream_t st) {
+  const Shapes& s = s_;
+  const LlmLayer& L = layers_[static_cast<std::size_t>(l - lb_)];
+  const int M = c.M;
+  GemmArgs g;
+  g.A = x; g.lda = s.d; g.B = L.gu_w; g.ldb = s.d; g.C = h_; g.ldc = s.ff;
+  g.M = M; g.N = 2 * s.ff; g.K = s.d;
+  g.ss_in = ss; g.ss_inv_dim = 1.0f / static_cast<float>(s.d); g.ss_eps = s.eps;
+  gemm(g, Epi::SwiGLU, st);
+  g = GemmArgs{};
+  g.A = h_; g.lda = s.ff; g.B = L.down_w; g.ldb = s.ff; g.C = part; g.ldc = s.d;
+  g.M = M; g.N = s.d; g.K = s.ff;
+  gemm(g, Epi::Store, st);
+}
+
+void Llm::tp_begin(const ChunkDev& c, cudaStream_t st) {
+  mrope_table(c.rows, c.M, s_.hd, s_.cfg.rope_theta_llm, rope_table_, st);
+}
+
+void Llm::head_phase(const ChunkDev& c, const bf16* x, cudaStream_t st) {
+  if (head_ == nullptr || c.n_done <= 0) return;
+  const Shapes& s = s_;
+  rmsnorm(x, s.d, final_ln_, xf_, s.d, c.n_done, s.d, s.eps, st, c.done_rows);
+  GemmArgs g;
+  g.A = xf_; g.lda = s.d; g.B = head_; g.ldb = s.d; g.C = logits_; g.ldc = s.vocab;
+  g.row_map = c.done_slots; g.M = c.n_done; g.N = s.vocab; g.K = s.d;
+  gemm(g, Epi::StoreF32, st);
+  argmax_rows(logits_, c.n_done, s.vocab, argmax_, st, c.done_slots);
 }
 
 std::uint64_t Llm::dense_flops(std::uint64_t tokens) const {

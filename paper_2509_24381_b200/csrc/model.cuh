@@ -139,9 +139,27 @@ struct ChunkDev {
 
 class Llm {
  public:
+  /// tp_size > 1: this object is tensor-parallel shard tp_rank (SURVEY §8
+  /// f4): q / kv heads and the SwiGLU width split T ways, O / down by input
+  /// columns; weights are the exact slices of the full (hashed) tensors.
   void init(const Shapes& s, DeviceArena& arena, int layer_begin, int layer_end, bool with_embed,
             bool with_head, int max_chunk, std::int64_t kv_pages, int page_size,
-            int logits_slots, cudaStream_t st);
+            int logits_slots, cudaStream_t st, int tp_rank = 0, int tp_size = 1);
+  /// Tensor-parallel layer phases (tp_forward in device_context.cu drives all
+  /// shards): attention block -> this shard's O-projection partial [M, d];
+  /// MLP block -> this shard's down-projection partial. The residual stream x
+  /// is read (never written) and normalised on the fly from ss (the previous
+  /// reduction's sums of squares) or explicitly on the stage's first layer.
+  void tp_attn_partial(int layer, const ChunkDev& c, const bf16* slab, bf16* x, bool first,
+                       const unsigned long long* ss, const int* const* page_tables, bf16* part,
+                       cudaStream_t st);
+  void tp_mlp_partial(int layer, const ChunkDev& c, const bf16* x, const unsigned long long* ss,
+                      bf16* part, cudaStream_t st);
+  /// Per-chunk setup of a tensor-parallel pass (the M-RoPE table).
+  void tp_begin(const ChunkDev& c, cudaStream_t st);
+  /// Final norm + LM head + argmax for the rows of c that end a prompt.
+  void head_phase(const ChunkDev& c, const bf16* x, cudaStream_t st);
+  const Shapes& shapes() const { return s_; }
   /// One micro-batch through layers [begin, end). x: [M, d] residual stream
   /// (in/out). First stage: x is gathered from the embedding slab.
   void forward_stage(const ChunkDev& c, const bf16* slab, bf16* x, const int* const* page_tables,
