@@ -145,6 +145,18 @@ def group_profile(raw):
     return out, shapes
 
 
+def bench_config(args, ws):
+    """The workload every arm reports (cfg2 of BASELINE.json at N=1)."""
+    return {"workload": "cfg2: Qwen2.5-VL-7B-shaped (random init), 1 request "
+                        "T128|(M1024|T32)x8 = 8576 tokens, 8 images of 896x896",
+            "model": "qwen2.5-vl-7b-shaped", "global_batch": 1, "seq_len": PROMPT_TOKENS,
+            "policy": args.policy, "C": C_TOKENS, "B": args.budget, "stages": 1,
+            "placement": "encoder+prefill co-located, 2 streams" if ws == 1 else
+                         f"{ws} independent co-located replicas",
+            "parallelism": "replicas" if ws > 1 else "single",
+            "l2": "inputs (16 GB weights) >> 126 MB L2; no flush"}
+
+
 def run_ours(args):
     import torch
     ws, rank, local = dist_env()
@@ -289,14 +301,7 @@ def run_ours(args):
                     "roofline_bound_ms_burst_peak": bound_ms,
                     "roofline_note": "bound = model FLOPs / measured sustained bf16 peak (the step "
                                      "runs ~190 ms under the 1 kW power cap); burst-peak bound beside"},
-        "config": {"workload": "cfg2: Qwen2.5-VL-7B-shaped (random init), 1 request "
-                               "T128|(M1024|T32)x8 = 8576 tokens, 8 images of 896x896",
-                   "model": "qwen2.5-vl-7b-shaped", "global_batch": 1, "seq_len": PROMPT_TOKENS,
-                   "policy": args.policy, "C": C_TOKENS, "B": args.budget, "stages": 1,
-                   "placement": "encoder+prefill co-located, 2 streams" if ws == 1 else
-                                f"{ws} independent co-located replicas",
-                   "parallelism": "replicas" if ws > 1 else "single",
-                   "l2": "inputs (16 GB weights) >> 126 MB L2; no flush"},
+        "config": bench_config(args, ws),
         "e2e": {"value": e2e_value, "unit": "tokens/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "p50_ms": statistics.median(e2e_wall),
                 "wall_ms_per_step": [round(x, 2) for x in e2e_wall],
@@ -516,9 +521,7 @@ def run_reference(args):
         "ms_per_step": 1e3 * wall / args.steps, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "ttft_ms": {"p50": 1e3 * per_req[len(per_req) // 2], "p99": 1e3 * per_req[-1]},
-        "config": {"workload": "cfg2 (extrapolated CPU sample)", "model": "qwen2.5-vl-7b-shaped",
-                   "global_batch": 1, "seq_len": PROMPT_TOKENS, "policy": "rserve", "C": C_TOKENS,
-                   "B": args.budget},
+        "config": dict(bench_config(args, ws), sample="extrapolated CPU sample (see cpu_baseline)"),
         "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": os.cpu_count(), "kind": "port",
                          "sample": "per step: numpy fp32 oracle, 1 ViT layer (4096 patches) + 1 LLM "
                                    "layer (B-token chunk), extrapolated by FLOPs to the cfg2 request; "

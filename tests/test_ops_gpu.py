@@ -77,10 +77,17 @@ SK_SHAPES = [(2048, 3584, 18944, 224), (1024, 5120, 5120, 160), (1024, 5120, 512
 
 
 @pytest.fixture(scope="module", autouse=True)
-def _pair_split(request):
-    # exercise the CTA-pair split-tail path too (off by default in the heuristic)
+def _pair_split():
+    # exercise the CTA-pair split-tail path too (off by default in the heuristic);
+    # restored afterwards so later modules see the product default
     import os
+    old = os.environ.get("RS_GEMM_PAIR_SPLIT")
     os.environ["RS_GEMM_PAIR_SPLIT"] = "1"
+    yield
+    if old is None:
+        os.environ.pop("RS_GEMM_PAIR_SPLIT", None)
+    else:
+        os.environ["RS_GEMM_PAIR_SPLIT"] = old
 
 
 @pytest.mark.parametrize("epi", [0, 1, 2, 3])
