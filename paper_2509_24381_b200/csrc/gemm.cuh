@@ -29,6 +29,8 @@ enum class Epi : int {
   SwiGLU = 2,    // C[:, j] = silu(g_j) * u_j, N/2 columns  bf16
   Gelu = 3,      // C = gelu_erf(acc + bias)                bf16
   StoreF32 = 4,  // C = acc (+ bias)                       fp32
+  QkvRope = 5,   // LLM QKV: C = acc (+ bias), q / k rotated (M-RoPE), k / v
+                 // appended to the paged KV cache (V transposed)   bf16
 };
 
 struct GemmArgs {
@@ -57,6 +59,14 @@ struct GemmArgs {
   unsigned long long* ss_out = nullptr;
   unsigned long long* ss_clear = nullptr;
   int ss_clear_n = 0;
+  // Epi::QkvRope: per-row chunk info (ChunkRowInfo: req slot, position), the
+  // chunk's [M, hd/2] (cos, sin) table, paged KV of this layer
+  const void* rope_rows = nullptr;
+  const float2* rope_table = nullptr;
+  const int* const* page_tables = nullptr;
+  bf16* k_cache = nullptr;
+  bf16* v_cache = nullptr;
+  int rope_hq = 0, rope_hkv = 0, rope_hd = 0, page_size = 0;
 };
 constexpr float kSsFixedScale = 65536.f;  // 2^16
 

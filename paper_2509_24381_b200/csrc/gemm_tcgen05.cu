@@ -11,6 +11,7 @@
 
 #include "common.cuh"
 #include "gemm.cuh"
+#include "kernels.cuh"
 #include "sm100.cuh"
 
 namespace rserve {
@@ -45,6 +46,13 @@ struct GemmParams {
   unsigned long long* ss_out;
   unsigned long long* ss_clear;
   int ss_clear_n;
+  // Epi::QkvRope
+  const ChunkRowInfo* rope_rows;
+  const float2* rope_table;
+  const int* const* page_tables;
+  bf16* k_cache;
+  bf16* v_cache;
+  int rope_hq, rope_hkv, rope_hd, page_size;
 };
 
 // Row scale of a norm-consumer GEMM (1 when the GEMM has no folded norm).
@@ -180,6 +188,16 @@ __device__ __forceinline__ void epilogue_tile_tma(const GemmParams& p, const CUt
   const int my_row = m0 + quad * 32 + lane;
   const float rs = row_scale(p, my_row);
   float ss = 0.f;  // sum of squares of this thread's output row segment (ss_out)
+  constexpr bool kRope = EPI == static_cast<int>(Epi::QkvRope);
+  std::int64_t kv_page = 0;
+  int kv_off = 0;
+  if constexpr (kRope) {
+    if (my_row < p.M) {
+      const ChunkRowInfo ri = p.rope_rows[my_row];
+      kv_page = p.page_tables[ri.req_slot][ri.pos / p.page_size];
+      kv_off = ri.pos % p.page_size;
+    }
+  }
   constexpr bool kRes = EPI == static_cast<int>(Epi::Residual);
   constexpr bool kSwi = EPI == static_cast<int>(Epi::SwiGLU);
   constexpr bool kF32 = EPI == static_cast<int>(Epi::StoreF32);
@@ -263,6 +281,64 @@ __device__ __forceinline__ void epilogue_tile_tma(const GemmParams& p, const CUt
         if constexpr (EPI == static_cast<int>(Epi::Gelu)) {
 #pragma unroll
           for (int t = 0; t < 32; ++t) x[t] = gelu_erf(x[t]);
+        }
+        if constexpr (kRope) {
+          // M-RoPE on q / k (rotate-half partner 64 columns away, in this tile:
+          // tiles are whole heads), then k / v into the paged cache
+          const int hd = p.rope_hd, half_hd = hd / 2;
+          const int head = col / hd, i0 = col % hd;
+          const bool is_v = head >= p.rope_hq + p.rope_hkv;
+          if (!is_v && col < p.N) {
+            const int delta = i0 < half_hd ? half_hd : -half_hd;
+            std::uint32_t w[32];
+            if constexpr (FROM_WS) ws_sum32<BN>(parts, n_parts, prow, c * 32 + delta, w);
+            else {
+              sm100::tmem_ld_32x32b_x32(t_row + static_cast<std::uint32_t>(c * 32 + delta), w);
+              sm100::tmem_ld_wait();
+            }
+            const float4* cs = reinterpret_cast<const float4*>(
+                p.rope_table + static_cast<std::int64_t>(min(my_row, p.M - 1)) * half_hd + (i0 % half_hd));
+            const float sgn = i0 < half_hd ? -1.f : 1.f;
+            if (p.bias != nullptr) {  // partner bias, 8 columns per 16-byte load
+#pragma unroll
+              for (int q = 0; q < 4; ++q) {
+                const uint4 bb = *reinterpret_cast<const uint4*>(p.bias + col + delta + q * 8);
+                const std::uint32_t bw[4] = {bb.x, bb.y, bb.z, bb.w};
+#pragma unroll
+                for (int t = 0; t < 4; ++t) {
+                  const float2 f = unpack_bf16x2(bw[t]);
+                  w[q * 8 + 2 * t] = __float_as_uint(rs * __uint_as_float(w[q * 8 + 2 * t]) + f.x);
+                  w[q * 8 + 2 * t + 1] = __float_as_uint(rs * __uint_as_float(w[q * 8 + 2 * t + 1]) + f.y);
+                }
+              }
+            } else {
+#pragma unroll
+              for (int t = 0; t < 32; ++t) w[t] = __float_as_uint(rs * __uint_as_float(w[t]));
+            }
+#pragma unroll
+            for (int q = 0; q < 16; ++q) {  // (cos, sin) of two columns per 16-byte load
+              const float4 c4 = __ldg(cs + q);
+              x[2 * q] = x[2 * q] * c4.x + sgn * __uint_as_float(w[2 * q]) * c4.y;
+              x[2 * q + 1] = x[2 * q + 1] * c4.z + sgn * __uint_as_float(w[2 * q + 1]) * c4.w;
+            }
+          }
+          if (head >= p.rope_hq && my_row < p.M && col < p.N) {
+            std::uint32_t o[16];
+#pragma unroll
+            for (int t = 0; t < 16; ++t) o[t] = pack_bf16x2(x[2 * t], x[2 * t + 1]);
+            if (!is_v) {  // K: [page][kv head][token][hd]
+              const int kvh = head - p.rope_hq;
+              uint4* dst = reinterpret_cast<uint4*>(
+                  p.k_cache + ((kv_page * p.rope_hkv + kvh) * p.page_size + kv_off) * hd + i0);
+#pragma unroll
+              for (int q = 0; q < 4; ++q) dst[q] = make_uint4(o[4 * q], o[4 * q + 1], o[4 * q + 2], o[4 * q + 3]);
+            } else {      // V transposed: [page][kv head][hd][token]
+              const int kvh = head - p.rope_hq - p.rope_hkv;
+              bf16* dst = p.v_cache + ((kv_page * p.rope_hkv + kvh) * hd + i0) * p.page_size + kv_off;
+#pragma unroll
+              for (int t = 0; t < 32; ++t) dst[static_cast<std::int64_t>(t) * p.page_size] = __float2bfloat16_rn(x[t]);
+            }
+          }
         }
       }
     }
@@ -829,7 +905,9 @@ void launch(const GemmArgs& a, cudaStream_t stream) {
   }
   GemmParams p{a.C, a.ldc, a.bias, a.residual, a.ldr, a.row_map, a.M, a.N, a.K, a.M_dev,
                0, 0, 0, nullptr, nullptr, 0,
-               a.ss_in, a.ss_inv_dim, a.ss_eps, a.ss_out, a.ss_clear, a.ss_clear_n};
+               a.ss_in, a.ss_inv_dim, a.ss_eps, a.ss_out, a.ss_clear, a.ss_clear_n,
+               static_cast<const ChunkRowInfo*>(a.rope_rows), a.rope_table, a.page_tables, a.k_cache, a.v_cache,
+               a.rope_hq, a.rope_hkv, a.rope_hd, a.page_size};
   if (const char* dbg = std::getenv("RS_GEMM_SK_DEBUG")) p.sk_debug = std::atoi(dbg);
   const int tiles = ceil_div(a.M, kBM * CG) * ceil_div(a.N, BN);
   int grid = CG * (tiles < kNumSMs / CG ? tiles : kNumSMs / CG);
@@ -871,6 +949,9 @@ void dispatch_epi(const GemmArgs& a, Epi epi, cudaStream_t s) {
         return launch<BN, 2, false, CG>(a, s);
     case Epi::Gelu: return tma ? launch<BN, 3, true, CG>(a, s) : launch<BN, 3, false, CG>(a, s);
     case Epi::StoreF32: return launch<BN, 4, false, CG>(a, s);  // LM-head logits (row-mapped)
+    case Epi::QkvRope:
+      if constexpr (BN % 64 == 0) return launch<BN, 5, true, CG>(a, s);
+      else throw DeviceError(RS_ERR_CUDA, "gemm: QkvRope needs whole-head tiles");
   }
 }
 
@@ -892,7 +973,7 @@ int cg_override() {
   }();
   return v;
 }
-TileChoice pick_tile(int M, int N, int K, bool swiglu) {
+TileChoice pick_tile(int M, int N, int K, bool swiglu, int tile_multiple = 0) {
   static constexpr int kCandidates[] = {256, 224, 192, 160, 128};
   const int num_kb = ceil_div(K, kBK);
   TileChoice best{256, 1};
@@ -901,6 +982,7 @@ TileChoice pick_tile(int M, int N, int K, bool swiglu) {
     if (cg_override() != 0 && cg != cg_override()) continue;
     for (int bn : kCandidates) {
       if (swiglu && bn % 64 != 0) continue;  // 64-column gate/up chunks (TMA epilogue)
+      if (tile_multiple > 0 && bn % tile_multiple != 0) continue;  // QkvRope: whole heads per tile
       const long tiles = static_cast<long>(ceil_div(M, kBM * cg)) * ceil_div(N, bn);
       const long slots = kNumSMs / cg;
       const long waves = (tiles + slots - 1) / slots;
@@ -925,7 +1007,7 @@ void gemm(const GemmArgs& a, Epi epi, cudaStream_t stream, int force_bn) {
                                        std::to_string(a.K) + ", N=" + std::to_string(a.N) + ")");
   if (epi == Epi::SwiGLU && a.N % 32 != 0)
     throw DeviceError(RS_ERR_CUDA, "gemm: SwiGLU needs N%32==0");
-  if (force_bn == 0 && a.M <= 8) {  // decode-sized: weight streaming on the CUDA cores
+  if (force_bn == 0 && a.M <= 8 && epi != Epi::QkvRope) {  // decode-sized: weight streaming on the CUDA cores
     const int tok = prof::begin(stream);
     if (gemv_small_m(a, epi, stream)) {
       prof::end(tok, stream, "gemv_small_m", 2.0 * a.M * a.N * a.K, 2.0 * a.N * a.K);
@@ -935,7 +1017,8 @@ void gemm(const GemmArgs& a, Epi epi, cudaStream_t stream, int force_bn) {
   // force_bn > 0: single-CTA tiles of that width; < 0: CTA-pair tiles of |force_bn|
   const TileChoice tc = force_bn > 0   ? TileChoice{force_bn, 1}
                         : force_bn < 0 ? TileChoice{-force_bn, 2}
-                                       : pick_tile(a.M, a.N, a.K, epi == Epi::SwiGLU);
+                                       : pick_tile(a.M, a.N, a.K, epi == Epi::SwiGLU,
+                                                   epi == Epi::QkvRope ? a.rope_hd : 0);
   const int tok = prof::begin(stream);
   const int key = tc.bn * 4 + tc.cg;
   switch (key) {

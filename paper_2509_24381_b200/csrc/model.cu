@@ -425,9 +425,7 @@ void Llm::forward_stage(const ChunkDev& c, const bf16* slab, bf16* x,
     }
     g.lda = s.d; g.B = L.qkv_w; g.ldb = s.d; g.C = qkv_; g.ldc = s.qkv_dim;
     g.bias = L.qkv_b; g.M = M; g.N = s.qkv_dim; g.K = s.d;
-    gemm(g, Epi::Store, st);
-    rope_kv_append(qkv_, s.qkv_dim, c.rows, M, s.hq, s.hkv, s.hd, s.cfg.rope_theta_llm, L.k_cache,
-                   L.v_cache, page_tables, page_size_, st, nullptr, rope_table_);
+    qkv_rope_append(g, c, L, page_tables, st);
     PagedKV kv{L.k_cache, L.v_cache, page_tables, page_size_};
     if (c.decode)
       attention_decode_paged(qkv_, s.qkv_dim, att_, s.hq * s.hd, c.work, c.n_work, c.max_keys, kv, s.hq,
@@ -461,6 +459,34 @@ void Llm::forward_stage(const ChunkDev& c, const bf16* slab, bf16* x,
   }
 }
 
+// QKV projection + M-RoPE + paged-KV append: fused into the GEMM
+// epilogue (Epi::QkvRope) for chunks; decode-sized M goes through the skinny
+// GEMM and the separate rope / append kernel. RS_QKV_FUSE=0: unfused (A/B).
+void Llm::qkv_rope_append(GemmArgs g, const ChunkDev& c, const LlmLayer& L, const int* const* page_tables,
+                          cudaStream_t st) {
+  const Shapes& s = s_;
+  static const bool fuse = [] {
+    const char* e = std::getenv("RS_QKV_FUSE");
+    return e == nullptr || e[0] != '0';
+  }();
+  if (fuse && g.M > 8 && s.hd % 64 == 0) {
+    g.rope_rows = c.rows;
+    g.rope_table = rope_table_;
+    g.page_tables = page_tables;
+    g.k_cache = L.k_cache;
+    g.v_cache = L.v_cache;
+    g.rope_hq = s.hq;
+    g.rope_hkv = s.hkv;
+    g.rope_hd = s.hd;
+    g.page_size = page_size_;
+    gemm(g, Epi::QkvRope, st);
+    return;
+  }
+  gemm(g, Epi::Store, st);
+  rope_kv_append(qkv_, s.qkv_dim, c.rows, g.M, s.hq, s.hkv, s.hd, s.cfg.rope_theta_llm, L.k_cache, L.v_cache,
+                 page_tables, page_size_, st, nullptr, rope_table_);
+}
+
 // ---- tensor-parallel phases (tp_forward, device_context.cu) --------------------------
 void Llm::tp_attn_partial(int l, const ChunkDev& c, const bf16* slab, bf16* x, bool first,
                           const unsigned long long* ss, const int* const* page_tables, bf16* part,
@@ -482,9 +508,7 @@ void Llm::tp_attn_partial(int l, const ChunkDev& c, const bf16* slab, bf16* x, b
   }
   g.lda = s.d; g.B = L.qkv_w; g.ldb = s.d; g.C = qkv_; g.ldc = s.qkv_dim;
   g.bias = L.qkv_b; g.M = M; g.N = s.qkv_dim; g.K = s.d;
-  gemm(g, Epi::Store, st);
-  rope_kv_append(qkv_, s.qkv_dim, c.rows, M, s.hq, s.hkv, s.hd, s.cfg.rope_theta_llm, L.k_cache,
-                 L.v_cache, page_tables, page_size_, st, nullptr, rope_table_);
+  qkv_rope_append(g, c, L, page_tables, st);
   PagedKV kv{L.k_cache, L.v_cache, page_tables, page_size_};
   if (c.decode)
     attention_decode_paged(qkv_, s.qkv_dim, att_, s.hq * s.hd, c.work, c.n_work, c.max_keys, kv, s.hq,

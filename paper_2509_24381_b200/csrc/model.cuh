@@ -20,6 +20,7 @@
 
 #include "attention.cuh"
 #include "common.cuh"
+#include "gemm.cuh"
 #include "kernels.cuh"
 #include "rserve.h"
 
@@ -155,6 +156,9 @@ class Llm {
                        cudaStream_t st);
   void tp_mlp_partial(int layer, const ChunkDev& c, const bf16* x, const unsigned long long* ss,
                       bf16* part, cudaStream_t st);
+  /// QKV GEMM + M-RoPE + KV append (fused epilogue for chunks).
+  void qkv_rope_append(GemmArgs g, const ChunkDev& c, const LlmLayer& L, const int* const* page_tables,
+                       cudaStream_t st);
   /// Per-chunk setup of a tensor-parallel pass (the M-RoPE table).
   void tp_begin(const ChunkDev& c, cudaStream_t st);
   /// Final norm + LM head + argmax for the rows of c that end a prompt.
