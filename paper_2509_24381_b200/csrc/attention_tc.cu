@@ -88,22 +88,6 @@ __device__ __forceinline__ float poly_exp2(float x) {
   const int bits = __float_as_int(p) + (static_cast<int>(n) << 23);
   return x <= -127.f ? 0.f : __int_as_float(bits);
 }
-// Packed fp32x2 arithmetic (sm_100 FFMA2 / FADD2: two lanes per instruction).
-__device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) {
-  unsigned long long r;
-  asm("fma.rn.f32x2 %0, %1, %2, %3;"
-      : "=l"(r)
-      : "l"(*reinterpret_cast<unsigned long long*>(&a)), "l"(*reinterpret_cast<unsigned long long*>(&b)),
-        "l"(*reinterpret_cast<unsigned long long*>(&c)));
-  return *reinterpret_cast<float2*>(&r);
-}
-__device__ __forceinline__ float2 add2(float2 a, float2 b) {
-  unsigned long long r;
-  asm("add.rn.f32x2 %0, %1, %2;"
-      : "=l"(r)
-      : "l"(*reinterpret_cast<unsigned long long*>(&a)), "l"(*reinterpret_cast<unsigned long long*>(&b)));
-  return *reinterpret_cast<float2*>(&r);
-}
 // poly_exp2_fma below on a pair, with the FMAs packed.
 __device__ __forceinline__ float2 poly_exp2_fma2(float2 x) {
   x.x = fmaxf(x.x, -125.5f);

@@ -258,21 +258,21 @@ __device__ __forceinline__ void epilogue_tile_tma(const GemmParams& p, const CUt
         }
       } else {
         if constexpr (!FROM_WS) sm100::tmem_ld_wait();
-        if (p.ss_in != nullptr) {
-#pragma unroll
-          for (int t = 0; t < 32; ++t) v[t] = __float_as_uint(rs * __uint_as_float(v[t]));
-        }
         const int col = n0 + c * 32;
-        if (p.bias != nullptr && col < p.N) {
+        if (p.ss_in != nullptr || (p.bias != nullptr && col < p.N)) {
+          // v = rs * acc + bias, two columns per packed FFMA2
+          const float2 rs2 = make_float2(rs, rs);
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
-            const uint4 bb = *reinterpret_cast<const uint4*>(p.bias + col + q * 8);
+            uint4 bb = make_uint4(0, 0, 0, 0);
+            if (p.bias != nullptr && col < p.N) bb = *reinterpret_cast<const uint4*>(p.bias + col + q * 8);
             const std::uint32_t bw[4] = {bb.x, bb.y, bb.z, bb.w};
 #pragma unroll
             for (int t = 0; t < 4; ++t) {
-              const float2 f = unpack_bf16x2(bw[t]);
-              v[q * 8 + 2 * t] = __float_as_uint(__uint_as_float(v[q * 8 + 2 * t]) + f.x);
-              v[q * 8 + 2 * t + 1] = __float_as_uint(__uint_as_float(v[q * 8 + 2 * t + 1]) + f.y);
+              const float2 y = fma2(make_float2(__uint_as_float(v[q * 8 + 2 * t]), __uint_as_float(v[q * 8 + 2 * t + 1])),
+                                    rs2, unpack_bf16x2(bw[t]));
+              v[q * 8 + 2 * t] = __float_as_uint(y.x);
+              v[q * 8 + 2 * t + 1] = __float_as_uint(y.y);
             }
           }
         }
@@ -299,27 +299,28 @@ __device__ __forceinline__ void epilogue_tile_tma(const GemmParams& p, const CUt
             const float4* cs = reinterpret_cast<const float4*>(
                 p.rope_table + static_cast<std::int64_t>(min(my_row, p.M - 1)) * half_hd + (i0 % half_hd));
             const float sgn = i0 < half_hd ? -1.f : 1.f;
-            if (p.bias != nullptr) {  // partner bias, 8 columns per 16-byte load
+            const float2 rs2 = make_float2(rs, rs);
 #pragma unroll
-              for (int q = 0; q < 4; ++q) {
-                const uint4 bb = *reinterpret_cast<const uint4*>(p.bias + col + delta + q * 8);
-                const std::uint32_t bw[4] = {bb.x, bb.y, bb.z, bb.w};
+            for (int q = 0; q < 4; ++q) {  // partner: rs * acc + bias (8 columns per 16-byte load)
+              uint4 bb = make_uint4(0, 0, 0, 0);
+              if (p.bias != nullptr) bb = *reinterpret_cast<const uint4*>(p.bias + col + delta + q * 8);
+              const std::uint32_t bw[4] = {bb.x, bb.y, bb.z, bb.w};
 #pragma unroll
-                for (int t = 0; t < 4; ++t) {
-                  const float2 f = unpack_bf16x2(bw[t]);
-                  w[q * 8 + 2 * t] = __float_as_uint(rs * __uint_as_float(w[q * 8 + 2 * t]) + f.x);
-                  w[q * 8 + 2 * t + 1] = __float_as_uint(rs * __uint_as_float(w[q * 8 + 2 * t + 1]) + f.y);
-                }
+              for (int t = 0; t < 4; ++t) {
+                const float2 y = fma2(make_float2(__uint_as_float(w[q * 8 + 2 * t]), __uint_as_float(w[q * 8 + 2 * t + 1])),
+                                      rs2, unpack_bf16x2(bw[t]));
+                w[q * 8 + 2 * t] = __float_as_uint(y.x);
+                w[q * 8 + 2 * t + 1] = __float_as_uint(y.y);
               }
-            } else {
-#pragma unroll
-              for (int t = 0; t < 32; ++t) w[t] = __float_as_uint(rs * __uint_as_float(w[t]));
             }
 #pragma unroll
             for (int q = 0; q < 16; ++q) {  // (cos, sin) of two columns per 16-byte load
               const float4 c4 = __ldg(cs + q);
-              x[2 * q] = x[2 * q] * c4.x + sgn * __uint_as_float(w[2 * q]) * c4.y;
-              x[2 * q + 1] = x[2 * q + 1] * c4.z + sgn * __uint_as_float(w[2 * q + 1]) * c4.w;
+              const float2 xr = fma2(make_float2(__uint_as_float(w[2 * q]), __uint_as_float(w[2 * q + 1])),
+                                     make_float2(sgn * c4.y, sgn * c4.w),
+                                     mul2(make_float2(x[2 * q], x[2 * q + 1]), make_float2(c4.x, c4.z)));
+              x[2 * q] = xr.x;
+              x[2 * q + 1] = xr.y;
             }
           }
           if (head >= p.rope_hq && my_row < p.M && col < p.N) {
