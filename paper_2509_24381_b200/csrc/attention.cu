@@ -257,7 +257,7 @@ __device__ void flash_block(const bf16* q_ptr, int ld_q, int q_rows, int q_pos0,
 }
 
 template <int HD, int NBUF>
-__global__ void __launch_bounds__(128) varlen_bidir_kernel(const bf16* __restrict__ qkv, int ld,
+__global__ void __launch_bounds__(128, NBUF == 1 ? 4 : 1) varlen_bidir_kernel(const bf16* __restrict__ qkv, int ld,
                                                            bf16* __restrict__ out, int ld_out,
                                                            const int* __restrict__ cu, int heads,
                                                            float scale_log2, const float2* rope) {
