@@ -69,9 +69,11 @@ void attention_decode_paged(const bf16* qkv, int ld_q, bf16* out, int ld_out, co
                             int head_dim, float scale, cudaStream_t st);
 
 /// tcgen05 / TMEM flash attention (attention_tc.cu). q: packed QKV rows of
-/// the chunk ([q_rows_alloc, (Hq + 2 Hkv) hd], q columns first).
+/// the chunk ([q_rows_alloc, (Hq + 2 Hkv) hd], q columns first). max_keys:
+/// the longest item's key count (0: unknown); with few (item, head) units and
+/// long keys the keys are split over more CTAs and merged (split-KV).
 void attention_prefill_paged_tc(const bf16* q, int ld_q, int q_rows_alloc, bf16* out, int ld_out,
-                                const PrefillWork* work, int n_work, const PagedKV& kv,
+                                const PrefillWork* work, int n_work, int max_keys, const PagedKV& kv,
                                 std::int64_t kv_pages, int q_heads, int kv_heads, int head_dim,
                                 float scale, cudaStream_t stream);
 

@@ -63,7 +63,18 @@ struct TcParams {
   float scale_log2;
   bf16* out;
   int ld_out;
+  // kPaged split-KV (few units): unit u = ((w * H + head) * kv_splits + split);
+  // split s covers key tiles [s n / S, (s + 1) n / S) of the unit's n tiles and
+  // writes unnormalised fp32 O plus (m, l) per row; pp_merge_kernel combines.
+  int kv_splits;                    // 1: no split (always 1 for kVarlen)
+  float* part_o;                    // [units * S * 256, HD]
+  float* part_ml;                   // [units * S * 256, 2]
 };
+
+__host__ __device__ __forceinline__ void kv_split_range(int n_tiles, int splits, int s, int& jb, int& je) {
+  jb = s * n_tiles / splits;
+  je = (s + 1) * n_tiles / splits;
+}
 
 __device__ __forceinline__ void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -454,12 +465,18 @@ struct PpCfg {
 struct PpUnit {
   int head, kvh, q_row0, q_rows, q_pos0, key_begin, key_end;
   int rows_t[2], n_t[2], n_max;
+  int ws_unit;     // index into the split workspace
+  int jb, je;      // key tiles [jb, je) of this split (all of them without a split)
+  int e_t[2];      // tile t's end: min(je, n_t); tile t takes part iff e_t > jb
   const int* pt;
 };
 
 template <KvMode MODE>
 __device__ __forceinline__ PpUnit pp_unit(const TcParams& p, int u) {
   PpUnit x;
+  x.ws_unit = u;
+  const int split = u % p.kv_splits;
+  u /= p.kv_splits;
   const int w = u / p.q_heads;
   x.head = u - w * p.q_heads;
   x.kvh = x.head / (p.q_heads / p.kv_heads);
@@ -488,6 +505,9 @@ __device__ __forceinline__ PpUnit pp_unit(const TcParams& p, int u) {
     x.n_t[t] = x.rows_t[t] > 0 ? (hi - x.key_begin + 127) / 128 : 0;
   }
   x.n_max = max(x.n_t[0], x.n_t[1]);
+  kv_split_range(x.n_max, p.kv_splits, split, x.jb, x.je);
+  x.e_t[0] = min(x.je, x.n_t[0]);
+  x.e_t[1] = min(x.je, x.n_t[1]);
   return x;
 }
 
@@ -568,7 +588,7 @@ __global__ void __launch_bounds__(kPpThreads, 1)
       if (u < 0) break;
       const PpUnit x = pp_unit<MODE>(p, u);
       for (int t = 0; t < 2; ++t) {
-        if (x.rows_t[t] == 0) continue;
+        if (x.e_t[t] <= x.jb) continue;
         sm100::mbar_wait(&q_empty[t], (qn[t] & 1) ^ 1);
         ++qn[t];
         sm100::mbar_expect_tx(&q_full[t], C::kQBytes);
@@ -576,7 +596,7 @@ __global__ void __launch_bounds__(kPpThreads, 1)
           sm100::tma_load_2d(sQ + t * C::kQBytes + h * kAtom, &tmQ, &q_full[t],
                              x.head * p.q_head_stride + h * 64, x.q_row0 + 128 * t);
       }
-      for (int j = 0; j < x.n_max; ++j, ++kn) {
+      for (int j = x.jb; j < x.je; ++j, ++kn) {
         const int st = static_cast<int>(kn % SK);
         std::uint8_t* k = sK + st * C::kKBytes;
         sm100::mbar_wait(&k_empty[st], ((kn / SK) & 1) ^ 1);
@@ -603,7 +623,7 @@ __global__ void __launch_bounds__(kPpThreads, 1)
       const int u = pp_unit_index(r, n_units);
       if (u < 0) break;
       const PpUnit x = pp_unit<MODE>(p, u);
-      for (int j = 0; j < x.n_max; ++j, ++vn) {
+      for (int j = x.jb; j < x.je; ++j, ++vn) {
         const int st = static_cast<int>(vn % SV);
         std::uint8_t* v = sV + st * C::kVBytes;
         sm100::mbar_wait(&v_empty[st], ((vn / SV) & 1) ^ 1);
@@ -631,14 +651,14 @@ __global__ void __launch_bounds__(kPpThreads, 1)
       if (u < 0) break;
       const PpUnit x = pp_unit<MODE>(p, u);
       for (int t = 0; t < 2; ++t)
-        if (x.rows_t[t] > 0) {
+        if (x.e_t[t] > x.jb) {
           sm100::mbar_wait(&q_full[t], qn[t] & 1);
           ++qn[t];
         }
       // last consumer of K_j / V_j (tile 1 covers every key tile tile 0 does)
-      auto last_user = [&](int j) { return j < x.n_t[1] ? 1 : 0; };
+      auto last_user = [&](int j) { return j < x.e_t[1] ? 1 : 0; };
       auto mma_s = [&](int t, int j) {
-        const std::uint32_t kn = kbase + static_cast<std::uint32_t>(j);
+        const std::uint32_t kn = kbase + static_cast<std::uint32_t>(j - x.jb);
         const int st = static_cast<int>(kn % SK);
         sm100::mbar_wait(&k_full[st], (kn / SK) & 1);
         sm100::tc_fence_after();
@@ -653,10 +673,10 @@ __global__ void __launch_bounds__(kPpThreads, 1)
         }
         sm100::umma_commit(&s_full[t]);
         if (t == last_user(j)) sm100::umma_commit(&k_empty[st]);
-        if (j == (t == 0 ? x.n_t[0] : x.n_t[1]) - 1) sm100::umma_commit(&q_empty[t]);
+        if (j == (t == 0 ? x.e_t[0] : x.e_t[1]) - 1) sm100::umma_commit(&q_empty[t]);
       };
       auto mma_pv = [&](int t, int j) {
-        const std::uint32_t vn = kbase + static_cast<std::uint32_t>(j);
+        const std::uint32_t vn = kbase + static_cast<std::uint32_t>(j - x.jb);
         const int st = static_cast<int>(vn % SV);
         sm100::mbar_wait(&v_full[st], (vn / SV) & 1);
         sm100::mbar_wait(&p_full[t], pn[t] & 1);
@@ -669,20 +689,20 @@ __global__ void __launch_bounds__(kPpThreads, 1)
 #pragma unroll
           for (int kk = 0; kk < 4; ++kk)
             sm100::umma_bf16_ts(tmem + 256 * t + 128, tmem + 256 * t + 32 * a + 8 * kk, vd + 2 * kk,
-                                idesc_o, (j | a | kk) != 0 ? 1u : 0u);
+                                idesc_o, (j > x.jb || (a | kk) != 0) ? 1u : 0u);
         }
         if (t == last_user(j)) sm100::umma_commit(&v_empty[st]);
-        if (j == (t == 0 ? x.n_t[0] : x.n_t[1]) - 1) sm100::umma_commit(&o_final[t]);
+        if (j == (t == 0 ? x.e_t[0] : x.e_t[1]) - 1) sm100::umma_commit(&o_final[t]);
       };
-      if (x.n_t[0] > 0) mma_s(0, 0);
-      if (x.n_t[1] > 0) mma_s(1, 0);
-      for (int j = 1; j <= x.n_max; ++j) {
-        if (j - 1 < x.n_t[0]) mma_pv(0, j - 1);
-        if (j < x.n_t[0]) mma_s(0, j);
-        if (j - 1 < x.n_t[1]) mma_pv(1, j - 1);
-        if (j < x.n_t[1]) mma_s(1, j);
+      if (x.e_t[0] > x.jb) mma_s(0, x.jb);
+      if (x.e_t[1] > x.jb) mma_s(1, x.jb);
+      for (int j = x.jb + 1; j <= x.je; ++j) {
+        if (j - 1 < x.e_t[0]) mma_pv(0, j - 1);
+        if (j < x.e_t[0]) mma_s(0, j);
+        if (j - 1 < x.e_t[1]) mma_pv(1, j - 1);
+        if (j < x.e_t[1]) mma_s(1, j);
       }
-      kbase += static_cast<std::uint32_t>(x.n_max);
+      kbase += static_cast<std::uint32_t>(x.je - x.jb);
     }
   } else if (warp >= 2 && warp < 10) {
     // ---------------- softmax: tile t, one query row per thread ----------------
@@ -697,9 +717,9 @@ __global__ void __launch_bounds__(kPpThreads, 1)
       const int u = pp_unit_index(rr, n_units);
       if (u < 0) break;
       const PpUnit x = pp_unit<MODE>(p, u);
-      const int n_it = t == 0 ? x.n_t[0] : x.n_t[1];
+      const int j_end = t == 0 ? x.e_t[0] : x.e_t[1];
       const int my_rows = t == 0 ? x.rows_t[0] : x.rows_t[1];
-      if (n_it == 0) continue;
+      if (j_end <= x.jb) continue;
       int lo, hi;
       if constexpr (MODE == KvMode::kPaged) {
         lo = 0;
@@ -716,7 +736,7 @@ __global__ void __launch_bounds__(kPpThreads, 1)
         hi = p.cu_seqlens[a + 1];
       }
       float m = -INFINITY, l = 0.f;
-      for (int j = 0; j < n_it; ++j) {
+      for (int j = x.jb; j < j_end; ++j) {
         sm100::mbar_wait(&s_full[t], sn & 1);
         ++sn;
         sm100::tc_fence_after();
@@ -748,7 +768,7 @@ __global__ void __launch_bounds__(kPpThreads, 1)
           alpha = m == -INFINITY ? 0.f : exp2f(m - mx);
           m = mx;
         }
-        if (j > 0 && __any_sync(0xffffffffu, raise && alpha != 1.f)) {
+        if (j > x.jb && __any_sync(0xffffffffu, raise && alpha != 1.f)) {
           // rare: rescale O_t in TMEM (PV_t,j-1 is complete: S_t,j was issued after it)
 #pragma unroll 1
           for (int c = 0; c < HD / 32; ++c) {
@@ -794,6 +814,27 @@ __global__ void __launch_bounds__(kPpThreads, 1)
       sm100::mbar_wait(&o_final[t], on & 1);
       ++on;
       sm100::tc_fence_after();
+      if constexpr (MODE == KvMode::kPaged) {
+        if (p.kv_splits > 1) {  // unnormalised partial + (m, l) for pp_merge_kernel
+          const std::int64_t prow = static_cast<std::int64_t>(x.ws_unit) * 256 + 128 * t + r;
+          float4* po = reinterpret_cast<float4*>(p.part_o + prow * HD);
+#pragma unroll
+          for (int c = 0; c < HD / 32; ++c) {
+            std::uint32_t v[32];
+            sm100::tmem_ld_32x32b_x32(o_tm + 32 * c, v);
+            sm100::tmem_ld_wait();
+            if (r < my_rows) {
+#pragma unroll
+              for (int q = 0; q < 8; ++q)
+                po[8 * c + q] = make_float4(__uint_as_float(v[4 * q]), __uint_as_float(v[4 * q + 1]),
+                                            __uint_as_float(v[4 * q + 2]), __uint_as_float(v[4 * q + 3]));
+            }
+          }
+          if (r < my_rows) reinterpret_cast<float2*>(p.part_ml)[prow] = make_float2(m, l);
+          sm100::tc_fence_before();
+          continue;
+        }
+      }
       const float inv = l > 0.f ? 1.f / l : 0.f;
       bf16* orow = p.out + static_cast<std::int64_t>(x.q_row0 + 128 * t + r) * p.ld_out + x.head * p.out_hd;
 #pragma unroll
@@ -822,6 +863,65 @@ __global__ void __launch_bounds__(kPpThreads, 1)
     sm100::tc_fence_after();
     sm100::tmem_dealloc(tmem, 512);
   }
+}
+
+// Split-KV merge: one warp per (work item, head, query row), splits combined
+// in index order (deterministic): O = sum_s 2^(m_s - M) O_s / sum_s 2^(m_s - M) l_s.
+// Split s holds row q iff its range is non-empty and starts at or below q
+// (then key jb * 128 <= q is visible and m_s is finite).
+template <int HD>
+__global__ void __launch_bounds__(256) pp_merge_kernel(const TcParams p) {
+  pdl_wait();
+  pdl_launch_dependents();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int wh = blockIdx.x;
+  const int w = wh / p.q_heads, head = wh - w * p.q_heads;
+  const int row = blockIdx.y * 8 + warp;
+  const PrefillWork wk = p.work[w];
+  if (row >= wk.q_rows) return;
+  const int q = wk.q_pos0 + row;
+  const int n_tiles = (wk.q_pos0 + wk.q_rows + 127) / 128;
+  const int S = p.kv_splits;
+  const std::int64_t row0 = static_cast<std::int64_t>(wh) * S * 256 + row;  // split s: + s * 256
+  const float2* ml = reinterpret_cast<const float2*>(p.part_ml);
+  float M = -INFINITY;
+  for (int s = 0; s < S; ++s) {
+    int jb, je;
+    kv_split_range(n_tiles, S, s, jb, je);
+    if (je > jb && q >= jb * 128) M = fmaxf(M, ml[row0 + s * 256].x);
+  }
+  constexpr int kPer = HD / 32;
+  float acc[kPer];
+#pragma unroll
+  for (int i = 0; i < kPer; ++i) acc[i] = 0.f;
+  float L = 0.f;
+  for (int s = 0; s < S; ++s) {
+    int jb, je;
+    kv_split_range(n_tiles, S, s, jb, je);
+    if (!(je > jb && q >= jb * 128)) continue;
+    const float2 v = ml[row0 + s * 256];
+    const float wgt = exp2f(v.x - M);
+    L += wgt * v.y;
+    const float* po = p.part_o + (row0 + s * 256) * HD + lane * kPer;
+    if constexpr (kPer == 4) {
+      const float4 o = *reinterpret_cast<const float4*>(po);
+      acc[0] += wgt * o.x;
+      acc[1] += wgt * o.y;
+      acc[2] += wgt * o.z;
+      acc[3] += wgt * o.w;
+    } else {
+      const float2 o = *reinterpret_cast<const float2*>(po);
+      acc[0] += wgt * o.x;
+      acc[1] += wgt * o.y;
+    }
+  }
+  const float inv = L > 0.f ? 1.f / L : 0.f;
+  bf16* orow = p.out + static_cast<std::int64_t>(wk.q_row0 + row) * p.ld_out + head * p.out_hd + lane * kPer;
+  if constexpr (kPer == 4)
+    *reinterpret_cast<uint2*>(orow) = make_uint2(pack_bf16x2(acc[0] * inv, acc[1] * inv),
+                                                 pack_bf16x2(acc[2] * inv, acc[3] * inv));
+  else
+    *reinterpret_cast<std::uint32_t*>(orow) = pack_bf16x2(acc[0] * inv, acc[1] * inv);
 }
 
 // ---- tensor maps ----------------------------------------------------------------
@@ -902,9 +1002,13 @@ void launch(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
   dim3 grid(p.q_heads, n_blocks);
   const int tok = prof::begin(st);
   if (attn_unit_rows() == 256) {
-    const int units = p.q_heads * n_blocks;
+    const int units = p.q_heads * n_blocks * p.kv_splits;
     launch_kernel(fa_pp_kernel<HD, MODE>, dim3(std::min(units, kNumSMs)), dim3(kPpThreads), PpCfg<HD>::kSmem,
                   st, 1, tq, tk, tv, p, units);
+    if (p.kv_splits > 1) {
+      launch_kernel(pp_merge_kernel<HD>, dim3(p.q_heads * n_blocks, 256 / 8), dim3(256), 0, st, 1, p);
+      count_launch();
+    }
   }
   else
     launch_kernel(fa_tc_kernel<HD, MODE>, grid, dim3(kTcThreads), TcCfg<HD>::kSmem, st, 1, tq, tk, tv, p);
@@ -923,13 +1027,50 @@ int attn_unit_rows() {
   return rows;
 }
 
+int prefill_kv_splits(int units, int max_keys) {
+  const char* e = std::getenv("RS_ATTN_KV_SPLITS");  // A/B and tests: force a split count
+  if (e != nullptr && e[0] != '\0') return std::max(1, std::min(16, std::atoi(e)));
+  if (max_keys <= 0 || units >= kNumSMs || attn_unit_rows() != 256) return 1;
+  const int n_tiles = (max_keys + 127) / 128;
+  // fewest waves per unit of work: ceil(units * S / SMs) / S, each split
+  // keeping >= 4 key tiles (its Q load, epilogue and the merge amortised)
+  int best = 1;
+  double best_cost = 1.0;
+  for (int s = 2; s <= 8 && 4 * s <= n_tiles; ++s) {
+    const double cost = static_cast<double>((units * s + kNumSMs - 1) / kNumSMs) / s + 0.02 * s;
+    if (cost < best_cost) {
+      best_cost = cost;
+      best = s;
+    }
+  }
+  return best;
+}
+
 void attention_prefill_paged_tc(const bf16* q, int ld_q, int q_rows_alloc, bf16* out, int ld_out,
-                                const PrefillWork* work, int n_work, const PagedKV& kv,
+                                const PrefillWork* work, int n_work, int max_keys, const PagedKV& kv,
                                 std::int64_t kv_pages, int q_heads, int kv_heads, int head_dim,
                                 float scale, cudaStream_t stream) {
   if (n_work <= 0) return;
   if (kv.page_size != 64) throw DeviceError(RS_ERR_CUDA, "tc attention needs 64-token pages");
   TcParams p{};
+  p.kv_splits = attn_unit_rows() == 256 ? prefill_kv_splits(q_heads * n_work, max_keys) : 1;
+  if (p.kv_splits > 1) {
+    struct Ws {
+      float* buf = nullptr;
+      std::size_t floats = 0;
+    };
+    static thread_local std::unordered_map<cudaStream_t, Ws> ws_by_stream;
+    Ws& ws = ws_by_stream[stream];
+    const std::size_t rows = static_cast<std::size_t>(n_work) * q_heads * p.kv_splits * 256;
+    const std::size_t need = rows * (head_dim + 2);
+    if (ws.floats < need) {
+      if (ws.buf != nullptr) RS_CUDA_CHECK(cudaFreeAsync(ws.buf, stream));
+      RS_CUDA_CHECK(cudaMallocAsync(reinterpret_cast<void**>(&ws.buf), need * sizeof(float), stream));
+      ws.floats = need;
+    }
+    p.part_o = ws.buf;
+    p.part_ml = ws.buf + rows * head_dim;
+  }
   p.work = work;
   p.page_tables = kv.page_tables;
   p.q_heads = q_heads;
@@ -956,6 +1097,7 @@ void attention_varlen_tc(const bf16* qp, const bf16* kp, const bf16* vt, int row
   if (n_blocks <= 0) return;
   constexpr int HD = 128;
   TcParams p{};
+  p.kv_splits = 1;
   p.blocks = blocks;
   p.cu_seqlens = cu_seqlens;
   p.n_seqs = n_seqs;

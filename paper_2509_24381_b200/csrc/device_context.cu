@@ -447,6 +447,7 @@ void Context::prefill(const std::vector<SliceRef>& slices, bf16* x, cudaStream_t
   if (first) c.gather_rows = static_cast<const std::int64_t*>(up_.put(gather.data(), gather.size() * 8, st));
   c.work = static_cast<const PrefillWork*>(up_.put(work.data(), work.size() * sizeof(PrefillWork), st));
   c.n_work = static_cast<int>(work.size());
+  c.max_keys = work.empty() ? 0 : work.front().q_pos0 + work.front().q_rows;  // sorted: most keys first
   if (llm_->has_head() && l_to == llm_->layer_end() && !done_rows.empty()) {
     c.done_rows = static_cast<const std::int64_t*>(up_.put(done_rows.data(), done_rows.size() * 8, st));
     c.done_slots = static_cast<const std::int32_t*>(up_.put(done_slots.data(), done_slots.size() * 4, st));

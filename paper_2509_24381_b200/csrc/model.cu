@@ -431,7 +431,7 @@ void Llm::forward_stage(const ChunkDev& c, const bf16* slab, bf16* x,
       attention_decode_paged(qkv_, s.qkv_dim, att_, s.hq * s.hd, c.work, c.n_work, c.max_keys, kv, s.hq,
                              s.hkv, s.hd, scale, st);
     else
-      attention_prefill_paged_tc(qkv_, s.qkv_dim, max_m_, att_, s.hq * s.hd, c.work, c.n_work, kv,
+      attention_prefill_paged_tc(qkv_, s.qkv_dim, max_m_, att_, s.hq * s.hd, c.work, c.n_work, c.max_keys, kv,
                                  kv_pages_, s.hq, s.hkv, s.hd, scale, st);
     g = GemmArgs{};
     g.A = att_; g.lda = s.hq * s.hd; g.B = L.o_w; g.ldb = s.hq * s.hd; g.C = x; g.ldc = s.d;
@@ -514,7 +514,7 @@ void Llm::tp_attn_partial(int l, const ChunkDev& c, const bf16* slab, bf16* x, b
     attention_decode_paged(qkv_, s.qkv_dim, att_, s.hq * s.hd, c.work, c.n_work, c.max_keys, kv, s.hq,
                            s.hkv, s.hd, scale, st);
   else
-    attention_prefill_paged_tc(qkv_, s.qkv_dim, max_m_, att_, s.hq * s.hd, c.work, c.n_work, kv,
+    attention_prefill_paged_tc(qkv_, s.qkv_dim, max_m_, att_, s.hq * s.hd, c.work, c.n_work, c.max_keys, kv,
                                kv_pages_, s.hq, s.hkv, s.hd, scale, st);
   g = GemmArgs{};
   g.A = att_; g.lda = s.hq * s.hd; g.B = L.o_w; g.ldb = s.hq * s.hd; g.C = part; g.ldc = s.d;

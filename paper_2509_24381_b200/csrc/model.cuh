@@ -135,7 +135,7 @@ struct ChunkDev {
   const std::int32_t* done_slots = nullptr;   // their logits-table slots
   int n_done = 0;
   bool decode = false;  // one row per work item (decode step): split-KV decode attention
-  int max_keys = 0;     // decode: longest key range
+  int max_keys = 0;     // longest key range (prefill: picks the attention KV split)
 };
 
 class Llm {

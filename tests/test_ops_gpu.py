@@ -309,6 +309,18 @@ def test_attention_prefill_tcgen05(nat, hd, hq, hkv, pos0, rows):
     _close(out, ref)
 
 
+@pytest.mark.parametrize("splits", [2, 3, 8])
+@pytest.mark.parametrize("hd,hq,hkv,pos0,rows", [(128, 28, 4, 8192, 384), (128, 4, 1, 300, 77),
+                                                 (64, 8, 2, 63, 130), (64, 8, 2, 0, 130),
+                                                 (128, 7, 7, 1000, 256), (128, 2, 1, 5000, 1)])
+def test_attention_prefill_kv_split(nat, monkeypatch, splits, hd, hq, hkv, pos0, rows):
+    """Split-KV path (few units, long keys): splits forced, including splits
+    with empty key ranges and rows that see no key of a split."""
+    monkeypatch.setenv("RS_ATTN_KV_SPLITS", str(splits))
+    out, ref = _paged_case(nat, hd, hq, hkv, pos0, rows, seed=splits)
+    _close(out, ref)
+
+
 @pytest.mark.parametrize("tc", [False, True])
 @pytest.mark.parametrize("hd,heads,lens", [(80, 4, [64, 64, 37, 64]), (80, 2, [1024, 300]),
                                            (64, 4, [256, 256, 5]), (128, 2, [130, 1]),
