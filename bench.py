@@ -130,19 +130,24 @@ def group_profile(raw):
     """Kernel classes from the profiler's labels: GEMM launches are labelled
     per shape ("gemm_tcgen05|M|N|K|epi|BN|CG") and grouped on the prefix; the
     per-shape rows are returned separately (sorted by time)."""
-    out, shapes = {}, []
+    out, shapes, attn = {}, [], []
     for k, v in raw.items():
         base = k.split("|")[0]
         a = out.setdefault(base, {"launches": 0, "ms": 0.0, "flops": 0.0, "bytes": 0.0})
         for f in a:
             a[f] += v[f]
-        if "|" in k:
+        if base == "attn_prefill_tcgen05" and "|" in k:
+            items, keys, splits = (int(x) for x in k.split("|")[1:])
+            attn.append({"items": items, "max_keys": keys, "kv_splits": splits,
+                         "launches": v["launches"], "ms": round(v["ms"], 3)})
+        elif "|" in k:
             M, Nn, K, epi, bn, cg = (int(x) for x in k.split("|")[1:])
             shapes.append({"M": M, "N": Nn, "K": K, "epi": epi, "tile": f"{128 * cg}x{bn}",
                            "launches": v["launches"], "ms": round(v["ms"], 3),
                            "tflops": round(v["flops"] / (v["ms"] / 1e3) / 1e12, 1) if v["ms"] else None})
     shapes.sort(key=lambda r: -r["ms"])
-    return out, shapes
+    attn.sort(key=lambda r: -r["ms"])
+    return out, shapes, attn
 
 
 def bench_config(args, ws):
@@ -229,7 +234,7 @@ def run_ours(args):
     torch.cuda.synchronize()
     N.check(N.lib.rs_profile_enable(0))
     prof_raw = N.profile_drain()
-    prof, gemm_shapes = group_profile(prof_raw)
+    prof, gemm_shapes, attn_shapes = group_profile(prof_raw)
     prof_steps = 1
     # e2e through the public API: H2D pixels from pinned host + D2H logits in the timed region
     e2e_wall, e2e_gpu, h2d, d2h, e2e_gaps = [], [], 0, 0, []
@@ -338,6 +343,7 @@ def run_ours(args):
                                "gbs": v["bytes"] / (v["ms"] / 1e3) / 1e9 if v["ms"] and v["bytes"] else None}
                            for k, v in prof.items()},
         "gemm_shapes": gemm_shapes[:16],
+        "attn_prefill_shapes": attn_shapes,
         "decode": decode,
         "prefill_chunk_tokens": chunk_sizes,
         "model_tflop_per_request": {"encode": vit_f / 1e12, "prefill": llm_f / 1e12},

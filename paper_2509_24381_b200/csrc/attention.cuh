@@ -58,8 +58,8 @@ struct AttnBlock {
 /// sequence [cu[s], cu[s+1]).
 void attention_varlen_tc(const bf16* qp, const bf16* kp, const bf16* vt, int rows_alloc,
                          int heads, bf16* out, int ld_out, int out_hd, const AttnBlock* blocks,
-                         int n_blocks, const int* cu_seqlens, int n_seqs, float scale,
-                         cudaStream_t stream);
+                         const AttnBlock* blocks_host, int n_blocks, const int* cu_seqlens, int n_seqs,
+                         float scale, cudaStream_t stream);
 
 /// Decode attention (one query row per work item, q_rows == 1, keys
 /// [0, q_pos0]) over the paged KV: split along the keys, GQA-packed,
@@ -69,12 +69,14 @@ void attention_decode_paged(const bf16* qkv, int ld_q, bf16* out, int ld_out, co
                             int head_dim, float scale, cudaStream_t st);
 
 /// tcgen05 / TMEM flash attention (attention_tc.cu). q: packed QKV rows of
-/// the chunk ([q_rows_alloc, (Hq + 2 Hkv) hd], q columns first). max_keys:
+/// the chunk ([q_rows_alloc, (Hq + 2 Hkv) hd], q columns first); work /
+/// blocks: device list, *_host: the same list on the host (inlined into the
+/// kernel parameters). max_keys:
 /// the longest item's key count (0: unknown); with few (item, head) units and
 /// long keys the keys are split over more CTAs and merged (split-KV).
 void attention_prefill_paged_tc(const bf16* q, int ld_q, int q_rows_alloc, bf16* out, int ld_out,
-                                const PrefillWork* work, int n_work, int max_keys, const PagedKV& kv,
-                                std::int64_t kv_pages, int q_heads, int kv_heads, int head_dim,
-                                float scale, cudaStream_t stream);
+                                const PrefillWork* work, const PrefillWork* work_host, int n_work,
+                                int max_keys, const PagedKV& kv, std::int64_t kv_pages, int q_heads,
+                                int kv_heads, int head_dim, float scale, cudaStream_t stream);
 
 }  // namespace rserve

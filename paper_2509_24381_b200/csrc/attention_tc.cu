@@ -21,10 +21,12 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <unordered_map>
+#include <vector>
 
 #include "attention.cuh"
 #include "common.cuh"
@@ -51,6 +53,9 @@ constexpr std::uint32_t kTmemS = 0, kTmemO = 256, kTmemP = 384;
 
 enum class KvMode { kPaged, kVarlen };
 
+constexpr int kInlineUnits = 128;  // work items per launch (larger launches are batched)
+constexpr int kMaxPieces = 256;    // item key-splits per launch
+
 struct TcParams {
   const PrefillWork* work;          // kPaged
   const int* const* page_tables;    // kPaged
@@ -63,12 +68,24 @@ struct TcParams {
   float scale_log2;
   bf16* out;
   int ld_out;
-  // kPaged split-KV (few units): unit u = ((w * H + head) * kv_splits + split);
-  // split s covers key tiles [s n / S, (s + 1) n / S) of the unit's n tiles and
-  // writes unnormalised fp32 O plus (m, l) per row; pp_merge_kernel combines.
-  int kv_splits;                    // 1: no split (always 1 for kVarlen)
-  float* part_o;                    // [units * S * 256, HD]
-  float* part_ml;                   // [units * S * 256, 2]
+  // The launch's work items / blocks, inlined in the kernel parameters
+  // (constant bank): the ping-pong kernel's MMA warp derives its loop bounds
+  // and ring stages from them, so they stay in uniform registers and the
+  // tcgen05.mma operands need no per-instruction uniformisation.
+  int4 inl[kInlineUnits];
+  // Pieces (ping-pong kernel): an item's keys may be split S ways (kPaged);
+  // piece = (item, split s, S, first piece of the item), in descending cost
+  // order; unit u = piece u / H, head u % H. Split s covers key tiles
+  // [s n / S, (s + 1) n / S) of the item's n tiles and writes unnormalised
+  // fp32 O plus (m, l) per row to the workspace (row (u * 256 + r));
+  // pp_merge_kernel combines an item's splits in order.
+  int4 pieces[kMaxPieces];
+  int2 item_split[kInlineUnits];    // (S, first piece) per item
+  int n_pieces;
+  int max_split;                    // > 1: the workspace / merge are in use
+  int max_keys;                     // kPaged: longest item's keys (host info, profiling label)
+  float* part_o;                    // [n_pieces * H * 256, HD]
+  float* part_ml;                   // [n_pieces * H * 256, 2]
 };
 
 __host__ __device__ __forceinline__ void kv_split_range(int n_tiles, int splits, int s, int& jb, int& je) {
@@ -132,7 +149,7 @@ __device__ __forceinline__ float poly_exp2_fma(float x) {
 template <int HD, KvMode MODE>
 __global__ void __launch_bounds__(kTcThreads, 1)
     fa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
-                 const __grid_constant__ CUtensorMap tmV, const TcParams p) {
+                 const __grid_constant__ CUtensorMap tmV, const __grid_constant__ TcParams p) {
   using C = TcCfg<HD>;
   constexpr int S = C::kStages;
   extern __shared__ __align__(1024) std::uint8_t smem_raw[];
@@ -440,6 +457,41 @@ __global__ void __launch_bounds__(kTcThreads, 1)
 // softmax of Q0, 6-9 softmax of Q1 (warp w reads TMEM lanes 32 * (w % 4)),
 // 10 TMA producer (V ring).
 constexpr int kPpThreads = 352;
+#ifndef RS_PP_POLY_EVERY
+#define RS_PP_POLY_EVERY 4
+#endif
+constexpr int kPolyEvery = RS_PP_POLY_EVERY;  // exp2 pairs on the FMA pipe: 1 in kPolyEvery (0: none)
+// dev timing builds only (wrong results): -DRS_PP_TIMING_NOEXP / -DRS_PP_TIMING_SKIP_SOFTMAX
+#ifdef RS_PP_TIMING_NOEXP
+constexpr bool kTimingNoExp = true;
+#else
+constexpr bool kTimingNoExp = false;
+#endif
+#ifdef RS_PP_TIMING_NO_PV
+constexpr bool kTimingNoPv = true;
+#else
+constexpr bool kTimingNoPv = false;
+#endif
+#ifdef RS_PP_TIMING_NO_S
+constexpr bool kTimingNoS = true;
+#else
+constexpr bool kTimingNoS = false;
+#endif
+#ifdef RS_PP_TIMING_NO_PWAIT
+constexpr bool kTimingNoPWait = true;
+#else
+constexpr bool kTimingNoPWait = false;
+#endif
+#ifdef RS_PP_TIMING_NO_LOAD
+constexpr bool kTimingNoLoad = true;
+#else
+constexpr bool kTimingNoLoad = false;
+#endif
+#ifdef RS_PP_TIMING_SKIP_SOFTMAX
+constexpr bool kTimingSkipSoftmax = true;
+#else
+constexpr bool kTimingSkipSoftmax = false;
+#endif
 
 template <int HD>
 struct PpCfg {
@@ -466,6 +518,7 @@ struct PpUnit {
   int head, kvh, q_row0, q_rows, q_pos0, key_begin, key_end;
   int rows_t[2], n_t[2], n_max;
   int ws_unit;     // index into the split workspace
+  int splits;      // > 1: this unit writes a partial (split-KV)
   int jb, je;      // key tiles [jb, je) of this split (all of them without a split)
   int e_t[2];      // tile t's end: min(je, n_t); tile t takes part iff e_t > jb
   const int* pt;
@@ -475,27 +528,27 @@ template <KvMode MODE>
 __device__ __forceinline__ PpUnit pp_unit(const TcParams& p, int u) {
   PpUnit x;
   x.ws_unit = u;
-  const int split = u % p.kv_splits;
-  u /= p.kv_splits;
-  const int w = u / p.q_heads;
-  x.head = u - w * p.q_heads;
+  const int pi = u / p.q_heads;
+  x.head = u - pi * p.q_heads;
+  const int4 pc = p.pieces[pi];
+  const int w = pc.x, split = pc.y;
+  x.splits = pc.z;
   x.kvh = x.head / (p.q_heads / p.kv_heads);
   x.q_pos0 = 0;
   x.pt = nullptr;
+  const int4 it = p.inl[w];  // PrefillWork / AttnBlock, both 4 ints
   if constexpr (MODE == KvMode::kPaged) {
-    const PrefillWork wk = p.work[w];
-    x.q_row0 = wk.q_row0;
-    x.q_rows = wk.q_rows;
-    x.q_pos0 = wk.q_pos0;
+    x.q_row0 = it.x;
+    x.q_rows = it.y;
+    x.q_pos0 = it.z;
     x.key_begin = 0;
-    x.key_end = wk.q_pos0 + wk.q_rows;
-    x.pt = p.page_tables[wk.req_slot];
+    x.key_end = it.z + it.y;
+    x.pt = p.page_tables[it.w];  // producers only
   } else {
-    const AttnBlock b = p.blocks[w];
-    x.q_row0 = b.q_row0;
-    x.q_rows = b.q_rows;
-    x.key_begin = b.key_begin & ~7;  // 16-B aligned V^T tile start (extra keys masked)
-    x.key_end = b.key_end;
+    x.q_row0 = it.x;
+    x.q_rows = it.y;
+    x.key_begin = it.z & ~7;  // 16-B aligned V^T tile start (extra keys masked)
+    x.key_end = it.w;
   }
   x.rows_t[0] = min(x.q_rows, 128);
   x.rows_t[1] = max(x.q_rows - 128, 0);
@@ -505,7 +558,7 @@ __device__ __forceinline__ PpUnit pp_unit(const TcParams& p, int u) {
     x.n_t[t] = x.rows_t[t] > 0 ? (hi - x.key_begin + 127) / 128 : 0;
   }
   x.n_max = max(x.n_t[0], x.n_t[1]);
-  kv_split_range(x.n_max, p.kv_splits, split, x.jb, x.je);
+  kv_split_range(x.n_max, x.splits, split, x.jb, x.je);
   x.e_t[0] = min(x.je, x.n_t[0]);
   x.e_t[1] = min(x.je, x.n_t[1]);
   return x;
@@ -521,7 +574,7 @@ __device__ __forceinline__ int pp_unit_index(int r, int n_units) {
 template <int HD, KvMode MODE>
 __global__ void __launch_bounds__(kPpThreads, 1)
     fa_pp_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
-                 const __grid_constant__ CUtensorMap tmV, const TcParams p, int n_units) {
+                 const __grid_constant__ CUtensorMap tmV, const __grid_constant__ TcParams p, int n_units) {
   using C = PpCfg<HD>;
   constexpr int SK = C::kKStages, SV = C::kVStages;
   extern __shared__ __align__(1024) std::uint8_t smem_raw[];
@@ -538,7 +591,7 @@ __global__ void __launch_bounds__(kPpThreads, 1)
   std::uint64_t* v_full = k_empty + SK;    // [SV]
   std::uint64_t* v_empty = v_full + SV;    // [SV]
   std::uint64_t* s_full = v_empty + SV;    // [2] S_t,j ready (and PV_t,j-1 done)
-  std::uint64_t* p_full = s_full + 2;      // [2] P_t,j written (128 softmax threads)
+  std::uint64_t* p_full = s_full + 2;      // [2] P_t,j written (4 softmax warps)
   std::uint64_t* o_final = p_full + 2;     // [2] last PV_t of a unit done
   std::uint32_t* tmem_holder = reinterpret_cast<std::uint32_t*>(o_final + 2);
 
@@ -553,7 +606,7 @@ __global__ void __launch_bounds__(kPpThreads, 1)
       sm100::mbar_init(&q_full[t], 1);
       sm100::mbar_init(&q_empty[t], 1);
       sm100::mbar_init(&s_full[t], 1);
-      sm100::mbar_init(&p_full[t], 128);
+      sm100::mbar_init(&p_full[t], 4);  // one arrive per softmax warp
       sm100::mbar_init(&o_final[t], 1);
     }
     for (int i = 0; i < SK; ++i) {
@@ -600,6 +653,10 @@ __global__ void __launch_bounds__(kPpThreads, 1)
         const int st = static_cast<int>(kn % SK);
         std::uint8_t* k = sK + st * C::kKBytes;
         sm100::mbar_wait(&k_empty[st], ((kn / SK) & 1) ^ 1);
+        if (kTimingNoLoad && kn >= SK) {
+          sm100::mbar_arrive(&k_full[st]);
+          continue;
+        }
         sm100::mbar_expect_tx(&k_full[st], C::kKBytes);
         if constexpr (MODE == KvMode::kPaged) {
           int pa, pb;
@@ -627,6 +684,10 @@ __global__ void __launch_bounds__(kPpThreads, 1)
         const int st = static_cast<int>(vn % SV);
         std::uint8_t* v = sV + st * C::kVBytes;
         sm100::mbar_wait(&v_empty[st], ((vn / SV) & 1) ^ 1);
+        if (kTimingNoLoad && vn >= SV) {
+          sm100::mbar_arrive(&v_full[st]);
+          continue;
+        }
         sm100::mbar_expect_tx(&v_full[st], C::kVBytes);
         if constexpr (MODE == KvMode::kPaged) {
           int pa, pb;
@@ -640,8 +701,12 @@ __global__ void __launch_bounds__(kPpThreads, 1)
         }
       }
     }
-  } else if (warp == 1 && lane == 0) {
-    // ---------------- MMA issuer ----------------
+  } else if (warp == 1) {
+    // ---------------- MMA issuer: the whole warp runs the loop (converged,
+    // every value derived from the kernel parameters: uniform registers);
+    // one elected lane issues each tcgen05.mma / commit. The 512-column
+    // allocation can only start at column 0: TMEM addresses are constants.
+    if (tmem != 0) __trap();
     constexpr std::uint32_t idesc_s = sm100::idesc_bf16_f32(128, 128);
     constexpr std::uint32_t idesc_o = sm100::idesc_bf16_f32(128, HD);
     std::uint32_t qn[2] = {0, 0}, pn[2] = {0, 0};
@@ -663,36 +728,50 @@ __global__ void __launch_bounds__(kPpThreads, 1)
         sm100::mbar_wait(&k_full[st], (kn / SK) & 1);
         sm100::tc_fence_after();
         std::uint8_t* k = sK + st * C::kKBytes;
+        if (sm100::elect_one()) {
 #pragma unroll
-        for (int h = 0; h < C::kHdAtoms; ++h) {
-          const std::uint64_t qd = sm100::sw128_kmajor_desc(sm100::smem_u32(sQ + t * C::kQBytes + h * kAtom));
-          const std::uint64_t kd = sm100::sw128_kmajor_desc(sm100::smem_u32(k + h * kAtom));
+          for (int h = 0; h < C::kHdAtoms; ++h) {
+            const std::uint64_t qd = sm100::sw128_kmajor_desc(sm100::smem_u32(sQ + t * C::kQBytes + h * kAtom));
+            const std::uint64_t kd = sm100::sw128_kmajor_desc(sm100::smem_u32(k + h * kAtom));
 #pragma unroll
-          for (int kk = 0; kk < 4; ++kk)
-            sm100::umma_bf16(tmem + 256 * t, qd + 2 * kk, kd + 2 * kk, idesc_s, (h | kk) != 0 ? 1u : 0u);
+            for (int kk = 0; kk < 4; ++kk)
+              if (!kTimingNoS)
+                sm100::umma_bf16(256u * t, qd + 2 * kk, kd + 2 * kk, idesc_s, (h | kk) != 0 ? 1u : 0u);
+          }
         }
-        sm100::umma_commit(&s_full[t]);
-        if (t == last_user(j)) sm100::umma_commit(&k_empty[st]);
-        if (j == (t == 0 ? x.e_t[0] : x.e_t[1]) - 1) sm100::umma_commit(&q_empty[t]);
+        __syncwarp();
+        if (sm100::elect_one()) {
+          sm100::umma_commit(&s_full[t]);
+          if (t == last_user(j)) sm100::umma_commit(&k_empty[st]);
+          if (j == (t == 0 ? x.e_t[0] : x.e_t[1]) - 1) sm100::umma_commit(&q_empty[t]);
+        }
+        __syncwarp();
       };
       auto mma_pv = [&](int t, int j) {
         const std::uint32_t vn = kbase + static_cast<std::uint32_t>(j - x.jb);
         const int st = static_cast<int>(vn % SV);
         sm100::mbar_wait(&v_full[st], (vn / SV) & 1);
-        sm100::mbar_wait(&p_full[t], pn[t] & 1);
+        if (!kTimingNoPWait) sm100::mbar_wait(&p_full[t], pn[t] & 1);
         ++pn[t];
         sm100::tc_fence_after();
         std::uint8_t* v = sV + st * C::kVBytes;
+        if (sm100::elect_one()) {
 #pragma unroll
-        for (int a = 0; a < 2; ++a) {
-          const std::uint64_t vd = sm100::sw128_kmajor_desc(sm100::smem_u32(v + a * C::kVAtom));
+          for (int a = 0; a < 2; ++a) {
+            const std::uint64_t vd = sm100::sw128_kmajor_desc(sm100::smem_u32(v + a * C::kVAtom));
 #pragma unroll
-          for (int kk = 0; kk < 4; ++kk)
-            sm100::umma_bf16_ts(tmem + 256 * t + 128, tmem + 256 * t + 32 * a + 8 * kk, vd + 2 * kk,
-                                idesc_o, (j > x.jb || (a | kk) != 0) ? 1u : 0u);
+            for (int kk = 0; kk < 4; ++kk)
+              if (!kTimingNoPv)
+                sm100::umma_bf16_ts(256u * t + 128, 256u * t + 32 * a + 8 * kk, vd + 2 * kk, idesc_o,
+                                    (j > x.jb || (a | kk) != 0) ? 1u : 0u);
+          }
         }
-        if (t == last_user(j)) sm100::umma_commit(&v_empty[st]);
-        if (j == (t == 0 ? x.e_t[0] : x.e_t[1]) - 1) sm100::umma_commit(&o_final[t]);
+        __syncwarp();
+        if (sm100::elect_one()) {
+          if (t == last_user(j)) sm100::umma_commit(&v_empty[st]);
+          if (j == (t == 0 ? x.e_t[0] : x.e_t[1]) - 1) sm100::umma_commit(&o_final[t]);
+        }
+        __syncwarp();
       };
       if (x.e_t[0] > x.jb) mma_s(0, x.jb);
       if (x.e_t[1] > x.jb) mma_s(1, x.jb);
@@ -740,6 +819,12 @@ __global__ void __launch_bounds__(kPpThreads, 1)
         sm100::mbar_wait(&s_full[t], sn & 1);
         ++sn;
         sm100::tc_fence_after();
+        if constexpr (kTimingSkipSoftmax) {  // dev timing: pipeline floor (P = raw S bits)
+          sm100::tc_fence_before();
+          __syncwarp();
+          if (lane == 0) sm100::mbar_arrive(&p_full[t]);
+          continue;
+        }
         const int key0 = x.key_begin + j * 128;
         const int c_lo = lo - key0, c_hi = hi - key0;  // visible columns [c_lo, c_hi)
         std::uint32_t sv[128];
@@ -793,8 +878,10 @@ __global__ void __launch_bounds__(kPpThreads, 1)
                                               __uint_as_float(sv[32 * c + 2 * q + 1])),
                                   scale2, mneg2);
             float2 e;
-            if ((q & 3) == 3) {  // every 4th pair on the FMA pipe
+            if (kPolyEvery > 0 && q % kPolyEvery == kPolyEvery - 1) {  // every 4th pair on the FMA pipe
               e = poly_exp2_fma2(x);
+            } else if (kTimingNoExp) {
+              e = x;
             } else {
               e.x = fast_exp2(x.x);
               e.y = fast_exp2(x.y);
@@ -806,7 +893,8 @@ __global__ void __launch_bounds__(kPpThreads, 1)
         }
         sm100::tmem_st_wait();
         sm100::tc_fence_before();
-        sm100::mbar_arrive(&p_full[t]);
+        __syncwarp();  // the warp's P stores are complete
+        if (lane == 0) sm100::mbar_arrive(&p_full[t]);
         const float2 r01 = add2(rs2[0], rs2[1]), r23 = add2(rs2[2], rs2[3]);
         const float2 rsum = add2(r01, r23);
         l = l * alpha + (rsum.x + rsum.y);
@@ -815,7 +903,7 @@ __global__ void __launch_bounds__(kPpThreads, 1)
       ++on;
       sm100::tc_fence_after();
       if constexpr (MODE == KvMode::kPaged) {
-        if (p.kv_splits > 1) {  // unnormalised partial + (m, l) for pp_merge_kernel
+        if (x.splits > 1) {  // unnormalised partial + (m, l) for pp_merge_kernel
           const std::int64_t prow = static_cast<std::int64_t>(x.ws_unit) * 256 + 128 * t + r;
           float4* po = reinterpret_cast<float4*>(p.part_o + prow * HD);
 #pragma unroll
@@ -865,30 +953,35 @@ __global__ void __launch_bounds__(kPpThreads, 1)
   }
 }
 
-// Split-KV merge: one warp per (work item, head, query row), splits combined
-// in index order (deterministic): O = sum_s 2^(m_s - M) O_s / sum_s 2^(m_s - M) l_s.
-// Split s holds row q iff its range is non-empty and starts at or below q
-// (then key jb * 128 <= q is visible and m_s is finite).
+// Split-KV merge: one warp per (work item, head, query row) of the items
+// with S > 1, splits combined in index order (deterministic):
+// O = sum_s 2^(m_s - M) O_s / sum_s 2^(m_s - M) l_s. Split s holds row q iff
+// its range is non-empty and starts at or below q (then key jb * 128 <= q is
+// visible and m_s is finite).
 template <int HD>
-__global__ void __launch_bounds__(256) pp_merge_kernel(const TcParams p) {
+__global__ void __launch_bounds__(256) pp_merge_kernel(const __grid_constant__ TcParams p) {
   pdl_wait();
   pdl_launch_dependents();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int wh = blockIdx.x;
   const int w = wh / p.q_heads, head = wh - w * p.q_heads;
+  const int2 sp = p.item_split[w];
+  const int S = sp.x;
+  if (S <= 1) return;
   const int row = blockIdx.y * 8 + warp;
-  const PrefillWork wk = p.work[w];
-  if (row >= wk.q_rows) return;
-  const int q = wk.q_pos0 + row;
-  const int n_tiles = (wk.q_pos0 + wk.q_rows + 127) / 128;
-  const int S = p.kv_splits;
-  const std::int64_t row0 = static_cast<std::int64_t>(wh) * S * 256 + row;  // split s: + s * 256
+  const int4 wk = p.inl[w];  // PrefillWork
+  if (row >= wk.y) return;
+  const int q = wk.z + row;
+  const int n_tiles = (wk.z + wk.y + 127) / 128;
+  auto prow = [&](int s) {  // workspace row of split s
+    return (static_cast<std::int64_t>(sp.y + s) * p.q_heads + head) * 256 + row;
+  };
   const float2* ml = reinterpret_cast<const float2*>(p.part_ml);
   float M = -INFINITY;
   for (int s = 0; s < S; ++s) {
     int jb, je;
     kv_split_range(n_tiles, S, s, jb, je);
-    if (je > jb && q >= jb * 128) M = fmaxf(M, ml[row0 + s * 256].x);
+    if (je > jb && q >= jb * 128) M = fmaxf(M, ml[prow(s)].x);
   }
   constexpr int kPer = HD / 32;
   float acc[kPer];
@@ -899,10 +992,10 @@ __global__ void __launch_bounds__(256) pp_merge_kernel(const TcParams p) {
     int jb, je;
     kv_split_range(n_tiles, S, s, jb, je);
     if (!(je > jb && q >= jb * 128)) continue;
-    const float2 v = ml[row0 + s * 256];
+    const float2 v = ml[prow(s)];
     const float wgt = exp2f(v.x - M);
     L += wgt * v.y;
-    const float* po = p.part_o + (row0 + s * 256) * HD + lane * kPer;
+    const float* po = p.part_o + prow(s) * HD + lane * kPer;
     if constexpr (kPer == 4) {
       const float4 o = *reinterpret_cast<const float4*>(po);
       acc[0] += wgt * o.x;
@@ -916,7 +1009,7 @@ __global__ void __launch_bounds__(256) pp_merge_kernel(const TcParams p) {
     }
   }
   const float inv = L > 0.f ? 1.f / L : 0.f;
-  bf16* orow = p.out + static_cast<std::int64_t>(wk.q_row0 + row) * p.ld_out + head * p.out_hd + lane * kPer;
+  bf16* orow = p.out + static_cast<std::int64_t>(wk.x + row) * p.ld_out + head * p.out_hd + lane * kPer;
   if constexpr (kPer == 4)
     *reinterpret_cast<uint2*>(orow) = make_uint2(pack_bf16x2(acc[0] * inv, acc[1] * inv),
                                                  pack_bf16x2(acc[2] * inv, acc[3] * inv));
@@ -1002,10 +1095,10 @@ void launch(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
   dim3 grid(p.q_heads, n_blocks);
   const int tok = prof::begin(st);
   if (attn_unit_rows() == 256) {
-    const int units = p.q_heads * n_blocks * p.kv_splits;
+    const int units = p.q_heads * p.n_pieces;
     launch_kernel(fa_pp_kernel<HD, MODE>, dim3(std::min(units, kNumSMs)), dim3(kPpThreads), PpCfg<HD>::kSmem,
                   st, 1, tq, tk, tv, p, units);
-    if (p.kv_splits > 1) {
+    if (p.max_split > 1) {
       launch_kernel(pp_merge_kernel<HD>, dim3(p.q_heads * n_blocks, 256 / 8), dim3(256), 0, st, 1, p);
       count_launch();
     }
@@ -1013,7 +1106,14 @@ void launch(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
   else
     launch_kernel(fa_tc_kernel<HD, MODE>, grid, dim3(kTcThreads), TcCfg<HD>::kSmem, st, 1, tq, tk, tv, p);
   RS_LAUNCH_CHECK();
-  prof::end(tok, st, klass, 0, 0);
+  if (tok >= 0 && MODE == KvMode::kPaged) {
+    // per-shape class "attn_prefill_tcgen05|items|max_keys|splits" (bench groups on the prefix)
+    char label[96];
+    std::snprintf(label, sizeof label, "%s|%d|%d|%d", klass, n_blocks, p.max_keys, p.n_pieces);
+    prof::end(tok, st, label, 0, 0);
+  } else {
+    prof::end(tok, st, klass, 0, 0);
+  }
   count_launch();
 }
 
@@ -1027,41 +1127,179 @@ int attn_unit_rows() {
   return rows;
 }
 
-int prefill_kv_splits(int units, int max_keys) {
-  const char* e = std::getenv("RS_ATTN_KV_SPLITS");  // A/B and tests: force a split count
-  if (e != nullptr && e[0] != '\0') return std::max(1, std::min(16, std::atoi(e)));
-  if (max_keys <= 0 || units >= kNumSMs || attn_unit_rows() != 256) return 1;
-  const int n_tiles = (max_keys + 127) / 128;
-  // fewest waves per unit of work: ceil(units * S / SMs) / S, each split
-  // keeping >= 4 key tiles (its Q load, epilogue and the merge amortised)
-  int best = 1;
-  double best_cost = 1.0;
-  for (int s = 2; s <= 8 && 4 * s <= n_tiles; ++s) {
-    const double cost = static_cast<double>((units * s + kNumSMs - 1) / kNumSMs) / s + 0.02 * s;
-    if (cost < best_cost) {
-      best_cost = cost;
-      best = s;
-    }
+// ---- piece planning (host) -------------------------------------------------
+// Cost of one (item, split) piece in (query tile, key tile) pairs plus a fixed
+// per-unit cost (Q load, pipeline fill, epilogue) and, for splits, the partial
+// write + merge; mirrors pp_unit's ranges.
+double piece_cost(const int4& it, bool paged, int S, int s) {
+  const int q_rows = it.y;
+  const int q_pos0 = paged ? it.z : 0;
+  const int key_begin = paged ? 0 : (it.z & ~7);
+  const int key_end = paged ? it.z + it.y : it.w;
+  const int rows_t[2] = {std::min(q_rows, 128), std::max(q_rows - 128, 0)};
+  int n_t[2];
+  for (int t = 0; t < 2; ++t) {
+    const int hi = paged ? q_pos0 + 128 * t + rows_t[t] : key_end;
+    n_t[t] = rows_t[t] > 0 ? (hi - key_begin + 127) / 128 : 0;
   }
-  return best;
+  int jb, je;
+  kv_split_range(std::max(n_t[0], n_t[1]), S, s, jb, je);
+  int pairs = 0;
+  for (int t = 0; t < 2; ++t) pairs += std::max(0, std::min(je, n_t[t]) - jb);
+  return pairs + 4.0 + (S > 1 ? 6.0 : 0.0);
+}
+
+struct PiecePlan {
+  std::vector<int4> items;  // cache key
+  int heads = 0;
+  bool paged = false;
+  int forced = 0;
+  std::vector<int4> pieces;
+  std::vector<int2> item_split;
+  int max_split = 1;
+};
+
+void build_pieces(PiecePlan& pl, const std::vector<int>& S, std::vector<double>* costs) {
+  struct P {
+    int4 pc;
+    double cost;
+  };
+  std::vector<P> ps;
+  const int n = static_cast<int>(pl.items.size());
+  pl.item_split.assign(static_cast<std::size_t>(n), make_int2(1, 0));
+  for (int w = 0; w < n; ++w)
+    for (int s = 0; s < S[w]; ++s)
+      ps.push_back({make_int4(w, s, S[w], 0), piece_cost(pl.items[w], pl.paged, S[w], s)});
+  std::stable_sort(ps.begin(), ps.end(), [](const P& a, const P& b) { return a.cost > b.cost; });
+  // each item's splits must be contiguous for the merge: order items by their
+  // largest piece, splits of an item adjacent
+  std::vector<int> first(static_cast<std::size_t>(n), -1);
+  std::vector<P> out;
+  for (const P& x : ps) {
+    const int w = x.pc.x;
+    if (first[w] >= 0) continue;
+    first[w] = static_cast<int>(out.size());
+    for (int s = 0; s < S[w]; ++s)
+      out.push_back({make_int4(w, s, S[w], first[w]), piece_cost(pl.items[w], pl.paged, S[w], s)});
+    pl.item_split[w] = make_int2(S[w], first[w]);
+  }
+  pl.pieces.clear();
+  if (costs) costs->clear();
+  pl.max_split = 1;
+  for (const P& x : out) {
+    pl.pieces.push_back(x.pc);
+    if (costs) costs->push_back(x.cost);
+    pl.max_split = std::max(pl.max_split, x.pc.z);
+  }
+}
+
+// Longest CTA of the kernel's snake dealing (grid = min(units, SMs)).
+double snake_makespan(const std::vector<double>& cost, int heads) {
+  const int units = static_cast<int>(cost.size()) * heads;
+  const int G = std::min(units, kNumSMs);
+  std::vector<double> load(static_cast<std::size_t>(G), 0.0);
+  for (int u = 0; u < units; ++u) {
+    const int r = u / G, i = u - r * G;
+    load[static_cast<std::size_t>((r & 1) ? G - 1 - i : i)] += cost[static_cast<std::size_t>(u / heads)];
+  }
+  return *std::max_element(load.begin(), load.end());
+}
+
+// Pieces of a launch: no split for kVarlen; for kPaged, items are split
+// greedily (the item owning the costliest piece first, up to 8 ways, >= 2 key
+// tiles per split) while that shortens the snake makespan. Cached: the 28
+// layers of a chunk plan the same list.
+const PiecePlan& plan_pieces(const int4* items, int n, int heads, bool paged) {
+  static thread_local PiecePlan pl;
+  int forced = 0;
+  if (paged) {
+    const char* e = std::getenv("RS_ATTN_KV_SPLITS");  // A/B and tests: every item split S ways
+    if (e != nullptr && e[0] != '\0') forced = std::max(1, std::min(16, std::atoi(e)));
+  }
+  const bool same = pl.heads == heads && pl.paged == paged && pl.forced == forced &&
+                    static_cast<int>(pl.items.size()) == n &&
+                    std::memcmp(pl.items.data(), items, static_cast<std::size_t>(n) * sizeof(int4)) == 0;
+  if (same) return pl;
+  pl.items.assign(items, items + n);
+  pl.heads = heads;
+  pl.paged = paged;
+  pl.forced = forced;
+  std::vector<int> S(static_cast<std::size_t>(n), 1);
+  std::vector<double> cost;
+  if (forced > 0) {
+    std::fill(S.begin(), S.end(), std::max(1, std::min(forced, kMaxPieces / std::max(1, n))));
+    build_pieces(pl, S, nullptr);
+    return pl;
+  }
+  build_pieces(pl, S, &cost);
+  if (!paged || attn_unit_rows() != 256) return pl;
+  double best = snake_makespan(cost, heads);
+  for (int iter = 0; iter < 64; ++iter) {
+    bool improved = false;
+    // candidates: the items of the three costliest pieces
+    std::vector<int> cand;
+    for (const int4& pc : pl.pieces) {
+      if (std::find(cand.begin(), cand.end(), pc.x) == cand.end()) cand.push_back(pc.x);
+      if (cand.size() == 3) break;
+    }
+    for (int w : cand) {
+      const int4& it = pl.items[static_cast<std::size_t>(w)];
+      const int n_tiles = (it.z + it.y + 127) / 128;
+      if (S[w] >= 8 || n_tiles < 2 * (S[w] + 1) || static_cast<int>(pl.pieces.size()) + 1 > kMaxPieces) continue;
+      ++S[w];
+      PiecePlan trial = pl;
+      std::vector<double> c2;
+      build_pieces(trial, S, &c2);
+      const double m = snake_makespan(c2, heads);
+      if (m < 0.97 * best) {  // clear gains only (the merge and partial writes are not free)
+        best = m;
+        pl.pieces = trial.pieces;
+        pl.item_split = trial.item_split;
+        pl.max_split = trial.max_split;
+        improved = true;
+        break;
+      }
+      --S[w];
+    }
+    if (!improved) break;
+  }
+  return pl;
+}
+
+void set_pieces(TcParams& p, const PiecePlan& pl) {
+  std::memcpy(p.pieces, pl.pieces.data(), pl.pieces.size() * sizeof(int4));
+  std::memcpy(p.item_split, pl.item_split.data(), pl.item_split.size() * sizeof(int2));
+  p.n_pieces = static_cast<int>(pl.pieces.size());
+  p.max_split = pl.max_split;
 }
 
 void attention_prefill_paged_tc(const bf16* q, int ld_q, int q_rows_alloc, bf16* out, int ld_out,
-                                const PrefillWork* work, int n_work, int max_keys, const PagedKV& kv,
-                                std::int64_t kv_pages, int q_heads, int kv_heads, int head_dim,
-                                float scale, cudaStream_t stream) {
+                                const PrefillWork* work, const PrefillWork* work_host, int n_work,
+                                int max_keys, const PagedKV& kv, std::int64_t kv_pages, int q_heads,
+                                int kv_heads, int head_dim, float scale, cudaStream_t stream) {
   if (n_work <= 0) return;
   if (kv.page_size != 64) throw DeviceError(RS_ERR_CUDA, "tc attention needs 64-token pages");
+  if (work_host == nullptr) throw DeviceError(RS_ERR_CUDA, "tc attention: host work list required");
+  if (n_work > kInlineUnits) {  // batches of inlined work items (independent rows)
+    for (int o = 0; o < n_work; o += kInlineUnits)
+      attention_prefill_paged_tc(q, ld_q, q_rows_alloc, out, ld_out, work + o, work_host + o,
+                                 std::min(kInlineUnits, n_work - o), max_keys, kv, kv_pages, q_heads,
+                                 kv_heads, head_dim, scale, stream);
+    return;
+  }
   TcParams p{};
-  p.kv_splits = attn_unit_rows() == 256 ? prefill_kv_splits(q_heads * n_work, max_keys) : 1;
-  if (p.kv_splits > 1) {
+  static_assert(sizeof(PrefillWork) == sizeof(int4), "inline work item layout");
+  std::memcpy(p.inl, work_host, static_cast<std::size_t>(n_work) * sizeof(int4));
+  set_pieces(p, plan_pieces(p.inl, n_work, q_heads, true));
+  p.max_keys = max_keys;
+  if (p.max_split > 1) {
     struct Ws {
       float* buf = nullptr;
       std::size_t floats = 0;
     };
     static thread_local std::unordered_map<cudaStream_t, Ws> ws_by_stream;
     Ws& ws = ws_by_stream[stream];
-    const std::size_t rows = static_cast<std::size_t>(n_work) * q_heads * p.kv_splits * 256;
+    const std::size_t rows = static_cast<std::size_t>(p.n_pieces) * q_heads * 256;
     const std::size_t need = rows * (head_dim + 2);
     if (ws.floats < need) {
       if (ws.buf != nullptr) RS_CUDA_CHECK(cudaFreeAsync(ws.buf, stream));
@@ -1092,12 +1330,21 @@ void attention_prefill_paged_tc(const bf16* q, int ld_q, int q_rows_alloc, bf16*
 
 void attention_varlen_tc(const bf16* qp, const bf16* kp, const bf16* vt, int rows_alloc,
                          int heads, bf16* out, int ld_out, int out_hd, const AttnBlock* blocks,
-                         int n_blocks, const int* cu_seqlens, int n_seqs, float scale,
-                         cudaStream_t stream) {
+                         const AttnBlock* blocks_host, int n_blocks, const int* cu_seqlens, int n_seqs,
+                         float scale, cudaStream_t stream) {
   if (n_blocks <= 0) return;
+  if (blocks_host == nullptr) throw DeviceError(RS_ERR_CUDA, "tc attention: host block list required");
+  if (n_blocks > kInlineUnits) {
+    for (int o = 0; o < n_blocks; o += kInlineUnits)
+      attention_varlen_tc(qp, kp, vt, rows_alloc, heads, out, ld_out, out_hd, blocks + o, blocks_host + o,
+                          std::min(kInlineUnits, n_blocks - o), cu_seqlens, n_seqs, scale, stream);
+    return;
+  }
   constexpr int HD = 128;
   TcParams p{};
-  p.kv_splits = 1;
+  static_assert(sizeof(AttnBlock) == sizeof(int4), "inline block layout");
+  std::memcpy(p.inl, blocks_host, static_cast<std::size_t>(n_blocks) * sizeof(int4));
+  set_pieces(p, plan_pieces(p.inl, n_blocks, heads, false));
   p.blocks = blocks;
   p.cu_seqlens = cu_seqlens;
   p.n_seqs = n_seqs;

@@ -98,7 +98,7 @@ rs_status rs_op_attention_varlen_tc(const void* qkv, int ld_qkv, void* out, int 
     RS_CUDA_CHECK(cudaFreeAsync(table, st));
     attention_varlen_tc(static_cast<bf16*>(qp), static_cast<bf16*>(kp), static_cast<bf16*>(vt),
                         rows_alloc, heads, static_cast<bf16*>(out), ld_out, head_dim,
-                        static_cast<const AttnBlock*>(bd), static_cast<int>(blocks.size()),
+                        static_cast<const AttnBlock*>(bd), blocks.data(), static_cast<int>(blocks.size()),
                         cu_seqlens, n_seqs, scale, st);
     RS_CUDA_CHECK(cudaStreamSynchronize(st));
     for (void* p : {qp, kp, vt, pos, bd}) RS_CUDA_CHECK(cudaFreeAsync(p, st));
@@ -126,7 +126,7 @@ rs_status rs_op_attention_prefill(const void* q, int ld_q, int rows_alloc, void*
     PagedKV kv{const_cast<bf16*>(static_cast<const bf16*>(k_cache)),
                const_cast<bf16*>(static_cast<const bf16*>(v_cache)), ptd, 64};
     attention_prefill_paged_tc(static_cast<const bf16*>(q), ld_q, rows_alloc, static_cast<bf16*>(out),
-                               ld_out, wd, static_cast<int>(work.size()), q_pos0 + q_rows, kv, kv_pages, q_heads,
+                               ld_out, wd, work.data(), static_cast<int>(work.size()), q_pos0 + q_rows, kv, kv_pages, q_heads,
                                kv_heads, head_dim, scale, st);
     RS_CUDA_CHECK(cudaStreamSynchronize(st));  // host vectors above go out of scope
     RS_CUDA_CHECK(cudaFreeAsync(wd, st));

@@ -446,6 +446,7 @@ void Context::prefill(const std::vector<SliceRef>& slices, bf16* x, cudaStream_t
   c.rows = static_cast<const ChunkRowInfo*>(up_.put(rows.data(), rows.size() * sizeof(ChunkRowInfo), st));
   if (first) c.gather_rows = static_cast<const std::int64_t*>(up_.put(gather.data(), gather.size() * 8, st));
   c.work = static_cast<const PrefillWork*>(up_.put(work.data(), work.size() * sizeof(PrefillWork), st));
+  c.work_host = work.data();
   c.n_work = static_cast<int>(work.size());
   c.max_keys = work.empty() ? 0 : work.front().q_pos0 + work.front().q_rows;  // sorted: most keys first
   if (llm_->has_head() && l_to == llm_->layer_end() && !done_rows.empty()) {
@@ -551,6 +552,7 @@ double Context::decode(const std::vector<lmmsim::RequestId>& ids, int steps, std
     c.M = n;
     c.rows = static_cast<const ChunkRowInfo*>(up_.put(info.data(), info.size() * sizeof(ChunkRowInfo), st));
     c.work = static_cast<const PrefillWork*>(up_.put(work.data(), work.size() * sizeof(PrefillWork), st));
+    c.work_host = work.data();
     c.n_work = n;
     c.done_rows = rows_idx;
     c.done_slots = slots_dev;

@@ -236,7 +236,7 @@ void Vit::encode(const VitBatchPlan& plan, const bf16* patches, const std::int32
       // and transposed v (long sequences, tensor-bound)
       vit_qkv_split(qkv_, 3 * s.vd, rope_table_, P, s.vh, s.vhd, qp_, kp_, vt_, max_p_, st);
       attention_varlen_tc(qp_, kp_, vt_, max_p_, s.vh, att_, s.vd, s.vhd, full_blocks,
-                          static_cast<int>(plan.full_blocks.size()), cu_item, n_items, scale, st);
+                          plan.full_blocks.data(), static_cast<int>(plan.full_blocks.size()), cu_item, n_items, scale, st);
     } else {
       // 8x8-patch windows (<= 64 keys): latency-bound tiles; the register-
       // tiled kernel reads qkv in place (no padding / transpose pass)
@@ -431,7 +431,7 @@ void Llm::forward_stage(const ChunkDev& c, const bf16* slab, bf16* x,
       attention_decode_paged(qkv_, s.qkv_dim, att_, s.hq * s.hd, c.work, c.n_work, c.max_keys, kv, s.hq,
                              s.hkv, s.hd, scale, st);
     else
-      attention_prefill_paged_tc(qkv_, s.qkv_dim, max_m_, att_, s.hq * s.hd, c.work, c.n_work, c.max_keys, kv,
+      attention_prefill_paged_tc(qkv_, s.qkv_dim, max_m_, att_, s.hq * s.hd, c.work, c.work_host, c.n_work, c.max_keys, kv,
                                  kv_pages_, s.hq, s.hkv, s.hd, scale, st);
     g = GemmArgs{};
     g.A = att_; g.lda = s.hq * s.hd; g.B = L.o_w; g.ldb = s.hq * s.hd; g.C = x; g.ldc = s.d;
@@ -514,7 +514,7 @@ void Llm::tp_attn_partial(int l, const ChunkDev& c, const bf16* slab, bf16* x, b
     attention_decode_paged(qkv_, s.qkv_dim, att_, s.hq * s.hd, c.work, c.n_work, c.max_keys, kv, s.hq,
                            s.hkv, s.hd, scale, st);
   else
-    attention_prefill_paged_tc(qkv_, s.qkv_dim, max_m_, att_, s.hq * s.hd, c.work, c.n_work, c.max_keys, kv,
+    attention_prefill_paged_tc(qkv_, s.qkv_dim, max_m_, att_, s.hq * s.hd, c.work, c.work_host, c.n_work, c.max_keys, kv,
                                kv_pages_, s.hq, s.hkv, s.hd, scale, st);
   g = GemmArgs{};
   g.A = att_; g.lda = s.hq * s.hd; g.B = L.o_w; g.ldb = s.hq * s.hd; g.C = part; g.ldc = s.d;

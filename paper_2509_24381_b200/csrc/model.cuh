@@ -129,6 +129,7 @@ struct ChunkDev {
   const ChunkRowInfo* rows = nullptr;
   const std::int64_t* gather_rows = nullptr;  // slab rows (first stage)
   const PrefillWork* work = nullptr;
+  const PrefillWork* work_host = nullptr;  // same list on the host (alive during the launches)
   int n_work = 0;
   int M = 0;
   const std::int64_t* done_rows = nullptr;    // chunk rows that end a prompt

@@ -38,6 +38,17 @@ __device__ __forceinline__ void mbar_wait(std::uint64_t* bar, std::uint32_t pari
       : "memory");
 }
 
+// One lane of the (converged) warp: true on the elected lane.
+__device__ __forceinline__ bool elect_one() {
+  std::uint32_t pred = 0;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "elect.sync _|p, 0xffffffff;\n\t"
+      "selp.u32 %0, 1, 0, p;\n}"
+      : "=r"(pred));
+  return pred != 0;
+}
+
 // ---- TMA -----------------------------------------------------------------
 __device__ __forceinline__ void tma_prefetch_desc(const CUtensorMap* tm) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(tm) : "memory");
