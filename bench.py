@@ -82,7 +82,12 @@ class ClockSampler:
             p.terminate()
         self._t = threading.Thread(target=run, daemon=True)
         self._t.start()
-        time.sleep(0.3)
+        # nvidia-smi's NVML start-up takes driver locks that can stall CUDA
+        # calls for ~100 ms: let it reach its first sample before timing
+        t0 = time.time()
+        while not self.samples and time.time() - t0 < 5.0:
+            time.sleep(0.05)
+        time.sleep(0.2)
         return self
 
     def __exit__(self, *a):
