@@ -25,6 +25,9 @@ def main():
     shapes = SHAPES
     if len(sys.argv) > 1 and sys.argv[1] == "--quick":
         shapes = SHAPES[:4] + SHAPES[7:11]
+    if len(sys.argv) > 1 and sys.argv[1] == "--small-m":  # the first / last prefill chunks
+        shapes = [(m, n, k, e) for m in (256, 128)
+                  for n, k, e in ((4608, 3584, 0), (3584, 3584, 1), (37888, 3584, 2), (3584, 18944, 1))]
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     st = torch.cuda.current_stream()
     res = []
