@@ -977,6 +977,14 @@ int cg_override() {
 TileChoice pick_tile(int M, int N, int K, bool swiglu, int tile_multiple = 0) {
   static constexpr int kCandidates[] = {256, 224, 192, 160, 128};
   const int num_kb = ceil_div(K, kBK);
+  // first / last prefill chunks (M <= 256): few tiles, weight-streaming and
+  // latency bound; measured fastest with the most 128 x 128 tiles (+ split-K
+  // on long K) except SwiGLU (scripts/gemm_sweep.py --small-m)
+  static const bool small_m_rule = [] {  // RS_GEMM_SMALLM=0: A/B
+    const char* e = std::getenv("RS_GEMM_SMALLM");
+    return e == nullptr || e[0] != '0';
+  }();
+  if (small_m_rule && M <= 2 * kBM && !swiglu && N % 128 == 0 && cg_override() == 0) return {128, 1};
   TileChoice best{256, 1};
   double best_cost = -1;
   for (int cg = 1; cg <= 2; ++cg) {
