@@ -708,7 +708,10 @@ __global__ void __launch_bounds__(kPpThreads, 1)
     // allocation can only start at column 0: TMEM addresses are constants.
     if (tmem != 0) __trap();
     constexpr std::uint32_t idesc_s = sm100::idesc_bf16_f32(128, 128);
-    constexpr std::uint32_t idesc_o = sm100::idesc_bf16_f32(128, HD);
+    // head-padded inputs (ViT: hd 80 in 128-wide tiles): the zero columns need
+    // no MMA — S uses ceil(out_hd / 16) K steps, PV writes out_hd (rounded to 16) columns
+    const int k_steps = (p.out_hd + 15) / 16;
+    const std::uint32_t idesc_o = sm100::idesc_bf16_f32(128, min(HD, k_steps * 16));
     std::uint32_t qn[2] = {0, 0}, pn[2] = {0, 0};
     std::uint32_t kbase = 0;  // K / V tiles consumed before this unit
     for (int r = 0;; ++r) {
@@ -735,7 +738,7 @@ __global__ void __launch_bounds__(kPpThreads, 1)
             const std::uint64_t kd = sm100::sw128_kmajor_desc(sm100::smem_u32(k + h * kAtom));
 #pragma unroll
             for (int kk = 0; kk < 4; ++kk)
-              if (!kTimingNoS)
+              if (!kTimingNoS && 4 * h + kk < k_steps)
                 sm100::umma_bf16(256u * t, qd + 2 * kk, kd + 2 * kk, idesc_s, (h | kk) != 0 ? 1u : 0u);
           }
         }
@@ -927,6 +930,7 @@ __global__ void __launch_bounds__(kPpThreads, 1)
       bf16* orow = p.out + static_cast<std::int64_t>(x.q_row0 + 128 * t + r) * p.ld_out + x.head * p.out_hd;
 #pragma unroll
       for (int c = 0; c < HD / 32; ++c) {
+        if (32 * c >= p.out_hd) break;  // head padding (uniform)
         std::uint32_t v[32];
         sm100::tmem_ld_32x32b_x32(o_tm + 32 * c, v);
         sm100::tmem_ld_wait();
@@ -1210,16 +1214,25 @@ double snake_makespan(const std::vector<double>& cost, int heads) {
 // tiles per split) while that shortens the snake makespan. Cached: the 28
 // layers of a chunk plan the same list.
 const PiecePlan& plan_pieces(const int4* items, int n, int heads, bool paged) {
-  static thread_local PiecePlan pl;
+  // several live plans: the encoder's and the prefill's launches interleave
+  // on the host thread (a single entry would re-plan every prefill layer)
+  static thread_local std::vector<PiecePlan> cache;
   int forced = 0;
   if (paged) {
     const char* e = std::getenv("RS_ATTN_KV_SPLITS");  // A/B and tests: every item split S ways
     if (e != nullptr && e[0] != '\0') forced = std::max(1, std::min(16, std::atoi(e)));
   }
-  const bool same = pl.heads == heads && pl.paged == paged && pl.forced == forced &&
-                    static_cast<int>(pl.items.size()) == n &&
-                    std::memcmp(pl.items.data(), items, static_cast<std::size_t>(n) * sizeof(int4)) == 0;
-  if (same) return pl;
+  for (std::size_t i = 0; i < cache.size(); ++i) {
+    const PiecePlan& c = cache[i];
+    if (c.heads == heads && c.paged == paged && c.forced == forced && static_cast<int>(c.items.size()) == n &&
+        std::memcmp(c.items.data(), items, static_cast<std::size_t>(n) * sizeof(int4)) == 0) {
+      if (i != 0) std::swap(cache[0], cache[i]);  // most recent first
+      return cache[0];
+    }
+  }
+  if (cache.size() >= 16) cache.pop_back();
+  cache.insert(cache.begin(), PiecePlan{});
+  PiecePlan& pl = cache[0];
   pl.items.assign(items, items + n);
   pl.heads = heads;
   pl.paged = paged;
@@ -1232,36 +1245,25 @@ const PiecePlan& plan_pieces(const int4* items, int n, int heads, bool paged) {
     return pl;
   }
   build_pieces(pl, S, &cost);
-  if (!paged || attn_unit_rows() != 256) return pl;
+  // host cost matters (planned once per chunk, on the launch path): only
+  // launches of at most two waves are planned, one candidate per step
+  if (!paged || attn_unit_rows() != 256 || n * heads > 2 * kNumSMs) return pl;
   double best = snake_makespan(cost, heads);
-  for (int iter = 0; iter < 64; ++iter) {
-    bool improved = false;
-    // candidates: the items of the three costliest pieces
-    std::vector<int> cand;
-    for (const int4& pc : pl.pieces) {
-      if (std::find(cand.begin(), cand.end(), pc.x) == cand.end()) cand.push_back(pc.x);
-      if (cand.size() == 3) break;
-    }
-    for (int w : cand) {
-      const int4& it = pl.items[static_cast<std::size_t>(w)];
-      const int n_tiles = (it.z + it.y + 127) / 128;
-      if (S[w] >= 8 || n_tiles < 2 * (S[w] + 1) || static_cast<int>(pl.pieces.size()) + 1 > kMaxPieces) continue;
-      ++S[w];
-      PiecePlan trial = pl;
-      std::vector<double> c2;
-      build_pieces(trial, S, &c2);
-      const double m = snake_makespan(c2, heads);
-      if (m < 0.97 * best) {  // clear gains only (the merge and partial writes are not free)
-        best = m;
-        pl.pieces = trial.pieces;
-        pl.item_split = trial.item_split;
-        pl.max_split = trial.max_split;
-        improved = true;
-        break;
-      }
-      --S[w];
-    }
-    if (!improved) break;
+  PiecePlan trial = pl;
+  std::vector<double> c2;
+  for (int iter = 0; iter < 16; ++iter) {
+    const int w = pl.pieces.front().x;  // the item owning the costliest piece
+    const int4& it = pl.items[static_cast<std::size_t>(w)];
+    const int n_tiles = (it.z + it.y + 127) / 128;
+    if (S[w] >= 8 || n_tiles < 2 * (S[w] + 1) || static_cast<int>(pl.pieces.size()) + 1 > kMaxPieces) break;
+    ++S[w];
+    build_pieces(trial, S, &c2);
+    const double m = snake_makespan(c2, heads);
+    if (!(m < 0.97 * best)) break;  // clear gains only (the merge and partial writes are not free)
+    best = m;
+    pl.pieces.swap(trial.pieces);
+    pl.item_split.swap(trial.item_split);
+    pl.max_split = trial.max_split;
   }
   return pl;
 }
