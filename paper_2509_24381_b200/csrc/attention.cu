@@ -8,6 +8,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <mutex>
 #include <unordered_map>
 
 #include "attention.cuh"
@@ -496,6 +497,14 @@ struct DecodeWs {
   float* buf = nullptr;
   std::size_t floats = 0;
 };
+std::mutex& decode_ws_mutex() {
+  static std::mutex mu;
+  return mu;
+}
+std::unordered_map<cudaStream_t, DecodeWs>& decode_ws_all() {  // per stream, released with it
+  static std::unordered_map<cudaStream_t, DecodeWs> all;
+  return all;
+}
 
 }  // namespace
 
@@ -514,8 +523,8 @@ void attention_decode_paged(const bf16* qkv, int ld_q, bf16* out, int ld_out, co
   splits = std::min(splits, max_tiles);
   const int tiles_per_split = (max_tiles + splits - 1) / splits;
   splits = (max_tiles + tiles_per_split - 1) / tiles_per_split;
-  static thread_local std::unordered_map<cudaStream_t, DecodeWs> ws_by_stream;
-  DecodeWs& ws = ws_by_stream[st];
+  std::lock_guard<std::mutex> g(decode_ws_mutex());
+  DecodeWs& ws = decode_ws_all()[st];
   const std::size_t need = static_cast<std::size_t>(n_req) * q_heads * splits * (head_dim + 2);
   if (ws.floats < need) {
     if (ws.buf != nullptr) RS_CUDA_CHECK(cudaFreeAsync(ws.buf, st));
@@ -548,6 +557,15 @@ void attention_decode_paged(const bf16* qkv, int ld_q, bf16* out, int ld_out, co
   RS_LAUNCH_CHECK();
   prof::end(tok, st, "attn_decode", 0, 0);
   count_launch(2);
+}
+
+void attention_release_stream(cudaStream_t st) {
+  attention_tc_release_stream(st);
+  std::lock_guard<std::mutex> g(decode_ws_mutex());
+  auto it = decode_ws_all().find(st);
+  if (it == decode_ws_all().end()) return;
+  if (it->second.buf) cudaFreeAsync(it->second.buf, st);
+  decode_ws_all().erase(it);
 }
 
 }  // namespace rserve

@@ -79,4 +79,9 @@ void attention_prefill_paged_tc(const bf16* q, int ld_q, int q_rows_alloc, bf16*
                                 int max_keys, const PagedKV& kv, std::int64_t kv_pages, int q_heads,
                                 int kv_heads, int head_dim, float scale, cudaStream_t stream);
 
+/// Frees the per-stream attention workspaces (split-KV partials) of a stream
+/// that is about to be destroyed.
+void attention_tc_release_stream(cudaStream_t st);
+void attention_release_stream(cudaStream_t st);
+
 }  // namespace rserve

@@ -1131,6 +1131,20 @@ int attn_unit_rows() {
   return rows;
 }
 
+// split-KV workspace per stream (stream-ordered; released with the stream)
+struct PpWs {
+  float* buf = nullptr;
+  std::size_t floats = 0;
+};
+std::mutex& pp_ws_mutex() {
+  static std::mutex mu;
+  return mu;
+}
+std::unordered_map<cudaStream_t, PpWs>& pp_ws_all() {
+  static std::unordered_map<cudaStream_t, PpWs> all;
+  return all;
+}
+
 // ---- piece planning (host) -------------------------------------------------
 // Cost of one (item, split) piece in (query tile, key tile) pairs plus a fixed
 // per-unit cost (Q load, pipeline fill, epilogue) and, for splits, the partial
@@ -1292,15 +1306,14 @@ void attention_prefill_paged_tc(const bf16* q, int ld_q, int q_rows_alloc, bf16*
   TcParams p{};
   static_assert(sizeof(PrefillWork) == sizeof(int4), "inline work item layout");
   std::memcpy(p.inl, work_host, static_cast<std::size_t>(n_work) * sizeof(int4));
-  set_pieces(p, plan_pieces(p.inl, n_work, q_heads, true));
+  {
+    HostPhase ph("attn.plan");
+    set_pieces(p, plan_pieces(p.inl, n_work, q_heads, true));
+  }
   p.max_keys = max_keys;
   if (p.max_split > 1) {
-    struct Ws {
-      float* buf = nullptr;
-      std::size_t floats = 0;
-    };
-    static thread_local std::unordered_map<cudaStream_t, Ws> ws_by_stream;
-    Ws& ws = ws_by_stream[stream];
+    std::lock_guard<std::mutex> g(pp_ws_mutex());
+    PpWs& ws = pp_ws_all()[stream];
     const std::size_t rows = static_cast<std::size_t>(p.n_pieces) * q_heads * 256;
     const std::size_t need = rows * (head_dim + 2);
     if (ws.floats < need) {
@@ -1361,6 +1374,14 @@ void attention_varlen_tc(const bf16* qp, const bf16* kp, const bf16* vt, int row
   const CUtensorMap tk = cached_map(kp, rows_alloc, heads * HD, heads * HD, 128);
   const CUtensorMap tv = cached_map(vt, static_cast<std::int64_t>(heads) * HD, rows_alloc, rows_alloc, HD);
   launch<HD, KvMode::kVarlen>(tq, tk, tv, p, n_blocks, stream, "attn_vit_tcgen05");
+}
+
+void attention_tc_release_stream(cudaStream_t st) {
+  std::lock_guard<std::mutex> g(pp_ws_mutex());
+  auto it = pp_ws_all().find(st);
+  if (it == pp_ws_all().end()) return;
+  if (it->second.buf) cudaFreeAsync(it->second.buf, st);
+  pp_ws_all().erase(it);
 }
 
 }  // namespace rserve

@@ -36,6 +36,16 @@ std::uint64_t launches_so_far();
 
 // Optional live per-kernel-class timing (CUDA events on the launch stream),
 // enabled per engine run for bench.py's roofline figures.
+// RS_HOST_TRACE=<ms>: host phases (launch path) longer than <ms> are
+// reported on stderr with their label (diagnostics for launch-path stalls).
+double host_trace_ms();
+struct HostPhase {
+  const char* label;
+  std::chrono::steady_clock::time_point t0;
+  explicit HostPhase(const char* l) : label(l), t0(std::chrono::steady_clock::now()) {}
+  ~HostPhase();
+};
+
 namespace prof {
 bool enabled();
 void enable(bool on);

@@ -111,9 +111,19 @@ DeviceBackend::~DeviceBackend() {
   for (bf16* p : xbufs_) cudaFree(p);
   for (cudaEvent_t e : event_pool_) cudaEventDestroy(e);
   if (origin_) cudaEventDestroy(origin_);
+  auto release = [](cudaStream_t st) {  // per-stream kernel workspaces
+    gemm_release_stream(st);
+    attention_release_stream(st);
+  };
   if (!shared_streams_)
-    for (auto st : enc_streams_) cudaStreamDestroy(st);
-  for (auto st : stage_streams_) cudaStreamDestroy(st);
+    for (auto st : enc_streams_) {
+      release(st);
+      cudaStreamDestroy(st);
+    }
+  for (auto st : stage_streams_) {
+    release(st);
+    cudaStreamDestroy(st);
+  }
   if (copy_stream_) cudaStreamDestroy(copy_stream_);
   remote_ops_.clear();
   slot_xfer_.clear();
@@ -238,6 +248,7 @@ void DeviceBackend::note_call(int kind, double ms) {
 
 double DeviceBackend::launch_encode(int worker, std::size_t slot, const lmmsim::EncodeBatch& b) {
   CallTimer timer{this, 0};
+  HostPhase phase_("launch_encode");
   if (remote_ != nullptr) {
     launch_remote_encode(worker, slot, b);
     return realtime_ ? 0.0 : lmmsim::encode_time_ms(cfg_.cost, b);
@@ -270,7 +281,10 @@ double DeviceBackend::launch_encode(int worker, std::size_t slot, const lmmsim::
     patches = pay.patches_dev + p0 * s.pdim;
   }
   const VitBatchPlan plan = ctx_.plan_batch(r, items);
-  ctx_.encode(plan, patches, staging_[static_cast<std::size_t>(ring)], st);
+  {
+    HostPhase ph("launch_encode.ctx_encode");
+    ctx_.encode(plan, patches, staging_[static_cast<std::size_t>(ring)], st);
+  }
   RS_CUDA_CHECK(cudaEventRecord(end, st));
   slot_done_[slot] = end;
   last_encode_end_ = end;
@@ -292,6 +306,7 @@ double DeviceBackend::launch_transfer(int /*worker*/, std::size_t slot, const lm
 
 void DeviceBackend::on_embeddings_ready(std::size_t slot, const lmmsim::EncodeBatch& b) {
   CallTimer timer{this, 2};
+  HostPhase phase_("on_embeddings_ready");
   cudaStream_t st = ctx_.tracker_stream();
   if (remote_ != nullptr) remote_->t->wait_posted(*slot_xfer_.at(slot));
   RS_CUDA_CHECK(cudaStreamWaitEvent(st, slot_done_.at(slot), 0));
@@ -310,6 +325,7 @@ void DeviceBackend::on_embeddings_ready(std::size_t slot, const lmmsim::EncodeBa
 
 double DeviceBackend::launch_stage(int stage, const lmmsim::ChunkView& c) {
   CallTimer timer{this, 1};
+  HostPhase phase_("launch_stage");
   const double cost = realtime_ ? 0.0 : lmmsim::stage_time_ms(cfg_.cost, c.total_tokens, c.weighted_context);
   if (remote_ != nullptr && stage > 0) {  // runs on rank P_stage; completion = its DONE message
     for (RemoteOp& op : remote_ops_)
@@ -347,7 +363,10 @@ double DeviceBackend::launch_stage(int stage, const lmmsim::ChunkView& c) {
   const int from = lb + n * stage / S, to = lb + n * (stage + 1) / S;
   cudaEvent_t begin = timing_event(), end = timing_event();
   RS_CUDA_CHECK(cudaEventRecord(begin, st));
-  ctx_.prefill(slices, cs.x, st, from, to);
+  {
+    HostPhase ph("launch_stage.ctx_prefill");
+    ctx_.prefill(slices, cs.x, st, from, to);
+  }
   RS_CUDA_CHECK(cudaEventRecord(end, st));
   cs.last = end;
   if (stage == 0) cs.s0_end = end;

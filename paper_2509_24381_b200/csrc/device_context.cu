@@ -454,7 +454,11 @@ void Context::prefill(const std::vector<SliceRef>& slices, bf16* x, cudaStream_t
     c.done_slots = static_cast<const std::int32_t*>(up_.put(done_slots.data(), done_slots.size() * 4, st));
     c.n_done = static_cast<int>(done_rows.size());
   }
-  run_llm(c, slab_, x, st, l_from, l_to);
+  {
+    HostPhase ph("prefill.run_llm");
+    run_llm(c, slab_, x, st, l_from, l_to);
+  }
+  HostPhase ph("prefill.fence");
   up_.fence(st);
 }
 

@@ -77,6 +77,9 @@ void gemm(const GemmArgs& args, Epi epi, cudaStream_t stream, int force_bn = 0);
 /// Skinny GEMM for M <= 8 rows (decode) on the CUDA cores, same epilogues
 /// (gemv.cu). Returns false when the shape is not supported (caller falls
 /// back to the tcgen05 kernel). gemm() routes here by default.
+/// Frees the split-K workspace of a stream that is about to be destroyed.
+void gemm_release_stream(cudaStream_t st);
+
 bool gemv_small_m(const GemmArgs& args, Epi epi, cudaStream_t stream);
 
 }  // namespace rserve

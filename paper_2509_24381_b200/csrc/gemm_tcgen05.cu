@@ -813,20 +813,28 @@ CUtensorMap make_map(const void* base, bool f32, int rows, int cols, int ld, int
 
 // Stream-K workspace of one stream (GEMMs on a stream are serialised, so one
 // workspace per stream suffices): 2 partial slots per CTA + tile counters.
+// Stream-ordered allocation from the device pool (no host synchronisation on
+// the launch path); released with the stream (gemm_release_stream).
 struct SkWorkspace {
   float* ws = nullptr;
   int* counters = nullptr;
 };
 constexpr std::size_t kSkWsBytes = 64ull << 20;
-SkWorkspace& sk_workspace(cudaStream_t st) {
+std::mutex& sk_mutex() {
   static std::mutex mu;
+  return mu;
+}
+std::unordered_map<cudaStream_t, SkWorkspace>& sk_all() {
   static std::unordered_map<cudaStream_t, SkWorkspace> all;
-  std::lock_guard<std::mutex> g(mu);
-  SkWorkspace& w = all[st];
+  return all;
+}
+SkWorkspace& sk_workspace(cudaStream_t st) {
+  std::lock_guard<std::mutex> g(sk_mutex());
+  SkWorkspace& w = sk_all()[st];
   if (w.ws == nullptr) {
-    RS_CUDA_CHECK(cudaMalloc(&w.ws, kSkWsBytes));
-    RS_CUDA_CHECK(cudaMalloc(&w.counters, sizeof(int) * kNumSMs));
-    RS_CUDA_CHECK(cudaMemset(w.counters, 0, sizeof(int) * kNumSMs));
+    RS_CUDA_CHECK(cudaMallocAsync(reinterpret_cast<void**>(&w.ws), kSkWsBytes, st));
+    RS_CUDA_CHECK(cudaMallocAsync(reinterpret_cast<void**>(&w.counters), sizeof(int) * kNumSMs, st));
+    RS_CUDA_CHECK(cudaMemsetAsync(w.counters, 0, sizeof(int) * kNumSMs, st));
   }
   return w;
 }
@@ -1010,6 +1018,7 @@ TileChoice pick_tile(int M, int N, int K, bool swiglu, int tile_multiple = 0) {
 }  // namespace
 
 void gemm(const GemmArgs& a, Epi epi, cudaStream_t stream, int force_bn) {
+  HostPhase phase_("gemm");
   if (a.M <= 0 || a.N <= 0) return;
   if (a.K % 8 != 0 || a.N % 16 != 0 || a.lda % 8 != 0 || a.ldb % 8 != 0)
     throw DeviceError(RS_ERR_CUDA, "gemm: need K%8==0, N%16==0, lda/ldb%8==0 (K=" +
@@ -1054,6 +1063,15 @@ void gemm(const GemmArgs& a, Epi epi, cudaStream_t stream, int force_bn) {
                 static_cast<int>(epi), tc.bn, tc.cg);
   prof::end(tok, stream, label, 2.0 * m * n * k,
             2.0 * (m * k + n * k) + out_bytes * m * n + (epi == Epi::Residual ? 2.0 * m * n : 0.0));
+}
+
+void gemm_release_stream(cudaStream_t st) {
+  std::lock_guard<std::mutex> g(sk_mutex());
+  auto it = sk_all().find(st);
+  if (it == sk_all().end()) return;
+  if (it->second.ws) cudaFreeAsync(it->second.ws, st);
+  if (it->second.counters) cudaFreeAsync(it->second.counters, st);
+  sk_all().erase(it);
 }
 
 }  // namespace rserve

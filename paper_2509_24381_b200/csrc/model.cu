@@ -411,6 +411,7 @@ void Llm::forward_stage(const ChunkDev& c, const bf16* slab, bf16* x,
   const float inv_d = 1.0f / static_cast<float>(s.d);
   mrope_table(c.rows, M, s.hd, s.cfg.rope_theta_llm, rope_table_, st);  // shared by every layer
   for (int l = l_from; l < l_to; ++l) {
+    HostPhase ph("llm.layer");
     const LlmLayer& L = layers_[static_cast<std::size_t>(l - lb_)];
     g = GemmArgs{};
     if (l == l_from) {

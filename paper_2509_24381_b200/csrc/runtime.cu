@@ -1,3 +1,4 @@
+#include <cstdio>
 // rserve-b200 — process-wide runtime bits: launch counter, live kernel timing.
 #include <atomic>
 #include <cstdlib>
@@ -111,5 +112,20 @@ std::string drain() {
   return out;
 }
 }  // namespace prof
+
+double host_trace_ms() {
+  static const double v = [] {
+    const char* e = std::getenv("RS_HOST_TRACE");
+    return e != nullptr ? std::atof(e) : 0.0;
+  }();
+  return v;
+}
+
+HostPhase::~HostPhase() {
+  const double lim = host_trace_ms();
+  if (lim <= 0.0) return;
+  const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  if (ms > lim) std::fprintf(stderr, "[rs host] %s took %.2f ms\n", label, ms);
+}
 
 }  // namespace rserve
