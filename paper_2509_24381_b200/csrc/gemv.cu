@@ -16,7 +16,11 @@
 namespace rserve {
 namespace {
 
+#ifndef RS_GEMV_UNROLL
+#define RS_GEMV_UNROLL 2
+#endif
 constexpr int kRows = 4, kWarps = 8, kMaxM = 8;
+constexpr int kUnroll = RS_GEMV_UNROLL;  // k iterations in flight per thread
 
 __device__ __forceinline__ float gelu_erf_v(float x) { return 0.5f * x * (1.f + erff(x * 0.70710678118654752f)); }
 __device__ __forceinline__ float silu_v(float x) { return __fdividef(x, 1.f + __expf(-x)); }
@@ -36,10 +40,28 @@ template <int MM, int EPI>
 __global__ void __launch_bounds__(kWarps * 32) gemv_kernel(GemmArgs a) {
   constexpr bool kSwi = EPI == static_cast<int>(Epi::SwiGLU);
   __shared__ float part[kWarps][kRows][MM];
-  pdl_wait();
-  pdl_launch_dependents();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int b = blockIdx.x;
+  // The weights are not written by the kernels this one depends on: start
+  // pulling this thread's first k iterations into L2 before waiting on the
+  // previous kernel (PDL), so the stream overlaps its tail.
+#ifndef RS_GEMV_NO_PREFETCH
+  {
+    const int k8n0 = a.K / 8;
+#pragma unroll
+    for (int r = 0; r < kRows; ++r) {
+      const uint4* row = reinterpret_cast<const uint4*>(
+          a.B + static_cast<std::int64_t>(min(brow_of<EPI == static_cast<int>(Epi::SwiGLU)>(b, r), a.N - 1)) * a.ldb);
+#pragma unroll
+      for (int i = 0; i < kUnroll; ++i) {
+        const int k8 = warp * 32 + lane + i * kWarps * 32;
+        if (k8 < k8n0) asm volatile("prefetch.global.L2 [%0];" ::"l"(row + k8));
+      }
+    }
+  }
+#endif
+  pdl_wait();
+  pdl_launch_dependents();
   float acc[kRows][MM];
 #pragma unroll
   for (int r = 0; r < kRows; ++r)
@@ -51,7 +73,7 @@ __global__ void __launch_bounds__(kWarps * 32) gemv_kernel(GemmArgs a) {
   for (int r = 0; r < kRows; ++r)
     brow[r] = reinterpret_cast<const uint4*>(
         a.B + static_cast<std::int64_t>(min(brow_of<kSwi>(b, r), a.N - 1)) * a.ldb);
-#pragma unroll 2
+#pragma unroll kUnroll
   for (int k8 = warp * 32 + lane; k8 < k8n; k8 += kWarps * 32) {
     uint4 bv[kRows];
 #pragma unroll
