@@ -25,6 +25,7 @@ rs_status rs_op_gemm(const void* A, int lda, const void* B, int ldb, void* C, in
     a.lda = lda;
     a.B = static_cast<const bf16*>(B);
     a.ldb = ldb;
+    a.b_stable = false;
     a.C = C;
     a.ldc = ldc;
     a.bias = static_cast<const bf16*>(bias);

@@ -67,6 +67,10 @@ struct GemmArgs {
   bf16* k_cache = nullptr;
   bf16* v_cache = nullptr;
   int rope_hq = 0, rope_hkv = 0, rope_hd = 0, page_size = 0;
+  // B is not written by the kernels launched before this GEMM on its stream
+  // (model weights): its first tiles may load before the PDL wait. The
+  // public op (rs_op_gemm) clears it: there B may be a preceding op's output.
+  bool b_stable = true;
 };
 constexpr float kSsFixedScale = 65536.f;  // 2^16
 

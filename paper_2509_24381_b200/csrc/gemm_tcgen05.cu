@@ -53,6 +53,7 @@ struct GemmParams {
   bf16* k_cache;
   bf16* v_cache;
   int rope_hq, rope_hkv, rope_hd, page_size;
+  int early_b;   // issue the first ring's B tiles before the PDL wait (RS_GEMM_EARLY_B=0: off)
 };
 
 // Row scale of a norm-consumer GEMM (1 when the GEMM has no folded norm).
@@ -539,6 +540,27 @@ __global__ void __launch_bounds__(kThreads, 1)
   else __syncthreads();
   sm100::tc_fence_after();
   const std::uint32_t tmem_base = *tmem_holder;
+  // B (the weights) is never produced by the kernels this one depends on:
+  // the producer issues the first ring's B tiles before the PDL wait, so the
+  // weight stream starts under the previous kernel's tail; A follows the wait.
+  int pre_b = 0;  // leading k-blocks whose B (and expect_tx) were issued early
+  if (warp == 0 && lane == 0 && p.early_b) {
+    UnitIter it0 = sched.begin(unit0);
+    Unit u0;
+    if (sched.next(it0, u0)) {
+      const int n0 = (u0.tile / m_tiles) * BN + static_cast<int>(rank) * (BN / CG);
+      for (int kb = u0.kb0; kb < u0.kb1 && pre_b < C::kStages; ++kb, ++pre_b) {
+        if constexpr (CG == 2) {
+          if (rank == 0) sm100::mbar_expect_tx(&full[pre_b], 2 * C::kStageBytes);
+          const std::uint32_t fb = sm100::mapa(sm100::smem_u32(&full[pre_b]), 0);
+          sm100::tma_load_2d_cg2(smem_b + pre_b * C::kBBytes, &tmB, fb, kb * kBK, n0);
+        } else {
+          sm100::mbar_expect_tx(&full[pre_b], C::kStageBytes);
+          sm100::tma_load_2d(smem_b + pre_b * C::kBBytes, &tmB, &full[pre_b], kb * kBK, n0);
+        }
+      }
+    }
+  }
   // PDL: the setup above (barriers, TMEM, descriptor prefetch) overlapped the
   // previous kernel's tail; its outputs are visible from here on.
   pdl_wait();
@@ -556,16 +578,18 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int n0 = (u.tile / m_tiles) * BN + static_cast<int>(rank) * (BN / CG);
       for (int kb = u.kb0; kb < u.kb1; ++kb) {
         sm100::mbar_wait(&empty[stage], phase ^ 1);
+        const bool early = pre_b > 0;  // B + expect_tx already issued (first ring, first unit)
+        if (early) --pre_b;
         if constexpr (CG == 2) {
           // both CTAs' bytes complete on the leader's full barrier
-          if (rank == 0) sm100::mbar_expect_tx(&full[stage], 2 * C::kStageBytes);
+          if (rank == 0 && !early) sm100::mbar_expect_tx(&full[stage], 2 * C::kStageBytes);
           const std::uint32_t fb = sm100::mapa(sm100::smem_u32(&full[stage]), 0);
           sm100::tma_load_2d_cg2(smem_a + stage * C::kABytes, &tmA, fb, kb * kBK, m0);
-          sm100::tma_load_2d_cg2(smem_b + stage * C::kBBytes, &tmB, fb, kb * kBK, n0);
+          if (!early) sm100::tma_load_2d_cg2(smem_b + stage * C::kBBytes, &tmB, fb, kb * kBK, n0);
         } else {
-          sm100::mbar_expect_tx(&full[stage], C::kStageBytes);
+          if (!early) sm100::mbar_expect_tx(&full[stage], C::kStageBytes);
           sm100::tma_load_2d(smem_a + stage * C::kABytes, &tmA, &full[stage], kb * kBK, m0);
-          sm100::tma_load_2d(smem_b + stage * C::kBBytes, &tmB, &full[stage], kb * kBK, n0);
+          if (!early) sm100::tma_load_2d(smem_b + stage * C::kBBytes, &tmB, &full[stage], kb * kBK, n0);
         }
         if (++stage == C::kStages) {
           stage = 0;
@@ -918,6 +942,11 @@ void launch(const GemmArgs& a, cudaStream_t stream) {
                static_cast<const ChunkRowInfo*>(a.rope_rows), a.rope_table, a.page_tables, a.k_cache, a.v_cache,
                a.rope_hq, a.rope_hkv, a.rope_hd, a.page_size};
   if (const char* dbg = std::getenv("RS_GEMM_SK_DEBUG")) p.sk_debug = std::atoi(dbg);
+  static const int early_b = [] {
+    const char* e = std::getenv("RS_GEMM_EARLY_B");
+    return e != nullptr && e[0] == '0' ? 0 : 1;
+  }();
+  p.early_b = early_b && a.b_stable ? 1 : 0;
   const int tiles = ceil_div(a.M, kBM * CG) * ceil_div(a.N, BN);
   int grid = CG * (tiles < kNumSMs / CG ? tiles : kNumSMs / CG);
   // Tail split-K: the last, partial wave of whole tiles (R tiles) costs one
