@@ -461,6 +461,10 @@ constexpr int kPpThreads = 352;
 #define RS_PP_POLY_EVERY 4
 #endif
 constexpr int kPolyEvery = RS_PP_POLY_EVERY;  // exp2 pairs on the FMA pipe: 1 in kPolyEvery (0: none)
+#ifndef RS_PP_POLY_EVERY_VIT
+#define RS_PP_POLY_EVERY_VIT 4
+#endif
+constexpr int kPolyEveryVit = RS_PP_POLY_EVERY_VIT;  // kVarlen (ViT: fewer MMAs per key with hd 80)
 // dev timing builds only (wrong results): -DRS_PP_TIMING_NOEXP / -DRS_PP_TIMING_SKIP_SOFTMAX
 #ifdef RS_PP_TIMING_NOEXP
 constexpr bool kTimingNoExp = true;
@@ -881,7 +885,8 @@ __global__ void __launch_bounds__(kPpThreads, 1)
                                               __uint_as_float(sv[32 * c + 2 * q + 1])),
                                   scale2, mneg2);
             float2 e;
-            if (kPolyEvery > 0 && q % kPolyEvery == kPolyEvery - 1) {  // every 4th pair on the FMA pipe
+            constexpr int kPe = MODE == KvMode::kVarlen ? kPolyEveryVit : kPolyEvery;
+            if (kPe > 0 && q % kPe == kPe - 1) {  // every kPe-th pair on the FMA pipe
               e = poly_exp2_fma2(x);
             } else if (kTimingNoExp) {
               e = x;
