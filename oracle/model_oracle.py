@@ -8,11 +8,14 @@ window / full attention, SwiGLU MLP, 2x2 patch merger) and the decoder LLM
 
 PARITY STATUS: the reference (lmmsim) contains no model arithmetic at all
 ("Numerical parity is unpinned by the reference"), so this
-oracle is NOT pinned by reference golden vectors. It restates the public
-Qwen2.5-VL architecture; tests/test_model_oracle.py checks its
-self-consistency (chunked == unchunked prefill, encoder output independent
-of batch composition) and, where the `transformers` Qwen2 implementation is
-importable, its decoder layer against that independent implementation.
+oracle cannot be pinned by reference golden vectors. It restates the public
+Qwen2.5-VL architecture and is pinned to an independent implementation:
+tests/test_oracle_hf.py loads these weights into Hugging Face transformers'
+Qwen2.5-VL modules (v5.5: the whole vision tower incl. window permutation and
+patch merger, get_rope_index, the text model + LM head) at tiny size (full
+depth) and at 7B widths, and requires fp32 agreement to 1e-4 relative.
+tests/test_model_oracle.py adds self-consistency (chunked == unchunked
+prefill, encoder output independent of batch composition).
 
 Synthetic values reproduce the device generators bit for bit:
   u = splitmix64(seed * G + stream * H + i) >> 40, scaled to [0, 1) with
