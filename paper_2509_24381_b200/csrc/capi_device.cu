@@ -211,12 +211,18 @@ rs_status rs_encode(rs_ctx* c, const uint64_t* items, int32_t n_items, const voi
 rs_status rs_prefill_chunk(rs_ctx* c, const uint64_t* slices, int32_t n_slices) {
   return guarded([&] {
     rs_ctx& x = need(c);
+    // Validate every slice on scratch copies of the trackers first (frontier,
+    // readiness — the reference's DependencyViolation text — and the chunk
+    // size), so a rejected chunk leaves no tracker advanced.
+    std::unordered_map<lmmsim::RequestId, lmmsim::EmbeddingTracker> scratch;
     std::vector<SliceRef> refs;
     std::uint64_t total = 0;
     for (int i = 0; i < n_slices; ++i) {
       const lmmsim::RequestId id = slices[3 * i];
       const std::uint64_t b = slices[3 * i + 1], e = slices[3 * i + 2];
-      lmmsim::EmbeddingTracker& t = x.registry.get(id);
+      auto it = scratch.find(id);
+      if (it == scratch.end()) it = scratch.emplace(id, x.registry.get(id)).first;
+      lmmsim::EmbeddingTracker& t = it->second;
       if (b != t.prefilled_frontier() || e <= b)
         throw lmmsim::InternalError("rs_prefill_chunk: slice [" + lmmsim::format_u64(b) + "," +
                                     lmmsim::format_u64(e) + ") of request " +
@@ -227,6 +233,8 @@ rs_status rs_prefill_chunk(rs_ctx* c, const uint64_t* slices, int32_t n_slices) 
     }
     if (total > x.ctx->options().max_chunk_tokens)
       throw lmmsim::ConfigError("rs_prefill_chunk: chunk exceeds max_chunk_tokens");
+    for (int i = 0; i < n_slices; ++i)
+      x.registry.get(slices[3 * i]).advance_prefill(slices[3 * i + 2] - slices[3 * i + 1]);
     cudaStream_t st = x.ctx->aux_stream();
     RS_CUDA_CHECK(cudaStreamSynchronize(x.ctx->tracker_stream()));
     x.ctx->prefill(refs, x.manual_x, st);

@@ -60,8 +60,8 @@ DeviceBackend::DeviceBackend(Context& ctx, const lmmsim::SimConfig& cfg, bool re
     RS_CUDA_CHECK(cudaMalloc(&p, max_tok * s.d * sizeof(bf16)));
     staging_.push_back(static_cast<bf16*>(p));
     staging_free_.push_back(nullptr);
+    staging_busy_.push_back(false);
   }
-  enc_ring_pos_.assign(static_cast<std::size_t>(workers), 0);
   if (e2e_ && remote_ == nullptr) {
     for (int w = 0; w < workers; ++w) {
       void* p = nullptr;
@@ -239,6 +239,29 @@ struct CallTimer {
   ~CallTimer() { be->note_call(kind, std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count()); }
 };
 
+/// A staging buffer for one encode batch's embeddings, held from
+/// launch_encode until that batch's on_embeddings_ready has enqueued its
+/// scatter (the scatter's event then guards the next writer). Batches whose
+/// transfers are still outstanding keep theirs, so with more of them in
+/// flight than the initial ring holds (slow links, EP receives posted ahead)
+/// the pool grows instead of handing out a buffer that is still unread.
+int DeviceBackend::acquire_staging() {
+  const std::size_t n = staging_.size();
+  for (std::size_t k = 0; k < n; ++k) {
+    const std::size_t i = (staging_next_ + k) % n;
+    if (staging_busy_[i]) continue;
+    staging_busy_[i] = true;
+    staging_next_ = (i + 1) % n;
+    return static_cast<int>(i);
+  }
+  void* p = nullptr;
+  RS_CUDA_CHECK(cudaMalloc(&p, ctx_.options().max_encode_tokens * ctx_.shapes().d * sizeof(bf16)));
+  staging_.push_back(static_cast<bf16*>(p));
+  staging_free_.push_back(nullptr);
+  staging_busy_.push_back(true);
+  return static_cast<int>(staging_.size() - 1);
+}
+
 void DeviceBackend::note_call(int kind, double ms) {
   if (ms > stats_.host_max_call_ms) {
     stats_.host_max_call_ms = ms;
@@ -256,8 +279,7 @@ double DeviceBackend::launch_encode(int worker, std::size_t slot, const lmmsim::
   cudaStream_t st = enc_streams_[static_cast<std::size_t>(worker)];
   DevRequest& r = ctx_.get(b.request_id);
   const Shapes& s = ctx_.shapes();
-  const int ring = worker * kRing + enc_ring_pos_[static_cast<std::size_t>(worker)];
-  enc_ring_pos_[static_cast<std::size_t>(worker)] = (enc_ring_pos_[static_cast<std::size_t>(worker)] + 1) % kRing;
+  const int ring = acquire_staging();
   if (staging_free_[static_cast<std::size_t>(ring)] != nullptr)
     RS_CUDA_CHECK(cudaStreamWaitEvent(st, staging_free_[static_cast<std::size_t>(ring)], 0));
   slot_staging_[slot] = ring;
@@ -319,6 +341,7 @@ void DeviceBackend::on_embeddings_ready(std::size_t slot, const lmmsim::EncodeBa
   cudaEvent_t ev = ctx_.new_event();
   RS_CUDA_CHECK(cudaEventRecord(ev, st));
   staging_free_[static_cast<std::size_t>(ring)] = ev;
+  staging_busy_[static_cast<std::size_t>(ring)] = false;  // reusable once `ev` completes
   if (!tracker_tail_) tracker_tail_ = ctx_.new_event();
   RS_CUDA_CHECK(cudaEventRecord(tracker_tail_, st));
 }
@@ -398,8 +421,7 @@ void DeviceBackend::launch_remote_encode(int worker, std::size_t slot, const lmm
   ep::Transport& t = *remote_->t;
   DevRequest& r = ctx_.get(b.request_id);
   const Shapes& s = ctx_.shapes();
-  const int ring = worker * kRing + enc_ring_pos_[static_cast<std::size_t>(worker)];
-  enc_ring_pos_[static_cast<std::size_t>(worker)] = (enc_ring_pos_[static_cast<std::size_t>(worker)] + 1) % kRing;
+  const int ring = acquire_staging();
   slot_staging_[slot] = ring;
   ep::EncodeCmd cmd;
   cmd.slot = slot;

@@ -120,11 +120,13 @@ class DeviceBackend final : public lmmsim::ExecutionBackend {
   std::chrono::steady_clock::time_point t0_;
   std::unordered_map<lmmsim::RequestId, Payload> payloads_;
   // encode staging: ring per worker
-  static constexpr int kRing = 4;
-  std::vector<bf16*> staging_;          // [workers * kRing] x [max_encode_tokens, d]
+  static constexpr int kRing = 4;       // initial staging buffers per encoder worker (pool grows)
+  std::vector<bf16*> staging_;          // [>= workers * kRing] x [max_encode_tokens, d]
   std::vector<cudaEvent_t> staging_free_;
+  std::vector<bool> staging_busy_;      // held by a batch not yet scattered
+  std::size_t staging_next_ = 0;
+  int acquire_staging();
   std::vector<bf16*> enc_input_;        // [workers] patches input (e2e)
-  std::vector<int> enc_ring_pos_;
   std::unordered_map<std::size_t, int> slot_staging_;     // encode slot -> staging index
   std::unordered_map<std::size_t, cudaEvent_t> slot_done_; // encode slot -> completion
   std::unordered_map<std::size_t, double> slot_done_ms_;

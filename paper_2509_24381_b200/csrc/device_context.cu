@@ -504,9 +504,12 @@ double Context::decode(const std::vector<lmmsim::RequestId>& ids, int steps, std
     DevRequest& r = get(id);
     reqs.push_back(&r);
     slots.push_back(r.slot);
-    std::int32_t mx = -1;
-    for (const auto& p : r.rope) mx = std::max({mx, p[0], p[1], p[2]});
-    next_rope.push_back(mx + 1);  // Qwen2-VL: generated text continues after the prompt's max id
+    if (r.next_rope < 0) {  // first decode call: generated text continues after the prompt's max id
+      std::int32_t mx = -1;
+      for (const auto& p : r.rope) mx = std::max({mx, p[0], p[1], p[2]});
+      r.next_rope = mx + 1;
+    }
+    next_rope.push_back(r.next_rope);
     // KV pages for every decoded token, appended to the request's page table
     const std::uint64_t need = (r.total + static_cast<std::uint64_t>(steps) + kPageTokens - 1) / kPageTokens;
     if (need > r.kv_pages.size()) {
@@ -588,7 +591,10 @@ double Context::decode(const std::vector<lmmsim::RequestId>& ids, int steps, std
   RS_CUDA_CHECK(cudaEventElapsedTime(&ms, e0, e1));
   RS_CUDA_CHECK(cudaEventDestroy(e0));
   RS_CUDA_CHECK(cudaEventDestroy(e1));
-  for (DevRequest* r : reqs) r->total += static_cast<std::uint64_t>(steps);  // KV now holds the decoded tokens
+  for (DevRequest* r : reqs) {  // KV now holds the decoded tokens; M-RoPE ids move on with them
+    r->total += static_cast<std::uint64_t>(steps);
+    r->next_rope += steps;
+  }
   return ms;
 }
 

@@ -87,6 +87,7 @@ struct DevRequest {
   std::uint32_t* bitmap = nullptr;     // device readiness words
   int* kv_table = nullptr;             // device page table (kv_pages)
   std::vector<std::array<std::int32_t, 3>> rope;  // M-RoPE ids per token
+  std::int32_t next_rope = -1;         // decode: M-RoPE id of the next generated token (-1: not started)
   std::vector<std::uint64_t> item_patch_offset;   // first patch of each item
   std::vector<std::pair<int, int>> item_grids;     // merged-token grid of each item
   std::uint64_t patches = 0;

@@ -1,11 +1,9 @@
 """End-to-end numerics and decisions of the B200 pipeline vs the oracles.
 
 Tolerances (bf16 storage, fp32 accumulation; the reference has no model math,
-so these are the builder-stated bars of SURVEY.md §8c):
-  * embeddings: per-row cosine >= 0.999 (tiny) / 0.995 (7B width) and
-    max|err| <= 2e-2 * max|ref| + 2e-2
-  * first-token logits: max|err| <= 0.1 * std(ref); argmax equal unless the
-    oracle's top-2 gap is below that error bound (near tie).
+so these are the builder-stated bars of SURVEY.md §8c, tests/_tol.py):
+  * embeddings: per-row cosine >= 0.999 and max|err| <= 2e-2 * max|ref| + 2e-2
+  * first-token logits: max|err| <= 0.05 * std(ref) and the same argmax.
 Decisions (lock-step clock) must equal the reference simulator's byte for byte.
 """
 import numpy as np
@@ -14,32 +12,9 @@ import pytest
 torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
 
+from _tol import check_emb as _check_emb, check_logits as _check_logits  # noqa: E402
+
 CFG1 = "T64|M256|M256|T32|M256|M256"
-
-
-def _cos_rows(a, b):
-    na = np.linalg.norm(a, axis=1)
-    nb = np.linalg.norm(b, axis=1)
-    return (a * b).sum(1) / np.maximum(na * nb, 1e-12)
-
-
-def _bf16_to_f32(u16):
-    return (u16.astype(np.uint32) << 16).view(np.float32)
-
-
-def _check_emb(got, ref, cos_min):
-    cos = _cos_rows(got, ref)
-    assert cos.min() >= cos_min, f"min row cosine {cos.min():.5f}"
-    assert np.abs(got - ref).max() <= 2e-2 * np.abs(ref).max() + 2e-2
-
-
-def _check_logits(got, am, ref):
-    err = np.abs(got - ref).max()
-    bound = 0.1 * ref.std()
-    assert err <= bound, f"max|dlogit| {err:.4g} > {bound:.4g}"
-    top = np.sort(ref)[-2:]
-    if top[1] - top[0] > 2 * err:
-        assert am == int(ref.argmax())
 
 
 @pytest.fixture(scope="module")
@@ -126,6 +101,27 @@ def test_engine_lockstep_decisions_and_logits(tiny, oracle_tiny, policy, C, B, s
         emb = mo.request_embeddings(cfg, w, rid, layout, 7, C)
         h = llm.forward(emb, mo.mrope_positions(mo.parse_layout(layout)))
         _check_logits(*tiny.logits(rid), llm.first_token_logits(h[-1]))
+
+
+def test_many_batches_in_flight_keep_their_staging(tiny, oracle_tiny):
+    """A slow link (lock-step cost model with a 1 s transfer) leaves all nine
+    encode batches' embeddings waiting for their transfers at once — more
+    than the initial staging ring of 4 per worker: every batch
+    must keep its own buffer until its scatter, so the logits stay right."""
+    from oracle import ref
+    from paper_2509_24381_b200 import api
+    mo, cfg, w = oracle_tiny
+    layout = "T16|" + "|".join(["M64"] * 9) + "|T8"
+    wl = f"0,0,-,{layout}\n"
+    sc = api.SimConfig(policy="rserve", stages=1, token_budget=512, embedding_batch_tokens=64,
+                       hidden_size=512, cost=api.CostModel(beta_enc_ms_per_token=0.01, eps_tx_ms=1000.0,
+                                                           delta_stage_ms_per_token=0.01))
+    log, _, _ = tiny.run(wl, sc, clock="lockstep", payload_seed=13)
+    assert log == ref.simulate(wl, sc.to_c())
+    llm = mo.LlmOracle(cfg, w)
+    emb = mo.request_embeddings(cfg, w, 0, layout, 13, 64)
+    h = llm.forward(emb, mo.mrope_positions(mo.parse_layout(layout)))
+    _check_logits(*tiny.logits(0), llm.first_token_logits(h[-1]))
 
 
 def test_engine_realclock_journal_replay(tiny, oracle_tiny):

@@ -68,7 +68,7 @@ def test_generated_payload_matches_oracle(tiny):
         ref = llm.first_token_logits(h[-1])
         got, am = tiny.logits(rid)
         err = np.abs(got - ref).max()
-        assert err <= 0.1 * ref.std(), f"request {rid}: max|dlogit| {err:.4g}"
+        assert err <= 0.05 * ref.std(), f"request {rid}: max|dlogit| {err:.4g}"
     # and it really changed the inputs
     tiny.run(WL, _cfg(), clock="lockstep", payload_seed=7)
     for rid in LAYOUTS:

@@ -115,3 +115,21 @@ def test_tracker_errors_match_reference(pipe):
     with pytest.raises(N.RegistryError, match="unknown request id 99"):
         pipe.mark_encoded(99, 0, 10, emb.data_ptr())
     pipe.erase(5)
+
+
+def test_rejected_prefill_chunk_leaves_trackers_untouched(pipe):
+    """rs_prefill_chunk validates every slice before advancing any tracker
+    (ADVICE r1): an oversized or not-ready chunk raises and the frontiers stay
+    where they were, so a corrected retry succeeds."""
+    from paper_2509_24381_b200 import _native as N
+    pipe.request_create(61, "T100|M50|T20")
+    pipe.request_create(62, "T1100")
+    with pytest.raises(N.ConfigError, match="exceeds max_chunk_tokens"):
+        pipe.prefill_chunk([(61, 0, 100), (62, 0, 1000)])
+    with pytest.raises(N.DependencyViolation, match="exceeds schedulable frontier"):
+        pipe.prefill_chunk([(62, 0, 500), (61, 0, 120)])
+    assert pipe.tracker_stats(61)["frontier"] == 0 and pipe.tracker_stats(62)["frontier"] == 0
+    pipe.prefill_chunk([(61, 0, 100), (62, 0, 500)])
+    assert pipe.tracker_stats(61)["frontier"] == 100 and pipe.tracker_stats(62)["frontier"] == 500
+    pipe.erase(61)
+    pipe.erase(62)
