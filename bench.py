@@ -619,8 +619,6 @@ def run_ep(args):
                          slot_tokens=1 << 19, kv_tokens=1 << 19, max_chunk_tokens=args.budget,
                          max_encode_tokens=C_TOKENS)
     transport = args.ep_transport
-    if args.ep_same_device and transport == "nccl":
-        transport = "ipc"  # NCCL refuses two ranks of a communicator on one GPU
     role = api.ep_role(rank, stages, encoders)
     links = api.ep_links(stages, encoders)
     manifest = {"rank": rank, "role": f"{role[0]}{role[1]}", "device": dev, "transport": transport,
@@ -705,6 +703,10 @@ def run_ep(args):
         if not args.no_parity:
             parity.update(cfg2_logit_parity(*single_logits, f"cuda:{dev}"))
         st_e = timed_e2e[-1][2]
+        # pixels are uploaded on the encoder ranks: 4 patches x 1176 bf16 per image token
+        px_bytes = sum(4 * n * m["patch_dim"] * 2 for wl in tput_wls[:len(timed_e2e)]
+                       for lay in workload_layouts(wl) for n in
+                       (int(f[1:]) for f in lay.split("|") if f[0] == "M")) / len(timed_e2e)
         line = {
             "metric": "encode+prefill tokens/s (p50/p99 TTFT ms alongside)",
             "value": tokens / (total_ms / 1e3), "unit": "tokens/s", "n_gpus": ws,
@@ -723,7 +725,8 @@ def run_ep(args):
             "cfg2": {"ttft_ms": {"p50": nearest_rank(single_ttft, 50), "p99": nearest_rank(single_ttft, 99)},
                      "runs": len(single_ttft), "tokens": PROMPT_TOKENS},
             "e2e": {"value": e2e_tokens / (e2e_total / 1e3), "unit": "tokens/s",
-                    "h2d_bytes_per_step": st_e["h2d_bytes"], "d2h_bytes_per_step": st_e["d2h_bytes"],
+                    "h2d_bytes_per_step": st_e["h2d_bytes"] + px_bytes, "d2h_bytes_per_step": st_e["d2h_bytes"],
+                    "h2d_note": "P0's uploads (control, token ids) + the encoder ranks' pixel uploads",
                     "ttft_ms": e2["ttft_ms"],
                     "timing": "host wall clock of each run (H2D pixels from pinned memory on the "
                               "encoder ranks + D2H logits inside)"},
@@ -961,6 +964,8 @@ def main():
         sys.exit(relaunch_under_torchrun(args.gpus))
     if "WORLD_SIZE" in os.environ and ws != args.gpus:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={ws}")
+    if args.ep_same_device:
+        args.ep_transport = "ipc"  # NCCL refuses two ranks of a communicator on one GPU
     if args.dry_run:
         dry_run(args)
     elif args.impl == "reference":

@@ -1,6 +1,7 @@
 // rserve-b200 — model weights + ViT / LLM forward passes (see model.cuh).
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 
 #include "attention.cuh"
 #include "gemm.cuh"
@@ -180,16 +181,16 @@ void finalize_plan(VitBatchPlan& plan) {
   std::stable_sort(plan.full_blocks.begin(), plan.full_blocks.end(), [](const AttnBlock& x, const AttnBlock& y) {
     return x.key_end - x.key_begin > y.key_end - y.key_begin;
   });
-  // window layers: 128-row blocks over the packed tokens; keys = union of the
-  // windows the block's rows belong to.
+  // window layers: tiles of WHOLE consecutive windows of <= 128 packed rows
+  // (two 8x8-patch windows in the common case) — one S tile per (tile, head)
+  // holds every key its rows can see (attention_win.cu).
   const std::vector<std::int32_t>& cu = plan.cu_window;
-  std::size_t s = 0;
-  for (int r = 0; r < plan.patches; r += kPrefillRows) {
-    const int r1 = std::min(plan.patches, r + kPrefillRows);
-    while (s + 1 < cu.size() && cu[s + 1] <= r) ++s;
-    std::size_t e = s;
-    while (e + 1 < cu.size() && cu[e + 1] < r1) ++e;
-    plan.win_blocks.push_back({r, r1 - r, cu[s], cu[e + 1]});
+  for (std::size_t w = 0; w + 1 < cu.size();) {
+    const int r0 = cu[w];
+    std::size_t e = w + 1;
+    while (e + 1 < cu.size() && cu[e + 1] - r0 <= kPrefillRows) ++e;
+    plan.win_blocks.push_back({r0, cu[e] - r0, r0, cu[e]});
+    w = e;
   }
 }
 
@@ -218,6 +219,16 @@ void Vit::encode(const VitBatchPlan& plan, const bf16* patches, const std::int32
   // layer 0's ln1 input comes from the patch embedding: explicit norm.
   RS_CUDA_CHECK(cudaMemsetAsync(ss_b_, 0, static_cast<std::size_t>(P) * 8, st));
   const float inv_vd = 1.0f / static_cast<float>(s.vd);
+  static const bool win_tc_env = [] {
+    const char* e = std::getenv("RS_VIT_WIN_TC");
+    return e == nullptr || e[0] != '0';
+  }();
+  const bool win_tc = win_tc_env && attention_window_tc_supported(s.vhd, plan.max_window);
+  double win_flops = 0;  // 4 n^2 hd per head per window
+  for (std::size_t i = 0; i + 1 < plan.cu_window.size(); ++i) {
+    const double n = plan.cu_window[i + 1] - plan.cu_window[i];
+    win_flops += 4.0 * n * n * s.vhd * s.vh;
+  }
   for (int l = 0; l < s.vl; ++l) {
     const VitLayer& L = layers_[static_cast<std::size_t>(l)];
     g = GemmArgs{};
@@ -238,11 +249,17 @@ void Vit::encode(const VitBatchPlan& plan, const bf16* patches, const std::int32
       attention_varlen_tc(qp_, kp_, vt_, max_p_, s.vh, att_, s.vd, s.vhd, full_blocks,
                           plan.full_blocks.data(), static_cast<int>(plan.full_blocks.size()), cu_item, n_items, scale, st);
     } else {
-      // 8x8-patch windows (<= 64 keys): latency-bound tiles; the register-
-      // tiled kernel reads qkv in place (no padding / transpose pass)
-      // (2D RoPE applied to q / k in shared memory inside the kernel)
-      attention_varlen_bidir(qkv_, 3 * s.vd, att_, s.vd, cu_window, n_win, plan.max_window, P, s.vh,
-                             s.vhd, scale, st, rope_table_);
+      // 8x8-patch windows (<= 64 keys): tcgen05 over tiles of whole windows,
+      // Q / K / V read in place by TMA (no padding / transpose pass), 2D RoPE
+      // applied in shared memory (attention_win.cu); the mma.sync kernel
+      // covers head sizes / windows it does not (and RS_VIT_WIN_TC=0)
+      if (win_tc)
+        attention_window_tc(qkv_, 3 * s.vd, P, att_, s.vd, win_blocks,
+                            static_cast<int>(plan.win_blocks.size()), cu_window, n_win, s.vh, s.vhd, scale,
+                            rope_table_, win_flops, st);
+      else
+        attention_varlen_bidir(qkv_, 3 * s.vd, att_, s.vd, cu_window, n_win, plan.max_window, P, s.vh,
+                               s.vhd, scale, st, rope_table_);
     }
     g = GemmArgs{};
     g.A = att_; g.lda = s.vd; g.B = L.o_w; g.ldb = s.vd; g.C = x_; g.ldc = s.vd; g.bias = L.o_b;
