@@ -7,7 +7,7 @@
 // every exception class and message text. The representation is B200-first:
 // readiness is a packed uint32 bitmap, bit (i % 32) of word (i / 32) for
 // prompt token i — byte-for-byte the layout the device tracker keeps in HBM
-// (paper_2509_24381_b200/csrc/tracker_kernels.cu), so host and device state
+// (paper_2509_24381_b200/csrc/elementwise.cu K6/K7), so host and device state
 // can be compared word by word. Item lookup is a binary search over the
 // (sorted, disjoint) item starts and the ready run advances a word at a time.
 //

@@ -214,6 +214,62 @@ RS_API rs_status rs_encode(rs_ctx* ctx, const uint64_t* items, int32_t n_items,
  * prompt end get first-token logits (rs_logits).                        */
 RS_API rs_status rs_prefill_chunk(rs_ctx* ctx, const uint64_t* slices, int32_t n_slices);
 RS_API rs_status rs_logits(rs_ctx* ctx, uint64_t id, float* out_host, int32_t* out_argmax);
+
+/* ---- caller-owned event loop (asynchronous seam) -------------------------
+ * For a host scheduler that owns its event loop — the reference's
+ * Simulation handlers (simengine.hpp:275-441) calling the cost seam
+ * (encode_time_ms / stage_time_ms, cost_model.hpp:68-82) — the launches below
+ * return at once (work queued on the context's encode / stage streams, or on
+ * `stream` when non-NULL: a cudaStream_t of the context's device) and their
+ * completions come back from rs_poll, tagged with the caller's `tag`, in the
+ * reference's event classes (simengine.hpp:211-248: encode before stage at
+ * equal times, then issue order). Times are device milliseconds since the
+ * context's first asynchronous launch. On one GPU the encoder -> prefill
+ * link is the reference's zero-cost transfer: the caller's TransferDone is
+ * its EncodeDone, at which it calls rs_embeddings_ready.                  */
+typedef struct rs_segment {   /* request.hpp:47-52 SegmentSpec */
+  int32_t kind;               /* RS_SEG_TEXT / RS_SEG_MULTIMODAL */
+  uint64_t tokens;
+} rs_segment;
+enum { RS_SEG_TEXT = 0, RS_SEG_MULTIMODAL = 1 };
+/* = rs_request_create with a POD segment array (request.hpp:94-102 validate
+ * errors: RS_ERR_INPUT with the reference's text).                        */
+RS_API rs_status rs_request_create_segments(rs_ctx* ctx, uint64_t id, const rs_segment* segs,
+                                            int32_t n_segs, const int32_t* text_token_ids);
+/* completion classes (PipelineEngine::EventKind numbering) */
+enum { RS_EV_ENCODE_DONE = 1, RS_EV_TRANSFER_DONE = 2, RS_EV_STAGE_DONE = 3, RS_EV_CHUNK_COMPLETE = 4 };
+typedef struct rs_event {
+  int32_t kind;     /* RS_EV_* */
+  int32_t stage;    /* pipeline stage (0 on a one-stage context) */
+  uint64_t tag;     /* the launch's tag */
+  double time_ms;   /* device completion time */
+} rs_event;
+/* encode_time_ms seam, non-blocking: ViT forward of one Algorithm-1 batch of
+ * request `id` (items = (start,end) pairs; patches as for rs_encode; host
+ * patches must stay valid until the ENCODE_DONE of `tag`). The embeddings
+ * wait in a staging buffer owned by `tag`.                                */
+RS_API rs_status rs_encode_batch_async(rs_ctx* ctx, uint64_t id, const uint64_t* items, int32_t n_items,
+                                       const void* patches, int32_t patches_on_host, void* stream,
+                                       uint64_t tag);
+/* on_embeddings_ready (token_sched.hpp:184-187) for every item of encode
+ * `tag`, at the caller's TransferDone: host tracker mirror updated at once
+ * (reference errors), K6 scatter + bitmap queued after the encode.         */
+RS_API rs_status rs_embeddings_ready(rs_ctx* ctx, uint64_t tag);
+/* stage_time_ms seam, non-blocking: one chunk (n x (id, start, end)); the
+ * slices are validated against the trackers before any is advanced. Its
+ * completion is STAGE_DONE and, on a context with the LM head, a
+ * CHUNK_COMPLETE at the same time, after which rs_logits serves the
+ * requests whose prompt ended in the chunk.                               */
+RS_API rs_status rs_prefill_chunk_async(rs_ctx* ctx, const uint64_t* slices, int32_t n_slices,
+                                        void* stream, uint64_t tag);
+/* release (tracker.hpp:126-135) of [start, end): the slot pages return to the
+ * pool once chunk `after_tag` (the last reader) has completed.             */
+RS_API rs_status rs_release_async(rs_ctx* ctx, uint64_t id, uint64_t start, uint64_t end,
+                                  uint64_t after_tag);
+RS_API rs_status rs_request_erase_async(rs_ctx* ctx, uint64_t id, uint64_t after_tag);
+/* Completed launches since the last call (<= cap events), in completion
+ * order. wait != 0: block until at least one completes (if any pending).  */
+RS_API rs_status rs_poll(rs_ctx* ctx, rs_event* out, int32_t cap, int32_t wait, int32_t* n_out);
 RS_API rs_status rs_synchronize(rs_ctx* ctx);
 
 /* ---- the engine on the device ------------------------------------------

@@ -177,6 +177,26 @@ _sig("rs_weight_info", [C.c_void_p, C.c_char_p, C.POINTER(C.c_void_p), C.POINTER
                         C.POINTER(C.c_int64), C.POINTER(C.c_int64)])
 _sig("rs_debug_buffer", [C.c_void_p, C.c_char_p, C.POINTER(C.c_void_p), C.POINTER(C.c_int64)])
 
+# asynchronous seam (caller-owned event loop)
+class rs_segment(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("tokens", C.c_uint64)]
+
+
+class rs_event(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("stage", C.c_int32), ("tag", C.c_uint64), ("time_ms", C.c_double)]
+
+
+EV_ENCODE_DONE, EV_TRANSFER_DONE, EV_STAGE_DONE, EV_CHUNK_COMPLETE = 1, 2, 3, 4
+_sig("rs_request_create_segments", [C.c_void_p, C.c_uint64, C.POINTER(rs_segment), C.c_int32, C.c_void_p])
+_sig("rs_encode_batch_async", [C.c_void_p, C.c_uint64, C.POINTER(C.c_uint64), C.c_int32, C.c_void_p,
+                               C.c_int32, C.c_void_p, C.c_uint64])
+_sig("rs_embeddings_ready", [C.c_void_p, C.c_uint64])
+_sig("rs_prefill_chunk_async", [C.c_void_p, C.POINTER(C.c_uint64), C.c_int32, C.c_void_p, C.c_uint64])
+_sig("rs_release_async", [C.c_void_p, C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint64])
+_sig("rs_request_erase_async", [C.c_void_p, C.c_uint64, C.c_uint64])
+_sig("rs_poll", [C.c_void_p, C.POINTER(rs_event), C.c_int32, C.c_int32, C.POINTER(C.c_int32)])
+
+
 # EP disaggregation
 class rs_ep_options(C.Structure):
     _fields_ = [("stages", C.c_int32), ("encoders", C.c_int32), ("transport", C.c_int32),

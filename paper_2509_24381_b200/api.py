@@ -122,6 +122,9 @@ def experiment_from_json(j: dict):
     """(WorkloadConfig template, SimConfig, policies, rates, seeds, slo) from an
     experiment JSON (config.hpp:171-300 key names)."""
     w = j["workload"]
+    if "file" in w:  # fixed workload file (config.hpp:184-188): no generator
+        templates = []
+        w = dict(w, duration_s=0.0, templates=[])
     templates = [RequestTemplate(t["pattern"], _dist_from_json(t["num_mm_items"]),
                                  _dist_from_json(t["mm_item_tokens"]),
                                  _dist_from_json(t["text_segment_tokens"]), float(t["probability"]))
@@ -311,6 +314,42 @@ class Pipeline:
         out = C.c_void_p(out_ptr)
         N.check(N.lib.rs_encode(self.h, arr, len(items), patches_ptr, int(on_host), C.byref(out)))
         return out.value
+
+    # asynchronous seam (include/rserve.h "caller-owned event loop") -----------
+    def request_create_segments(self, req_id: int, segments: Sequence[Tuple[str, int]], text_ids=None):
+        arr = (N.rs_segment * len(segments))(*[N.rs_segment(0 if k == "T" else 1, n) for k, n in segments])
+        ptr = None
+        if text_ids is not None:
+            import numpy as np
+            self._keep = np.ascontiguousarray(text_ids, dtype=np.int32)
+            ptr = self._keep.ctypes.data
+        N.check(N.lib.rs_request_create_segments(self.h, req_id, arr, len(segments), ptr))
+
+    def encode_batch_async(self, req_id: int, items: Sequence[Tuple[int, int]], patches_ptr: int,
+                           on_host: bool, tag: int, stream: Optional[int] = None):
+        arr = (C.c_uint64 * (2 * len(items)))(*[v for it in items for v in it])
+        N.check(N.lib.rs_encode_batch_async(self.h, req_id, arr, len(items), patches_ptr, int(on_host),
+                                            stream, tag))
+
+    def embeddings_ready(self, tag: int):
+        N.check(N.lib.rs_embeddings_ready(self.h, tag))
+
+    def prefill_chunk_async(self, slices: Sequence[Tuple[int, int, int]], tag: int, stream: Optional[int] = None):
+        arr = (C.c_uint64 * (3 * len(slices)))(*[v for s in slices for v in s])
+        N.check(N.lib.rs_prefill_chunk_async(self.h, arr, len(slices), stream, tag))
+
+    def release_async(self, req_id: int, start: int, end: int, after_tag: int):
+        N.check(N.lib.rs_release_async(self.h, req_id, start, end, after_tag))
+
+    def erase_async(self, req_id: int, after_tag: int):
+        N.check(N.lib.rs_request_erase_async(self.h, req_id, after_tag))
+
+    def poll(self, wait: bool = False, cap: int = 64) -> List[Tuple[int, int, int, float]]:
+        """Completed launches: [(kind, stage, tag, time_ms)] in completion order."""
+        ev = (N.rs_event * cap)()
+        n = C.c_int32()
+        N.check(N.lib.rs_poll(self.h, ev, cap, int(wait), C.byref(n)))
+        return [(ev[i].kind, ev[i].stage, ev[i].tag, ev[i].time_ms) for i in range(n.value)]
 
     def prefill_chunk(self, slices: Sequence[Tuple[int, int, int]]):
         arr = (C.c_uint64 * (3 * len(slices)))(*[v for s in slices for v in s])

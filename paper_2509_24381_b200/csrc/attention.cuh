@@ -62,13 +62,16 @@ void attention_varlen_tc(const bf16* qp, const bf16* kp, const bf16* vt, int row
                          float scale, cudaStream_t stream);
 
 /// tcgen05 / TMA ViT window attention (attention_win.cu): qkv [rows, 3 H hd]
-/// read in place (q | k | v head blocks), 2D RoPE applied to q / k from
-/// rope_table ([rows, hd/2] cos/sin); tiles: whole consecutive windows of
-/// <= 128 rows (finalize_plan); out [rows, H hd]. flops: profiler label.
-bool attention_window_tc_supported(int head_dim, int max_window);
+/// read in place (q | k | v head blocks), 2D RoPE applied to q / k from the
+/// compact table freq [n_pos, hd/4] (cos, sin) at the rows' pos_hw [rows, 2];
+/// tiles: whole consecutive windows of <= 128 rows, {q_row0, q_rows, first
+/// window, windows} (finalize_plan), followed in the same device buffer by
+/// [rows] u32 per-row windows as tile columns (lo | hi << 16); out
+/// [rows, H hd]. flops: profiler label.
+bool attention_window_tc_supported(int head_dim, int max_window, int n_pos);
 void attention_window_tc(const bf16* qkv, int ld_qkv, int rows, bf16* out, int ld_out, const AttnBlock* tiles,
-                         int n_tiles, const int* cu_window, int n_win, int heads, int head_dim, float scale,
-                         const float2* rope_table, double flops, cudaStream_t st);
+                         int n_tiles, int heads, int head_dim, float scale, const std::int32_t* pos_hw,
+                         const float2* freq, int n_pos, double flops, cudaStream_t st);
 
 /// Decode attention (one query row per work item, q_rows == 1, keys
 /// [0, q_pos0]) over the paged KV: split along the keys, GQA-packed,

@@ -67,6 +67,7 @@ rs_status rs_ctx_destroy(rs_ctx* c) {
   return guarded([&] {
     if (c == nullptr) return;
     cudaDeviceSynchronize();
+    rs_async_teardown(c);
     if (c->manual_out) cudaFree(c->manual_out);
     if (c->manual_in) cudaFree(c->manual_in);
     if (c->manual_x) cudaFree(c->manual_x);

@@ -401,8 +401,11 @@ void Context::encode(const VitBatchPlan& plan, const bf16* patches_dev, bf16* ou
   const auto* cuw = static_cast<const std::int32_t*>(up_.put(plan.cu_window.data(), plan.cu_window.size() * 4, st));
   const auto* cui = static_cast<const std::int32_t*>(up_.put(plan.cu_item.data(), plan.cu_item.size() * 4, st));
   const auto* orow = static_cast<const std::int32_t*>(up_.put(plan.out_row.data(), plan.out_row.size() * 4, st));
-  const auto* wb = static_cast<const AttnBlock*>(
-      up_.put(plan.win_blocks.data(), plan.win_blocks.size() * sizeof(AttnBlock), st));
+  // window tiles followed by the per-row window table (attention_window_tc)
+  std::vector<std::uint8_t> wbuf(plan.win_blocks.size() * sizeof(AttnBlock) + plan.win_row.size() * 4);
+  std::memcpy(wbuf.data(), plan.win_blocks.data(), plan.win_blocks.size() * sizeof(AttnBlock));
+  std::memcpy(wbuf.data() + plan.win_blocks.size() * sizeof(AttnBlock), plan.win_row.data(), plan.win_row.size() * 4);
+  const auto* wb = static_cast<const AttnBlock*>(up_.put(wbuf.data(), wbuf.size(), st));
   const auto* fb = static_cast<const AttnBlock*>(
       up_.put(plan.full_blocks.data(), plan.full_blocks.size() * sizeof(AttnBlock), st));
   vit_->encode(plan, patches_dev, pos, cuw, cui, orow, wb, fb, out, st);

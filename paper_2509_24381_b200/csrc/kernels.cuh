@@ -74,6 +74,9 @@ void vit_qkv_split(const bf16* qkv, int ld, const float2* rope_table, int rows, 
 /// attention reads qkv directly).
 void vit_qk_rope_inplace(bf16* qkv, int ld, const float2* rope_table, int rows, int heads, int hd,
                          cudaStream_t st);
+/// Compact ViT 2D-RoPE table: out[pos * (hd/4) + j] = (cos, sin)(pos * theta^(-4j/hd))
+/// for pos < n_pos — the same values vit_rope_table stores per row and pair.
+void vit_rope_freq_table(int n_pos, int hd, float theta, float2* out, cudaStream_t st);
 void vit_rope_table(const std::int32_t* pos_hw, int rows, int hd, float theta, float2* table,
                     cudaStream_t st);
 

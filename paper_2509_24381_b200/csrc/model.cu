@@ -164,6 +164,8 @@ void Vit::init(const Shapes& s, DeviceArena& a, int max_patches, cudaStream_t st
   RS_CUDA_CHECK(cudaMemsetAsync(kp_, 0, padded * 2, st));
   RS_CUDA_CHECK(cudaMemsetAsync(vt_, 0, padded * 2, st));
   rope_table_ = static_cast<float2*>(a.alloc(static_cast<std::size_t>(P) * (s.vhd / 2) * sizeof(float2)));
+  rope_freq_ = static_cast<float2*>(a.alloc(static_cast<std::size_t>(kVitRopePositions) * (s.vhd / 4) * sizeof(float2)));
+  vit_rope_freq_table(kVitRopePositions, s.vhd, s.cfg.rope_theta_vit, rope_freq_, st);
   ss_a_ = static_cast<unsigned long long*>(a.alloc(static_cast<std::size_t>(P) * 8));
   ss_b_ = static_cast<unsigned long long*>(a.alloc(static_cast<std::size_t>(P) * 8));
 }
@@ -185,11 +187,16 @@ void finalize_plan(VitBatchPlan& plan) {
   // (two 8x8-patch windows in the common case) — one S tile per (tile, head)
   // holds every key its rows can see (attention_win.cu).
   const std::vector<std::int32_t>& cu = plan.cu_window;
+  plan.win_row.assign(static_cast<std::size_t>(plan.patches) + 128, 0u);  // padded: unguarded loads
   for (std::size_t w = 0; w + 1 < cu.size();) {
     const int r0 = cu[w];
     std::size_t e = w + 1;
     while (e + 1 < cu.size() && cu[e + 1] - r0 <= kPrefillRows) ++e;
-    plan.win_blocks.push_back({r0, cu[e] - r0, r0, cu[e]});
+    plan.win_blocks.push_back({r0, cu[e] - r0, static_cast<int>(w), static_cast<int>(e - w)});
+    for (std::size_t k = w; k < e; ++k)
+      for (int row = cu[k]; row < cu[k + 1]; ++row)
+        plan.win_row[static_cast<std::size_t>(row)] =
+            static_cast<std::uint32_t>(cu[k] - r0) | (static_cast<std::uint32_t>(cu[k + 1] - r0) << 16);
     w = e;
   }
 }
@@ -223,7 +230,10 @@ void Vit::encode(const VitBatchPlan& plan, const bf16* patches, const std::int32
     const char* e = std::getenv("RS_VIT_WIN_TC");
     return e == nullptr || e[0] != '0';
   }();
-  const bool win_tc = win_tc_env && attention_window_tc_supported(s.vhd, plan.max_window);
+  int n_pos = 0;
+  for (std::int32_t v : plan.pos_hw) n_pos = std::max(n_pos, v + 1);
+  const bool win_tc = win_tc_env && n_pos <= kVitRopePositions &&
+                      attention_window_tc_supported(s.vhd, plan.max_window, n_pos);
   double win_flops = 0;  // 4 n^2 hd per head per window
   for (std::size_t i = 0; i + 1 < plan.cu_window.size(); ++i) {
     const double n = plan.cu_window[i + 1] - plan.cu_window[i];
@@ -255,8 +265,8 @@ void Vit::encode(const VitBatchPlan& plan, const bf16* patches, const std::int32
       // covers head sizes / windows it does not (and RS_VIT_WIN_TC=0)
       if (win_tc)
         attention_window_tc(qkv_, 3 * s.vd, P, att_, s.vd, win_blocks,
-                            static_cast<int>(plan.win_blocks.size()), cu_window, n_win, s.vh, s.vhd, scale,
-                            rope_table_, win_flops, st);
+                            static_cast<int>(plan.win_blocks.size()), s.vh, s.vhd, scale, pos_hw, rope_freq_,
+                            n_pos, win_flops, st);
       else
         attention_varlen_bidir(qkv_, 3 * s.vd, att_, s.vd, cu_window, n_win, plan.max_window, P, s.vh,
                                s.vhd, scale, st, rope_table_);

@@ -83,6 +83,7 @@ struct VitBatchPlan {  // host-side metadata of one encode batch
   std::vector<std::int32_t> out_row;    // merged row (window-major) -> output row (LLM order)
   int max_window = 0, max_item = 0;
   std::vector<AttnBlock> win_blocks, full_blocks;  // tcgen05 attention work (finalize_plan)
+  std::vector<std::uint32_t> win_row;  // [P] window of each row as columns of its win_blocks tile (lo | hi << 16)
 };
 
 /// 128-row attention blocks for the window and full-attention layers.
@@ -92,6 +93,9 @@ void finalize_plan(VitBatchPlan& plan);
 void item_grid(std::uint64_t tokens, int* gh, int* gw);
 /// Window-major patch order of one item; appends to `plan`.
 void plan_item(int gh, int gw, int window, int out_row_base, VitBatchPlan& plan);
+
+/// Patch positions (per axis) covered by the ViT's compact 2D-RoPE table.
+constexpr int kVitRopePositions = 512;
 
 class Vit {
  public:
@@ -122,6 +126,7 @@ class Vit {
   bf16* unit_ln_ = nullptr;
   unsigned long long *ss_a_ = nullptr, *ss_b_ = nullptr;  // [max patches], 2^-16 fixed point
   float2* rope_table_ = nullptr;                         // [P, hd/2] cos/sin, per batch
+  float2* rope_freq_ = nullptr;                          // [kVitRopePositions, hd/4] cos/sin per (position, freq)
 };
 
 /// Per-chunk device descriptor (uploaded before a stage runs).
