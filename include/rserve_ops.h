@@ -33,6 +33,15 @@ RS_API rs_status rs_op_attention_varlen(const void* qkv, int ld_qkv, void* out, 
 RS_API rs_status rs_op_attention_varlen_tc(const void* qkv, int ld_qkv, void* out, int ld_out,
                                            const int* cu_seqlens, int n_seqs, int total,
                                            int heads, int head_dim, float scale, void* stream);
+/* ViT window attention on the tcgen05 / TMA kernel the encoder runs
+ * (attention_win.cu): Q / K / V read in place from packed QKV, windows of
+ * <= 128 rows (cu_seqlens, device int32), 2D RoPE (theta) applied to q / k at
+ * pos_hw (device int32 [total, 2] = (h, w) per row; NULL = identity).
+ * Synchronous. */
+RS_API rs_status rs_op_attention_window_tc(const void* qkv, int ld_qkv, void* out, int ld_out,
+                                           const int* cu_seqlens, int n_seqs, int total, int heads,
+                                           int head_dim, float scale, const int* pos_hw,
+                                           float rope_theta, void* stream);
 /* Causal chunked-prefill attention (tcgen05) of ONE slice: q rows
  * [0, q_rows) at prompt positions q_pos0.. attend to keys [0, q_pos0+q_rows)
  * of a paged cache: K [pages][kv_heads][64][hd], V^T [pages][kv_heads][hd][64],

@@ -228,6 +228,7 @@ _sig("rs_op_gemm", [VP, I, VP, I, VP, I, VP, VP, I, VP, I, I, I, I, I, VP])
 _sig("rs_op_rmsnorm", [VP, I, VP, VP, I, I, I, C.c_float, VP])
 _sig("rs_op_attention_varlen", [VP, I, VP, I, VP, I, I, I, I, I, C.c_float, VP])
 _sig("rs_op_attention_varlen_tc", [VP, I, VP, I, VP, I, I, I, I, C.c_float, VP])
+_sig("rs_op_attention_window_tc", [VP, I, VP, I, VP, I, I, I, I, C.c_float, VP, C.c_float, VP])
 _sig("rs_op_attention_prefill", [VP, I, I, VP, I, I, I, VP, VP, C.c_longlong, VP, I, I, I,
                                   C.c_float, VP])
 _sig("rs_kernel_launches", [], C.c_ulonglong)

@@ -3,6 +3,7 @@
 // Each op takes raw device pointers and runs ONE of the product kernels on
 // the given stream; tests compare them against a plain fp32 reference.
 #include <algorithm>
+#include <cstring>
 #include <vector>
 
 #include "attention.cuh"
@@ -10,6 +11,7 @@
 #include "gemm.cuh"
 #include "host/status.hpp"
 #include "kernels.cuh"
+#include "model.cuh"
 #include "rserve_ops.h"
 
 using namespace rserve;
@@ -103,6 +105,50 @@ rs_status rs_op_attention_varlen_tc(const void* qkv, int ld_qkv, void* out, int 
                         cu_seqlens, n_seqs, scale, st);
     RS_CUDA_CHECK(cudaStreamSynchronize(st));
     for (void* p : {qp, kp, vt, pos, bd}) RS_CUDA_CHECK(cudaFreeAsync(p, st));
+  });
+}
+
+rs_status rs_op_attention_window_tc(const void* qkv, int ld_qkv, void* out, int ld_out,
+                                    const int* cu_seqlens, int n_seqs, int total, int heads,
+                                    int head_dim, float scale, const int* pos_hw, float rope_theta,
+                                    void* stream) {
+  return guarded([&] {
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    std::vector<int> cu(static_cast<std::size_t>(n_seqs) + 1);
+    RS_CUDA_CHECK(cudaMemcpyAsync(cu.data(), cu_seqlens, cu.size() * 4, cudaMemcpyDeviceToHost, st));
+    std::vector<std::int32_t> pos(static_cast<std::size_t>(total) * 2, 0);
+    if (pos_hw != nullptr)
+      RS_CUDA_CHECK(cudaMemcpyAsync(pos.data(), pos_hw, pos.size() * 4, cudaMemcpyDeviceToHost, st));
+    RS_CUDA_CHECK(cudaStreamSynchronize(st));
+    int max_window = 0, n_pos = 1;
+    for (int i = 0; i < n_seqs; ++i) max_window = std::max(max_window, cu[i + 1] - cu[i]);
+    for (std::int32_t v : pos) n_pos = std::max(n_pos, v + 1);
+    if (!attention_window_tc_supported(head_dim, max_window, n_pos))
+      throw lmmsim::InputError("rs_op_attention_window_tc: unsupported head_dim / window / positions");
+    // the model's tile plan (finalize_plan): whole consecutive windows of <= 128 rows
+    VitBatchPlan plan;
+    plan.patches = total;
+    plan.cu_window.assign(cu.begin(), cu.end());
+    finalize_plan(plan);
+    std::vector<std::uint8_t> buf(plan.win_blocks.size() * sizeof(AttnBlock) + plan.win_row.size() * 4);
+    std::memcpy(buf.data(), plan.win_blocks.data(), plan.win_blocks.size() * sizeof(AttnBlock));
+    std::memcpy(buf.data() + plan.win_blocks.size() * sizeof(AttnBlock), plan.win_row.data(),
+                plan.win_row.size() * 4);
+    void *bd, *posd, *freq;
+    RS_CUDA_CHECK(cudaMallocAsync(&bd, buf.size(), st));
+    RS_CUDA_CHECK(cudaMallocAsync(&posd, pos.size() * 4, st));
+    RS_CUDA_CHECK(cudaMallocAsync(&freq, static_cast<std::size_t>(n_pos) * (head_dim / 4) * sizeof(float2), st));
+    RS_CUDA_CHECK(cudaMemcpyAsync(bd, buf.data(), buf.size(), cudaMemcpyHostToDevice, st));
+    RS_CUDA_CHECK(cudaMemcpyAsync(posd, pos.data(), pos.size() * 4, cudaMemcpyHostToDevice, st));
+    vit_rope_freq_table(n_pos, head_dim, rope_theta, static_cast<float2*>(freq), st);
+    double flops = 0;
+    for (int i = 0; i < n_seqs; ++i) flops += 4.0 * (cu[i + 1] - cu[i]) * (cu[i + 1] - cu[i]) * head_dim * heads;
+    attention_window_tc(static_cast<const bf16*>(qkv), ld_qkv, total, static_cast<bf16*>(out), ld_out,
+                        static_cast<const AttnBlock*>(bd), static_cast<int>(plan.win_blocks.size()), heads,
+                        head_dim, scale, static_cast<const std::int32_t*>(posd), static_cast<const float2*>(freq),
+                        n_pos, flops, st);
+    RS_CUDA_CHECK(cudaStreamSynchronize(st));
+    for (void* p : {bd, posd, freq}) RS_CUDA_CHECK(cudaFreeAsync(p, st));
   });
 }
 

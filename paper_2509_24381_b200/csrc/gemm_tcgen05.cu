@@ -146,11 +146,13 @@ __device__ __forceinline__ void ws_sum32(const float* const (&parts)[kMaxParts],
   float a[32];
 #pragma unroll
   for (int i = 0; i < 32; ++i) a[i] = 0.f;
+  // partial layout: float4 (chunk, q, row) -> ((col/32) * 8 + q) * kBM + row, so
+  // a warp's 32 rows of one float4 column are 512 contiguous bytes
   for (int k = 0; k < n_parts; ++k) {
-    const float4* src = reinterpret_cast<const float4*>(parts[k] + row * BN + col);
+    const float4* src = reinterpret_cast<const float4*>(parts[k]) + (col / 32) * 8 * kBM + row;
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
-      const float4 f = __ldcg(src + q);
+      const float4 f = __ldcg(src + q * kBM);
       a[4 * q] += f.x;
       a[4 * q + 1] += f.y;
       a[4 * q + 2] += f.z;
@@ -677,7 +679,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           continue;
         }
         {
-          float* mine = part_ptr(u.split) + (quad * 32 + lane) * BN;
+          // coalesced partial layout (ws_sum32): warp stores of 512 contiguous bytes
+          float4* mine = reinterpret_cast<float4*>(part_ptr(u.split)) + quad * 32 + lane;
           constexpr int kCh = BN / 32;
           const int c0 = half == 0 ? 0 : (kCh + 1) / 2, c1 = half == 0 ? (kCh + 1) / 2 : kCh;
 #pragma unroll 1
@@ -685,10 +688,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             std::uint32_t v[32];
             sm100::tmem_ld_32x32b_x32(t_row + static_cast<std::uint32_t>(c * 32), v);
             sm100::tmem_ld_wait();
-            float4* dst = reinterpret_cast<float4*>(mine + c * 32);
+            float4* dst = mine + c * 8 * kBM;
 #pragma unroll
             for (int q = 0; q < 8; ++q)
-              __stcg(dst + q, make_float4(__uint_as_float(v[4 * q]), __uint_as_float(v[4 * q + 1]),
+              __stcg(dst + q * kBM, make_float4(__uint_as_float(v[4 * q]), __uint_as_float(v[4 * q + 1]),
                                           __uint_as_float(v[4 * q + 2]), __uint_as_float(v[4 * q + 3])));
           }
         }

@@ -355,6 +355,51 @@ def test_attention_varlen_bidir(nat, hd, heads, lens, tc):
     _close(out, ref.view(total, heads * hd))
 
 
+def _vit_rope_ref(x, pos, hd, theta):
+    """Qwen2.5-VL vision 2D RoPE (rotate-half; first hd/4 pairs use the row
+    position, the next hd/4 the column position), fp32."""
+    half, quarter = hd // 2, hd // 4
+    j = torch.arange(half, device=x.device) % quarter
+    freq = theta ** (-(4.0 * j) / hd)
+    p = torch.where(torch.arange(half, device=x.device) < quarter, pos[:, :1].float(), pos[:, 1:].float())
+    ang = (p * freq)[:, None, :]
+    c, s_ = ang.cos(), ang.sin()
+    a, b = x[..., :half], x[..., half:]
+    return torch.cat([a * c - b * s_, b * c + a * s_], -1)
+
+
+@pytest.mark.parametrize("rope", [False, True])
+@pytest.mark.parametrize("hd,heads,lens", [(80, 16, [64] * 40 + [16, 48]),  # cfg2: 64-row windows
+                                           (80, 4, [64, 64, 37, 64, 1]),     # ragged image edges
+                                           (80, 2, [128, 3, 125, 64]),       # whole 128-row tiles
+                                           (64, 4, [16, 48, 100, 28, 7])])
+def test_attention_window_tcgen05(nat, hd, heads, lens, rope):
+    """The encoder's tcgen05 / TMA window-attention kernel (attention_win.cu)
+    vs an fp32 torch reference, with and without the fused 2D RoPE."""
+    total = sum(lens)
+    g = torch.Generator(device="cuda").manual_seed(total + hd)
+    qkv = torch.randn(total, 3 * heads * hd, device="cuda", dtype=torch.bfloat16, generator=g)
+    cu = torch.tensor([0] + list(torch.tensor(lens).cumsum(0)), dtype=torch.int32, device="cuda")
+    pos = torch.randint(0, 64, (total, 2), device="cuda", dtype=torch.int32, generator=g) if rope else None
+    out = torch.empty(total, heads * hd, device="cuda", dtype=torch.bfloat16)
+    scale = 1.0 / math.sqrt(hd)
+    nat.check(nat.lib.rs_op_attention_window_tc(qkv.data_ptr(), qkv.stride(0), out.data_ptr(), out.stride(0),
+                                                cu.data_ptr(), len(lens), total, heads, hd, scale,
+                                                pos.data_ptr() if rope else None, 10000.0, _stream()))
+    torch.cuda.synchronize()
+    q, k, v = qkv.float().view(total, 3, heads, hd).unbind(1)
+    if rope:  # the kernel rotates bf16 q / k in shared memory: round like it
+        q = _vit_rope_ref(q, pos, hd, 10000.0).bfloat16().float()
+        k = _vit_rope_ref(k, pos, hd, 10000.0).bfloat16().float()
+    ref = torch.empty(total, heads, hd, device="cuda")
+    s0 = 0
+    for n in lens:
+        att = torch.einsum("qhd,khd->hqk", q[s0:s0 + n], k[s0:s0 + n]) * scale
+        ref[s0:s0 + n] = torch.einsum("hqk,khd->qhd", att.softmax(-1), v[s0:s0 + n])
+        s0 += n
+    _close(out, ref.view(total, heads * hd))
+
+
 @pytest.mark.parametrize("M", [1, 3, 8])
 @pytest.mark.parametrize("epi", [0, 1, 2, 3, 4])
 def test_gemv_small_m(nat, M, epi):
