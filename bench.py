@@ -14,7 +14,9 @@ A step = one request through the real-clock engine (encode -> tracker ->
 chunked prefill -> first-token logits); value = prompt tokens / device time
 (CUDA events, origin -> last completion) over K steps. The line also carries
 a "cfg3" block: the same Poisson request stream the N > 1 runs measure, here
-co-located, so every N reports that workload.
+co-located, so every N reports that workload; "cfg4" (the C sweep
+128-2048 over that stream) and "cfg5" (64 x M256 + T128 on the 72B-shaped LLM,
+145 GB of weights) run co-located after it — their 4E+4P placement needs 8 GPUs.
 
 N > 1 (configs[2]/[3], "cfg3"): the paper's EP deployment, one process per
 GPU — 1E+1P (N=2), 2E+2P with a 2-stage CPP pipeline (N=4), 4E+4P with 4
@@ -567,6 +569,11 @@ def run_ours(args):
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(args, reps=1)
     pipe.close()
+    if ws == 1 and args.cfg45:
+        # configs 4 / 5 (their 4E+4P placement needs 8 GPUs): co-located here,
+        # after the cfg2 context is gone (cfg5's 72B weights take 145 GB)
+        line["cfg4"] = run_cfg4(1)
+        line["cfg5"] = run_cfg5(2)
     if rank == 0:
         print(json.dumps(line))
     if ws > 1:
@@ -590,6 +597,82 @@ def run_cfg3_colocated(args, pipe, m, replay):
             runs.append((stream_stats(log), st))
         out[mode] = dict(summarize_stream(runs), rate_req_s=rate, duration_s=dur, seeds=list(seeds))
     return dict(out, placement="co-located", note="same workload as the N>1 EP lines")
+
+
+# ---- north_star configs 4 and 5 on one GPU (appended to the N = 1 line) ------------------------
+CFG5_LAYOUT = "|".join(["M256"] * 64) + "|T128"
+
+
+def run_cfg4(steps):
+    import torch
+    from paper_2509_24381_b200 import _native as N
+    from paper_2509_24381_b200 import api
+    mcfg = api.model_preset("qwen2.5-vl-7b")
+    m = {k: getattr(mcfg, k) for k, _ in N.rs_model_config._fields_}
+    pipe = api.Pipeline(mcfg, max_prompt_tokens=MAX_PROMPT, slot_tokens=1 << 19, kv_tokens=1 << 19,
+                        max_chunk_tokens=2048, max_encode_tokens=2048 + 1024)
+    replay = Replayer()
+    wl = cfg3_workload(1, CFG3["lat_rate"], CFG3["lat_duration_s"])
+    rows = []
+    for C in (128, 256, 512, 1024, 2048):
+        ns = argparse.Namespace(policy="rserve", budget=2048)
+        sc = sim_cfg(ns, m, c_tokens=C)
+        pipe.run(wl, sc, clock="real", payload_seed=1234)  # warm (plans, workspaces)
+        runs = []
+        for _ in range(steps):
+            log, journal, st = pipe.run(wl, sc, clock="real", payload_seed=1234)
+            replay.check(wl, sc, log, journal)
+            runs.append((stream_stats(log), st))
+        s = summarize_stream(runs)
+        rows.append({"C": C, "ttft_p50_ms": s["ttft_ms"]["p50"], "ttft_p99_ms": s["ttft_ms"]["p99"],
+                     "tokens_per_s": s["tokens_per_s"], "requests": s["requests"] // steps,
+                     "all_completed": s["all_completed"]})
+        print(json.dumps(rows[-1]), file=sys.stderr, flush=True)
+    pipe.close()
+    return {"workload": "cfg4: cfg3 stream (alternating, U[4,16] x M1024, text U[32,256], Poisson "
+                        f"{CFG3['lat_rate']} req/s for {CFG3['lat_duration_s']} s, seed 1), "
+                        "7B-shaped, B=2048, co-located on 1 GPU (the paper's 4E+4P needs 8)",
+            "sweep": rows, **replay.summary()}
+
+
+def run_cfg5(steps):
+    import torch
+    from paper_2509_24381_b200 import _native as N
+    from paper_2509_24381_b200 import api
+    mcfg = api.model_preset("qwen2.5-vl-72b-llm")
+    m = {k: getattr(mcfg, k) for k, _ in N.rs_model_config._fields_}
+    T = 64 * 256 + 128
+    pipe = api.Pipeline(mcfg, max_prompt_tokens=T, slot_tokens=T + 4096, kv_tokens=T + 4096,
+                        max_chunk_tokens=2048, max_encode_tokens=1024)
+    wl = f"0,0,-,{CFG5_LAYOUT}\n"
+    ns = argparse.Namespace(policy="rserve", budget=2048)
+    sc = sim_cfg(ns, m, c_tokens=1024)
+    replay = Replayer()
+    enc_f, pre_f, T2 = layout_flops(m, CFG5_LAYOUT)
+    assert T2 == T
+    for _ in range(2):
+        pipe.run(wl, sc, clock="real", payload_seed=99)
+    ttfts, dev = [], []
+    for _ in range(steps):
+        log, journal, st = pipe.run(wl, sc, clock="real", payload_seed=99)
+        replay.check(wl, sc, log, journal)
+        rec = api.parse_decision_log(log)["req"][0]
+        ttfts.append(float(rec["ttft"]))
+        dev.append(st["gpu_ms"])
+    logits, am = pipe.logits(0)
+    pipe.close()
+    ttfts.sort()
+    peak = peaks()[0]
+    bound_ms = (enc_f + pre_f) / (peak * 1e12) * 1e3
+    p50 = nearest_rank(ttfts, 50)
+    return {"workload": "cfg5: ConsecutiveMm 64 x M256 + T128 = 16512 tokens, 72B-shaped LLM + 1280-wide ViT "
+                        "(random init), C=1024, B=2048, rserve, co-located on 1 GPU (the paper's 4E+4P needs 8)",
+            "ttft_ms": {"p50": p50, "p99": nearest_rank(ttfts, 99), "per_step": [round(t, 2) for t in ttfts]},
+            "tokens_per_s": T / (p50 / 1e3),
+            "tflop_per_request": {"encode": enc_f / 1e12, "prefill": pre_f / 1e12},
+            "roofline": {"bound_ms_burst_peak": bound_ms, "frac": bound_ms / p50, "peak_tflops": peak},
+            "logits_finite": bool(torch.isfinite(torch.as_tensor(logits)).all()), "argmax": am,
+            **replay.summary()}
 
 
 # ---- our arm, N > 1: EP deployment -----------------------------------------------------------
@@ -947,6 +1030,7 @@ def main():
                     help="nvidia-smi sampling interval during the timed steps")
     ap.add_argument("--decode-steps", type=int, default=32,
                     help="greedy decode steps after the first token (0: skip)")
+    ap.add_argument("--cfg45", type=int, default=1, help="N=1: also run cfg4 (C sweep) and cfg5 (72B) (0: skip)")
     ap.add_argument("--launch-list", action="store_true",
                     help="run only the warm-up + timed steps (for the ncu launch list); no JSON bench line")
     ap.add_argument("--ep", action="store_true", help="(compat) same as --mode ep")

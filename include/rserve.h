@@ -303,6 +303,30 @@ RS_API rs_status rs_decode(rs_ctx* ctx, const uint64_t* request_ids, int32_t n_r
                            double* out_ms);
 RS_API rs_status rs_decode_release(rs_ctx* ctx, uint64_t request_id);
 
+/* ---- PD (prefill -> decode) KV transfer -------------------
+ * The paper serves EPD-disaggregated (§5.1: encode, prefill and
+ * decode on separate nodes); the reference stops at the first token. A
+ * request kept after its prefill (keep_kv) is exported as one contiguous
+ * device image — a 64-byte header (first token, next M-RoPE id) followed by
+ * its paged KV, [tp shard][layer][page][K page | V^T page] — which the
+ * caller moves to the decode GPU (NCCL send/recv, CUDA IPC, cudaMemcpyPeer),
+ * and imported there as a kept request that rs_decode continues. Both
+ * contexts must hold the same LLM layers / kv heads / TP; the importer needs
+ * the whole LLM and its head. Export leaves the source request kept (free it
+ * with rs_decode_release). Both calls enqueue on `stream` (NULL: the
+ * context's aux stream) and return without synchronising.              */
+typedef struct rs_kv_meta {
+  uint64_t tokens;       /* KV length (prompt tokens)                        */
+  uint64_t image_bytes;  /* header + KV pages                               */
+  int32_t next_rope;     /* M-RoPE id of the next generated token            */
+  int32_t layer_begin, layer_end, kv_heads, head_dim, page_tokens, tp_size;
+} rs_kv_meta;
+RS_API rs_status rs_kv_image_bytes(rs_ctx* ctx, uint64_t tokens, uint64_t* out_bytes);
+RS_API rs_status rs_kv_export(rs_ctx* ctx, uint64_t request_id, void* dst_dev, uint64_t cap_bytes,
+                              rs_kv_meta* out_meta, void* stream);
+RS_API rs_status rs_kv_import(rs_ctx* ctx, uint64_t request_id, const rs_kv_meta* meta,
+                              const void* src_dev, void* stream);
+
 /* ---- payload files ---------------------------------------
  * The reference's workload file (workload.hpp:217-265) carries layouts only.
  * A payload file beside it pins per-segment inputs: image grids and pixel

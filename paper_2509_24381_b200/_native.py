@@ -238,6 +238,17 @@ _sig("rs_payload_validate", [C.c_char_p, C.c_char_p, C.c_int32, PCHAR])
 _sig("rs_decode", [C.c_void_p, C.POINTER(C.c_uint64), C.c_int32, C.c_int32, C.POINTER(C.c_int32),
                   C.POINTER(C.c_float), C.POINTER(C.c_double)])
 _sig("rs_decode_release", [C.c_void_p, C.c_uint64])
+
+
+class rs_kv_meta(C.Structure):
+    _fields_ = [("tokens", C.c_uint64), ("image_bytes", C.c_uint64), ("next_rope", C.c_int32),
+                ("layer_begin", C.c_int32), ("layer_end", C.c_int32), ("kv_heads", C.c_int32),
+                ("head_dim", C.c_int32), ("page_tokens", C.c_int32), ("tp_size", C.c_int32)]
+
+
+_sig("rs_kv_image_bytes", [C.c_void_p, C.c_uint64, C.POINTER(C.c_uint64)])
+_sig("rs_kv_export", [C.c_void_p, C.c_uint64, C.c_void_p, C.c_uint64, C.POINTER(rs_kv_meta), C.c_void_p])
+_sig("rs_kv_import", [C.c_void_p, C.c_uint64, C.POINTER(rs_kv_meta), C.c_void_p, C.c_void_p])
 _sig("rs_profile_drain", [PCHAR])
 
 

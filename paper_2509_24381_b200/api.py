@@ -383,6 +383,23 @@ class Pipeline:
     def decode_release(self, request_id: int):
         N.check(N.lib.rs_decode_release(self.h, request_id))
 
+    # PD (prefill -> decode) KV transfer (rserve.h rs_kv_export / rs_kv_import)
+    def kv_image_bytes(self, tokens: int) -> int:
+        out = C.c_uint64()
+        N.check(N.lib.rs_kv_image_bytes(self.h, tokens, C.byref(out)))
+        return out.value
+
+    def kv_export(self, request_id: int, dst_ptr: int, cap_bytes: int, stream: int = 0) -> "N.rs_kv_meta":
+        """Packs a kept request's KV (+ first token) into the device buffer
+        dst_ptr; enqueued on `stream` (0: the context's aux stream)."""
+        meta = N.rs_kv_meta()
+        N.check(N.lib.rs_kv_export(self.h, request_id, dst_ptr, cap_bytes, C.byref(meta), stream or None))
+        return meta
+
+    def kv_import(self, request_id: int, meta: "N.rs_kv_meta", src_ptr: int, stream: int = 0):
+        """Creates kept request `request_id` from a KV image (device pointer)."""
+        N.check(N.lib.rs_kv_import(self.h, request_id, C.byref(meta), src_ptr, stream or None))
+
     def run(self, workload: str, cfg: SimConfig, clock: str = "lockstep", e2e: bool = False,
             payload_seed: int = 7, serialize: bool = False, payload: Optional[str] = None,
             keep_kv: bool = False):

@@ -435,14 +435,17 @@ __global__ void __launch_bounds__(kWinThreads, 1)
         for (int i = 0; i < 32; ++i) zeros[i] = 0u;
         sm100::tmem_st_32x32b_x32(srow + 32 * (1 - half), zeros);
       } else {  // windows across the halves: max over both, then exp per half
-        load_half(0, sv);
-        const float mx0 = half_max(sv);
+        // P of half h lands on S columns [32 h, 32 h + 32): half 0's P only
+        // covers S columns half 0 has already consumed, half 1's would
+        // overwrite half 0's upper S columns, so half 0 is exponentiated first
         load_half(1, sv);
-        const float mx = fmaxf(mx0, half_max(sv));
+        const float mx1 = half_max(sv);
+        load_half(0, sv);
+        const float mx = fmaxf(mx1, half_max(sv));
         const float mneg = mx == -INFINITY ? 0.f : -mx * p.scale_log2;
-        l = exp_half(1, sv, mneg);
-        load_half(0, sv);  // (re-read: one half of S in registers at a time)
-        l += exp_half(0, sv, mneg);
+        l = exp_half(0, sv, mneg);
+        load_half(1, sv);  // (re-read: one half of S in registers at a time; S columns 64-127 intact)
+        l += exp_half(1, sv, mneg);
       }
       sm100::tmem_st_wait();
       sm100::tc_fence_before();

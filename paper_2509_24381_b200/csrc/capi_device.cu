@@ -331,3 +331,34 @@ rs_status rs_decode_release(rs_ctx* c, uint64_t request_id) {
 }
 
 }  // extern "C"
+
+extern "C" {
+
+rs_status rs_kv_image_bytes(rs_ctx* c, uint64_t tokens, uint64_t* out_bytes) {
+  return guarded([&] {
+    rs_ctx& x = need(c);
+    if (out_bytes == nullptr) throw lmmsim::ConfigError("rs_kv_image_bytes: null output");
+    *out_bytes = x.ctx->kv_image_bytes(tokens);
+  });
+}
+
+rs_status rs_kv_export(rs_ctx* c, uint64_t request_id, void* dst_dev, uint64_t cap_bytes, rs_kv_meta* out_meta,
+                       void* stream) {
+  return guarded([&] {
+    rs_ctx& x = need(c);
+    if (dst_dev == nullptr || out_meta == nullptr) throw lmmsim::ConfigError("rs_kv_export: null buffer / meta");
+    cudaStream_t st = stream != nullptr ? static_cast<cudaStream_t>(stream) : x.ctx->aux_stream();
+    x.ctx->export_kv(request_id, dst_dev, cap_bytes, out_meta, st);
+  });
+}
+
+rs_status rs_kv_import(rs_ctx* c, uint64_t request_id, const rs_kv_meta* meta, const void* src_dev, void* stream) {
+  return guarded([&] {
+    rs_ctx& x = need(c);
+    if (src_dev == nullptr || meta == nullptr) throw lmmsim::ConfigError("rs_kv_import: null image / meta");
+    cudaStream_t st = stream != nullptr ? static_cast<cudaStream_t>(stream) : x.ctx->aux_stream();
+    x.ctx->import_kv(request_id, *meta, src_dev, st);
+  });
+}
+
+}  // extern "C"

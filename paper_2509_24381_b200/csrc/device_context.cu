@@ -630,3 +630,136 @@ void Context::copy_logits(int slot, float* host, cudaStream_t st) {
 }
 
 }  // namespace rserve
+
+// ---- PD (prefill -> decode) KV transfer ----------------------------------------
+namespace rserve {
+namespace {
+constexpr std::uint64_t kKvImageHeader = 64;  // [0] first token (i32), [4] next M-RoPE id, [8] tokens (u64)
+}
+
+std::uint64_t Context::kv_image_bytes(std::uint64_t tokens) const {
+  if (!llm_) throw lmmsim::ConfigError("KV image: this context holds no LLM layers");
+  const Shapes& ls = llm_->shapes();
+  const std::uint64_t pages = (tokens + kPageTokens - 1) / kPageTokens;
+  const std::uint64_t page_bytes = static_cast<std::uint64_t>(ls.hkv) * kPageTokens * ls.hd * 2;
+  const std::uint64_t shards = 1 + tp_shards_.size();
+  const std::uint64_t layers = static_cast<std::uint64_t>(llm_->layer_end() - llm_->layer_begin());
+  return kKvImageHeader + shards * layers * pages * 2 * page_bytes;
+}
+
+namespace {
+// (src, dst) page pairs of a request's KV image, in image order.
+std::vector<PageCopy> kv_image_pages(const std::vector<Llm*>& shards, const std::vector<int>& kv_pages,
+                                     std::uint64_t n_pages, std::uint8_t* image, std::size_t page_bytes,
+                                     bool to_image) {
+  std::vector<PageCopy> list;
+  list.reserve(shards.size() * n_pages * 2 * 80);
+  std::uint8_t* cur = image + kKvImageHeader;
+  for (Llm* sh : shards) {
+    for (int l = sh->layer_begin(); l < sh->layer_end(); ++l) {
+      for (std::uint64_t i = 0; i < n_pages; ++i) {
+        for (int kv = 0; kv < 2; ++kv) {
+          std::uint8_t* page = reinterpret_cast<std::uint8_t*>(kv == 0 ? sh->k_cache(l) : sh->v_cache(l)) +
+                               static_cast<std::size_t>(kv_pages[i]) * page_bytes;
+          list.push_back(to_image ? PageCopy{page, cur} : PageCopy{cur, page});
+          cur += page_bytes;
+        }
+      }
+    }
+  }
+  return list;
+}
+}  // namespace
+
+void Context::export_kv(lmmsim::RequestId id, void* dst, std::uint64_t cap, rs_kv_meta* meta, cudaStream_t st) {
+  DevRequest& r = get(id);
+  if (!llm_ || !llm_->has_head())
+    throw lmmsim::ConfigError("KV export: the request's first token lives on the last stage (needs the LM head)");
+  if (r.kv_pages.empty()) throw lmmsim::InternalError("KV export: request " + lmmsim::format_u64(id) + " holds no KV");
+  const std::uint64_t bytes = kv_image_bytes(r.total);
+  if (cap < bytes)
+    throw lmmsim::ConfigError("KV export: buffer of " + lmmsim::format_u64(cap) + " bytes < image of " +
+                              lmmsim::format_u64(bytes));
+  if (r.next_rope < 0) {  // as Context::decode: generated text continues after the prompt's max id
+    std::int32_t mx = -1;
+    for (const auto& p : r.rope) mx = std::max({mx, p[0], p[1], p[2]});
+    r.next_rope = mx + 1;
+  }
+  const Shapes& ls = llm_->shapes();
+  const std::size_t page_bytes = static_cast<std::size_t>(ls.hkv) * kPageTokens * ls.hd * 2;
+  const std::uint64_t n_pages = (r.total + kPageTokens - 1) / kPageTokens;
+  std::vector<Llm*> shards{llm_.get()};
+  for (auto& p : tp_shards_) shards.push_back(p.get());
+  auto* image = static_cast<std::uint8_t*>(dst);
+  const std::vector<PageCopy> list = kv_image_pages(shards, r.kv_pages, n_pages, image, page_bytes, true);
+  struct {
+    std::int32_t rope;
+    std::int32_t pad;
+    std::uint64_t tokens;
+  } hdr{r.next_rope, 0, r.total};
+  RS_CUDA_CHECK(cudaMemcpyAsync(image, llm_->argmax_dev() + r.slot, 4, cudaMemcpyDeviceToDevice, st));
+  RS_CUDA_CHECK(cudaMemcpyAsync(image + 4, up_.put(&hdr, sizeof hdr, st), sizeof hdr, cudaMemcpyDeviceToDevice, st));
+  const auto* ld = static_cast<const PageCopy*>(up_.put(list.data(), list.size() * sizeof(PageCopy), st));
+  copy_pages(ld, static_cast<int>(list.size()), page_bytes, st, "kv_image_pack");
+  up_.fence(st);
+  rs_kv_meta m{};
+  m.tokens = r.total;
+  m.image_bytes = bytes;
+  m.next_rope = r.next_rope;
+  m.layer_begin = llm_->layer_begin();
+  m.layer_end = llm_->layer_end();
+  m.kv_heads = ls.hkv * static_cast<int>(shards.size());
+  m.head_dim = ls.hd;
+  m.page_tokens = kPageTokens;
+  m.tp_size = static_cast<int>(shards.size());
+  *meta = m;
+}
+
+void Context::import_kv(lmmsim::RequestId id, const rs_kv_meta& meta, const void* src, cudaStream_t st) {
+  if (!llm_ || !llm_->has_head() || llm_->layer_begin() != 0)
+    throw lmmsim::ConfigError("KV import: decode needs the whole LLM and its head on this context");
+  if (find(id) != nullptr) throw lmmsim::RegistryError("duplicate request id " + lmmsim::format_u64(id));
+  const Shapes& ls = llm_->shapes();
+  const int shards_n = 1 + static_cast<int>(tp_shards_.size());
+  if (meta.layer_begin != llm_->layer_begin() || meta.layer_end != llm_->layer_end() ||
+      meta.kv_heads != ls.hkv * shards_n || meta.head_dim != ls.hd || meta.page_tokens != kPageTokens ||
+      meta.tp_size != shards_n)
+    throw lmmsim::ConfigError("KV import: image of layers [" + std::to_string(meta.layer_begin) + ", " +
+                              std::to_string(meta.layer_end) + "), " + std::to_string(meta.kv_heads) +
+                              " kv heads x " + std::to_string(meta.head_dim) + ", TP " +
+                              std::to_string(meta.tp_size) + " does not match this context");
+  if (meta.tokens == 0 || meta.tokens > opt_.kv_tokens)
+    throw lmmsim::ConfigError("KV import: " + lmmsim::format_u64(meta.tokens) + " tokens exceed the KV pool");
+  if (meta.image_bytes != kv_image_bytes(meta.tokens)) throw lmmsim::InputError("KV import: image size mismatch");
+  auto owned = std::make_unique<DevRequest>();
+  DevRequest& r = *owned;
+  r.id = id;
+  r.total = meta.tokens;
+  r.next_rope = meta.next_rope;
+  r.slot_freed_tokens = r.total;  // no embedding slot on the decode side
+  r.slot = take_request_slot();
+  const std::int64_t pages = static_cast<std::int64_t>((r.total + kPageTokens - 1) / kPageTokens);
+  std::vector<cudaEvent_t> guards;
+  r.kv_pages = kv_pages_.take(pages, guards);
+  for (cudaEvent_t g : guards) RS_CUDA_CHECK(cudaStreamWaitEvent(st, g, 0));
+  RS_CUDA_CHECK(cudaMallocAsync(reinterpret_cast<void**>(&r.kv_table), static_cast<std::size_t>(pages) * 4, st));
+  RS_CUDA_CHECK(cudaMemcpyAsync(r.kv_table, up_.put(r.kv_pages.data(), r.kv_pages.size() * 4, st),
+                                r.kv_pages.size() * 4, cudaMemcpyDeviceToDevice, st));
+  RS_CUDA_CHECK(cudaMemcpyAsync(page_tables_dev_ + r.slot, up_.put(&r.kv_table, sizeof(int*), st), sizeof(int*),
+                                cudaMemcpyDeviceToDevice, st));
+  page_tables_host_[static_cast<std::size_t>(r.slot)] = r.kv_table;
+  // the prefill's first token -> this slot's argmax (rs_decode embeds it first)
+  RS_CUDA_CHECK(cudaMemcpyAsync(llm_->argmax_dev() + r.slot, src, 4, cudaMemcpyDeviceToDevice, st));
+  std::vector<Llm*> shards{llm_.get()};
+  for (auto& p : tp_shards_) shards.push_back(p.get());
+  const std::size_t page_bytes = static_cast<std::size_t>(ls.hkv) * kPageTokens * ls.hd * 2;
+  const std::vector<PageCopy> list =
+      kv_image_pages(shards, r.kv_pages, static_cast<std::uint64_t>(pages),
+                     static_cast<std::uint8_t*>(const_cast<void*>(src)), page_bytes, false);
+  const auto* ld = static_cast<const PageCopy*>(up_.put(list.data(), list.size() * sizeof(PageCopy), st));
+  copy_pages(ld, static_cast<int>(list.size()), page_bytes, st, "kv_image_unpack");
+  up_.fence(st);
+  reqs_.emplace(id, std::move(owned));
+}
+
+}  // namespace rserve

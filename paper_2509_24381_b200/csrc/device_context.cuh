@@ -163,6 +163,16 @@ class Context {
                 float* out_logits, cudaStream_t st);
   /// Frees a request kept for decode (KV pages, tables, request slot).
   void free_kept(lmmsim::RequestId id);
+  // ---- PD (prefill -> decode) KV transfer ----
+  /// Bytes of a kept request's KV image: [shard][layer][page][K | V^T page].
+  std::uint64_t kv_image_bytes(std::uint64_t tokens) const;
+  /// Packs a kept request's KV pages (+ its first token) into `dst` (device,
+  /// >= kv_image_bytes + kKvImageHeader) on `st`; fills the host metadata.
+  void export_kv(lmmsim::RequestId id, void* dst, std::uint64_t cap, rs_kv_meta* meta, cudaStream_t st);
+  /// Creates kept request `id` from an image exported by a context with the
+  /// same LLM (layers, kv heads, TP): KV pages unpacked, first token into its
+  /// argmax slot; rs_decode continues it.
+  void import_kv(lmmsim::RequestId id, const rs_kv_meta& meta, const void* src, cudaStream_t st);
   void prefill(const std::vector<SliceRef>& slices, bf16* x, cudaStream_t st,
                int layer_from = -1, int layer_to = -1);
   std::uint64_t chunk_flops(const std::vector<SliceRef>& slices) const;

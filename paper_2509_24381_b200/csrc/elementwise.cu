@@ -628,6 +628,39 @@ void fill_uniform_interleaved(bf16* dst, int rows_valid, int rows_pad, int cols,
   count_launch();
 }
 
+__global__ void __launch_bounds__(256) copy_pages_kernel(const PageCopy* __restrict__ list, int n,
+                                                         int vec_per_page) {
+  pdl_wait();
+  pdl_launch_dependents();
+  for (int pg = blockIdx.x; pg < n; pg += gridDim.x) {
+    const PageCopy c = list[pg];
+    const uint4* src = static_cast<const uint4*>(c.src);
+    uint4* dst = static_cast<uint4*>(c.dst);
+    int i = threadIdx.x;
+    for (; i + 3 * 256 < vec_per_page; i += 4 * 256) {  // 4 loads in flight per thread
+      const uint4 a = __ldcs(src + i), b = __ldcs(src + i + 256), d = __ldcs(src + i + 512),
+                  e = __ldcs(src + i + 768);
+      __stcs(dst + i, a);
+      __stcs(dst + i + 256, b);
+      __stcs(dst + i + 512, d);
+      __stcs(dst + i + 768, e);
+    }
+    for (; i < vec_per_page; i += 256) __stcs(dst + i, __ldcs(src + i));
+  }
+}
+
+void copy_pages(const PageCopy* list_dev, int n, std::size_t page_bytes, cudaStream_t st, const char* label) {
+  if (n <= 0) return;
+  if (page_bytes % 16 != 0) throw DeviceError(RS_ERR_CUDA, "copy_pages: page bytes must be a multiple of 16");
+  const int tok = prof::begin(st);
+  const int grid = std::min(n, 8 * kNumSMs);
+  launch_kernel(copy_pages_kernel, dim3(grid), dim3(256), 0, st, 1, list_dev, n,
+                static_cast<int>(page_bytes / 16));
+  RS_LAUNCH_CHECK();
+  prof::end(tok, st, label, 0, 2.0 * static_cast<double>(page_bytes) * n);
+  count_launch();
+}
+
 __global__ void gather_slots_i32_kernel(const std::int32_t* src, const std::int32_t* idx, int n,
                                         std::int32_t* out) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) out[i] = src[idx[i]];

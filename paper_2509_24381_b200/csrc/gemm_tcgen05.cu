@@ -347,7 +347,10 @@ __device__ __forceinline__ void epilogue_tile_tma(const GemmParams& p, const CUt
       }
     }
     if constexpr (kRes) {
-      sm100::mbar_wait(&rbar[b], (rphase >> b) & 1);
+      // lane 0 waits for the residual tile's TMA bytes, __syncwarp orders the
+      // other lanes' smem reads after it
+      if (lane == 0) sm100::mbar_wait(&rbar[b], (rphase >> b) & 1);
+      __syncwarp();
       rphase ^= 1u << b;
 #pragma unroll
       for (int q = 0; q < 4; ++q) {

@@ -125,6 +125,15 @@ void gather_slots_i32(const std::int32_t* src, const std::int32_t* idx, int n, s
 void bitmap_set_ranges(std::uint32_t* bitmap, const std::uint64_t* ranges, int n_ranges,
                        cudaStream_t st);
 
+// ---- PD KV transfer -------------------------------------------------------------------
+struct PageCopy {  // one KV page: src -> dst, page_bytes each (16-byte aligned)
+  const void* src;
+  void* dst;
+};
+/// Copies n pages of page_bytes (multiple of 16) — the KV image pack / unpack
+/// (one CTA per page, 16-byte vector loads: HBM-bound). label: profiler class.
+void copy_pages(const PageCopy* list_dev, int n, std::size_t page_bytes, cudaStream_t st, const char* label);
+
 // ---- LM head helpers ---------------------------------------------------------------------
 /// out[row(i)] = argmax(logits[row(i), :vocab]) (first max); row(i) =
 /// rows_idx ? rows_idx[i] : i.

@@ -180,6 +180,10 @@ class Llm {
   int layer_begin() const { return lb_; }
   int layer_end() const { return le_; }
   bool has_head() const { return head_ != nullptr; }
+  /// Paged KV of local layer l in [layer_begin, layer_end): K [pages][hkv][page][hd],
+  /// V^T [pages][hkv][hd][page] (this shard's kv heads).
+  bf16* k_cache(int l) const { return layers_[static_cast<std::size_t>(l - lb_)].k_cache; }
+  bf16* v_cache(int l) const { return layers_[static_cast<std::size_t>(l - lb_)].v_cache; }
   std::uint64_t dense_flops(std::uint64_t tokens) const;
 
  private:
