@@ -159,6 +159,9 @@ typedef struct rs_ctx_options {
   int32_t with_vit;            /* allocate the vision encoder here           */
   int32_t with_lm_head;        /* allocate final norm + LM head here         */
   int32_t tp_size;             /* tensor-parallel LLM shards (0/1 = none); all on `device` (loopback) */
+  int32_t tp_rank;             /* tp_group: this context's rank in [0, tp_size)          */
+  int32_t tp_group;            /* 1: one rank of a tp_size-rank TP group (one shard here,
+                                  peers in other processes / GPUs, rs_tp_connect)         */
 } rs_ctx_options;
 
 RS_API rs_status rs_ctx_create(const rs_model_config* model, const rs_ctx_options* opt,
@@ -302,6 +305,32 @@ RS_API rs_status rs_decode(rs_ctx* ctx, const uint64_t* request_ids, int32_t n_r
                            int32_t n_steps, int32_t* out_tokens, float* out_logits,
                            double* out_ms);
 RS_API rs_status rs_decode_release(rs_ctx* ctx, uint64_t request_id);
+
+/* ---- tensor parallelism across GPUs ------------------------
+ * The reference models TP only as stage_time_ms / tp_speedup
+ * (cost_model.hpp:35-36,76-82). A TP group is tp_size contexts created with
+ * tp_group = 1, one per GPU (one process each, or several in one process):
+ * rank r holds q / kv heads [r H/T, (r+1) H/T) and SwiGLU width slice r, O /
+ * down by input columns. Each layer's O and down partials go to the rank's
+ * exchange buffer; a reduction kernel signals every rank through flags in
+ * peer memory (release / acquire, system scope) and sums the T partials in
+ * rank order straight over NVLink — the same bf16 residual on every rank, no
+ * NCCL. Setup: every rank exports its buffer (rs_tp_buffer: device pointer +
+ * CUDA IPC handle), the caller exchanges them (e.g. torch.distributed
+ * all_gather), and every rank calls rs_tp_connect(ptrs, handles) — ptrs[r]
+ * for ranks of this process, the IPC handle otherwise. Requests on a rank are
+ * KV-only (rs_kv_request_create); rs_tp_prefill runs one chunk whose input
+ * rows [M, d] (bf16, device, the chunk's embeddings — the tracker lives on
+ * the engine's rank) are updated in place to the last layer's residual; the
+ * rank(s) created with_lm_head produce first-token logits (rs_tp_logits).
+ * rs_tp_prefill only enqueues (on `stream`, NULL = the context's aux stream):
+ * every rank must issue the same chunk sequence.                          */
+RS_API rs_status rs_tp_buffer(rs_ctx* ctx, void** out_dev_ptr, void* out_ipc_handle /* 64 B */);
+RS_API rs_status rs_tp_connect(rs_ctx* ctx, const void* const* peer_ptrs, const void* ipc_handles);
+RS_API rs_status rs_kv_request_create(rs_ctx* ctx, uint64_t id, const char* layout);
+RS_API rs_status rs_tp_prefill(rs_ctx* ctx, const uint64_t* slices, int32_t n_slices, void* x_dev,
+                               void* stream);
+RS_API rs_status rs_tp_logits(rs_ctx* ctx, uint64_t id, float* out_host, int32_t* out_argmax);
 
 /* ---- PD (prefill -> decode) KV transfer -------------------
  * The paper serves EPD-disaggregated (§5.1: encode, prefill and

@@ -119,7 +119,8 @@ class rs_ctx_options(C.Structure):
                 ("slot_tokens", C.c_uint64), ("kv_tokens", C.c_uint64),
                 ("max_chunk_tokens", C.c_uint64), ("max_encode_tokens", C.c_uint64),
                 ("layer_begin", C.c_int32), ("layer_end", C.c_int32), ("with_vit", C.c_int32),
-                ("with_lm_head", C.c_int32), ("tp_size", C.c_int32)]
+                ("with_lm_head", C.c_int32), ("tp_size", C.c_int32), ("tp_rank", C.c_int32),
+                ("tp_group", C.c_int32)]
 
 
 class rs_run_options(C.Structure):
@@ -246,6 +247,11 @@ class rs_kv_meta(C.Structure):
                 ("head_dim", C.c_int32), ("page_tokens", C.c_int32), ("tp_size", C.c_int32)]
 
 
+_sig("rs_tp_buffer", [C.c_void_p, C.POINTER(C.c_void_p), C.c_void_p])
+_sig("rs_tp_connect", [C.c_void_p, C.POINTER(C.c_void_p), C.c_void_p])
+_sig("rs_kv_request_create", [C.c_void_p, C.c_uint64, C.c_char_p])
+_sig("rs_tp_prefill", [C.c_void_p, C.POINTER(C.c_uint64), C.c_int32, C.c_void_p, C.c_void_p])
+_sig("rs_tp_logits", [C.c_void_p, C.c_uint64, C.POINTER(C.c_float), C.POINTER(C.c_int32)])
 _sig("rs_kv_image_bytes", [C.c_void_p, C.c_uint64, C.POINTER(C.c_uint64)])
 _sig("rs_kv_export", [C.c_void_p, C.c_uint64, C.c_void_p, C.c_uint64, C.POINTER(rs_kv_meta), C.c_void_p])
 _sig("rs_kv_import", [C.c_void_p, C.c_uint64, C.POINTER(rs_kv_meta), C.c_void_p, C.c_void_p])

@@ -228,7 +228,8 @@ class Pipeline:
     def __init__(self, model: N.rs_model_config, device: int = 0, max_prompt_tokens: int = 32768,
                  slot_tokens: int = 65536, kv_tokens: int = 65536, max_chunk_tokens: int = 2048,
                  max_encode_tokens: int = 2048, layer_begin: int = 0, layer_end: int = 0,
-                 with_vit: bool = True, with_lm_head: bool = True, tp_size: int = 1):
+                 with_vit: bool = True, with_lm_head: bool = True, tp_size: int = 1,
+                 tp_rank: int = 0, tp_group: bool = False):
         self.model = model
         o = N.rs_ctx_options()
         o.device = device
@@ -242,6 +243,8 @@ class Pipeline:
         o.with_vit = int(with_vit)
         o.with_lm_head = int(with_lm_head)
         o.tp_size = tp_size
+        o.tp_rank = tp_rank
+        o.tp_group = int(tp_group)
         self.opts = o
         h = C.c_void_p()
         N.check(N.lib.rs_ctx_create(C.byref(model), C.byref(o), C.byref(h)))
@@ -382,6 +385,40 @@ class Pipeline:
 
     def decode_release(self, request_id: int):
         N.check(N.lib.rs_decode_release(self.h, request_id))
+
+    # tensor parallelism across GPUs (rserve.h rs_tp_*)
+    def tp_buffer(self):
+        """(device pointer, 64-byte CUDA IPC handle) of this rank's exchange buffer."""
+        ptr = C.c_void_p()
+        handle = (C.c_uint8 * 64)()
+        N.check(N.lib.rs_tp_buffer(self.h, C.byref(ptr), handle))
+        return ptr.value, bytes(handle)
+
+    def tp_connect(self, ptrs, handles=None):
+        """ptrs[r]: rank r's buffer when it lives in this process (else None);
+        handles[r]: its IPC handle (64 bytes) otherwise."""
+        T = len(ptrs)
+        arr = (C.c_void_p * T)(*[p or None for p in ptrs])
+        hb = None
+        if handles is not None:
+            hb = (C.c_uint8 * (64 * T)).from_buffer_copy(b"".join(h or bytes(64) for h in handles))
+        N.check(N.lib.rs_tp_connect(self.h, arr, hb))
+
+    def kv_request_create(self, req_id: int, layout: str):
+        N.check(N.lib.rs_kv_request_create(self.h, req_id, layout.encode()))
+
+    def tp_prefill(self, slices, x_ptr: int, stream: int = 0):
+        """Enqueue one chunk on this TP rank: slices [(id, start, end)], x_ptr the
+        chunk's input rows [M, d] bf16 (device; updated in place)."""
+        flat = (C.c_uint64 * (3 * len(slices)))(*[v for s in slices for v in s])
+        N.check(N.lib.rs_tp_prefill(self.h, flat, len(slices), x_ptr, stream or None))
+
+    def tp_logits(self, req_id: int):
+        import numpy as np
+        out = np.empty(self.model.vocab, dtype=np.float32)
+        am = C.c_int32()
+        N.check(N.lib.rs_tp_logits(self.h, req_id, out.ctypes.data_as(C.POINTER(C.c_float)), C.byref(am)))
+        return out, am.value
 
     # PD (prefill -> decode) KV transfer (rserve.h rs_kv_export / rs_kv_import)
     def kv_image_bytes(self, tokens: int) -> int:

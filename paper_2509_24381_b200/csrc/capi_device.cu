@@ -362,3 +362,69 @@ rs_status rs_kv_import(rs_ctx* c, uint64_t request_id, const rs_kv_meta* meta, c
 }
 
 }  // extern "C"
+
+// ---- tensor parallelism across GPUs -------------------------------------------
+extern "C" {
+
+rs_status rs_tp_buffer(rs_ctx* c, void** out_dev_ptr, void* out_ipc_handle) {
+  return guarded([&] {
+    rs_ctx& x = need(c);
+    x.ctx->tp_buffer(out_dev_ptr, static_cast<cudaIpcMemHandle_t*>(out_ipc_handle));
+  });
+}
+
+rs_status rs_tp_connect(rs_ctx* c, const void* const* peer_ptrs, const void* ipc_handles) {
+  return guarded([&] {
+    rs_ctx& x = need(c);
+    x.ctx->tp_connect(peer_ptrs, static_cast<const cudaIpcMemHandle_t*>(ipc_handles));
+  });
+}
+
+rs_status rs_kv_request_create(rs_ctx* c, uint64_t id, const char* layout) {
+  return guarded([&] {
+    rs_ctx& x = need(c);
+    lmmsim::RequestSpec req;
+    req.id = id;
+    req.segments = lmmsim::parse_layout(layout ? layout : "");
+    req.validate();
+    x.ctx->create_kv_request(req, x.ctx->aux_stream());
+  });
+}
+
+rs_status rs_tp_prefill(rs_ctx* c, const uint64_t* slices, int32_t n_slices, void* x_dev, void* stream) {
+  return guarded([&] {
+    rs_ctx& x = need(c);
+    if (x_dev == nullptr || slices == nullptr || n_slices <= 0)
+      throw lmmsim::ConfigError("rs_tp_prefill: need slices and the chunk's input rows");
+    std::vector<SliceRef> refs;
+    std::uint64_t total = 0;
+    for (int i = 0; i < n_slices; ++i) {
+      const std::uint64_t b = slices[3 * i + 1], e = slices[3 * i + 2];
+      DevRequest& r = x.ctx->get(slices[3 * i]);
+      if (e <= b || e > r.total)
+        throw lmmsim::InternalError("rs_tp_prefill: slice [" + lmmsim::format_u64(b) + "," + lmmsim::format_u64(e) +
+                                    ") outside request " + lmmsim::format_u64(r.id));
+      refs.push_back({&r, b, e});
+      total += e - b;
+    }
+    if (total > x.ctx->options().max_chunk_tokens)
+      throw lmmsim::ConfigError("rs_tp_prefill: chunk exceeds max_chunk_tokens");
+    cudaStream_t st = stream != nullptr ? static_cast<cudaStream_t>(stream) : x.ctx->aux_stream();
+    x.ctx->prefill(refs, static_cast<bf16*>(x_dev), st);
+  });
+}
+
+rs_status rs_tp_logits(rs_ctx* c, uint64_t id, float* out_host, int32_t* out_argmax) {
+  return guarded([&] {
+    rs_ctx& x = need(c);
+    if (!x.ctx->llm()->has_head()) throw lmmsim::ConfigError("rs_tp_logits: this rank holds no LM head");
+    DevRequest& r = x.ctx->get(id);
+    cudaStream_t st = x.ctx->aux_stream();
+    if (out_host) x.ctx->copy_logits(r.slot, out_host, st);
+    if (out_argmax)
+      RS_CUDA_CHECK(cudaMemcpyAsync(out_argmax, x.ctx->device_argmax() + r.slot, 4, cudaMemcpyDeviceToHost, st));
+    RS_CUDA_CHECK(cudaStreamSynchronize(st));
+  });
+}
+
+}  // extern "C"

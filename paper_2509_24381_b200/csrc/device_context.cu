@@ -113,7 +113,15 @@ Context::Context(const rs_model_config& model, const rs_ctx_options& opt) : opt_
   up_.init(64ull << 20);
   max_requests_ = 512;
 
-  const bool first_stage = opt_.layer_begin == 0;
+  // TP group rank (rs_ctx_options.tp_group): one shard per context, chunk
+  // inputs handed in, no embedding slab / vision tower here
+  tp_group_ = opt_.tp_group != 0;
+  if (tp_group_) {
+    if (opt_.tp_size < 2 || opt_.tp_size > kMaxTpRanks || opt_.tp_rank < 0 || opt_.tp_rank >= opt_.tp_size)
+      throw lmmsim::ConfigError("tp group: need 2 <= tp_size <= 8 and 0 <= tp_rank < tp_size");
+    if (opt_.with_vit) throw lmmsim::ConfigError("tp group: the vision tower does not live on a TP rank");
+  }
+  const bool first_stage = opt_.layer_begin == 0 && !tp_group_;
   if (opt_.with_vit) {
     vit_ = std::make_unique<Vit>();
     vit_->init(s_, arena_, static_cast<int>(4 * opt_.max_encode_tokens), aux_);
@@ -124,8 +132,18 @@ Context::Context(const rs_model_config& model, const rs_ctx_options& opt) : opt_
   if (tp > 1 && (opt_.layer_begin != 0 || opt_.layer_end != s_.L))
     throw lmmsim::ConfigError("tensor parallelism: the context must own every LLM layer");
   llm_->init(s_, arena_, opt_.layer_begin, opt_.layer_end, first_stage, opt_.with_lm_head != 0,
-             static_cast<int>(opt_.max_chunk_tokens), kv_pages, kPageTokens, max_requests_, aux_, 0, tp);
-  if (tp > 1) {
+             static_cast<int>(opt_.max_chunk_tokens), kv_pages, kPageTokens, max_requests_, aux_,
+             tp_group_ ? opt_.tp_rank : 0, tp);
+  if (tp_group_) {
+    // exchange buffer: [2 phases][max_chunk, d] bf16 partials + flag slots;
+    // cudaMalloc'd on its own so one IPC handle maps it into peer processes
+    const std::size_t part = static_cast<std::size_t>(opt_.max_chunk_tokens) * s_.d * sizeof(bf16);
+    tpx_bytes_ = 2 * part + sizeof(unsigned) * kTpBlocks * kMaxTpRanks;
+    RS_CUDA_CHECK(cudaMalloc(&tpx_, tpx_bytes_));
+    RS_CUDA_CHECK(cudaMemsetAsync(tpx_, 0, tpx_bytes_, aux_));
+    tp_ss_ = static_cast<unsigned long long*>(arena_.alloc(static_cast<std::size_t>(opt_.max_chunk_tokens) * 8));
+    tpx_peers_.assign(static_cast<std::size_t>(tp), nullptr);
+  } else if (tp > 1) {
     const std::int64_t M = static_cast<std::int64_t>(opt_.max_chunk_tokens);
     for (int r = 1; r < tp; ++r) {
       tp_shards_.push_back(std::make_unique<Llm>());
@@ -158,6 +176,9 @@ Context::Context(const rs_model_config& model, const rs_ctx_options& opt) : opt_
 
 Context::~Context() {
   cudaDeviceSynchronize();
+  for (std::size_t r = 0; r < tpx_opened_.size(); ++r)
+    if (tpx_opened_[r]) cudaIpcCloseMemHandle(tpx_peers_[r]);
+  if (tpx_) cudaFree(tpx_);
   if (decode_x_) cudaFree(decode_x_);
   if (decode_ids_) cudaFree(decode_ids_);
   reqs_.clear();
@@ -421,7 +442,7 @@ void Context::prefill(const std::vector<SliceRef>& slices, bf16* x, cudaStream_t
   std::vector<std::int32_t> done_slots;
   const int l_from = layer_from < 0 ? llm_->layer_begin() : layer_from;
   const int l_to = layer_to < 0 ? llm_->layer_end() : layer_to;
-  const bool first = l_from == 0;
+  const bool first = l_from == 0 && slab_ != nullptr;  // TP group ranks: chunk input handed in
   for (const SliceRef& sl : slices) {
     const int base = static_cast<int>(rows.size());
     for (std::uint64_t p = sl.start; p < sl.end; ++p) {
@@ -471,6 +492,44 @@ void Context::prefill(const std::vector<SliceRef>& slices, bf16* x, cudaStream_t
 // block -> O partial, reduce into x (shard order, + folded-norm sums of
 // squares), every shard's MLP -> down partial, reduce.
 void Context::run_llm(const ChunkDev& c, const bf16* slab, bf16* x, cudaStream_t st, int l_from, int l_to) {
+  if (tp_group_) {
+    if (!tp_connected_) throw lmmsim::ConfigError("tp group: rs_tp_connect first");
+    if (l_from < 0) l_from = llm_->layer_begin();
+    if (l_to < 0) l_to = llm_->layer_end();
+    const int T = opt_.tp_size;
+    const std::size_t part = static_cast<std::size_t>(opt_.max_chunk_tokens) * s_.d * sizeof(bf16);
+    TpGroupArgs a{};
+    a.x = x;
+    a.rows = c.M;
+    a.d = s_.d;
+    a.T = T;
+    a.rank = opt_.tp_rank;
+    a.ss = tp_ss_;
+    for (int r = 0; r < T; ++r)
+      a.flags[r] = reinterpret_cast<unsigned*>(static_cast<std::uint8_t*>(tpx_peers_[static_cast<std::size_t>(r)]) + 2 * part);
+    auto reduce = [&]() {
+      const int ph = static_cast<int>((tp_epoch_ + 1) & 1u);  // = my_part()'s phase
+      for (int r = 0; r < T; ++r)
+        a.parts[r] = reinterpret_cast<const bf16*>(static_cast<std::uint8_t*>(tpx_peers_[static_cast<std::size_t>(r)]) + ph * part);
+      a.epoch = ++tp_epoch_;
+      tp_group_reduce(a, st);
+    };
+    auto my_part = [&]() {  // the partial of the coming reduce (epoch + 1)
+      return reinterpret_cast<bf16*>(static_cast<std::uint8_t*>(tpx_) + ((tp_epoch_ + 1) & 1u) * part);
+    };
+    llm_->tp_begin(c, st);
+    for (int l = l_from; l < l_to; ++l) {
+      // O partial -> this rank's exchange buffer, then the peer-memory reduction
+      // (double-buffered by phase: a rank rewrites a phase buffer only after every
+      // rank has signalled the next phase, i.e. finished reading it)
+      llm_->tp_attn_partial(l, c, slab, x, l == l_from, tp_ss_, page_tables_dev_, my_part(), st);
+      reduce();
+      llm_->tp_mlp_partial(l, c, x, tp_ss_, my_part(), st);
+      reduce();
+    }
+    if (l_to == llm_->layer_end()) llm_->head_phase(c, x, st);
+    return;
+  }
   if (tp_shards_.empty()) {
     llm_->forward_stage(c, slab, x, page_tables_dev_, st, l_from, l_to);
     return;
@@ -497,6 +556,7 @@ double Context::decode(const std::vector<lmmsim::RequestId>& ids, int steps, std
                        float* out_logits, cudaStream_t st) {
   if (!llm_ || !llm_->has_head() || llm_->layer_begin() != 0)
     throw lmmsim::ConfigError("decode needs the whole LLM and its head on this context");
+  if (tp_group_) throw lmmsim::ConfigError("decode: not on a TP group rank (prefill only)");
   const int n = static_cast<int>(ids.size());
   if (n <= 0 || steps <= 0) return 0.0;
   if (n > opt_.max_chunk_tokens) throw lmmsim::ConfigError("decode: more requests than max_chunk_tokens");
@@ -762,4 +822,34 @@ void Context::import_kv(lmmsim::RequestId id, const rs_kv_meta& meta, const void
   reqs_.emplace(id, std::move(owned));
 }
 
+}  // namespace rserve
+
+// ---- tensor parallelism across GPUs: exchange buffers -------------------------
+namespace rserve {
+void Context::tp_buffer(void** dev, cudaIpcMemHandle_t* handle) {
+  if (!tp_group_) throw lmmsim::ConfigError("tp buffer: not a TP group rank (rs_ctx_options.tp_group)");
+  if (dev) *dev = tpx_;
+  if (handle) RS_CUDA_CHECK(cudaIpcGetMemHandle(handle, tpx_));
+}
+
+void Context::tp_connect(const void* const* ptrs, const cudaIpcMemHandle_t* handles) {
+  if (!tp_group_) throw lmmsim::ConfigError("tp connect: not a TP group rank");
+  if (tp_connected_) throw lmmsim::ConfigError("tp connect: already connected");
+  const int T = opt_.tp_size;
+  tpx_opened_.assign(static_cast<std::size_t>(T), false);
+  for (int r = 0; r < T; ++r) {
+    void*& p = tpx_peers_[static_cast<std::size_t>(r)];
+    if (r == opt_.tp_rank) {
+      p = tpx_;
+    } else if (ptrs != nullptr && ptrs[r] != nullptr) {  // a rank of this process (same address space)
+      p = const_cast<void*>(ptrs[r]);
+    } else {
+      if (handles == nullptr) throw lmmsim::ConfigError("tp connect: rank " + std::to_string(r) + " has no address");
+      RS_CUDA_CHECK(cudaIpcOpenMemHandle(&p, handles[r], cudaIpcMemLazyEnablePeerAccess));
+      tpx_opened_[static_cast<std::size_t>(r)] = true;
+    }
+  }
+  RS_CUDA_CHECK(cudaStreamSynchronize(aux_));  // the zeroed flags are in place before any peer signals
+  tp_connected_ = true;
+}
 }  // namespace rserve

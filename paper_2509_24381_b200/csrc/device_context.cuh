@@ -163,6 +163,11 @@ class Context {
                 float* out_logits, cudaStream_t st);
   /// Frees a request kept for decode (KV pages, tables, request slot).
   void free_kept(lmmsim::RequestId id);
+  // ---- TP group across GPUs ----
+  /// This rank's exchange buffer and its CUDA IPC handle.
+  void tp_buffer(void** dev, cudaIpcMemHandle_t* handle);
+  /// Maps every rank's exchange buffer: ptrs[r] (same process) or handles[r] (IPC).
+  void tp_connect(const void* const* ptrs, const cudaIpcMemHandle_t* handles);
   // ---- PD (prefill -> decode) KV transfer ----
   /// Bytes of a kept request's KV image: [shard][layer][page][K | V^T page].
   std::uint64_t kv_image_bytes(std::uint64_t tokens) const;
@@ -198,6 +203,14 @@ class Context {
   // tensor parallelism: shards 1..T-1 of the LLM (shard 0 is
   // llm_), their O / down partials and the reduction's sums of squares
   std::vector<std::unique_ptr<Llm>> tp_shards_;
+  // TP group rank (f4 across GPUs): exchange buffer (partials x 2 phases +
+  // flag slots), every rank's mapping of it, reduction epoch
+  bool tp_group_ = false, tp_connected_ = false;
+  void* tpx_ = nullptr;
+  std::size_t tpx_bytes_ = 0;
+  std::vector<void*> tpx_peers_;
+  std::vector<bool> tpx_opened_;
+  unsigned tp_epoch_ = 0;
   std::vector<bf16*> tp_parts_;
   bf16** tp_parts_dev_ = nullptr;
   unsigned long long* tp_ss_ = nullptr;

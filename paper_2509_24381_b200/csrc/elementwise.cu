@@ -860,6 +860,67 @@ void tp_reduce_residual(bf16* x, int rows, int d, bf16* const* parts, int n_part
   count_launch();
 }
 
+__global__ void __launch_bounds__(128, 16) tp_group_reduce_kernel(const TpGroupArgs a) {
+  pdl_wait();  // this rank's partial (previous kernel) is complete
+  const int t = threadIdx.x;
+  if (t < a.T) {
+    unsigned* peer = a.flags[t] + blockIdx.x * kMaxTpRanks + a.rank;
+    asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(peer), "r"(a.epoch) : "memory");
+    const unsigned* mine = a.flags[a.rank] + blockIdx.x * kMaxTpRanks + t;
+    unsigned v;
+    do {
+      asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(mine) : "memory");
+    } while (static_cast<int>(v - a.epoch) < 0);
+  }
+  __syncthreads();
+  // only now may the next kernel of this stream start (PDL): a dependent grid
+  // holding SMs while a peer sharing this GPU has not signalled could starve it
+  pdl_launch_dependents();
+  const int lane = t & 31, wpb = blockDim.x >> 5;
+  for (int row = blockIdx.x * wpb + (t >> 5); row < a.rows; row += gridDim.x * wpb) {
+    float sq = 0.f;
+    bf16* xr = a.x + static_cast<std::int64_t>(row) * a.d;
+    for (int c = lane * 8; c < a.d; c += 256) {
+      const uint4 xv = *reinterpret_cast<const uint4*>(xr + c);
+      const std::uint32_t xw[4] = {xv.x, xv.y, xv.z, xv.w};
+      float part[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+      for (int r = 0; r < a.T; ++r) {  // rank order: the same sum on every rank
+        const uint4 pv = __ldcv(reinterpret_cast<const uint4*>(a.parts[r] + static_cast<std::int64_t>(row) * a.d + c));
+        const std::uint32_t pw[4] = {pv.x, pv.y, pv.z, pv.w};
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const float2 f = unpack_bf16x2(pw[k]);
+          part[2 * k] += f.x;
+          part[2 * k + 1] += f.y;
+        }
+      }
+      std::uint32_t o[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const float2 xf = unpack_bf16x2(xw[k]);
+        o[k] = pack_bf16x2(xf.x + part[2 * k], xf.y + part[2 * k + 1]);
+        const float2 f = unpack_bf16x2(o[k]);
+        sq = fmaf(f.x, f.x, fmaf(f.y, f.y, sq));
+      }
+      *reinterpret_cast<uint4*>(xr + c) = make_uint4(o[0], o[1], o[2], o[3]);
+    }
+    sq = warp_sum(sq);
+    if (lane == 0) a.ss[row] = static_cast<unsigned long long>(__float2ull_rn(sq * kSsFixedScale));
+  }
+}
+
+void tp_group_reduce(const TpGroupArgs& a, cudaStream_t st) {
+  if (a.rows <= 0) return;
+  if (a.d % 256 != 0) throw DeviceError(RS_ERR_CUDA, "tp group reduce: d % 256 != 0");
+  if (a.T < 1 || a.T > kMaxTpRanks) throw DeviceError(RS_ERR_CUDA, "tp group reduce: 1..8 ranks");
+  const int tok = prof::begin(st);
+  // a fixed grid: every rank must use the same flag slots
+  launch_kernel(tp_group_reduce_kernel, dim3(kTpBlocks), dim3(128), 0, st, 1, a);
+  RS_LAUNCH_CHECK();
+  prof::end(tok, st, "tp_group_reduce", 0, 2.0 * a.rows * a.d * (a.T + 2));
+  count_launch();
+}
+
 __global__ void mrope_table_kernel(const ChunkRowInfo* __restrict__ info, int rows, int hd,
                                    float log2_theta, float2* table) {
   pdl_wait();

@@ -101,7 +101,11 @@ constexpr int kMaxParts = 8;  // units per split tile (launch() guarantees the b
 // CG = CTAs per tile: 1, or 2 for a CTA pair (cluster of 2 on one TPC) running
 // 256 x BN tiles with cta_group::2 MMAs — each CTA stages its own 128 A rows
 // and half of the B rows, halving per-SM shared-memory operand traffic.
-template <int BN, bool TMA_OUT = false, int CG = 1>
+// QkvRope epilogue staging (ROPE): the tile's 128 rows of the chunk's M-RoPE
+// (cos, sin) table (hd = 128: 512 B per row, as 4 SW128 boxes of 32 floats)
+// and the tile's BN bias values, loaded while the tile's MMAs run.
+constexpr int kRopeTableBytes = 4 * 128 * 128;
+template <int BN, bool TMA_OUT = false, int CG = 1, bool ROPE = false>
 struct Cfg {
   static_assert(BN % 32 == 0 && BN >= 128 && BN <= 256, "tile width");
   static_assert(CG == 1 || (CG == 2 && BN % 32 == 0), "pair tiles split B in halves of 16-row multiples");
@@ -111,12 +115,13 @@ struct Cfg {
   // epilogue staging: 8 warps x 2 buffers x [32 rows x 64 B] (bf16 TMA stores)
   static constexpr int kEpiBuf = 2048;
   static constexpr int kEpiBytes = TMA_OUT ? kEpiWarps * 2 * kEpiBuf : 0;
+  static constexpr int kRopeBytes = ROPE ? kRopeTableBytes + 2 * BN : 0;
   // as many pipeline stages as the 227 KB of shared memory allow (<= 8)
-  static constexpr int kStagesFit = (227 * 1024 - 1024 - 512 - kEpiBytes) / kStageBytes;
+  static constexpr int kStagesFit = (227 * 1024 - 1024 - 512 - kEpiBytes - kRopeBytes) / kStageBytes;
   static constexpr int kStages = kStagesFit > 8 ? 8 : kStagesFit;
   // double-buffered accumulator, allocation rounded up to a power of two
   static constexpr int kTmemCols = 2 * BN <= 256 ? 256 : 512;
-  static constexpr int kSmem = kStages * kStageBytes + kEpiBytes + 1024 /*align*/ + 512 /*barriers*/;
+  static constexpr int kSmem = kStages * kStageBytes + kEpiBytes + kRopeBytes + 1024 /*align*/ + 512 /*barriers*/;
 };
 
 __device__ __forceinline__ float gelu_erf(float x) {
@@ -187,7 +192,8 @@ __device__ __forceinline__ void epilogue_tile_tma(const GemmParams& p, const CUt
                                                   std::uint32_t& ec, std::uint32_t t_row, int m0,
                                                   int n0, int quad, int half, int lane,
                                                   const float* const (&parts)[kMaxParts] = {},
-                                                  int n_parts = 0, bool res_issued = false) {
+                                                  int n_parts = 0, bool res_issued = false,
+                                                  const std::uint8_t* rope_smem = nullptr) {
   const int my_row = m0 + quad * 32 + lane;
   const float rs = row_scale(p, my_row);
   float ss = 0.f;  // sum of squares of this thread's output row segment (ss_out)
@@ -262,13 +268,16 @@ __device__ __forceinline__ void epilogue_tile_tma(const GemmParams& p, const CUt
       } else {
         if constexpr (!FROM_WS) sm100::tmem_ld_wait();
         const int col = n0 + c * 32;
+        // staged tile bias (QkvRope): [BN] bf16 after the rope table
+        const std::uint8_t* sbias = kRope && rope_smem != nullptr ? rope_smem + kRopeTableBytes : nullptr;
         if (p.ss_in != nullptr || (p.bias != nullptr && col < p.N)) {
           // v = rs * acc + bias, two columns per packed FFMA2
           const float2 rs2 = make_float2(rs, rs);
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
             uint4 bb = make_uint4(0, 0, 0, 0);
-            if (p.bias != nullptr && col < p.N) bb = *reinterpret_cast<const uint4*>(p.bias + col + q * 8);
+            if (sbias != nullptr) bb = *reinterpret_cast<const uint4*>(sbias + (c * 32 + q * 8) * 2);
+            else if (p.bias != nullptr && col < p.N) bb = *reinterpret_cast<const uint4*>(p.bias + col + q * 8);
             const std::uint32_t bw[4] = {bb.x, bb.y, bb.z, bb.w};
 #pragma unroll
             for (int t = 0; t < 4; ++t) {
@@ -306,7 +315,8 @@ __device__ __forceinline__ void epilogue_tile_tma(const GemmParams& p, const CUt
 #pragma unroll
             for (int q = 0; q < 4; ++q) {  // partner: rs * acc + bias (8 columns per 16-byte load)
               uint4 bb = make_uint4(0, 0, 0, 0);
-              if (p.bias != nullptr) bb = *reinterpret_cast<const uint4*>(p.bias + col + delta + q * 8);
+              if (sbias != nullptr) bb = *reinterpret_cast<const uint4*>(sbias + (c * 32 + delta + q * 8) * 2);
+              else if (p.bias != nullptr) bb = *reinterpret_cast<const uint4*>(p.bias + col + delta + q * 8);
               const std::uint32_t bw[4] = {bb.x, bb.y, bb.z, bb.w};
 #pragma unroll
               for (int t = 0; t < 4; ++t) {
@@ -316,9 +326,21 @@ __device__ __forceinline__ void epilogue_tile_tma(const GemmParams& p, const CUt
                 w[q * 8 + 2 * t + 1] = __float_as_uint(y.y);
               }
             }
+            // staged table row (4 SW128 boxes of [128 rows x 32 floats]): pair j at byte 8 j
+            const int trow = quad * 32 + lane;
+            const std::uint32_t tsm = rope_smem != nullptr ? sm100::smem_u32(rope_smem) : 0u;
 #pragma unroll
             for (int q = 0; q < 16; ++q) {  // (cos, sin) of two columns per 16-byte load
-              const float4 c4 = __ldg(cs + q);
+              float4 c4;
+              if (rope_smem != nullptr) {
+                const int off = (i0 % half_hd) * 8 + q * 16;  // byte offset in the table row
+                const std::uint32_t a = tsm + static_cast<std::uint32_t>((off >> 7) * 16384 + trow * 128 +
+                                                                         ((((off >> 4) & 7) ^ (trow & 7)) << 4));
+                asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];"
+                             : "=f"(c4.x), "=f"(c4.y), "=f"(c4.z), "=f"(c4.w) : "r"(a));
+              } else {
+                c4 = __ldg(cs + q);
+              }
               const float2 xr = fma2(make_float2(__uint_as_float(w[2 * q]), __uint_as_float(w[2 * q + 1])),
                                      make_float2(sgn * c4.y, sgn * c4.w),
                                      mul2(make_float2(x[2 * q], x[2 * q + 1]), make_float2(c4.x, c4.z)));
@@ -487,14 +509,17 @@ __global__ void __launch_bounds__(kThreads, 1)
                         const __grid_constant__ CUtensorMap tmB,
                         const __grid_constant__ CUtensorMap tmC,
                         const __grid_constant__ CUtensorMap tmR, const GemmParams p) {
-  using C = Cfg<BN, TMA_OUT, CG>;
+  // QkvRope: tmR maps the chunk's M-RoPE table, staged per tile into smem
+  constexpr bool kRopeStage = TMA_OUT && EPI == static_cast<int>(Epi::QkvRope);
+  using C = Cfg<BN, TMA_OUT, CG, kRopeStage>;
   extern __shared__ __align__(1024) std::uint8_t smem_raw[];
   std::uint8_t* smem = reinterpret_cast<std::uint8_t*>(
       (reinterpret_cast<std::uintptr_t>(smem_raw) + 1023) & ~std::uintptr_t(1023));
   std::uint8_t* smem_a = smem;
   std::uint8_t* smem_b = smem + C::kStages * C::kABytes;
   std::uint8_t* smem_epi = smem + C::kStages * C::kStageBytes;  // 1024-aligned
-  std::uint64_t* bars = reinterpret_cast<std::uint64_t*>(smem_epi + C::kEpiBytes);
+  std::uint8_t* rope_smem = smem_epi + C::kEpiBytes;  // [kRopeTableBytes] table + [BN] bias (kRopeStage)
+  std::uint64_t* bars = reinterpret_cast<std::uint64_t*>(rope_smem + C::kRopeBytes);
   std::uint64_t* full = bars;
   std::uint64_t* empty = bars + C::kStages;
   std::uint64_t* tfull = bars + 2 * C::kStages;
@@ -502,6 +527,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   std::uint64_t* rbar = tempty + 2;  // [epilogue warps][2] residual-load barriers
   std::uint32_t* tmem_holder = reinterpret_cast<std::uint32_t*>(rbar + 2 * kEpiWarps);
   volatile int* sk_finisher = reinterpret_cast<volatile int*>(tmem_holder + 1);
+  std::uint64_t* tbar = bars + 60;  // rope table TMA (kRopeStage)
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -530,9 +556,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       sm100::mbar_init(&tempty[a], kEpiWarps * CG);  // pair: both CTAs' epilogue warps
     }
     for (int r = 0; r < 2 * kEpiWarps; ++r) sm100::mbar_init(&rbar[r], 1);
+    sm100::mbar_init(tbar, 1);
     if constexpr (TMA_OUT) {
       sm100::tma_prefetch_desc(&tmC);
-      if (EPI == static_cast<int>(Epi::Residual)) sm100::tma_prefetch_desc(&tmR);
+      if (EPI == static_cast<int>(Epi::Residual) || kRopeStage) sm100::tma_prefetch_desc(&tmR);
     }
     sm100::fence_mbar_init();
   }
@@ -650,7 +677,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int quad = warp & 3;         // TMEM lanes [32*quad, 32*quad + 32) (warp % 4 rule)
     const int half = (warp - 4) >> 2;  // which half of the tile's columns
     int local = 0;
-    std::uint32_t ec = 0, rphase = 0;  // TMA-epilogue chunk counter / residual phases
+    std::uint32_t ec = 0, rphase = 0, tphase = 0;  // TMA-epilogue chunk counter / residual / rope-table phases
     UnitIter it = sched.begin(unit0);
     Unit u;
     // accumulator-free signal goes to the MMA issuer's CTA (the pair leader)
@@ -728,12 +755,33 @@ __global__ void __launch_bounds__(kThreads, 1)
         if constexpr (kRes)
           prefetch_residual<BN, EPI>(&tmR, smem_epi + (warp - 4) * 2 * C::kEpiBuf, rbar + 2 * (warp - 4), ec,
                                      m0, n0, quad, half, lane);
+        if constexpr (kRopeStage) {
+          // stage this tile's table rows + bias while its MMAs run (the
+          // previous tile's epilogue has finished reading them)
+          asm volatile("bar.sync 2, %0;" ::"n"(32 * kEpiWarps));
+          if (warp == 4 && lane == 0) {
+            sm100::mbar_expect_tx(tbar, static_cast<std::uint32_t>(p.rope_hd) * 4 * kBM);
+            for (int b = 0; b < p.rope_hd / 32; ++b)
+              sm100::tma_load_2d(rope_smem + b * (kBM * 128), &tmR, tbar, b * 32, m0);
+          }
+          const int t = static_cast<int>(threadIdx.x) - 128;
+          if (t < BN) {
+            bf16 bv = __float2bfloat16_rn(0.f);
+            if (p.bias != nullptr && n0 + t < p.N) bv = p.bias[n0 + t];
+            reinterpret_cast<bf16*>(rope_smem + kRopeTableBytes)[t] = bv;
+          }
+          asm volatile("bar.sync 2, %0;" ::"n"(32 * kEpiWarps));
+        }
         sm100::mbar_wait(&tfull[acc], acc_phase);
         sm100::tc_fence_after();
+        if constexpr (kRopeStage) {
+          sm100::mbar_wait(tbar, tphase);
+          tphase ^= 1;
+        }
         const float* const no_parts[kMaxParts] = {};
         epilogue_tile_tma<BN, EPI>(p, &tmC, &tmR, smem_epi + (warp - 4) * 2 * C::kEpiBuf,
                                    rbar + 2 * (warp - 4), rphase, ec, t_row, m0, n0, quad, half,
-                                   lane, no_parts, 0, kRes);
+                                   lane, no_parts, 0, kRes, kRopeStage ? rope_smem : nullptr);
       } else {
         sm100::mbar_wait(&tfull[acc], acc_phase);
         sm100::tc_fence_after();
@@ -897,8 +945,13 @@ SplitPlan plan_split(int tiles, int num_kb, int bn, int cg = 1) {
   const int rem = tiles % slots;
   const int full = tiles / slots;
   best.cost = full + (rem > 0 ? 1.0 : 0.0);
-  // (measured: at K = 3584 the partials' round trip eats the gain; K = 18944 wins 30%)
-  const bool small = tiles <= slots / 2 && num_kb >= 128;
+  // small grids split K from RS_GEMM_SMALL_MIN_KB k-blocks (r1, strided partial
+  // layout: at K = 3584 the partials' round trip ate the gain; K = 18944 won 30%)
+  static const int small_min_kb = [] {
+    const char* e = std::getenv("RS_GEMM_SMALL_MIN_KB");
+    return e != nullptr ? std::atoi(e) : 128;
+  }();
+  const bool small = tiles <= slots / 2 && num_kb >= small_min_kb;
   const bool tail = tiles > slots && rem > 0 && num_kb >= 48;
   // Pair tiles: measured slower with split tails at every cfg2 shape (both
   // CTAs' fp32 partials round-trip), so they run whole tiles only; the kernel
@@ -925,7 +978,7 @@ SplitPlan plan_split(int tiles, int num_kb, int bn, int cg = 1) {
 
 template <int BN, int EPI, bool TMA_OUT, int CG>
 void launch(const GemmArgs& a, cudaStream_t stream) {
-  using C = Cfg<BN, TMA_OUT, CG>;
+  using C = Cfg<BN, TMA_OUT, CG, TMA_OUT && EPI == static_cast<int>(Epi::QkvRope)>;
   auto* kernel = gemm_tcgen05_kernel<BN, EPI, TMA_OUT, CG>;
   static bool attr_set = false;
   if (!attr_set) {
@@ -941,6 +994,12 @@ void launch(const GemmArgs& a, cudaStream_t stream) {
     tmC = make_map(a.C, f32, a.M, out_cols, a.ldc, 32, 32);
     if constexpr (EPI == static_cast<int>(Epi::Residual))
       tmR = make_map(a.residual, false, a.M, a.N, a.ldr, 32, 32);
+    if constexpr (EPI == static_cast<int>(Epi::QkvRope)) {
+      // the chunk's M-RoPE (cos, sin) table [M, hd/2] float2 = [M, hd] fp32, boxes of 32 floats x 128 rows
+      if (a.rope_hd % 32 != 0 || a.rope_hd > 128)
+        throw DeviceError(RS_ERR_CUDA, "gemm: QkvRope staging needs head_dim % 32 == 0, <= 128");
+      tmR = make_map(a.rope_table, true, a.M, a.rope_hd, a.rope_hd, 32, kBM);
+    }
   }
   GemmParams p{a.C, a.ldc, a.bias, a.residual, a.ldr, a.row_map, a.M, a.N, a.K, a.M_dev,
                0, 0, 0, nullptr, nullptr, 0,

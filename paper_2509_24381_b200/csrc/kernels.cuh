@@ -102,6 +102,25 @@ void rope_kv_append(bf16* qkv, int ld, const ChunkRowInfo* rows_info, int rows, 
 /// parts: device array of `n_parts` pointers to [rows, d] bf16.
 void tp_reduce_residual(bf16* x, int rows, int d, bf16* const* parts, int n_parts, unsigned long long* ss,
                         cudaStream_t st);
+/// Tensor-parallel group reduction over peer memory: T ranks
+/// (one per GPU over NVSwitch, or contexts sharing a GPU) each hold their O /
+/// down partial in an exchange buffer every rank can address. Every block
+/// signals each rank (release, system scope) that this rank's partial of
+/// `epoch` is complete, waits for all ranks' signals of the same block
+/// (acquire), then reduces its rows reading the T partials in rank order:
+/// x += sum_t parts[t] and ss = sum of squares of the new bf16 row — the same
+/// bits on every rank. No NCCL: the reads go straight over NVLink.
+constexpr int kMaxTpRanks = 8;
+constexpr int kTpBlocks = 64;  // reduce grid (flag slots per rank: kTpBlocks x kMaxTpRanks)
+struct TpGroupArgs {
+  bf16* x;
+  int rows, d, T, rank;
+  unsigned epoch;
+  const bf16* parts[kMaxTpRanks];  // this phase's partial of each rank
+  unsigned* flags[kMaxTpRanks];    // each rank's flag slots [kTpBlocks][kMaxTpRanks]
+  unsigned long long* ss;
+};
+void tp_group_reduce(const TpGroupArgs& a, cudaStream_t st);
 /// M-RoPE (cos, sin) of every chunk row and rotary frequency: [rows, hd/2].
 void mrope_table(const ChunkRowInfo* rows_info, int rows, int hd, float theta, float2* table,
                  cudaStream_t st);

@@ -28,8 +28,13 @@ SHAPES = [  # (M, N, K, epi, label)
 BNS = [0, 128, 160, 192, 256, -128, -160, -192, -224, -256]
 
 
+SMALL_M = [(m, n, k, e, f"{lab}_m{m}") for m in (128, 256)
+           for n, k, e, lab in ((4608, 3584, 0, "qkv"), (3584, 3584, 1, "o"), (37888, 3584, 2, "gateup"),
+                                (3584, 18944, 1, "down"))]
+
+
 def main():
-    shapes = SHAPES[:3] if "--quick" in sys.argv else SHAPES
+    shapes = SHAPES[:3] if "--quick" in sys.argv else SMALL_M if "--small-m" in sys.argv else SHAPES
     st = torch.cuda.current_stream()
     res = []
     for M, Nn, K, epi, label in shapes:
