@@ -86,7 +86,29 @@ struct TcParams {
   int max_keys;                     // kPaged: longest item's keys (host info, profiling label)
   float* part_o;                    // [n_pieces * H * 256, HD]
   float* part_ml;                   // [n_pieces * H * 256, 2]
+  // RS_PP_TRACE (dev): globaltimer stamps of CTA 0's pipeline handshakes
+  // [role][iteration][event], else null
+  unsigned long long* trace;
 };
+constexpr int kPpTraceIters = 24;  // key-tile iterations traced (first unit of CTA 0)
+constexpr int kPpTraceEv = 4;
+__device__ __forceinline__ unsigned long long pp_gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+// role: 0 MMA warp (tile 0 events), 1 MMA warp (tile 1), 2 softmax tile 0, 3 softmax tile 1
+#ifdef RS_PP_TRACE_BUILD  // dev builds only: the stamps sit in the hot loops
+#define PP_TRACE(role, it, ev)                                                                      \
+  do {                                                                                              \
+    if (p.trace != nullptr && blockIdx.x == 0 && (it) >= 0 && (it) < kPpTraceIters)                 \
+      p.trace[((role) * kPpTraceIters + (it)) * kPpTraceEv + (ev)] = pp_gtimer();                  \
+  } while (0)
+#else
+#define PP_TRACE(role, it, ev) \
+  do {                         \
+  } while (0)
+#endif
 
 __host__ __device__ __forceinline__ void kv_split_range(int n_tiles, int splits, int s, int& jb, int& je) {
   jb = s * n_tiles / splits;
@@ -747,6 +769,7 @@ __global__ void __launch_bounds__(kPpThreads, 1)
           }
         }
         __syncwarp();
+        if (r == 0 && lane == 0) PP_TRACE(t, j - x.jb, 2);
         if (sm100::elect_one()) {
           sm100::umma_commit(&s_full[t]);
           if (t == last_user(j)) sm100::umma_commit(&k_empty[st]);
@@ -758,7 +781,9 @@ __global__ void __launch_bounds__(kPpThreads, 1)
         const std::uint32_t vn = kbase + static_cast<std::uint32_t>(j - x.jb);
         const int st = static_cast<int>(vn % SV);
         sm100::mbar_wait(&v_full[st], (vn / SV) & 1);
+        if (r == 0 && lane == 0) PP_TRACE(t, j - x.jb, 0);
         if (!kTimingNoPWait) sm100::mbar_wait(&p_full[t], pn[t] & 1);
+        if (r == 0 && lane == 0) PP_TRACE(t, j - x.jb, 1);
         ++pn[t];
         sm100::tc_fence_after();
         std::uint8_t* v = sV + st * C::kVBytes;
@@ -823,7 +848,9 @@ __global__ void __launch_bounds__(kPpThreads, 1)
       }
       float m = -INFINITY, l = 0.f;
       for (int j = x.jb; j < j_end; ++j) {
+        if (rr == 0 && r == 0) PP_TRACE(2 + t, j - x.jb, 0);
         sm100::mbar_wait(&s_full[t], sn & 1);
+        if (rr == 0 && r == 0) PP_TRACE(2 + t, j - x.jb, 1);
         ++sn;
         sm100::tc_fence_after();
         if constexpr (kTimingSkipSoftmax) {  // dev timing: pipeline floor (P = raw S bits)
@@ -902,6 +929,7 @@ __global__ void __launch_bounds__(kPpThreads, 1)
         sm100::tmem_st_wait();
         sm100::tc_fence_before();
         __syncwarp();  // the warp's P stores are complete
+        if (rr == 0 && r == 0) PP_TRACE(2 + t, j - x.jb, 2);
         if (lane == 0) sm100::mbar_arrive(&p_full[t]);
         const float2 r01 = add2(rs2[0], rs2[1]), r23 = add2(rs2[2], rs2[3]);
         const float2 rsum = add2(r01, r23);
@@ -1105,8 +1133,33 @@ void launch(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
   const int tok = prof::begin(st);
   if (attn_unit_rows() == 256) {
     const int units = p.q_heads * p.n_pieces;
+    static const bool trace = std::getenv("RS_PP_TRACE") != nullptr;
+    TcParams q = p;
+    const std::size_t tn = 4 * kPpTraceIters * kPpTraceEv;
+    if (trace) {
+      RS_CUDA_CHECK(cudaMallocAsync(reinterpret_cast<void**>(&q.trace), tn * 8, st));
+      RS_CUDA_CHECK(cudaMemsetAsync(q.trace, 0, tn * 8, st));
+    }
     launch_kernel(fa_pp_kernel<HD, MODE>, dim3(std::min(units, kNumSMs)), dim3(kPpThreads), PpCfg<HD>::kSmem,
-                  st, 1, tq, tk, tv, p, units);
+                  st, 1, tq, tk, tv, q, units);
+    if (trace) {  // ns relative to the first stamp: MMA (wait-P begin, end, S issued), softmax (wait-S begin, end, P arrive)
+      std::vector<unsigned long long> h(tn);
+      RS_CUDA_CHECK(cudaMemcpyAsync(h.data(), q.trace, tn * 8, cudaMemcpyDeviceToHost, st));
+      RS_CUDA_CHECK(cudaStreamSynchronize(st));
+      RS_CUDA_CHECK(cudaFree(q.trace));
+      unsigned long long t0 = ~0ull;
+      for (unsigned long long v : h) if (v) t0 = std::min(t0, v);
+      auto at = [&](int role, int it, int ev) {
+        const unsigned long long v = h[(static_cast<std::size_t>(role) * kPpTraceIters + it) * kPpTraceEv + ev];
+        return v ? static_cast<long long>(v - t0) : -1ll;
+      };
+      std::fprintf(stderr, "[pp-trace] it | mma t0: waitP0 gotP0 S0issued | mma t1: waitP1 gotP1 S1issued | "
+                           "sm0: waitS gotS Parrive | sm1: waitS gotS Parrive (ns)\n");
+      for (int it = 0; it < kPpTraceIters; ++it)
+        std::fprintf(stderr, "[pp-trace] %2d | %6lld %6lld %6lld | %6lld %6lld %6lld | %6lld %6lld %6lld | %6lld %6lld %6lld\n", it,
+                     at(0, it, 0), at(0, it, 1), at(0, it, 2), at(1, it, 0), at(1, it, 1), at(1, it, 2),
+                     at(2, it, 0), at(2, it, 1), at(2, it, 2), at(3, it, 0), at(3, it, 1), at(3, it, 2));
+    }
     if (p.max_split > 1) {
       launch_kernel(pp_merge_kernel<HD>, dim3(p.q_heads * n_blocks, 256 / 8), dim3(256), 0, st, 1, p);
       count_launch();
