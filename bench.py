@@ -724,7 +724,23 @@ def run_ep(args):
                                    f"(transport {transport})"}), flush=True), os._exit(3)))
     watchdog.daemon = True
     watchdog.start()
-    g = make_group(transport)
+    fallback = None
+    try:
+        g = make_group(transport)
+        ok = 1
+    except Exception as e:  # e.g. NCCL refuses the link comms: keep the run on CUDA IPC
+        fallback = f"{transport} link setup failed on rank {rank}: {str(e)[:200]}"
+        print("[ep] " + fallback, file=sys.stderr, flush=True)
+        ok = 0
+    flag = torch.tensor([ok], device=pdev) if pdev is not None else torch.tensor([ok])
+    dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+    if int(flag.item()) == 0:
+        if ok:
+            g.close()
+        transport = "nccl" if transport == "ipc" else "ipc"
+        manifest["transport"] = transport
+        fallback = fallback or f"a peer's link setup failed: switched to {transport}"
+        g = make_group(transport)
     replay = Replayer() if rank == 0 else None
 
     def runs(workloads, e2e=False, sc=None, check=True):
@@ -818,6 +834,7 @@ def run_ep(args):
             "roofline": ep_roofline(m, tput_wls, total_ms, ws),
             "parity": parity,
             "transport_alt": alt,
+            "transport": transport, "transport_fallback": fallback,
             "ep_manifest": {"ranks": ws, "process_group": backend, "links": [f"{a}->{b}" for a, b in links],
                             "p2p_communicators": len(links) if transport == "nccl" else 0,
                             "rank0": manifest},

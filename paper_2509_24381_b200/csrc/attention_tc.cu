@@ -513,6 +513,16 @@ constexpr bool kTimingNoLoad = true;
 #else
 constexpr bool kTimingNoLoad = false;
 #endif
+#ifdef RS_PP_TIMING_NO_SLOAD
+constexpr bool kTimingNoSLoad = true;
+#else
+constexpr bool kTimingNoSLoad = false;
+#endif
+#ifdef RS_PP_TIMING_NO_PSTORE
+constexpr bool kTimingNoPStore = true;
+#else
+constexpr bool kTimingNoPStore = false;
+#endif
 #ifdef RS_PP_TIMING_SKIP_SOFTMAX
 constexpr bool kTimingSkipSoftmax = true;
 #else
@@ -862,12 +872,17 @@ __global__ void __launch_bounds__(kPpThreads, 1)
         const int key0 = x.key_begin + j * 128;
         const int c_lo = lo - key0, c_hi = hi - key0;  // visible columns [c_lo, c_hi)
         std::uint32_t sv[128];
+        if constexpr (kTimingNoSLoad) {  // dev timing: S not read from TMEM (wrong results)
 #pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          std::uint32_t(&v)[32] = *reinterpret_cast<std::uint32_t(*)[32]>(&sv[32 * c]);
-          sm100::tmem_ld_32x32b_x32(s_tm + 32 * c, v);
+          for (int c = 0; c < 128; ++c) sv[c] = __float_as_uint(static_cast<float>((c * 7 + lane) & 15) * 0.25f);
+        } else {
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            std::uint32_t(&v)[32] = *reinterpret_cast<std::uint32_t(*)[32]>(&sv[32 * c]);
+            sm100::tmem_ld_32x32b_x32(s_tm + 32 * c, v);
+          }
+          sm100::tmem_ld_wait();
         }
-        sm100::tmem_ld_wait();
         if (!(c_lo <= 0 && c_hi >= 128)) {
 #pragma unroll
           for (int q = 0; q < 128; ++q)
@@ -924,7 +939,8 @@ __global__ void __launch_bounds__(kPpThreads, 1)
             rs2[q & 3] = add2(rs2[q & 3], e);
             packed[q] = pack_bf16x2(e.x, e.y);
           }
-          sm100::tmem_st_32x32b_x16(s_tm + 16 * c, packed);
+          if constexpr (!kTimingNoPStore) sm100::tmem_st_32x32b_x16(s_tm + 16 * c, packed);
+          else if (packed[0] == 0x12345u && packed[15] == 0x54321u) sm100::tmem_st_32x32b_x16(s_tm + 16 * c, packed);
         }
         sm100::tmem_st_wait();
         sm100::tc_fence_before();
