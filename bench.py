@@ -347,6 +347,34 @@ def group_profile(raw):
     return out, shapes, attn
 
 
+# Bound of each kernel class: tensor-bound classes against the
+# burst bf16 peak, HBM-bound ones against the copy peak.
+KERNEL_BOUNDS = {"gemm_tcgen05": "tensor", "attn_prefill_tcgen05": "tensor", "attn_vit_tcgen05": "tensor",
+                 "attn_vit_window_tc": "hbm", "tracker_scatter_k6": "hbm", "rmsnorm": "hbm",
+                 "rmsnorm_gather": "hbm", "vit_qkv_split": "hbm", "gemv_small_m": "hbm"}
+
+
+def kernel_rooflines(prof, pk_tflops, hbm_gbs):
+    """Per kernel class of the profiling step: algorithmic FLOPs (tensor) or
+    bytes (HBM) each launch declares / its CUDA-event time, as a fraction of
+    the bound's measured peak. Event-bracketed launches (no PDL overlap), so
+    microsecond kernels read low."""
+    out = {}
+    for k, v in sorted(prof.items(), key=lambda kv: -kv[1]["ms"]):
+        bound = KERNEL_BOUNDS.get(k)
+        if bound is None or v["ms"] <= 0:
+            continue
+        if bound == "tensor" and v["flops"] > 0:
+            a = v["flops"] / (v["ms"] / 1e3) / 1e12
+            out[k] = {"bound": "tensor", "achieved": round(a, 1), "peak": pk_tflops, "unit": "TFLOP/s",
+                      "frac": round(a / pk_tflops, 3), "ms_per_step": round(v["ms"], 3)}
+        elif bound == "hbm" and v["bytes"] > 0:
+            a = v["bytes"] / (v["ms"] / 1e3) / 1e9
+            out[k] = {"bound": "hbm", "achieved": round(a, 1), "peak": hbm_gbs, "unit": "GB/s",
+                      "frac": round(a / hbm_gbs, 3), "ms_per_step": round(v["ms"], 3)}
+    return out
+
+
 def sim_cfg(args, m, stages=1, encoders=1, c_tokens=C_TOKENS, beta_enc=0.01):
     from paper_2509_24381_b200 import api
     return api.SimConfig(policy=args.policy, stages=stages, token_budget=args.budget,
@@ -558,6 +586,7 @@ def run_ours(args):
                                "tflops": v["flops"] / (v["ms"] / 1e3) / 1e12 if v["ms"] and v["flops"] else None,
                                "gbs": v["bytes"] / (v["ms"] / 1e3) / 1e9 if v["ms"] and v["bytes"] else None}
                            for k, v in prof.items()},
+        "rooflines": kernel_rooflines(prof, pk, hbm),
         "gemm_shapes": gemm_shapes[:16],
         "attn_prefill_shapes": attn_shapes,
         "cfg3": cfg3,

@@ -1184,13 +1184,26 @@ void launch(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
   else
     launch_kernel(fa_tc_kernel<HD, MODE>, grid, dim3(kTcThreads), TcCfg<HD>::kSmem, st, 1, tq, tk, tv, p);
   RS_LAUNCH_CHECK();
+  // algorithmic FLOPs (4 hd per (query, visible key) per head): paged items
+  // see keys [0, q_pos0 + r]; varlen blocks their sequence [key_begin, key_end)
+  double flops = 0;
+  if (tok >= 0) {
+    for (int i = 0; i < n_blocks; ++i) {
+      const int4 it = p.inl[i];
+      if (MODE == KvMode::kPaged)
+        flops += static_cast<double>(it.y) * it.z + 0.5 * static_cast<double>(it.y) * (it.y + 1);
+      else
+        flops += static_cast<double>(it.y) * (it.w - it.z);
+    }
+    flops *= 4.0 * p.out_hd * p.q_heads;
+  }
   if (tok >= 0 && MODE == KvMode::kPaged) {
     // per-shape class "attn_prefill_tcgen05|items|max_keys|splits" (bench groups on the prefix)
     char label[96];
     std::snprintf(label, sizeof label, "%s|%d|%d|%d", klass, n_blocks, p.max_keys, p.n_pieces);
-    prof::end(tok, st, label, 0, 0);
+    prof::end(tok, st, label, flops, 0);
   } else {
-    prof::end(tok, st, klass, 0, 0);
+    prof::end(tok, st, klass, flops, 0);
   }
   count_launch();
 }

@@ -585,7 +585,8 @@ const MapPair& cached_maps(const void* base, int rows, int cols, int ld) {  // k
 }
 
 template <int HD>
-void launch_win(const MapPair& m, const MapPair& mo, const WinParams& p, double flops, cudaStream_t st) {
+void launch_win(const MapPair& m, const MapPair& mo, const WinParams& p, double flops, double bytes,
+                cudaStream_t st) {
   static std::once_flag once;
   std::call_once(once, [] {
     RS_CUDA_CHECK(cudaFuncSetAttribute(win_attn_tc_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -625,7 +626,7 @@ void launch_win(const MapPair& m, const MapPair& mo, const WinParams& p, double 
                           v0 ? static_cast<double>(v0 - t0) : -1.0, sum / n, n);
     }
   }
-  prof::end(tok, st, "attn_vit_window_tc", flops, 0);
+  prof::end(tok, st, "attn_vit_window_tc", flops, bytes);
   count_launch();
 }
 
@@ -656,8 +657,9 @@ void attention_window_tc(const bf16* qkv, int ld_qkv, int rows, bf16* out, int l
   const MapPair m = cached_maps(qkv, rows, 3 * heads * head_dim, ld_qkv);
   const MapPair mo = cached_maps(out, rows, heads * head_dim, ld_out);
   switch (head_dim) {
-    case 80: return launch_win<80>(m, mo, p, flops, st);
-    case 64: return launch_win<64>(m, mo, p, flops, st);
+    // algorithmic bytes: packed q | k | v rows read once, o written once
+    case 80: return launch_win<80>(m, mo, p, flops, 2.0 * 4 * heads * 80 * static_cast<double>(rows), st);
+    case 64: return launch_win<64>(m, mo, p, flops, 2.0 * 4 * heads * 64 * static_cast<double>(rows), st);
     default: throw DeviceError(RS_ERR_CUDA, "window attention: unsupported head_dim " + std::to_string(head_dim));
   }
 }
