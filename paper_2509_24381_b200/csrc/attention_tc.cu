@@ -513,6 +513,13 @@ constexpr bool kTimingNoLoad = true;
 #else
 constexpr bool kTimingNoLoad = false;
 #endif
+// P in two halves (keys 0-63, 64-127), each signalled as soon as it is in
+// TMEM: the PV MMAs of the first half start while the softmax still
+// exponentiates the second (-DRS_PP_PHALF=0: one signal per tile).
+#ifndef RS_PP_PHALF
+#define RS_PP_PHALF 1
+#endif
+constexpr bool kPHalf = RS_PP_PHALF != 0;
 #ifdef RS_PP_TIMING_NO_SLOAD
 constexpr bool kTimingNoSLoad = true;
 #else
@@ -627,8 +634,8 @@ __global__ void __launch_bounds__(kPpThreads, 1)
   std::uint64_t* v_full = k_empty + SK;    // [SV]
   std::uint64_t* v_empty = v_full + SV;    // [SV]
   std::uint64_t* s_full = v_empty + SV;    // [2] S_t,j ready (and PV_t,j-1 done)
-  std::uint64_t* p_full = s_full + 2;      // [2] P_t,j written (4 softmax warps)
-  std::uint64_t* o_final = p_full + 2;     // [2] last PV_t of a unit done
+  std::uint64_t* p_full = s_full + 2;      // [2 tiles][2 halves] P_t,j keys 0-63 / 64-127 written (4 softmax warps)
+  std::uint64_t* o_final = p_full + 4;     // [2] last PV_t of a unit done
   std::uint32_t* tmem_holder = reinterpret_cast<std::uint32_t*>(o_final + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -642,7 +649,8 @@ __global__ void __launch_bounds__(kPpThreads, 1)
       sm100::mbar_init(&q_full[t], 1);
       sm100::mbar_init(&q_empty[t], 1);
       sm100::mbar_init(&s_full[t], 1);
-      sm100::mbar_init(&p_full[t], 4);  // one arrive per softmax warp
+      sm100::mbar_init(&p_full[2 * t], 4);  // one arrive per softmax warp
+      sm100::mbar_init(&p_full[2 * t + 1], 4);
       sm100::mbar_init(&o_final[t], 1);
     }
     for (int i = 0; i < SK; ++i) {
@@ -792,14 +800,15 @@ __global__ void __launch_bounds__(kPpThreads, 1)
         const int st = static_cast<int>(vn % SV);
         sm100::mbar_wait(&v_full[st], (vn / SV) & 1);
         if (r == 0 && lane == 0) PP_TRACE(t, j - x.jb, 0);
-        if (!kTimingNoPWait) sm100::mbar_wait(&p_full[t], pn[t] & 1);
-        if (r == 0 && lane == 0) PP_TRACE(t, j - x.jb, 1);
-        ++pn[t];
-        sm100::tc_fence_after();
         std::uint8_t* v = sV + st * C::kVBytes;
-        if (sm100::elect_one()) {
 #pragma unroll
-          for (int a = 0; a < 2; ++a) {
+        for (int a = 0; a < 2; ++a) {  // key half a: P columns [32a, 32a + 32), V^T atom a
+          if (a == 0 || kPHalf) {
+            if (!kTimingNoPWait) sm100::mbar_wait(&p_full[2 * t + a], pn[t] & 1);
+            sm100::tc_fence_after();
+          }
+          if (a == 0 && r == 0 && lane == 0) PP_TRACE(t, j - x.jb, 1);
+          if (sm100::elect_one()) {
             const std::uint64_t vd = sm100::sw128_kmajor_desc(sm100::smem_u32(v + a * C::kVAtom));
 #pragma unroll
             for (int kk = 0; kk < 4; ++kk)
@@ -807,8 +816,9 @@ __global__ void __launch_bounds__(kPpThreads, 1)
                 sm100::umma_bf16_ts(256u * t + 128, 256u * t + 32 * a + 8 * kk, vd + 2 * kk, idesc_o,
                                     (j > x.jb || (a | kk) != 0) ? 1u : 0u);
           }
+          __syncwarp();
         }
-        __syncwarp();
+        ++pn[t];
         if (sm100::elect_one()) {
           if (t == last_user(j)) sm100::umma_commit(&v_empty[st]);
           if (j == (t == 0 ? x.e_t[0] : x.e_t[1]) - 1) sm100::umma_commit(&o_final[t]);
@@ -866,7 +876,10 @@ __global__ void __launch_bounds__(kPpThreads, 1)
         if constexpr (kTimingSkipSoftmax) {  // dev timing: pipeline floor (P = raw S bits)
           sm100::tc_fence_before();
           __syncwarp();
-          if (lane == 0) sm100::mbar_arrive(&p_full[t]);
+          if (lane == 0) {
+            sm100::mbar_arrive(&p_full[2 * t]);
+            if (kPHalf) sm100::mbar_arrive(&p_full[2 * t + 1]);
+          }
           continue;
         }
         const int key0 = x.key_begin + j * 128;
@@ -941,12 +954,18 @@ __global__ void __launch_bounds__(kPpThreads, 1)
           }
           if constexpr (!kTimingNoPStore) sm100::tmem_st_32x32b_x16(s_tm + 16 * c, packed);
           else if (packed[0] == 0x12345u && packed[15] == 0x54321u) sm100::tmem_st_32x32b_x16(s_tm + 16 * c, packed);
+          if (kPHalf && c == 1) {  // keys 0-63 in TMEM: their PV MMAs may start
+            sm100::tmem_st_wait();
+            sm100::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) sm100::mbar_arrive(&p_full[2 * t]);
+          }
         }
         sm100::tmem_st_wait();
         sm100::tc_fence_before();
         __syncwarp();  // the warp's P stores are complete
         if (rr == 0 && r == 0) PP_TRACE(2 + t, j - x.jb, 2);
-        if (lane == 0) sm100::mbar_arrive(&p_full[t]);
+        if (lane == 0) sm100::mbar_arrive(&p_full[kPHalf ? 2 * t + 1 : 2 * t]);
         const float2 r01 = add2(rs2[0], rs2[1]), r23 = add2(rs2[2], rs2[3]);
         const float2 rsum = add2(r01, r23);
         l = l * alpha + (rsum.x + rsum.y);
