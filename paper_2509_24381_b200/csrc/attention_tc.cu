@@ -91,7 +91,7 @@ struct TcParams {
   unsigned long long* trace;
 };
 constexpr int kPpTraceIters = 24;  // key-tile iterations traced (first unit of CTA 0)
-constexpr int kPpTraceEv = 4;
+constexpr int kPpTraceEv = 8;
 __device__ __forceinline__ unsigned long long pp_gtimer() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -896,6 +896,7 @@ __global__ void __launch_bounds__(kPpThreads, 1)
           }
           sm100::tmem_ld_wait();
         }
+        if (rr == 0 && r == 0) PP_TRACE(2 + t, j - x.jb, 3);
         if (!(c_lo <= 0 && c_hi >= 128)) {
 #pragma unroll
           for (int q = 0; q < 128; ++q)
@@ -909,6 +910,7 @@ __global__ void __launch_bounds__(kPpThreads, 1)
         float mx = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
                          fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7])));
         mx *= p.scale_log2;
+        if (rr == 0 && r == 0) PP_TRACE(2 + t, j - x.jb, 4);
         const bool raise = mx > m + 8.f || (m == -INFINITY && mx != -INFINITY);
         float alpha = 1.f;
         if (raise) {
@@ -961,7 +963,9 @@ __global__ void __launch_bounds__(kPpThreads, 1)
             if (lane == 0) sm100::mbar_arrive(&p_full[2 * t]);
           }
         }
+        if (rr == 0 && r == 0) PP_TRACE(2 + t, j - x.jb, 5);
         sm100::tmem_st_wait();
+        if (rr == 0 && r == 0) PP_TRACE(2 + t, j - x.jb, 6);
         sm100::tc_fence_before();
         __syncwarp();  // the warp's P stores are complete
         if (rr == 0 && r == 0) PP_TRACE(2 + t, j - x.jb, 2);
@@ -1189,11 +1193,11 @@ void launch(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
         return v ? static_cast<long long>(v - t0) : -1ll;
       };
       std::fprintf(stderr, "[pp-trace] it | mma t0: waitP0 gotP0 S0issued | mma t1: waitP1 gotP1 S1issued | "
-                           "sm0: waitS gotS Parrive | sm1: waitS gotS Parrive (ns)\n");
+                           "sm0: waitS gotS ldS max expd stw Parrive (ns)\n");
       for (int it = 0; it < kPpTraceIters; ++it)
-        std::fprintf(stderr, "[pp-trace] %2d | %6lld %6lld %6lld | %6lld %6lld %6lld | %6lld %6lld %6lld | %6lld %6lld %6lld\n", it,
+        std::fprintf(stderr, "[pp-trace] %2d | %6lld %6lld %6lld | %6lld %6lld %6lld | %6lld %6lld %6lld %6lld %6lld %6lld %6lld\n", it,
                      at(0, it, 0), at(0, it, 1), at(0, it, 2), at(1, it, 0), at(1, it, 1), at(1, it, 2),
-                     at(2, it, 0), at(2, it, 1), at(2, it, 2), at(3, it, 0), at(3, it, 1), at(3, it, 2));
+                     at(2, it, 0), at(2, it, 1), at(2, it, 3), at(2, it, 4), at(2, it, 5), at(2, it, 6), at(2, it, 2));
     }
     if (p.max_split > 1) {
       launch_kernel(pp_merge_kernel<HD>, dim3(p.q_heads * n_blocks, 256 / 8), dim3(256), 0, st, 1, p);
