@@ -1,13 +1,30 @@
 // rserve-b200 — the B200 ExecutionBackend (see device_backend.cuh).
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <string>
+
+#include <nvtx3/nvToolsExt.h>
 
 #include "device_backend.cuh"
 #include "kernels.cuh"
 
 namespace rserve {
+namespace {
+// NVTX range over a launch call, named as the reference's TraceEvent for the
+// same work (simengine.hpp:296-303,316-323,377-384): encode_r<id>_b<slot>,
+// transfer_r<id>_b<slot>, chunk<k>_s<s> — nsys / ncu timelines line up with
+// the Chrome trace the engine exports.
+struct NvtxRange {
+  explicit NvtxRange(const char* fmt, unsigned long long a, unsigned long long b) {
+    char name[64];
+    std::snprintf(name, sizeof name, fmt, a, b);
+    nvtxRangePushA(name);
+  }
+  ~NvtxRange() { nvtxRangePop(); }
+};
+}  // namespace
 
 DeviceBackend::DeviceBackend(Context& ctx, const lmmsim::SimConfig& cfg, bool realtime, bool e2e,
                              std::uint64_t payload_seed, bool serialize_streams,
@@ -270,6 +287,7 @@ void DeviceBackend::note_call(int kind, double ms) {
 }
 
 double DeviceBackend::launch_encode(int worker, std::size_t slot, const lmmsim::EncodeBatch& b) {
+  NvtxRange nvtx_("encode_r%llu_b%llu", b.request_id, slot);
   CallTimer timer{this, 0};
   HostPhase phase_("launch_encode");
   if (remote_ != nullptr) {
@@ -315,6 +333,7 @@ double DeviceBackend::launch_encode(int worker, std::size_t slot, const lmmsim::
 }
 
 double DeviceBackend::launch_transfer(int /*worker*/, std::size_t slot, const lmmsim::EncodeBatch& b) {
+  NvtxRange nvtx_("transfer_r%llu_b%llu", b.request_id, slot);
   if (remote_ != nullptr) {  // EP: the embeddings' receive was posted at launch_encode
     for (RemoteOp& op : remote_ops_)
       if (op.kind == lmmsim::OpKind::Transfer && op.b == slot) op.launched = true;
@@ -347,6 +366,7 @@ void DeviceBackend::on_embeddings_ready(std::size_t slot, const lmmsim::EncodeBa
 }
 
 double DeviceBackend::launch_stage(int stage, const lmmsim::ChunkView& c) {
+  NvtxRange nvtx_("chunk%llu_s%llu", c.chunk_id, static_cast<unsigned long long>(stage));
   CallTimer timer{this, 1};
   HostPhase phase_("launch_stage");
   const double cost = realtime_ ? 0.0 : lmmsim::stage_time_ms(cfg_.cost, c.total_tokens, c.weighted_context);
