@@ -520,6 +520,12 @@ constexpr bool kTimingNoLoad = false;
 #define RS_PP_PHALF 1
 #endif
 constexpr bool kPHalf = RS_PP_PHALF != 0;
+// Row sum of P after P is handed to the MMA warp (the exp loop only does
+// scale, exp2, pack): -DRS_PP_SUM_AFTER_P=0 sums inside the loop.
+#ifndef RS_PP_SUM_AFTER_P
+#define RS_PP_SUM_AFTER_P 1
+#endif
+constexpr bool kSumAfterP = RS_PP_SUM_AFTER_P != 0;
 #ifdef RS_PP_TIMING_NO_SLOAD
 constexpr bool kTimingNoSLoad = true;
 #else
@@ -951,7 +957,12 @@ __global__ void __launch_bounds__(kPpThreads, 1)
               e.x = fast_exp2(x.x);
               e.y = fast_exp2(x.y);
             }
-            rs2[q & 3] = add2(rs2[q & 3], e);
+            if constexpr (kSumAfterP) {  // keep e: the row sum runs after P is released
+              sv[32 * c + 2 * q] = __float_as_uint(e.x);
+              sv[32 * c + 2 * q + 1] = __float_as_uint(e.y);
+            } else {
+              rs2[q & 3] = add2(rs2[q & 3], e);
+            }
             packed[q] = pack_bf16x2(e.x, e.y);
           }
           if constexpr (!kTimingNoPStore) sm100::tmem_st_32x32b_x16(s_tm + 16 * c, packed);
@@ -970,6 +981,11 @@ __global__ void __launch_bounds__(kPpThreads, 1)
         __syncwarp();  // the warp's P stores are complete
         if (rr == 0 && r == 0) PP_TRACE(2 + t, j - x.jb, 2);
         if (lane == 0) sm100::mbar_arrive(&p_full[kPHalf ? 2 * t + 1 : 2 * t]);
+        if constexpr (kSumAfterP) {  // off the S -> P -> PV critical path
+#pragma unroll
+          for (int q = 0; q < 64; ++q)
+            rs2[q & 3] = add2(rs2[q & 3], make_float2(__uint_as_float(sv[2 * q]), __uint_as_float(sv[2 * q + 1])));
+        }
         const float2 r01 = add2(rs2[0], rs2[1]), r23 = add2(rs2[2], rs2[3]);
         const float2 rsum = add2(r01, r23);
         l = l * alpha + (rsum.x + rsum.y);
