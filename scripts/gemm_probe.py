@@ -25,7 +25,7 @@ SHAPES = [  # (M, N, K, epi, label)
     (2048, 37888, 3584, 2, "llm_gateup"), (256, 3584, 18944, 1, "llm_down_m256"),
     (256, 37888, 3584, 2, "llm_gateup_m256"),
 ]
-BNS = [0, 128, 144, 160, 192, 208, 224, 256, -128, -144, -160, -192, -208, -224, -256]
+BNS = [0, 128, 160, 192, 224, 256, -128, -160, -192, -224, -256]
 
 
 SMALL_M = [(m, n, k, e, f"{lab}_m{m}") for m in (128, 256)
