@@ -143,6 +143,7 @@ DeviceBackend::~DeviceBackend() {
   }
   if (copy_stream_) cudaStreamDestroy(copy_stream_);
   remote_ops_.clear();
+  chunk_logits_.clear();
   slot_xfer_.clear();
   for (void* p : ctrl_dev_) cudaFree(p);
   for (std::int64_t* p : ctrl_host_) cudaFreeHost(p);
@@ -496,7 +497,7 @@ void DeviceBackend::forward_chunk(const lmmsim::ChunkView& c, const ChunkState& 
         op.xfers.push_back(t.post_recv(topo.p_rank(st), remote_logits_ + static_cast<std::int64_t>(r.slot) * s.vocab,
                                        static_cast<std::size_t>(s.vocab) * 4, nullptr));
       }
-      chunk_logits_[c.chunk_id] = op.xfers.back()->done;
+      chunk_logits_[c.chunk_id] = op.xfers.back();
     }
     remote_ops_.push_back(std::move(op));
   }
@@ -530,7 +531,7 @@ void DeviceBackend::on_request_complete(lmmsim::RequestId id, std::size_t chunk)
     for (RemoteOp& op : remote_ops_)
       if (op.kind == lmmsim::OpKind::Stage && op.b == chunk)
         for (auto& x : op.xfers) remote_->t->wait_posted(*x);
-    RS_CUDA_CHECK(cudaStreamWaitEvent(copy_stream_, chunk_logits_.at(chunk), 0));
+    RS_CUDA_CHECK(cudaStreamWaitEvent(copy_stream_, chunk_logits_.at(chunk)->done, 0));
     RS_CUDA_CHECK(cudaMemcpyAsync(logits_host_.at(id),
                                   remote_logits_ + static_cast<std::int64_t>(done_slots_.at(id)) * ctx_.shapes().vocab,
                                   static_cast<std::size_t>(ctx_.shapes().vocab) * 4, cudaMemcpyDeviceToHost,

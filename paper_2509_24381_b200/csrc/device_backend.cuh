@@ -153,7 +153,9 @@ class DeviceBackend final : public lmmsim::ExecutionBackend {
   std::unordered_map<lmmsim::RequestId, std::vector<lmmsim::SegmentSpec>> layouts_;
   std::vector<RemoteOp> remote_ops_;
   std::unordered_map<std::size_t, std::shared_ptr<ep::Xfer>> slot_xfer_;
-  std::unordered_map<std::size_t, cudaEvent_t> chunk_logits_;  // chunk -> last logits arrival
+  // chunk -> its last logits arrival: the transfer itself is held (its event
+  // goes back to the transport's pool, and is re-recorded, once released)
+  std::unordered_map<std::size_t, std::shared_ptr<ep::Xfer>> chunk_logits_;
   static constexpr int kCtrlRing = 16;
   std::vector<void*> ctrl_dev_;
   std::vector<std::int64_t*> ctrl_host_;

@@ -47,19 +47,22 @@ def rank_main(rank, world, port, same, transport, q):
                            cost=api.CostModel(alpha_enc_ms=0.5, beta_enc_ms_per_token=0.01, eps_tx_ms=0.2,
                                               zeta_tx_ms_per_token=0.001, delta_stage_ms_per_token=0.01))
         out = None
-        for clock in ("lockstep", "real"):
-            print(f"rank {rank}: {clock} run", flush=True)
+        # the third run: real clock with host inputs and the logits read back
+        # through the C-ABI (e2e) — the last stage's logits transfers are
+        # waited on after their completion was polled
+        for clock, e2e in (("lockstep", False), ("real", False), ("real", True)):
+            print(f"rank {rank}: {clock} run (e2e={e2e})", flush=True)
             if rank == 0:
                 dist.barrier()
-                log, journal, stats = g.run(ctx, None, WL, sc, clock=clock, payload_seed=7)
+                log, journal, stats = g.run(ctx, None, WL, sc, clock=clock, payload_seed=7, e2e=e2e)
                 ok = log == api.simulate(WL, sc)[0] if clock == "lockstep" else True
-                out = dict(clock=clock, decisions_equal=ok, gpu_ms=stats["gpu_ms"], log=log,
+                out = dict(clock=clock + ("_e2e" if e2e else ""), decisions_equal=ok, gpu_ms=stats["gpu_ms"], log=log,
                            journal=journal,
                            logits={r: ctx.logits(r)[0].tolist() for r in (0, 1, 2)},
                            argmax={r: ctx.logits(r)[1] for r in (0, 1, 2)})
                 q.put((rank, init_s, out))
             else:
-                g.worker_prepare(ctx, WL, payload_seed=7)
+                g.worker_prepare(ctx, WL, payload_seed=7, e2e=e2e)
                 dist.barrier()
                 g.worker_run(ctx)
         dist.barrier()
@@ -93,7 +96,7 @@ def main():
     # Drain the queue before joining: a child blocks at exit until its queued
     # results are written to the pipe.
     results = []
-    expected = 2 + (a.world - 1)  # rank 0: one per clock; workers: one each
+    expected = 3 + (a.world - 1)  # rank 0: one per run; workers: one each
     import queue
     while len(results) < expected:
         try:

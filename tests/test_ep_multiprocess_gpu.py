@@ -36,6 +36,6 @@ def test_ep_ipc_processes(world, tmp_path):
     for rid, layout in LAYOUTS.items():
         emb = mo.request_embeddings(cfg, w, rid, layout, 7, 256)
         ref = llm.first_token_logits(llm.forward(emb, mo.mrope_positions(mo.parse_layout(layout)))[-1])
-        for clock in ("lockstep", "real"):
+        for clock in ("lockstep", "real", "real_e2e"):
             got = np.asarray(runs[clock]["logits"][str(rid)], dtype=np.float32)
             assert np.abs(got - ref).max() <= 0.05 * ref.std()
