@@ -1000,6 +1000,13 @@ def run_reference(args):
     ws, rank, _ = dist_env()
     if rank != 0:
         return
+    # every host thread for the BLAS the numpy oracle runs on (torch.distributed.run
+    # exports OMP_NUM_THREADS=1 to its children; BLAS read it at import)
+    try:
+        from threadpoolctl import threadpool_limits
+        threadpool_limits(os.cpu_count())
+    except ImportError:  # pragma: no cover - threadpoolctl is in the image
+        pass
     from oracle import ref
     m = qwen7b_shapes()
     ep = ep_mode(args, ws)
