@@ -1000,13 +1000,15 @@ def run_reference(args):
     ws, rank, _ = dist_env()
     if rank != 0:
         return
-    # every host thread for the BLAS the numpy oracle runs on (torch.distributed.run
-    # exports OMP_NUM_THREADS=1 to its children; BLAS read it at import)
-    try:
-        from threadpoolctl import threadpool_limits
-        threadpool_limits(os.cpu_count())
-    except ImportError:  # pragma: no cover - threadpoolctl is in the image
-        pass
+    # every host thread for the BLAS the numpy oracle runs on: torch.distributed.run
+    # exports OMP_NUM_THREADS=1 to its children and BLAS size their pools at
+    # import, so rank 0 re-runs this arm in a child with the full count
+    nproc = str(os.cpu_count())
+    if ws > 1 and os.environ.get("OMP_NUM_THREADS") != nproc and not os.environ.get("RS_REF_CHILD"):
+        env = dict(os.environ, OMP_NUM_THREADS=nproc, OPENBLAS_NUM_THREADS=nproc, MKL_NUM_THREADS=nproc,
+                   RS_REF_CHILD="1")
+        subprocess.run([sys.executable] + sys.argv, env=env, check=True)
+        return
     from oracle import ref
     m = qwen7b_shapes()
     ep = ep_mode(args, ws)
