@@ -138,9 +138,17 @@ Context::Context(const rs_model_config& model, const rs_ctx_options& opt) : opt_
     // exchange buffer: [2 phases][max_chunk, d] bf16 partials + flag slots;
     // cudaMalloc'd on its own so one IPC handle maps it into peer processes
     const std::size_t part = static_cast<std::size_t>(opt_.max_chunk_tokens) * s_.d * sizeof(bf16);
-    tpx_bytes_ = 2 * part + sizeof(unsigned) * kTpBlocks * kMaxTpRanks;
+    // + a 64-byte header (magic, rank, ranks, max chunk rows, d) that peers
+    // check at connect: ranks with different shapes would read past each
+    // other's partials
+    tpx_bytes_ = 2 * part + sizeof(unsigned) * kTpBlocks * kMaxTpRanks + kTpHeaderBytes;
     RS_CUDA_CHECK(cudaMalloc(&tpx_, tpx_bytes_));
     RS_CUDA_CHECK(cudaMemsetAsync(tpx_, 0, tpx_bytes_, aux_));
+    const std::int32_t hdr[5] = {kTpMagic, opt_.tp_rank, opt_.tp_size, static_cast<std::int32_t>(opt_.max_chunk_tokens),
+                                 s_.d};
+    RS_CUDA_CHECK(cudaMemcpyAsync(static_cast<std::uint8_t*>(tpx_) + tpx_bytes_ - kTpHeaderBytes, hdr, sizeof hdr,
+                                  cudaMemcpyHostToDevice, aux_));
+    RS_CUDA_CHECK(cudaStreamSynchronize(aux_));
     tp_ss_ = static_cast<unsigned long long*>(arena_.alloc(static_cast<std::size_t>(opt_.max_chunk_tokens) * 8));
     tpx_peers_.assign(static_cast<std::size_t>(tp), nullptr);
   } else if (tp > 1) {
@@ -848,6 +856,17 @@ void Context::tp_connect(const void* const* ptrs, const cudaIpcMemHandle_t* hand
       RS_CUDA_CHECK(cudaIpcOpenMemHandle(&p, handles[r], cudaIpcMemLazyEnablePeerAccess));
       tpx_opened_[static_cast<std::size_t>(r)] = true;
     }
+  }
+  // every rank's header: same group size / chunk rows / width, rank r at slot r
+  for (int r = 0; r < T; ++r) {
+    std::int32_t h[5];
+    RS_CUDA_CHECK(cudaMemcpy(h, static_cast<std::uint8_t*>(tpx_peers_[static_cast<std::size_t>(r)]) + tpx_bytes_ -
+                                    kTpHeaderBytes, sizeof h, cudaMemcpyDeviceToHost));
+    if (h[0] != kTpMagic || h[1] != r || h[2] != T || h[3] != static_cast<std::int32_t>(opt_.max_chunk_tokens) ||
+        h[4] != s_.d)
+      throw lmmsim::ConfigError("tp connect: rank " + std::to_string(r) + "'s exchange buffer is not a rank " +
+                                std::to_string(r) + " of this group (ranks " + std::to_string(h[2]) + ", chunk rows " +
+                                std::to_string(h[3]) + ", width " + std::to_string(h[4]) + ")");
   }
   RS_CUDA_CHECK(cudaStreamSynchronize(aux_));  // the zeroed flags are in place before any peer signals
   tp_connected_ = true;

@@ -23,6 +23,8 @@
 namespace rserve {
 
 constexpr int kPageTokens = 64;  // slot pages and KV pages
+constexpr std::size_t kTpHeaderBytes = 64;       // TP exchange buffer header (at its end)
+constexpr std::int32_t kTpMagic = 0x52535450;    // "RSTP"
 
 /// Hash stream of the synthetic pixels of multimodal item `item` of request `req`.
 inline std::uint64_t pixel_stream(std::uint64_t req, std::uint64_t item) {

@@ -868,9 +868,17 @@ __global__ void __launch_bounds__(128, 16) tp_group_reduce_kernel(const TpGroupA
     asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(peer), "r"(a.epoch) : "memory");
     const unsigned* mine = a.flags[a.rank] + blockIdx.x * kMaxTpRanks + t;
     unsigned v;
-    do {
+    unsigned long long t0 = 0;
+    for (unsigned spins = 0;; ++spins) {
       asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(mine) : "memory");
-    } while (static_cast<int>(v - a.epoch) < 0);
+      if (static_cast<int>(v - a.epoch) >= 0) break;
+      if ((spins & 1023u) == 1023u) {  // a rank that never joins: fail the launch instead of hanging the GPU
+        unsigned long long now;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+        if (t0 == 0) t0 = now;
+        else if (now - t0 > 30ull * 1000 * 1000 * 1000) __trap();
+      }
+    }
   }
   __syncthreads();
   // only now may the next kernel of this stream start (PDL): a dependent grid

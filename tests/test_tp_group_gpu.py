@@ -105,4 +105,12 @@ def test_tp_group_config_errors():
     x = torch.zeros(16, m.llm_dim, device="cuda", dtype=torch.bfloat16)
     with pytest.raises(N.ConfigError, match="rs_tp_connect"):
         r.tp_prefill([(1, 0, 16)], x.data_ptr())  # not connected: refused before any kernel spins
+    # a peer of another shape (chunk rows) or the buffers in the wrong rank order: refused at connect
+    other = api.Pipeline(m, max_prompt_tokens=512, slot_tokens=64, kv_tokens=1024, max_chunk_tokens=128,
+                         max_encode_tokens=64, with_vit=False, tp_size=2, tp_rank=1, tp_group=True)
+    with pytest.raises(N.ConfigError, match="exchange buffer"):
+        r.tp_connect([r.tp_buffer()[0], other.tp_buffer()[0]])
+    with pytest.raises(N.ConfigError, match="exchange buffer"):
+        r.tp_connect([other.tp_buffer()[0], r.tp_buffer()[0]])
+    other.close()
     r.close()
