@@ -600,9 +600,13 @@ def run_ours(args):
     pipe.close()
     if ws == 1 and args.cfg45:
         # configs 4 / 5 (their 4E+4P placement needs 8 GPUs): co-located here,
-        # after the cfg2 context is gone (cfg5's 72B weights take 145 GB)
-        line["cfg4"] = run_cfg4(1)
-        line["cfg5"] = run_cfg5(2)
+        # after the cfg2 context is gone (cfg5's 72B weights take 145 GB); a
+        # failure is recorded, never allowed to cost the headline line
+        for key, fn, steps in (("cfg4", run_cfg4, 1), ("cfg5", run_cfg5, 2)):
+            try:
+                line[key] = fn(steps)
+            except Exception as e:  # e.g. a box with less free HBM than cfg5's 150 GB
+                line[key] = {"error": f"{type(e).__name__}: {str(e)[:300]}"}
     if rank == 0:
         print(json.dumps(line))
     if ws > 1:

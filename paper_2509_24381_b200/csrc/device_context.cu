@@ -744,6 +744,8 @@ void Context::export_kv(lmmsim::RequestId id, void* dst, std::uint64_t cap, rs_k
   if (!llm_ || !llm_->has_head())
     throw lmmsim::ConfigError("KV export: the request's first token lives on the last stage (needs the LM head)");
   if (r.kv_pages.empty()) throw lmmsim::InternalError("KV export: request " + lmmsim::format_u64(id) + " holds no KV");
+  if (r.slot_freed_tokens < r.total)  // a kept request has been prefilled (and its slab released) to the end
+    throw lmmsim::InternalError("KV export: request " + lmmsim::format_u64(id) + " is not fully prefilled");
   const std::uint64_t bytes = kv_image_bytes(r.total);
   if (cap < bytes)
     throw lmmsim::ConfigError("KV export: buffer of " + lmmsim::format_u64(cap) + " bytes < image of " +
