@@ -485,30 +485,18 @@ def run_ours(args):
     # cfg3: the Poisson request stream the N > 1 runs measure, co-located here
     cfg3 = None
     if args.cfg3_steps > 0 and ws == 1:
-        cfg3 = run_cfg3_colocated(args, pipe, m, replay)
+        try:
+            cfg3 = run_cfg3_colocated(args, pipe, m, replay)
+        except Exception as e:  # recorded; the headline line must still print
+            cfg3 = {"error": f"{type(e).__name__}: {str(e)[:300]}"}
     # Decode after the first token (the reference stops at TTFT):
     # the request's KV stays on the device, then greedy decode steps.
     decode = None
     if args.decode_steps > 0:
-        pipe.run(wl, sc, clock="real", payload_seed=1234, keep_kv=True)
-        pipe.decode([0], 2)
-        pipe.decode_release(0)
-        pipe.run(wl, sc, clock="real", payload_seed=1234, keep_kv=True)
-        toks, _, dms = pipe.decode([0], args.decode_steps)
-        pipe.decode_release(0)
-        hbm_gbs = peaks()[2]
-        llm_bytes = 2.0 * (m["llm_layers"] * (m["llm_dim"] * (m["llm_q_heads"] + 2 * m["llm_kv_heads"]) *
-                                               m["llm_head_dim"] + m["llm_q_heads"] * m["llm_head_dim"] *
-                                               m["llm_dim"] + 3 * m["llm_dim"] * m["llm_ff"]) +
-                           m["vocab"] * m["llm_dim"])
-        decode = {"steps": args.decode_steps, "batch": 1, "ms_per_step": dms / args.decode_steps,
-                  "tokens_per_s": args.decode_steps / (dms / 1e3),
-                  "context_tokens": PROMPT_TOKENS,
-                  "roofline": {"bound": "hbm", "bytes_per_step": llm_bytes,
-                               "bound_ms": llm_bytes / (hbm_gbs * 1e9) * 1e3,
-                               "frac": (llm_bytes / (hbm_gbs * 1e9) * 1e3) / (dms / args.decode_steps)},
-                  "note": "greedy decode of the cfg2 request after its first token (device time, "
-                          "CUDA events); per step every LLM weight is read once (batch 1)"}
+        try:
+            decode = run_decode(args, pipe, wl, sc, m)
+        except Exception as e:  # recorded; the headline line must still print
+            decode = {"error": f"{type(e).__name__}: {str(e)[:300]}"}
     total_ms = sum(dev_ms)
     if ws > 1:
         import torch.distributed as dist
@@ -535,7 +523,10 @@ def run_ours(args):
         ncu_full = json.load(open(ncu_path))
     parity = replay.summary()
     if rank == 0 and not args.no_parity:
-        parity.update(cfg2_logit_parity(logits_cfg2, am_cfg2, f"cuda:{local}"))
+        try:
+            parity.update(cfg2_logit_parity(logits_cfg2, am_cfg2, f"cuda:{local}"))
+        except Exception as e:
+            parity["logit_check_error"] = f"{type(e).__name__}: {str(e)[:300]}"
     line = {
         "metric": "encode+prefill tokens/s (p50/p99 TTFT ms alongside)",
         "value": value, "unit": "tokens/s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
@@ -596,7 +587,10 @@ def run_ours(args):
         "clocks": clk.summary(),
     }
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
-        line["cpu_baseline"] = cpu_baseline(args, reps=1)
+        try:
+            line["cpu_baseline"] = cpu_baseline(args, reps=1)
+        except Exception as e:
+            line["cpu_baseline"] = {"error": f"{type(e).__name__}: {str(e)[:300]}"}
     pipe.close()
     if ws == 1 and args.cfg45:
         # configs 4 / 5 (their 4E+4P placement needs 8 GPUs): co-located here,
@@ -611,6 +605,53 @@ def run_ours(args):
         print(json.dumps(line))
     if ws > 1:
         torch.distributed.destroy_process_group()
+
+
+def run_decode(args, pipe, wl, sc, m):
+    """Greedy decode of the cfg2 request after its first token:
+    the request's KV stays on the device (keep_kv), then batched decode steps."""
+    pipe.run(wl, sc, clock="real", payload_seed=1234, keep_kv=True)
+    pipe.decode([0], 2)
+    pipe.decode_release(0)
+    pipe.run(wl, sc, clock="real", payload_seed=1234, keep_kv=True)
+    # PD (prefill -> decode) transfer of the request's KV image, imported as
+    # request 1 on the same context (the cross-GPU move is the caller's copy)
+    import torch
+    nbytes = pipe.kv_image_bytes(PROMPT_TOKENS)
+    img = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+    st = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(st)
+    meta = pipe.kv_export(0, img.data_ptr(), nbytes, stream=st.cuda_stream)
+    pipe.kv_import(1, meta, img.data_ptr(), stream=st.cuda_stream)
+    e1.record(st)
+    e1.synchronize()
+    pd_ms = e0.elapsed_time(e1)
+    toks, _, dms = pipe.decode([0], args.decode_steps)
+    toks_pd, _, _ = pipe.decode([1], args.decode_steps)
+    pipe.decode_release(0)
+    pipe.decode_release(1)
+    del img
+    hbm_gbs = peaks()[2]
+    llm_bytes = 2.0 * (m["llm_layers"] * (m["llm_dim"] * (m["llm_q_heads"] + 2 * m["llm_kv_heads"]) *
+                                           m["llm_head_dim"] + m["llm_q_heads"] * m["llm_head_dim"] *
+                                           m["llm_dim"] + 3 * m["llm_dim"] * m["llm_ff"]) +
+                       m["vocab"] * m["llm_dim"])
+    decode = {"steps": args.decode_steps, "batch": 1, "ms_per_step": dms / args.decode_steps,
+              "tokens_per_s": args.decode_steps / (dms / 1e3),
+              "context_tokens": PROMPT_TOKENS,
+              "roofline": {"bound": "hbm", "bytes_per_step": llm_bytes,
+                           "bound_ms": llm_bytes / (hbm_gbs * 1e9) * 1e3,
+                           "frac": (llm_bytes / (hbm_gbs * 1e9) * 1e3) / (dms / args.decode_steps)},
+              "note": "greedy decode of the cfg2 request after its first token (device time, "
+                      "CUDA events); per step every LLM weight is read once (batch 1)",
+              "pd_transfer": {"image_bytes": nbytes, "export_import_ms": pd_ms,
+                              "gbs": 2.0 * 2 * nbytes / (pd_ms / 1e3) / 1e9,
+                              "decoded_tokens_equal": bool((toks == toks_pd).all()),
+                              "note": "rs_kv_export + rs_kv_import of the 8576-token KV (pack + unpack, "
+                                      "each reads and writes the image: 4 x bytes); decoding the imported "
+                                      "request gives the local request's tokens"}}
+    return decode
 
 
 def run_cfg3_colocated(args, pipe, m, replay):
