@@ -380,14 +380,22 @@ __global__ void __launch_bounds__(kDecThreads) decode_attn_split_kernel(
     const std::int64_t page = pt[t];
     const bf16* kp = k_cache + (page * kv_heads + kvh) * kDecTile * HD;
     const bf16* vp = v_cache + (page * kv_heads + kvh) * HD * kDecTile;
-    __syncthreads();  // previous tile's k / vt / p consumed
-    for (int i = tid; i < kDecTile * HD / 8; i += kDecThreads) {
-      const int r = i / (HD / 8), c = (i % (HD / 8)) * 8;
-      *reinterpret_cast<uint4*>(&sm.k[r][c]) = *reinterpret_cast<const uint4*>(kp + r * HD + c);
+    // every 16-byte load of the K and V^T pages in flight before the first
+    // shared-memory store (the kernel is bound by the loads' latency)
+    constexpr int kVec = kDecTile * HD / 8 / kDecThreads;  // uint4 per thread per page
+    uint4 kr[kVec], vr[kVec];
+#pragma unroll
+    for (int j = 0; j < kVec; ++j) {
+      const int i = tid + j * kDecThreads;
+      kr[j] = __ldcs(reinterpret_cast<const uint4*>(kp) + i);
+      vr[j] = __ldcs(reinterpret_cast<const uint4*>(vp) + i);
     }
-    for (int i = tid; i < HD * kDecTile / 8; i += kDecThreads) {
-      const int r = i / (kDecTile / 8), c = (i % (kDecTile / 8)) * 8;
-      *reinterpret_cast<uint4*>(&sm.vt[r][c]) = *reinterpret_cast<const uint4*>(vp + r * kDecTile + c);
+    __syncthreads();  // previous tile's k / vt / p consumed
+#pragma unroll
+    for (int j = 0; j < kVec; ++j) {
+      const int i = tid + j * kDecThreads;
+      *reinterpret_cast<uint4*>(&sm.k[i / (HD / 8)][(i % (HD / 8)) * 8]) = kr[j];
+      *reinterpret_cast<uint4*>(&sm.vt[i / (kDecTile / 8)][(i % (kDecTile / 8)) * 8]) = vr[j];
     }
     __syncthreads();
     // S[g][key]: thread -> key (tid % 64), heads g = tid / 64 + 2j
