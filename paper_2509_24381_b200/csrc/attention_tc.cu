@@ -526,6 +526,15 @@ constexpr bool kPHalf = RS_PP_PHALF != 0;
 #define RS_PP_SUM_AFTER_P 1
 #endif
 constexpr bool kSumAfterP = RS_PP_SUM_AFTER_P != 0;
+// Softmax turn-taking (FA3-style ping-pong between the two softmax
+// warpgroups): named barriers hand a token back and forth so only one tile's
+// exp loop runs at a time while the tensor pipe works on the other tile.
+// 0: off; 1: the token covers S load + max + exp; 2: the exp loop only.
+#ifndef RS_PP_ORDER
+#define RS_PP_ORDER 0
+#endif
+constexpr int kOrder = RS_PP_ORDER;
+constexpr int kTurnBar0 = 8;  // named barrier ids 8 (tile 0's turn), 9 (tile 1's turn)
 #ifdef RS_PP_TIMING_NO_SLOAD
 constexpr bool kTimingNoSLoad = true;
 #else
@@ -850,10 +859,13 @@ __global__ void __launch_bounds__(kPpThreads, 1)
     const std::uint32_t s_tm = tmem + lane_off + 256 * t;
     const std::uint32_t o_tm = s_tm + 128;
     std::uint32_t sn = 0, on = 0;
+    if (kOrder != 0 && t == 1) sm100::named_bar_arrive(kTurnBar0, 256);  // tile 0 goes first
     for (int rr = 0;; ++rr) {
       const int u = pp_unit_index(rr, n_units);
       if (u < 0) break;
       const PpUnit x = pp_unit<MODE>(p, u);
+      // iterations both tiles run take turns; a tile's extra ones do not
+      const int n_common = max(0, min(x.e_t[0], x.e_t[1]) - x.jb);
       const int j_end = t == 0 ? x.e_t[0] : x.e_t[1];
       const int my_rows = t == 0 ? x.rows_t[0] : x.rows_t[1];
       if (j_end <= x.jb) continue;
@@ -879,6 +891,8 @@ __global__ void __launch_bounds__(kPpThreads, 1)
         if (rr == 0 && r == 0) PP_TRACE(2 + t, j - x.jb, 1);
         ++sn;
         sm100::tc_fence_after();
+        const bool turn = kOrder != 0 && j - x.jb < n_common;
+        if (kOrder == 1 && turn) sm100::named_bar_sync(kTurnBar0 + t, 256);
         if constexpr (kTimingSkipSoftmax) {  // dev timing: pipeline floor (P = raw S bits)
           sm100::tc_fence_before();
           __syncwarp();
@@ -935,6 +949,7 @@ __global__ void __launch_bounds__(kPpThreads, 1)
             sm100::tmem_st_32x32b_x32(o_tm + 32 * c, v);
           }
         }
+        if (kOrder == 2 && turn) sm100::named_bar_sync(kTurnBar0 + t, 256);
         const float mneg = m == -INFINITY ? 0.f : -m;
         const float2 scale2 = make_float2(p.scale_log2, p.scale_log2), mneg2 = make_float2(mneg, mneg);
         float2 rs2[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f),
@@ -975,6 +990,7 @@ __global__ void __launch_bounds__(kPpThreads, 1)
           }
         }
         if (rr == 0 && r == 0) PP_TRACE(2 + t, j - x.jb, 5);
+        if (turn) sm100::named_bar_arrive(kTurnBar0 + (t ^ 1), 256);  // the other tile's turn
         sm100::tmem_st_wait();
         if (rr == 0 && r == 0) PP_TRACE(2 + t, j - x.jb, 6);
         sm100::tc_fence_before();
@@ -1037,6 +1053,7 @@ __global__ void __launch_bounds__(kPpThreads, 1)
       // O_t is read out (tcgen05.ld waited): the next unit's first PV may overwrite it
       sm100::tc_fence_before();
     }
+    if (kOrder != 0 && t == 0) sm100::named_bar_sync(kTurnBar0, 256);  // tile 1's last hand-back
   }
   __syncthreads();
   if (warp == 1) {

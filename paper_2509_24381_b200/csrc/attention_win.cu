@@ -270,6 +270,19 @@ __global__ void __launch_bounds__(kWinThreads, 1)
       int it = 0;
       for (int u = blockIdx.x; u < p.n_units; u += gridDim.x, ++it) {
         const int s = it % kWinStages, b = it & 1;
+        // PV of the previous unit as soon as its P is in TMEM, unless this
+        // unit's prep finishes first (then S first): whichever is ready
+        bool pv_done = it == 0;
+        if (!pv_done) {
+          for (;;) {
+            if (sm100::mbar_test(&p_full[(it - 1) & 1], ((it - 1) >> 1) & 1)) {
+              issue_pv(it - 1);
+              pv_done = true;
+              break;
+            }
+            if (sm100::mbar_test(&prepped[s], (it / kWinStages) & 1)) break;
+          }
+        }
         sm100::mbar_wait(&prepped[s], (it / kWinStages) & 1);
         sm100::mbar_wait(&tmem_free[b], ((it >> 1) & 1) ^ 1);
         sm100::tc_fence_after();
@@ -283,7 +296,7 @@ __global__ void __launch_bounds__(kWinThreads, 1)
           sm100::umma_bf16(tmem + 128 * b, make_desc(so + kQt, 16, 256, kLayoutSW32),
                            make_desc(so + kKt, 16, 256, kLayoutSW32), idesc_s, 1u);
         sm100::umma_commit(&s_full[b]);
-        if (it > 0) issue_pv(it - 1);
+        if (!pv_done) issue_pv(it - 1);
       }
       if (it > 0) issue_pv(it - 1);
     }
@@ -326,14 +339,21 @@ __global__ void __launch_bounds__(kWinThreads, 1)
             cz[e] = make_float2(v.x, v.y);
             cz[e + 1] = make_float2(v.z, v.w);
           }
+          // all four chunk loads (Q, K halves) in flight before any math / store
+          std::uint32_t pa[2], pb[2];
+          uint4 a[2], bv[2];
 #pragma unroll
           for (int which = 0; which < 2; ++which) {  // Q, K
             const std::uint32_t mo = which == 0 ? kQm : kKm, to = which == 0 ? kQt : kKt;
-            const std::uint32_t pa = so + chunk_off<HD>(r, c, mo, to);
-            const std::uint32_t pb = so + chunk_off<HD>(r, c + C::kChunkPairs, mo, to);
-            uint4 a = lds128(pa), bv = lds128(pb);
-            std::uint32_t* aw = reinterpret_cast<std::uint32_t*>(&a);
-            std::uint32_t* bw = reinterpret_cast<std::uint32_t*>(&bv);
+            pa[which] = so + chunk_off<HD>(r, c, mo, to);
+            pb[which] = so + chunk_off<HD>(r, c + C::kChunkPairs, mo, to);
+            a[which] = lds128(pa[which]);
+            bv[which] = lds128(pb[which]);
+          }
+#pragma unroll
+          for (int which = 0; which < 2; ++which) {
+            std::uint32_t* aw = reinterpret_cast<std::uint32_t*>(&a[which]);
+            std::uint32_t* bw = reinterpret_cast<std::uint32_t*>(&bv[which]);
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
               const float2 x = unpack_bf16x2(aw[e]), y = unpack_bf16x2(bw[e]);
@@ -341,8 +361,11 @@ __global__ void __launch_bounds__(kWinThreads, 1)
               aw[e] = pack_bf16x2(x.x * c0.x - y.x * c0.y, x.y * c1.x - y.y * c1.y);
               bw[e] = pack_bf16x2(y.x * c0.x + x.x * c0.y, y.y * c1.x + x.y * c1.y);
             }
-            sts128(pa, a);
-            sts128(pb, bv);
+          }
+#pragma unroll
+          for (int which = 0; which < 2; ++which) {
+            sts128(pa[which], a[which]);
+            sts128(pb[which], bv[which]);
           }
         }
       }
