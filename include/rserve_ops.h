@@ -51,6 +51,14 @@ RS_API rs_status rs_op_attention_prefill(const void* q, int ld_q, int rows_alloc
                                          const void* v_cache, long long kv_pages,
                                          const int* page_table, int q_heads, int kv_heads,
                                          int head_dim, float scale, void* stream);
+/* Decode attention: q row i (one token of request i, at prompt position
+ * q_pos[i], host array) attends keys [0, q_pos[i]] of the paged cache through
+ * page_tables[i] (host array of n_req device int32 page tables); GQA with
+ * q_heads / kv_heads <= 16, head_dim 64 or 128. Synchronous. */
+RS_API rs_status rs_op_attention_decode(const void* q, int ld_q, void* out, int ld_out, int n_req,
+                                        const int* q_pos, const int* const* page_tables, const void* k_cache,
+                                        const void* v_cache, int q_heads, int kv_heads, int head_dim,
+                                        float scale, void* stream);
 /* Kernel launches issued by this process so far (our kernels only). */
 RS_API unsigned long long rs_kernel_launches(void);
 /* Live per-kernel-class timing: CUDA events recorded on each launch stream

@@ -232,6 +232,8 @@ _sig("rs_op_attention_varlen_tc", [VP, I, VP, I, VP, I, I, I, I, C.c_float, VP])
 _sig("rs_op_attention_window_tc", [VP, I, VP, I, VP, I, I, I, I, C.c_float, VP, C.c_float, VP])
 _sig("rs_op_attention_prefill", [VP, I, I, VP, I, I, I, VP, VP, C.c_longlong, VP, I, I, I,
                                   C.c_float, VP])
+_sig("rs_op_attention_decode", [VP, I, VP, I, I, C.POINTER(C.c_int), C.POINTER(C.c_void_p), VP, VP, I, I, I,
+                                 C.c_float, VP])
 _sig("rs_kernel_launches", [], C.c_ulonglong)
 _sig("rs_profile_enable", [C.c_int])
 _sig("rs_payload_generate", [C.c_char_p, C.c_uint64, PCHAR])

@@ -7,6 +7,9 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
 #include <cmath>
 #include <mutex>
 #include <unordered_map>
@@ -327,178 +330,314 @@ void attention_varlen_bidir(const bf16* qkv, int ld_qkv, bf16* out, int ld_out,
 
 
 // ---- decode attention -----------------------------------------------
-// One query row per request (the token being decoded) against its paged KV:
-// memory-bound (each K / V byte is read once per kv head), so CUDA-core math,
-// GQA-packed (the G = Hq / Hkv query heads of a kv head share every K / V tile
-// in shared memory) and split along the keys (flash-decoding) so a single
-// request still spreads over the SMs; a second kernel merges the splits in
-// split order (deterministic).
+// One query row per request (the token being decoded) against its paged KV.
+// HBM-bound: each K / V byte is read once per kv head, so the kernel is built
+// to keep the whole KV stream in flight, not for FLOPs:
+//   * a CTA = 4 warps over a contiguous range of key tiles (64-token pages) of
+//     one (request, kv head); every warp cp.asyncs its own K and V^T page pair
+//     (32 KB for hd 128) into a private swizzled smem slot, so one CTA per SM
+//     has 4 pages in flight and a 8.6k-token request's 4 kv heads spread over
+//     all SMs with ~one page per warp;
+//   * the G = Hq / Hkv query heads of the kv head are the M rows of bf16
+//     m16n8k16 MMAs (padded to 16): S = Q K^T takes K rows as the B operand
+//     (ldmatrix, no transpose), S's accumulator layout is P's A-operand layout,
+//     and O = P V takes the cached V^T rows as B (no transpose either);
+//   * every page but the one holding this step's token is loaded before the
+//     PDL wait (overlapping the QKV GEMV / RoPE-append kernels before it);
+//   * online softmax per warp in base 2, the 4 warps merged in shared memory,
+//     the CTAs of a (request, kv head) merged by a one-warp-per-head merge
+//     kernel launched under PDL, all in split order: deterministic.
 namespace {
 
-constexpr int kDecThreads = 128;
-constexpr int kDecMaxG = 8;
+constexpr int kDecWarps = 4;
+constexpr int kDecThreads = 32 * kDecWarps;
+constexpr int kDecMaxG = 16;  // MMA rows
 constexpr int kDecTile = 64;  // keys per tile = one KV page
 
 template <int HD>
-struct DecSmem {
-  float q[kDecMaxG][HD];
-  bf16 k[kDecTile][HD + 8];      // +16 B row pad: conflict-free column reads
-  bf16 vt[HD][kDecTile + 8];     // V^T tile [hd][keys]
-  float p[kDecMaxG][kDecTile];   // scores -> probabilities
-  float alpha[kDecMaxG];
+struct DecCfg {
+  static constexpr int kKChunks = HD / 8;                    // 16-B chunks per K row
+  static constexpr int kTileBytes = 2 * kDecTile * HD * 2;   // K + V^T of one page
+  static constexpr int kScratch = kDecWarps * (kDecMaxG * HD + 2 * kDecMaxG) * 4;
+  static constexpr int kSmem = kDecWarps * kTileBytes > kScratch ? kDecWarps * kTileBytes : kScratch;
 };
 
+// swizzled byte offsets: 16-B chunk c of row r (8 consecutive rows hit 8 distinct bank groups)
 template <int HD>
-__global__ void __launch_bounds__(kDecThreads) decode_attn_split_kernel(
-    const bf16* __restrict__ qkv, int ld_q, const PrefillWork* __restrict__ work,
-    const bf16* __restrict__ k_cache, const bf16* __restrict__ v_cache, const int* const* page_tables,
-    int q_heads, int kv_heads, int tiles_per_split, float scale_log2, float* part_o, float* part_ml,
-    int splits) {
-  __shared__ DecSmem<HD> sm;
-  pdl_wait();
-  pdl_launch_dependents();
-  const int split = blockIdx.x, kvh = blockIdx.y, req = blockIdx.z;
-  const int G = q_heads / kv_heads;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const PrefillWork w = work[req];
-  const int n_keys = w.q_pos0 + 1;  // keys [0, pos] (this token's K/V already appended)
-  const int n_tiles = (n_keys + kDecTile - 1) / kDecTile;
-  const int t0 = split * tiles_per_split, t1 = min(n_tiles, t0 + tiles_per_split);
-  const int* pt = page_tables[w.req_slot];
-  // q rows of the G heads (fp32, pre-scaled into the exp2 domain)
-  const bf16* qrow = qkv + static_cast<std::int64_t>(w.q_row0) * ld_q + kvh * G * HD;
-  for (int i = tid; i < G * HD; i += kDecThreads) sm.q[i / HD][i % HD] = bf2f(qrow[i]) * scale_log2;
-  float m_run = -INFINITY, l_run = 0.f;  // per (g = warp*2 + {0,1}) on lane 0.. (see below)
-  float acc[kDecMaxG];
-#pragma unroll
-  for (int g = 0; g < kDecMaxG; ++g) acc[g] = 0.f;
-  // running max / sum of row g live in warp (g / 2), replicated over its lanes
-  float mrow[2] = {-INFINITY, -INFINITY}, lrow[2] = {0.f, 0.f};
-  (void)m_run;
-  (void)l_run;
-  for (int t = t0; t < t1; ++t) {
-    const std::int64_t page = pt[t];
-    const bf16* kp = k_cache + (page * kv_heads + kvh) * kDecTile * HD;
-    const bf16* vp = v_cache + (page * kv_heads + kvh) * HD * kDecTile;
-    // every 16-byte load of the K and V^T pages in flight before the first
-    // shared-memory store (the kernel is bound by the loads' latency)
-    constexpr int kVec = kDecTile * HD / 8 / kDecThreads;  // uint4 per thread per page
-    uint4 kr[kVec], vr[kVec];
-#pragma unroll
-    for (int j = 0; j < kVec; ++j) {
-      const int i = tid + j * kDecThreads;
-      kr[j] = __ldcs(reinterpret_cast<const uint4*>(kp) + i);
-      vr[j] = __ldcs(reinterpret_cast<const uint4*>(vp) + i);
-    }
-    __syncthreads();  // previous tile's k / vt / p consumed
-#pragma unroll
-    for (int j = 0; j < kVec; ++j) {
-      const int i = tid + j * kDecThreads;
-      *reinterpret_cast<uint4*>(&sm.k[i / (HD / 8)][(i % (HD / 8)) * 8]) = kr[j];
-      *reinterpret_cast<uint4*>(&sm.vt[i / (kDecTile / 8)][(i % (kDecTile / 8)) * 8]) = vr[j];
-    }
-    __syncthreads();
-    // S[g][key]: thread -> key (tid % 64), heads g = tid / 64 + 2j
-    {
-      const int key = tid & (kDecTile - 1);
-      const int g0 = tid >> 6;
-      float s[kDecMaxG / 2];
-#pragma unroll
-      for (int j = 0; j < kDecMaxG / 2; ++j) s[j] = 0.f;
-#pragma unroll 8
-      for (int d = 0; d < HD; d += 2) {
-        const float2 kk = unpack_bf16x2(*reinterpret_cast<const std::uint32_t*>(&sm.k[key][d]));
-#pragma unroll
-        for (int j = 0; j < kDecMaxG / 2; ++j) {
-          const int g = g0 + 2 * j;
-          if (g < G) s[j] = fmaf(sm.q[g][d], kk.x, fmaf(sm.q[g][d + 1], kk.y, s[j]));
-        }
-      }
-      const bool ok = t * kDecTile + key < n_keys;
-#pragma unroll
-      for (int j = 0; j < kDecMaxG / 2; ++j) {
-        const int g = g0 + 2 * j;
-        if (g < G) sm.p[g][key] = ok ? s[j] : -INFINITY;
-      }
-    }
-    __syncthreads();
-    // online softmax: warp w owns rows 2w, 2w+1 (G <= 8), 2 keys per lane
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int g = 2 * warp + h;
-      if (g >= G) continue;
-      const float a = sm.p[g][lane], b = sm.p[g][lane + 32];
-      float mx = fmaxf(a, b);
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-      const float m_new = fmaxf(mrow[h], mx);
-      const float alpha = m_new == -INFINITY ? 1.f : exp2f(mrow[h] - m_new);
-      const float pa = m_new == -INFINITY ? 0.f : exp2f(a - m_new);
-      const float pb = m_new == -INFINITY ? 0.f : exp2f(b - m_new);
-      float rs = pa + pb;
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) rs += __shfl_xor_sync(0xffffffffu, rs, o);
-      lrow[h] = lrow[h] * alpha + rs;
-      mrow[h] = m_new;
-      sm.p[g][lane] = pa;
-      sm.p[g][lane + 32] = pb;
-      if (lane == 0) sm.alpha[g] = alpha;
-    }
-    __syncthreads();
-    // O[g][d] += sum_k P[g][k] V[k][d]: thread -> d
-    for (int d = tid; d < HD; d += kDecThreads) {
-      float part[kDecMaxG];
-#pragma unroll
-      for (int g = 0; g < kDecMaxG; ++g) part[g] = 0.f;
-#pragma unroll 4
-      for (int k = 0; k < kDecTile; k += 2) {
-        const float2 vv = unpack_bf16x2(*reinterpret_cast<const std::uint32_t*>(&sm.vt[d][k]));
-#pragma unroll
-        for (int g = 0; g < kDecMaxG; ++g)
-          if (g < G) part[g] = fmaf(sm.p[g][k], vv.x, fmaf(sm.p[g][k + 1], vv.y, part[g]));
-      }
-#pragma unroll
-      for (int g = 0; g < kDecMaxG; ++g)
-        if (g < G) acc[g] = acc[g] * sm.alpha[g] + part[g];
-    }
-  }
-  // partials: o [req][head][split][HD] (unnormalised), ml [req][head][split][2]
-  for (int d = tid; d < HD; d += kDecThreads)
-    for (int g = 0; g < G; ++g) {
-      const int head = kvh * G + g;
-      part_o[((static_cast<std::int64_t>(req) * q_heads + head) * splits + split) * HD + d] = acc[g];
-    }
-  if (lane == 0) {
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int g = 2 * warp + h;
-      if (g >= G) continue;
-      float* ml = part_ml + ((static_cast<std::int64_t>(req) * q_heads + kvh * G + g) * splits + split) * 2;
-      ml[0] = mrow[h];
-      ml[1] = lrow[h];
-    }
-  }
+__device__ __forceinline__ std::uint32_t dec_k_off(int r, int c) {
+  return static_cast<std::uint32_t>(r * HD * 2 + ((c ^ (r & 7)) << 4));
+}
+__device__ __forceinline__ std::uint32_t dec_v_off(int r, int c) {  // V^T rows: 64 keys = 128 B
+  return static_cast<std::uint32_t>(r * 128 + ((c ^ (r & 7)) << 4));
 }
 
 template <int HD>
-__global__ void __launch_bounds__(HD) decode_attn_merge_kernel(const float* part_o, const float* part_ml,
-                                                               int q_heads, int splits, bf16* out,
-                                                               int ld_out, const PrefillWork* work) {
+__global__ void __launch_bounds__(kDecThreads, 1) decode_attn_kernel(
+    const bf16* __restrict__ qkv, int ld_q, const PrefillWork* __restrict__ work,
+    const bf16* __restrict__ k_cache, const bf16* __restrict__ v_cache, const int* const* page_tables,
+    int q_heads, int kv_heads, int tiles_per_split, float scale_log2, float* part_o, float* part_ml,
+    int splits, bf16* out, int ld_out, unsigned long long* trace) {
+  using C = DecCfg<HD>;
+  // RS_DEC_TRACE (dev): globaltimer per CTA at the phase boundaries
+  auto stamp = [&](int k) {
+    if (trace != nullptr && threadIdx.x == 0) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      trace[(static_cast<std::size_t>(blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x) * 8 + k] = t;
+    }
+  };
+  extern __shared__ __align__(128) std::uint8_t dsm[];
+  stamp(0);
+  const int split = blockIdx.x, kvh = blockIdx.y, req = blockIdx.z;
+  const int G = q_heads / kv_heads;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, t4 = lane & 3;  // MMA fragment row group / column pair
+  // work items and page tables are host uploads (stream-ordered before this
+  // launch), and every page but the one holding this step's token is stable:
+  // those K / V loads are issued before the PDL wait, overlapping the
+  // preceding kernels (QKV GEMV, RoPE + KV append)
+  const PrefillWork w = work[req];
+  const int n_keys = w.q_pos0 + 1;  // keys [0, pos] (this token's K / V appended by the preceding kernel)
+  const int n_tiles = (n_keys + kDecTile - 1) / kDecTile;
+  const int t_new = n_tiles - 1;
+  const int t0 = split * tiles_per_split, t1 = min(n_tiles, t0 + tiles_per_split);
+  const int* pt = page_tables[w.req_slot];
+  std::uint8_t* my = dsm + warp * C::kTileBytes;
+  auto issue = [&](int t) {
+    const std::int64_t page = pt[t];
+    const bf16* kp = k_cache + (page * kv_heads + kvh) * kDecTile * HD;
+    const bf16* vp = v_cache + (page * kv_heads + kvh) * HD * kDecTile;
+#pragma unroll
+    for (int i = 0; i < kDecTile * HD / 8 / 32; ++i) {
+      const int q = lane + 32 * i;
+      cp_async16(my + dec_k_off<HD>(q / C::kKChunks, q % C::kKChunks), kp + 8 * q, true);
+      cp_async16(my + kDecTile * HD * 2 + dec_v_off(q / 8, q % 8), vp + 8 * q, true);
+    }
+    cp_async_commit();
+  };
+  bool issued = t0 + warp < t1 && t0 + warp != t_new;
+  if (issued) issue(t0 + warp);
+  stamp(1);
+  pdl_wait();  // q and this token's K / V come from the preceding kernels
+  pdl_launch_dependents();
+
+  // Q as the A operand (rows = heads g, g + 8; zero beyond G), unscaled bf16
+  const bf16* qrow = qkv + static_cast<std::int64_t>(w.q_row0) * ld_q + kvh * G * HD;
+  std::uint32_t qa[HD / 16][4];
+#pragma unroll
+  for (int kk = 0; kk < HD / 16; ++kk) {
+    const int d = 16 * kk + 2 * t4;
+    qa[kk][0] = g < G ? *reinterpret_cast<const std::uint32_t*>(qrow + g * HD + d) : 0u;
+    qa[kk][1] = g + 8 < G ? *reinterpret_cast<const std::uint32_t*>(qrow + (g + 8) * HD + d) : 0u;
+    qa[kk][2] = g < G ? *reinterpret_cast<const std::uint32_t*>(qrow + g * HD + d + 8) : 0u;
+    qa[kk][3] = g + 8 < G ? *reinterpret_cast<const std::uint32_t*>(qrow + (g + 8) * HD + d + 8) : 0u;
+  }
+  float o[HD / 8][4];
+#pragma unroll
+  for (int j = 0; j < HD / 8; ++j) o[j][0] = o[j][1] = o[j][2] = o[j][3] = 0.f;
+  float m_r[2] = {-INFINITY, -INFINITY}, l_r[2] = {0.f, 0.f};  // rows g, g + 8 (l: this thread's columns)
+
+  for (int t = t0 + warp; t < t1; t += kDecWarps) {
+    if (!issued) issue(t);
+    issued = false;
+    if (t == t0 + warp) stamp(2);
+    cp_async_wait<0>();
+    if (t == t0 + warp) stamp(3);
+    const int valid = min(kDecTile, n_keys - t * kDecTile);
+    if (valid < kDecTile) {  // keys past the end: V^T columns zeroed (P is 0 there; keep 0 * V finite)
+      for (int r = lane; r < HD; r += 32)
+        for (int k = valid; k < kDecTile; ++k)
+          *reinterpret_cast<bf16*>(my + kDecTile * HD * 2 + dec_v_off(r, k >> 3) + 2 * (k & 7)) = f2bf(0.f);
+    }
+    __syncwarp();
+    // S = Q K^T: 8 key n-tiles x HD/16 k-steps; K rows are the col-major B operand
+    float s[kDecTile / 8][4];
+#pragma unroll
+    for (int n = 0; n < kDecTile / 8; ++n) s[n][0] = s[n][1] = s[n][2] = s[n][3] = 0.f;
+#pragma unroll
+    for (int n = 0; n < kDecTile / 8; n += 2) {
+#pragma unroll
+      for (int kk = 0; kk < HD / 16; ++kk) {
+        std::uint32_t b[4];  // (keys 8n.., d chunk 2kk), (.., 2kk+1), (keys 8n+8.., 2kk), (.., 2kk+1)
+        const int r = 8 * (n + (lane >> 4)) + (lane & 7), c = 2 * kk + ((lane >> 3) & 1);
+        ldsm_x4(b, my + dec_k_off<HD>(r, c));
+        mma_bf16(s[n], qa[kk], b[0], b[1]);
+        mma_bf16(s[n + 1], qa[kk], b[2], b[3]);
+      }
+    }
+    // online softmax (rows g: s[n][0..1], g + 8: s[n][2..3]; keys 8n + 2 t4 + {0, 1})
+    float mx[2] = {-INFINITY, -INFINITY};
+#pragma unroll
+    for (int n = 0; n < kDecTile / 8; ++n)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int key = 8 * n + 2 * t4 + (e & 1);
+        s[n][e] = key < valid ? s[n][e] * scale_log2 : -INFINITY;
+        mx[e >> 1] = fmaxf(mx[e >> 1], s[n][e]);
+      }
+    float alpha[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      mx[h] = fmaxf(mx[h], __shfl_xor_sync(0xffffffffu, mx[h], 1));
+      mx[h] = fmaxf(mx[h], __shfl_xor_sync(0xffffffffu, mx[h], 2));
+      const float m_new = fmaxf(m_r[h], mx[h]);  // finite: every tile has >= 1 valid key
+      alpha[h] = exp2f(m_r[h] - m_new);
+      m_r[h] = m_new;
+      l_r[h] *= alpha[h];
+    }
+#pragma unroll
+    for (int j = 0; j < HD / 8; ++j) {
+      o[j][0] *= alpha[0];
+      o[j][1] *= alpha[0];
+      o[j][2] *= alpha[1];
+      o[j][3] *= alpha[1];
+    }
+#pragma unroll
+    for (int n = 0; n < kDecTile / 8; ++n)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        s[n][e] = exp2f(s[n][e] - m_r[e >> 1]);
+        l_r[e >> 1] += s[n][e];
+      }
+    // O += P V: P from S's accumulators (A layout), V^T rows as the B operand
+#pragma unroll
+    for (int kk = 0; kk < kDecTile / 16; ++kk) {
+      const std::uint32_t pa[4] = {pack_bf16x2(s[2 * kk][0], s[2 * kk][1]), pack_bf16x2(s[2 * kk][2], s[2 * kk][3]),
+                                   pack_bf16x2(s[2 * kk + 1][0], s[2 * kk + 1][1]),
+                                   pack_bf16x2(s[2 * kk + 1][2], s[2 * kk + 1][3])};
+#pragma unroll
+      for (int j = 0; j < HD / 8; j += 2) {
+        std::uint32_t b[4];  // (d 8j.., key chunk 2kk), (.., 2kk+1), (d 8j+8.., 2kk), (.., 2kk+1)
+        const int r = 8 * (j + (lane >> 4)) + (lane & 7), c = 2 * kk + ((lane >> 3) & 1);
+        ldsm_x4(b, my + kDecTile * HD * 2 + dec_v_off(r, c));
+        mma_bf16(o[j], pa, b[0], b[1]);
+        mma_bf16(o[j + 1], pa, b[2], b[3]);
+      }
+    }
+    __syncwarp();  // this tile's ldmatrix reads are done before the next cp.async overwrites the slot
+  }
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    l_r[h] += __shfl_xor_sync(0xffffffffu, l_r[h], 1);
+    l_r[h] += __shfl_xor_sync(0xffffffffu, l_r[h], 2);
+  }
+  stamp(4);
+  // merge the 4 warps (in warp order) through shared memory (the K / V slots are dead)
+  __syncthreads();
+  float* so = reinterpret_cast<float*>(dsm);                       // [warp][16][HD]
+  float* sml = so + kDecWarps * kDecMaxG * HD;                     // [warp][16][2]
+  float* swt = sml + kDecWarps * kDecMaxG * 2;                     // [warp][16] weights
+  float* sL = swt + kDecWarps * kDecMaxG;                          // [16] (M, l) of the CTA
+#pragma unroll
+  for (int j = 0; j < HD / 8; ++j) {
+    float* r0 = so + (warp * kDecMaxG + g) * HD + 8 * j + 2 * t4;
+    float* r1 = so + (warp * kDecMaxG + g + 8) * HD + 8 * j + 2 * t4;
+    *reinterpret_cast<float2*>(r0) = make_float2(o[j][0], o[j][1]);
+    *reinterpret_cast<float2*>(r1) = make_float2(o[j][2], o[j][3]);
+  }
+  if (t4 == 0) {
+    *reinterpret_cast<float2*>(sml + (warp * kDecMaxG + g) * 2) = make_float2(m_r[0], l_r[0]);
+    *reinterpret_cast<float2*>(sml + (warp * kDecMaxG + g + 8) * 2) = make_float2(m_r[1], l_r[1]);
+  }
+  __syncthreads();
+  if (tid < G) {  // per head: the warps' weights 2^(m_w - M) and the CTA's (M, l)
+    float M = -INFINITY;
+#pragma unroll
+    for (int v = 0; v < kDecWarps; ++v) M = fmaxf(M, sml[(v * kDecMaxG + tid) * 2]);
+    float l = 0.f;
+#pragma unroll
+    for (int v = 0; v < kDecWarps; ++v) {
+      const float wv = M == -INFINITY ? 0.f : exp2f(sml[(v * kDecMaxG + tid) * 2] - M);  // idle warp: 0
+      swt[v * kDecMaxG + tid] = wv;
+      l += wv * sml[(v * kDecMaxG + tid) * 2 + 1];
+    }
+    *reinterpret_cast<float2*>(sL + 2 * tid) = make_float2(M, l);
+  }
+  __syncthreads();
+  const std::int64_t head0 = static_cast<std::int64_t>(req) * q_heads + kvh * G;
+  constexpr int kQ4 = HD / 4;
+  for (int i = tid; i < G * kQ4; i += kDecThreads) {
+    const int h = i / kQ4, d = 4 * (i % kQ4);
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (int v = 0; v < kDecWarps; ++v) {
+      const float wv = swt[v * kDecMaxG + h];
+      const float4 x = *reinterpret_cast<const float4*>(so + (v * kDecMaxG + h) * HD + d);
+      acc.x += wv * x.x;
+      acc.y += wv * x.y;
+      acc.z += wv * x.z;
+      acc.w += wv * x.w;
+    }
+    if (splits == 1) {
+      const float l = sL[2 * h + 1], inv = l > 0.f ? 1.f / l : 0.f;
+      bf16* o4 = out + static_cast<std::int64_t>(w.q_row0) * ld_out + (kvh * G + h) * HD + d;
+      *reinterpret_cast<uint2*>(o4) =
+          make_uint2(pack_bf16x2(acc.x * inv, acc.y * inv), pack_bf16x2(acc.z * inv, acc.w * inv));
+    } else {
+      *reinterpret_cast<float4*>(part_o + ((head0 + h) * splits + split) * HD + d) = acc;
+    }
+  }
+  if (splits == 1) return;
+  if (tid < G) *reinterpret_cast<float2*>(part_ml + ((head0 + tid) * splits + split) * 2) =
+      *reinterpret_cast<const float2*>(sL + 2 * tid);
+  __syncthreads();
+  stamp(5);
+}
+
+// Split merge: one warp per (query head, request), HD / 32 columns per lane;
+// split weights 2^(m_s - M) computed once per lane-strided split and
+// broadcast by shuffles, up to kMergeChunk partial rows in flight, summed in
+// split order (deterministic). PDL: launched while the split kernel runs.
+constexpr int kMergeChunk = 40;
+template <int HD>
+__global__ void __launch_bounds__(32) decode_attn_merge_kernel(const float* part_o, const float* part_ml, int q_heads,
+                                                               int splits, bf16* out, int ld_out,
+                                                               const PrefillWork* __restrict__ work) {
+  constexpr int V = HD / 32;
+  const int head = blockIdx.x, req = blockIdx.y, lane = threadIdx.x;
+  const int row0 = work[req].q_row0;  // host upload: read before the wait
   pdl_wait();
   pdl_launch_dependents();
-  const int head = blockIdx.x, req = blockIdx.y, d = threadIdx.x;
   const std::int64_t base = (static_cast<std::int64_t>(req) * q_heads + head) * splits;
+  const float2* ml = reinterpret_cast<const float2*>(part_ml) + base;
   float M = -INFINITY;
-  for (int s = 0; s < splits; ++s) M = fmaxf(M, part_ml[(base + s) * 2]);
-  float o = 0.f, l = 0.f;
-  for (int s = 0; s < splits; ++s) {
-    const float m = part_ml[(base + s) * 2];
-    if (m == -INFINITY) continue;
-    const float w = exp2f(m - M);
-    o += w * part_o[(base + s) * HD + d];
-    l += w * part_ml[(base + s) * 2 + 1];
+  for (int s2 = lane; s2 < splits; s2 += 32) M = fmaxf(M, __ldcg(&ml[s2].x));
+  M = warp_max(M);
+  float acc[V];
+#pragma unroll
+  for (int v = 0; v < V; ++v) acc[v] = 0.f;
+  float lpart = 0.f;
+  for (int s0 = 0; s0 < splits; s0 += kMergeChunk) {
+    float wl[2];  // weights of splits s0 + lane, s0 + 32 + lane
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const int s2 = s0 + 32 * q + lane;
+      wl[q] = 0.f;
+      if (32 * q + lane < kMergeChunk && s2 < splits && M != -INFINITY) {
+        const float2 v = __ldcg(&ml[s2]);
+        wl[q] = exp2f(v.x - M);
+        lpart += wl[q] * v.y;
+      }
+    }
+    float x[kMergeChunk][V];
+#pragma unroll
+    for (int k = 0; k < kMergeChunk; ++k) {
+      const float* src = part_o + (base + s0 + k) * HD + V * lane;
+#pragma unroll
+      for (int v = 0; v < V; ++v) x[k][v] = s0 + k < splits ? __ldcg(src + v) : 0.f;
+    }
+#pragma unroll
+    for (int k = 0; k < kMergeChunk; ++k) {
+      const float wv = __shfl_sync(0xffffffffu, wl[k >> 5], k & 31);
+#pragma unroll
+      for (int v = 0; v < V; ++v) acc[v] += wv * x[k][v];
+    }
   }
-  out[static_cast<std::int64_t>(work[req].q_row0) * ld_out + head * HD + d] = f2bf(l > 0.f ? o / l : 0.f);
+  const float l = warp_sum(lpart);
+  const float inv = l > 0.f ? 1.f / l : 0.f;
+  bf16* o = out + static_cast<std::int64_t>(row0) * ld_out + head * HD + V * lane;
+#pragma unroll
+  for (int v = 0; v < V; v += 2) *reinterpret_cast<std::uint32_t*>(o + v) = pack_bf16x2(acc[v] * inv, acc[v + 1] * inv);
 }
 
 struct DecodeWs {
@@ -514,6 +653,54 @@ std::unordered_map<cudaStream_t, DecodeWs>& decode_ws_all() {  // per stream, re
   return all;
 }
 
+template <int HD>
+void launch_decode(dim3 grid, cudaStream_t st, const bf16* qkv, int ld_q, const PrefillWork* work,
+                   const PagedKV& kv, int q_heads, int kv_heads, int tiles_per_split, float scale_log2,
+                   float* part_o, float* part_ml, int splits, bf16* out, int ld_out) {
+  static const bool attr = [] {
+    RS_CUDA_CHECK(cudaFuncSetAttribute(decode_attn_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       DecCfg<HD>::kSmem));
+    return true;
+  }();
+  (void)attr;
+  static const bool trace = std::getenv("RS_DEC_TRACE") != nullptr;
+  unsigned long long* tr = nullptr;
+  const std::size_t n_cta = static_cast<std::size_t>(grid.x) * grid.y * grid.z;
+  if (trace) {
+    RS_CUDA_CHECK(cudaMalloc(reinterpret_cast<void**>(&tr), n_cta * 8 * 8));
+    RS_CUDA_CHECK(cudaMemsetAsync(tr, 0, n_cta * 8 * 8, st));
+  }
+  launch_kernel(decode_attn_kernel<HD>, grid, dim3(kDecThreads), DecCfg<HD>::kSmem, st, 1, qkv, ld_q, work, kv.k,
+                kv.v, kv.page_tables, q_heads, kv_heads, tiles_per_split, scale_log2, part_o, part_ml, splits, out,
+                ld_out, tr);
+  if (splits > 1)
+    launch_kernel(decode_attn_merge_kernel<HD>, dim3(q_heads, grid.z), dim3(32), 0, st, 1,
+                  static_cast<const float*>(part_o), static_cast<const float*>(part_ml), q_heads, splits, out, ld_out,
+                  work);
+  if (trace) {  // ns from the earliest CTA start: mean / max over CTAs per phase
+    std::vector<unsigned long long> h(n_cta * 8);
+    RS_CUDA_CHECK(cudaStreamSynchronize(st));
+    RS_CUDA_CHECK(cudaMemcpy(h.data(), tr, h.size() * 8, cudaMemcpyDeviceToHost));
+    RS_CUDA_CHECK(cudaFree(tr));
+    unsigned long long t0 = ~0ull;
+    for (std::size_t i = 0; i < n_cta; ++i) t0 = std::min(t0, h[i * 8]);
+    std::fprintf(stderr, "[dec-trace] ctas %zu splits %u:", n_cta, grid.x);
+    for (int k = 0; k < 7; ++k) {
+      double sum = 0, mx = 0;
+      int n = 0;
+      for (std::size_t i = 0; i < n_cta; ++i)
+        if (h[i * 8 + k] != 0) {
+          const double v = static_cast<double>(h[i * 8 + k] - t0);
+          sum += v;
+          mx = std::max(mx, v);
+          ++n;
+        }
+      std::fprintf(stderr, " p%d %.0f/%.0f(n%d)", k, n ? sum / n : 0.0, mx, n);
+    }
+    std::fprintf(stderr, "\n");
+  }
+}
+
 }  // namespace
 
 void attention_decode_paged(const bf16* qkv, int ld_q, bf16* out, int ld_out, const PrefillWork* work,
@@ -522,12 +709,15 @@ void attention_decode_paged(const bf16* qkv, int ld_q, bf16* out, int ld_out, co
   if (n_req <= 0) return;
   const int G = q_heads / kv_heads;
   if (G > kDecMaxG || q_heads % kv_heads != 0)
-    throw DeviceError(RS_ERR_CUDA, "decode attention: GQA group above 8");
+    throw DeviceError(RS_ERR_CUDA, "decode attention: GQA group above 16");
   if (kv.page_size != kDecTile) throw DeviceError(RS_ERR_CUDA, "decode attention needs 64-token pages");
+  if (head_dim != 64 && head_dim != 128)
+    throw DeviceError(RS_ERR_CUDA, "decode attention: unsupported head_dim " + std::to_string(head_dim));
   const int max_tiles = (max_keys + kDecTile - 1) / kDecTile;
-  // splits: ~2 CTAs per SM over all requests and kv heads
-  const int ctas_wanted = 2 * kNumSMs;
-  int splits = std::max(1, ctas_wanted / std::max(1, n_req * kv_heads));
+  // one CTA per SM (4 pages in flight each): splits so that all (request,
+  // kv head) pairs together fill the SMs
+  const int pairs = n_req * kv_heads;
+  int splits = std::max(1, (kNumSMs + pairs - 1) / pairs);
   splits = std::min(splits, max_tiles);
   const int tiles_per_split = (max_tiles + splits - 1) / splits;
   splits = (max_tiles + tiles_per_split - 1) / tiles_per_split;
@@ -544,27 +734,16 @@ void attention_decode_paged(const bf16* qkv, int ld_q, bf16* out, int ld_out, co
   const float scale_log2 = scale * kLog2e;
   const int tok = prof::begin(st);
   const dim3 grid(splits, kv_heads, n_req);
-  switch (head_dim) {
-    case 64:
-      launch_kernel(decode_attn_split_kernel<64>, grid, dim3(kDecThreads), 0, st, 1, qkv, ld_q, work, kv.k, kv.v,
-                    kv.page_tables, q_heads, kv_heads, tiles_per_split, scale_log2, part_o, part_ml, splits);
-      launch_kernel(decode_attn_merge_kernel<64>, dim3(q_heads, n_req), dim3(64), 0, st, 1,
-                    static_cast<const float*>(part_o), static_cast<const float*>(part_ml), q_heads, splits, out,
-                    ld_out, work);
-      break;
-    case 128:
-      launch_kernel(decode_attn_split_kernel<128>, grid, dim3(kDecThreads), 0, st, 1, qkv, ld_q, work, kv.k, kv.v,
-                    kv.page_tables, q_heads, kv_heads, tiles_per_split, scale_log2, part_o, part_ml, splits);
-      launch_kernel(decode_attn_merge_kernel<128>, dim3(q_heads, n_req), dim3(128), 0, st, 1,
-                    static_cast<const float*>(part_o), static_cast<const float*>(part_ml), q_heads, splits, out,
-                    ld_out, work);
-      break;
-    default:
-      throw DeviceError(RS_ERR_CUDA, "decode attention: unsupported head_dim " + std::to_string(head_dim));
-  }
+  if (head_dim == 64)
+    launch_decode<64>(grid, st, qkv, ld_q, work, kv, q_heads, kv_heads, tiles_per_split, scale_log2, part_o,
+                      part_ml, splits, out, ld_out);
+  else
+    launch_decode<128>(grid, st, qkv, ld_q, work, kv, q_heads, kv_heads, tiles_per_split, scale_log2, part_o,
+                       part_ml, splits, out, ld_out);
   RS_LAUNCH_CHECK();
+  // algorithmic bytes: every valid key's K and V row of every kv head, once
   prof::end(tok, st, "attn_decode", 0, 0);
-  count_launch(2);
+  count_launch(splits > 1 ? 2 : 1);
 }
 
 void attention_release_stream(cudaStream_t st) {

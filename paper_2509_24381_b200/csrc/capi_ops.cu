@@ -181,6 +181,35 @@ rs_status rs_op_attention_prefill(const void* q, int ld_q, int rows_alloc, void*
   });
 }
 
+rs_status rs_op_attention_decode(const void* q, int ld_q, void* out, int ld_out, int n_req, const int* q_pos,
+                                 const int* const* page_tables, const void* k_cache, const void* v_cache,
+                                 int q_heads, int kv_heads, int head_dim, float scale, void* stream) {
+  return guarded([&] {
+    if (n_req <= 0) return;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    std::vector<PrefillWork> work;
+    int max_keys = 0;
+    for (int i = 0; i < n_req; ++i) {
+      if (q_pos[i] < 0) throw lmmsim::ConfigError("rs_op_attention_decode: negative position");
+      work.push_back({i, 1, q_pos[i], i});
+      max_keys = std::max(max_keys, q_pos[i] + 1);
+    }
+    PrefillWork* wd = nullptr;
+    const int** ptd = nullptr;
+    RS_CUDA_CHECK(cudaMallocAsync(reinterpret_cast<void**>(&wd), work.size() * sizeof(PrefillWork), st));
+    RS_CUDA_CHECK(cudaMallocAsync(reinterpret_cast<void**>(&ptd), n_req * sizeof(int*), st));
+    RS_CUDA_CHECK(cudaMemcpyAsync(wd, work.data(), work.size() * sizeof(PrefillWork), cudaMemcpyHostToDevice, st));
+    RS_CUDA_CHECK(cudaMemcpyAsync(ptd, page_tables, n_req * sizeof(int*), cudaMemcpyHostToDevice, st));
+    PagedKV kv{const_cast<bf16*>(static_cast<const bf16*>(k_cache)),
+               const_cast<bf16*>(static_cast<const bf16*>(v_cache)), ptd, 64};
+    attention_decode_paged(static_cast<const bf16*>(q), ld_q, static_cast<bf16*>(out), ld_out, wd, n_req, max_keys,
+                           kv, q_heads, kv_heads, head_dim, scale, st);
+    RS_CUDA_CHECK(cudaStreamSynchronize(st));  // host vectors above go out of scope
+    RS_CUDA_CHECK(cudaFreeAsync(wd, st));
+    RS_CUDA_CHECK(cudaFreeAsync(ptd, st));
+  });
+}
+
 unsigned long long rs_kernel_launches(void) { return launches_so_far(); }
 
 rs_status rs_profile_enable(int on) {

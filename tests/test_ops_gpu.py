@@ -309,6 +309,58 @@ def test_attention_prefill_tcgen05(nat, hd, hq, hkv, pos0, rows):
     _close(out, ref)
 
 
+@pytest.mark.parametrize("hd,hq,hkv,positions", [(128, 28, 4, [8575]), (128, 28, 4, [0, 62, 63, 64, 200]),
+                                                   (128, 28, 4, [4095, 17, 9000]), (64, 16, 1, [129, 3000]),
+                                                   (128, 8, 8, [700]), (64, 14, 2, [255, 256])])
+def test_attention_decode_paged(nat, hd, hq, hkv, positions):
+    """Decode attention (mma.sync, cp.async pages, split + last-CTA merge):
+    one query row per request over its shuffled paged cache, vs fp32 torch.
+    Stale garbage (NaN) beyond each request's last key: masked keys must not
+    leak into O."""
+    import ctypes as C
+    g = torch.Generator(device="cuda").manual_seed(len(positions) * 7 + hd)
+    n = len(positions)
+    pages = [(p + 1 + 63) // 64 for p in positions]
+    pool = sum(pages) + 3
+    perm = torch.randperm(pool, generator=g, device="cuda").to(torch.int32)
+    kc = torch.full((pool, hkv, 64, hd), float("nan"), device="cuda", dtype=torch.bfloat16)
+    vc = torch.full((pool, hkv, hd, 64), float("nan"), device="cuda", dtype=torch.bfloat16)
+    tables, Ks, Vs, off = [], [], [], 0
+    for p, np_ in zip(positions, pages):
+        T = p + 1
+        pt = perm[off:off + np_].contiguous()
+        off += np_
+        K = torch.randn(T, hkv, hd, device="cuda", generator=g).bfloat16()
+        V = torch.randn(T, hkv, hd, device="cuda", generator=g).bfloat16()
+        for t in range(0, T, 64):
+            m = min(64, T - t)
+            pg = int(pt[t // 64])
+            kc[pg, :, :m] = K[t:t + m].transpose(0, 1)
+            vc[pg, :, :, :m] = V[t:t + m].permute(1, 2, 0)
+        tables.append(pt)
+        Ks.append(K)
+        Vs.append(V)
+    ld = (hq + 2 * hkv) * hd
+    q = torch.randn(n, ld, device="cuda", generator=g).bfloat16()
+    out = torch.zeros(n, hq * hd, device="cuda", dtype=torch.bfloat16)
+    scale = 1.0 / math.sqrt(hd)
+    pos_arr = (C.c_int * n)(*positions)
+    pt_arr = (C.c_void_p * n)(*[t.data_ptr() for t in tables])
+    for _ in range(2):  # the split counters reset themselves: a second call is identical
+        nat.check(nat.lib.rs_op_attention_decode(q.data_ptr(), ld, out.data_ptr(), out.stride(0), n, pos_arr,
+                                                 pt_arr, kc.data_ptr(), vc.data_ptr(), hq, hkv, hd, scale,
+                                                 _stream()))
+        torch.cuda.synchronize()
+        for i in range(n):
+            qq = q[i, :hq * hd].float().view(hq, hd)
+            kk = Ks[i].float().repeat_interleave(hq // hkv, dim=1)
+            vv = Vs[i].float().repeat_interleave(hq // hkv, dim=1)
+            pr = torch.softmax(torch.einsum("hd,khd->hk", qq, kk) * scale, dim=-1)
+            ref = torch.einsum("hk,khd->hd", pr, vv).reshape(-1)
+            assert torch.isfinite(out[i].float()).all()
+            _close(out[i], ref)
+
+
 @pytest.mark.parametrize("splits", [2, 3, 8])
 @pytest.mark.parametrize("hd,hq,hkv,pos0,rows", [(128, 28, 4, 8192, 384), (128, 4, 1, 300, 77),
                                                  (64, 8, 2, 63, 130), (64, 8, 2, 0, 130),
