@@ -684,6 +684,22 @@ __global__ void __launch_bounds__(kPpThreads, 1)
   sm100::tc_fence_after();
   const std::uint32_t tmem = *tmem_holder;
   pdl_wait();  // setup overlapped the previous kernel's tail
+#ifdef RS_PP_TRACE_BUILD  // per-CTA span + work (dev): [start, end, units, tile products]
+  unsigned long long* cta_tr = p.trace != nullptr ? p.trace + 4 * kPpTraceIters * kPpTraceEv + 4 * blockIdx.x : nullptr;
+  if (cta_tr != nullptr && threadIdx.x == 0) {
+    cta_tr[0] = pp_gtimer();
+    unsigned long long nu = 0, np = 0;
+    for (int r = 0;; ++r) {
+      const int u = pp_unit_index(r, n_units);
+      if (u < 0) break;
+      const PpUnit x = pp_unit<MODE>(p, u);
+      ++nu;
+      np += max(0, x.e_t[0] - x.jb) + max(0, x.e_t[1] - x.jb);
+    }
+    cta_tr[2] = nu;
+    cta_tr[3] = np;
+  }
+#endif
 
   auto pages = [&](const PpUnit& x, int j, int& pa, int& pb) {
     const int n_real_pages = (x.key_end - x.key_begin + 63) / 64;
@@ -1056,6 +1072,9 @@ __global__ void __launch_bounds__(kPpThreads, 1)
     if (kOrder != 0 && t == 0) sm100::named_bar_sync(kTurnBar0, 256);  // tile 1's last hand-back
   }
   __syncthreads();
+#ifdef RS_PP_TRACE_BUILD
+  if (cta_tr != nullptr && threadIdx.x == 0) cta_tr[1] = pp_gtimer();
+#endif
   if (warp == 1) {
     sm100::tc_fence_after();
     sm100::tmem_dealloc(tmem, 512);
@@ -1207,7 +1226,7 @@ void launch(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
     const int units = p.q_heads * p.n_pieces;
     static const bool trace = std::getenv("RS_PP_TRACE") != nullptr;
     TcParams q = p;
-    const std::size_t tn = 4 * kPpTraceIters * kPpTraceEv;
+    const std::size_t tn = 4 * kPpTraceIters * kPpTraceEv + 4 * kNumSMs;
     if (trace) {
       RS_CUDA_CHECK(cudaMallocAsync(reinterpret_cast<void**>(&q.trace), tn * 8, st));
       RS_CUDA_CHECK(cudaMemsetAsync(q.trace, 0, tn * 8, st));
@@ -1220,7 +1239,23 @@ void launch(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
       RS_CUDA_CHECK(cudaStreamSynchronize(st));
       RS_CUDA_CHECK(cudaFree(q.trace));
       unsigned long long t0 = ~0ull;
-      for (unsigned long long v : h) if (v) t0 = std::min(t0, v);
+      for (std::size_t i = 0; i < 4 * kPpTraceIters * kPpTraceEv; ++i) if (h[i]) t0 = std::min(t0, h[i]);
+      {  // per-CTA spans (dev build): start / end spread, work per CTA
+        const unsigned long long* c = h.data() + 4 * kPpTraceIters * kPpTraceEv;
+        const int G = std::min(units, kNumSMs);
+        unsigned long long s0 = ~0ull, s1 = 0, e0 = ~0ull, e1 = 0, p0 = ~0ull, p1 = 0, u1 = 0;
+        double ps = 0;
+        for (int i = 0; i < G; ++i) {
+          if (c[4 * i] == 0) continue;
+          s0 = std::min(s0, c[4 * i]); s1 = std::max(s1, c[4 * i]);
+          e0 = std::min(e0, c[4 * i + 1]); e1 = std::max(e1, c[4 * i + 1]);
+          p0 = std::min(p0, c[4 * i + 3]); p1 = std::max(p1, c[4 * i + 3]); u1 = std::max(u1, c[4 * i + 2]);
+          ps += static_cast<double>(c[4 * i + 3]);
+        }
+        std::fprintf(stderr, "[pp-cta] ctas %d units %d: start spread %llu ns, end first %llu last %llu ns; "
+                     "products/CTA min %llu mean %.1f max %llu; max units/CTA %llu\n", G, units, s1 - s0, e0 - s0,
+                     e1 - s0, p0, ps / G, p1, u1);
+      }
       auto at = [&](int role, int it, int ev) {
         const unsigned long long v = h[(static_cast<std::size_t>(role) * kPpTraceIters + it) * kPpTraceEv + ev];
         return v ? static_cast<long long>(v - t0) : -1ll;
