@@ -1119,7 +1119,7 @@ void gemm(const GemmArgs& a, Epi epi, cudaStream_t stream, int force_bn) {
                                        std::to_string(a.K) + ", N=" + std::to_string(a.N) + ")");
   if (epi == Epi::SwiGLU && a.N % 32 != 0)
     throw DeviceError(RS_ERR_CUDA, "gemm: SwiGLU needs N%32==0");
-  if (force_bn == 0 && a.M <= 8 && epi != Epi::QkvRope) {  // decode-sized: weight streaming on the CUDA cores
+  if (force_bn == 0 && a.M <= 8) {  // decode-sized: weight streaming on the CUDA cores
     const int tok = prof::begin(stream);
     if (gemv_small_m(a, epi, stream)) {
       prof::end(tok, stream, "gemv_small_m", 2.0 * a.M * a.N * a.K, 2.0 * a.N * a.K);

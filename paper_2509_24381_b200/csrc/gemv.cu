@@ -8,10 +8,13 @@
 // 16-byte loads (A rows come through L1); warp partials are summed in warp
 // order (deterministic) and the CTA applies the same fused epilogues as the
 // tcgen05 GEMM (bias, residual + folded-norm sums of squares, SwiGLU, GELU,
-// fp32 row-mapped logits, folded-norm row scale).
+// fp32 row-mapped logits, folded-norm row scale, and the QKV projection's
+// M-RoPE + paged K / V append: a block of q / k columns holds two
+// rotate-half pairs (i, i + hd/2), (i + 1, i + 1 + hd/2) of one head).
 #include <cuda_runtime.h>
 
 #include "gemm.cuh"
+#include "kernels.cuh"
 
 namespace rserve {
 namespace {
@@ -35,10 +38,22 @@ __device__ __forceinline__ int brow_of(int b, int r) {
     return b * kRows + r;
   }
 }
+// QkvRope: q / k heads take rotate-half pairs, r = {i, i + hd/2, i + 1, i + 1 + hd/2}
+// with i = 2 (b mod hd/4); v heads take 4 consecutive columns
+__device__ __forceinline__ int brow_rope(int b, int r, int hd, int qk_heads) {
+  const int per_head = hd / 4, head = b / per_head, j = b % per_head;
+  if (head >= qk_heads) return b * kRows + r;
+  return head * hd + 2 * j + (r >> 1) + (r & 1) * (hd / 2);
+}
 
 template <int MM, int EPI>
 __global__ void __launch_bounds__(kWarps * 32) gemv_kernel(GemmArgs a) {
   constexpr bool kSwi = EPI == static_cast<int>(Epi::SwiGLU);
+  constexpr bool kRope = EPI == static_cast<int>(Epi::QkvRope);
+  auto brow = [&](int bb, int r) {
+    if constexpr (kRope) return brow_rope(bb, r, a.rope_hd, a.rope_hq + a.rope_hkv);
+    else return brow_of<kSwi>(bb, r);
+  };
   __shared__ float part[kWarps][kRows][MM];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int b = blockIdx.x;
@@ -51,7 +66,7 @@ __global__ void __launch_bounds__(kWarps * 32) gemv_kernel(GemmArgs a) {
 #pragma unroll
     for (int r = 0; r < kRows; ++r) {
       const uint4* row = reinterpret_cast<const uint4*>(
-          a.B + static_cast<std::int64_t>(min(brow_of<EPI == static_cast<int>(Epi::SwiGLU)>(b, r), a.N - 1)) * a.ldb);
+          a.B + static_cast<std::int64_t>(min(brow(b, r), a.N - 1)) * a.ldb);
 #pragma unroll
       for (int i = 0; i < kUnroll; ++i) {
         const int k8 = warp * 32 + lane + i * kWarps * 32;
@@ -68,16 +83,15 @@ __global__ void __launch_bounds__(kWarps * 32) gemv_kernel(GemmArgs a) {
 #pragma unroll
     for (int m = 0; m < MM; ++m) acc[r][m] = 0.f;
   const int k8n = a.K / 8;
-  const uint4* brow[kRows];
+  const uint4* brow_p[kRows];
 #pragma unroll
   for (int r = 0; r < kRows; ++r)
-    brow[r] = reinterpret_cast<const uint4*>(
-        a.B + static_cast<std::int64_t>(min(brow_of<kSwi>(b, r), a.N - 1)) * a.ldb);
+    brow_p[r] = reinterpret_cast<const uint4*>(a.B + static_cast<std::int64_t>(min(brow(b, r), a.N - 1)) * a.ldb);
 #pragma unroll kUnroll
   for (int k8 = warp * 32 + lane; k8 < k8n; k8 += kWarps * 32) {
     uint4 bv[kRows];
 #pragma unroll
-    for (int r = 0; r < kRows; ++r) bv[r] = __ldcs(brow[r] + k8);  // streamed once
+    for (int r = 0; r < kRows; ++r) bv[r] = __ldcs(brow_p[r] + k8);  // streamed once
 #pragma unroll
     for (int m = 0; m < MM; ++m) {
       if (m >= a.M) break;
@@ -119,7 +133,38 @@ __global__ void __launch_bounds__(kWarps * 32) gemv_kernel(GemmArgs a) {
   if (a.ss_in != nullptr)
     rs = rsqrtf(static_cast<float>(__ldcg(a.ss_in + m)) * (1.f / kSsFixedScale) * a.ss_inv_dim + a.ss_eps);
   const int out_row = a.row_map != nullptr ? a.row_map[m] : m;
-  if constexpr (kSwi) {
+  if constexpr (kRope) {
+    // x = rs * acc + bias, rotated with its rotate-half partner (q / k), then
+    // stored to C; k / v rows also go to this token's KV page (as the tcgen05
+    // QkvRope epilogue: fp32 rotation, one bf16 rounding)
+    const int hd = a.rope_hd, half = hd / 2;
+    const int col = brow(b, r);
+    if (col >= a.N) return;
+    const int head = col / hd, i0 = col % hd;
+    float x = rs * dot(r);
+    if (a.bias != nullptr) x += __bfloat162float(a.bias[col]);
+    if (head < a.rope_hq + a.rope_hkv) {
+      const int pc = brow(b, r ^ 1);  // partner column i0 -/+ hd/2
+      float w = rs * dot(r ^ 1);
+      if (a.bias != nullptr) w += __bfloat162float(a.bias[pc]);
+      const float2 cs = a.rope_table[static_cast<std::int64_t>(m) * half + (i0 % half)];
+      x = i0 < half ? x * cs.x - w * cs.y : x * cs.x + w * cs.y;
+    }
+    const bf16 o = __float2bfloat16_rn(x);
+    static_cast<bf16*>(a.C)[static_cast<std::int64_t>(out_row) * a.ldc + col] = o;
+    if (head >= a.rope_hq) {
+      const ChunkRowInfo ri = static_cast<const ChunkRowInfo*>(a.rope_rows)[m];
+      const std::int64_t page = a.page_tables[ri.req_slot][ri.pos / a.page_size];
+      const int off = ri.pos % a.page_size;
+      if (head < a.rope_hq + a.rope_hkv) {  // K: [page][kv head][token][hd]
+        const int kvh = head - a.rope_hq;
+        a.k_cache[((page * a.rope_hkv + kvh) * a.page_size + off) * hd + i0] = o;
+      } else {  // V transposed: [page][kv head][hd][token]
+        const int kvh = head - a.rope_hq - a.rope_hkv;
+        a.v_cache[((page * a.rope_hkv + kvh) * hd + i0) * a.page_size + off] = o;
+      }
+    }
+  } else if constexpr (kSwi) {
     if (r >= 2) return;
     const int gr = brow_of<true>(b, r), ur = brow_of<true>(b, r + 2);
     float g = rs * dot(r), u = rs * dot(r + 2);
@@ -175,6 +220,7 @@ void launch_m(const GemmArgs& a, Epi epi, cudaStream_t st) {
     case Epi::SwiGLU: return launch_kernel(gemv_kernel<MM, 2>, grid, block, 0, st, 1, a);
     case Epi::Gelu: return launch_kernel(gemv_kernel<MM, 3>, grid, block, 0, st, 1, a);
     case Epi::StoreF32: return launch_kernel(gemv_kernel<MM, 4>, grid, block, 0, st, 1, a);
+    case Epi::QkvRope: return launch_kernel(gemv_kernel<MM, 5>, grid, block, 0, st, 1, a);
   }
 }
 
@@ -183,6 +229,9 @@ void launch_m(const GemmArgs& a, Epi epi, cudaStream_t st) {
 bool gemv_small_m(const GemmArgs& a, Epi epi, cudaStream_t st) {
   if (a.M > kMaxM || a.M_dev != nullptr || a.K % 8 != 0 || a.lda % 8 != 0 || a.ldb % 8 != 0) return false;
   if (epi == Epi::SwiGLU && a.N % 32 != 0) return false;
+  if (epi == Epi::QkvRope && (a.rope_hd % 4 != 0 || a.N % a.rope_hd != 0 || a.rope_rows == nullptr ||
+                              a.rope_table == nullptr || a.page_tables == nullptr || a.row_map != nullptr))
+    return false;
   if (a.ss_clear != nullptr && a.ss_clear_n > 0)
     launch_kernel(clear_u64_kernel, dim3((a.ss_clear_n + 255) / 256), dim3(256), 0, st, 1, a.ss_clear, a.ss_clear_n);
   if (a.M <= 1) launch_m<1>(a, epi, st);

@@ -497,7 +497,9 @@ void Llm::qkv_rope_append(GemmArgs g, const ChunkDev& c, const LlmLayer& L, cons
     const char* e = std::getenv("RS_QKV_FUSE");
     return e == nullptr || e[0] != '0';
   }();
-  if (fuse && g.M > 8 && s.hd % 64 == 0) {
+  // chunks: the tcgen05 GEMM's QkvRope epilogue; decode-sized steps (M <= 8):
+  // the skinny GEMM's (same math: fp32 rotation, one rounding)
+  if (fuse && s.hd % 64 == 0) {
     g.rope_rows = c.rows;
     g.rope_table = rope_table_;
     g.page_tables = page_tables;
