@@ -445,6 +445,7 @@ __global__ void __launch_bounds__(kDecThreads, 1) decode_attn_kernel(
     if (t == t0 + warp) stamp(3);
     const int valid = min(kDecTile, n_keys - t * kDecTile);
     if (valid < kDecTile) {  // keys past the end: V^T columns zeroed (P is 0 there; keep 0 * V finite)
+      __syncwarp();  // every lane's copies have landed before any lane overwrites part of them
       for (int r = lane; r < HD; r += 32)
         for (int k = valid; k < kDecTile; ++k)
           *reinterpret_cast<bf16*>(my + kDecTile * HD * 2 + dec_v_off(r, k >> 3) + 2 * (k & 7)) = f2bf(0.f);
