@@ -105,10 +105,23 @@ constexpr int kMaxParts = 8;  // units per split tile (launch() guarantees the b
 // (cos, sin) table (hd = 128: 512 B per row, as 4 SW128 boxes of 32 floats)
 // and the tile's BN bias values, loaded while the tile's MMAs run.
 constexpr int kRopeTableBytes = 4 * 128 * 128;
+// Wide pair tiles (BN = 320 / 448 / 512, CG = 2 only): the tile is issued as
+// kSub = 2 MMAs of N = BN / 2 per k-step into adjacent TMEM columns; each CTA
+// stages its half of each sub-tile's B rows ([sub 0: BN/4 rows][sub 1: BN/4
+// rows]). One accumulator (2 x BN columns do not fit in TMEM): meant for
+// launches of <= 1 wave, where the per-SM operand feed (A + B bytes per MMA
+// FLOP, from L2) of the narrower tiles is the limit — e.g. the N = 1280 ViT
+// projections as 64 tiles of 256 x 320 instead of 128 of 256 x 160.
 template <int BN, bool TMA_OUT = false, int CG = 1, bool ROPE = false>
 struct Cfg {
-  static_assert(BN % 32 == 0 && BN >= 128 && BN <= 256, "tile width");
+  static_assert(BN % 32 == 0 && BN >= 128 &&
+                    (BN <= 256 || ((BN == 320 || BN == 448 || BN == 512) && CG == 2 && !ROPE)),
+                "tile width");
   static_assert(CG == 1 || (CG == 2 && BN % 32 == 0), "pair tiles split B in halves of 16-row multiples");
+  static constexpr int kSub = BN > 256 ? 2 : 1;       // MMAs per k-step
+  static constexpr int kSubN = BN / kSub;             // N of one MMA
+  static constexpr int kSubRows = kSubN / CG;         // B rows per CTA per sub-tile (one TMA box)
+  static constexpr int kAccBufs = 2 * BN <= 512 ? 2 : 1;
   static constexpr int kABytes = kBM * kBK * 2;
   static constexpr int kBBytes = (BN / CG) * kBK * 2;
   static constexpr int kStageBytes = kABytes + kBBytes;
@@ -119,8 +132,8 @@ struct Cfg {
   // as many pipeline stages as the 227 KB of shared memory allow (<= 8)
   static constexpr int kStagesFit = (227 * 1024 - 1024 - 512 - kEpiBytes - kRopeBytes) / kStageBytes;
   static constexpr int kStages = kStagesFit > 8 ? 8 : kStagesFit;
-  // double-buffered accumulator, allocation rounded up to a power of two
-  static constexpr int kTmemCols = 2 * BN <= 256 ? 256 : 512;
+  // double-buffered accumulator (kAccBufs), allocation rounded up to a power of two
+  static constexpr int kTmemCols = kAccBufs * BN <= 256 ? 256 : 512;
   static constexpr int kSmem = kStages * kStageBytes + kEpiBytes + kRopeBytes + 1024 /*align*/ + 512 /*barriers*/;
 };
 
@@ -503,6 +516,17 @@ __device__ __forceinline__ void epilogue_chunk(const GemmParams& p, int row, int
   }
 }
 
+// One CTA's share of a pair tile's B k-block (tile column tn): per sub-tile,
+// rows [tn * BN + sub * kSubN + rank * kSubRows, + kSubRows).
+template <class C>
+__device__ __forceinline__ void load_b_cg2(std::uint8_t* dst, const CUtensorMap* tmB, std::uint32_t fb, int k0,
+                                           int tn, std::uint32_t rank) {
+#pragma unroll
+  for (int sub = 0; sub < C::kSub; ++sub)
+    sm100::tma_load_2d_cg2(dst + sub * C::kSubRows * kBK * 2, tmB, fb, k0,
+                           tn * C::kSub * C::kSubN + sub * C::kSubN + static_cast<int>(rank) * C::kSubRows);
+}
+
 template <int BN, int EPI, bool TMA_OUT, int CG>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmA,
@@ -585,7 +609,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         if constexpr (CG == 2) {
           if (rank == 0) sm100::mbar_expect_tx(&full[pre_b], 2 * C::kStageBytes);
           const std::uint32_t fb = sm100::mapa(sm100::smem_u32(&full[pre_b]), 0);
-          sm100::tma_load_2d_cg2(smem_b + pre_b * C::kBBytes, &tmB, fb, kb * kBK, n0);
+          load_b_cg2<C>(smem_b + pre_b * C::kBBytes, &tmB, fb, kb * kBK, u0.tile / m_tiles, rank);
         } else {
           sm100::mbar_expect_tx(&full[pre_b], C::kStageBytes);
           sm100::tma_load_2d(smem_b + pre_b * C::kBBytes, &tmB, &full[pre_b], kb * kBK, n0);
@@ -617,7 +641,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (rank == 0 && !early) sm100::mbar_expect_tx(&full[stage], 2 * C::kStageBytes);
           const std::uint32_t fb = sm100::mapa(sm100::smem_u32(&full[stage]), 0);
           sm100::tma_load_2d_cg2(smem_a + stage * C::kABytes, &tmA, fb, kb * kBK, m0);
-          if (!early) sm100::tma_load_2d_cg2(smem_b + stage * C::kBBytes, &tmB, fb, kb * kBK, n0);
+          if (!early) load_b_cg2<C>(smem_b + stage * C::kBBytes, &tmB, fb, kb * kBK, u.tile / m_tiles, rank);
         } else {
           if (!early) sm100::mbar_expect_tx(&full[stage], C::kStageBytes);
           sm100::tma_load_2d(smem_a + stage * C::kABytes, &tmA, &full[stage], kb * kBK, m0);
@@ -631,15 +655,15 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else if (warp == 1 && lane == 0 && rank == 0) {
     // ---------------- MMA issuer (single thread; pair leader) ----------------
-    constexpr std::uint32_t idesc = sm100::idesc_bf16_f32(kBM * CG, BN);
+    constexpr std::uint32_t idesc = sm100::idesc_bf16_f32(kBM * CG, C::kSubN);
     int stage = 0;
     std::uint32_t phase = 0;
     int local = 0;
     UnitIter it = sched.begin(unit0);
     Unit u;
     for (; sched.next(it, u); ++local) {
-      const int acc = local & 1;
-      const std::uint32_t acc_phase = (local >> 1) & 1;
+      const int acc = local % C::kAccBufs;
+      const std::uint32_t acc_phase = (local / C::kAccBufs) & 1;
       sm100::mbar_wait(&tempty[acc], acc_phase ^ 1);
       sm100::tc_fence_after();
       const std::uint32_t d_tmem = tmem_base + static_cast<std::uint32_t>(acc * BN);
@@ -653,12 +677,16 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int kk = 0; kk < kBK / 16; ++kk) {
           // +32 B along K inside the 128B swizzle atom = +2 in the >>4 field.
-          if constexpr (CG == 2)
-            sm100::umma_bf16_cg2(d_tmem, adesc + 2 * kk, bdesc + 2 * kk, idesc,
-                                 (kb != u.kb0 || kk != 0) ? 1u : 0u);
-          else
-            sm100::umma_bf16(d_tmem, adesc + 2 * kk, bdesc + 2 * kk, idesc,
-                             (kb != u.kb0 || kk != 0) ? 1u : 0u);
+#pragma unroll
+          for (int sub = 0; sub < C::kSub; ++sub) {
+            // sub-tile B rows start kSubRows * 128 B further (whole 1 KB swizzle atoms)
+            const std::uint64_t bd = bdesc + 2 * kk + static_cast<std::uint64_t>(sub * C::kSubRows * 128 / 16);
+            const std::uint32_t dt = d_tmem + static_cast<std::uint32_t>(sub * C::kSubN);
+            if constexpr (CG == 2)
+              sm100::umma_bf16_cg2(dt, adesc + 2 * kk, bd, idesc, (kb != u.kb0 || kk != 0) ? 1u : 0u);
+            else
+              sm100::umma_bf16(dt, adesc + 2 * kk, bd, idesc, (kb != u.kb0 || kk != 0) ? 1u : 0u);
+          }
         }
         // frees the smem slot (in both CTAs of a pair) when the MMAs finish
         if constexpr (CG == 2) sm100::umma_commit_cg2(&empty[stage], 3);
@@ -688,8 +716,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (; sched.next(it, u); ++local) {
       const int m0 = (u.tile % m_tiles) * (kBM * CG) + static_cast<int>(rank) * kBM;
       const int n0 = (u.tile / m_tiles) * BN;
-      const int acc = local & 1;
-      const std::uint32_t acc_phase = (local >> 1) & 1;
+      const int acc = local % C::kAccBufs;
+      const std::uint32_t acc_phase = (local / C::kAccBufs) & 1;
       const std::uint32_t t_row =
           tmem_base + (static_cast<std::uint32_t>(quad * 32) << 16) + static_cast<std::uint32_t>(acc * BN);
       if (TMA_OUT && u.split >= 0) {
@@ -986,7 +1014,7 @@ void launch(const GemmArgs& a, cudaStream_t stream) {
     attr_set = true;
   }
   const CUtensorMap tmA = make_map(a.A, false, a.M, a.K, a.lda, kBK, kBM);
-  const CUtensorMap tmB = make_map(a.B, false, a.N, a.K, a.ldb, kBK, BN / CG);
+  const CUtensorMap tmB = make_map(a.B, false, a.N, a.K, a.ldb, kBK, C::kSubRows);
   CUtensorMap tmC = tmA, tmR = tmA;  // unused placeholders unless TMA_OUT
   if constexpr (TMA_OUT) {
     constexpr bool f32 = EPI == static_cast<int>(Epi::StoreF32);
@@ -1053,7 +1081,7 @@ void dispatch_epi(const GemmArgs& a, Epi epi, cudaStream_t s) {
     case Epi::Gelu: return tma ? launch<BN, 3, true, CG>(a, s) : launch<BN, 3, false, CG>(a, s);
     case Epi::StoreF32: return launch<BN, 4, false, CG>(a, s);  // LM-head logits (row-mapped)
     case Epi::QkvRope:
-      if constexpr (BN % 64 == 0) return launch<BN, 5, true, CG>(a, s);
+      if constexpr (BN % 64 == 0 && BN <= 256) return launch<BN, 5, true, CG>(a, s);
       else throw DeviceError(RS_ERR_CUDA, "gemm: QkvRope needs whole-head tiles");
   }
 }
@@ -1106,6 +1134,21 @@ TileChoice pick_tile(int M, int N, int K, bool swiglu, int tile_multiple = 0) {
       }
     }
   }
+  // 256 x 320 pair tiles (one wave, one accumulator): twice the operand reuse
+  // per SM of 256 x 160. Measured on B200 (scripts/gemm_probe.py --wide,
+  // profiles/r02_gemm_wide.txt): ViT down 4096 x 1280 x 3424 35.9 -> 31.4 us;
+  // neutral at short K (ViT O, K = 1280) and slower past one wave (ViT QKV),
+  // so long-K single-wave launches only. The 448 / 512 widths measured no
+  // better than 224 / 256 on the LLM shapes and are left to force_bn.
+  static const bool wide = [] {
+    const char* e = std::getenv("RS_GEMM_WIDE");
+    return e == nullptr || e[0] != '0';
+  }();
+  if (wide && !swiglu && tile_multiple == 0 && cg_override() != 1 && N % 320 == 0 && num_kb >= 32 &&
+      static_cast<long>(ceil_div(M, 2 * kBM)) * (N / 320) <= kNumSMs / 2) {
+    const double pair_gain = 0.85;
+    if (320 * pair_gain * 0.9 < best_cost) best = {320, 2};
+  }
   return best;
 }
 
@@ -1144,6 +1187,9 @@ void gemm(const GemmArgs& a, Epi epi, cudaStream_t stream, int force_bn) {
     case 192 * 4 + 2: dispatch_epi<192, 2>(a, epi, stream); break;
     case 160 * 4 + 2: dispatch_epi<160, 2>(a, epi, stream); break;
     case 128 * 4 + 2: dispatch_epi<128, 2>(a, epi, stream); break;
+    case 320 * 4 + 2: dispatch_epi<320, 2>(a, epi, stream); break;
+    case 448 * 4 + 2: dispatch_epi<448, 2>(a, epi, stream); break;
+    case 512 * 4 + 2: dispatch_epi<512, 2>(a, epi, stream); break;
     default:
       throw DeviceError(RS_ERR_CUDA, "gemm: unsupported tile " + std::to_string(tc.bn) + " x cg" +
                                          std::to_string(tc.cg));

@@ -25,7 +25,10 @@ SHAPES = [  # (M, N, K, epi, label)
     (2048, 37888, 3584, 2, "llm_gateup"), (256, 3584, 18944, 1, "llm_down_m256"),
     (256, 37888, 3584, 2, "llm_gateup_m256"),
 ]
-BNS = [0, 128, 160, 192, 224, 256, -128, -160, -192, -224, -256]
+BNS = [0, 128, 160, 192, 224, 256, -128, -160, -192, -224, -256, -320]
+WIDE = {"vit_o": [0, 160, -160, -320], "vit_down": [0, -160, -320], "vit_qkv": [0, -224, -320],
+        "llm_o": [0, -224, -256, -448, -512], "llm_down": [0, -224, -256, -448, -512],
+        "llm_gateup": [0, -256, -512]}
 
 
 SMALL_M = [(m, n, k, e, f"{lab}_m{m}") for m in (128, 256)
@@ -34,7 +37,7 @@ SMALL_M = [(m, n, k, e, f"{lab}_m{m}") for m in (128, 256)
 
 
 def main():
-    shapes = SHAPES[:3] if "--quick" in sys.argv else SMALL_M if "--small-m" in sys.argv else SHAPES
+    shapes = [x for x in SHAPES if x[4] in WIDE] if "--wide" in sys.argv else SHAPES[:3] if "--quick" in sys.argv else SMALL_M if "--small-m" in sys.argv else SHAPES
     st = torch.cuda.current_stream()
     res = []
     for M, Nn, K, epi, label in shapes:
@@ -46,8 +49,10 @@ def main():
         ref = None
         for split in ("0", "1"):
             os.environ["RS_GEMM_PAIR_SPLIT"] = split
-            for bn in BNS:
+            for bn in (WIDE[label] if "--wide" in sys.argv else BNS):
                 if epi == 2 and abs(bn) % 64 != 0:
+                    continue
+                if "--wide" in sys.argv and split == "1":
                     continue
                 if split == "1" and bn > 0:
                     continue  # single-CTA tiles do not read the pair-split knob

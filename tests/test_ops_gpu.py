@@ -73,7 +73,10 @@ SK_SHAPES = [(2048, 3584, 18944, 224), (1024, 5120, 5120, 160), (1024, 5120, 512
              (128, 3584, 18944, 128), (128, 4608, 3584, 128), (100, 3584, 3584, 128), (128, 37888, 3584, 0),
              # CTA-pair tiles with split tails (bn < 0), incl. a ragged M
              (2048, 3584, 18944, -256), (2048, 3584, 3584, -256), (1056, 3584, 18944, -256),
-             (128, 3584, 18944, -128), (2048, 4608, 3584, -160)]
+             (128, 3584, 18944, -128), (2048, 4608, 3584, -160),
+             # 320-wide pair tiles (two N = 160 MMAs per k-step, one accumulator)
+             (4096, 3840, 3424, -320), (4096, 1280, 3424, -320), (2048, 3584, 18944, -448),
+             (1056, 3584, 18944, -512)]
 
 
 @pytest.fixture(scope="module", autouse=True)
@@ -125,7 +128,7 @@ PAIR_SHAPES = [(256, 256, 64), (1, 256, 64), (300, 384, 200), (4096, 1280, 1176)
 
 
 @pytest.mark.parametrize("M,N,K", PAIR_SHAPES)
-@pytest.mark.parametrize("bn", [128, 160, 192, 224, 256])
+@pytest.mark.parametrize("bn", [128, 160, 192, 224, 256, 320, 448, 512])
 @pytest.mark.parametrize("epi", [0, 1, 2, 3])
 def test_gemm_cta_pair(nat, M, N, K, bn, epi):
     """CTA-pair tiles (cluster of 2, cta_group::2 MMAs, 256 x BN): every fused
