@@ -112,7 +112,21 @@ constexpr int kRopeTableBytes = 4 * 128 * 128;
 // launches of <= 1 wave, where the per-SM operand feed (A + B bytes per MMA
 // FLOP, from L2) of the narrower tiles is the limit — e.g. the N = 1280 ViT
 // projections as 64 tiles of 256 x 320 instead of 128 of 256 x 160.
-template <int BN, bool TMA_OUT = false, int CG = 1, bool ROPE = false>
+// Residual epilogues prefetch EVERY residual chunk of a warp's share of the
+// tile (one 2 KB buffer + mbarrier each, <= 5 per warp) before the
+// accumulator wait, and store each output chunk from its residual buffer:
+// the epilogue no longer waits one HBM round trip per chunk, which was the
+// tail of single-wave launches (the N = 1280 ViT projections). Other
+// epilogues keep a 2-buffer store ring.
+template <int BN, int EPI, bool TMA_OUT>
+constexpr bool res_deep() {
+  return TMA_OUT && EPI == 1 /* Epi::Residual */ && (BN / 32 + 1) / 2 <= 5;
+}
+template <int BN, int EPI, bool TMA_OUT>
+constexpr int epi_bufs() {
+  return res_deep<BN, EPI, TMA_OUT>() && (BN / 32 + 1) / 2 > 2 ? (BN / 32 + 1) / 2 : 2;
+}
+template <int BN, bool TMA_OUT = false, int CG = 1, bool ROPE = false, int NB = 2>
 struct Cfg {
   static_assert(BN % 32 == 0 && BN >= 128 &&
                     (BN <= 256 || ((BN == 320 || BN == 448 || BN == 512) && CG == 2 && !ROPE)),
@@ -125,9 +139,9 @@ struct Cfg {
   static constexpr int kABytes = kBM * kBK * 2;
   static constexpr int kBBytes = (BN / CG) * kBK * 2;
   static constexpr int kStageBytes = kABytes + kBBytes;
-  // epilogue staging: 8 warps x 2 buffers x [32 rows x 64 B] (bf16 TMA stores)
+  // epilogue staging: 8 warps x NB buffers x [32 rows x 64 B] (bf16 TMA stores)
   static constexpr int kEpiBuf = 2048;
-  static constexpr int kEpiBytes = TMA_OUT ? kEpiWarps * 2 * kEpiBuf : 0;
+  static constexpr int kEpiBytes = TMA_OUT ? kEpiWarps * NB * kEpiBuf : 0;
   static constexpr int kRopeBytes = ROPE ? kRopeTableBytes + 2 * BN : 0;
   // as many pipeline stages as the 227 KB of shared memory allow (<= 8)
   static constexpr int kStagesFit = (227 * 1024 - 1024 - 512 - kEpiBytes - kRopeBytes) / kStageBytes;
@@ -183,13 +197,23 @@ __device__ __forceinline__ void ws_sum32(const float* const (&parts)[kMaxParts],
 
 // The first residual chunk of a tile, issued by lane 0 of the epilogue warp
 // before it waits for the accumulator (its latency hides behind the mainloop).
-template <int BN, int EPI>
+template <int BN, int EPI, bool DEEP = false>
 __device__ __forceinline__ void prefetch_residual(const CUtensorMap* tmR, std::uint8_t* bufs,
                                                   std::uint64_t* rbar, std::uint32_t ec, int m0, int n0,
                                                   int quad, int half, int lane) {
   constexpr int kChunks = BN / 32;
   const int c_begin = half == 0 ? 0 : (kChunks + 1) / 2;
   const int c_end = half == 0 ? (kChunks + 1) / 2 : kChunks;
+  if constexpr (DEEP) {
+    if (lane == 0 && c_begin < c_end) {
+      sm100::bulk_wait_read<0>();  // the previous tile's stores no longer read the buffers
+      for (int i = 0; i < c_end - c_begin; ++i) {
+        sm100::mbar_expect_tx(&rbar[i], 32 * 64);
+        sm100::tma_load_2d(bufs + i * 2048, tmR, &rbar[i], n0 + (c_begin + i) * 32, m0 + quad * 32);
+      }
+    }
+    return;
+  }
   if (lane == 0 && c_begin < c_end) {
     sm100::bulk_wait_read<0>();  // the previous tile's stores no longer read the buffers
     const std::uint32_t b = ec & 1;
@@ -198,7 +222,7 @@ __device__ __forceinline__ void prefetch_residual(const CUtensorMap* tmR, std::u
   }
 }
 
-template <int BN, int EPI, bool FROM_WS = false>
+template <int BN, int EPI, bool FROM_WS = false, bool DEEP = false>
 __device__ __forceinline__ void epilogue_tile_tma(const GemmParams& p, const CUtensorMap* tmC,
                                                   const CUtensorMap* tmR, std::uint8_t* bufs,
                                                   std::uint64_t* rbar, std::uint32_t& rphase,
@@ -240,15 +264,22 @@ __device__ __forceinline__ void epilogue_tile_tma(const GemmParams& p, const CUt
   if constexpr (kRes) {
     if (lane == 0 && c_begin < c_end && !res_issued) {
       sm100::bulk_wait_read<0>();
-      issue_res(c_begin, ec & 1);
+      if constexpr (DEEP) {
+        for (int i = 0; i < c_end - c_begin; ++i) issue_res(c_begin + i, i);
+      } else {
+        issue_res(c_begin, ec & 1);
+      }
     }
   }
 #pragma unroll 1
   for (int c = c_begin; c < c_end; ++c, ++ec) {
-    const std::uint32_t b = ec & 1;
+    // DEEP: chunk i of the warp's share has its own residual / output buffer
+    const std::uint32_t b = DEEP ? static_cast<std::uint32_t>(c - c_begin) : ec & 1;
     std::uint8_t* buf = bufs + b * kBuf;
     if (lane == 0) {
-      if constexpr (kRes) {
+      if constexpr (kRes && DEEP) {
+        // every residual chunk already in flight; no buffer is reused within the tile
+      } else if constexpr (kRes) {
         sm100::bulk_wait_read<0>();  // buffer b^1 (chunk c-1's store) drained
         if (c + 1 < c_end) issue_res(c + 1, b ^ 1);
       } else {
@@ -535,7 +566,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                         const __grid_constant__ CUtensorMap tmR, const GemmParams p) {
   // QkvRope: tmR maps the chunk's M-RoPE table, staged per tile into smem
   constexpr bool kRopeStage = TMA_OUT && EPI == static_cast<int>(Epi::QkvRope);
-  using C = Cfg<BN, TMA_OUT, CG, kRopeStage>;
+  constexpr bool kDeep = res_deep<BN, EPI, TMA_OUT>();
+  constexpr int kNB = epi_bufs<BN, EPI, TMA_OUT>();
+  using C = Cfg<BN, TMA_OUT, CG, kRopeStage, kNB>;
+  static_assert(2 * C::kStages + 4 + kNB * kEpiWarps + 1 <= 60, "barrier slots overlap the rope-table barrier");
   extern __shared__ __align__(1024) std::uint8_t smem_raw[];
   std::uint8_t* smem = reinterpret_cast<std::uint8_t*>(
       (reinterpret_cast<std::uintptr_t>(smem_raw) + 1023) & ~std::uintptr_t(1023));
@@ -548,8 +582,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   std::uint64_t* empty = bars + C::kStages;
   std::uint64_t* tfull = bars + 2 * C::kStages;
   std::uint64_t* tempty = tfull + 2;
-  std::uint64_t* rbar = tempty + 2;  // [epilogue warps][2] residual-load barriers
-  std::uint32_t* tmem_holder = reinterpret_cast<std::uint32_t*>(rbar + 2 * kEpiWarps);
+  std::uint64_t* rbar = tempty + 2;  // [epilogue warps][kNB] residual-load barriers
+  std::uint32_t* tmem_holder = reinterpret_cast<std::uint32_t*>(rbar + kNB * kEpiWarps);
   volatile int* sk_finisher = reinterpret_cast<volatile int*>(tmem_holder + 1);
   std::uint64_t* tbar = bars + 60;  // rope table TMA (kRopeStage)
 
@@ -579,7 +613,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       sm100::mbar_init(&tfull[a], 1);
       sm100::mbar_init(&tempty[a], kEpiWarps * CG);  // pair: both CTAs' epilogue warps
     }
-    for (int r = 0; r < 2 * kEpiWarps; ++r) sm100::mbar_init(&rbar[r], 1);
+    for (int r = 0; r < kNB * kEpiWarps; ++r) sm100::mbar_init(&rbar[r], 1);
     sm100::mbar_init(tbar, 1);
     if constexpr (TMA_OUT) {
       sm100::tma_prefetch_desc(&tmC);
@@ -771,8 +805,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int k = 0; k < kMaxParts; ++k) parts[k] = k < n_parts ? part_ptr(k) : nullptr;
           if constexpr (TMA_OUT)
-            epilogue_tile_tma<BN, EPI, true>(p, &tmC, &tmR, smem_epi + (warp - 4) * 2 * C::kEpiBuf,
-                                             rbar + 2 * (warp - 4), rphase, ec, t_row, m0, n0, quad, half,
+            epilogue_tile_tma<BN, EPI, true, kDeep>(p, &tmC, &tmR, smem_epi + (warp - 4) * kNB * C::kEpiBuf,
+                                             rbar + kNB * (warp - 4), rphase, ec, t_row, m0, n0, quad, half,
                                              lane, parts, n_parts);
         }
         asm volatile("bar.sync 1, %0;" ::"n"(32 * kEpiWarps));  // sk_finisher reuse
@@ -781,7 +815,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       if constexpr (TMA_OUT) {
         constexpr bool kRes = EPI == static_cast<int>(Epi::Residual);
         if constexpr (kRes)
-          prefetch_residual<BN, EPI>(&tmR, smem_epi + (warp - 4) * 2 * C::kEpiBuf, rbar + 2 * (warp - 4), ec,
+          prefetch_residual<BN, EPI, kDeep>(&tmR, smem_epi + (warp - 4) * kNB * C::kEpiBuf, rbar + kNB * (warp - 4), ec,
                                      m0, n0, quad, half, lane);
         if constexpr (kRopeStage) {
           // stage this tile's table rows + bias while its MMAs run (the
@@ -807,8 +841,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           tphase ^= 1;
         }
         const float* const no_parts[kMaxParts] = {};
-        epilogue_tile_tma<BN, EPI>(p, &tmC, &tmR, smem_epi + (warp - 4) * 2 * C::kEpiBuf,
-                                   rbar + 2 * (warp - 4), rphase, ec, t_row, m0, n0, quad, half,
+        epilogue_tile_tma<BN, EPI, false, kDeep>(p, &tmC, &tmR, smem_epi + (warp - 4) * kNB * C::kEpiBuf,
+                                   rbar + kNB * (warp - 4), rphase, ec, t_row, m0, n0, quad, half,
                                    lane, no_parts, 0, kRes, kRopeStage ? rope_smem : nullptr);
       } else {
         sm100::mbar_wait(&tfull[acc], acc_phase);
@@ -1006,7 +1040,7 @@ SplitPlan plan_split(int tiles, int num_kb, int bn, int cg = 1) {
 
 template <int BN, int EPI, bool TMA_OUT, int CG>
 void launch(const GemmArgs& a, cudaStream_t stream) {
-  using C = Cfg<BN, TMA_OUT, CG, TMA_OUT && EPI == static_cast<int>(Epi::QkvRope)>;
+  using C = Cfg<BN, TMA_OUT, CG, TMA_OUT && EPI == static_cast<int>(Epi::QkvRope), epi_bufs<BN, EPI, TMA_OUT>()>;
   auto* kernel = gemm_tcgen05_kernel<BN, EPI, TMA_OUT, CG>;
   static bool attr_set = false;
   if (!attr_set) {
