@@ -77,6 +77,7 @@ struct WinParams {
   bf16* out;
   int ld_out;
   unsigned long long* trace;  // RS_WIN_TRACE: per-CTA phase timestamps (diagnostics), else null
+  int skip_rope;              // RS_WIN_SKIP_ROPE=1: dev timing only (no RoPE: wrong results)
 };
 constexpr int kTraceUnits = 8, kTraceSlots = 2 + 6 * kTraceUnits;
 
@@ -323,7 +324,7 @@ __global__ void __launch_bounds__(kWinThreads, 1)
       if (pw == 0 && lane == 0 && it < kTraceUnits) WIN_TRACE(2 + 6 * it);
       const std::uint32_t so = sbase + stage_off(s);
 #pragma unroll 1
-      for (int task = pw; task < kTasks; task += kPrepWarps) {
+      for (int task = pw; task < (p.skip_rope ? 0 : kTasks); task += kPrepWarps) {
         const int g = task / C::kChunkPairs, c = task % C::kChunkPairs;
         const int r = 32 * g + lane;
         if (32 * g >= t.q_rows) continue;  // warp-uniform
@@ -618,6 +619,8 @@ void launch_win(const MapPair& m, const MapPair& mo, const WinParams& p, double 
   const int grid = std::min(p.n_units, kNumSMs);
   static const bool trace = std::getenv("RS_WIN_TRACE") != nullptr;
   WinParams q = p;
+  static const int skip_rope = std::getenv("RS_WIN_SKIP_ROPE") != nullptr ? std::atoi(std::getenv("RS_WIN_SKIP_ROPE")) : 0;
+  q.skip_rope = skip_rope;
   unsigned long long* tbuf = nullptr;
   if (trace) {
     RS_CUDA_CHECK(cudaMallocAsync(reinterpret_cast<void**>(&tbuf), grid * kTraceSlots * 8, st));
