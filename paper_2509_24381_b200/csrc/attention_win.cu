@@ -77,7 +77,7 @@ struct WinParams {
   bf16* out;
   int ld_out;
   unsigned long long* trace;  // RS_WIN_TRACE: per-CTA phase timestamps (diagnostics), else null
-  int skip_rope;              // RS_WIN_SKIP_ROPE=1: dev timing only (no RoPE: wrong results)
+  int skip_rope;              // RS_WIN_SKIP_ROPE=1 in a -DRS_WIN_DEV_BUILD build: timing only (no RoPE)
 };
 constexpr int kTraceUnits = 8, kTraceSlots = 2 + 6 * kTraceUnits;
 
@@ -619,8 +619,12 @@ void launch_win(const MapPair& m, const MapPair& mo, const WinParams& p, double 
   const int grid = std::min(p.n_units, kNumSMs);
   static const bool trace = std::getenv("RS_WIN_TRACE") != nullptr;
   WinParams q = p;
+#ifdef RS_WIN_DEV_BUILD  // dev timing builds only (-DRS_WIN_DEV_BUILD): results are wrong with the knob set
   static const int skip_rope = std::getenv("RS_WIN_SKIP_ROPE") != nullptr ? std::atoi(std::getenv("RS_WIN_SKIP_ROPE")) : 0;
   q.skip_rope = skip_rope;
+#else
+  q.skip_rope = 0;
+#endif
   unsigned long long* tbuf = nullptr;
   if (trace) {
     RS_CUDA_CHECK(cudaMallocAsync(reinterpret_cast<void**>(&tbuf), grid * kTraceSlots * 8, st));
