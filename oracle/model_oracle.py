@@ -123,6 +123,17 @@ class ModelConfig:
         base.update(kw)
         return ModelConfig(**base)
 
+    @staticmethod
+    def qwen72b_llm(**kw) -> "ModelConfig":
+        """cfg5: the 7B's vision tower with a Qwen2.5-VL-72B-shaped LLM
+        (product preset RS_MODEL_QWEN25VL_72B_LLM, include/rserve.h)."""
+        base = dict(vit_dim=1280, vit_layers=32, vit_heads=16, vit_ff=3420, vit_window=4,
+                    vit_fullatt_every=8, patch_dim=1176, llm_dim=8192, llm_layers=80,
+                    llm_q_heads=64, llm_kv_heads=8, llm_head_dim=128, llm_ff=29568,
+                    vocab=152064)
+        base.update(kw)
+        return ModelConfig(**base)
+
     def full_attention(self, layer: int) -> bool:
         e = self.vit_fullatt_every
         return e > 0 and layer % e == e - 1

@@ -74,6 +74,19 @@ def test_shapes_match_product_preset():
         assert prod[k] == v, k
 
 
+def test_oracle_presets_match_product_presets():
+    """The oracle's model configs are the product's presets (7B and cfg5's 72B-shaped LLM)."""
+    from oracle import model_oracle as mo
+    from paper_2509_24381_b200 import _native as N
+    from paper_2509_24381_b200 import api
+    for name, oc in (("qwen2.5-vl-7b", mo.ModelConfig.qwen7b()), ("qwen2.5-vl-72b-llm", mo.ModelConfig.qwen72b_llm())):
+        p = api.model_preset(name)
+        prod = {k: getattr(p, k) for k, _ in N.rs_model_config._fields_}
+        for k in ("vit_dim", "vit_layers", "vit_heads", "vit_ff", "vit_fullatt_every", "patch_dim", "llm_dim",
+                  "llm_layers", "llm_q_heads", "llm_kv_heads", "llm_head_dim", "llm_ff", "vocab"):
+            assert prod[k] == getattr(oc, k), (name, k)
+
+
 def test_oracle_structs_match_product_structs():
     """oracle/ref.py's standalone SimConfig / WorkloadConfig mirrors give the
     reference the same inputs as the product's ctypes structs."""

@@ -176,3 +176,32 @@ def test_qwen7b_width_shallow(oracle_tiny):
     h = llm.forward(emb, mo.mrope_positions(mo.parse_layout(layout)))
     _check_logits(logits, am, llm.first_token_logits(h[-1]))
     p.close()
+
+
+def test_qwen72b_llm_width_shallow():
+    """cfg5's 72B-shaped LLM widths (8192 / 64q / 8kv / 29568, vocab 152064)
+    behind the 7B vision tower, 2 ViT + 2 LLM layers, against the torch fp32
+    mirror of the oracle on the same GPU (TF32 off)."""
+    from oracle import model_oracle as mo
+    from oracle import model_oracle_torch as mt
+    from paper_2509_24381_b200 import api
+    m = api.model_preset("qwen2.5-vl-72b-llm", vit_layers=2, vit_fullatt_every=2, llm_layers=2)
+    p = api.Pipeline(m, max_prompt_tokens=4096, slot_tokens=8192, kv_tokens=8192,
+                     max_chunk_tokens=1024, max_encode_tokens=1024)
+    layout = "T48|M256|T16|M64|T8"
+    sc = api.SimConfig(policy="rserve", stages=1, token_budget=128, embedding_batch_tokens=256,
+                       hidden_size=8192, cost=api.CostModel(beta_enc_ms_per_token=0.01,
+                                                           delta_stage_ms_per_token=0.01))
+    log, _, _ = p.run(f"0,0,-,{layout}\n", sc, payload_seed=11)
+    assert log == api.simulate(f"0,0,-,{layout}\n", sc)[0]
+    logits, am = p.logits(0)
+    p.close()
+    cfg = mo.ModelConfig.qwen72b_llm(vit_layers=2, vit_fullatt_every=2, llm_layers=2)
+    _, ref = mt.first_token_logits(cfg, layout, 11, req_id=0, device="cuda")
+    # 8192-wide rows: bf16 storage alone moves the logits by more than at the
+    # 7B width, so the bar is the bf16-storage oracle's own deviation (tests/_tol.py)
+    _, ref16 = mt.first_token_logits(cfg, layout, 11, req_id=0, device="cuda", bf16_acts=True)
+    ref, ref16 = ref.cpu().numpy(), ref16.cpu().numpy()
+    print(f"72B-width shallow: device {np.abs(logits - ref).max() / ref.std():.4f} std, "
+          f"bf16-storage oracle {np.abs(ref16 - ref).max() / ref.std():.4f} std")
+    _check_logits(logits, am, ref, ref_bf16=ref16)
