@@ -1001,18 +1001,19 @@ struct SplitPlan {
 };
 // cg = 2: pair tiles (256 x bn) on 74 cluster slots; each CTA of a pair keeps
 // its own 128-row partials / counter.
-SplitPlan plan_split(int tiles, int num_kb, int bn, int cg = 1) {
+SplitPlan plan_split(int tiles, int num_kb, int bn, int cg = 1, bool small_m = false) {
   SplitPlan best;
   const int slots = kNumSMs / cg;
   const int rem = tiles % slots;
   const int full = tiles / slots;
   best.cost = full + (rem > 0 ? 1.0 : 0.0);
   // small grids split K from RS_GEMM_SMALL_MIN_KB k-blocks (r1, strided partial
-  // layout: at K = 3584 the partials' round trip ate the gain; K = 18944 won 30%)
-  static const int small_min_kb = [] {
-    const char* e = std::getenv("RS_GEMM_SMALL_MIN_KB");
-    return e != nullptr ? std::atoi(e) : 128;
-  }();
+  // layout: at K = 3584 the partials' round trip ate the gain; K = 18944 won 30%).
+  // r2, coalesced partials: the <= 256-row QKV and O projections of the first /
+  // last prefill chunk gain 17.5 -> 14.5 / 18.1 -> 16.3 us when split from 32
+  // k-blocks (profiles/r02_gemm_smallm.txt); other shapes keep the r1 threshold.
+  static const char* const min_kb_env = std::getenv("RS_GEMM_SMALL_MIN_KB");  // A/B: one threshold for all
+  const int small_min_kb = min_kb_env != nullptr ? std::atoi(min_kb_env) : (small_m ? 32 : 128);
   const bool small = tiles <= slots / 2 && num_kb >= small_min_kb;
   const bool tail = tiles > slots && rem > 0 && num_kb >= 48;
   // Pair tiles: measured slower with split tails at every cfg2 shape (both
@@ -1083,7 +1084,7 @@ void launch(const GemmArgs& a, cudaStream_t stream) {
   // Long-K GEMMs only: the fp32 partials' round trip must stay small next to
   // the saved tail.
   if (TMA_OUT && a.M_dev == nullptr && streamk_enabled()) {
-    const SplitPlan sp = plan_split(tiles, ceil_div(a.K, kBK), BN, CG);
+    const SplitPlan sp = plan_split(tiles, ceil_div(a.K, kBK), BN, CG, a.M <= 2 * kBM);
     if (sp.splits > 1) {
       SkWorkspace& w = sk_workspace(stream);
       p.dp_tiles = tiles - sp.sk_tiles;
