@@ -1024,6 +1024,17 @@ SplitPlan plan_split(int tiles, int num_kb, int bn, int cg = 1, bool small_m = f
     if (e == nullptr || e[0] != '1') return best;
   }
   if (!small && !tail) return best;
+  static const int force_sp = [] {  // A/B only: fixed split count for small grids
+    const char* e = std::getenv("RS_GEMM_FORCE_SPLITS");
+    return e != nullptr ? std::atoi(e) : 0;
+  }();
+  if (small && force_sp >= 2 && force_sp <= kMaxParts && num_kb / force_sp >= 4 &&
+      static_cast<std::size_t>(rem) * cg * force_sp * kBM * bn * sizeof(float) <= kSkWsBytes) {
+    best.sk_tiles = rem;
+    best.splits = force_sp;
+    best.cost = static_cast<double>(ceil_div(rem * force_sp, slots)) / force_sp;
+    return best;
+  }
   const int min_kb = 16;
   for (int sp = 2; sp <= kMaxParts && num_kb / sp >= min_kb; ++sp) {
     if (static_cast<std::size_t>(rem) * cg * sp * kBM * bn * sizeof(float) > kSkWsBytes) break;
