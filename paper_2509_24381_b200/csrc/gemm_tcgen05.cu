@@ -1019,7 +1019,7 @@ SplitPlan plan_split(int tiles, int num_kb, int bn, int cg = 1, bool small_m = f
   // Pair tiles: measured slower with split tails at every cfg2 shape (both
   // CTAs' fp32 partials round-trip), so they run whole tiles only; the kernel
   // path is kept and tested (RS_GEMM_PAIR_SPLIT=1).
-  if (cg == 2) {
+  if (cg == 2 && !small_m) {  // (<= 256-row launches: pair split tails measured faster, above)
     const char* e = std::getenv("RS_GEMM_PAIR_SPLIT");
     if (e == nullptr || e[0] != '1') return best;
   }
@@ -1160,7 +1160,14 @@ TileChoice pick_tile(int M, int N, int K, bool swiglu, int tile_multiple = 0) {
     const char* e = std::getenv("RS_GEMM_SMALLM");
     return e == nullptr || e[0] != '0';
   }();
-  if (small_m_rule && M <= 2 * kBM && !swiglu && N % 128 == 0 && cg_override() == 0) return {128, 1};
+  if (small_m_rule && M <= 2 * kBM && !swiglu && N % 128 == 0 && cg_override() == 0) {
+    // 129-256 rows with long K (the last chunk's down projection): one 256 x 160
+    // pair tile row with a split-K tail reads A once per 160 columns instead of
+    // per 128 and B once, not twice (L2 -> SM traffic, not HBM, was the limit):
+    // 49.3 -> 43.5 us (profiles/r02_gemm_smallm_sweep.txt)
+    if (M > kBM && num_kb >= 128 && tile_multiple == 0) return {160, 2};
+    return {128, 1};
+  }
   TileChoice best{256, 1};
   double best_cost = -1;
   for (int cg = 1; cg <= 2; ++cg) {
