@@ -1150,7 +1150,7 @@ int cg_override() {
   }();
   return v;
 }
-TileChoice pick_tile(int M, int N, int K, bool swiglu, int tile_multiple = 0) {
+TileChoice pick_tile(int M, int N, int K, bool swiglu, int tile_multiple = 0, bool residual = false) {
   static constexpr int kCandidates[] = {256, 224, 192, 160, 128};
   const int num_kb = ceil_div(K, kBK);
   // first / last prefill chunks (M <= 256): few tiles, weight-streaming and
@@ -1190,14 +1190,16 @@ TileChoice pick_tile(int M, int N, int K, bool swiglu, int tile_multiple = 0) {
   // 256 x 320 pair tiles (one wave, one accumulator): twice the operand reuse
   // per SM of 256 x 160. Measured on B200 (scripts/gemm_probe.py --wide,
   // profiles/r02_gemm_wide.txt): ViT down 4096 x 1280 x 3424 35.9 -> 31.4 us;
-  // neutral at short K (ViT O, K = 1280) and slower past one wave (ViT QKV),
-  // so long-K single-wave launches only. The 448 / 512 widths measured no
-  // better than 224 / 256 on the LLM shapes and are left to force_bn.
+  // neutral at short K with a residual epilogue (ViT O, K = 1280) and slower
+  // past one wave (ViT QKV), so single-wave launches with long K or a plain
+  // store (patch embed 4096 x 1280 x 1176: 21.6 -> 14.9 us in a same-process
+  // A/B, profiles/r02_gemm_ab.txt). The 448 / 512 widths measured no better
+  // than 224 / 256 on the LLM shapes and are left to force_bn.
   static const bool wide = [] {
     const char* e = std::getenv("RS_GEMM_WIDE");
     return e == nullptr || e[0] != '0';
   }();
-  if (wide && !swiglu && tile_multiple == 0 && cg_override() != 1 && N % 320 == 0 && num_kb >= 32 &&
+  if (wide && !swiglu && tile_multiple == 0 && cg_override() != 1 && N % 320 == 0 && (num_kb >= 32 || !residual) &&
       static_cast<long>(ceil_div(M, 2 * kBM)) * (N / 320) <= kNumSMs / 2) {
     const double pair_gain = 0.85;
     if (320 * pair_gain * 0.9 < best_cost) best = {320, 2};
@@ -1226,7 +1228,7 @@ void gemm(const GemmArgs& a, Epi epi, cudaStream_t stream, int force_bn) {
   const TileChoice tc = force_bn > 0   ? TileChoice{force_bn, 1}
                         : force_bn < 0 ? TileChoice{-force_bn, 2}
                                        : pick_tile(a.M, a.N, a.K, epi == Epi::SwiGLU,
-                                                   epi == Epi::QkvRope ? a.rope_hd : 0);
+                                                   epi == Epi::QkvRope ? a.rope_hd : 0, epi == Epi::Residual);
   const int tok = prof::begin(stream);
   const int key = tc.bn * 4 + tc.cg;
   switch (key) {
