@@ -36,9 +36,14 @@ def t(bn, reps=50):
 
 
 t(bns[0])
+N.check(N.lib.rs_profile_enable(1))  # which tile the heuristic (bn 0) picks
+t(0, reps=1)
+torch.cuda.synchronize()
+N.check(N.lib.rs_profile_enable(0))
+picked = [k for k in N.profile_drain() if k.startswith("gemm_tcgen05|")]
 res = {bn: [] for bn in bns}
 for _ in range(rounds):
     for bn in bns:
         res[bn].append(t(bn))
-print(f"{M}x{Nn}x{K} epi{epi}: " + ", ".join(f"bn {bn}: {min(v):.2f} us (min of {rounds})" for bn, v in res.items()),
+print(f"{M}x{Nn}x{K} epi{epi} (heuristic {picked}): " + ", ".join(f"bn {bn}: {min(v):.2f} us (min of {rounds})" for bn, v in res.items()),
       flush=True)
