@@ -1179,8 +1179,14 @@ TileChoice pick_tile(int M, int N, int K, bool swiglu, int tile_multiple = 0, bo
       const long slots = kNumSMs / cg;
       const long waves = (tiles + slots - 1) / slots;
       const double pair_gain = num_kb >= 32 ? 0.85 : (waves <= 2 ? 1.05 : 0.93);
+      // long runs (>= 4 waves): narrow tiles are limited by the per-SM operand
+      // feed (A + B bytes per MMA clock: 8192/bn + 32 for a pair CTA, + 64 for a
+      // single CTA), above ~68 / ~80 B/clk measured (profiles/r02_gemm_ab.txt:
+      // 8192x3840x1280 256x128 pairs 75 us vs 256x256 57 us)
+      const double demand = 8192.0 / bn + (cg == 2 ? 32.0 : 64.0);
+      const double feed = waves >= 4 ? std::max(1.0, demand / (cg == 2 ? 68.0 : 80.0)) : 1.0;
       const double cost = plan_split(static_cast<int>(tiles), num_kb, bn, cg).cost * bn *
-                          (cg == 2 ? pair_gain : 1.0);
+                          (cg == 2 ? pair_gain : 1.0) * feed;
       if (best_cost < 0 || cost < best_cost - 1e-9) {
         best = {bn, cg};
         best_cost = cost;
